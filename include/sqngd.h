@@ -1,0 +1,173 @@
+/* sqngd.h -- C-ABI of the B200 (sm_100a) SQNGD AF/CAF loss+gradient hot path.
+ *
+ * Method: arXiv 2604.25728 ("SQNGD", joint transmit-receive design of unimodular
+ * discrete-phase waveforms and mismatched filters).  Citations are to
+ * /root/reference/PAPER.md lines (P:Lx) and equation numbers; readings of the
+ * paper (Q1..Q25) are listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ *   - Array pointers are CUDA DEVICE pointers unless stated otherwise, owned by
+ *     the caller (e.g. torch tensors); the library never frees them.
+ *   - Complex arrays are interleaved fp32 pairs (re, im): "float*" of 2x length.
+ *   - Layouts are row-major: s, w, z = [R][M][N] (the paper's X[:, m] = s[m][:],
+ *     P:L91-94; vec() column stacking = this flattening);
+ *     rho = [R][B*r_n]; the optional AF magnitude map = [R][M][M][K][2N-1] with
+ *     lag tau stored at index tau + N - 1 (Eq. 6 labels, Q1).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default
+ *     stream).  The return status reports launch-time errors; device-side
+ *     conditions (non-finite values, degenerate mainlobe, unsorted thresholds)
+ *     are latched in the context and returned by the next call or sqngd_sync().
+ *   - One context per (device, stream owner); no internal threads.
+ *   - Multi-GPU (world > 1): every rank creates its context with the same config
+ *     and a shared ncclUniqueId; each rank evaluates a contiguous slice of the
+ *     (restart, channel, Doppler) units and one NCCL all-reduce per evaluation
+ *     combines the partials, so every rank returns the full reduced outputs.
+ */
+#ifndef SQNGD_H
+#define SQNGD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sqngd_ctx_s* sqngd_ctx;
+typedef void* sqngd_stream; /* cudaStream_t */
+
+typedef enum {
+  SQNGD_OK = 0,
+  SQNGD_E_INVALID = 1,    /* bad dims, B<2, ROI outside [-N+1, N-1], K<1, empty ROI, rho unsorted */
+  SQNGD_E_DEGENERATE = 2, /* |w_m^H s_m| == 0 or a zero-energy filter row (Eq. 32 undefined) */
+  SQNGD_E_NONFINITE = 3,  /* NaN/Inf in a loss or gradient; sqngd_step leaves the state unchanged */
+  SQNGD_E_CUDA = 4,
+  SQNGD_E_NCCL = 5,
+  SQNGD_E_NOMEM = 6
+} sqngd_status;
+
+typedef enum {
+  SQNGD_LOSS_MAX = 0,   /* Eq. 37 max(WAPSL, WCPSL); subgradient to the unique argmax (Q17)   */
+  SQNGD_LOSS_LSE = 1,   /* (1/beta) ln sum_S e^{beta v}, v = w|A|/N (north-star surrogate)    */
+  SQNGD_LOSS_PNORM = 2  /* (sum_S v^p)^{1/p}                                                  */
+} sqngd_loss_mode;
+
+enum { SQNGD_WRT_FILTERS = 1, /* Step A: waveform fixed, gradient to the filters w */
+       SQNGD_WRT_TRANSMIT = 2 /* Step B: filters fixed, gradient to z and rho      */ };
+enum { SQNGD_BLOCK_A = 1, SQNGD_BLOCK_B = 2, SQNGD_BLOCK_AB = 3 };
+enum { SQNGD_FLAG_NO_CROSS = 1,     /* M == 1: WCPSL := 0 (no cross terms, Eq. 9)              */
+       SQNGD_FLAG_DOPPLER_ALIAS = 4 /* grid reaches beyond [-N/2, N/2]; |A| is N-periodic in f */ };
+
+/* Problem definition (copied into the context at create). */
+typedef struct {
+  int32_t R;         /* independent restarts batched in one call                           */
+  int32_t M;         /* channels: M transmit waveforms and M receive filters */
+  int32_t N;         /* code length, 2 <= N <= 4096                                          */
+  int32_t B;         /* phase alphabet size (Eq. 5), >= 2                                    */
+  int32_t r_n;       /* quantizer copies (Eq. 24); thresholds per restart = B * r_n          */
+  double c;          /* quantizer steepness (Eq. 21)                                         */
+  int32_t K;         /* Doppler bins: inclusive uniform grid f_k = f_lo + k (f_hi-f_lo)/(K-1) */
+  double f_lo, f_hi; /* paper units: f = f_d T, exponent e^{j 2 pi n f / N} (Q8) */
+  int32_t tau_lo, tau_hi;          /* ROI delays, inside [-(N-1), N-1]                    */
+  int32_t exclude_auto_zero_delay; /* 1: Eq. 8 "tau != 0" drops the whole tau=0 column (Q6) */
+  int32_t loss_mode;               /* sqngd_loss_mode                                     */
+  double beta_or_p;                /* LSE beta or p-norm p                                */
+  double eps_w;                    /* Eq. 42 epsilon                                      */
+  double mu_db;                    /* SNRL target (dB), p_tar = 10^{-mu/20} (Eq. 39)      */
+  double lr_w, lr_z;               /* Adam rates: filters (eta_h), z and rho (Q14) */
+  double adam_b1, adam_b2, adam_eps; /* Q15                                               */
+  int32_t n_h, n_x;                /* inner steps per block (Alg. 1)      */
+  const float* weights;            /* device [K][2N-1] w(tau,f) >= 0 (Eqs. 8-9), NULL => 1;
+                                      must stay valid for the context's lifetime          */
+} sqngd_config;
+
+/* One per restart, written by the library into caller-owned DEVICE memory. */
+typedef struct {
+  double loss;       /* Eq. 42: eps * loss_wpsl + (1 - eps) * loss_snrl                  */
+  double loss_wpsl;  /* Eq. 37 (MAX) or the LSE / p-norm surrogate                      */
+  double loss_snrl;  /* Eq. 41                                                          */
+  double wapsl;      /* Eq. 8 / N: exact max over auto maps of w|A|/N                   */
+  double wcpsl;      /* Eq. 9 / N: exact max over cross maps                            */
+  double wpsl;       /* Eq. 7                                                           */
+  int32_t argmax_auto[4];  /* (m, l, tau, k) of WAPSL, ties -> lowest lexicographic     */
+  int32_t argmax_cross[4]; /* (m, l, tau, k) of WCPSL ((-1,...) when M == 1)            */
+  uint32_t flags;          /* SQNGD_FLAG_*                                              */
+  uint32_t n_cells;        /* |S|: sidelobe cells in the ROI                            */
+} sqngd_metrics;
+
+/* Optimizer state: caller-owned DEVICE buffers, mutated in place by sqngd_step.
+   t_a / t_b (host integers) are the Adam step counts of the two blocks. */
+typedef struct {
+  float* z;     /* [R][M][N] phase parameters z = phi / 2pi (Q13)                       */
+  float* rho;   /* [R][B*r_n] ascending thresholds (Eq. 24)                             */
+  float* w;     /* [R][M][N] complex filters (H_Re + j H_Im, Eqs. 26-28)                */
+  float *m_z, *v_z, *m_rho, *v_rho; /* Adam moments, same shapes as z / rho               */
+  float *m_w, *v_w;                 /* Adam moments of (Re w, Im w): [R][M][N][2]         */
+  int64_t t_a, t_b;
+} sqngd_state;
+
+/* Build the context: validates the config (SQNGD_E_INVALID), builds the fp64
+   Doppler twiddle table and the workspace on `cuda_device`.  nccl_unique_id:
+   NULL for one GPU, else 128 bytes of an ncclUniqueId shared by all ranks. */
+sqngd_status sqngd_create(const sqngd_config* cfg, int cuda_device, const void* nccl_unique_id,
+                          int rank, int world, sqngd_ctx* out);
+void sqngd_destroy(sqngd_ctx ctx);
+/* Message for the last non-OK status (ctx may be NULL: last create error). */
+const char* sqngd_last_error(sqngd_ctx ctx);
+/* Synchronize `stream` and return (and clear) the latched device-side status. */
+sqngd_status sqngd_sync(sqngd_ctx ctx, sqngd_stream stream);
+
+/* a1: soft/hard quantizer + phase map (Eqs. 21-24, 43, 23).
+   z [R][M][N], rho [R][B r_n] (ascending) -> s_soft, s_hard (complex [R][M][N]),
+   b_hard [R][M][N] phase index in [0,B) (u8), dq = Q_A'(z) [R][M][N].  Any output may be NULL. */
+sqngd_status sqngd_quantize(sqngd_ctx ctx, const float* z, const float* rho, float* s_soft,
+                            float* s_hard, uint8_t* b_hard, float* dq, sqngd_stream stream);
+
+/* a2-a6: all M^2 AF/CAF maps over (2N-1) lags x K Doppler bins by Doppler-modulated,
+   zero-padded FFT correlation (Eqs. 33-36), fused with the ROI reduction (Eqs. 7-9,
+   37-42).  s, w: complex [R][M][N].  af_mag: NULL or [R][M][M][K][2N-1] |A| (fp32).
+   metrics: [R] sqngd_metrics.  p_out: NULL or [R][M] doubles p_m (Eq. 38). */
+sqngd_status sqngd_af_forward(sqngd_ctx ctx, const float* s, const float* w, float* af_mag,
+                              sqngd_metrics* metrics, double* p_out, sqngd_stream stream);
+
+/* a7-a8 for an explicit waveform s: loss and gradient by adjoint correlations.
+   wrt = SQNGD_WRT_FILTERS: grad_w = dL/dRe w + j dL/dIm w = 2 dL/dw^* (Q16) [R][M][N] complex.
+   wrt = SQNGD_WRT_TRANSMIT: grad_s = dL/ds^* (Wirtinger) [R][M][N] complex.
+   Either gradient pointer may be NULL when not requested. */
+sqngd_status sqngd_loss_grad_s(sqngd_ctx ctx, const float* s, const float* w, int wrt,
+                               sqngd_metrics* metrics, float* grad_w, float* grad_s,
+                               sqngd_stream stream);
+
+/* a1-a8: quantize (z, rho) then loss + gradient.  wrt = SQNGD_WRT_FILTERS uses s_hard
+   (Alg. 1 Step A) and writes grad_w; wrt = SQNGD_WRT_TRANSMIT uses s_soft (Step B) and
+   writes grad_z [R][M][N] and grad_rho [R][B r_n] through Q_A (Eqs. 23-24). */
+sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho, const float* w,
+                                int wrt, sqngd_metrics* metrics, float* grad_w, float* grad_z,
+                                float* grad_rho, sqngd_stream stream);
+
+/* a9: one Alg. 1 outer iteration restricted to `block`:
+   A: n_h x [loss_grad(s_hard) -> Adam(Re w, Im w) -> Pi_H (Eq. 32)];
+   B: n_x x [loss_grad(s_soft) -> Adam(z), Adam(rho) -> threshold projection (Q22)].
+   loss_hist: NULL or DEVICE [R][n_h + n_x] doubles (loss of each inner step, in order,
+   A first).  hard_out: NULL or DEVICE [R] metrics of the hard waveform after the block.
+   On a latched non-finite value the remaining updates are skipped (state unchanged). */
+sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* state, int block, double* loss_hist,
+                        sqngd_metrics* hard_out, sqngd_stream stream);
+
+/* Profiling (for the roofline in bench.py): when enabled, every fused AF kernel launch
+   is bracketed by CUDA events on its launch stream.  sqngd_profile_read synchronizes and
+   returns, per kernel class (0 forward, 1 Step-A adjoint, 2 Step-B adjoint), the summed
+   device milliseconds ms[3] and launch counts count[3], plus `launches` = every kernel the
+   library launched since the last reset (all classes, small kernels included). */
+sqngd_status sqngd_profile_enable(sqngd_ctx ctx, int on);
+sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64_t* launches, int reset);
+
+/* Host utilities (no GPU needed). */
+int64_t sqngd_num_units(const sqngd_config* cfg); /* R * M * K evaluation units */
+/* Contiguous slice [lo, hi) of the units owned by `rank` of `world`. */
+void sqngd_shard_range(int64_t units, int rank, int world, int64_t* lo, int64_t* hi);
+const char* sqngd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SQNGD_H */

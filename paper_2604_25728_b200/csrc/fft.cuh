@@ -1,0 +1,226 @@
+// In-CTA complex FFTs for sm_100a: registers + swizzled shared memory.
+//
+// The paper's Eq. 36 evaluates every Doppler bin's aperiodic
+// correlation as IFFT(FFT(x_pad) . conj(FFT(h_pad))).  Here one FFT of length P
+// (power of two, P >= 2N-1, Q23) is carried by a *group* of T = P/E threads; each
+// thread owns E elements in "strided ownership": v[i] <-> element t + i*T.
+//
+// A transform is a sequence of Stockham autosort passes (radix E, the last one
+// radix P / E^(passes-1)).  Pass p (span Ns = E^p) takes butterfly j's inputs
+// x[j + r P/R], multiplies by W^{(j mod Ns) r / (Ns R)}, does an R-point DFT in
+// registers and writes y[(j/Ns) Ns R + (j mod Ns) + r Ns].  With the strided
+// ownership the first pass reads registers and the last pass writes registers,
+// so a P-point transform costs (passes - 1) shared-memory exchanges and the
+// output lands in the same strided ownership as the input: an IFFT can follow an
+// FFT (or an epilogue + FFT can follow an IFFT) with no extra data movement.
+//
+// Shared-memory addresses are XOR-swizzled (i ^ ((i >> 4) & 15)) so that every
+// write pattern (stride-R for the first pass, contiguous afterwards) and every
+// strided read is bank-conflict free for 64-bit accesses.
+// Exchanges double-buffer (two P-element buffers) so one barrier per exchange.
+#pragma once
+#include <cuda_runtime.h>
+#include <type_traits>
+
+namespace sq {
+
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+
+template <int I, int N, class Fn>
+__device__ __forceinline__ void static_for(Fn&& fn) {
+  if constexpr (I < N) {
+    fn(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(fn);
+  }
+}
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+
+// cos(2 pi i / 64), i = 0..16, to full float precision (first quadrant).
+__host__ __device__ constexpr double kCos64(int i) {
+  constexpr double t[17] = {1.0,
+                            0.99518472667219688624,
+                            0.98078528040323044913,
+                            0.95694033573220886494,
+                            0.92387953251128675613,
+                            0.88192126434835502971,
+                            0.83146961230254523708,
+                            0.77301045336273696081,
+                            0.70710678118654752440,
+                            0.63439328416364549822,
+                            0.55557023301960222474,
+                            0.47139673682599764856,
+                            0.38268343236508977173,
+                            0.29028467725446236764,
+                            0.19509032201612826785,
+                            0.09801714032956060199,
+                            0.0};
+  return t[i];
+}
+// cos / sin of 2 pi k / 64 for any k (exact table symmetries).
+__host__ __device__ constexpr double cos64(int k) {
+  k &= 63;
+  return k <= 16 ? kCos64(k) : k <= 32 ? -kCos64(32 - k) : k <= 48 ? -kCos64(k - 32) : kCos64(64 - k);
+}
+__host__ __device__ constexpr double sin64(int k) { return cos64(k - 16); }
+
+// x * W_R^{DIR*k}, W_R = e^{2 pi i / R}; DIR = -1 forward transform.
+template <int R, int DIR, int k>
+__device__ __forceinline__ float2 twc(float2 x) {
+  constexpr int kk = ((k % R) + R) % R;
+  constexpr int q = kk * (64 / R);  // angle in units of 2 pi / 64
+  if constexpr (kk == 0) {
+    return x;
+  } else if constexpr (q == 16) {  // i^DIR
+    return DIR < 0 ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
+  } else if constexpr (q == 32) {
+    return make_float2(-x.x, -x.y);
+  } else if constexpr (q == 48) {
+    return DIR < 0 ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
+  } else if constexpr (q == 8 || q == 24 || q == 40 || q == 56) {  // odd multiples of pi/4
+    constexpr float h = 0.70710678118654752440f;
+    constexpr float c = (float)cos64(q) > 0 ? h : -h;
+    constexpr float s = (float)(DIR * sin64(q)) > 0 ? h : -h;
+    // (x.x + i x.y)(c + i s) with |c| = |s| = h
+    return make_float2(h * ((c > 0 ? x.x : -x.x) - (s > 0 ? x.y : -x.y)),
+                       h * ((s > 0 ? x.x : -x.x) + (c > 0 ? x.y : -x.y)));
+  } else {
+    constexpr float c = (float)cos64(q);
+    constexpr float s = (float)(DIR * sin64(q));
+    return make_float2(fmaf(x.x, c, -x.y * s), fmaf(x.x, s, x.y * c));
+  }
+}
+
+// R-point DFT in registers (natural order in and out), radix-2 decimation in time.
+// DIR = -1: X[q] = sum_n x[n] e^{-2 pi i q n / R};  DIR = +1: unnormalized inverse.
+template <int R, int DIR>
+__device__ __forceinline__ void dft(float2* v) {
+  if constexpr (R == 1) {
+    return;
+  } else if constexpr (R == 2) {
+    float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else {
+    float2 ev[R / 2], od[R / 2];
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) {
+      ev[i] = v[2 * i];
+      od[i] = v[2 * i + 1];
+    }
+    dft<R / 2, DIR>(ev);
+    dft<R / 2, DIR>(od);
+    static_for<0, R / 2>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      float2 t = twc<R, DIR, k>(od[k]);
+      v[k] = cadd(ev[k], t);
+      v[k + R / 2] = csub(ev[k], t);
+    });
+  }
+}
+
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
+
+// Plan of a P-point transform carried by T = P/E threads.
+template <int P_, int E_>
+struct Plan {
+  static constexpr int P = P_, E = E_, T = P_ / E_;
+  static constexpr int LP = ilog2c(P_), LE = ilog2c(E_);
+  static constexpr int NP = (LP + LE - 1) / LE;  // passes
+  static constexpr int LAST_R = 1 << (LP - LE * (NP - 1));
+  static_assert((1 << LP) == P_ && (1 << LE) == E_ && E_ <= P_, "power-of-two sizes");
+  __host__ __device__ static constexpr int R(int p) { return p < NP - 1 ? E : LAST_R; }
+  __host__ __device__ static constexpr int NS(int p) { return 1 << (LE * p); }
+  __host__ __device__ static constexpr int twoff(int p) {
+    int n = 0;
+    for (int q = 1; q < p; ++q) n += (E / R(q)) * (R(q) - 1);
+    return n;
+  }
+  static constexpr int NTW = twoff(NP) > 0 ? twoff(NP) : 1;  // per-thread twiddle registers
+};
+
+// Per-thread Stockham twiddles W_P^{-(j mod Ns) r P/(Ns R)} of the forward transform.
+template <class PL>
+__device__ __forceinline__ void init_twiddles(float2 (&tw)[PL::NTW], int t) {
+  static_for<1, PL::NP>([&](auto pc) {
+    constexpr int p = decltype(pc)::value;
+    constexpr int R = PL::R(p), Ns = PL::NS(p), NB = PL::E / R;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      int jm = (t + b * PL::T) & (Ns - 1);
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        int k = (jm * r * (PL::P / (Ns * R))) & (PL::P - 1);
+        float s, c;
+        sincospif(2.0f * (float)k / (float)PL::P, &s, &c);
+        tw[PL::twoff(p) + b * (R - 1) + r - 1] = make_float2(c, -s);
+      }
+    }
+  });
+}
+
+// Barrier among the threads of one FFT group.
+struct GroupSync {
+  int id, nthreads;
+  unsigned mask;  // lanes of the group when nthreads <= 32
+  __device__ __forceinline__ void operator()() const {
+    if (nthreads <= 32) {
+      __syncwarp(mask);
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+    }
+  }
+};
+
+// In-place P-point transform of the group's data v (strided ownership in and out).
+// DIR = -1 forward, +1 unnormalized inverse.  sbuf: 2*P float2 of group-private smem.
+// par: exchange parity (alternates the two buffers); must start equal in all threads.
+template <class PL, int DIR>
+__device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2 (&tw)[PL::NTW], float2* sbuf,
+                                    int t, int& par, const GroupSync& sync) {
+  constexpr int E = PL::E, T = PL::T;
+  static_for<0, PL::NP>([&](auto pc) {
+    constexpr int p = decltype(pc)::value;
+    constexpr int R = PL::R(p), Ns = PL::NS(p), NB = E / R;
+    float2* buf = sbuf + (par ? PL::P : 0);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float2 x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = v[b + r * NB];
+      if constexpr (p > 0) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          float2 w = tw[PL::twoff(p) + b * (R - 1) + r - 1];
+          x[r] = DIR < 0 ? cmul(x[r], w) : cmulc(x[r], w);
+        }
+      }
+      dft<R, DIR>(x);
+      if constexpr (p == PL::NP - 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b + r * NB] = x[r];
+      } else {
+        int j = t + b * T;
+        int base = (j / Ns) * Ns * R + (j & (Ns - 1));
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[swz(base + r * Ns)] = x[r];
+      }
+    }
+    if constexpr (p < PL::NP - 1) {
+      sync();
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = buf[swz(t + i * T)];
+      par ^= 1;
+    }
+  });
+}
+
+}  // namespace sq

@@ -1,0 +1,670 @@
+// libsqngd.so -- host side of the C-ABI (include/sqngd.h): context, validation,
+// launch configuration, and the orchestration of the kernels in af_kernels.cuh /
+// misc_kernels.cuh.  Every arithmetic step of the hot path runs on the GPU.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sqngd.h"
+#include "comm.h"
+#include "misc_kernels.cuh"
+
+using namespace sq;
+
+static_assert(sizeof(MetricsOut) == sizeof(sqngd_metrics), "metrics layout");
+
+namespace {
+
+thread_local std::string g_last_error;
+
+// Launch geometry per FFT length: E elements per thread, G groups per CTA.
+constexpr int plan_E(int P) { return P <= 16 ? P : 16; }
+constexpr int plan_G(int P) { return (P / plan_E(P)) >= 128 ? 1 : 128 / (P / plan_E(P)); }
+
+}  // namespace
+
+struct sqngd_ctx_s {
+  sqngd_config cfg{};
+  int dev = 0, rank = 0, world = 1;
+  int P = 0, L = 0, BR = 0, sms = 0;
+  uint32_t n_cells = 0, flags = 0;
+  // chunking of the Doppler axis per mode (0 fwd, 1 adj A, 2 adj B)
+  int C[3] = {1, 1, 1}, chunk[3] = {1, 1, 1};
+  int gtot_max = 0;
+  std::string err;
+  // device workspace
+  float2* tw = nullptr;     // [K][N] e^{j 2 pi (n+1) f_k / N} (fp64-built)
+  float2* H = nullptr;      // [R][M][P] filter spectra / P
+  float2* s_soft = nullptr; // [R][M][N]
+  float2* s_hard = nullptr;
+  float* dq = nullptr;      // [R][M][N]
+  int* lut = nullptr;       // [R][BR+1]
+  Part part{};              // [gtot] keys, shifts, sums; [gtot][N] gradient partials
+  Red* red = nullptr;       // [R]
+  double2* cm = nullptr;    // [R][M]
+  float2* red_grad = nullptr;  // [R][M][N]
+  float* dy = nullptr;         // [R][M][N]
+  float* rho_part = nullptr;   // [R][nchunk][BR]
+  int rho_chunk = 1024, rho_nchunk = 1;
+  float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
+  float* gz = nullptr;         // [R][M][N]
+  float* grho = nullptr;       // [R][BR]
+  MetricsOut* met = nullptr;   // [R] scratch
+  int* status = nullptr;       // latched device status bits
+  Comm comm;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> ev_marks;  // (class, index of start event)
+  int64_t launches = 0;
+  cudaEvent_t ev_get() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+};
+
+// Brackets one fused-kernel launch with events when profiling is on.
+struct ProfScope {
+  sqngd_ctx_s* c;
+  int cls;
+  size_t idx = 0;
+  cudaStream_t st;
+  ProfScope(sqngd_ctx_s* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+    if (c->prof) {
+      idx = c->ev_used;
+      cudaEventRecord(c->ev_get(), st);
+    }
+  }
+  ~ProfScope() {
+    if (c->prof) {
+      cudaEventRecord(c->ev_get(), st);
+      c->ev_marks.push_back({cls, idx});
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------- helpers
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, SQNGD_E_CUDA, #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+static sqngd_status fail(sqngd_ctx ctx, sqngd_status st, const char* what, const char* why = "") {
+  std::string msg = std::string(what) + (why && *why ? std::string(": ") + why : std::string());
+  if (ctx) ctx->err = msg;
+  g_last_error = msg;
+  return st;
+}
+
+static inline cudaStream_t S(sqngd_stream st) { return reinterpret_cast<cudaStream_t>(st); }
+
+// ----------------------------------------------------------------------------- per-P dispatch
+template <int P>
+struct Launch {
+  static constexpr int E = plan_E(P);
+  using PL = Plan<P, E>;
+  static constexpr int G = plan_G(P);
+  static constexpr int THREADS = PL::T * G;
+
+  template <int MODE>
+  static size_t smem() { return (size_t)G * GroupSmem<PL, MODE>::TOTAL * sizeof(float2); }
+  static size_t smem_filter() { return (size_t)G * (PL::NP > 1 ? 2 * P : 0) * sizeof(float2) + 16; }
+
+  static cudaError_t prepare(int* blocks_per_sm) {
+    cudaError_t e;
+    e = cudaFuncSetAttribute(k_af<PL, G, MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_FWD>());
+    if (e) return e;
+    e = cudaFuncSetAttribute(k_af<PL, G, MODE_ADJ_A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_ADJ_A>());
+    if (e) return e;
+    e = cudaFuncSetAttribute(k_af<PL, G, MODE_ADJ_B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_ADJ_B>());
+    if (e) return e;
+    e = cudaFuncSetAttribute(k_filter_fft<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_filter());
+    if (e) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MODE_FWD>, THREADS, smem<MODE_FWD>());
+    if (e) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], k_af<PL, G, MODE_ADJ_A>, THREADS, smem<MODE_ADJ_A>());
+    if (e) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[2], k_af<PL, G, MODE_ADJ_B>, THREADS, smem<MODE_ADJ_B>());
+  }
+  static void filter(int RM, int N, const float2* w, float2* H, cudaStream_t st) {
+    const int blocks = (RM + G - 1) / G;
+    k_filter_fft<PL, G><<<blocks, THREADS, smem_filter(), st>>>(RM, N, w, H);
+  }
+  static void af(int mode, const KP& kp, const float2* s, const float2* H, const float2* tw, float* af_mag,
+                 const Part& part, cudaStream_t st) {
+    const int groups = kp.g_hi - kp.g_lo;
+    if (groups <= 0) return;
+    const int blocks = (groups + G - 1) / G;
+    if (mode == MODE_FWD)
+      k_af<PL, G, MODE_FWD><<<blocks, THREADS, smem<MODE_FWD>(), st>>>(kp, s, H, tw, af_mag, part);
+    else if (mode == MODE_ADJ_A)
+      k_af<PL, G, MODE_ADJ_A><<<blocks, THREADS, smem<MODE_ADJ_A>(), st>>>(kp, s, H, tw, nullptr, part);
+    else
+      k_af<PL, G, MODE_ADJ_B><<<blocks, THREADS, smem<MODE_ADJ_B>(), st>>>(kp, s, H, tw, nullptr, part);
+  }
+  static int groups_per_block() { return G; }
+};
+
+template <class Fn>
+static bool with_P(int P, Fn&& fn) {
+  switch (P) {
+    case 4: fn(Launch<4>{}); return true;
+    case 8: fn(Launch<8>{}); return true;
+    case 16: fn(Launch<16>{}); return true;
+    case 32: fn(Launch<32>{}); return true;
+    case 64: fn(Launch<64>{}); return true;
+    case 128: fn(Launch<128>{}); return true;
+    case 256: fn(Launch<256>{}); return true;
+    case 512: fn(Launch<512>{}); return true;
+    case 1024: fn(Launch<1024>{}); return true;
+    case 2048: fn(Launch<2048>{}); return true;
+    case 4096: fn(Launch<4096>{}); return true;
+    case 8192: fn(Launch<8192>{}); return true;
+    default: return false;
+  }
+}
+
+static KP make_kp(const sqngd_ctx_s* c, int mode, int want_S) {
+  KP kp;
+  const sqngd_config& g = c->cfg;
+  kp.R = g.R; kp.M = g.M; kp.N = g.N; kp.K = g.K; kp.L = c->L; kp.P = c->P;
+  kp.tau_lo = g.tau_lo; kp.tau_hi = g.tau_hi; kp.excl0 = g.exclude_auto_zero_delay;
+  kp.loss_mode = g.loss_mode; kp.beta_or_p = (float)g.beta_or_p; kp.invN = 1.0f / (float)g.N;
+  kp.weights = g.weights;
+  kp.C = c->C[mode]; kp.chunk = c->chunk[mode];
+  const int64_t gtot = (int64_t)g.R * g.M * kp.C;
+  int64_t lo, hi;
+  sqngd_shard_range(gtot, c->rank, c->world, &lo, &hi);
+  kp.g_lo = (int)lo; kp.g_hi = (int)hi;
+  kp.want_S = want_S;
+  return kp;
+}
+
+// Choose the number of Doppler chunks C per (r, a) row minimizing the makespan on `slots`
+// concurrently resident groups: ceil(K / C) units per group, ceil(rows * C_eff / slots) waves.
+static void choose_chunks(int rows, int K, int64_t slots, int* C_out, int* chunk_out) {
+  int bestC = 1;
+  double best = 1e300;
+  for (int C = 1; C <= K; ++C) {
+    const int ch = (K + C - 1) / C;
+    const int Ceff = (K + ch - 1) / ch;
+    if (Ceff != C) continue;
+    const double waves = std::ceil((double)rows * Ceff / (double)std::max<int64_t>(1, slots));
+    const double cost = waves * ch + 1e-3 * Ceff;  // prefer fewer partials on ties
+    if (cost < best) { best = cost; bestC = C; }
+  }
+  *C_out = bestC;
+  *chunk_out = (K + bestC - 1) / bestC;
+}
+
+// ----------------------------------------------------------------------------- C-ABI
+extern "C" {
+
+const char* sqngd_version(void) { return "sqngd-b200 0.1 (sm_100a)"; }
+
+int64_t sqngd_num_units(const sqngd_config* cfg) {
+  return cfg ? (int64_t)cfg->R * cfg->M * cfg->K : 0;
+}
+
+void sqngd_shard_range(int64_t units, int rank, int world, int64_t* lo, int64_t* hi) {
+  if (world < 1) world = 1;
+  const int64_t base = units / world, rem = units % world;
+  const int64_t l = rank * base + std::min<int64_t>(rank, rem);
+  *lo = l;
+  *hi = l + base + (rank < rem ? 1 : 0);
+}
+
+const char* sqngd_last_error(sqngd_ctx ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void* nccl_unique_id, int rank,
+                          int world, sqngd_ctx* out) {
+  sqngd_ctx ctx = nullptr;
+  if (!cfgp || !out) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: null argument");
+  *out = nullptr;
+  const sqngd_config cfg = *cfgp;
+  if (cfg.R < 1 || cfg.M < 1 || cfg.N < 2 || cfg.N > 4096 || cfg.B < 2 || cfg.r_n < 1 || cfg.K < 1 ||
+      !(cfg.c > 0) || cfg.loss_mode < 0 || cfg.loss_mode > 2)
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: dims (need R,M>=1, 2<=N<=4096, B>=2, r_n>=1, K>=1, c>0)");
+  if (cfg.tau_lo < -(cfg.N - 1) || cfg.tau_hi > cfg.N - 1 || cfg.tau_lo > cfg.tau_hi)
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: ROI lags outside [-(N-1), N-1]");
+  if (cfg.loss_mode != 0 && !(cfg.beta_or_p > 0))
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: beta_or_p must be > 0 for LSE / PNORM");
+  if (cfg.B * cfg.r_n > 8192) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: B*r_n > 8192");
+  if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: rank/world");
+  const int L = 2 * cfg.N - 1;
+  if ((double)cfg.M * cfg.M * L * cfg.K >= 4294967295.0)
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: M^2 (2N-1) K cell index exceeds 32 bits");
+
+  ctx = new sqngd_ctx_s();
+  ctx->cfg = cfg;
+  ctx->dev = cuda_device;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->L = L;
+  ctx->BR = cfg.B * cfg.r_n;
+  int P = 1;
+  while (P < L) P <<= 1;
+  ctx->P = P;
+
+  // ROI cell count |S| and flags (host copy of the weights, if any)
+  {
+    std::vector<float> wts;
+    if (cfg.weights) {
+      wts.resize((size_t)cfg.K * L);
+      if (cudaSetDevice(cuda_device) != cudaSuccess ||
+          cudaMemcpy(wts.data(), cfg.weights, wts.size() * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        delete ctx;
+        return fail(nullptr, SQNGD_E_CUDA, "sqngd_create: reading weights");
+      }
+    }
+    uint64_t cells = 0;
+    for (int m = 0; m < cfg.M; ++m)
+      for (int l = 0; l < cfg.M; ++l)
+        for (int tau = cfg.tau_lo; tau <= cfg.tau_hi; ++tau) {
+          if (m == l && cfg.exclude_auto_zero_delay && tau == 0) continue;
+          for (int k = 0; k < cfg.K; ++k)
+            if (!cfg.weights || wts[(size_t)k * L + tau + cfg.N - 1] > 0.f) ++cells;
+        }
+    if (cells == 0) {
+      delete ctx;
+      return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: empty ROI");
+    }
+    ctx->n_cells = (uint32_t)std::min<uint64_t>(cells, 0xFFFFFFFFu);
+    if (cfg.M == 1) ctx->flags |= SQNGD_FLAG_NO_CROSS;
+    if (std::max(std::fabs(cfg.f_lo), std::fabs(cfg.f_hi)) > 0.5 * cfg.N) ctx->flags |= SQNGD_FLAG_DOPPLER_ALIAS;
+  }
+
+  CK(cudaSetDevice(cuda_device));
+  CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, cuda_device));
+  int bps[3] = {1, 1, 1}, G = 1;
+  cudaError_t perr = cudaSuccess;
+  bool okP = with_P(P, [&](auto Lc) {
+    using LC = decltype(Lc);
+    perr = LC::prepare(bps);
+    G = LC::groups_per_block();
+  });
+  if (!okP) {
+    delete ctx;
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: unsupported FFT length");
+  }
+  if (perr != cudaSuccess) {
+    std::string m = cudaGetErrorString(perr);
+    delete ctx;
+    return fail(nullptr, SQNGD_E_CUDA, "sqngd_create: kernel setup", m.c_str());
+  }
+  for (int md = 0; md < 3; ++md) {
+    const int64_t slots = (int64_t)ctx->sms * std::max(1, bps[md]) * G * world;
+    choose_chunks(cfg.R * cfg.M, cfg.K, slots, &ctx->C[md], &ctx->chunk[md]);
+    ctx->gtot_max = std::max(ctx->gtot_max, cfg.R * cfg.M * ctx->C[md]);
+  }
+
+  const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
+  CK(cudaMalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
+  CK(cudaMalloc(&ctx->H, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
+  CK(cudaMalloc(&ctx->s_soft, sizeof(float2) * RMN));
+  CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
+  CK(cudaMalloc(&ctx->dq, sizeof(float) * RMN));
+  CK(cudaMalloc(&ctx->lut, sizeof(int) * (size_t)cfg.R * (ctx->BR + 1)));
+  CK(cudaMalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * ctx->gtot_max));
+  CK(cudaMalloc(&ctx->part.m, sizeof(float) * ctx->gtot_max));
+  CK(cudaMalloc(&ctx->part.S, sizeof(float) * ctx->gtot_max));
+  CK(cudaMalloc(&ctx->part.g, sizeof(float2) * (size_t)ctx->gtot_max * cfg.N));
+  CK(cudaMalloc(&ctx->red, sizeof(Red) * cfg.R));
+  CK(cudaMalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
+  CK(cudaMalloc(&ctx->red_grad, sizeof(float2) * RMN));
+  CK(cudaMalloc(&ctx->dy, sizeof(float) * RMN));
+  ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
+  CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
+  CK(cudaMalloc(&ctx->gw, sizeof(float2) * RMN));
+  CK(cudaMalloc(&ctx->gz, sizeof(float) * RMN));
+  CK(cudaMalloc(&ctx->grho, sizeof(float) * (size_t)cfg.R * ctx->BR));
+  CK(cudaMalloc(&ctx->met, sizeof(MetricsOut) * cfg.R));
+  CK(cudaMalloc(&ctx->status, sizeof(int)));
+  CK(cudaMemset(ctx->status, 0, sizeof(int)));
+
+  // Doppler twiddles e^{j 2 pi n f_k / N}, n one-based (Eq. 33, Q2), phase reduced mod 1 in fp64.
+  {
+    std::vector<float2> tw((size_t)cfg.K * cfg.N);
+    for (int k = 0; k < cfg.K; ++k) {
+      const double f = cfg.K == 1 ? cfg.f_lo : cfg.f_lo + (cfg.f_hi - cfg.f_lo) * (double)k / (double)(cfg.K - 1);
+      for (int n = 0; n < cfg.N; ++n) {
+        double cyc = (double)(n + 1) * f / (double)cfg.N;
+        cyc -= std::floor(cyc);
+        tw[(size_t)k * cfg.N + n] = make_float2((float)std::cos(2.0 * M_PI * cyc), (float)std::sin(2.0 * M_PI * cyc));
+      }
+    }
+    CK(cudaMemcpy(ctx->tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
+
+  if (world > 1) {
+    if (!nccl_unique_id) {
+      sqngd_destroy(ctx);
+      return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: world > 1 needs an ncclUniqueId");
+    }
+    std::string why;
+    if (!ctx->comm.init(nccl_unique_id, rank, world, &why)) {
+      sqngd_destroy(ctx);
+      return fail(nullptr, SQNGD_E_NCCL, "sqngd_create: NCCL init", why.c_str());
+    }
+  }
+  *out = ctx;
+  return SQNGD_OK;
+}
+
+void sqngd_destroy(sqngd_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->dev);
+  void* ptrs[] = {ctx->tw, ctx->H, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+                  ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
+                  ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  ctx->comm.destroy();
+  delete ctx;
+}
+
+sqngd_status sqngd_profile_enable(sqngd_ctx ctx, int on) {
+  if (!ctx) return fail(nullptr, SQNGD_E_INVALID, "sqngd_profile_enable: null ctx");
+  ctx->prof = on != 0;
+  return SQNGD_OK;
+}
+
+sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64_t* launches, int reset) {
+  if (!ctx) return fail(nullptr, SQNGD_E_INVALID, "sqngd_profile_read: null ctx");
+  CK(cudaSetDevice(ctx->dev));
+  CK(cudaDeviceSynchronize());
+  double acc[3] = {0, 0, 0};
+  int64_t cnt[3] = {0, 0, 0};
+  for (auto& mk : ctx->ev_marks) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ctx->ev_pool[mk.second], ctx->ev_pool[mk.second + 1]));
+    acc[mk.first] += t;
+    cnt[mk.first] += 1;
+  }
+  for (int i = 0; i < 3; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (count) count[i] = cnt[i];
+  }
+  if (launches) *launches = ctx->launches;
+  if (reset) {
+    ctx->ev_marks.clear();
+    ctx->ev_used = 0;
+    ctx->launches = 0;
+  }
+  return SQNGD_OK;
+}
+
+sqngd_status sqngd_sync(sqngd_ctx ctx, sqngd_stream stream) {
+  if (!ctx) return fail(nullptr, SQNGD_E_INVALID, "sqngd_sync: null ctx");
+  CK(cudaSetDevice(ctx->dev));
+  CK(cudaStreamSynchronize(S(stream)));
+  int st = 0;
+  CK(cudaMemcpy(&st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(ctx->status, 0, sizeof(int)));
+  if (st & ST_NONFINITE) return fail(ctx, SQNGD_E_NONFINITE, "non-finite loss or gradient");
+  if (st & ST_DEGENERATE) return fail(ctx, SQNGD_E_DEGENERATE, "degenerate mainlobe or zero-energy filter");
+  if (st & ST_INVALID) return fail(ctx, SQNGD_E_INVALID, "thresholds rho not ascending");
+  return SQNGD_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------- internal pipeline
+static sqngd_status launch_check(sqngd_ctx ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, SQNGD_E_CUDA, what, cudaGetErrorString(e));
+  return SQNGD_OK;
+}
+
+static sqngd_status run_quantize(sqngd_ctx ctx, const float* z, const float* rho, float2* s_soft, float2* s_hard,
+                                 uint8_t* b_hard, float* dq, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  if (s_hard || b_hard) {
+    k_hard_lut<<<c.R, 256, 0, st>>>(c.B, ctx->BR, c.c, rho, ctx->lut, ctx->status);
+    ctx->launches += 1;
+  }
+  ctx->launches += 1;
+  const int n = c.R * c.M * c.N;
+  k_quantize<<<(n + 255) / 256, 256, 0, st>>>(c.R, c.M * c.N, c.B, ctx->BR, (float)c.c, z, rho, ctx->lut, s_soft,
+                                               s_hard, b_hard, dq);
+  return launch_check(ctx, "quantize");
+}
+
+static sqngd_status run_filter_fft(sqngd_ctx ctx, const float2* w, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::filter(c.R * c.M, c.N, w, ctx->H, st); });
+  ctx->launches += 1;
+  return launch_check(ctx, "filter fft");
+}
+
+// Multi-GPU: max-then-sum protocol over the per-restart partials.
+static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad, int mode);
+
+// Forward AF + metrics of (s, w).  Assumes H = FFT(w) is current.
+static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w, float* af_mag, MetricsOut* met,
+                                double* p_out, double* hist, int hist_col, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  KP kp = make_kp(ctx, MODE_FWD, c.loss_mode != 0);
+  {
+    ProfScope ps(ctx, MODE_FWD, st);
+    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::af(MODE_FWD, kp, s, ctx->H, ctx->tw, af_mag, ctx->part, st); });
+  }
+  ctx->launches += 4;
+  sqngd_status rc = launch_check(ctx, "af forward");
+  if (rc) return rc;
+  k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
+  if (ctx->world > 1 && (rc = allreduce_red(ctx, st, false, MODE_FWD))) return rc;
+  k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
+  const double ptar = std::pow(10.0, -c.mu_db / 20.0);
+  k_metrics<<<c.R, 32, 0, st>>>(c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells,
+                                ctx->flags, ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col,
+                                ctx->status);
+  return launch_check(ctx, "metrics");
+}
+
+// Loss + gradient of an explicit waveform s.  Assumes H = FFT(w) is current.
+// wrt 1: writes grad_w (2 dL/dw^*); wrt 2: grad_s (dL/ds^*), dy and grad_z if dq/grad_z given.
+static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* w, int wrt, MetricsOut* met,
+                                  float2* grad_w, float2* grad_s, const float* dq, float* grad_z, double* hist,
+                                  int hist_col, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  sqngd_status rc;
+  const double ptar = std::pow(10.0, -c.mu_db / 20.0);
+  if (c.loss_mode == SQNGD_LOSS_MAX) {
+    if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st))) return rc;
+    ctx->launches += 1;
+    k_sparse_adj<<<c.R, 256, 0, st>>>(c.M, c.N, c.K, ctx->L, wrt, c.eps_w, c.weights, s, w, ctx->tw, ctx->red,
+                                      ctx->red_grad);
+    if ((rc = launch_check(ctx, "sparse adjoint"))) return rc;
+  } else {
+    const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
+    KP kp = make_kp(ctx, mode, 1);
+    {
+      ProfScope ps(ctx, mode, st);
+      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::af(mode, kp, s, ctx->H, ctx->tw, nullptr, ctx->part, st); });
+    }
+    ctx->launches += 5;
+    if ((rc = launch_check(ctx, "af adjoint"))) return rc;
+    k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part,
+                                         ctx->red);
+    if (ctx->world > 1 && (rc = allreduce_red(ctx, st, false, mode))) return rc;
+    dim3 grid((c.N + 255) / 256, c.R * c.M);
+    const double extra = mode == MODE_ADJ_A ? 1.0 / ctx->P : 1.0;
+    k_combine_grad<<<grid, 256, 0, st>>>(c.M, c.N, kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, c.eps_w,
+                                         extra, ctx->part, ctx->red, ctx->red_grad);
+    if (ctx->world > 1 && (rc = allreduce_red(ctx, st, true, mode))) return rc;
+    k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
+    k_metrics<<<c.R, 32, 0, st>>>(c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells,
+                                  ctx->flags, ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col,
+                                  ctx->status);
+    if ((rc = launch_check(ctx, "metrics"))) return rc;
+  }
+  const size_t n = (size_t)c.R * c.M * c.N;
+  ctx->launches += 1;
+  k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c.R, c.M, c.N, wrt, c.eps_w, ptar, ctx->cm,
+                                                                ctx->red_grad, s, w, dq, grad_w, grad_s, ctx->dy,
+                                                                grad_z, ctx->status);
+  return launch_check(ctx, "finalize grad");
+}
+
+static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho, float* grad_rho, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  const int MN = c.M * c.N;
+  dim3 g1((ctx->BR + 127) / 128, ctx->rho_nchunk, c.R);
+  k_grad_rho_part<<<g1, 128, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part);
+  dim3 g2((ctx->BR + 127) / 128, c.R);
+  const float coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
+  k_grad_rho_sum<<<g2, 128, 0, st>>>(ctx->BR, ctx->rho_nchunk, coef, ctx->rho_part, grad_rho);
+  ctx->launches += 2;
+  return launch_check(ctx, "grad rho");
+}
+
+static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad, int mode) {
+  const sqngd_config& c = ctx->cfg;
+  std::string why;
+  if (!with_grad) {
+    if (!ctx->comm.reduce_red(ctx->red, c.R, c.loss_mode, c.beta_or_p, st, &why))
+      return fail(ctx, SQNGD_E_NCCL, "all-reduce (loss partials)", why.c_str());
+  } else {
+    if (!ctx->comm.sum_f32(reinterpret_cast<float*>(ctx->red_grad), (size_t)c.R * c.M * c.N * 2, st, &why))
+      return fail(ctx, SQNGD_E_NCCL, "all-reduce (gradient)", why.c_str());
+  }
+  (void)mode;
+  return SQNGD_OK;
+}
+
+// ----------------------------------------------------------------------------- C-ABI compute entry points
+extern "C" {
+
+sqngd_status sqngd_quantize(sqngd_ctx ctx, const float* z, const float* rho, float* s_soft, float* s_hard,
+                            uint8_t* b_hard, float* dq, sqngd_stream stream) {
+  if (!ctx || !z || !rho) return fail(ctx, SQNGD_E_INVALID, "sqngd_quantize: null argument");
+  CK(cudaSetDevice(ctx->dev));
+  return run_quantize(ctx, z, rho, reinterpret_cast<float2*>(s_soft), reinterpret_cast<float2*>(s_hard), b_hard,
+                      dq, S(stream));
+}
+
+sqngd_status sqngd_af_forward(sqngd_ctx ctx, const float* s, const float* w, float* af_mag,
+                              sqngd_metrics* metrics, double* p_out, sqngd_stream stream) {
+  if (!ctx || !s || !w) return fail(ctx, SQNGD_E_INVALID, "sqngd_af_forward: null argument");
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = S(stream);
+  sqngd_status rc = run_filter_fft(ctx, reinterpret_cast<const float2*>(w), st);
+  if (rc) return rc;
+  MetricsOut* met = metrics ? reinterpret_cast<MetricsOut*>(metrics) : ctx->met;
+  return run_forward(ctx, reinterpret_cast<const float2*>(s), reinterpret_cast<const float2*>(w), af_mag, met, p_out,
+                     nullptr, 0, st);
+}
+
+sqngd_status sqngd_loss_grad_s(sqngd_ctx ctx, const float* s, const float* w, int wrt, sqngd_metrics* metrics,
+                               float* grad_w, float* grad_s, sqngd_stream stream) {
+  if (!ctx || !s || !w || (wrt != SQNGD_WRT_FILTERS && wrt != SQNGD_WRT_TRANSMIT))
+    return fail(ctx, SQNGD_E_INVALID, "sqngd_loss_grad_s: bad argument");
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = S(stream);
+  sqngd_status rc = run_filter_fft(ctx, reinterpret_cast<const float2*>(w), st);
+  if (rc) return rc;
+  MetricsOut* met = metrics ? reinterpret_cast<MetricsOut*>(metrics) : ctx->met;
+  return run_loss_grad(ctx, reinterpret_cast<const float2*>(s), reinterpret_cast<const float2*>(w), wrt, met,
+                       reinterpret_cast<float2*>(grad_w), reinterpret_cast<float2*>(grad_s), nullptr, nullptr,
+                       nullptr, 0, st);
+}
+
+sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho, const float* w, int wrt,
+                                sqngd_metrics* metrics, float* grad_w, float* grad_z, float* grad_rho,
+                                sqngd_stream stream) {
+  if (!ctx || !z || !rho || !w || (wrt != SQNGD_WRT_FILTERS && wrt != SQNGD_WRT_TRANSMIT))
+    return fail(ctx, SQNGD_E_INVALID, "sqngd_af_loss_grad: bad argument");
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = S(stream);
+  const float2* w2 = reinterpret_cast<const float2*>(w);
+  MetricsOut* met = metrics ? reinterpret_cast<MetricsOut*>(metrics) : ctx->met;
+  sqngd_status rc;
+  if (wrt == SQNGD_WRT_FILTERS) {
+    if ((rc = run_quantize(ctx, z, rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
+    if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+    return run_loss_grad(ctx, ctx->s_hard, w2, wrt, met, reinterpret_cast<float2*>(grad_w), nullptr, nullptr,
+                         nullptr, nullptr, 0, st);
+  }
+  if ((rc = run_quantize(ctx, z, rho, ctx->s_soft, nullptr, nullptr, ctx->dq, st))) return rc;
+  if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+  if ((rc = run_loss_grad(ctx, ctx->s_soft, w2, wrt, met, nullptr, nullptr, ctx->dq, grad_z, nullptr, 0, st)))
+    return rc;
+  if (grad_rho) return run_grad_rho(ctx, z, rho, grad_rho, st);
+  return SQNGD_OK;
+}
+
+sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss_hist, sqngd_metrics* hard_out,
+                        sqngd_stream stream) {
+  if (!ctx || !stt || !stt->z || !stt->rho || !stt->w || (block & ~3) || !block)
+    return fail(ctx, SQNGD_E_INVALID, "sqngd_step: bad argument");
+  CK(cudaSetDevice(ctx->dev));
+  const sqngd_config& c = ctx->cfg;
+  const cudaStream_t st = S(stream);
+  const size_t RMN = (size_t)c.R * c.M * c.N;
+  float2* w2 = reinterpret_cast<float2*>(stt->w);
+  sqngd_status rc;
+  auto adam = [&](size_t n, float* x, float* m, float* v, const float* g, int64_t t, double lr) {
+    const float c1 = (float)(1.0 - std::pow(c.adam_b1, (double)t));
+    const float c2 = (float)(1.0 - std::pow(c.adam_b2, (double)t));
+    k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, x, m, v, g, (float)lr, (float)c.adam_b1, (float)c.adam_b2,
+                                                         (float)c.adam_eps, c1, c2, ctx->status);
+    ctx->launches += 1;
+  };
+  if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
+    if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
+    for (int i = 0; i < c.n_h; ++i) {
+      if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+      if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, ctx->gw, nullptr, nullptr, nullptr,
+                              loss_hist, i, st)))
+        return rc;
+      stt->t_a += 1;
+      adam(2 * RMN, stt->w, stt->m_w, stt->v_w, reinterpret_cast<const float*>(ctx->gw), stt->t_a, c.lr_w);
+      k_project_w<<<c.R * c.M, 256, 0, st>>>(c.N, w2, ctx->status);
+      ctx->launches += 1;
+      if ((rc = launch_check(ctx, "step A update"))) return rc;
+    }
+  }
+  if (block & SQNGD_BLOCK_B) {  // Step B: transmit parameters with H fixed
+    if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+    const int col0 = (block & SQNGD_BLOCK_A) ? c.n_h : 0;
+    for (int i = 0; i < c.n_x; ++i) {
+      if ((rc = run_quantize(ctx, stt->z, stt->rho, ctx->s_soft, nullptr, nullptr, ctx->dq, st))) return rc;
+      if ((rc = run_loss_grad(ctx, ctx->s_soft, w2, SQNGD_WRT_TRANSMIT, ctx->met, nullptr, nullptr, ctx->dq, ctx->gz,
+                              loss_hist, col0 + i, st)))
+        return rc;
+      if ((rc = run_grad_rho(ctx, stt->z, stt->rho, ctx->grho, st))) return rc;
+      stt->t_b += 1;
+      adam(RMN, stt->z, stt->m_z, stt->v_z, ctx->gz, stt->t_b, c.lr_z);
+      adam((size_t)c.R * ctx->BR, stt->rho, stt->m_rho, stt->v_rho, ctx->grho, stt->t_b, c.lr_z);
+      int n2 = 1;
+      while (n2 < ctx->BR) n2 <<= 1;
+      k_project_rho<<<c.R, 1024, n2 * sizeof(float), st>>>(ctx->BR, stt->rho, 1e-4f, 1.0f - 1e-4f, 1e-6f, ctx->status);
+      ctx->launches += 1;
+      if ((rc = launch_check(ctx, "step B update"))) return rc;
+    }
+  }
+  if (hard_out) {
+    if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
+    if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+    if ((rc = run_forward(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), nullptr, nullptr, 0,
+                          st)))
+      return rc;
+  }
+  return SQNGD_OK;
+}
+
+}  // extern "C"
