@@ -1,0 +1,357 @@
+"""Benchmark of the SQNGD AF/CAF loss+gradient hot path (BASELINE.json metric).
+
+A *step* is one Algorithm-1 outer iteration through the
+public C-ABI call sqngd_step(block = A+B): n_h = 10 Step-A loss+gradient
+evaluations (X_hard fixed, gradient to the filters, Adam, energy projection) and
+n_x = 10 Step-B evaluations (soft quantizer, gradient to z and rho through Q_A,
+Adam, threshold projection), then the hard-waveform metrics -- every row of
+SURVEY.md §8(a).  value = loss+gradient evaluations per second over all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+N > 1 (torchrun, one rank per GPU): every rank optimizes its own independent
+seeded restart(s) (restart index = rank), no data-path collective -> "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2604_25728_b200 import configs as CF  # noqa: E402
+from paper_2604_25728_b200 import inputs  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "loss+grad evals/s"
+
+
+def fft_flops(P):
+    return 5.0 * P * math.log2(P)
+
+
+def work_model(c):
+    """Algorithmic FP32 flops per launch of each fused kernel,
+    per restart: 5 P log2 P per complex FFT, 6 per complex multiply, 7 / 10 per cell."""
+    M, N, K, P = c.M, c.N, c.K, c.P
+    cells = c.cells
+    F = fft_flops(P)
+    fwd_body = K * (M * (6 * N + F) + M * M * (6 * P + F)) + 7 * cells      # F_fwd minus the filter FFTs
+    F_A = 10 * cells + K * M * M * (F + 8 * P) + M * F
+    F_B = 10 * cells + K * (M * M * (F + 8 * P) + M * (F + 6 * N))
+    return {"fwd": fwd_body * c.R, "adjA": (fwd_body + F_A) * c.R, "adjB": (fwd_body + F_B) * c.R,
+            "filter": M * F * c.R, "cells": cells * c.R}
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p.get("sm_max_mhz", 1965.0)), float(p.get("hbm_gbs", 6545.9)), "measured"
+    except Exception:
+        return 1965.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle (CPU) leg
+def oracle_sample(c, budget_s: float = 10.0):
+    """One Step-B loss+gradient evaluation of the fp64 oracle (quantize -> AF -> loss ->
+    adjoint sums -> chain to z, rho), measured on a sample of the workload's Doppler bins
+    (evenly spaced, evaluated one bin at a time until `budget_s` is spent) and scaled to the
+    full grid: the oracle's AF and adjoint cost is exactly linear in the bin count."""
+    from oracle import oracle as O
+
+    z = inputs.phase_params(1, c.M, c.N, c.index)
+    rho = inputs.init_thresholds(1, c.B, c.r_n)
+    order = np.linspace(0, c.K - 1, c.K).round().astype(int)
+    order = np.concatenate([order[::max(1, c.K // 16)], order])      # spread the first picks
+    t0 = time.perf_counter()
+    q = O.quantize(c.with_(R=1), z, rho)
+    t_q = time.perf_counter() - t0
+    w = q["s_hard"]
+    t_bins, nb, gs = 0.0, 0, None
+    seen = set()
+    for k in order:
+        if k in seen:
+            continue
+        seen.add(k)
+        f = c.f_lo + (c.f_hi - c.f_lo) * k / max(1, c.K - 1)
+        cc = c.with_(R=1, K=1, f_lo=float(f), f_hi=float(f))
+        t1 = time.perf_counter()
+        _, _, gs = O.loss_grad(cc, q["s_soft"], w, want_w=False)
+        t_bins += time.perf_counter() - t1
+        nb += 1
+        if t_bins >= budget_s:
+            break
+    t1 = time.perf_counter()
+    O.chain(c.with_(R=1), z, rho, q["s_soft"], gs)
+    t_chain = time.perf_counter() - t1
+    return t_q + t_bins * c.K / nb + t_chain, nb
+
+
+def cpu_info():
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count()
+    return n
+
+
+def run_reference(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_info()))
+    times = []
+    nb = 1
+    for i in range(args.warmup + args.steps):
+        t, nb = oracle_sample(c, budget_s=2.0)
+        if i >= args.warmup:
+            times.append(t)
+    per_eval = statistics.mean(times)
+    v = 1.0 / per_eval
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_eval * 1e3 * 20, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(c),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
+                         "sample": f"Step-B loss+grad (quantize, AF, LSE loss, adjoint, chain) of the fp64 oracle with "
+                                   f"{nb} of {c.K} Doppler bins evaluated, AF/adjoint time scaled by K/{nb}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(c):
+    return {"workload": f"{c.name}: M={c.M} N={c.N} L={c.B} K={c.K} f=[{c.f_lo},{c.f_hi}] R={c.R}",
+            "M": c.M, "N": c.N, "B": c.B, "K": c.K, "R_per_gpu": c.R, "P": c.P,
+            "cells_per_eval": c.cells, "loss": {0: "max", 1: f"lse beta={c.beta_or_p}",
+                                                  2: f"pnorm p={c.beta_or_p}"}[c.loss_mode],
+            "step": "1 Alg.1 outer iteration: 10 Step-A + 10 Step-B loss+grad evals, Adam, projections, "
+                    "hard-waveform metrics",
+            "l2": "256 MiB L2 flush between timed steps (outside the per-step events)"}
+
+
+# --------------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--loss", default="lse", choices=["lse", "max", "pnorm"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    c = CF.CONFIGS[args.config]
+    mode = {"max": CF.LOSS_MAX, "lse": CF.LOSS_LSE, "pnorm": CF.LOSS_PNORM}[args.loss]
+    c = c.with_(loss_mode=mode, beta_or_p={0: 0.0, 1: 200.0, 2: 16.0}[mode])
+    if args.impl == "reference":
+        run_reference(args, c)
+        return
+
+    import torch
+
+    from paper_2604_25728_b200 import sqngd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    # inputs: this rank's restarts r = rank*R .. (independent seeded problems)
+    R = c.R
+    z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, rank * R + r), c.M * c.N).reshape(c.M, c.N)
+                  for r in range(R)])
+    rho = inputs.init_thresholds(R, c.B, c.r_n)
+    ctx = sqngd.Context(c, device=local)
+    zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
+    q = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)
+    st = ctx.new_state(zt, rt, q["s_hard"])                    # w = s_hard (matched start, Q3)
+    hist = torch.zeros((R, c.n_h + c.n_x), dtype=torch.float64, device=dev)
+    hard = torch.empty(R * sqngd.METRICS_BYTES, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+    ctx.sync()
+
+    ctx.profile(True)
+    ctx.profile_read(reset=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))                                   # evict L2 between steps
+            evs[i][0].record(stream)
+            ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        t_wall = time.perf_counter() - t_wall
+    if dist:
+        dist.barrier()
+    ctx.sync()
+    prof = ctx.profile_read(reset=True)
+    ctx.profile(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = sum(step_ms)
+    if dist:
+        tt = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot_ms = float(tt.item())
+    evals_per_step = (c.n_h + c.n_x) * R * world
+    value = evals_per_step * args.steps / (tot_ms / 1e3)
+
+    # ---- roofline of the dominant fused kernel (live CUDA events on the launch stream)
+    wm = work_model(c)
+    names = ["fwd", "adjA", "adjB"]
+    dom = max(range(3), key=lambda i: prof["ms"][i])
+    avg_ms = prof["ms"][dom] / max(1, prof["count"][dom])
+    achieved = wm[names[dom]] / (avg_ms / 1e3) / 1e12
+    sm_mhz, _, src = peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+    clocks = clk.summary()
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the timing
+    keys = ["z", "rho", "w", "m_z", "v_z", "m_rho", "v_rho", "m_w", "v_w"]
+    host = {k: st[k].cpu().pin_memory() for k in keys}
+    host_hist = torch.empty_like(hist, device="cpu").pin_memory()
+    host_hard = torch.empty_like(hard, device="cpu").pin_memory()
+    h2d = sum(host[k].numel() * host[k].element_size() for k in keys)
+    d2h = h2d + hist.numel() * 8 + hard.numel()
+    e2e_ev = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in keys:
+            st[k].copy_(host[k], non_blocking=True)
+        ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+        for k in keys:
+            host[k].copy_(st[k], non_blocking=True)
+        host_hist.copy_(hist, non_blocking=True)
+        host_hard.copy_(hard, non_blocking=True)
+        b.record(stream)
+        if i >= args.warmup:
+            e2e_ev.append((a, b))
+    torch.cuda.synchronize(dev)
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    if dist:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = evals_per_step * args.steps / (e2e_ms / 1e3)
+    hm = sqngd.metrics_from_bytes(host_hard.numpy())
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {**config_dict(c), "parallelism": f"restarts x{world} (independent, no collective)"},
+        "cells_per_s": value * c.cells / c.R,
+        "roofline": {"bound": "alu", "kernel": {"fwd": "k_af<FWD>", "adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>"}[names[dom]],
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": None, "avg_launch_ms": avg_ms, "launches": prof["count"][dom],
+                     "flops_per_launch": wm[names[dom]],
+                     "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
+                     "share_of_step": prof["ms"][dom] / (tot_ms if world == 1 else sum(step_ms))},
+        "kernel_ms": {n: prof["ms"][i] / args.steps for i, n in enumerate(names)},
+        "gpu_launches": prof["launches"],
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "wall_s": t_wall,
+        "final_hard_pslr_db": 20 * math.log10(max(hm[0]["wpsl"], 1e-30)),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OMP_NUM_THREADS", str(cpu_info()))
+        per_eval, nb = oracle_sample(c, budget_s=10.0)
+        line["cpu_baseline"] = {"value": 1.0 / per_eval, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
+                                "kind": "oracle",
+                                "sample": f"Step-B loss+grad (quantize, AF, LSE loss, adjoint, chain) of the fp64 "
+                                          f"oracle with {nb} of {c.K} Doppler bins evaluated, AF/adjoint time "
+                                          f"scaled by K/{nb}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,26 +1,27 @@
 // Fused AF/CAF forward + adjoint kernels.
 //
-// A *group* of T = P/E threads owns one Doppler evaluation unit at a time and
-// keeps every spectrum in registers (strided ownership, fft.cuh):
+// A *group* of T = P/E threads owns one evaluation unit at a time and keeps its
+// spectra in registers (strided ownership, fft.cuh).
 //
-//   forward (MODE_FWD), unit (r, m, k):
-//     x_hat = s_m . e^{j 2 pi n f_k / N}      Eq. 33 (twiddle table built in fp64)
-//     X = FFT_P(x_hat_pad)                      Eq. 35-36
-//     for l:  r = IFFT_P(X . conj(H_l)/P)       Eq. 36, A(tau) = r[(-tau) mod P] (Q1)
-//             fused epilogue: |A|, ROI mask, packed (value, ~index) max keys for
-//             WAPSL / WCPSL (Eqs. 7-9), LSE / p-norm partial sums, optional |A| map.
-//   Step B adjoint (MODE_ADJ_B), unit (r, m, k): as forward, then per l
-//     G = dL/dA^* (unnormalized: phi * w * A / |A|) in place, G_hat = FFT_P(G),
-//     acc += G_hat . H_l/P ;  after the l loop e = IFFT_P(acc) and the group adds
-//     conj(e^{j 2 pi n f/N}) e[n] into its per-(r, m) gradient partial (a8B).
-//   Step A adjoint (MODE_ADJ_A), group (r, l, chunk of k), loop over (k, m):
-//     X, r, G, G_hat as above and acc += X . conj(G_hat); at the end of the chunk
-//     d = IFFT_P(acc) is the group's dL/dw_l^* partial (a8A).
+//   k_xhat, unit (r, m, k):                        a3
+//     x_hat = s_m . e^{j 2 pi n f_k / N}            Eq. 33 (twiddle table built in fp64)
+//     X_{m,k} = FFT_P(x_hat_pad)  -> X cache [R][M][K][P] (L2-resident for C1-C4)
+//   forward (MODE_FWD), group (r, m, chunk of k):   a4-a5
+//     for l: r = IFFT_P(X . conj(H_l)/P)            Eq. 36; A(tau) = r[(-tau) mod P] (Q1)
+//            fused epilogue: |A|, ROI mask, packed (value, ~index) max keys for
+//            WAPSL / WCPSL (Eqs. 7-9), LSE / p-norm partial sums, optional |A| map.
+//   Step B adjoint (MODE_ADJ_B), group (r, m, chunk of k):  a4-a7, a8B
+//     per l: r, then G = dL/dA^* (unnormalized: phi * w * A / |A|) in place,
+//     G_hat = FFT_P(G), acc += G_hat . H_l/P;  after the l loop e = IFFT_P(acc) and
+//     the group adds conj(e^{j 2 pi n f/N}) e[n] into its per-(r, m) partial.
+//   Step A adjoint (MODE_ADJ_A), group (r, l, chunk of k), loop (k, m):  a4-a7, a8A
+//     r, G, G_hat as above and acc += X . conj(G_hat); at the end of the chunk
+//     d = IFFT_P(acc) is the group's dL/dw_l^* partial.
 //
 // The cotangent needs the LSE / p-norm normalizer of the *whole* loss, so the
 // adjoint kernels accumulate with a group-uniform running shift m (online
-// rescaling): phi = e^{beta (v - m)} (LSE) or (v / m)^{p-1} (PNORM), and the
-// combine kernel rescales every group to the global shift, so one pass is exact.
+// rescaling): phi = e^{beta (v - m)} (LSE) or (v / m)^{p-1} (PNORM); the combine
+// kernel rescales every group to the global shift, so one pass is exact.
 //
 // Reductions are deterministic: fixed per-group partial slots, fixed-order
 // combine, no floating-point atomics.
@@ -36,7 +37,7 @@ enum { MODE_FWD = 0, MODE_ADJ_A = 1, MODE_ADJ_B = 2 };
 struct KP {
   int R, M, N, K, L, P;
   int tau_lo, tau_hi, excl0;
-  int loss_mode;    // 0 MAX, 1 LSE, 2 PNORM
+  int loss_mode;  // 0 MAX, 1 LSE, 2 PNORM
   float beta_or_p;
   float invN;
   const float* weights;  // [K][L] or nullptr
@@ -49,6 +50,7 @@ struct Part {
   unsigned long long* key;  // [Gtot][2]  (auto, cross)
   float* m;                 // [Gtot] shift of the group's sums
   float* S;                 // [Gtot] sum of phi (LSE: e^{b(v-m)}, PNORM: (v/m)^p)
+  float* scale;             // [Gtot] rescale to the restart's global shift (combine)
   float2* g;                // [Gtot][N] adjoint partial (time domain)
 };
 
@@ -56,19 +58,23 @@ __device__ __forceinline__ unsigned long long pack_key(float val, uint32_t idx) 
   return ((unsigned long long)__float_as_uint(val) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
 }
 
+__device__ __forceinline__ unsigned group_mask(int T) {
+  return T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << ((threadIdx.x & 31) & ~(T - 1)));
+}
+
 // Group-level helpers: T <= 32 -> shuffles inside the group's lanes; T > 32 -> shuffles
-// + one smem slot per warp + a group barrier.
+// + one smem slot per warp + a group barrier (double-buffered slots).
 template <int T>
 struct Group {
   GroupSync sync;
   unsigned mask;
-  float* red;  // 2 * 32 floats (double-buffered)
+  float* red;
   unsigned long long* redk;
   int par;
   int t;
 
   __device__ __forceinline__ float max_f(float x) {
-    const int W = T < 32 ? T : 32;
+    constexpr int W = T < 32 ? T : 32;
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(mask, x, o));
     if constexpr (T > 32) {
@@ -82,9 +88,8 @@ struct Group {
     }
     return x;
   }
-  // Fixed-order sums (bitwise identical across runs).
-  __device__ __forceinline__ float sum_f(float x) {
-    const int W = T < 32 ? T : 32;
+  __device__ __forceinline__ float sum_f(float x) {  // fixed order: bitwise reproducible
+    constexpr int W = T < 32 ? T : 32;
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o);
     if constexpr (T > 32) {
@@ -99,10 +104,10 @@ struct Group {
     return x;
   }
   __device__ __forceinline__ unsigned long long max_u64(unsigned long long x) {
-    const int W = T < 32 ? T : 32;
+    constexpr int W = T < 32 ? T : 32;
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) {
-      unsigned long long y = __shfl_xor_sync(mask, x, o);
+      const unsigned long long y = __shfl_xor_sync(mask, x, o);
       x = y > x ? y : x;
     }
     if constexpr (T > 32) {
@@ -121,60 +126,71 @@ struct Group {
 // Per-group shared memory (float2 units).
 template <class PL, int MODE>
 struct GroupSmem {
-  static constexpr int XBUF = PL::NP > 1 ? 2 * PL::P : 0;
+  static constexpr int XBUF = PL::NP > 1 ? 2 * PL::PADDED : 0;
   static constexpr int GACC = MODE == MODE_ADJ_B ? PL::P / 2 : 0;  // N <= P/2
-  static constexpr int RED = 64;                                    // 64 float2 = 2x32 u64 / 2x32 f32
-  static constexpr int TOTAL = XBUF + GACC + 2 * RED;
+  static constexpr int RED = 32;                                    // 64 floats (2 x 32)
+  static constexpr int REDK = 64;                                   // 64 u64 (2 x 32)
+  static constexpr int TOTAL = XBUF + GACC + RED + REDK;
 };
 
-// phi for the surrogate sums, with a shift m: LSE e^{beta (v - m)}, PNORM (v/m)^p (0 if m <= 0).
-__device__ __forceinline__ float surrogate_term(int mode, float v, float m, float bp) {
-  if (mode == 1) return __expf(bp * (v - m));
-  return m > 0.f ? __powf(v / m, bp) : 0.f;
-}
-
-// Epilogue on one IFFT output slice r[j] (j = t + i T) of map (m, l, k).
-// Returns per-element v = w |A| / N (or -1 outside the ROI) in vv[], updates keys,
-// writes the optional |A| map.
+// Per-thread ROI bitmasks over its E elements (bit i <-> j = t + i T), weights aside:
+// auto maps drop tau = 0 when excl0 (Eq. 8), cross maps keep it (Eq. 9).
 template <class PL>
-__device__ __forceinline__ void epilogue_cells(const KP& kp, const float2 (&v)[PL::E], float (&vv)[PL::E],
-                                               float (&rs)[PL::E], int t, int r, int m, int l, int k,
-                                               unsigned long long& key_a, unsigned long long& key_c,
-                                               float* __restrict__ af_mag) {
-  constexpr int E = PL::E, T = PL::T, P = PL::P;
-  const int N = kp.N;
-  const bool is_auto = (m == l);
-  const uint32_t base_idx = (uint32_t)((m * kp.M + l) * kp.L);
-  float* mrow = af_mag ? af_mag + ((((size_t)r * kp.M + m) * kp.M + l) * kp.K + k) * (size_t)kp.L : nullptr;
+__device__ __forceinline__ void roi_masks(const KP& kp, int t, uint32_t& roi_auto, uint32_t& roi_cross) {
+  roi_auto = roi_cross = 0u;
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const int j = t + i * T;
-    const int tau = (j < N) ? -j : (j > P - N ? P - j : (1 << 24));
-    const float a2 = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
-    const float rsq = a2 > 0.f ? rsqrtf(a2) : 0.f;
-    const float mag = a2 * rsq;
-    rs[i] = rsq;
-    if (mrow && tau != (1 << 24)) mrow[tau + N - 1] = mag;
-    bool in = tau >= kp.tau_lo && tau <= kp.tau_hi && !(is_auto && kp.excl0 && tau == 0);
-    float wt = 1.f;
-    if (in && kp.weights) {
-      wt = __ldg(kp.weights + (size_t)k * kp.L + tau + N - 1);
-      in = wt > 0.f;
-    }
-    vv[i] = in ? wt * mag * kp.invN : -1.f;
-    if (in) {
-      const uint32_t idx = (base_idx + (uint32_t)(tau + N - 1)) * (uint32_t)kp.K + (uint32_t)k;
-      const unsigned long long key = pack_key(wt * wt * a2, idx);
-      if (is_auto) key_a = key > key_a ? key : key_a;
-      else key_c = key > key_c ? key : key_c;
-    }
+  for (int i = 0; i < PL::E; ++i) {
+    const int j = t + i * PL::T;
+    const int tau = (j < kp.N) ? -j : (j > PL::P - kp.N ? PL::P - j : (1 << 24));
+    const bool in = tau >= kp.tau_lo && tau <= kp.tau_hi;
+    if (in) roi_cross |= 1u << i;
+    if (in && !(kp.excl0 && tau == 0)) roi_auto |= 1u << i;
   }
 }
 
-template <class PL, int G, int MODE>
-__global__ void __launch_bounds__(PL::T* G)
-    k_af(const KP kp, const float2* __restrict__ s, const float2* __restrict__ Hh,
-         const float2* __restrict__ dtw, float* __restrict__ af_mag, Part part) {
+__device__ __forceinline__ int lag_of(int j, int N, int P) { return (j < N) ? -j : P - j; }
+
+// Running max with the oracle's tie rule (lowest lexicographic (m, l, tau, k) index wins).
+__device__ __forceinline__ void best_update(float kv, uint32_t idx, float& best, uint32_t& bidx) {
+  if (kv > best || (kv == best && idx < bidx)) {
+    best = kv;
+    bidx = idx;
+  }
+}
+
+// a3: X_{m,k} = FFT_P(s_m e^{j 2 pi n f_k / N}) for every unit (r, m, k) -> X cache.
+template <class PL, int G, int MINB>
+__global__ void __launch_bounds__(PL::T* G, MINB)
+    k_xhat(int units, int M, int N, int K, const float2* __restrict__ s, const float2* __restrict__ dtw,
+           const float2* __restrict__ ftw, float2* __restrict__ Xc) {
+  constexpr int E = PL::E, T = PL::T, P = PL::P;
+  extern __shared__ float4 smem_raw[];
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  const int u = blockIdx.x * G + grp;
+  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * PL::PADDED : 0);
+  GroupSync sync{1 + grp, T, group_mask(T)};
+  const int uu = u < units ? u : units - 1;
+  const int k = uu % K, rm = uu / K;
+  const float2* sr = s + (size_t)rm * N;
+  const float2* twr = dtw + (size_t)k * N;
+  float2 v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    v[i] = n < N ? cmul(__ldg(sr + n), __ldg(twr + n)) : make_float2(0.f, 0.f);
+  }
+  int par = 0;
+  fft<PL, -1>(v, ftw, xbuf, t, par, sync);
+  if (u >= units) return;
+  float2* out = Xc + (size_t)u * P;
+#pragma unroll
+  for (int i = 0; i < E; ++i) out[t + i * T] = v[i];
+}
+
+template <class PL, int G, int MINB, int MODE>
+__global__ void __launch_bounds__(PL::T* G, MINB)
+    k_af(const KP kp, const float2* __restrict__ Xc, const float2* __restrict__ Hh,
+         const float2* __restrict__ dtw, const float2* __restrict__ ftw, float* __restrict__ af_mag, Part part) {
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   using GS = GroupSmem<PL, MODE>;
   extern __shared__ float4 smem_raw[];
@@ -183,39 +199,35 @@ __global__ void __launch_bounds__(PL::T* G)
   float2* gsm = reinterpret_cast<float2*>(smem_raw) + grp * GS::TOTAL;
   float2* xbuf = gsm;
   float2* gacc = gsm + GS::XBUF;
-  float* red = reinterpret_cast<float*>(gsm + GS::XBUF + GS::GACC);
-  unsigned long long* redk = reinterpret_cast<unsigned long long*>(gsm + GS::XBUF + GS::GACC + GS::RED);
 
   Group<T> grpops;
-  grpops.sync.id = 1 + grp;
-  grpops.sync.nthreads = T;
-  grpops.sync.mask = T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << ((threadIdx.x & 31) & ~(T - 1)));
+  grpops.sync = GroupSync{1 + grp, T, group_mask(T)};
   grpops.mask = grpops.sync.mask;
-  grpops.red = red;
-  grpops.redk = redk;
+  grpops.red = reinterpret_cast<float*>(gsm + GS::XBUF + GS::GACC);
+  grpops.redk = reinterpret_cast<unsigned long long*>(gsm + GS::XBUF + GS::GACC + GS::RED);
   grpops.par = 0;
   grpops.t = t;
 
   const bool active = gg < kp.g_hi;
-  const int M = kp.M, N = kp.N;
+  const int M = kp.M, N = kp.N, K = kp.K;
   const int ra = active ? gg / kp.C : 0, c = active ? gg % kp.C : 0;
   const int r = ra / M, a = ra % M;
   const int k0 = c * kp.chunk;
-  const int k1 = active ? min(kp.K, k0 + kp.chunk) : k0;
+  const int k1 = active ? min(K, k0 + kp.chunk) : k0;
 
-  float2 tw[PL::NTW];
-  init_twiddles<PL>(tw, t);
   int par = 0;
-
-  unsigned long long key_a = 0ull, key_c = 0ull;
+  float best_a = -1.f, best_c = -1.f;  // running max of w^2 |A|^2 (auto, cross) and its cell index
+  uint32_t bidx_a = 0xFFFFFFFFu, bidx_c = 0xFFFFFFFFu;
+  uint32_t roi_auto, roi_cross;
+  roi_masks<PL>(kp, t, roi_auto, roi_cross);
+  const bool has_w = kp.weights != nullptr;
   const int mode = kp.loss_mode;
   const float bp = kp.beta_or_p;
-  // forward: per-thread shift; adjoint: group-uniform shift (starts at -inf / 0)
-  float shift = (mode == 2) ? 0.f : -INFINITY;
+  float shift = (mode == 2) ? 0.f : -INFINITY;  // forward: per-thread; adjoint: group-uniform
   float Ssum = 0.f;
 
-  float2 v[E], xh[E], acc[E];
-  float vv[E], rs[E];
+  float2 v[E];
+  float2 acc[MODE == MODE_FWD ? 1 : E];
   if constexpr (MODE != MODE_FWD) {
 #pragma unroll
     for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
@@ -228,17 +240,7 @@ __global__ void __launch_bounds__(PL::T* G)
   for (int k = k0; k < k1; ++k) {
     for (int mi = 0; mi < inner; ++mi) {
       const int m = (MODE == MODE_ADJ_A) ? mi : a;
-      // ---- a3: Doppler modulation (Eq. 33) + forward FFT of the zero-padded code
-      const float2* sr = s + ((size_t)r * M + m) * N;
-      const float2* twr = dtw + (size_t)k * N;
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int n = t + i * T;
-        v[i] = n < N ? cmul(__ldg(sr + n), __ldg(twr + n)) : make_float2(0.f, 0.f);
-      }
-      fft<PL, -1>(v, tw, xbuf, t, par, grpops.sync);
-#pragma unroll
-      for (int i = 0; i < E; ++i) xh[i] = v[i];
+      const float2* Xr = Xc + (((size_t)r * M + m) * K + k) * P;
       if constexpr (MODE == MODE_ADJ_B) {
 #pragma unroll
         for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
@@ -246,30 +248,60 @@ __global__ void __launch_bounds__(PL::T* G)
       const int l_lo = (MODE == MODE_ADJ_A) ? a : 0, l_hi = (MODE == MODE_ADJ_A) ? a + 1 : M;
       for (int l = l_lo; l < l_hi; ++l) {
         const float2* Hl = Hh + ((size_t)r * M + l) * P;
+        const bool is_auto = (m == l);
+        const uint32_t roi = is_auto ? roi_auto : roi_cross;
+        const uint32_t base_idx = (uint32_t)((m * M + l) * kp.L + N - 1);
+        const float* wrow = has_w ? kp.weights + (size_t)k * kp.L + N - 1 : nullptr;
         // ---- a4: cross-spectrum + IFFT (Eq. 36); H is stored pre-scaled by 1/P
 #pragma unroll
-        for (int i = 0; i < E; ++i) v[i] = cmulc(xh[i], __ldg(Hl + t + i * T));
-        fft<PL, +1>(v, tw, xbuf, t, par, grpops.sync);
-        // ---- a5: fused cell epilogue
-        epilogue_cells<PL>(kp, v, vv, rs, t, r, m, l, k, key_a, key_c, af_mag);
+        for (int i = 0; i < E; ++i) v[i] = cmulc(__ldg(Xr + t + i * T), __ldg(Hl + t + i * T));
+        fft<PL, +1>(v, ftw, xbuf, t, par, grpops.sync);
+        // ---- a5: fused cell epilogue (max keys; forward sums / map)
+        float lmax2 = -1.f, lbest = -1.f;
+        uint32_t lidx = 0xFFFFFFFFu;
         if constexpr (MODE == MODE_FWD) {
-          if (kp.want_S) {
+          if (af_mag) {
+            float* mrow = af_mag + ((((size_t)r * M + m) * M + l) * K + k) * (size_t)kp.L + N - 1;
 #pragma unroll
             for (int i = 0; i < E; ++i) {
-              if (vv[i] < 0.f) continue;
-              if (vv[i] > shift) {  // per-thread online rescale
-                if (Ssum > 0.f) Ssum *= (mode == 1) ? __expf(bp * (shift - vv[i])) : __powf(shift / vv[i], bp);
-                shift = vv[i];
-              }
-              Ssum += surrogate_term(mode, vv[i], shift, bp);
+              const int j = t + i * T;
+              if (j < N || j > P - N) mrow[lag_of(j, N, P)] = sqrtf(fmaf(v[i].x, v[i].x, v[i].y * v[i].y));
             }
           }
-        } else {
-          // ---- a7: cotangent with a group-uniform running shift
-          float lmax = -INFINITY;
+        }
 #pragma unroll
-          for (int i = 0; i < E; ++i) lmax = fmaxf(lmax, vv[i]);
-          const float gmax = grpops.max_f(lmax);
+        for (int i = 0; i < E; ++i) {
+          if (!((roi >> i) & 1u)) continue;
+          float kv = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
+          if (has_w) {
+            const float wt = __ldg(wrow + lag_of(t + i * T, N, P));
+            if (!(wt > 0.f)) continue;
+            kv *= wt * wt;
+          }
+          lmax2 = fmaxf(lmax2, kv);
+          if (kv >= lbest) {  // rare after the first few cells: index only on a new max
+            const uint32_t idx = (base_idx + (uint32_t)lag_of(t + i * T, N, P)) * (uint32_t)K + (uint32_t)k;
+            best_update(kv, idx, lbest, lidx);
+          }
+          if constexpr (MODE == MODE_FWD) {
+            if (kp.want_S) {
+              const float vv = sqrtf(kv) * kp.invN;
+              if (vv > shift) {  // per-thread online rescale
+                if (Ssum > 0.f) Ssum *= (mode == 1) ? __expf(bp * (shift - vv)) : __powf(shift / vv, bp);
+                shift = vv;
+              }
+              Ssum += (mode == 1) ? __expf(bp * (vv - shift)) : (shift > 0.f ? __powf(vv / shift, bp) : 0.f);
+            }
+          }
+        }
+        if (lbest >= 0.f) {
+          if (is_auto) best_update(lbest, lidx, best_a, bidx_a);
+          else best_update(lbest, lidx, best_c, bidx_c);
+        }
+        if constexpr (MODE != MODE_FWD) {
+          // ---- a7: cotangent with a group-uniform running shift
+          const float gmax2 = grpops.max_f(lmax2);
+          const float gmax = gmax2 >= 0.f ? sqrtf(gmax2) * kp.invN : -1.f;
           if (gmax >= 0.f && gmax > shift) {
             float sc_S = 0.f, sc_G = 0.f;  // PNORM with shift 0: nothing accumulated (0^p = 0)
             if (mode == 1) {
@@ -286,58 +318,66 @@ __global__ void __launch_bounds__(PL::T* G)
             }
             shift = gmax;
           }
+          const float lb = bp * 1.4426950408889634f;  // exp(b x) = exp2(lb x)
 #pragma unroll
           for (int i = 0; i < E; ++i) {
-            float phi = 0.f, gphi = 0.f;
-            if (vv[i] >= 0.f) {
-              if (mode == 1) {
-                phi = __expf(bp * (vv[i] - shift));
-                gphi = phi;
-              } else if (shift > 0.f) {
-                const float q = vv[i] / shift;
-                gphi = __powf(q, bp - 1.f);
-                phi = gphi * q;
+            float gfac = 0.f;
+            if ((roi >> i) & 1u) {
+              float wt = 1.f;
+              if (has_w) wt = __ldg(wrow + lag_of(t + i * T, N, P));
+              if (wt > 0.f) {
+                const float a2 = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
+                const float rsq = a2 > 0.f ? rsqrtf(a2) : 0.f;
+                const float vv = wt * a2 * rsq * kp.invN;
+                float phi, gphi;
+                if (mode == 1) {
+                  phi = exp2f(lb * (vv - shift));
+                  gphi = phi;
+                } else if (shift > 0.f) {
+                  const float q = vv / shift;
+                  gphi = __powf(q, bp - 1.f);
+                  phi = gphi * q;
+                } else {
+                  phi = gphi = 0.f;
+                }
+                Ssum += phi;
+                gfac = gphi * wt * rsq;  // unnormalized G = gphi * w * A / |A|  (0 at A = 0)
               }
             }
-            Ssum += phi;
-            // unnormalized G = gphi * w * A / |A|; w |A| / N = vv  ->  w / |A| = vv * N / |A|^2
-            const float wfac = vv[i] >= 0.f ? gphi * vv[i] * (float)N * rs[i] * rs[i] : 0.f;
-            v[i] = make_float2(v[i].x * wfac, v[i].y * wfac);
+            v[i] = make_float2(v[i].x * gfac, v[i].y * gfac);
           }
-          // ---- a7: G_hat = FFT(G placed at (-tau) mod P) -- same positions as r
-          fft<PL, -1>(v, tw, xbuf, t, par, grpops.sync);
+          // ---- a7: G_hat = FFT(G placed at (-tau) mod P) -- the same positions as r
+          fft<PL, -1>(v, ftw, xbuf, t, par, grpops.sync);
           if constexpr (MODE == MODE_ADJ_B) {
 #pragma unroll
             for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], __ldg(Hl + t + i * T)));
           } else {
 #pragma unroll
-            for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(xh[i], v[i]));  // X . conj(G_hat)
+            for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(__ldg(Xr + t + i * T), v[i]));  // X conj(G_hat)
           }
         }
       }  // l
       if constexpr (MODE == MODE_ADJ_B) {
         // ---- a8B: e = IFFT(sum_l G_hat H_l / P), demodulate, accumulate over the chunk's bins
-        fft<PL, +1>(acc, tw, xbuf, t, par, grpops.sync);
+        fft<PL, +1>(acc, ftw, xbuf, t, par, grpops.sync);
+        const float2* twr = dtw + (size_t)k * N;
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           const int n = t + i * T;
-          if (n < N) {
-            float2 g = gacc[n];
-            gacc[n] = cadd(g, cmulc(acc[i], __ldg(twr + n)));
-          }
+          if (n < N) gacc[n] = cadd(gacc[n], cmulc(acc[i], __ldg(twr + n)));
         }
       }
     }  // m (Step A)
   }    // k
 
   // ---- group partials
-  key_a = grpops.max_u64(key_a);
-  key_c = grpops.max_u64(key_c);
-  float gshift = shift;
-  float gS;
+  const unsigned long long key_a =
+      grpops.max_u64(best_a >= 0.f ? pack_key(best_a, bidx_a) : 0ull);
+  const unsigned long long key_c =
+      grpops.max_u64(best_c >= 0.f ? pack_key(best_c, bidx_c) : 0ull);
+  float gshift = shift, gS;
   if constexpr (MODE == MODE_FWD) {
-    // combine per-thread shifts inside the group
-    gshift = grpops.max_f(shift);
+    gshift = grpops.max_f(shift);  // combine per-thread shifts inside the group
     float term = 0.f;
     if (Ssum > 0.f) term = (mode == 1) ? Ssum * __expf(bp * (shift - gshift)) : Ssum * __powf(shift / gshift, bp);
     gS = grpops.sum_f(term);
@@ -352,8 +392,8 @@ __global__ void __launch_bounds__(PL::T* G)
     part.S[gg] = gS;
   }
   if constexpr (MODE == MODE_ADJ_A) {
-    // ---- a8A: d = IFFT(sum X conj(G_hat)) -> the group's dL/dw_l^* partial (x 1/P later)
-    fft<PL, +1>(acc, tw, xbuf, t, par, grpops.sync);
+    // ---- a8A: d = IFFT(sum X conj(G_hat)) -> the group's dL/dw_l^* partial (x 1/P in the combine)
+    fft<PL, +1>(acc, ftw, xbuf, t, par, grpops.sync);
     float2* gout = part.g + (size_t)gg * N;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
@@ -369,18 +409,13 @@ __global__ void __launch_bounds__(PL::T* G)
 // a2: H_l = FFT_P([w_l; 0]) / P for every (r, l); one group per filter.
 template <class PL, int G>
 __global__ void __launch_bounds__(PL::T* G)
-    k_filter_fft(int RM, int N, const float2* __restrict__ w, float2* __restrict__ Hh) {
+    k_filter_fft(int RM, int N, const float2* __restrict__ w, const float2* __restrict__ ftw, float2* __restrict__ Hh) {
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
   const int id = blockIdx.x * G + grp;
-  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * P : 0);
-  GroupSync sync;
-  sync.id = 1 + grp;
-  sync.nthreads = T;
-  sync.mask = T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << ((threadIdx.x & 31) & ~(T - 1)));
-  float2 tw[PL::NTW];
-  init_twiddles<PL>(tw, t);
+  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * PL::PADDED : 0);
+  GroupSync sync{1 + grp, T, group_mask(T)};
   const int rl = id < RM ? id : RM - 1;
   float2 v[E];
   const float2* wr = w + (size_t)rl * N;
@@ -390,7 +425,7 @@ __global__ void __launch_bounds__(PL::T* G)
     v[i] = n < N ? __ldg(wr + n) : make_float2(0.f, 0.f);
   }
   int par = 0;
-  fft<PL, -1>(v, tw, xbuf, t, par, sync);
+  fft<PL, -1>(v, ftw, xbuf, t, par, sync);
   if (id >= RM) return;
   const float sc = 1.0f / (float)P;
 #pragma unroll

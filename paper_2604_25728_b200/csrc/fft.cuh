@@ -14,10 +14,13 @@
 // output lands in the same strided ownership as the input: an IFFT can follow an
 // FFT (or an epilogue + FFT can follow an IFFT) with no extra data movement.
 //
-// Shared-memory addresses are XOR-swizzled (i ^ ((i >> 4) & 15)) so that every
-// write pattern (stride-R for the first pass, contiguous afterwards) and every
-// strided read is bank-conflict free for 64-bit accesses.
-// Exchanges double-buffer (two P-element buffers) so one barrier per exchange.
+// Shared-memory addresses are padded (one float2 after every 16: i + i/16) so that
+// every write pattern (stride-R for the first pass, contiguous afterwards) and
+// every strided read is bank-conflict free for 64-bit accesses, and the unrolled
+// offsets stay compile-time constants.  Exchanges double-buffer (two padded
+// P-element buffers) so one barrier per exchange.
+// Stockham twiddles come from a per-P table in global memory (L1-resident,
+// [pass][r-1][j mod Ns] so a warp's loads coalesce), built in fp64 on the host.
 #pragma once
 #include <cuda_runtime.h>
 #include <type_traits>
@@ -127,7 +130,7 @@ __device__ __forceinline__ void dft(float2* v) {
   }
 }
 
-__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
 // Plan of a P-point transform carried by T = P/E threads.
 template <int P_, int E_>
@@ -136,35 +139,31 @@ struct Plan {
   static constexpr int LP = ilog2c(P_), LE = ilog2c(E_);
   static constexpr int NP = (LP + LE - 1) / LE;  // passes
   static constexpr int LAST_R = 1 << (LP - LE * (NP - 1));
+  static constexpr int PADDED = P_ + P_ / 16;  // float2 per exchange buffer
   static_assert((1 << LP) == P_ && (1 << LE) == E_ && E_ <= P_, "power-of-two sizes");
   __host__ __device__ static constexpr int R(int p) { return p < NP - 1 ? E : LAST_R; }
   __host__ __device__ static constexpr int NS(int p) { return 1 << (LE * p); }
+  // twiddle table: pass p >= 1 occupies NS(p) * (R(p) - 1) entries starting at twoff(p)
   __host__ __device__ static constexpr int twoff(int p) {
     int n = 0;
-    for (int q = 1; q < p; ++q) n += (E / R(q)) * (R(q) - 1);
+    for (int q = 1; q < p; ++q) n += NS(q) * (R(q) - 1);
     return n;
   }
-  static constexpr int NTW = twoff(NP) > 0 ? twoff(NP) : 1;  // per-thread twiddle registers
+  static constexpr int TWSIZE = twoff(NP) > 0 ? twoff(NP) : 1;
 };
 
-// Per-thread Stockham twiddles W_P^{-(j mod Ns) r P/(Ns R)} of the forward transform.
+// Host-side builder of the Stockham twiddle table (fp64 -> fp32):
+// tw[twoff(p) + (r-1) * Ns + jm] = e^{-2 pi i jm r / (Ns R)}.
 template <class PL>
-__device__ __forceinline__ void init_twiddles(float2 (&tw)[PL::NTW], int t) {
-  static_for<1, PL::NP>([&](auto pc) {
-    constexpr int p = decltype(pc)::value;
-    constexpr int R = PL::R(p), Ns = PL::NS(p), NB = PL::E / R;
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      int jm = (t + b * PL::T) & (Ns - 1);
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        int k = (jm * r * (PL::P / (Ns * R))) & (PL::P - 1);
-        float s, c;
-        sincospif(2.0f * (float)k / (float)PL::P, &s, &c);
-        tw[PL::twoff(p) + b * (R - 1) + r - 1] = make_float2(c, -s);
+inline void build_twiddle_table(float2* out) {
+  for (int p = 1; p < PL::NP; ++p) {
+    const int R = PL::R(p), Ns = PL::NS(p);
+    for (int r = 1; r < R; ++r)
+      for (int jm = 0; jm < Ns; ++jm) {
+        const double a = -2.0 * 3.14159265358979323846 * (double)jm * r / ((double)Ns * R);
+        out[PL::twoff(p) + (r - 1) * Ns + jm] = make_float2((float)cos(a), (float)sin(a));
       }
-    }
-  });
+  }
 }
 
 // Barrier among the threads of one FFT group.
@@ -181,25 +180,28 @@ struct GroupSync {
 };
 
 // In-place P-point transform of the group's data v (strided ownership in and out).
-// DIR = -1 forward, +1 unnormalized inverse.  sbuf: 2*P float2 of group-private smem.
+// DIR = -1 forward, +1 unnormalized inverse.  sbuf: 2 * PADDED float2 of group-private
+// smem; tw: the plan's twiddle table (global, read through L1).
 // par: exchange parity (alternates the two buffers); must start equal in all threads.
 template <class PL, int DIR>
-__device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2 (&tw)[PL::NTW], float2* sbuf,
-                                    int t, int& par, const GroupSync& sync) {
+__device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2* __restrict__ tw, float2* sbuf, int t,
+                                    int& par, const GroupSync& sync) {
   constexpr int E = PL::E, T = PL::T;
   static_for<0, PL::NP>([&](auto pc) {
     constexpr int p = decltype(pc)::value;
     constexpr int R = PL::R(p), Ns = PL::NS(p), NB = E / R;
-    float2* buf = sbuf + (par ? PL::P : 0);
+    float2* buf = sbuf + (par ? PL::PADDED : 0);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       float2 x[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = v[b + r * NB];
+      const int j = t + b * T;
       if constexpr (p > 0) {
+        const float2* twp = tw + PL::twoff(p) + (j & (Ns - 1));
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          float2 w = tw[PL::twoff(p) + b * (R - 1) + r - 1];
+          const float2 w = __ldg(twp + (r - 1) * Ns);
           x[r] = DIR < 0 ? cmul(x[r], w) : cmulc(x[r], w);
         }
       }
@@ -208,16 +210,17 @@ __device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2 (&tw)[PL::N
 #pragma unroll
         for (int r = 0; r < R; ++r) v[b + r * NB] = x[r];
       } else {
-        int j = t + b * T;
-        int base = (j / Ns) * Ns * R + (j & (Ns - 1));
+        const int base = (j / Ns) * Ns * R + (j & (Ns - 1));
+        float2* wb = buf + pad16(base);
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[swz(base + r * Ns)] = x[r];
+        for (int r = 0; r < R; ++r) wb[r * Ns + (r * Ns) / 16] = x[r];  // pad16(base + r Ns), Ns % 16 == 0 or Ns == 1
       }
     }
     if constexpr (p < PL::NP - 1) {
       sync();
+      const float2* rb = buf + pad16(t);
 #pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = buf[swz(t + i * T)];
+      for (int i = 0; i < E; ++i) v[i] = rb[i * T + (i * T) / 16];  // pad16(t + i T), T % 16 == 0
       par ^= 1;
     }
   });

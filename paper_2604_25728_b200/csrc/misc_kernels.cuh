@@ -22,87 +22,97 @@ struct Red {               // per restart, after combining all groups
 // (Eq. 43 with the nearest-level snap of Q12; decision in fp64 like the oracle).
 __global__ void k_hard_lut(int B, int BR, double c, const float* __restrict__ rho, int* __restrict__ lut,
                            int* __restrict__ status) {
-  const int r = blockIdx.x;
+  const int r = blockIdx.y;
   const float* rr = rho + (size_t)r * BR;
   int* out = lut + (size_t)r * (BR + 1);
-  const double a = 1.0 / (2.0 * B), W = 20.0 / c;
-  for (int i = threadIdx.x; i <= BR; i += blockDim.x) {
-    int k;
-    if (i == 0) {
-      k = 0;
-    } else if (i == BR) {
-      k = (int)floor(B * (2.0 * BR * a) + 0.5);
-    } else {
-      if (rr[i - 1] > rr[i]) atomicOr(status, ST_INVALID);
-      const double x = 0.5 * ((double)rr[i - 1] + (double)rr[i]);
-      int lo = 0, hi = BR;  // cnt = #{rho_j <= x}
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((double)rr[mid] <= x) lo = mid + 1; else hi = mid;
-      }
-      const int cnt = lo;
-      // window [i0, i1): |c (x - rho)| < 20 ; outside, tanh + 1 is 0 or 2 to < 1e-17
-      lo = 0; hi = BR;
-      while (lo < hi) { int mid = (lo + hi) >> 1; if ((double)rr[mid] < x - W) lo = mid + 1; else hi = mid; }
-      const int i0 = lo;
-      lo = 0; hi = BR;
-      while (lo < hi) { int mid = (lo + hi) >> 1; if ((double)rr[mid] <= x + W) lo = mid + 1; else hi = mid; }
-      const int i1 = lo;
-      double resid = 0.0;  // y = cnt/B + a * resid
-      for (int j = i0; j < i1; ++j) {
-        const double u = c * (x - (double)rr[j]);
-        const double e2 = exp(-2.0 * fabs(u));
-        const double tt = 2.0 * e2 / (1.0 + e2);  // 1 - tanh|u|
-        resid += (j >= cnt) ? tt : -tt;
-      }
-      k = cnt + (int)floor(0.5 * resid + 0.5);  // floor(B y + 1/2), B a = 1/2
-    }
-    out[i] = k;
+  const double W = 20.0 / c;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one warp per entry
+  if (i > BR) return;
+  if (i == 0 || i == BR) {
+    if (lane == 0) out[i] = i == 0 ? 0 : (int)floor(B * (2.0 * BR / (2.0 * B)) + 0.5);
+    return;
   }
+  if (lane == 0 && rr[i - 1] > rr[i]) atomicOr(status, ST_INVALID);
+  const double x = 0.5 * ((double)rr[i - 1] + (double)rr[i]);
+  int lo = 0, hi = BR;  // cnt = #{rho_j <= x}
+  while (lo < hi) { int mid = (lo + hi) >> 1; if ((double)rr[mid] <= x) lo = mid + 1; else hi = mid; }
+  const int cnt = lo;
+  // window [i0, i1): |c (x - rho)| < 20 ; outside, tanh + 1 is 0 or 2 to < 1e-17
+  lo = 0; hi = cnt;
+  while (lo < hi) { int mid = (lo + hi) >> 1; if ((double)rr[mid] < x - W) lo = mid + 1; else hi = mid; }
+  const int i0 = lo;
+  lo = cnt; hi = BR;
+  while (lo < hi) { int mid = (lo + hi) >> 1; if ((double)rr[mid] <= x + W) lo = mid + 1; else hi = mid; }
+  const int i1 = lo;
+  double resid = 0.0;  // y = cnt/B + a * resid
+  for (int j = i0 + lane; j < i1; j += 32) {
+    const double u = c * (x - (double)rr[j]);
+    const double e2 = exp(-2.0 * fabs(u));
+    const double tt = 2.0 * e2 / (1.0 + e2);  // 1 - tanh|u|
+    resid += (j >= cnt) ? tt : -tt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) resid += __shfl_xor_sync(0xffffffffu, resid, o);
+  if (lane == 0) out[i] = cnt + (int)floor(0.5 * resid + 0.5);  // floor(B y + 1/2), B a = 1/2
 }
 
 // y_soft = Q_A(z) (Eq. 24) as cnt/B + a*resid (integer plateau count + small residual, so the
 // phase 2 pi y keeps fp32 precision although y reaches r_n), s_soft = e^{j 2 pi y} (Eq. 23),
 // dq = Q_A'(z); hard: s_hard = e^{j 2 pi b / B}, b = lut[cnt] mod B.
-__global__ void k_quantize(int R, int MN, int B, int BR, float c, const float* __restrict__ z,
+// 8 lanes per element split the tanh window; fixed xor-shuffle order (deterministic).
+__global__ void k_quantize(int MN, int B, int BR, float c, const float* __restrict__ z,
                            const float* __restrict__ rho, const int* __restrict__ lut, float2* s_soft,
                            float2* s_hard, uint8_t* b_hard, float* dq) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= R * MN) return;
-  const int r = e / MN;
+  extern __shared__ float rs[];
+  constexpr int LPE = 8;
+  const int r = blockIdx.y;
   const float* rr = rho + (size_t)r * BR;
+  for (int i = threadIdx.x; i < BR; i += blockDim.x) rs[i] = rr[i];
+  __syncthreads();
+  const int sub = threadIdx.x & (LPE - 1);
+  const int e0 = blockIdx.x * (blockDim.x / LPE) + threadIdx.x / LPE;
+  const bool ok = e0 < MN;
+  const size_t e = (size_t)r * MN + (ok ? e0 : 0);
   const float x = z[e];
   int lo = 0, hi = BR;
-  while (lo < hi) { int mid = (lo + hi) >> 1; if (rr[mid] <= x) lo = mid + 1; else hi = mid; }
+  while (lo < hi) { int mid = (lo + hi) >> 1; if (rs[mid] <= x) lo = mid + 1; else hi = mid; }
   const int cnt = lo;
   if (s_soft || dq) {
     const float W = 12.0f / c;
-    lo = 0; hi = BR;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if (rr[mid] < x - W) lo = mid + 1; else hi = mid; }
+    lo = 0; hi = cnt;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (rs[mid] < x - W) lo = mid + 1; else hi = mid; }
     const int i0 = lo;
-    lo = 0; hi = BR;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if (rr[mid] <= x + W) lo = mid + 1; else hi = mid; }
+    lo = cnt; hi = BR;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (rs[mid] <= x + W) lo = mid + 1; else hi = mid; }
     const int i1 = lo;
     float resid = 0.f, sech = 0.f;
-    for (int j = i0; j < i1; ++j) {
-      const float u = c * (x - rr[j]);
-      const float e2 = expf(-2.f * fabsf(u));
-      const float inv = 1.f / (1.f + e2);
+    for (int j = i0 + sub; j < i1; j += LPE) {
+      const float u = c * (x - rs[j]);
+      const float e2 = __expf(-2.f * fabsf(u));
+      const float inv = __frcp_rn(1.f + e2);
       const float tt = 2.f * e2 * inv;
       resid += (j >= cnt) ? tt : -tt;
       sech += 4.f * e2 * inv * inv;
     }
+#pragma unroll
+    for (int o = LPE / 2; o > 0; o >>= 1) {
+      resid += __shfl_xor_sync(0xffffffffu, resid, o);
+      sech += __shfl_xor_sync(0xffffffffu, sech, o);
+    }
     const float a = 1.f / (2.f * B);
-    if (dq) dq[e] = a * c * sech;
-    if (s_soft) {
-      float ph = (float)(cnt % B) / (float)B + a * resid;
-      ph -= floorf(ph);
-      float sn, cs;
-      sincospif(2.f * ph, &sn, &cs);
-      s_soft[e] = make_float2(cs, sn);
+    if (ok && sub == 0) {
+      if (dq) dq[e] = a * c * sech;
+      if (s_soft) {
+        float ph = (float)(cnt % B) / (float)B + a * resid;
+        ph -= floorf(ph);
+        float sn, cs;
+        sincospif(2.f * ph, &sn, &cs);
+        s_soft[e] = make_float2(cs, sn);
+      }
     }
   }
-  if (s_hard || b_hard) {
+  if (ok && sub == 0 && (s_hard || b_hard)) {
     const int k = lut[(size_t)r * (BR + 1) + cnt];
     const int b = ((k % B) + B) % B;
     if (b_hard) b_hard[e] = (uint8_t)b;
@@ -186,6 +196,28 @@ __global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp
     red[r].key_a = ka[0];
     red[r].key_c = kc[0];
   }
+  // per-group rescale of the gradient partials to the restart's shift (used by the combine)
+  if (part.scale && mode != 0) {
+    for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
+      float sc = 0.f;
+      if (part.S[g] > 0.f && m > -INFINITY)
+        sc = (float)(mode == 1 ? exp(bp * ((double)part.m[g] - m)) : pow((double)part.m[g] / m, bp - 1.0));
+      part.scale[g] = sc;
+    }
+  }
+}
+
+// Multi-GPU: the shift m arrived from the all-reduce; refresh the per-group scales.
+__global__ void k_group_scales(int GPR, int g_lo, int g_hi, int mode, double bp, Part part, const Red* red) {
+  const int r = blockIdx.x;
+  const int lo = max(g_lo, r * GPR), hi = min(g_hi, (r + 1) * GPR);
+  const double m = red[r].m;
+  for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
+    float sc = 0.f;
+    if (part.S[g] > 0.f && m > -INFINITY)
+      sc = (float)(mode == 1 ? exp(bp * ((double)part.m[g] - m)) : pow((double)part.m[g] / m, bp - 1.0));
+    part.scale[g] = sc;
+  }
 }
 
 // Gradient partials -> red_grad[r][a][n] in true units of dL_wpsl / d(.)^*:
@@ -196,26 +228,23 @@ __global__ void k_combine_grad(int M, int N, int C, int g_lo, int g_hi, int mode
   const int r = ra / M;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
-  const double m = red[r].m, S = red[r].S;
-  double re = 0.0, im = 0.0;
-  if (m > -INFINITY && S > 0.0) {
-    for (int c = 0; c < C; ++c) {
-      const int g = ra * C + c;
-      if (g < g_lo || g >= g_hi) continue;
-      const double Sg = part.S[g];
-      if (!(Sg > 0.0)) continue;
-      const double mg = part.m[g];
-      const double sc = mode == 1 ? exp(bp * (mg - m)) : pow(mg / m, bp - 1.0);
+  const double S = red[r].S;
+  float re = 0.f, im = 0.f;
+  if (red[r].m > -INFINITY && S > 0.0) {
+    const int glo = max(g_lo, ra * C), ghi = min(g_hi, (ra + 1) * C);
+#pragma unroll 8
+    for (int g = glo; g < ghi; ++g) {
+      const float sc = part.scale[g];
       const float2 v = part.g[(size_t)g * N + n];
-      re += sc * v.x;
-      im += sc * v.y;
+      re = fmaf(sc, v.x, re);
+      im = fmaf(sc, v.y, im);
     }
     double norm = eps / (2.0 * N) * extra;
     norm *= (mode == 1) ? 1.0 / S : pow(S, 1.0 / bp - 1.0);
-    re *= norm;
-    im *= norm;
+    re = (float)(re * norm);
+    im = (float)(im * norm);
   }
-  red_grad[(size_t)ra * N + n] = make_float2((float)re, (float)im);
+  red_grad[(size_t)ra * N + n] = make_float2(re, im);
 }
 
 // ------------------------------------------------------------------ MAX-mode sparse adjoint
@@ -389,7 +418,7 @@ __global__ void k_finalize_grad(int R, int M, int N, int wrt, double eps, double
 // elements (partials [R][nchunk][BR], then a fixed-order sum).  Culled outside |c(z - rho)| < 12.
 __global__ void k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
                                 const float* __restrict__ rho, const float* __restrict__ dy, float* part) {
-  __shared__ float zs[256], ds[256];
+  __shared__ float zs[256], ds[256];  // chunk <= 256
   const int r = blockIdx.z;
   const int ch = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -479,20 +508,39 @@ __global__ void k_project_rho(int BR, float* rho, float lo, float hi, float gap,
   for (int i = threadIdx.x; i + 1 < BR; i += blockDim.x)
     if (sr[i] > sr[i + 1]) flag = 1;
   __syncthreads();
-  if (flag) {  // bitonic sort (rare: Adam steps are far smaller than the threshold spacing)
-    for (int kk = 2; kk <= n2; kk <<= 1)
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const bool up = (i & kk) == 0;
-            const float a = sr[i], b = sr[ixj];
-            if ((a > b) == up) { sr[i] = b; sr[ixj] = a; }
-          }
+  if (flag) {
+    // nearly sorted (Adam moves each threshold by ~lr per step): odd-even transposition
+    // rounds with early exit; a full bitonic sort only if that does not converge.
+    __shared__ int swapped;
+    int rounds = 0;
+    do {
+      __syncthreads();
+      if (threadIdx.x == 0) swapped = 0;
+      __syncthreads();
+      for (int ph = 0; ph < 2; ++ph) {
+        for (int i = 2 * threadIdx.x + ph; i + 1 < BR; i += 2 * blockDim.x) {
+          const float a = sr[i], b = sr[i + 1];
+          if (a > b) { sr[i] = b; sr[i + 1] = a; swapped = 1; }
         }
         __syncthreads();
       }
+    } while (swapped && ++rounds < 64);
+    if (swapped) {
+      for (int kk = 2; kk <= n2; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+            const int ixj = i ^ j;
+            if (ixj > i) {
+              const bool up = (i & kk) == 0;
+              const float a = sr[i], b = sr[ixj];
+              if ((a > b) == up) { sr[i] = b; sr[ixj] = a; }
+            }
+          }
+          __syncthreads();
+        }
+    }
   }
+  __syncthreads();
   for (int i = threadIdx.x; i < BR; i += blockDim.x) sr[i] = fminf(fmaxf(sr[i], lo), hi);
   __syncthreads();
   if (threadIdx.x == 0) flag = 0;
@@ -500,8 +548,26 @@ __global__ void k_project_rho(int BR, float* rho, float lo, float hi, float gap,
   for (int i = threadIdx.x + 1; i < BR; i += blockDim.x)
     if (sr[i] < sr[i - 1] + gap) flag = 1;
   __syncthreads();
-  if (flag && threadIdx.x == 0)
-    for (int i = 1; i < BR; ++i) sr[i] = fmaxf(sr[i], sr[i - 1] + gap);
+  if (flag) {
+    // forward sweep rho_i = max(rho_i, rho_{i-1} + gap) == max_{j<=i}(rho_j + (i-j) gap):
+    // inclusive prefix max of q_j = rho_j - j gap (Hillis-Steele), value kept exact where inactive.
+    float* q = sr + n2;
+    for (int i = threadIdx.x; i < BR; i += blockDim.x) q[i] = sr[i] - (float)i * gap;
+    __syncthreads();
+    for (int off = 1; off < BR; off <<= 1) {
+      float tmp[8];
+      int cnt = 0;
+      for (int i = threadIdx.x; i < BR; i += blockDim.x) tmp[cnt++] = (i >= off) ? fmaxf(q[i], q[i - off]) : q[i];
+      __syncthreads();
+      cnt = 0;
+      for (int i = threadIdx.x; i < BR; i += blockDim.x) q[i] = tmp[cnt++];
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < BR; i += blockDim.x) {
+      const float qi = sr[i] - (float)i * gap;
+      if (q[i] > qi) sr[i] = q[i] + (float)i * gap;
+    }
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < BR; i += blockDim.x) p[i] = sr[i];
 }

@@ -23,9 +23,11 @@ namespace {
 
 thread_local std::string g_last_error;
 
-// Launch geometry per FFT length: E elements per thread, G groups per CTA.
+// Launch geometry per FFT length: E elements per thread, G groups per CTA, and the
+// minimum resident CTAs per SM handed to __launch_bounds__ (caps registers at 128).
 constexpr int plan_E(int P) { return P <= 16 ? P : 16; }
 constexpr int plan_G(int P) { return (P / plan_E(P)) >= 128 ? 1 : 128 / (P / plan_E(P)); }
+constexpr int plan_MINB(int P) { return (P / plan_E(P)) * plan_G(P) >= 512 ? 1 : (P / plan_E(P)) * plan_G(P) >= 256 ? 2 : 4; }
 
 }  // namespace
 
@@ -41,6 +43,8 @@ struct sqngd_ctx_s {
   // device workspace
   float2* tw = nullptr;     // [K][N] e^{j 2 pi (n+1) f_k / N} (fp64-built)
   float2* H = nullptr;      // [R][M][P] filter spectra / P
+  float2* Xc = nullptr;     // [R][M][K][P] X cache: FFT_P of the Doppler-modulated codes (a3)
+  float2* ftw = nullptr;    // Stockham twiddle table of the plan
   float2* s_soft = nullptr; // [R][M][N]
   float2* s_hard = nullptr;
   float* dq = nullptr;      // [R][M][N]
@@ -51,7 +55,7 @@ struct sqngd_ctx_s {
   float2* red_grad = nullptr;  // [R][M][N]
   float* dy = nullptr;         // [R][M][N]
   float* rho_part = nullptr;   // [R][nchunk][BR]
-  int rho_chunk = 1024, rho_nchunk = 1;
+  int rho_chunk = 256, rho_nchunk = 1;
   float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
   float* gz = nullptr;         // [R][M][N]
   float* grho = nullptr;       // [R][BR]
@@ -116,43 +120,56 @@ struct Launch {
   static constexpr int E = plan_E(P);
   using PL = Plan<P, E>;
   static constexpr int G = plan_G(P);
+  static constexpr int MINB = plan_MINB(P);
   static constexpr int THREADS = PL::T * G;
 
   template <int MODE>
   static size_t smem() { return (size_t)G * GroupSmem<PL, MODE>::TOTAL * sizeof(float2); }
-  static size_t smem_filter() { return (size_t)G * (PL::NP > 1 ? 2 * P : 0) * sizeof(float2) + 16; }
+  static size_t smem_fft() { return (size_t)G * (PL::NP > 1 ? 2 * PL::PADDED : 0) * sizeof(float2) + 16; }
 
   static cudaError_t prepare(int* blocks_per_sm) {
     cudaError_t e;
-    e = cudaFuncSetAttribute(k_af<PL, G, MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_FWD>());
+    e = cudaFuncSetAttribute(k_af<PL, G, MINB, MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_FWD>());
     if (e) return e;
-    e = cudaFuncSetAttribute(k_af<PL, G, MODE_ADJ_A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_ADJ_A>());
+    e = cudaFuncSetAttribute(k_af<PL, G, MINB, MODE_ADJ_A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_ADJ_A>());
     if (e) return e;
-    e = cudaFuncSetAttribute(k_af<PL, G, MODE_ADJ_B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_ADJ_B>());
+    e = cudaFuncSetAttribute(k_af<PL, G, MINB, MODE_ADJ_B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<MODE_ADJ_B>());
     if (e) return e;
-    e = cudaFuncSetAttribute(k_filter_fft<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_filter());
+    e = cudaFuncSetAttribute(k_filter_fft<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
     if (e) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MODE_FWD>, THREADS, smem<MODE_FWD>());
+    e = cudaFuncSetAttribute(k_xhat<PL, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
     if (e) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], k_af<PL, G, MODE_ADJ_A>, THREADS, smem<MODE_ADJ_A>());
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MINB, MODE_FWD>, THREADS, smem<MODE_FWD>());
     if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[2], k_af<PL, G, MODE_ADJ_B>, THREADS, smem<MODE_ADJ_B>());
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], k_af<PL, G, MINB, MODE_ADJ_A>, THREADS, smem<MODE_ADJ_A>());
+    if (e) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[2], k_af<PL, G, MINB, MODE_ADJ_B>, THREADS, smem<MODE_ADJ_B>());
   }
-  static void filter(int RM, int N, const float2* w, float2* H, cudaStream_t st) {
+  static std::vector<float2> twiddles() {
+    std::vector<float2> t(PL::TWSIZE, make_float2(1.f, 0.f));
+    build_twiddle_table<PL>(t.data());
+    return t;
+  }
+  static void filter(int RM, int N, const float2* w, const float2* ftw, float2* H, cudaStream_t st) {
     const int blocks = (RM + G - 1) / G;
-    k_filter_fft<PL, G><<<blocks, THREADS, smem_filter(), st>>>(RM, N, w, H);
+    k_filter_fft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(RM, N, w, ftw, H);
   }
-  static void af(int mode, const KP& kp, const float2* s, const float2* H, const float2* tw, float* af_mag,
-                 const Part& part, cudaStream_t st) {
+  static void xhat(int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftw, float2* Xc,
+                   cudaStream_t st) {
+    const int blocks = (units + G - 1) / G;
+    k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(units, M, N, K, s, dtw, ftw, Xc);
+  }
+  static void af(int mode, const KP& kp, const float2* Xc, const float2* H, const float2* tw, const float2* ftw,
+                 float* af_mag, const Part& part, cudaStream_t st) {
     const int groups = kp.g_hi - kp.g_lo;
     if (groups <= 0) return;
     const int blocks = (groups + G - 1) / G;
     if (mode == MODE_FWD)
-      k_af<PL, G, MODE_FWD><<<blocks, THREADS, smem<MODE_FWD>(), st>>>(kp, s, H, tw, af_mag, part);
+      k_af<PL, G, MINB, MODE_FWD><<<blocks, THREADS, smem<MODE_FWD>(), st>>>(kp, Xc, H, tw, ftw, af_mag, part);
     else if (mode == MODE_ADJ_A)
-      k_af<PL, G, MODE_ADJ_A><<<blocks, THREADS, smem<MODE_ADJ_A>(), st>>>(kp, s, H, tw, nullptr, part);
+      k_af<PL, G, MINB, MODE_ADJ_A><<<blocks, THREADS, smem<MODE_ADJ_A>(), st>>>(kp, Xc, H, tw, ftw, nullptr, part);
     else
-      k_af<PL, G, MODE_ADJ_B><<<blocks, THREADS, smem<MODE_ADJ_B>(), st>>>(kp, s, H, tw, nullptr, part);
+      k_af<PL, G, MINB, MODE_ADJ_B><<<blocks, THREADS, smem<MODE_ADJ_B>(), st>>>(kp, Xc, H, tw, ftw, nullptr, part);
   }
   static int groups_per_block() { return G; }
 };
@@ -290,10 +307,12 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, cuda_device));
   int bps[3] = {1, 1, 1}, G = 1;
   cudaError_t perr = cudaSuccess;
+  std::vector<float2> ftw_host;
   bool okP = with_P(P, [&](auto Lc) {
     using LC = decltype(Lc);
     perr = LC::prepare(bps);
     G = LC::groups_per_block();
+    ftw_host = LC::twiddles();
   });
   if (!okP) {
     delete ctx;
@@ -313,6 +332,10 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
   CK(cudaMalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
   CK(cudaMalloc(&ctx->H, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
+  CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * cfg.K * P));
+  CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
+  CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->part.scale, sizeof(float) * ctx->gtot_max));
   CK(cudaMalloc(&ctx->s_soft, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->dq, sizeof(float) * RMN));
@@ -366,7 +389,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
 void sqngd_destroy(sqngd_ctx ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
-  void* ptrs[] = {ctx->tw, ctx->H, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+  void* ptrs[] = {ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status};
   for (void* p : ptrs)
@@ -433,21 +456,31 @@ static sqngd_status run_quantize(sqngd_ctx ctx, const float* z, const float* rho
                                  uint8_t* b_hard, float* dq, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   if (s_hard || b_hard) {
-    k_hard_lut<<<c.R, 256, 0, st>>>(c.B, ctx->BR, c.c, rho, ctx->lut, ctx->status);
+    k_hard_lut<<<dim3((ctx->BR + 1 + 7) / 8, c.R), 256, 0, st>>>(c.B, ctx->BR, c.c, rho, ctx->lut, ctx->status);
     ctx->launches += 1;
   }
   ctx->launches += 1;
-  const int n = c.R * c.M * c.N;
-  k_quantize<<<(n + 255) / 256, 256, 0, st>>>(c.R, c.M * c.N, c.B, ctx->BR, (float)c.c, z, rho, ctx->lut, s_soft,
-                                               s_hard, b_hard, dq);
+  const int MN = c.M * c.N;
+  k_quantize<<<dim3((MN + 31) / 32, c.R), 256, ctx->BR * sizeof(float), st>>>(MN, c.B, ctx->BR, (float)c.c, z, rho,
+                                                                                ctx->lut, s_soft, s_hard, b_hard, dq);
   return launch_check(ctx, "quantize");
 }
 
 static sqngd_status run_filter_fft(sqngd_ctx ctx, const float2* w, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
-  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::filter(c.R * c.M, c.N, w, ctx->H, st); });
+  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::filter(c.R * c.M, c.N, w, ctx->ftw, ctx->H, st); });
   ctx->launches += 1;
   return launch_check(ctx, "filter fft");
+}
+
+// a3: X cache of the waveform s (all units; each rank only needs its slice but the cache
+// is cheap next to the M^2 K correlations and keeps the slice logic in one place).
+static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  const int units = c.R * c.M * c.K;
+  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::xhat(units, c.M, c.N, c.K, s, ctx->tw, ctx->ftw, ctx->Xc, st); });
+  ctx->launches += 1;
+  return launch_check(ctx, "xhat");
 }
 
 // Multi-GPU: max-then-sum protocol over the per-restart partials.
@@ -455,12 +488,18 @@ static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad
 
 // Forward AF + metrics of (s, w).  Assumes H = FFT(w) is current.
 static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w, float* af_mag, MetricsOut* met,
-                                double* p_out, double* hist, int hist_col, cudaStream_t st) {
+                                double* p_out, double* hist, int hist_col, cudaStream_t st, bool xhat_ready = false) {
   const sqngd_config& c = ctx->cfg;
+  if (!xhat_ready) {
+    sqngd_status rx = run_xhat(ctx, s, st);
+    if (rx) return rx;
+  }
   KP kp = make_kp(ctx, MODE_FWD, c.loss_mode != 0);
   {
     ProfScope ps(ctx, MODE_FWD, st);
-    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::af(MODE_FWD, kp, s, ctx->H, ctx->tw, af_mag, ctx->part, st); });
+    with_P(ctx->P, [&](auto Lc) {
+      decltype(Lc)::af(MODE_FWD, kp, ctx->Xc, ctx->H, ctx->tw, ctx->ftw, af_mag, ctx->part, st);
+    });
   }
   ctx->launches += 4;
   sqngd_status rc = launch_check(ctx, "af forward");
@@ -479,12 +518,13 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
 // wrt 1: writes grad_w (2 dL/dw^*); wrt 2: grad_s (dL/ds^*), dy and grad_z if dq/grad_z given.
 static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* w, int wrt, MetricsOut* met,
                                   float2* grad_w, float2* grad_s, const float* dq, float* grad_z, double* hist,
-                                  int hist_col, cudaStream_t st) {
+                                  int hist_col, cudaStream_t st, bool xhat_ready = false) {
   const sqngd_config& c = ctx->cfg;
   sqngd_status rc;
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
+  if (!xhat_ready && (rc = run_xhat(ctx, s, st))) return rc;
   if (c.loss_mode == SQNGD_LOSS_MAX) {
-    if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st))) return rc;
+    if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st, true))) return rc;
     ctx->launches += 1;
     k_sparse_adj<<<c.R, 256, 0, st>>>(c.M, c.N, c.K, ctx->L, wrt, c.eps_w, c.weights, s, w, ctx->tw, ctx->red,
                                       ctx->red_grad);
@@ -494,16 +534,21 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     KP kp = make_kp(ctx, mode, 1);
     {
       ProfScope ps(ctx, mode, st);
-      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::af(mode, kp, s, ctx->H, ctx->tw, nullptr, ctx->part, st); });
+      with_P(ctx->P, [&](auto Lc) {
+        decltype(Lc)::af(mode, kp, ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
+      });
     }
     ctx->launches += 5;
     if ((rc = launch_check(ctx, "af adjoint"))) return rc;
     k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part,
                                          ctx->red);
-    if (ctx->world > 1 && (rc = allreduce_red(ctx, st, false, mode))) return rc;
-    dim3 grid((c.N + 255) / 256, c.R * c.M);
+    if (ctx->world > 1) {
+      if ((rc = allreduce_red(ctx, st, false, mode))) return rc;
+      k_group_scales<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
+    }
+    dim3 grid((c.N + 127) / 128, c.R * c.M);
     const double extra = mode == MODE_ADJ_A ? 1.0 / ctx->P : 1.0;
-    k_combine_grad<<<grid, 256, 0, st>>>(c.M, c.N, kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, c.eps_w,
+    k_combine_grad<<<grid, 128, 0, st>>>(c.M, c.N, kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, c.eps_w,
                                          extra, ctx->part, ctx->red, ctx->red_grad);
     if (ctx->world > 1 && (rc = allreduce_red(ctx, st, true, mode))) return rc;
     k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
@@ -523,7 +568,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
 static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho, float* grad_rho, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   const int MN = c.M * c.N;
-  dim3 g1((ctx->BR + 127) / 128, ctx->rho_nchunk, c.R);
+  dim3 g1((ctx->BR + 127) / 128, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
   k_grad_rho_part<<<g1, 128, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part);
   dim3 g2((ctx->BR + 127) / 128, c.R);
   const float coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
@@ -626,10 +671,11 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
   };
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
+    if ((rc = run_xhat(ctx, ctx->s_hard, st))) return rc;  // X_hard fixed for the whole block
     for (int i = 0; i < c.n_h; ++i) {
       if ((rc = run_filter_fft(ctx, w2, st))) return rc;
       if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, ctx->gw, nullptr, nullptr, nullptr,
-                              loss_hist, i, st)))
+                              loss_hist, i, st, true)))
         return rc;
       stt->t_a += 1;
       adam(2 * RMN, stt->w, stt->m_w, stt->v_w, reinterpret_cast<const float*>(ctx->gw), stt->t_a, c.lr_w);
@@ -652,7 +698,7 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
       adam((size_t)c.R * ctx->BR, stt->rho, stt->m_rho, stt->v_rho, ctx->grho, stt->t_b, c.lr_z);
       int n2 = 1;
       while (n2 < ctx->BR) n2 <<= 1;
-      k_project_rho<<<c.R, 1024, n2 * sizeof(float), st>>>(ctx->BR, stt->rho, 1e-4f, 1.0f - 1e-4f, 1e-6f, ctx->status);
+      k_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, 1e-4f, 1.0f - 1e-4f, 1e-6f, ctx->status);
       ctx->launches += 1;
       if ((rc = launch_check(ctx, "step B update"))) return rc;
     }
