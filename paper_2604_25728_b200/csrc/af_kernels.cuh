@@ -6,25 +6,27 @@
 //   k_xhat, unit (r, m, k):                        a3
 //     x_hat = s_m . e^{j 2 pi n f_k / N}            Eq. 33 (twiddle table built in fp64)
 //     X_{m,k} = FFT_P(x_hat_pad)  -> X cache [R][M][K][P] (L2-resident for C1-C4)
-//   forward (MODE_FWD), group (r, m, chunk of k):   a4-a5
+//   The fused kernel is persistent: each group pulls units (r, a, k) from an atomic
+//   counter and writes that unit's partials into the unit's own slot, so the load is
+//   balanced across SMs while every sum stays in a fixed order (deterministic).
+//   forward (MODE_FWD), unit (r, m, k):              a4-a5
 //     for l: r = IFFT_P(X . conj(H_l)/P)            Eq. 36; A(tau) = r[(-tau) mod P] (Q1)
-//            fused epilogue: |A|, ROI mask, packed (value, ~index) max keys for
-//            WAPSL / WCPSL (Eqs. 7-9), LSE / p-norm partial sums, optional |A| map.
-//   Step B adjoint (MODE_ADJ_B), group (r, m, chunk of k):  a4-a7, a8B
+//            fused epilogue: |A|, ROI mask, (value, index) max keys for WAPSL /
+//            WCPSL (Eqs. 7-9), LSE / p-norm partial sums, optional |A| map.
+//   Step B adjoint (MODE_ADJ_B), unit (r, m, k):     a4-a7, a8B
 //     per l: r, then G = dL/dA^* (unnormalized: phi * w * A / |A|) in place,
-//     G_hat = FFT_P(G), acc += G_hat . H_l/P;  after the l loop e = IFFT_P(acc) and
-//     the group adds conj(e^{j 2 pi n f/N}) e[n] into its per-(r, m) partial.
-//   Step A adjoint (MODE_ADJ_A), group (r, l, chunk of k), loop (k, m):  a4-a7, a8A
-//     r, G, G_hat as above and acc += X . conj(G_hat); at the end of the chunk
-//     d = IFFT_P(acc) is the group's dL/dw_l^* partial.
+//     G_hat = FFT_P(G), acc += G_hat . H_l/P;  after the l loop e = IFFT_P(acc),
+//     demodulated by conj(e^{j 2 pi n f/N}) -> the unit's time-domain slot.
+//   Step A adjoint (MODE_ADJ_A), unit (r, l, k), loop over m:   a4-a7, a8A
+//     r, G, G_hat as above and acc += X . conj(G_hat) -> the unit's spectral slot;
+//     the combine sums the slots over k and one IFFT_P per filter gives dL/dw_l^*.
+//   Every transform of a unit runs through ONE inlined forward FFT (a phase loop):
+//   IFFT(x) = conj(FFT(conj x)), the conjugations folded into the adjacent products.
 //
-// The cotangent needs the LSE / p-norm normalizer of the *whole* loss, so the
-// adjoint kernels accumulate with a group-uniform running shift m (online
-// rescaling): phi = e^{beta (v - m)} (LSE) or (v / m)^{p-1} (PNORM); the combine
-// kernel rescales every group to the global shift, so one pass is exact.
-//
-// Reductions are deterministic: fixed per-group partial slots, fixed-order
-// combine, no floating-point atomics.
+// The cotangent needs the LSE / p-norm normalizer of the *whole* loss, so each unit
+// accumulates with a unit-uniform running shift m (online rescaling):
+// phi = e^{beta (v - m)} (LSE) or (v / m)^{p-1} (PNORM); the combine rescales every
+// unit to the restart's global shift, so one pass is exact.
 #pragma once
 #include <stdint.h>
 
@@ -41,17 +43,17 @@ struct KP {
   float beta_or_p;
   float invN;
   const float* weights;  // [K][L] or nullptr
-  int C, chunk;          // Doppler chunks per (r, a) and bins per chunk
-  int g_lo, g_hi;        // groups evaluated by this rank (multi-GPU slice)
+  int u_lo, u_hi;        // units evaluated by this rank (multi-GPU slice of R*M*K)
   int want_S;            // forward: accumulate surrogate sums
+  int* counter;          // dynamic unit counter (zeroed before the launch)
 };
 
-struct Part {
-  unsigned long long* key;  // [Gtot][2]  (auto, cross)
-  float* m;                 // [Gtot] shift of the group's sums
-  float* S;                 // [Gtot] sum of phi (LSE: e^{b(v-m)}, PNORM: (v/m)^p)
-  float* scale;             // [Gtot] rescale to the restart's global shift (combine)
-  float2* g;                // [Gtot][N] adjoint partial (time domain)
+struct Part {                // one slot per unit u = (r * M + a) * K + k
+  unsigned long long* key;  // [U][2]  (auto, cross)
+  float* m;                 // [U] shift of the unit's sums
+  float* S;                 // [U] sum of phi (LSE: e^{b(v-m)}, PNORM: (v/m)^p)
+  float* scale;             // [U] rescale to the restart's global shift (combine)
+  float2* g;                // [U][P] adjoint partial: Step B time domain (N used), Step A spectral
 };
 
 __device__ __forceinline__ unsigned long long pack_key(float val, uint32_t idx) {
@@ -127,10 +129,10 @@ struct Group {
 template <class PL, int MODE>
 struct GroupSmem {
   static constexpr int XBUF = PL::NP > 1 ? 2 * PL::PADDED : 0;
-  static constexpr int GACC = MODE == MODE_ADJ_B ? PL::P / 2 : 0;  // N <= P/2
-  static constexpr int RED = 32;                                    // 64 floats (2 x 32)
-  static constexpr int REDK = 64;                                   // 64 u64 (2 x 32)
-  static constexpr int TOTAL = XBUF + GACC + RED + REDK;
+  static constexpr int RED = 32;    // 64 floats (2 x 32)
+  static constexpr int REDK = 64;   // 64 u64 (2 x 32)
+  static constexpr int GRAB = 1;    // 2 ints: the unit index broadcast (double-buffered)
+  static constexpr int TOTAL = XBUF + RED + REDK + GRAB;
 };
 
 // Per-thread ROI bitmasks over its E elements (bit i <-> j = t + i T), weights aside:
@@ -155,6 +157,108 @@ __device__ __forceinline__ void best_update(float kv, uint32_t idx, float& best,
   if (kv > best || (kv == best && idx < bidx)) {
     best = kv;
     bidx = idx;
+  }
+}
+
+// MUFU approximations (no denormal fix-up code): 2^x and 1/sqrt(x), |rel err| ~ 2^-22.
+__device__ __forceinline__ float ex2a(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2a(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqa(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Per-slice constants of the epilogue.
+struct SliceCtx {
+  uint32_t roi;         // ROI bitmask of this thread's elements for this map (auto / cross)
+  const float* wrow;    // weights row (HW) centred at tau = 0
+  uint32_t base_idx;    // (m M + l) L + N - 1
+  int k;
+};
+
+// Lowest cell index among this thread's in-ROI elements whose key value equals kv
+// (the rare path of the running argmax: taken only when a slice reaches the running max).
+template <class PL, bool HW>
+__device__ __forceinline__ uint32_t argmax_index(const float2 (&v)[PL::E], float kv, const SliceCtx& sc, int t, int N,
+                                              int K) {
+  uint32_t best = 0xFFFFFFFFu;
+#pragma unroll
+  for (int i = 0; i < PL::E; ++i) {
+    if (!((sc.roi >> i) & 1u)) continue;
+    const int lag = lag_of(t + i * PL::T, N, PL::P);
+    float x = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
+    if (HW) {
+      const float wt = __ldg(sc.wrow + lag);
+      if (!(wt > 0.f)) continue;
+      x *= wt * wt;
+    }
+    if (x == kv) {
+      const uint32_t idx = (sc.base_idx + (uint32_t)lag) * (uint32_t)K + (uint32_t)sc.k;
+      best = idx < best ? idx : best;
+    }
+  }
+  return best;
+}
+
+// Pass 1 of the cell epilogue: max over the thread's in-ROI cells of w^2 |A|^2 (-1 if none).
+template <class PL, bool HW>
+__device__ __forceinline__ float slice_max2(const float2 (&v)[PL::E], const SliceCtx& sc, int t, int N) {
+  float lmax2 = -1.f;
+#pragma unroll
+  for (int i = 0; i < PL::E; ++i) {
+    float kv = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
+    if (HW) {
+      const float wt = ((sc.roi >> i) & 1u) ? __ldg(sc.wrow + lag_of(t + i * PL::T, N, PL::P)) : 0.f;
+      kv = wt > 0.f ? kv * wt * wt : -1.f;
+    } else {
+      kv = ((sc.roi >> i) & 1u) ? kv : -1.f;
+    }
+    lmax2 = fmaxf(lmax2, kv);
+  }
+  return lmax2;
+}
+
+// Pass 2: surrogate terms phi with shift `shift` (LSE: e^{b(v-m)}, PNORM: (v/m)^p), summed
+// into Ssum; if GRAD, v <- G = gphi w A / |A| (v holds conj(A) on entry, hence the sign).
+// v = w |A| / N.  Cells outside the ROI get phi = 0 and G = 0; |A| = 0 gives G = 0.
+template <class PL, bool HW, int LM, bool GRAD>
+__device__ __forceinline__ void slice_terms(float2 (&v)[PL::E], const SliceCtx& sc, int t, int N, float invN,
+                                            float shift, float bp, float& Ssum) {
+  const float lb = bp * 1.4426950408889634f;
+  const float lbN = lb * invN, lbs = lb * shift;        // LSE: phi = 2^{lbN |A| w - lb m}
+  const float qN = shift > 0.f ? invN / shift : 0.f;    // PNORM: q = w |A| / (N m)
+#pragma unroll
+  for (int i = 0; i < PL::E; ++i) {
+    const float a2 = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
+    const float rsq = rsqa(fmaxf(a2, 1e-30f));
+    const float mag = a2 * rsq;
+    float wt = 1.f;
+    if (HW) wt = ((sc.roi >> i) & 1u) ? __ldg(sc.wrow + lag_of(t + i * PL::T, N, PL::P)) : 0.f;
+    const bool in = HW ? (wt > 0.f) : (((sc.roi >> i) & 1u) != 0u);
+    float phi, gphi;
+    if (LM == 1) {
+      phi = ex2a(fmaf(lbN, HW ? wt * mag : mag, -lbs));
+      gphi = phi;
+    } else {
+      const float q = (HW ? wt * mag : mag) * qN;
+      gphi = ex2a((bp - 1.f) * lg2a(q));  // q^(p-1); 0 at q = 0
+      phi = gphi * q;
+    }
+    phi = in ? phi : 0.f;
+    Ssum += phi;
+    if (GRAD) {
+      const float gfac = in ? gphi * (HW ? wt * rsq : rsq) : 0.f;
+      v[i] = make_float2(v[i].x * gfac, -v[i].y * gfac);
+    }
   }
 }
 
@@ -195,70 +299,83 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   using GS = GroupSmem<PL, MODE>;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
-  const int gg = kp.g_lo + blockIdx.x * G + grp;
   float2* gsm = reinterpret_cast<float2*>(smem_raw) + grp * GS::TOTAL;
   float2* xbuf = gsm;
-  float2* gacc = gsm + GS::XBUF;
+  int* grab = reinterpret_cast<int*>(gsm + GS::XBUF + GS::RED + GS::REDK);
 
   Group<T> grpops;
   grpops.sync = GroupSync{1 + grp, T, group_mask(T)};
   grpops.mask = grpops.sync.mask;
-  grpops.red = reinterpret_cast<float*>(gsm + GS::XBUF + GS::GACC);
-  grpops.redk = reinterpret_cast<unsigned long long*>(gsm + GS::XBUF + GS::GACC + GS::RED);
+  grpops.red = reinterpret_cast<float*>(gsm + GS::XBUF);
+  grpops.redk = reinterpret_cast<unsigned long long*>(gsm + GS::XBUF + GS::RED);
   grpops.par = 0;
   grpops.t = t;
 
-  const bool active = gg < kp.g_hi;
   const int M = kp.M, N = kp.N, K = kp.K;
-  const int ra = active ? gg / kp.C : 0, c = active ? gg % kp.C : 0;
-  const int r = ra / M, a = ra % M;
-  const int k0 = c * kp.chunk;
-  const int k1 = active ? min(K, k0 + kp.chunk) : k0;
-
-  int par = 0;
-  float best_a = -1.f, best_c = -1.f;  // running max of w^2 |A|^2 (auto, cross) and its cell index
-  uint32_t bidx_a = 0xFFFFFFFFu, bidx_c = 0xFFFFFFFFu;
+  const int mode = kp.loss_mode;
+  const float bp = kp.beta_or_p;
+  const float lb = bp * 1.4426950408889634f;  // e^{b x} = 2^{lb x}
   uint32_t roi_auto, roi_cross;
   roi_masks<PL>(kp, t, roi_auto, roi_cross);
   const bool has_w = kp.weights != nullptr;
-  const int mode = kp.loss_mode;
-  const float bp = kp.beta_or_p;
-  float shift = (mode == 2) ? 0.f : -INFINITY;  // forward: per-thread; adjoint: group-uniform
-  float Ssum = 0.f;
-
+  int par = 0, gpar = 0;
+  int cur_r = -1;
+  unsigned long long key_a = 0ull, key_c = 0ull;  // packed (w^2 |A|^2, ~index) maxima
   float2 v[E];
   float2 acc[MODE == MODE_FWD ? 1 : E];
-  if constexpr (MODE != MODE_FWD) {
-#pragma unroll
-    for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
-  }
-  if constexpr (MODE == MODE_ADJ_B) {
-    for (int n = t; n < N; n += T) gacc[n] = make_float2(0.f, 0.f);
-  }
 
-  const int inner = (MODE == MODE_ADJ_A) ? M : 1;
-  for (int k = k0; k < k1; ++k) {
-    for (int mi = 0; mi < inner; ++mi) {
-      const int m = (MODE == MODE_ADJ_A) ? mi : a;
+  for (;;) {
+    // ---- dynamic unit scheduling: one atomic per unit, broadcast through smem
+    if (t == 0) grab[gpar] = atomicAdd(kp.counter, 1);
+    grpops.sync();
+    const int u = kp.u_lo + grab[gpar];
+    gpar ^= 1;
+    if (u >= kp.u_hi) break;
+    const int k = u % K, ra = u / K;
+    const int r = ra / M, a = ra % M;
+    const float* wrow = has_w ? kp.weights + (size_t)k * kp.L + N - 1 : nullptr;
+
+    float shift = (mode == 2) ? 0.f : -INFINITY;  // unit-uniform running shift of the sums
+    float Ssum = 0.f;
+    if (r != cur_r) {  // group-uniform running (value, index) maxima, kept across units of one restart
+      cur_r = r;
+      key_a = key_c = 0ull;
+    }
+    if constexpr (MODE != MODE_FWD) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
+    }
+
+    // Phases: FWD: M slices; ADJ_A: (slice, G) x M; ADJ_B: (slice, G) x M + final IFFT(acc).
+    const int nph = (MODE == MODE_FWD) ? M : (MODE == MODE_ADJ_B ? 2 * M + 1 : 2 * M);
+#pragma unroll 1
+    for (int ph = 0; ph < nph; ++ph) {
+      const bool final_ph = (MODE == MODE_ADJ_B) && ph == 2 * M;
+      const bool slice_ph = (MODE == MODE_FWD) || (!final_ph && (ph & 1) == 0);
+      const int li = (MODE == MODE_FWD) ? ph : (ph >> 1);
+      const int m = (MODE == MODE_ADJ_A) ? li : a;
+      const int l = (MODE == MODE_ADJ_A) ? a : li;
       const float2* Xr = Xc + (((size_t)r * M + m) * K + k) * P;
-      if constexpr (MODE == MODE_ADJ_B) {
+      const float2* Hl = Hh + ((size_t)r * M + (final_ph ? 0 : l)) * P;
+      // ---- pre: the transform's input
+      if (slice_ph) {
+        // a4: conj(X . conj(H_l)/P) = conj(X) . H_l/P ; FFT of the conjugate = conj(IFFT) (Eq. 36)
 #pragma unroll
-        for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
-      }
-      const int l_lo = (MODE == MODE_ADJ_A) ? a : 0, l_hi = (MODE == MODE_ADJ_A) ? a + 1 : M;
-      for (int l = l_lo; l < l_hi; ++l) {
-        const float2* Hl = Hh + ((size_t)r * M + l) * P;
+        for (int i = 0; i < E; ++i) v[i] = cmulc(__ldg(Hl + t + i * T), __ldg(Xr + t + i * T));
+      } else if (final_ph) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = make_float2(acc[i].x, -acc[i].y);
+      }  // G phase: v already holds G
+      fft<PL, -1>(v, ftw, xbuf, t, par, grpops.sync);
+      // ---- post
+      if (slice_ph) {
+        // v[i] = conj(r[j]), j = t + i T, A(tau) = r[(-tau) mod P]  (a5: fused epilogue)
         const bool is_auto = (m == l);
-        const uint32_t roi = is_auto ? roi_auto : roi_cross;
-        const uint32_t base_idx = (uint32_t)((m * M + l) * kp.L + N - 1);
-        const float* wrow = has_w ? kp.weights + (size_t)k * kp.L + N - 1 : nullptr;
-        // ---- a4: cross-spectrum + IFFT (Eq. 36); H is stored pre-scaled by 1/P
-#pragma unroll
-        for (int i = 0; i < E; ++i) v[i] = cmulc(__ldg(Xr + t + i * T), __ldg(Hl + t + i * T));
-        fft<PL, +1>(v, ftw, xbuf, t, par, grpops.sync);
-        // ---- a5: fused cell epilogue (max keys; forward sums / map)
-        float lmax2 = -1.f, lbest = -1.f;
-        uint32_t lidx = 0xFFFFFFFFu;
+        SliceCtx sc;
+        sc.roi = is_auto ? roi_auto : roi_cross;
+        sc.wrow = wrow;
+        sc.base_idx = (uint32_t)((m * M + l) * kp.L + N - 1);
+        sc.k = k;
         if constexpr (MODE == MODE_FWD) {
           if (af_mag) {
             float* mrow = af_mag + ((((size_t)r * M + m) * M + l) * K + k) * (size_t)kp.L + N - 1;
@@ -269,140 +386,109 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
             }
           }
         }
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-          if (!((roi >> i) & 1u)) continue;
-          float kv = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
-          if (has_w) {
-            const float wt = __ldg(wrow + lag_of(t + i * T, N, P));
-            if (!(wt > 0.f)) continue;
-            kv *= wt * wt;
-          }
-          lmax2 = fmaxf(lmax2, kv);
-          if (kv >= lbest) {  // rare after the first few cells: index only on a new max
-            const uint32_t idx = (base_idx + (uint32_t)lag_of(t + i * T, N, P)) * (uint32_t)K + (uint32_t)k;
-            best_update(kv, idx, lbest, lidx);
-          }
-          if constexpr (MODE == MODE_FWD) {
-            if (kp.want_S) {
-              const float vv = sqrtf(kv) * kp.invN;
-              if (vv > shift) {  // per-thread online rescale
-                if (Ssum > 0.f) Ssum *= (mode == 1) ? __expf(bp * (shift - vv)) : __powf(shift / vv, bp);
-                shift = vv;
-              }
-              Ssum += (mode == 1) ? __expf(bp * (vv - shift)) : (shift > 0.f ? __powf(vv / shift, bp) : 0.f);
-            }
-          }
+        const float lmax2 = has_w ? slice_max2<PL, true>(v, sc, t, N) : slice_max2<PL, false>(v, sc, t, N);
+        const float gmax2 = grpops.max_f(lmax2);
+        // running argmax per map type (group-uniform branch, taken only when the running max is
+        // reached): the threads holding the max find their lowest cell index, one more reduction
+        unsigned long long& kcat = is_auto ? key_a : key_c;
+        if (gmax2 >= 0.f && __float_as_uint(gmax2) >= (uint32_t)(kcat >> 32)) {
+          uint32_t idx = 0xFFFFFFFFu;
+          if (lmax2 == gmax2)
+            idx = has_w ? argmax_index<PL, true>(v, lmax2, sc, t, N, K) : argmax_index<PL, false>(v, lmax2, sc, t, N, K);
+          const unsigned long long cand = grpops.max_u64(lmax2 == gmax2 ? pack_key(gmax2, idx) : 0ull);
+          kcat = cand > kcat ? cand : kcat;
         }
-        if (lbest >= 0.f) {
-          if (is_auto) best_update(lbest, lidx, best_a, bidx_a);
-          else best_update(lbest, lidx, best_c, bidx_c);
-        }
-        if constexpr (MODE != MODE_FWD) {
-          // ---- a7: cotangent with a group-uniform running shift
-          const float gmax2 = grpops.max_f(lmax2);
-          const float gmax = gmax2 >= 0.f ? sqrtf(gmax2) * kp.invN : -1.f;
-          if (gmax >= 0.f && gmax > shift) {
-            float sc_S = 0.f, sc_G = 0.f;  // PNORM with shift 0: nothing accumulated (0^p = 0)
-            if (mode == 1) {
-              if (shift > -INFINITY) sc_S = sc_G = __expf(bp * (shift - gmax));
-            } else if (shift > 0.f) {
-              sc_G = __powf(shift / gmax, bp - 1.f);
-              sc_S = sc_G * (shift / gmax);
-            }
-            Ssum *= sc_S;
+        // ---- surrogate sums (and a7: the cotangent) with a unit-uniform running shift
+        const float gmax = gmax2 >= 0.f ? sqrtf(gmax2) * kp.invN : -1.f;
+        if (mode != 0 && gmax >= 0.f && gmax > shift) {
+          float sc_S = 0.f, sc_G = 0.f;  // PNORM with shift 0: nothing accumulated yet (0^p = 0)
+          if (mode == 1) {
+            if (shift > -INFINITY) sc_S = sc_G = ex2a(lb * (shift - gmax));
+          } else if (shift > 0.f) {
+            sc_G = ex2a((bp - 1.f) * lg2a(shift / gmax));
+            sc_S = sc_G * (shift / gmax);
+          }
+          Ssum *= sc_S;
+          if constexpr (MODE != MODE_FWD) {
 #pragma unroll
             for (int i = 0; i < E; ++i) acc[i] = make_float2(acc[i].x * sc_G, acc[i].y * sc_G);
-            if constexpr (MODE == MODE_ADJ_B) {
-              for (int n = t; n < N; n += T) gacc[n] = make_float2(gacc[n].x * sc_G, gacc[n].y * sc_G);
-            }
-            shift = gmax;
           }
-          const float lb = bp * 1.4426950408889634f;  // exp(b x) = exp2(lb x)
-#pragma unroll
-          for (int i = 0; i < E; ++i) {
-            float gfac = 0.f;
-            if ((roi >> i) & 1u) {
-              float wt = 1.f;
-              if (has_w) wt = __ldg(wrow + lag_of(t + i * T, N, P));
-              if (wt > 0.f) {
-                const float a2 = fmaf(v[i].x, v[i].x, v[i].y * v[i].y);
-                const float rsq = a2 > 0.f ? rsqrtf(a2) : 0.f;
-                const float vv = wt * a2 * rsq * kp.invN;
-                float phi, gphi;
-                if (mode == 1) {
-                  phi = exp2f(lb * (vv - shift));
-                  gphi = phi;
-                } else if (shift > 0.f) {
-                  const float q = vv / shift;
-                  gphi = __powf(q, bp - 1.f);
-                  phi = gphi * q;
-                } else {
-                  phi = gphi = 0.f;
-                }
-                Ssum += phi;
-                gfac = gphi * wt * rsq;  // unnormalized G = gphi * w * A / |A|  (0 at A = 0)
-              }
-            }
-            v[i] = make_float2(v[i].x * gfac, v[i].y * gfac);
-          }
-          // ---- a7: G_hat = FFT(G placed at (-tau) mod P) -- the same positions as r
-          fft<PL, -1>(v, ftw, xbuf, t, par, grpops.sync);
-          if constexpr (MODE == MODE_ADJ_B) {
-#pragma unroll
-            for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], __ldg(Hl + t + i * T)));
-          } else {
-#pragma unroll
-            for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(__ldg(Xr + t + i * T), v[i]));  // X conj(G_hat)
-          }
+          shift = gmax;
         }
-      }  // l
-      if constexpr (MODE == MODE_ADJ_B) {
-        // ---- a8B: e = IFFT(sum_l G_hat H_l / P), demodulate, accumulate over the chunk's bins
-        fft<PL, +1>(acc, ftw, xbuf, t, par, grpops.sync);
+        constexpr bool GRAD = MODE != MODE_FWD;
+        if (mode == 1 && (GRAD || kp.want_S)) {
+          if (has_w) slice_terms<PL, true, 1, GRAD>(v, sc, t, N, kp.invN, shift, bp, Ssum);
+          else slice_terms<PL, false, 1, GRAD>(v, sc, t, N, kp.invN, shift, bp, Ssum);
+        } else if (mode == 2 && (GRAD || kp.want_S)) {
+          if (has_w) slice_terms<PL, true, 2, GRAD>(v, sc, t, N, kp.invN, shift, bp, Ssum);
+          else slice_terms<PL, false, 2, GRAD>(v, sc, t, N, kp.invN, shift, bp, Ssum);
+        }
+      } else if (final_ph) {
+        // a8B: v = conj(e), e = IFFT(sum_l G_hat H_l / P); slot <- e conj(tw) = conj(v tw)
         const float2* twr = dtw + (size_t)k * N;
+        float2* gout = part.g + (size_t)u * P;
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           const int n = t + i * T;
-          if (n < N) gacc[n] = cadd(gacc[n], cmulc(acc[i], __ldg(twr + n)));
+          if (n < N) {
+            const float2 q = cmul(v[i], __ldg(twr + n));
+            gout[n] = make_float2(q.x, -q.y);
+          }
+        }
+      } else {
+        // G phase: v = G_hat
+        if constexpr (MODE == MODE_ADJ_B) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], __ldg(Hl + t + i * T)));
+        } else if constexpr (MODE == MODE_ADJ_A) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(__ldg(Xr + t + i * T), v[i]));  // X conj(G_hat)
         }
       }
-    }  // m (Step A)
-  }    // k
+    }  // phases
 
-  // ---- group partials
-  const unsigned long long key_a =
-      grpops.max_u64(best_a >= 0.f ? pack_key(best_a, bidx_a) : 0ull);
-  const unsigned long long key_c =
-      grpops.max_u64(best_c >= 0.f ? pack_key(best_c, bidx_c) : 0ull);
-  float gshift = shift, gS;
-  if constexpr (MODE == MODE_FWD) {
-    gshift = grpops.max_f(shift);  // combine per-thread shifts inside the group
-    float term = 0.f;
-    if (Ssum > 0.f) term = (mode == 1) ? Ssum * __expf(bp * (shift - gshift)) : Ssum * __powf(shift / gshift, bp);
-    gS = grpops.sum_f(term);
-  } else {
-    gS = grpops.sum_f(Ssum);
-  }
-  if (!active) return;
-  if (t == 0) {
-    part.key[2 * gg] = key_a;
-    part.key[2 * gg + 1] = key_c;
-    part.m[gg] = gshift;
-    part.S[gg] = gS;
-  }
-  if constexpr (MODE == MODE_ADJ_A) {
-    // ---- a8A: d = IFFT(sum X conj(G_hat)) -> the group's dL/dw_l^* partial (x 1/P in the combine)
-    fft<PL, +1>(acc, ftw, xbuf, t, par, grpops.sync);
-    float2* gout = part.g + (size_t)gg * N;
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int n = t + i * T;
-      if (n < N) gout[n] = acc[i];
+    // ---- unit partials (keys: the group's running maxima of this restart)
+    const float uS = grpops.sum_f(Ssum);
+    const float ushift = shift;
+    if (t == 0) {
+      part.key[2 * (size_t)u] = key_a;
+      part.key[2 * (size_t)u + 1] = key_c;
+      part.m[u] = ushift;
+      part.S[u] = uS;
     }
-  } else if constexpr (MODE == MODE_ADJ_B) {
-    float2* gout = part.g + (size_t)gg * N;
-    for (int n = t; n < N; n += T) gout[n] = gacc[n];
+    if constexpr (MODE == MODE_ADJ_A) {
+      float2* gout = part.g + (size_t)u * P;  // spectral partial of dL/dw_l^* (unscaled)
+#pragma unroll
+      for (int i = 0; i < E; ++i) gout[t + i * T] = acc[i];
+    }
+  }
+}
+
+// Step A combine, second half: d_l = IFFT_P(spectral sum)[0..N) for each (r, l) row,
+// via the forward FFT of the conjugate.
+template <class PL, int G>
+__global__ void __launch_bounds__(PL::T* G)
+    k_rows_ifft(int rows, int N, const float2* __restrict__ in, const float2* __restrict__ ftw, float2* __restrict__ out) {
+  constexpr int E = PL::E, T = PL::T, P = PL::P;
+  extern __shared__ float4 smem_raw[];
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  const int id = blockIdx.x * G + grp;
+  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * PL::PADDED : 0);
+  GroupSync sync{1 + grp, T, group_mask(T)};
+  const int row = id < rows ? id : rows - 1;
+  float2 v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float2 x = __ldg(in + (size_t)row * P + t + i * T);
+    v[i] = make_float2(x.x, -x.y);
+  }
+  int par = 0;
+  fft<PL, -1>(v, ftw, xbuf, t, par, sync);
+  if (id >= rows) return;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    if (n < N) out[(size_t)row * N + n] = make_float2(v[i].x, -v[i].y);
   }
 }
 

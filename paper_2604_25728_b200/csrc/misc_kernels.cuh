@@ -220,31 +220,46 @@ __global__ void k_group_scales(int GPR, int g_lo, int g_hi, int mode, double bp,
   }
 }
 
-// Gradient partials -> red_grad[r][a][n] in true units of dL_wpsl / d(.)^*:
-// sum_c g_c[n] * rescale(m_c -> m_r) * norm,  norm = eps/(2N) * (LSE: 1/S, PNORM: S^{1/p-1}) * extra.
-__global__ void k_combine_grad(int M, int N, int C, int g_lo, int g_hi, int mode, double bp, double eps,
-                               double extra, Part part, const Red* __restrict__ red, float2* red_grad) {
+// Unit slots -> per-row sums in true units of dL_wpsl / d(.)^*:
+// out[ra][q] = norm_r * sum_k scale[u] slot[u][q],  u = ra K + k  (fixed order),
+// norm_r = eps/(2N) * extra * (LSE: 1/S_r, PNORM: S_r^{1/p-1}).  Block: 32 q x 8 k-lanes.
+__global__ void k_combine_rows(int M, int N, int K, int len, int slot_stride, int u_lo, int u_hi, int mode,
+                               double bp, double eps, double extra, Part part, const Red* __restrict__ red,
+                               float2* out) {
+  __shared__ float2 sh[8][33];
   const int ra = blockIdx.y;
   const int r = ra / M;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+  const int q = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int kl = threadIdx.x >> 5;  // 0..7
   const double S = red[r].S;
+  const bool live = red[r].m > -INFINITY && S > 0.0;
   float re = 0.f, im = 0.f;
-  if (red[r].m > -INFINITY && S > 0.0) {
-    const int glo = max(g_lo, ra * C), ghi = min(g_hi, (ra + 1) * C);
-#pragma unroll 8
-    for (int g = glo; g < ghi; ++g) {
-      const float sc = part.scale[g];
-      const float2 v = part.g[(size_t)g * N + n];
+  if (live && q < len) {
+    for (int k = kl; k < K; k += 8) {
+      const int u = ra * K + k;
+      if (u < u_lo || u >= u_hi) continue;
+      const float sc = part.scale[u];
+      const float2 v = part.g[(size_t)u * slot_stride + q];
       re = fmaf(sc, v.x, re);
       im = fmaf(sc, v.y, im);
     }
-    double norm = eps / (2.0 * N) * extra;
-    norm *= (mode == 1) ? 1.0 / S : pow(S, 1.0 / bp - 1.0);
-    re = (float)(re * norm);
-    im = (float)(im * norm);
   }
-  red_grad[(size_t)ra * N + n] = make_float2(re, im);
+  sh[kl][threadIdx.x & 31] = make_float2(re, im);
+  __syncthreads();
+  if (kl == 0 && q < len) {
+    float2 t = sh[0][threadIdx.x];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      t.x += sh[j][threadIdx.x].x;
+      t.y += sh[j][threadIdx.x].y;
+    }
+    double norm = 0.0;
+    if (live) {
+      norm = eps / (2.0 * N) * extra;
+      norm *= (mode == 1) ? 1.0 / S : pow(S, 1.0 / bp - 1.0);
+    }
+    out[(size_t)ra * len + q] = make_float2((float)(t.x * norm), (float)(t.y * norm));
+  }
 }
 
 // ------------------------------------------------------------------ MAX-mode sparse adjoint

@@ -25,9 +25,17 @@ thread_local std::string g_last_error;
 
 // Launch geometry per FFT length: E elements per thread, G groups per CTA, and the
 // minimum resident CTAs per SM handed to __launch_bounds__ (caps registers at 128).
-constexpr int plan_E(int P) { return P <= 16 ? P : 16; }
+#ifndef SQNGD_E
+#define SQNGD_E 16
+#endif
+#ifndef SQNGD_MINB256
+#define SQNGD_MINB256 2
+#endif
+constexpr int plan_E(int P) { return P <= SQNGD_E ? P : SQNGD_E; }
 constexpr int plan_G(int P) { return (P / plan_E(P)) >= 128 ? 1 : 128 / (P / plan_E(P)); }
-constexpr int plan_MINB(int P) { return (P / plan_E(P)) * plan_G(P) >= 512 ? 1 : (P / plan_E(P)) * plan_G(P) >= 256 ? 2 : 4; }
+constexpr int plan_MINB(int P) {
+  return (P / plan_E(P)) * plan_G(P) >= 512 ? 1 : (P / plan_E(P)) * plan_G(P) >= 256 ? SQNGD_MINB256 : 4;
+}
 
 }  // namespace
 
@@ -36,9 +44,11 @@ struct sqngd_ctx_s {
   int dev = 0, rank = 0, world = 1;
   int P = 0, L = 0, BR = 0, sms = 0;
   uint32_t n_cells = 0, flags = 0;
-  // chunking of the Doppler axis per mode (0 fwd, 1 adj A, 2 adj B)
-  int C[3] = {1, 1, 1}, chunk[3] = {1, 1, 1};
-  int gtot_max = 0;
+  // persistent grid: resident groups per fused-kernel mode (0 fwd, 1 adj A, 2 adj B)
+  int64_t slots[3] = {1, 1, 1};
+  int64_t units = 0;       // R * M * K
+  int* counter = nullptr;  // dynamic unit counter
+  float2* spec = nullptr;  // [R][M][P] Step-A spectral sums
   std::string err;
   // device workspace
   float2* tw = nullptr;     // [K][N] e^{j 2 pi (n+1) f_k / N} (fp64-built)
@@ -49,7 +59,7 @@ struct sqngd_ctx_s {
   float2* s_hard = nullptr;
   float* dq = nullptr;      // [R][M][N]
   int* lut = nullptr;       // [R][BR+1]
-  Part part{};              // [gtot] keys, shifts, sums; [gtot][N] gradient partials
+  Part part{};              // per unit u = (r M + a) K + k: keys, shift, sum, scale; [U][P] gradient slots
   Red* red = nullptr;       // [R]
   double2* cm = nullptr;    // [R][M]
   float2* red_grad = nullptr;  // [R][M][N]
@@ -139,6 +149,8 @@ struct Launch {
     if (e) return e;
     e = cudaFuncSetAttribute(k_xhat<PL, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
     if (e) return e;
+    e = cudaFuncSetAttribute(k_rows_ifft<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+    if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MINB, MODE_FWD>, THREADS, smem<MODE_FWD>());
     if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], k_af<PL, G, MINB, MODE_ADJ_A>, THREADS, smem<MODE_ADJ_A>());
@@ -159,11 +171,15 @@ struct Launch {
     const int blocks = (units + G - 1) / G;
     k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(units, M, N, K, s, dtw, ftw, Xc);
   }
-  static void af(int mode, const KP& kp, const float2* Xc, const float2* H, const float2* tw, const float2* ftw,
-                 float* af_mag, const Part& part, cudaStream_t st) {
-    const int groups = kp.g_hi - kp.g_lo;
-    if (groups <= 0) return;
-    const int blocks = (groups + G - 1) / G;
+  static void rows_ifft(int rows, int N, const float2* in, const float2* ftw, float2* out, cudaStream_t st) {
+    const int blocks = (rows + G - 1) / G;
+    k_rows_ifft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, N, in, ftw, out);
+  }
+  static void af(int mode, const KP& kp, int64_t slots, const float2* Xc, const float2* H, const float2* tw,
+                 const float2* ftw, float* af_mag, const Part& part, cudaStream_t st) {
+    const int64_t units = kp.u_hi - kp.u_lo;
+    if (units <= 0) return;
+    const int blocks = (int)((std::min<int64_t>(units, slots) + G - 1) / G);
     if (mode == MODE_FWD)
       k_af<PL, G, MINB, MODE_FWD><<<blocks, THREADS, smem<MODE_FWD>(), st>>>(kp, Xc, H, tw, ftw, af_mag, part);
     else if (mode == MODE_ADJ_A)
@@ -193,37 +209,19 @@ static bool with_P(int P, Fn&& fn) {
   }
 }
 
-static KP make_kp(const sqngd_ctx_s* c, int mode, int want_S) {
+static KP make_kp(const sqngd_ctx_s* c, int want_S) {
   KP kp;
   const sqngd_config& g = c->cfg;
   kp.R = g.R; kp.M = g.M; kp.N = g.N; kp.K = g.K; kp.L = c->L; kp.P = c->P;
   kp.tau_lo = g.tau_lo; kp.tau_hi = g.tau_hi; kp.excl0 = g.exclude_auto_zero_delay;
   kp.loss_mode = g.loss_mode; kp.beta_or_p = (float)g.beta_or_p; kp.invN = 1.0f / (float)g.N;
   kp.weights = g.weights;
-  kp.C = c->C[mode]; kp.chunk = c->chunk[mode];
-  const int64_t gtot = (int64_t)g.R * g.M * kp.C;
   int64_t lo, hi;
-  sqngd_shard_range(gtot, c->rank, c->world, &lo, &hi);
-  kp.g_lo = (int)lo; kp.g_hi = (int)hi;
+  sqngd_shard_range(c->units, c->rank, c->world, &lo, &hi);
+  kp.u_lo = (int)lo; kp.u_hi = (int)hi;
   kp.want_S = want_S;
+  kp.counter = c->counter;
   return kp;
-}
-
-// Choose the number of Doppler chunks C per (r, a) row minimizing the makespan on `slots`
-// concurrently resident groups: ceil(K / C) units per group, ceil(rows * C_eff / slots) waves.
-static void choose_chunks(int rows, int K, int64_t slots, int* C_out, int* chunk_out) {
-  int bestC = 1;
-  double best = 1e300;
-  for (int C = 1; C <= K; ++C) {
-    const int ch = (K + C - 1) / C;
-    const int Ceff = (K + ch - 1) / ch;
-    if (Ceff != C) continue;
-    const double waves = std::ceil((double)rows * Ceff / (double)std::max<int64_t>(1, slots));
-    const double cost = waves * ch + 1e-3 * Ceff;  // prefer fewer partials on ties
-    if (cost < best) { best = cost; bestC = C; }
-  }
-  *C_out = bestC;
-  *chunk_out = (K + bestC - 1) / bestC;
 }
 
 // ----------------------------------------------------------------------------- C-ABI
@@ -323,11 +321,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     delete ctx;
     return fail(nullptr, SQNGD_E_CUDA, "sqngd_create: kernel setup", m.c_str());
   }
-  for (int md = 0; md < 3; ++md) {
-    const int64_t slots = (int64_t)ctx->sms * std::max(1, bps[md]) * G * world;
-    choose_chunks(cfg.R * cfg.M, cfg.K, slots, &ctx->C[md], &ctx->chunk[md]);
-    ctx->gtot_max = std::max(ctx->gtot_max, cfg.R * cfg.M * ctx->C[md]);
-  }
+  for (int md = 0; md < 3; ++md) ctx->slots[md] = (int64_t)ctx->sms * std::max(1, bps[md]) * G;
+  ctx->units = (int64_t)cfg.R * cfg.M * cfg.K;
 
   const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
   CK(cudaMalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
@@ -335,15 +330,17 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * cfg.K * P));
   CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->part.scale, sizeof(float) * ctx->gtot_max));
+  CK(cudaMalloc(&ctx->part.scale, sizeof(float) * ctx->units));
+  CK(cudaMalloc(&ctx->counter, sizeof(int)));
+  CK(cudaMalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   CK(cudaMalloc(&ctx->s_soft, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->dq, sizeof(float) * RMN));
   CK(cudaMalloc(&ctx->lut, sizeof(int) * (size_t)cfg.R * (ctx->BR + 1)));
-  CK(cudaMalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * ctx->gtot_max));
-  CK(cudaMalloc(&ctx->part.m, sizeof(float) * ctx->gtot_max));
-  CK(cudaMalloc(&ctx->part.S, sizeof(float) * ctx->gtot_max));
-  CK(cudaMalloc(&ctx->part.g, sizeof(float2) * (size_t)ctx->gtot_max * cfg.N));
+  CK(cudaMalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * ctx->units));
+  CK(cudaMalloc(&ctx->part.m, sizeof(float) * ctx->units));
+  CK(cudaMalloc(&ctx->part.S, sizeof(float) * ctx->units));
+  CK(cudaMalloc(&ctx->part.g, sizeof(float2) * (size_t)ctx->units * P));
   CK(cudaMalloc(&ctx->red, sizeof(Red) * cfg.R));
   CK(cudaMalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
   CK(cudaMalloc(&ctx->red_grad, sizeof(float2) * RMN));
@@ -389,7 +386,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
 void sqngd_destroy(sqngd_ctx ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
-  void* ptrs[] = {ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+  void* ptrs[] = {ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status};
   for (void* p : ptrs)
@@ -494,17 +491,18 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
     sqngd_status rx = run_xhat(ctx, s, st);
     if (rx) return rx;
   }
-  KP kp = make_kp(ctx, MODE_FWD, c.loss_mode != 0);
+  KP kp = make_kp(ctx, c.loss_mode != 0);
+  cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
   {
     ProfScope ps(ctx, MODE_FWD, st);
     with_P(ctx->P, [&](auto Lc) {
-      decltype(Lc)::af(MODE_FWD, kp, ctx->Xc, ctx->H, ctx->tw, ctx->ftw, af_mag, ctx->part, st);
+      decltype(Lc)::af(MODE_FWD, kp, ctx->slots[MODE_FWD], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, af_mag, ctx->part, st);
     });
   }
   ctx->launches += 4;
   sqngd_status rc = launch_check(ctx, "af forward");
   if (rc) return rc;
-  k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
+  k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
   if (ctx->world > 1 && (rc = allreduce_red(ctx, st, false, MODE_FWD))) return rc;
   k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
@@ -531,25 +529,36 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     if ((rc = launch_check(ctx, "sparse adjoint"))) return rc;
   } else {
     const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
-    KP kp = make_kp(ctx, mode, 1);
+    KP kp = make_kp(ctx, 1);
+    cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
     {
       ProfScope ps(ctx, mode, st);
       with_P(ctx->P, [&](auto Lc) {
-        decltype(Lc)::af(mode, kp, ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
+        decltype(Lc)::af(mode, kp, ctx->slots[mode], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
       });
     }
     ctx->launches += 5;
     if ((rc = launch_check(ctx, "af adjoint"))) return rc;
-    k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part,
+    k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
                                          ctx->red);
     if (ctx->world > 1) {
       if ((rc = allreduce_red(ctx, st, false, mode))) return rc;
-      k_group_scales<<<c.R, 256, 0, st>>>(c.M * kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
+      k_group_scales<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
+                                          ctx->red);
     }
-    dim3 grid((c.N + 127) / 128, c.R * c.M);
-    const double extra = mode == MODE_ADJ_A ? 1.0 / ctx->P : 1.0;
-    k_combine_grad<<<grid, 128, 0, st>>>(c.M, c.N, kp.C, kp.g_lo, kp.g_hi, c.loss_mode, c.beta_or_p, c.eps_w,
-                                         extra, ctx->part, ctx->red, ctx->red_grad);
+    if (mode == MODE_ADJ_B) {
+      dim3 grid((c.N + 31) / 32, c.R * c.M);
+      k_combine_rows<<<grid, 256, 0, st>>>(c.M, c.N, c.K, c.N, ctx->P, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p,
+                                           c.eps_w, 1.0, ctx->part, ctx->red, ctx->red_grad);
+    } else {  // spectral sums, then one IFFT per (r, l) row (1/P folded into the norm)
+      dim3 grid((ctx->P + 31) / 32, c.R * c.M);
+      k_combine_rows<<<grid, 256, 0, st>>>(c.M, c.N, c.K, ctx->P, ctx->P, kp.u_lo, kp.u_hi, c.loss_mode,
+                                           c.beta_or_p, c.eps_w, 1.0 / ctx->P, ctx->part, ctx->red, ctx->spec);
+      with_P(ctx->P, [&](auto Lc) {
+        decltype(Lc)::rows_ifft(c.R * c.M, c.N, ctx->spec, ctx->ftw, ctx->red_grad, st);
+      });
+      ctx->launches += 1;
+    }
     if (ctx->world > 1 && (rc = allreduce_red(ctx, st, true, mode))) return rc;
     k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
     k_metrics<<<c.R, 32, 0, st>>>(c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells,

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsqngd.so")
+LIB_PATH = os.environ.get("SQNGD_LIB") or os.path.join(_HERE, "libsqngd.so")
 
 OK, E_INVALID, E_DEGENERATE, E_NONFINITE, E_CUDA, E_NCCL, E_NOMEM = range(7)
 WRT_FILTERS, WRT_TRANSMIT = 1, 2
