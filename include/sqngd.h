@@ -153,8 +153,11 @@ sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho,
 sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* state, int block, double* loss_hist,
                         sqngd_metrics* hard_out, sqngd_stream stream);
 
-/* Profiling (for the roofline in bench.py): when enabled, every fused AF kernel launch
-   is bracketed by CUDA events on its launch stream.  sqngd_profile_read synchronizes and
+/* sqngd_step captures itself into a CUDA graph on the first call with a given (state
+   buffers, block, outputs) on a non-legacy stream and replays the graph afterwards
+   (single GPU; SQNGD_NO_GRAPH=1 disables).
+   Profiling (for the roofline in bench.py): when enabled, sqngd_step runs eagerly and every
+   fused AF kernel launch is bracketed by CUDA events on its launch stream.  sqngd_profile_read synchronizes and
    returns, per kernel class (0 forward, 1 Step-A adjoint, 2 Step-B adjoint), the summed
    device milliseconds ms[3] and launch counts count[3], plus `launches` = every kernel the
    library launched since the last reset (all classes, small kernels included). */

@@ -105,6 +105,31 @@ struct Group {
     }
     return x;
   }
+  // fixed-order fp64 sum of a (re, im) pair; smem slots reuse the u64 area
+  __device__ __forceinline__ double2 sum_d2(double2 x) {
+    constexpr int W = T < 32 ? T : 32;
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+      x.x += __shfl_xor_sync(mask, x.x, o);
+      x.y += __shfl_xor_sync(mask, x.y, o);
+    }
+    if constexpr (T > 32) {
+      double* b = reinterpret_cast<double*>(redk) + (par ? 32 : 0);
+      par ^= 1;
+      if ((t & 31) == 0) {
+        b[(t >> 5)] = x.x;
+        b[(t >> 5) + 16] = x.y;
+      }
+      sync();
+      x = make_double2(b[0], b[16]);
+#pragma unroll
+      for (int w = 1; w < T / 32; ++w) {
+        x.x += b[w];
+        x.y += b[w + 16];
+      }
+    }
+    return x;
+  }
   __device__ __forceinline__ unsigned long long max_u64(unsigned long long x) {
     constexpr int W = T < 32 ? T : 32;
 #pragma unroll
@@ -123,6 +148,13 @@ struct Group {
     }
     return x;
   }
+};
+
+// Per-group shared memory of the single-FFT kernels (exchange buffers + reduction slots).
+template <class PL>
+struct FftSmem {
+  static constexpr int XBUF = PL::NP > 1 ? 2 * PL::PADDED : 0;
+  static constexpr int TOTAL = XBUF + 32 + 64;
 };
 
 // Per-group shared memory (float2 units).
@@ -266,13 +298,20 @@ __device__ __forceinline__ void slice_terms(float2 (&v)[PL::E], const SliceCtx& 
 template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB)
     k_xhat(int units, int M, int N, int K, const float2* __restrict__ s, const float2* __restrict__ dtw,
-           const float2* __restrict__ ftw, float2* __restrict__ Xc) {
+           const float2* __restrict__ ftw, float2* __restrict__ Xc, const float2* __restrict__ w, double2* cm) {
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
   const int u = blockIdx.x * G + grp;
-  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * PL::PADDED : 0);
-  GroupSync sync{1 + grp, T, group_mask(T)};
+  float2* gsm = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
+  float2* xbuf = gsm;
+  Group<T> gops;
+  gops.sync = GroupSync{1 + grp, T, group_mask(T)};
+  gops.mask = gops.sync.mask;
+  gops.red = reinterpret_cast<float*>(gsm + FftSmem<PL>::XBUF);
+  gops.redk = reinterpret_cast<unsigned long long*>(gsm + FftSmem<PL>::XBUF + 32);
+  gops.par = 0;
+  gops.t = t;
   const int uu = u < units ? u : units - 1;
   const int k = uu % K, rm = uu / K;
   const float2* sr = s + (size_t)rm * N;
@@ -283,8 +322,19 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
     const int n = t + i * T;
     v[i] = n < N ? cmul(__ldg(sr + n), __ldg(twr + n)) : make_float2(0.f, 0.f);
   }
+  if (w != nullptr && k == 0) {  // a6: c_m = sum_n s_m(n) conj(w_m(n)) = A_mm(0,0) (Eq. 38), fp64
+    const float2* wr = w + (size_t)rm * N;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int n = t; n < N; n += T) {
+      const float2 a = __ldg(sr + n), b = __ldg(wr + n);
+      acc.x += (double)a.x * b.x + (double)a.y * b.y;
+      acc.y += (double)a.y * b.x - (double)a.x * b.y;
+    }
+    acc = gops.sum_d2(acc);
+    if (t == 0 && u < units) cm[rm] = acc;
+  }
   int par = 0;
-  fft<PL, -1>(v, ftw, xbuf, t, par, sync);
+  fft<PL, -1>(v, ftw, xbuf, t, par, gops.sync);
   if (u >= units) return;
   float2* out = Xc + (size_t)u * P;
 #pragma unroll
@@ -473,7 +523,7 @@ __global__ void __launch_bounds__(PL::T* G)
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
   const int id = blockIdx.x * G + grp;
-  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * PL::PADDED : 0);
+  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
   GroupSync sync{1 + grp, T, group_mask(T)};
   const int row = id < rows ? id : rows - 1;
   float2 v[E];
@@ -495,14 +545,35 @@ __global__ void __launch_bounds__(PL::T* G)
 // a2: H_l = FFT_P([w_l; 0]) / P for every (r, l); one group per filter.
 template <class PL, int G>
 __global__ void __launch_bounds__(PL::T* G)
-    k_filter_fft(int RM, int N, const float2* __restrict__ w, const float2* __restrict__ ftw, float2* __restrict__ Hh) {
+    k_filter_fft(int RM, int N, const float2* __restrict__ w, const float2* __restrict__ ftw, float2* __restrict__ Hh,
+                 const float2* __restrict__ s, double2* cm) {
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
   const int id = blockIdx.x * G + grp;
-  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (PL::NP > 1 ? 2 * PL::PADDED : 0);
-  GroupSync sync{1 + grp, T, group_mask(T)};
+  float2* gsm = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
+  float2* xbuf = gsm;
+  Group<T> gops;
+  gops.sync = GroupSync{1 + grp, T, group_mask(T)};
+  gops.mask = gops.sync.mask;
+  gops.red = reinterpret_cast<float*>(gsm + FftSmem<PL>::XBUF);
+  gops.redk = reinterpret_cast<unsigned long long*>(gsm + FftSmem<PL>::XBUF + 32);
+  gops.par = 0;
+  gops.t = t;
+  const GroupSync& sync = gops.sync;
   const int rl = id < RM ? id : RM - 1;
+  if (s != nullptr) {  // a6: c_m = sum_n s_m(n) conj(w_m(n)) (Eq. 38), fp64
+    const float2* sr = s + (size_t)rl * N;
+    const float2* wr = w + (size_t)rl * N;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int n = t; n < N; n += T) {
+      const float2 a = __ldg(sr + n), b = __ldg(wr + n);
+      acc.x += (double)a.x * b.x + (double)a.y * b.y;
+      acc.y += (double)a.y * b.x - (double)a.x * b.y;
+    }
+    acc = gops.sum_d2(acc);
+    if (t == 0 && id < RM) cm[rl] = acc;
+  }
   float2 v[E];
   const float2* wr = w + (size_t)rl * N;
 #pragma unroll

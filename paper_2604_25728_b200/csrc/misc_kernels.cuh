@@ -11,6 +11,17 @@ namespace sq {
 
 enum : int { ST_INVALID = 1, ST_DEGENERATE = 2, ST_NONFINITE = 4 };
 
+__device__ __forceinline__ float ex2a_m(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_m(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct Red {               // per restart, after combining all groups
   double m;                // shift of S and of the gradient partials
   double S;                // sum of phi at shift m
@@ -89,8 +100,8 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
     float resid = 0.f, sech = 0.f;
     for (int j = i0 + sub; j < i1; j += LPE) {
       const float u = c * (x - rs[j]);
-      const float e2 = __expf(-2.f * fabsf(u));
-      const float inv = __frcp_rn(1.f + e2);
+      const float e2 = ex2a_m(-2.8853900817779268f * fabsf(u));  // e^{-2|u|}
+      const float inv = rcp_m(1.f + e2);
       const float tt = 2.f * e2 * inv;
       resid += (j >= cnt) ? tt : -tt;
       sech += 4.f * e2 * inv * inv;
@@ -124,36 +135,92 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
   }
 }
 
-// ------------------------------------------------------------------ a6 mainlobe
-// c_m = sum_n s_m(n) conj(w_m(n)) = A_mm(0,0) (Eq. 38), fp64 fixed-order tree.
-__global__ void k_mainlobe(int N, const float2* __restrict__ s, const float2* __restrict__ w, double2* cm) {
-  __shared__ double sre[256], sim[256];
-  const size_t row = blockIdx.x;
-  double re = 0.0, im = 0.0;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    const float2 a = s[row * N + n], b = w[row * N + n];
-    re += (double)a.x * b.x + (double)a.y * b.y;
-    im += (double)a.y * b.x - (double)a.x * b.y;
+// ------------------------------------------------------------------ a6 metrics / loss
+__device__ __forceinline__ void decode_key(unsigned long long key, int M, int N, int K, int L, int32_t out[4],
+                                           double* vsq) {
+  if (key == 0ull) {
+    out[0] = out[1] = out[2] = out[3] = -1;
+    *vsq = 0.0;
+    return;
   }
-  sre[threadIdx.x] = re;
-  sim[threadIdx.x] = im;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      sre[threadIdx.x] += sre[threadIdx.x + o];
-      sim[threadIdx.x] += sim[threadIdx.x + o];
-    }
-    __syncthreads();
+  const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+  out[3] = idx % K;
+  out[2] = (int)((idx / K) % L) - (N - 1);
+  out[1] = (idx / K / L) % M;
+  out[0] = idx / K / L / M;
+  *vsq = (double)__uint_as_float((uint32_t)(key >> 32));
+}
+
+struct MetricsOut {       // mirrors sqngd_metrics (include/sqngd.h)
+  double loss, loss_wpsl, loss_snrl, wapsl, wcpsl, wpsl;
+  int32_t argmax_auto[4], argmax_cross[4];
+  uint32_t flags, n_cells;
+};
+
+struct MetricsArgs {
+  int M, N, K, L, mode;
+  double bp, eps, ptar;
+  uint32_t n_cells, flags;
+  const Red* red;
+  const double2* cm;
+  MetricsOut* out;
+  double* p_out;
+  double* loss_hist;
+  int hist_stride, hist_col;
+};
+
+// Eqs. 7-10, 37-42 for restart r from the combined partials.
+__device__ void metrics_one(const MetricsArgs& a, int r, int* status) {
+  MetricsOut o;
+  double va, vc;
+  decode_key(a.red[r].key_a, a.M, a.N, a.K, a.L, o.argmax_auto, &va);
+  decode_key(a.red[r].key_c, a.M, a.N, a.K, a.L, o.argmax_cross, &vc);
+  o.wapsl = sqrt(va) / a.N;
+  o.wcpsl = sqrt(vc) / a.N;
+  o.wpsl = fmax(o.wapsl, o.wcpsl);
+  if (a.mode == 0) o.loss_wpsl = o.wpsl;
+  else if (a.red[r].m > -INFINITY && a.red[r].S > 0.0)
+    o.loss_wpsl = a.mode == 1 ? a.red[r].m + log(a.red[r].S) / a.bp : a.red[r].m * pow(a.red[r].S, 1.0 / a.bp);
+  else o.loss_wpsl = 0.0;
+  double lsn = 0.0;
+  for (int m = 0; m < a.M; ++m) {
+    const double2 c = a.cm[(size_t)r * a.M + m];
+    const double p = sqrt(c.x * c.x + c.y * c.y) / a.N;
+    if (a.p_out) a.p_out[(size_t)r * a.M + m] = p;
+    if (p == 0.0) atomicOr(status, ST_DEGENERATE);
+    lsn += (p - a.ptar) * (p - a.ptar);
   }
-  if (threadIdx.x == 0) cm[row] = make_double2(sre[0], sim[0]);
+  o.loss_snrl = lsn / a.M;
+  o.loss = a.eps * o.loss_wpsl + (1.0 - a.eps) * o.loss_snrl;
+  o.flags = a.flags;
+  o.n_cells = a.n_cells;
+  if (!isfinite(o.loss)) atomicOr(status, ST_NONFINITE);
+  if (a.out) a.out[r] = o;
+  if (a.loss_hist) a.loss_hist[(size_t)r * a.hist_stride + a.hist_col] = o.loss;
 }
 
 // ------------------------------------------------------------------ combines
-// Per restart: max keys, global shift and the rescaled sum S over the restart's groups
-// [r * GPR, (r+1) * GPR) intersected with [g_lo, g_hi).  Block of 256, fixed order.
-__global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp, Part part, Red* red) {
-  __shared__ double sh[256];
-  __shared__ unsigned long long ka[256], kc[256];
+// Block-wide fixed-order reductions (warp shuffles, then the warps in index order).
+template <class T_, class Op>
+__device__ __forceinline__ T_ block_reduce(T_ x, Op op, T_* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[w] = x;
+  __syncthreads();
+  x = sh[0];
+  for (int i = 1; i < nw; ++i) x = op(x, sh[i]);
+  return x;
+}
+
+// Per restart: max keys, global shift and the rescaled sum S over the restart's units
+// [r * GPR, (r+1) * GPR) intersected with [g_lo, g_hi); per-unit rescale factors for the
+// gradient combine.  One block of 1024 threads per restart, fixed order (deterministic).
+__global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp, Part part, Red* red,
+                                MetricsArgs ma, int* status) {
+  __shared__ double shd[32];
+  __shared__ unsigned long long shk[32];
   const int r = blockIdx.x;
   const int lo = max(g_lo, r * GPR), hi = min(g_hi, (r + 1) * GPR);
   double mloc = -INFINITY;
@@ -163,47 +230,32 @@ __global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp
     a = max(a, part.key[2 * g]);
     cc = max(cc, part.key[2 * g + 1]);
   }
-  sh[threadIdx.x] = mloc;
-  ka[threadIdx.x] = a;
-  kc[threadIdx.x] = cc;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-      ka[threadIdx.x] = max(ka[threadIdx.x], ka[threadIdx.x + o]);
-      kc[threadIdx.x] = max(kc[threadIdx.x], kc[threadIdx.x + o]);
-    }
-    __syncthreads();
-  }
-  const double m = sh[0];
-  __syncthreads();
+  auto dmax = [](double x, double y) { return fmax(x, y); };
+  auto umax = [](unsigned long long x, unsigned long long y) { return x > y ? x : y; };
+  const double m = block_reduce(mloc, dmax, shd);
+  a = block_reduce(a, umax, shk);
+  cc = block_reduce(cc, umax, shk);
   double S = 0.0;
-  if (mode != 0 && m > -INFINITY) {
-    for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
-      const double Sg = part.S[g];
-      if (Sg > 0.0) S += Sg * (mode == 1 ? exp(bp * ((double)part.m[g] - m)) : pow((double)part.m[g] / m, bp));
+  const float mf = (float)m;
+  const float lb = (float)(bp * 1.4426950408889634);
+  for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
+    float sc = 0.f;
+    const float Sg = part.S[g];
+    if (mode != 0 && Sg > 0.f && m > -INFINITY) {
+      const float mg = part.m[g];
+      sc = mode == 1 ? exp2f(lb * (mg - mf)) : exp2f((float)(bp - 1.0) * log2f(mg / mf));
+      S += (double)Sg * (mode == 1 ? sc : sc * (mg / mf));
     }
+    if (part.scale) part.scale[g] = sc;
   }
-  sh[threadIdx.x] = S;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
+  auto dsum = [](double x, double y) { return x + y; };
+  S = block_reduce(S, dsum, shd);
   if (threadIdx.x == 0) {
     red[r].m = m;
-    red[r].S = sh[0];
-    red[r].key_a = ka[0];
-    red[r].key_c = kc[0];
-  }
-  // per-group rescale of the gradient partials to the restart's shift (used by the combine)
-  if (part.scale && mode != 0) {
-    for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
-      float sc = 0.f;
-      if (part.S[g] > 0.f && m > -INFINITY)
-        sc = (float)(mode == 1 ? exp(bp * ((double)part.m[g] - m)) : pow((double)part.m[g] / m, bp - 1.0));
-      part.scale[g] = sc;
-    }
+    red[r].S = S;
+    red[r].key_a = a;
+    red[r].key_c = cc;
+    if (ma.out || ma.loss_hist || ma.p_out) metrics_one(ma, r, status);
   }
 }
 
@@ -214,8 +266,10 @@ __global__ void k_group_scales(int GPR, int g_lo, int g_hi, int mode, double bp,
   const double m = red[r].m;
   for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
     float sc = 0.f;
-    if (part.S[g] > 0.f && m > -INFINITY)
-      sc = (float)(mode == 1 ? exp(bp * ((double)part.m[g] - m)) : pow((double)part.m[g] / m, bp - 1.0));
+    if (part.S[g] > 0.f && m > -INFINITY) {
+      const float mg = part.m[g], mf = (float)m;
+      sc = mode == 1 ? exp2f((float)(bp * 1.4426950408889634) * (mg - mf)) : exp2f((float)(bp - 1.0) * log2f(mg / mf));
+    }
     part.scale[g] = sc;
   }
 }
@@ -223,45 +277,6 @@ __global__ void k_group_scales(int GPR, int g_lo, int g_hi, int mode, double bp,
 // Unit slots -> per-row sums in true units of dL_wpsl / d(.)^*:
 // out[ra][q] = norm_r * sum_k scale[u] slot[u][q],  u = ra K + k  (fixed order),
 // norm_r = eps/(2N) * extra * (LSE: 1/S_r, PNORM: S_r^{1/p-1}).  Block: 32 q x 8 k-lanes.
-__global__ void k_combine_rows(int M, int N, int K, int len, int slot_stride, int u_lo, int u_hi, int mode,
-                               double bp, double eps, double extra, Part part, const Red* __restrict__ red,
-                               float2* out) {
-  __shared__ float2 sh[8][33];
-  const int ra = blockIdx.y;
-  const int r = ra / M;
-  const int q = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int kl = threadIdx.x >> 5;  // 0..7
-  const double S = red[r].S;
-  const bool live = red[r].m > -INFINITY && S > 0.0;
-  float re = 0.f, im = 0.f;
-  if (live && q < len) {
-    for (int k = kl; k < K; k += 8) {
-      const int u = ra * K + k;
-      if (u < u_lo || u >= u_hi) continue;
-      const float sc = part.scale[u];
-      const float2 v = part.g[(size_t)u * slot_stride + q];
-      re = fmaf(sc, v.x, re);
-      im = fmaf(sc, v.y, im);
-    }
-  }
-  sh[kl][threadIdx.x & 31] = make_float2(re, im);
-  __syncthreads();
-  if (kl == 0 && q < len) {
-    float2 t = sh[0][threadIdx.x];
-#pragma unroll
-    for (int j = 1; j < 8; ++j) {
-      t.x += sh[j][threadIdx.x].x;
-      t.y += sh[j][threadIdx.x].y;
-    }
-    double norm = 0.0;
-    if (live) {
-      norm = eps / (2.0 * N) * extra;
-      norm *= (mode == 1) ? 1.0 / S : pow(S, 1.0 / bp - 1.0);
-    }
-    out[(size_t)ra * len + q] = make_float2((float)(t.x * norm), (float)(t.y * norm));
-  }
-}
-
 // ------------------------------------------------------------------ MAX-mode sparse adjoint
 // Eq. 37's subgradient goes to the unique argmax cell (Q17): recompute A there by the O(N)
 // correlation and write the whole red_grad[r] (zero elsewhere).
@@ -328,60 +343,8 @@ __global__ void k_sparse_adj(int M, int N, int K, int L, int wrt, double eps, co
   }
 }
 
-// ------------------------------------------------------------------ a6 metrics / loss
-__device__ __forceinline__ void decode_key(unsigned long long key, int M, int N, int K, int L, int32_t out[4],
-                                           double* vsq) {
-  if (key == 0ull) {
-    out[0] = out[1] = out[2] = out[3] = -1;
-    *vsq = 0.0;
-    return;
-  }
-  const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
-  out[3] = idx % K;
-  out[2] = (int)((idx / K) % L) - (N - 1);
-  out[1] = (idx / K / L) % M;
-  out[0] = idx / K / L / M;
-  *vsq = (double)__uint_as_float((uint32_t)(key >> 32));
-}
-
-struct MetricsOut {       // mirrors sqngd_metrics (include/sqngd.h)
-  double loss, loss_wpsl, loss_snrl, wapsl, wcpsl, wpsl;
-  int32_t argmax_auto[4], argmax_cross[4];
-  uint32_t flags, n_cells;
-};
-
-__global__ void k_metrics(int M, int N, int K, int L, int mode, double bp, double eps, double ptar,
-                          uint32_t n_cells, uint32_t flags, const Red* __restrict__ red,
-                          const double2* __restrict__ cm, MetricsOut* out, double* p_out, double* loss_hist,
-                          int hist_stride, int hist_col, int* status) {
-  const int r = blockIdx.x;
-  if (threadIdx.x != 0) return;
-  MetricsOut o;
-  double va, vc;
-  decode_key(red[r].key_a, M, N, K, L, o.argmax_auto, &va);
-  decode_key(red[r].key_c, M, N, K, L, o.argmax_cross, &vc);
-  o.wapsl = sqrt(va) / N;
-  o.wcpsl = sqrt(vc) / N;
-  o.wpsl = fmax(o.wapsl, o.wcpsl);
-  if (mode == 0) o.loss_wpsl = o.wpsl;
-  else if (red[r].m > -INFINITY && red[r].S > 0.0)
-    o.loss_wpsl = mode == 1 ? red[r].m + log(red[r].S) / bp : red[r].m * pow(red[r].S, 1.0 / bp);
-  else o.loss_wpsl = 0.0;
-  double lsn = 0.0;
-  for (int m = 0; m < M; ++m) {
-    const double2 c = cm[(size_t)r * M + m];
-    const double p = sqrt(c.x * c.x + c.y * c.y) / N;
-    if (p_out) p_out[(size_t)r * M + m] = p;
-    if (p == 0.0) atomicOr(status, ST_DEGENERATE);
-    lsn += (p - ptar) * (p - ptar);
-  }
-  o.loss_snrl = lsn / M;
-  o.loss = eps * o.loss_wpsl + (1.0 - eps) * o.loss_snrl;
-  o.flags = flags;
-  o.n_cells = n_cells;
-  if (!isfinite(o.loss)) atomicOr(status, ST_NONFINITE);
-  if (out) out[r] = o;
-  if (loss_hist) loss_hist[(size_t)r * hist_stride + hist_col] = o.loss;
+__global__ void k_metrics(MetricsArgs a, int* status) {
+  if (threadIdx.x == 0) metrics_one(a, blockIdx.x, status);
 }
 
 // ------------------------------------------------------------------ finalize gradients
@@ -389,74 +352,181 @@ __global__ void k_metrics(int M, int N, int K, int L, int mode, double bp, doubl
 // Step B: g = red_grad + Gc_m w_m = dL/ds^*; optional grad_s; dy = 4 pi Im(g conj(s)),
 //         grad_z = dq * dy (Eqs. 23-24 chain).
 // Gc_m = (1-eps)(2/M)(p_m - p_tar)/N * c_m / (2|c_m|)   (Eq. 41 on c_m = A_mm(0,0)).
-__global__ void k_finalize_grad(int R, int M, int N, int wrt, double eps, double ptar,
-                                const double2* __restrict__ cm, const float2* __restrict__ red_grad,
-                                const float2* __restrict__ s, const float2* __restrict__ w,
-                                const float* __restrict__ dq, float2* grad_w, float2* grad_s, float* dy,
-                                float* grad_z, int* status) {
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)R * M * N) return;
-  const size_t row = e / N;
-  const int m = (int)(row % M);
-  const double2 c = cm[row];
+struct FinArgs {
+  int R, M, N, wrt;
+  double eps, ptar;
+  const double2* cm;
+  const float2* s;
+  const float2* w;
+  const float* dq;
+  float2* grad_w;
+  float2* grad_s;
+  float* dy;
+  float* grad_z;
+};
+
+// Element e = (row, n) of the final gradient from the WPSL part rg (true units):
+// Step A: grad_w = 2 (rg + conj(Gc_l) s_l)           (Q16)
+// Step B: g = rg + Gc_m w_m = dL/ds^*; dy = 4 pi Im(g conj(s)), grad_z = dq * dy (Eqs. 23-24)
+// Gc_m = (1-eps)(2/M)(p_m - p_tar)/N * c_m / (2|c_m|)   (Eq. 41 on c_m = A_mm(0,0)).
+__device__ __forceinline__ double2 snrl_coef(const FinArgs& f, size_t row) {
+  const double2 c = f.cm[row];
   const double mag = sqrt(c.x * c.x + c.y * c.y);
-  double gr = 0.0, gi = 0.0;
-  if (mag > 0.0) {
-    const double f = (1.0 - eps) * (2.0 / M) * (mag / N - ptar) / N / (2.0 * mag);
-    gr = f * c.x;
-    gi = f * c.y;
-  }
-  (void)m;
-  const float2 rg = red_grad[e];
-  bool bad = false;
-  if (wrt == 1) {
-    const float2 sv = s[e];  // conj(Gc) s
-    const float re = rg.x + (float)(gr * sv.x + gi * sv.y);
-    const float im = rg.y + (float)(gr * sv.y - gi * sv.x);
-    if (grad_w) grad_w[e] = make_float2(2.f * re, 2.f * im);
+  if (!(mag > 0.0)) return make_double2(0.0, 0.0);
+  const double q = (1.0 - f.eps) * (2.0 / f.M) * (mag / f.N - f.ptar) / f.N / (2.0 * mag);
+  return make_double2(q * c.x, q * c.y);
+}
+
+__device__ __forceinline__ void finalize_elem(const FinArgs& f, size_t e, float2 rg, double2 gc, int* status) {
+  const float gr = (float)gc.x, gi = (float)gc.y;
+  bool bad;
+  if (f.wrt == 1) {
+    const float2 sv = f.s[e];  // conj(Gc) s
+    const float re = rg.x + (gr * sv.x + gi * sv.y);
+    const float im = rg.y + (gr * sv.y - gi * sv.x);
+    if (f.grad_w) f.grad_w[e] = make_float2(2.f * re, 2.f * im);
     bad = !isfinite(re) || !isfinite(im);
   } else {
-    const float2 wv = w[e];  // Gc w
-    const float re = rg.x + (float)(gr * wv.x - gi * wv.y);
-    const float im = rg.y + (float)(gr * wv.y + gi * wv.x);
-    if (grad_s) grad_s[e] = make_float2(re, im);
-    const float2 sv = s[e];
+    const float2 wv = f.w[e];  // Gc w
+    const float re = rg.x + (gr * wv.x - gi * wv.y);
+    const float im = rg.y + (gr * wv.y + gi * wv.x);
+    if (f.grad_s) f.grad_s[e] = make_float2(re, im);
+    const float2 sv = f.s[e];
     const float d = 4.f * 3.14159265358979f * (im * sv.x - re * sv.y);  // Im(g conj(s))
-    if (dy) dy[e] = d;
-    if (grad_z) grad_z[e] = dq[e] * d;
+    if (f.dy) f.dy[e] = d;
+    if (f.grad_z) f.grad_z[e] = f.dq[e] * d;
     bad = !isfinite(re) || !isfinite(im);
   }
   if (bad) atomicOr(status, ST_NONFINITE);
 }
 
+__global__ void k_finalize_grad(FinArgs f, const float2* __restrict__ red_grad, int* status, MetricsArgs ma) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0 && blockIdx.x < (unsigned)f.R && (ma.out || ma.loss_hist)) metrics_one(ma, blockIdx.x, status);
+  if (e >= (size_t)f.R * f.M * f.N) return;
+  finalize_elem(f, e, red_grad[e], snrl_coef(f, e / f.N), status);
+}
+
+// Step A tail: d_l = IFFT_P(spectral sum)[0..N) per (r, l) row (forward FFT of the conjugate),
+// then finalize.
+template <class PL, int G>
+__global__ void __launch_bounds__(PL::T* G)
+    k_rows_ifft_fin(int rows, const float2* __restrict__ in, const float2* __restrict__ ftw, FinArgs f, int* status) {
+  constexpr int E = PL::E, T = PL::T, P = PL::P;
+  extern __shared__ float4 smem_raw[];
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  const int id = blockIdx.x * G + grp;
+  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
+  GroupSync sync{1 + grp, T, group_mask(T)};
+  const int row = id < rows ? id : rows - 1;
+  float2 v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float2 x = __ldg(in + (size_t)row * P + t + i * T);
+    v[i] = make_float2(x.x, -x.y);
+  }
+  int par = 0;
+  fft<PL, -1>(v, ftw, xbuf, t, par, sync);
+  if (id >= rows) return;
+  const double2 gc = snrl_coef(f, row);
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    if (n < f.N) finalize_elem(f, (size_t)row * f.N + n, make_float2(v[i].x, -v[i].y), gc, status);
+  }
+}
+
+struct CombineArgs {
+  int M, N, K, len, slot_stride, u_lo, u_hi, mode;
+  double bp, eps, extra;
+  Part part;
+  const Red* red;     // restart shift / sum (from k_reduce_groups or the multi-GPU all-reduce)
+  float2* out;        // [R*M][len] (when !fin)
+  int fin;            // 1: apply finalize_elem to each output (len == N)
+  FinArgs f;
+};
+
+// Unit slots -> per-row sums in true units of dL_wpsl / d(.)^*:
+// out[ra][q] = norm_r * sum_k scale_u slot_u[q],  u = ra K + k  (fixed order),
+// norm_r = eps/(2N) * extra * (LSE: 1/S_r, PNORM: S_r^{1/p-1}).
+// Block: 32 lanes x 2 complex (q) x 8 k-lanes.
+__global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status) {
+  __shared__ float4 sh[8][33];
+  const int ra = blockIdx.y;
+  const int r = ra / a.M;
+  const double m = a.red[r].m, S = a.red[r].S;
+  const bool live = m > -INFINITY && S > 0.0;
+  const int q = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));  // two complex values per thread
+  const int kl = threadIdx.x >> 5;                              // 8 k-lanes
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (live && q < a.len) {
+    const int klo = max(0, a.u_lo - ra * a.K), khi = min(a.K, a.u_hi - ra * a.K);
+#pragma unroll 4
+    for (int k = klo + kl; k < khi; k += 8) {
+      const int u = ra * a.K + k;
+      const float sc = __ldg(a.part.scale + u);
+      const float4 v = __ldg(reinterpret_cast<const float4*>(a.part.g + (size_t)u * a.slot_stride + q));
+      acc.x = fmaf(sc, v.x, acc.x);
+      acc.y = fmaf(sc, v.y, acc.y);
+      acc.z = fmaf(sc, v.z, acc.z);
+      acc.w = fmaf(sc, v.w, acc.w);
+    }
+  }
+  sh[kl][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (kl == 0 && q < a.len) {
+    float4 t = sh[0][threadIdx.x];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      t.x += sh[j][threadIdx.x].x;
+      t.y += sh[j][threadIdx.x].y;
+      t.z += sh[j][threadIdx.x].z;
+      t.w += sh[j][threadIdx.x].w;
+    }
+    double norm = 0.0;
+    if (live) {
+      norm = a.eps / (2.0 * a.N) * a.extra;
+      norm *= (a.mode == 1) ? 1.0 / S : pow(S, 1.0 / a.bp - 1.0);
+    }
+    const float nf = (float)norm;
+    const float2 g0 = make_float2(t.x * nf, t.y * nf), g1 = make_float2(t.z * nf, t.w * nf);
+    if (a.fin) {
+      const double2 gc = snrl_coef(a.f, ra);
+      finalize_elem(a.f, (size_t)ra * a.N + q, g0, gc, status);
+      if (q + 1 < a.len) finalize_elem(a.f, (size_t)ra * a.N + q + 1, g1, gc, status);
+    } else {
+      float2* o = a.out + (size_t)ra * a.len + q;
+      o[0] = g0;
+      if (q + 1 < a.len) o[1] = g1;
+    }
+  }
+}
+
 // dL/drho_i = -a c sum_e sech^2(c (z_e - rho_i)) dy_e, gathered per threshold over a chunk of
-// elements (partials [R][nchunk][BR], then a fixed-order sum).  Culled outside |c(z - rho)| < 12.
+// elements (partials [R][nchunk][BR], then a fixed-order sum).  sech^2 via MUFU, culled
+// (branch-free) outside |c (z - rho)| < 12 where it is < 1.6e-10.
 __global__ void k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
                                 const float* __restrict__ rho, const float* __restrict__ dy, float* part) {
-  __shared__ float zs[256], ds[256];  // chunk <= 256
+  __shared__ float2 zd[256];  // chunk <= 256: (z, dy)
   const int r = blockIdx.z;
   const int ch = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const float ri = i < BR ? rho[(size_t)r * BR + i] : 0.f;
   const int e0 = ch * chunk, e1 = min(MN, e0 + chunk);
+  for (int e = e0 + threadIdx.x; e < e0 + 256; e += blockDim.x)
+    zd[e - e0] = e < e1 ? make_float2(z[(size_t)r * MN + e], dy[(size_t)r * MN + e]) : make_float2(1e30f, 0.f);
+  __syncthreads();
+  const float k2 = -2.f * 1.4426950408889634f;
   float acc = 0.f;
-  for (int base = e0; base < e1; base += 256) {
-    __syncthreads();
-    const int e = base + threadIdx.x;
-    if (threadIdx.x < 256) {
-      zs[threadIdx.x] = e < e1 ? z[(size_t)r * MN + e] : 1e30f;
-      ds[threadIdx.x] = e < e1 ? dy[(size_t)r * MN + e] : 0.f;
-    }
-    __syncthreads();
-    const int n = min(256, e1 - base);
-    for (int q = 0; q < n; ++q) {
-      const float u = c * (zs[q] - ri);
-      if (fabsf(u) < 12.f) {
-        const float e2 = __expf(-2.f * fabsf(u));
-        const float inv = 1.f / (1.f + e2);
-        acc += 4.f * e2 * inv * inv * ds[q];
-      }
-    }
+  const int n = e1 - e0;
+#pragma unroll 4
+  for (int q = 0; q < n; ++q) {
+    const float2 p = zd[q];
+    const float au = c * fabsf(p.x - ri);  // z - rho exact when close (Sterbenz)
+    const float e2 = ex2a_m(k2 * au);               // e^{-2|u|}
+    const float inv = rcp_m(1.f + e2);
+    const float sech2 = 4.f * e2 * inv * inv;        // sech^2(u)
+    acc = fmaf(au < 12.f ? sech2 : 0.f, p.y, acc);
   }
   if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
 }
@@ -471,10 +541,30 @@ __global__ void k_grad_rho_sum(int BR, int nchunk, float coef, const float* __re
 }
 
 // ------------------------------------------------------------------ a9 optimizer
+// Adam hyper-parameters; the step count t = dt[which] + off + 1 is read on the device so a
+// captured CUDA graph stays valid from one sqngd_step call to the next (bias corrections, Q15).
+struct AdamP {
+  float lr, b1, b2, eps;
+  const long long* dt;
+  int which, off;
+  __device__ __forceinline__ void corr(float& c1, float& c2) const {
+    const double t = (double)(dt[which] + off + 1);
+    c1 = (float)(1.0 - pow((double)b1, t));
+    c2 = (float)(1.0 - pow((double)b2, t));
+  }
+};
+
+__global__ void k_set_t(long long* dt, long long ta, long long tb) {
+  dt[0] = ta;
+  dt[1] = tb;
+}
+
 __global__ void k_adam(size_t n, float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
-                       const float* __restrict__ g, float lr, float b1, float b2, float eps, float c1, float c2,
-                       const int* __restrict__ status) {
+                       const float* __restrict__ g, AdamP ap, const int* __restrict__ status) {
   if (*status & ST_NONFINITE) return;  // keep the last finite iterate
+  float c1, c2;
+  ap.corr(c1, c2);
+  const float lr = ap.lr, b1 = ap.b1, b2 = ap.b2, eps = ap.eps;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float gi = g[i];
@@ -485,40 +575,66 @@ __global__ void k_adam(size_t n, float* __restrict__ x, float* __restrict__ m, f
   x[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
 }
 
-// Eq. 32: h_m <- sqrt(N / ||h_m||^2) h_m, one block per row, fp64 energy.
-__global__ void k_project_w(int N, float2* w, int* status) {
-  __shared__ double sh[256];
+// Adam on (Re w, Im w) of one filter row, then Eq. 32: h_m <- sqrt(N / ||h_m||^2) h_m (fp64 energy).
+// One block per row; skipped entirely when a non-finite value is latched.
+__global__ void k_adam_project_w(int N, float* w, float* mw, float* vw, const float* __restrict__ g, AdamP ap,
+                                 int* status) {
+  __shared__ double sh[32];
   if (*status & ST_NONFINITE) return;
-  float2* row = w + (size_t)blockIdx.x * N;
+  float c1, c2;
+  ap.corr(c1, c2);
+  const float lr = ap.lr, b1 = ap.b1, b2 = ap.b2, eps = ap.eps;
+  const size_t base = (size_t)blockIdx.x * 2 * N;
   double e = 0.0;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) e += (double)row[n].x * row[n].x + (double)row[n].y * row[n].y;
-  sh[threadIdx.x] = e;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
+  for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) {
+    const size_t j = base + i;
+    const float gi = g[j];
+    const float mi = b1 * mw[j] + (1.f - b1) * gi;
+    const float vi = b2 * vw[j] + (1.f - b2) * gi * gi;
+    mw[j] = mi;
+    vw[j] = vi;
+    const float x = w[j] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    w[j] = x;
+    e += (double)x * x;
   }
-  const double en = sh[0];
+  auto dsum = [](double x, double y) { return x + y; };
+  const double en = block_reduce(e, dsum, sh);
   if (en == 0.0) {
     if (threadIdx.x == 0) atomicOr(status, ST_DEGENERATE);
     return;
   }
   const float sc = (float)sqrt((double)N / en);
-  for (int n = threadIdx.x; n < N; n += blockDim.x) row[n] = make_float2(row[n].x * sc, row[n].y * sc);
+  for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) w[base + i] *= sc;
 }
 
 // Threshold projection: sort ascending, clamp to [lo, hi], forward min-gap sweep.
 // One block (1024 threads) per restart; BR <= 8192.
-__global__ void k_project_rho(int BR, float* rho, float lo, float hi, float gap, const int* status) {
+__global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
+                                   float lo, float hi, float gap, const int* status) {
   extern __shared__ float sr[];
   __shared__ int flag;
   if (*status & ST_NONFINITE) return;
+  float c1, c2;
+  ap.corr(c1, c2);
+  const float lr = ap.lr, b1 = ap.b1, b2 = ap.b2, eps = ap.eps;
   float* p = rho + (size_t)blockIdx.x * BR;
   int n2 = 1;
   while (n2 < BR) n2 <<= 1;
   if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) sr[i] = i < BR ? p[i] : INFINITY;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {  // Adam step, then the projection
+    float x = INFINITY;
+    if (i < BR) {
+      const size_t j = (size_t)blockIdx.x * BR + i;
+      const float gi = g[j];
+      const float mi = b1 * mr[j] + (1.f - b1) * gi;
+      const float vi = b2 * vr[j] + (1.f - b2) * gi * gi;
+      mr[j] = mi;
+      vr[j] = vi;
+      x = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    }
+    sr[i] = x;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i + 1 < BR; i += blockDim.x)
     if (sr[i] > sr[i + 1]) flag = 1;

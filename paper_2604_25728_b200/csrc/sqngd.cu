@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/sqngd.h"
@@ -72,6 +73,20 @@ struct sqngd_ctx_s {
   MetricsOut* met = nullptr;   // [R] scratch
   int* status = nullptr;       // latched device status bits
   Comm comm;
+  long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
+  // CUDA graphs of sqngd_step (one per (state buffers, block, outputs, profiling))
+  struct GraphEntry {
+    const void* key[12];
+    int block;
+    bool prof;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+    std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> marks;  // event-record nodes (profiling)
+    bool replayed = false;
+  };
+  std::vector<GraphEntry*> graphs;
+  GraphEntry* capturing = nullptr;
+  bool use_graphs = true;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -94,17 +109,16 @@ struct ProfScope {
   int cls;
   size_t idx = 0;
   cudaStream_t st;
+  // (profiling runs sqngd_step eagerly: events recorded as graph nodes cannot be timed)
   ProfScope(sqngd_ctx_s* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
-    if (c->prof) {
-      idx = c->ev_used;
-      cudaEventRecord(c->ev_get(), st);
-    }
+    if (!c->prof || c->capturing) return;
+    idx = c->ev_used;
+    cudaEventRecord(c->ev_get(), st);
   }
   ~ProfScope() {
-    if (c->prof) {
-      cudaEventRecord(c->ev_get(), st);
-      c->ev_marks.push_back({cls, idx});
-    }
+    if (!c->prof || c->capturing) return;
+    cudaEventRecord(c->ev_get(), st);
+    c->ev_marks.push_back({cls, idx});
   }
 };
 
@@ -135,7 +149,7 @@ struct Launch {
 
   template <int MODE>
   static size_t smem() { return (size_t)G * GroupSmem<PL, MODE>::TOTAL * sizeof(float2); }
-  static size_t smem_fft() { return (size_t)G * (PL::NP > 1 ? 2 * PL::PADDED : 0) * sizeof(float2) + 16; }
+  static size_t smem_fft() { return (size_t)G * FftSmem<PL>::TOTAL * sizeof(float2) + 16; }
 
   static cudaError_t prepare(int* blocks_per_sm) {
     cudaError_t e;
@@ -151,6 +165,8 @@ struct Launch {
     if (e) return e;
     e = cudaFuncSetAttribute(k_rows_ifft<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
     if (e) return e;
+    e = cudaFuncSetAttribute(k_rows_ifft_fin<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+    if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MINB, MODE_FWD>, THREADS, smem<MODE_FWD>());
     if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], k_af<PL, G, MINB, MODE_ADJ_A>, THREADS, smem<MODE_ADJ_A>());
@@ -162,18 +178,24 @@ struct Launch {
     build_twiddle_table<PL>(t.data());
     return t;
   }
-  static void filter(int RM, int N, const float2* w, const float2* ftw, float2* H, cudaStream_t st) {
+  static void filter(int RM, int N, const float2* w, const float2* ftw, float2* H, const float2* s, double2* cm,
+                     cudaStream_t st) {
     const int blocks = (RM + G - 1) / G;
-    k_filter_fft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(RM, N, w, ftw, H);
+    k_filter_fft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(RM, N, w, ftw, H, s, cm);
   }
   static void xhat(int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftw, float2* Xc,
-                   cudaStream_t st) {
+                   const float2* w, double2* cm, cudaStream_t st) {
     const int blocks = (units + G - 1) / G;
-    k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(units, M, N, K, s, dtw, ftw, Xc);
+    k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(units, M, N, K, s, dtw, ftw, Xc, w, cm);
   }
   static void rows_ifft(int rows, int N, const float2* in, const float2* ftw, float2* out, cudaStream_t st) {
     const int blocks = (rows + G - 1) / G;
     k_rows_ifft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, N, in, ftw, out);
+  }
+  static void rows_ifft_fin(int rows, const float2* in, const float2* ftw, const FinArgs& f, int* status,
+                            cudaStream_t st) {
+    const int blocks = (rows + G - 1) / G;
+    k_rows_ifft_fin<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, in, ftw, f, status);
   }
   static void af(int mode, const KP& kp, int64_t slots, const float2* Xc, const float2* H, const float2* tw,
                  const float2* ftw, float* af_mag, const Part& part, cudaStream_t st) {
@@ -332,6 +354,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&ctx->part.scale, sizeof(float) * ctx->units));
   CK(cudaMalloc(&ctx->counter, sizeof(int)));
+  CK(cudaMalloc(&ctx->d_t, 2 * sizeof(long long)));
+  if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
   CK(cudaMalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   CK(cudaMalloc(&ctx->s_soft, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
@@ -386,7 +410,15 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
 void sqngd_destroy(sqngd_ctx ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
-  void* ptrs[] = {ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+  for (auto* g : ctx->graphs) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    for (auto& mk : g->marks) {
+      cudaEventDestroy(std::get<1>(mk));
+      cudaEventDestroy(std::get<2>(mk));
+    }
+    delete g;
+  }
+  void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status};
   for (void* p : ptrs)
@@ -414,6 +446,15 @@ sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64
     acc[mk.first] += t;
     cnt[mk.first] += 1;
   }
+  for (auto* g : ctx->graphs) {  // graphs replayed since the last reset: their latest replay
+    if (!g->replayed) continue;
+    for (auto& mk : g->marks) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, std::get<1>(mk), std::get<2>(mk)));
+      acc[std::get<0>(mk)] += t;
+      cnt[std::get<0>(mk)] += 1;
+    }
+  }
   for (int i = 0; i < 3; ++i) {
     if (ms) ms[i] = acc[i];
     if (count) count[i] = cnt[i];
@@ -423,6 +464,7 @@ sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64
     ctx->ev_marks.clear();
     ctx->ev_used = 0;
     ctx->launches = 0;
+    for (auto* g : ctx->graphs) g->replayed = false;
   }
   return SQNGD_OK;
 }
@@ -463,19 +505,21 @@ static sqngd_status run_quantize(sqngd_ctx ctx, const float* z, const float* rho
   return launch_check(ctx, "quantize");
 }
 
-static sqngd_status run_filter_fft(sqngd_ctx ctx, const float2* w, cudaStream_t st) {
+// a2 (+ a6 when s is given): H = FFT(w)/P and c_m = sum_n s_m conj(w_m).
+static sqngd_status run_filter_fft(sqngd_ctx ctx, const float2* w, cudaStream_t st, const float2* s = nullptr) {
   const sqngd_config& c = ctx->cfg;
-  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::filter(c.R * c.M, c.N, w, ctx->ftw, ctx->H, st); });
+  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::filter(c.R * c.M, c.N, w, ctx->ftw, ctx->H, s, ctx->cm, st); });
   ctx->launches += 1;
   return launch_check(ctx, "filter fft");
 }
 
-// a3: X cache of the waveform s (all units; each rank only needs its slice but the cache
-// is cheap next to the M^2 K correlations and keeps the slice logic in one place).
-static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st) {
+// a3 (+ a6 when w is given): X cache of the waveform s over all units.
+static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st, const float2* w = nullptr) {
   const sqngd_config& c = ctx->cfg;
   const int units = c.R * c.M * c.K;
-  with_P(ctx->P, [&](auto Lc) { decltype(Lc)::xhat(units, c.M, c.N, c.K, s, ctx->tw, ctx->ftw, ctx->Xc, st); });
+  with_P(ctx->P, [&](auto Lc) {
+    decltype(Lc)::xhat(units, c.M, c.N, c.K, s, ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
+  });
   ctx->launches += 1;
   return launch_check(ctx, "xhat");
 }
@@ -488,7 +532,7 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
                                 double* p_out, double* hist, int hist_col, cudaStream_t st, bool xhat_ready = false) {
   const sqngd_config& c = ctx->cfg;
   if (!xhat_ready) {
-    sqngd_status rx = run_xhat(ctx, s, st);
+    sqngd_status rx = run_xhat(ctx, s, st, w);
     if (rx) return rx;
   }
   KP kp = make_kp(ctx, c.loss_mode != 0);
@@ -502,13 +546,20 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
   ctx->launches += 4;
   sqngd_status rc = launch_check(ctx, "af forward");
   if (rc) return rc;
-  k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
-  if (ctx->world > 1 && (rc = allreduce_red(ctx, st, false, MODE_FWD))) return rc;
-  k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
-  k_metrics<<<c.R, 32, 0, st>>>(c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells,
-                                ctx->flags, ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col,
-                                ctx->status);
+  MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
+                 ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
+  if (ctx->world == 1) {
+    k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
+                                          ctx->red, ma, ctx->status);
+  } else {
+    MetricsArgs none = ma;
+    none.out = nullptr; none.p_out = nullptr; none.loss_hist = nullptr;
+    k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
+                                          ctx->red, none, ctx->status);
+    if ((rc = allreduce_red(ctx, st, false, MODE_FWD))) return rc;
+    k_metrics<<<c.R, 32, 0, st>>>(ma, ctx->status);
+  }
   return launch_check(ctx, "metrics");
 }
 
@@ -520,65 +571,80 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
   const sqngd_config& c = ctx->cfg;
   sqngd_status rc;
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
-  if (!xhat_ready && (rc = run_xhat(ctx, s, st))) return rc;
+  if (!xhat_ready && (rc = run_xhat(ctx, s, st, w))) return rc;
+  FinArgs fa{c.R, c.M, c.N, wrt, c.eps_w, ptar, ctx->cm, s, w, dq, grad_w, grad_s, ctx->dy, grad_z};
+  MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
+                 ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col};
+  const size_t n = (size_t)c.R * c.M * c.N;
   if (c.loss_mode == SQNGD_LOSS_MAX) {
     if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st, true))) return rc;
-    ctx->launches += 1;
     k_sparse_adj<<<c.R, 256, 0, st>>>(c.M, c.N, c.K, ctx->L, wrt, c.eps_w, c.weights, s, w, ctx->tw, ctx->red,
                                       ctx->red_grad);
-    if ((rc = launch_check(ctx, "sparse adjoint"))) return rc;
-  } else {
-    const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
-    KP kp = make_kp(ctx, 1);
-    cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
-    {
-      ProfScope ps(ctx, mode, st);
-      with_P(ctx->P, [&](auto Lc) {
-        decltype(Lc)::af(mode, kp, ctx->slots[mode], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
-      });
-    }
-    ctx->launches += 5;
-    if ((rc = launch_check(ctx, "af adjoint"))) return rc;
-    k_reduce_groups<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
-                                         ctx->red);
-    if (ctx->world > 1) {
-      if ((rc = allreduce_red(ctx, st, false, mode))) return rc;
-      k_group_scales<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
-                                          ctx->red);
-    }
-    if (mode == MODE_ADJ_B) {
-      dim3 grid((c.N + 31) / 32, c.R * c.M);
-      k_combine_rows<<<grid, 256, 0, st>>>(c.M, c.N, c.K, c.N, ctx->P, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p,
-                                           c.eps_w, 1.0, ctx->part, ctx->red, ctx->red_grad);
-    } else {  // spectral sums, then one IFFT per (r, l) row (1/P folded into the norm)
-      dim3 grid((ctx->P + 31) / 32, c.R * c.M);
-      k_combine_rows<<<grid, 256, 0, st>>>(c.M, c.N, c.K, ctx->P, ctx->P, kp.u_lo, kp.u_hi, c.loss_mode,
-                                           c.beta_or_p, c.eps_w, 1.0 / ctx->P, ctx->part, ctx->red, ctx->spec);
-      with_P(ctx->P, [&](auto Lc) {
-        decltype(Lc)::rows_ifft(c.R * c.M, c.N, ctx->spec, ctx->ftw, ctx->red_grad, st);
-      });
-      ctx->launches += 1;
-    }
-    if (ctx->world > 1 && (rc = allreduce_red(ctx, st, true, mode))) return rc;
-    k_mainlobe<<<c.R * c.M, 256, 0, st>>>(c.N, s, w, ctx->cm);
-    k_metrics<<<c.R, 32, 0, st>>>(c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells,
-                                  ctx->flags, ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col,
-                                  ctx->status);
-    if ((rc = launch_check(ctx, "metrics"))) return rc;
+    MetricsArgs none = ma;
+    none.out = nullptr;
+    none.loss_hist = nullptr;
+    k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fa, ctx->red_grad, ctx->status, none);
+    ctx->launches += 2;
+    return launch_check(ctx, "sparse adjoint");
   }
-  const size_t n = (size_t)c.R * c.M * c.N;
+  const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
+  KP kp = make_kp(ctx, 1);
+  cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
+  {
+    ProfScope ps(ctx, mode, st);
+    with_P(ctx->P, [&](auto Lc) {
+      decltype(Lc)::af(mode, kp, ctx->slots[mode], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
+    });
+  }
   ctx->launches += 1;
-  k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c.R, c.M, c.N, wrt, c.eps_w, ptar, ctx->cm,
-                                                                ctx->red_grad, s, w, dq, grad_w, grad_s, ctx->dy,
-                                                                grad_z, ctx->status);
+  if ((rc = launch_check(ctx, "af adjoint"))) return rc;
+  CombineArgs ca{};
+  ca.M = c.M; ca.N = c.N; ca.K = c.K; ca.slot_stride = ctx->P; ca.u_lo = kp.u_lo; ca.u_hi = kp.u_hi;
+  ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.part = ctx->part; ca.red = ctx->red;
+  ca.f = fa;
+  MetricsArgs none = ma;
+  none.out = nullptr; none.loss_hist = nullptr;
+  k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red,
+                                        ctx->world == 1 ? ma : none, ctx->status);
+  ctx->launches += 1;
+  if (ctx->world == 1) {
+    // single GPU: Step B finalizes inside the combine, Step A inside the row IFFT.
+    if (mode == MODE_ADJ_B) {
+      ca.len = c.N; ca.extra = 1.0; ca.fin = 1; ca.out = nullptr;
+      k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      ctx->launches += 1;
+    } else {
+      ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
+      k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftw, fa, ctx->status, st); });
+      ctx->launches += 2;
+    }
+    return launch_check(ctx, "combine");
+  }
+  // multi-GPU: max-then-sum all-reduce of the loss partials, local combine with the global
+  // shift, all-reduce of the gradient, then finalize.
+  if ((rc = allreduce_red(ctx, st, false, mode))) return rc;
+  k_group_scales<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
+  ca.fin = 0;
+  if (mode == MODE_ADJ_B) {
+    ca.len = c.N; ca.extra = 1.0; ca.out = ctx->red_grad;
+    k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+  } else {
+    ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.out = ctx->spec;
+    k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft(c.R * c.M, c.N, ctx->spec, ctx->ftw, ctx->red_grad, st); });
+  }
+  if ((rc = allreduce_red(ctx, st, true, mode))) return rc;
+  k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fa, ctx->red_grad, ctx->status, ma);
+  ctx->launches += 4;
   return launch_check(ctx, "finalize grad");
 }
 
 static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho, float* grad_rho, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   const int MN = c.M * c.N;
-  dim3 g1((ctx->BR + 127) / 128, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
-  k_grad_rho_part<<<g1, 128, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part);
+  dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
+  k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part);
   dim3 g2((ctx->BR + 127) / 128, c.R);
   const float coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
   k_grad_rho_sum<<<g2, 128, 0, st>>>(ctx->BR, ctx->rho_nchunk, coef, ctx->rho_part, grad_rho);
@@ -661,34 +727,30 @@ sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho,
   return SQNGD_OK;
 }
 
-sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss_hist, sqngd_metrics* hard_out,
-                        sqngd_stream stream) {
-  if (!ctx || !stt || !stt->z || !stt->rho || !stt->w || (block & ~3) || !block)
-    return fail(ctx, SQNGD_E_INVALID, "sqngd_step: bad argument");
-  CK(cudaSetDevice(ctx->dev));
+}  // extern "C"
+
+// The body of one sqngd_step: every launch goes to `st` (capturable).  Adam reads the
+// step counters from ctx->d_t (set before the body), so the same graph serves every call.
+static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, double* loss_hist,
+                              sqngd_metrics* hard_out, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
-  const cudaStream_t st = S(stream);
   const size_t RMN = (size_t)c.R * c.M * c.N;
   float2* w2 = reinterpret_cast<float2*>(stt->w);
   sqngd_status rc;
-  auto adam = [&](size_t n, float* x, float* m, float* v, const float* g, int64_t t, double lr) {
-    const float c1 = (float)(1.0 - std::pow(c.adam_b1, (double)t));
-    const float c2 = (float)(1.0 - std::pow(c.adam_b2, (double)t));
-    k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, x, m, v, g, (float)lr, (float)c.adam_b1, (float)c.adam_b2,
-                                                         (float)c.adam_eps, c1, c2, ctx->status);
-    ctx->launches += 1;
+  auto ap = [&](double lr, int which, int off) {
+    return AdamP{(float)lr, (float)c.adam_b1, (float)c.adam_b2, (float)c.adam_eps, ctx->d_t, which, off};
   };
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
     if ((rc = run_xhat(ctx, ctx->s_hard, st))) return rc;  // X_hard fixed for the whole block
     for (int i = 0; i < c.n_h; ++i) {
-      if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+      if ((rc = run_filter_fft(ctx, w2, st, ctx->s_hard))) return rc;
       if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, ctx->gw, nullptr, nullptr, nullptr,
                               loss_hist, i, st, true)))
         return rc;
-      stt->t_a += 1;
-      adam(2 * RMN, stt->w, stt->m_w, stt->v_w, reinterpret_cast<const float*>(ctx->gw), stt->t_a, c.lr_w);
-      k_project_w<<<c.R * c.M, 256, 0, st>>>(c.N, w2, ctx->status);
+      k_adam_project_w<<<c.R * c.M, 1024, 0, st>>>(c.N, stt->w, stt->m_w, stt->v_w,
+                                                   reinterpret_cast<const float*>(ctx->gw), ap(c.lr_w, 0, i),
+                                                   ctx->status);
       ctx->launches += 1;
       if ((rc = launch_check(ctx, "step A update"))) return rc;
     }
@@ -696,19 +758,20 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
   if (block & SQNGD_BLOCK_B) {  // Step B: transmit parameters with H fixed
     if ((rc = run_filter_fft(ctx, w2, st))) return rc;
     const int col0 = (block & SQNGD_BLOCK_A) ? c.n_h : 0;
+    int n2 = 1;
+    while (n2 < ctx->BR) n2 <<= 1;
     for (int i = 0; i < c.n_x; ++i) {
       if ((rc = run_quantize(ctx, stt->z, stt->rho, ctx->s_soft, nullptr, nullptr, ctx->dq, st))) return rc;
       if ((rc = run_loss_grad(ctx, ctx->s_soft, w2, SQNGD_WRT_TRANSMIT, ctx->met, nullptr, nullptr, ctx->dq, ctx->gz,
                               loss_hist, col0 + i, st)))
         return rc;
       if ((rc = run_grad_rho(ctx, stt->z, stt->rho, ctx->grho, st))) return rc;
-      stt->t_b += 1;
-      adam(RMN, stt->z, stt->m_z, stt->v_z, ctx->gz, stt->t_b, c.lr_z);
-      adam((size_t)c.R * ctx->BR, stt->rho, stt->m_rho, stt->v_rho, ctx->grho, stt->t_b, c.lr_z);
-      int n2 = 1;
-      while (n2 < ctx->BR) n2 <<= 1;
-      k_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, 1e-4f, 1.0f - 1e-4f, 1e-6f, ctx->status);
-      ctx->launches += 1;
+      k_adam<<<(unsigned)((RMN + 255) / 256), 256, 0, st>>>(RMN, stt->z, stt->m_z, stt->v_z, ctx->gz, ap(c.lr_z, 1, i),
+                                                            ctx->status);
+      k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
+                                                                    ctx->grho, ap(c.lr_z, 1, i), 1e-4f, 1.0f - 1e-4f,
+                                                                    1e-6f, ctx->status);
+      ctx->launches += 2;
       if ((rc = launch_check(ctx, "step B update"))) return rc;
     }
   }
@@ -719,6 +782,66 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
                           st)))
       return rc;
   }
+  return SQNGD_OK;
+}
+
+extern "C" {
+
+sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss_hist, sqngd_metrics* hard_out,
+                        sqngd_stream stream) {
+  if (!ctx || !stt || !stt->z || !stt->rho || !stt->w || (block & ~3) || !block)
+    return fail(ctx, SQNGD_E_INVALID, "sqngd_step: bad argument");
+  CK(cudaSetDevice(ctx->dev));
+  const sqngd_config& c = ctx->cfg;
+  const cudaStream_t st = S(stream);
+  sqngd_status rc;
+  k_set_t<<<1, 1, 0, st>>>(ctx->d_t, stt->t_a, stt->t_b);
+  ctx->launches += 1;
+  // Graph path: single GPU, a capturable (non-legacy) stream.
+  const bool graph_ok = ctx->use_graphs && !ctx->prof && ctx->world == 1 && st != nullptr &&
+                        st != cudaStreamLegacy && st != cudaStreamPerThread;
+  if (!graph_ok) {
+    if ((rc = step_body(ctx, stt, block, loss_hist, hard_out, st))) return rc;
+  } else {
+    const void* key[12] = {stt->z, stt->rho, stt->w, stt->m_z, stt->v_z, stt->m_rho, stt->v_rho, stt->m_w, stt->v_w,
+                           loss_hist, hard_out, st};
+    sqngd_ctx_s::GraphEntry* ge = nullptr;
+    for (auto* g : ctx->graphs)
+      if (g->block == block && g->prof == ctx->prof && std::memcmp(g->key, key, sizeof(key)) == 0) ge = g;
+    if (!ge) {
+      ge = new sqngd_ctx_s::GraphEntry();
+      std::memcpy(ge->key, key, sizeof(key));
+      ge->block = block;
+      ge->prof = ctx->prof;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      ctx->capturing = ge;
+      const int64_t l0 = ctx->launches;
+      rc = step_body(ctx, stt, block, loss_hist, hard_out, st);
+      ctx->capturing = nullptr;
+      ge->launches = ctx->launches - l0;
+      ctx->launches = l0;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(st, &graph);
+      if (rc != SQNGD_OK || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        delete ge;
+        if (rc) return rc;
+        return fail(ctx, SQNGD_E_CUDA, "sqngd_step: graph capture", cudaGetErrorString(e));
+      }
+      e = cudaGraphInstantiate(&ge->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        delete ge;
+        return fail(ctx, SQNGD_E_CUDA, "sqngd_step: graph instantiate", cudaGetErrorString(e));
+      }
+      ctx->graphs.push_back(ge);
+    }
+    CK(cudaGraphLaunch(ge->exec, st));
+    ge->replayed = true;
+    ctx->launches += ge->launches;
+  }
+  if (block & SQNGD_BLOCK_A) stt->t_a += c.n_h;
+  if (block & SQNGD_BLOCK_B) stt->t_b += c.n_x;
   return SQNGD_OK;
 }
 

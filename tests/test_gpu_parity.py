@@ -241,3 +241,30 @@ def test_determinism():
     ctx.sync()
     for m_, g_ in outs[1:]:
         assert torch.equal(m_, outs[0][0]) and torch.equal(g_, outs[0][1])
+
+
+def test_step_graph_replay_matches_eager():
+    """sqngd_step on a side stream is captured into a CUDA graph and replayed; the result must be
+    bit-identical to the eager (legacy-stream) execution of the same steps."""
+    c = Cfg("graph", M=2, N=48, B=4, K=5, f_lo=-0.5, f_hi=0.5, r_n=4, n_h=2, n_x=2, lr_z=1e-3)
+    z = inputs.phase_params(1, c.M, c.N, config_index=14)
+    rho = inputs.init_thresholds(1, c.B, c.r_n)
+    w = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
+    ctx = sqngd.Context(c)
+    outs = []
+    for use_side in (False, True):
+        st = ctx.new_state(T(z), T(rho), T(w))
+        hist = torch.zeros((1, 4), dtype=torch.float64, device=DEV)
+        hard = torch.empty(sqngd.METRICS_BYTES, dtype=torch.uint8, device=DEV)
+        stream = torch.cuda.Stream() if use_side else torch.cuda.default_stream()
+        with torch.cuda.stream(stream):
+            for _ in range(3):  # first call captures, later calls replay
+                ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+        torch.cuda.synchronize()
+        ctx.sync()
+        outs.append((st, hist.clone(), hard.clone()))
+    (a, ha, ma), (b, hb, mb) = outs
+    for k in ("z", "rho", "w", "m_w", "v_w", "m_z", "v_z", "m_rho", "v_rho"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(ha, hb) and torch.equal(ma, mb)
+    assert a["t_a"] == b["t_a"] == 6 and a["t_b"] == b["t_b"] == 6
