@@ -32,10 +32,13 @@ thread_local std::string g_last_error;
 #ifndef SQNGD_MINB256
 #define SQNGD_MINB256 2
 #endif
+#ifndef SQNGD_MINB128
+#define SQNGD_MINB128 3
+#endif
 constexpr int plan_E(int P) { return P <= SQNGD_E ? P : SQNGD_E; }
 constexpr int plan_G(int P) { return (P / plan_E(P)) >= 128 ? 1 : 128 / (P / plan_E(P)); }
 constexpr int plan_MINB(int P) {
-  return (P / plan_E(P)) * plan_G(P) >= 512 ? 1 : (P / plan_E(P)) * plan_G(P) >= 256 ? SQNGD_MINB256 : 4;
+  return (P / plan_E(P)) * plan_G(P) >= 512 ? 1 : (P / plan_E(P)) * plan_G(P) >= 256 ? SQNGD_MINB256 : SQNGD_MINB128;
 }
 
 }  // namespace
