@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 from paper_2604_25728_b200 import configs as CF  # noqa: E402
-from paper_2604_25728_b200 import inputs  # noqa: E402
+from paper_2604_25728_b200 import inputs, parallel  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "loss+grad evals/s"
@@ -236,8 +236,8 @@ def main():
     torch.cuda.set_stream(side)
     # inputs: this rank's restarts r = rank*R .. (independent seeded problems)
     R = c.R
-    z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, rank * R + r), c.M * c.N).reshape(c.M, c.N)
-                  for r in range(R)])
+    z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, g), c.M * c.N).reshape(c.M, c.N)
+                  for g in parallel.restart_ids(R, rank)])
     rho = inputs.init_thresholds(R, c.B, c.r_n)
     ctx = sqngd.Context(c, device=local)
     zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
@@ -282,10 +282,7 @@ def main():
     ctx.profile(False)
     prof_step_ms = None
     tot_ms = sum(step_ms)
-    if dist:
-        tt = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tot_ms = float(tt.item())
+    tot_ms = parallel.max_over_ranks(tot_ms)
     evals_per_step = (c.n_h + c.n_x) * R * world
     value = evals_per_step * args.steps / (tot_ms / 1e3)
 
@@ -324,10 +321,7 @@ def main():
             e2e_ev.append((a, b))
     torch.cuda.synchronize(dev)
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
-    if dist:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    e2e_ms = parallel.max_over_ranks(e2e_ms)
     e2e_value = evals_per_step * args.steps / (e2e_ms / 1e3)
     hm = sqngd.metrics_from_bytes(host_hard.numpy())
 
