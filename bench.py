@@ -53,6 +53,16 @@ def work_model(c):
             "filter": M * F * c.R, "cells": cells * c.R}
 
 
+def traffic_bytes(kind):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
+    capture of this round (profiles/), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["dram_bytes_per_launch"]
+        return d.get({"adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>", "fwd": "k_af<FWD>"}[kind])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -333,7 +343,7 @@ def main():
         "cells_per_s": value * c.cells / c.R,
         "roofline": {"bound": "alu", "kernel": {"fwd": "k_af<FWD>", "adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>"}[names[dom]],
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None, "avg_launch_ms": avg_ms, "launches": prof["count"][dom],
+                     "traffic": traffic_bytes(names[dom]), "avg_launch_ms": avg_ms, "launches": prof["count"][dom],
                      "flops_per_launch": wm[names[dom]],
                      "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
                      "share_of_step": prof["ms"][dom] / tot_ms,
