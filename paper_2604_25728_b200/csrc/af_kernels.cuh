@@ -30,6 +30,7 @@
 #pragma once
 #include <stdint.h>
 
+#include "common.cuh"
 #include "fft.cuh"
 
 namespace sq {
@@ -48,13 +49,7 @@ struct KP {
   int* counter;          // dynamic unit counter (zeroed before the launch)
 };
 
-struct Part {                // one slot per unit u = (r * M + a) * K + k
-  unsigned long long* key;  // [U][2]  (auto, cross)
-  float* m;                 // [U] shift of the unit's sums
-  float* S;                 // [U] sum of phi (LSE: e^{b(v-m)}, PNORM: (v/m)^p)
-  float* scale;             // [U] rescale to the restart's global shift (combine)
-  float2* g;                // [U][P] adjoint partial: Step B time domain (N used), Step A spectral
-};
+
 
 __device__ __forceinline__ unsigned long long pack_key(float val, uint32_t idx) {
   return ((unsigned long long)__float_as_uint(val) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);

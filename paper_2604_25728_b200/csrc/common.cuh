@@ -1,0 +1,171 @@
+// Definitions shared by the fused kernels and the small kernels: status bits, MUFU helpers,
+// Adam parameters, the per-restart reduction record and metrics (a6), block reductions.
+#pragma once
+#include <stdint.h>
+
+namespace sq {
+
+enum : int { ST_INVALID = 1, ST_DEGENERATE = 2, ST_NONFINITE = 4 };
+
+__device__ __forceinline__ float ex2a_m(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_m(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Adam hyper-parameters; the step count t = dt[which] + off + 1 is read on the device so a
+// captured CUDA graph stays valid from one sqngd_step call to the next (bias corrections, Q15).
+struct AdamP {
+  float lr, b1, b2, eps;
+  const long long* dt;
+  int which, off;
+  __device__ __forceinline__ void corr(float& c1, float& c2) const {
+    const double t = (double)(dt[which] + off + 1);
+    c1 = (float)(1.0 - pow((double)b1, t));
+    c2 = (float)(1.0 - pow((double)b2, t));
+  }
+};
+
+struct Red {               // per restart, after combining all groups
+  double m;                // shift of S and of the gradient partials
+  double S;                // sum of phi at shift m
+  unsigned long long key_a, key_c;
+};
+
+
+struct Part {                // one slot per unit u = (r * M + a) * K + k
+  unsigned long long* key;  // [U][2]  (auto, cross)
+  float* m;                 // [U] shift of the unit's sums
+  float* S;                 // [U] sum of phi (LSE: e^{b(v-m)}, PNORM: (v/m)^p)
+  float* scale;             // [U] rescale to the restart's global shift (combine)
+  float2* g;                // [U][P] adjoint partial: Step B time domain (N used), Step A spectral
+};
+
+__device__ __forceinline__ void decode_key(unsigned long long key, int M, int N, int K, int L, int32_t out[4],
+                                           double* vsq) {
+  if (key == 0ull) {
+    out[0] = out[1] = out[2] = out[3] = -1;
+    *vsq = 0.0;
+    return;
+  }
+  const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+  out[3] = idx % K;
+  out[2] = (int)((idx / K) % L) - (N - 1);
+  out[1] = (idx / K / L) % M;
+  out[0] = idx / K / L / M;
+  *vsq = (double)__uint_as_float((uint32_t)(key >> 32));
+}
+
+struct MetricsOut {       // mirrors sqngd_metrics (include/sqngd.h)
+  double loss, loss_wpsl, loss_snrl, wapsl, wcpsl, wpsl;
+  int32_t argmax_auto[4], argmax_cross[4];
+  uint32_t flags, n_cells;
+};
+
+struct MetricsArgs {
+  int M, N, K, L, mode;
+  double bp, eps, ptar;
+  uint32_t n_cells, flags;
+  const Red* red;
+  const double2* cm;
+  MetricsOut* out;
+  double* p_out;
+  double* loss_hist;
+  int hist_stride, hist_col;
+};
+
+// Eqs. 7-10, 37-42 for restart r from the combined partials.
+__device__ void metrics_one(const MetricsArgs& a, int r, int* status) {
+  MetricsOut o;
+  double va, vc;
+  decode_key(a.red[r].key_a, a.M, a.N, a.K, a.L, o.argmax_auto, &va);
+  decode_key(a.red[r].key_c, a.M, a.N, a.K, a.L, o.argmax_cross, &vc);
+  o.wapsl = sqrt(va) / a.N;
+  o.wcpsl = sqrt(vc) / a.N;
+  o.wpsl = fmax(o.wapsl, o.wcpsl);
+  if (a.mode == 0) o.loss_wpsl = o.wpsl;
+  else if (a.red[r].m > -INFINITY && a.red[r].S > 0.0)
+    o.loss_wpsl = a.mode == 1 ? a.red[r].m + log(a.red[r].S) / a.bp : a.red[r].m * pow(a.red[r].S, 1.0 / a.bp);
+  else o.loss_wpsl = 0.0;
+  double lsn = 0.0;
+  for (int m = 0; m < a.M; ++m) {
+    const double2 c = a.cm[(size_t)r * a.M + m];
+    const double p = sqrt(c.x * c.x + c.y * c.y) / a.N;
+    if (a.p_out) a.p_out[(size_t)r * a.M + m] = p;
+    if (p == 0.0) atomicOr(status, ST_DEGENERATE);
+    lsn += (p - a.ptar) * (p - a.ptar);
+  }
+  o.loss_snrl = lsn / a.M;
+  o.loss = a.eps * o.loss_wpsl + (1.0 - a.eps) * o.loss_snrl;
+  o.flags = a.flags;
+  o.n_cells = a.n_cells;
+  if (!isfinite(o.loss)) atomicOr(status, ST_NONFINITE);
+  if (a.out) a.out[r] = o;
+  if (a.loss_hist) a.loss_hist[(size_t)r * a.hist_stride + a.hist_col] = o.loss;
+}
+
+// Block-wide fixed-order reductions (warp shuffles, then the warps in index order).
+template <class T_, class Op>
+__device__ __forceinline__ T_ block_reduce(T_ x, Op op, T_* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[w] = x;
+  __syncthreads();
+  x = sh[0];
+  for (int i = 1; i < nw; ++i) x = op(x, sh[i]);
+  return x;
+}
+
+// Per restart r: max keys, global shift and the rescaled sum S over the restart's units
+// [r * GPR, (r+1) * GPR) intersected with [g_lo, g_hi); per-unit rescale factors for the
+// gradient combine; the metrics.  Called by a whole block (fixed order, deterministic).
+// Partials are read with ld.global.cg: in the fused kernel's last CTA they were written by
+// other SMs in the same launch.
+__device__ void reduce_restart(int r, int GPR, int g_lo, int g_hi, int mode, double bp, Part part, Red* red,
+                               const MetricsArgs& ma, int* status, double* shd, unsigned long long* shk) {
+  const int lo = max(g_lo, r * GPR), hi = min(g_hi, (r + 1) * GPR);
+  double mloc = -INFINITY;
+  unsigned long long a = 0, cc = 0;
+  for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
+    if (__ldcg(part.S + g) > 0.f) mloc = fmax(mloc, (double)__ldcg(part.m + g));
+    a = max(a, __ldcg(part.key + 2 * g));
+    cc = max(cc, __ldcg(part.key + 2 * g + 1));
+  }
+  auto dmax = [](double x, double y) { return fmax(x, y); };
+  auto umax = [](unsigned long long x, unsigned long long y) { return x > y ? x : y; };
+  const double m = block_reduce(mloc, dmax, shd);
+  a = block_reduce(a, umax, shk);
+  cc = block_reduce(cc, umax, shk);
+  double S = 0.0;
+  const float mf = (float)m;
+  const float lb = (float)(bp * 1.4426950408889634);
+  for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
+    float sc = 0.f;
+    const float Sg = __ldcg(part.S + g);
+    if (mode != 0 && Sg > 0.f && m > -INFINITY) {
+      const float mg = __ldcg(part.m + g);
+      sc = mode == 1 ? exp2f(lb * (mg - mf)) : exp2f((float)(bp - 1.0) * log2f(mg / mf));
+      S += (double)Sg * (mode == 1 ? sc : sc * (mg / mf));
+    }
+    if (part.scale) part.scale[g] = sc;
+  }
+  auto dsum = [](double x, double y) { return x + y; };
+  S = block_reduce(S, dsum, shd);
+  if (threadIdx.x == 0) {
+    red[r].m = m;
+    red[r].S = S;
+    red[r].key_a = a;
+    red[r].key_c = cc;
+    if (ma.out || ma.loss_hist || ma.p_out) metrics_one(ma, r, status);
+  }
+  __syncthreads();
+}
+
+}  // namespace sq

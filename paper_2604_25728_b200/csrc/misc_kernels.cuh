@@ -5,28 +5,9 @@
 #pragma once
 #include <stdint.h>
 
-#include "af_kernels.cuh"
+#include "af_kernels.cuh"  // (+ common.cuh)
 
 namespace sq {
-
-enum : int { ST_INVALID = 1, ST_DEGENERATE = 2, ST_NONFINITE = 4 };
-
-__device__ __forceinline__ float ex2a_m(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rcp_m(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-struct Red {               // per restart, after combining all groups
-  double m;                // shift of S and of the gradient partials
-  double S;                // sum of phi at shift m
-  unsigned long long key_a, key_c;
-};
 
 // ------------------------------------------------------------------ a1 quantizer
 // fp64 table of the hard levels: lut[i*] = k with y_hard = k / B for i* = #{rho <= z}
@@ -136,84 +117,7 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
 }
 
 // ------------------------------------------------------------------ a6 metrics / loss
-__device__ __forceinline__ void decode_key(unsigned long long key, int M, int N, int K, int L, int32_t out[4],
-                                           double* vsq) {
-  if (key == 0ull) {
-    out[0] = out[1] = out[2] = out[3] = -1;
-    *vsq = 0.0;
-    return;
-  }
-  const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
-  out[3] = idx % K;
-  out[2] = (int)((idx / K) % L) - (N - 1);
-  out[1] = (idx / K / L) % M;
-  out[0] = idx / K / L / M;
-  *vsq = (double)__uint_as_float((uint32_t)(key >> 32));
-}
-
-struct MetricsOut {       // mirrors sqngd_metrics (include/sqngd.h)
-  double loss, loss_wpsl, loss_snrl, wapsl, wcpsl, wpsl;
-  int32_t argmax_auto[4], argmax_cross[4];
-  uint32_t flags, n_cells;
-};
-
-struct MetricsArgs {
-  int M, N, K, L, mode;
-  double bp, eps, ptar;
-  uint32_t n_cells, flags;
-  const Red* red;
-  const double2* cm;
-  MetricsOut* out;
-  double* p_out;
-  double* loss_hist;
-  int hist_stride, hist_col;
-};
-
-// Eqs. 7-10, 37-42 for restart r from the combined partials.
-__device__ void metrics_one(const MetricsArgs& a, int r, int* status) {
-  MetricsOut o;
-  double va, vc;
-  decode_key(a.red[r].key_a, a.M, a.N, a.K, a.L, o.argmax_auto, &va);
-  decode_key(a.red[r].key_c, a.M, a.N, a.K, a.L, o.argmax_cross, &vc);
-  o.wapsl = sqrt(va) / a.N;
-  o.wcpsl = sqrt(vc) / a.N;
-  o.wpsl = fmax(o.wapsl, o.wcpsl);
-  if (a.mode == 0) o.loss_wpsl = o.wpsl;
-  else if (a.red[r].m > -INFINITY && a.red[r].S > 0.0)
-    o.loss_wpsl = a.mode == 1 ? a.red[r].m + log(a.red[r].S) / a.bp : a.red[r].m * pow(a.red[r].S, 1.0 / a.bp);
-  else o.loss_wpsl = 0.0;
-  double lsn = 0.0;
-  for (int m = 0; m < a.M; ++m) {
-    const double2 c = a.cm[(size_t)r * a.M + m];
-    const double p = sqrt(c.x * c.x + c.y * c.y) / a.N;
-    if (a.p_out) a.p_out[(size_t)r * a.M + m] = p;
-    if (p == 0.0) atomicOr(status, ST_DEGENERATE);
-    lsn += (p - a.ptar) * (p - a.ptar);
-  }
-  o.loss_snrl = lsn / a.M;
-  o.loss = a.eps * o.loss_wpsl + (1.0 - a.eps) * o.loss_snrl;
-  o.flags = a.flags;
-  o.n_cells = a.n_cells;
-  if (!isfinite(o.loss)) atomicOr(status, ST_NONFINITE);
-  if (a.out) a.out[r] = o;
-  if (a.loss_hist) a.loss_hist[(size_t)r * a.hist_stride + a.hist_col] = o.loss;
-}
-
 // ------------------------------------------------------------------ combines
-// Block-wide fixed-order reductions (warp shuffles, then the warps in index order).
-template <class T_, class Op>
-__device__ __forceinline__ T_ block_reduce(T_ x, Op op, T_* sh) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sh[w] = x;
-  __syncthreads();
-  x = sh[0];
-  for (int i = 1; i < nw; ++i) x = op(x, sh[i]);
-  return x;
-}
-
 // Per restart: max keys, global shift and the rescaled sum S over the restart's units
 // [r * GPR, (r+1) * GPR) intersected with [g_lo, g_hi); per-unit rescale factors for the
 // gradient combine.  One block of 1024 threads per restart, fixed order (deterministic).
@@ -221,42 +125,7 @@ __global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp
                                 MetricsArgs ma, int* status) {
   __shared__ double shd[32];
   __shared__ unsigned long long shk[32];
-  const int r = blockIdx.x;
-  const int lo = max(g_lo, r * GPR), hi = min(g_hi, (r + 1) * GPR);
-  double mloc = -INFINITY;
-  unsigned long long a = 0, cc = 0;
-  for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
-    if (part.S[g] > 0.f) mloc = fmax(mloc, (double)part.m[g]);
-    a = max(a, part.key[2 * g]);
-    cc = max(cc, part.key[2 * g + 1]);
-  }
-  auto dmax = [](double x, double y) { return fmax(x, y); };
-  auto umax = [](unsigned long long x, unsigned long long y) { return x > y ? x : y; };
-  const double m = block_reduce(mloc, dmax, shd);
-  a = block_reduce(a, umax, shk);
-  cc = block_reduce(cc, umax, shk);
-  double S = 0.0;
-  const float mf = (float)m;
-  const float lb = (float)(bp * 1.4426950408889634);
-  for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
-    float sc = 0.f;
-    const float Sg = part.S[g];
-    if (mode != 0 && Sg > 0.f && m > -INFINITY) {
-      const float mg = part.m[g];
-      sc = mode == 1 ? exp2f(lb * (mg - mf)) : exp2f((float)(bp - 1.0) * log2f(mg / mf));
-      S += (double)Sg * (mode == 1 ? sc : sc * (mg / mf));
-    }
-    if (part.scale) part.scale[g] = sc;
-  }
-  auto dsum = [](double x, double y) { return x + y; };
-  S = block_reduce(S, dsum, shd);
-  if (threadIdx.x == 0) {
-    red[r].m = m;
-    red[r].S = S;
-    red[r].key_a = a;
-    red[r].key_c = cc;
-    if (ma.out || ma.loss_hist || ma.p_out) metrics_one(ma, r, status);
-  }
+  reduce_restart(blockIdx.x, GPR, g_lo, g_hi, mode, bp, part, red, ma, status, shd, shk);
 }
 
 // Multi-GPU: the shift m arrived from the all-reduce; refresh the per-group scales.
@@ -502,6 +371,100 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   }
 }
 
+// Step A tail for the optimizer step, one group per filter row (r, l):
+//   d = IFFT_P(spectral sum)[0..N), grad_w = 2 (d + conj(Gc_l) s_l) (finalize), Adam on
+//   (Re w, Im w), Pi_H (Eq. 32, fp64 energy), then the next inner step's H_l = FFT_P(w_l)/P and
+//   c_l = sum_n s_l conj(w_l).  A row whose gradient is non-finite is not updated (status latched).
+template <class PL, int G>
+__global__ void __launch_bounds__(PL::T* G)
+    k_rows_adam_w(int rows, const float2* __restrict__ in, const float2* __restrict__ ftw, FinArgs f, AdamP ap,
+                  float2* w, float* mw, float* vw, float2* Hh, double2* cm, int* status) {
+  constexpr int E = PL::E, T = PL::T, P = PL::P;
+  extern __shared__ float4 smem_raw[];
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  const int id = blockIdx.x * G + grp;
+  float2* gsm = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
+  Group<T> gops;
+  gops.sync = GroupSync{1 + grp, T, group_mask(T)};
+  gops.mask = gops.sync.mask;
+  gops.red = reinterpret_cast<float*>(gsm + FftSmem<PL>::XBUF);
+  gops.redk = reinterpret_cast<unsigned long long*>(gsm + FftSmem<PL>::XBUF + 32);
+  gops.par = 0;
+  gops.t = t;
+  const int row = id < rows ? id : rows - 1;
+  const int N = f.N;
+  const bool skip_all = (*status & ST_NONFINITE) != 0;  // uniform
+  float2 v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float2 x = __ldg(in + (size_t)row * P + t + i * T);
+    v[i] = make_float2(x.x, -x.y);
+  }
+  int par = 0;
+  fft<PL, -1>(v, ftw, gsm, t, par, gops.sync);
+  const double2 gc = snrl_coef(f, row);
+  float c1, c2;
+  ap.corr(c1, c2);
+  float bad = 0.f;
+  double e = 0.0;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    float2 wn = make_float2(0.f, 0.f);
+    if (n < N) {
+      const size_t j = (size_t)row * N + n;
+      const float2 sv = f.s[j];
+      const float re = 2.f * (v[i].x + ((float)gc.x * sv.x + (float)gc.y * sv.y));   // d = conj(v)
+      const float im = 2.f * (-v[i].y + ((float)gc.x * sv.y - (float)gc.y * sv.x));
+      if (!isfinite(re) || !isfinite(im)) bad = 1.f;
+      if (f.grad_w) f.grad_w[j] = make_float2(re, im);
+      const float g2[2] = {re, im};
+      float x2[2] = {w[j].x, w[j].y};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {  // Adam on the real parameters (Re w, Im w)
+        const size_t jj = 2 * j + q;
+        const float mi = ap.b1 * mw[jj] + (1.f - ap.b1) * g2[q];
+        const float vi = ap.b2 * vw[jj] + (1.f - ap.b2) * g2[q] * g2[q];
+        if (!skip_all) {
+          mw[jj] = mi;
+          vw[jj] = vi;
+        }
+        x2[q] -= ap.lr * (mi / c1) / (sqrtf(vi / c2) + ap.eps);
+      }
+      wn = make_float2(x2[0], x2[1]);
+      e += (double)wn.x * wn.x + (double)wn.y * wn.y;
+    }
+    v[i] = wn;
+  }
+  const float gbad = gops.max_f(bad);
+  const double en = gops.sum_d2(make_double2(e, 0.0)).x;
+  if (skip_all || gbad > 0.f || !(en > 0.0)) {
+    if (t == 0 && id < rows) atomicOr(status, gbad > 0.f ? ST_NONFINITE : (en > 0.0 ? 0 : ST_DEGENERATE));
+    return;  // uniform across the group
+  }
+  const float sc = (float)sqrt((double)N / en);
+  double2 cacc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    v[i] = make_float2(v[i].x * sc, v[i].y * sc);
+    if (n < N) {
+      const size_t j = (size_t)row * N + n;
+      if (id < rows) w[j] = v[i];
+      const float2 sv = f.s[j];  // c_l = sum_n s_l(n) conj(w_l(n)) for the next evaluation
+      cacc.x += (double)sv.x * v[i].x + (double)sv.y * v[i].y;
+      cacc.y += (double)sv.y * v[i].x - (double)sv.x * v[i].y;
+    }
+  }
+  cacc = gops.sum_d2(cacc);
+  fft<PL, -1>(v, ftw, gsm, t, par, gops.sync);  // next H_l = FFT_P(w_l) / P
+  if (id >= rows) return;
+  if (t == 0) cm[row] = cacc;
+  const float inv = 1.0f / (float)P;
+#pragma unroll
+  for (int i = 0; i < E; ++i) Hh[(size_t)row * P + t + i * T] = make_float2(v[i].x * inv, v[i].y * inv);
+}
+
 // dL/drho_i = -a c sum_e sech^2(c (z_e - rho_i)) dy_e, gathered per threshold over a chunk of
 // elements (partials [R][nchunk][BR], then a fixed-order sum).  sech^2 via MUFU, culled
 // (branch-free) outside |c (z - rho)| < 12 where it is < 1.6e-10.
@@ -541,19 +504,6 @@ __global__ void k_grad_rho_sum(int BR, int nchunk, float coef, const float* __re
 }
 
 // ------------------------------------------------------------------ a9 optimizer
-// Adam hyper-parameters; the step count t = dt[which] + off + 1 is read on the device so a
-// captured CUDA graph stays valid from one sqngd_step call to the next (bias corrections, Q15).
-struct AdamP {
-  float lr, b1, b2, eps;
-  const long long* dt;
-  int which, off;
-  __device__ __forceinline__ void corr(float& c1, float& c2) const {
-    const double t = (double)(dt[which] + off + 1);
-    c1 = (float)(1.0 - pow((double)b1, t));
-    c2 = (float)(1.0 - pow((double)b2, t));
-  }
-};
-
 __global__ void k_set_t(long long* dt, long long ta, long long tb) {
   dt[0] = ta;
   dt[1] = tb;
@@ -609,14 +559,39 @@ __global__ void k_adam_project_w(int N, float* w, float* mw, float* vw, const fl
 
 // Threshold projection: sort ascending, clamp to [lo, hi], forward min-gap sweep.
 // One block (1024 threads) per restart; BR <= 8192.
+// Step B update, one block per restart:
+//   grad_rho = coef * sum_chunks rho_part (when rho_part != nullptr, else g), Adam(rho), projection;
+//   Adam(z) on the restart's M N elements (when z != nullptr).
+struct ZAdam {
+  float* z;
+  float* m;
+  float* v;
+  const float* g;
+  int MN;
+  const float* rho_part;  // [R][nchunk][BR] gather partials of dL/drho (k_grad_rho_part)
+  int nchunk;
+  float coef;             // -a c
+};
+
 __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
-                                   float lo, float hi, float gap, const int* status) {
+                                   float lo, float hi, float gap, const int* status, ZAdam za) {
   extern __shared__ float sr[];
   __shared__ int flag;
   if (*status & ST_NONFINITE) return;
   float c1, c2;
   ap.corr(c1, c2);
   const float lr = ap.lr, b1 = ap.b1, b2 = ap.b2, eps = ap.eps;
+  if (za.z) {  // Adam on z (elementwise; the grad_rho gather already consumed the old z)
+    for (int i = threadIdx.x; i < za.MN; i += blockDim.x) {
+      const size_t j = (size_t)blockIdx.x * za.MN + i;
+      const float gi = za.g[j];
+      const float mi = b1 * za.m[j] + (1.f - b1) * gi;
+      const float vi = b2 * za.v[j] + (1.f - b2) * gi * gi;
+      za.m[j] = mi;
+      za.v[j] = vi;
+      za.z[j] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    }
+  }
   float* p = rho + (size_t)blockIdx.x * BR;
   int n2 = 1;
   while (n2 < BR) n2 <<= 1;
@@ -626,7 +601,14 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
     float x = INFINITY;
     if (i < BR) {
       const size_t j = (size_t)blockIdx.x * BR + i;
-      const float gi = g[j];
+      float gi;
+      if (za.rho_part) {
+        float acc = 0.f;
+        for (int ch = 0; ch < za.nchunk; ++ch) acc += za.rho_part[((size_t)blockIdx.x * za.nchunk + ch) * BR + i];
+        gi = za.coef * acc;
+      } else {
+        gi = g[j];
+      }
       const float mi = b1 * mr[j] + (1.f - b1) * gi;
       const float vi = b2 * vr[j] + (1.f - b2) * gi * gi;
       mr[j] = mi;

@@ -170,6 +170,8 @@ struct Launch {
     if (e) return e;
     e = cudaFuncSetAttribute(k_rows_ifft_fin<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
     if (e) return e;
+    e = cudaFuncSetAttribute(k_rows_adam_w<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+    if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MINB, MODE_FWD>, THREADS, smem<MODE_FWD>());
     if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[1], k_af<PL, G, MINB, MODE_ADJ_A>, THREADS, smem<MODE_ADJ_A>());
@@ -194,6 +196,11 @@ struct Launch {
   static void rows_ifft(int rows, int N, const float2* in, const float2* ftw, float2* out, cudaStream_t st) {
     const int blocks = (rows + G - 1) / G;
     k_rows_ifft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, N, in, ftw, out);
+  }
+  static void rows_adam_w(int rows, const float2* in, const float2* ftw, const FinArgs& f, const AdamP& ap,
+                          float2* w, float* mw, float* vw, float2* H, double2* cm, int* status, cudaStream_t st) {
+    const int blocks = (rows + G - 1) / G;
+    k_rows_adam_w<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, in, ftw, f, ap, w, mw, vw, H, cm, status);
   }
   static void rows_ifft_fin(int rows, const float2* in, const float2* ftw, const FinArgs& f, int* status,
                             cudaStream_t st) {
@@ -356,7 +363,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&ctx->part.scale, sizeof(float) * ctx->units));
-  CK(cudaMalloc(&ctx->counter, sizeof(int)));
+  CK(cudaMalloc(&ctx->counter, 2 * sizeof(int)));
   CK(cudaMalloc(&ctx->d_t, 2 * sizeof(long long)));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
   CK(cudaMalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
@@ -539,6 +546,9 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
     if (rx) return rx;
   }
   KP kp = make_kp(ctx, c.loss_mode != 0);
+  const double ptar = std::pow(10.0, -c.mu_db / 20.0);
+  MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
+                 ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
   cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
   {
     ProfScope ps(ctx, MODE_FWD, st);
@@ -549,9 +559,6 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
   ctx->launches += 4;
   sqngd_status rc = launch_check(ctx, "af forward");
   if (rc) return rc;
-  const double ptar = std::pow(10.0, -c.mu_db / 20.0);
-  MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
-                 ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
   if (ctx->world == 1) {
     k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
                                           ctx->red, ma, ctx->status);
@@ -568,9 +575,18 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
 
 // Loss + gradient of an explicit waveform s.  Assumes H = FFT(w) is current.
 // wrt 1: writes grad_w (2 dL/dw^*); wrt 2: grad_s (dL/ds^*), dy and grad_z if dq/grad_z given.
+// Step-A optimizer tail fused into the gradient's last kernel (sqngd_step, single GPU).
+struct StepATail {
+  AdamP ap;
+  float2* w;
+  float* mw;
+  float* vw;
+};
+
 static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* w, int wrt, MetricsOut* met,
                                   float2* grad_w, float2* grad_s, const float* dq, float* grad_z, double* hist,
-                                  int hist_col, cudaStream_t st, bool xhat_ready = false) {
+                                  int hist_col, cudaStream_t st, bool xhat_ready = false,
+                                  const StepATail* tail = nullptr) {
   const sqngd_config& c = ctx->cfg;
   sqngd_status rc;
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
@@ -619,7 +635,14 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     } else {
       ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
       k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
-      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftw, fa, ctx->status, st); });
+      if (tail) {  // + Adam(w), Pi_H, next H = FFT(w)/P and c_m, in the same row kernel
+        with_P(ctx->P, [&](auto Lc) {
+          decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftw, fa, tail->ap, tail->w, tail->mw, tail->vw,
+                                    ctx->H, ctx->cm, ctx->status, st);
+        });
+      } else {
+        with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftw, fa, ctx->status, st); });
+      }
       ctx->launches += 2;
     }
     return launch_check(ctx, "combine");
@@ -737,7 +760,6 @@ sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho,
 static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, double* loss_hist,
                               sqngd_metrics* hard_out, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
-  const size_t RMN = (size_t)c.R * c.M * c.N;
   float2* w2 = reinterpret_cast<float2*>(stt->w);
   sqngd_status rc;
   auto ap = [&](double lr, int which, int off) {
@@ -746,15 +768,23 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
     if ((rc = run_xhat(ctx, ctx->s_hard, st))) return rc;  // X_hard fixed for the whole block
+    const bool fused = ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
     for (int i = 0; i < c.n_h; ++i) {
-      if ((rc = run_filter_fft(ctx, w2, st, ctx->s_hard))) return rc;
-      if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, ctx->gw, nullptr, nullptr, nullptr,
-                              loss_hist, i, st, true)))
-        return rc;
-      k_adam_project_w<<<c.R * c.M, 1024, 0, st>>>(c.N, stt->w, stt->m_w, stt->v_w,
-                                                   reinterpret_cast<const float*>(ctx->gw), ap(c.lr_w, 0, i),
-                                                   ctx->status);
-      ctx->launches += 1;
+      if ((!fused || i == 0) && (rc = run_filter_fft(ctx, w2, st, ctx->s_hard))) return rc;
+      if (fused) {  // the row kernel also updates w and prepares H, c_m for the next inner step
+        const StepATail tail{ap(c.lr_w, 0, i), w2, stt->m_w, stt->v_w};
+        if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, nullptr, nullptr, nullptr, nullptr,
+                                loss_hist, i, st, true, &tail)))
+          return rc;
+      } else {
+        if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, ctx->gw, nullptr, nullptr,
+                                nullptr, loss_hist, i, st, true)))
+          return rc;
+        k_adam_project_w<<<c.R * c.M, 1024, 0, st>>>(c.N, stt->w, stt->m_w, stt->v_w,
+                                                     reinterpret_cast<const float*>(ctx->gw), ap(c.lr_w, 0, i),
+                                                     ctx->status);
+        ctx->launches += 1;
+      }
       if ((rc = launch_check(ctx, "step A update"))) return rc;
     }
   }
@@ -768,13 +798,17 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
       if ((rc = run_loss_grad(ctx, ctx->s_soft, w2, SQNGD_WRT_TRANSMIT, ctx->met, nullptr, nullptr, ctx->dq, ctx->gz,
                               loss_hist, col0 + i, st)))
         return rc;
-      if ((rc = run_grad_rho(ctx, stt->z, stt->rho, ctx->grho, st))) return rc;
-      k_adam<<<(unsigned)((RMN + 255) / 256), 256, 0, st>>>(RMN, stt->z, stt->m_z, stt->v_z, ctx->gz, ap(c.lr_z, 1, i),
-                                                            ctx->status);
-      k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
-                                                                    ctx->grho, ap(c.lr_z, 1, i), 1e-4f, 1.0f - 1e-4f,
-                                                                    1e-6f, ctx->status);
-      ctx->launches += 2;
+      {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
+        dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);
+        k_grad_rho_part<<<g1, 256, 0, st>>>(c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy,
+                                            ctx->rho_part);
+        const ZAdam za{stt->z, stt->m_z, stt->v_z, ctx->gz, c.M * c.N, ctx->rho_part, ctx->rho_nchunk,
+                       (float)(-(1.0 / (2.0 * c.B)) * c.c)};
+        k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
+                                                                      nullptr, ap(c.lr_z, 1, i), 1e-4f, 1.0f - 1e-4f,
+                                                                      1e-6f, ctx->status, za);
+        ctx->launches += 2;
+      }
       if ((rc = launch_check(ctx, "step B update"))) return rc;
     }
   }
