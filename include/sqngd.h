@@ -78,7 +78,22 @@ typedef struct {
   int32_t n_h, n_x;                /* inner steps per block (Alg. 1)      */
   const float* weights;            /* device [K][2N-1] w(tau,f) >= 0 (Eqs. 8-9), NULL => 1;
                                       must stay valid for the context's lifetime          */
+  int32_t doppler_engine;          /* SQNGD_ENGINE_*: how the K Doppler bins are evaluated */
+  double lr_tol;                   /* CHEBYSHEV: bound on |A_interp - A| / (||s|| ||w||)
+                                      (0 => 1e-7); picks the node count Q at create       */
 } sqngd_config;
+
+/* Doppler engine (sqngd_config.doppler_engine).
+   FFT:       one modulated FFT correlation per Doppler bin (Eqs. 33-36):
+              O(M^2 K) transforms, exact up to fp32 rounding.
+   CHEBYSHEV: SURVEY.md §8(f) NEXT-1 -- exact FFT correlations (Eq. 36) at Q Chebyshev
+              Doppler nodes of [f_lo, f_hi], then the K-bin AF by the dense (K x Q)
+              Lagrange contraction fused with the cell epilogue, and its adjoint;
+              O(M^2 Q) transforms.  |A| is reproduced to lr_tol * ||s|| ||w|| (DESIGN.md
+              §3 "Chebyshev engine").  Single GPU only (world == 1).
+   AUTO:      CHEBYSHEV when world == 1 and the node count Q for lr_tol is <= 16 and
+              <= K/3 (narrow grids such as the paper's [-0.5, 0.5]); FFT otherwise. */
+enum { SQNGD_ENGINE_AUTO = 0, SQNGD_ENGINE_FFT = 1, SQNGD_ENGINE_CHEBYSHEV = 2 };
 
 /* One per restart, written by the library into caller-owned DEVICE memory. */
 typedef struct {
@@ -113,6 +128,9 @@ sqngd_status sqngd_create(const sqngd_config* cfg, int cuda_device, const void* 
 void sqngd_destroy(sqngd_ctx ctx);
 /* Message for the last non-OK status (ctx may be NULL: last create error). */
 const char* sqngd_last_error(sqngd_ctx ctx);
+/* The Doppler engine the context selected (SQNGD_ENGINE_FFT or _CHEBYSHEV), its node count Q
+   (0 for FFT) and the host-computed interpolation error bound (relative to ||s|| ||w||). */
+sqngd_status sqngd_engine_info(sqngd_ctx ctx, int32_t* engine, int32_t* q_nodes, double* err_bound);
 /* Synchronize `stream` and return (and clear) the latched device-side status. */
 sqngd_status sqngd_sync(sqngd_ctx ctx, sqngd_stream stream);
 

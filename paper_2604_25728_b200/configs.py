@@ -41,6 +41,8 @@ class Cfg:
     adam_eps: float = 1e-8
     n_h: int = 10
     n_x: int = 10
+    doppler_engine: int = 0         # 0 auto, 1 per-bin FFT, 2 Chebyshev nodes (include/sqngd.h)
+    lr_tol: float = 0.0             # Chebyshev engine error bound (0 => library default 1e-7)
     iterations: int = 1
     index: int = 0                  # config number used for input seeds
 

@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
 #pragma unroll 4
     for (int k = klo + kl; k < khi; k += 8) {
       const int u = ra * a.K + k;
-      const float sc = __ldg(a.part.scale + u);
+      const float sc = a.part.scale ? __ldg(a.part.scale + u) : 1.f;  // null: slots pre-scaled (Chebyshev engine)
       const float4 v = __ldg(reinterpret_cast<const float4*>(a.part.g + (size_t)u * a.slot_stride + q));
       acc.x = fmaf(sc, v.x, acc.x);
       acc.y = fmaf(sc, v.y, acc.y);

@@ -14,6 +14,7 @@
 
 #include "../../include/sqngd.h"
 #include "comm.h"
+#include "lr_kernels.cuh"
 #include "misc_kernels.cuh"
 
 using namespace sq;
@@ -75,6 +76,18 @@ struct sqngd_ctx_s {
   float* grho = nullptr;       // [R][BR]
   MetricsOut* met = nullptr;   // [R] scratch
   int* status = nullptr;       // latched device status bits
+  // Chebyshev Doppler engine (lr_kernels.cuh): Q nodes, tables, node AFs / cotangents
+  bool lr = false;
+  int Q = 0, QS = 0, nch = 0, kparts = 1, LS = 0;
+  int64_t units_lr = 0;        // k_lr units: R M^2 nch kparts
+  double lr_err = 0.0;         // interpolation error bound of the chosen Q (host estimate)
+  float2* Vt = nullptr;        // [Q][N] e^{j 2 pi (n - n_c) f*_q / N}
+  float* coef = nullptr;       // [K/2 + 1][QS] alpha / beta rows
+  float* wmax = nullptr;       // [L] max_k weights (weighted ROI)
+  float2* Rn = nullptr;        // [R M M][Q][LS] node AFs
+  float2* Gn = nullptr;        // [kparts][R M M][Q][LS] node cotangents
+  float2* tslot = nullptr;     // [R M Q][N] Step-B node time-domain partials
+  int lr_bps = 1;              // k_lr CTAs per SM
   Comm comm;
   long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
   // CUDA graphs of sqngd_step (one per (state buffers, block, outputs, profiling))
@@ -220,7 +233,69 @@ struct Launch {
       k_af<PL, G, MINB, MODE_ADJ_B><<<blocks, THREADS, smem<MODE_ADJ_B>(), st>>>(kp, Xc, H, tw, ftw, nullptr, part);
   }
   static int groups_per_block() { return G; }
+  // Chebyshev engine: node AFs, node adjoint correlations, Step-B node tail
+  static void node(int units, int M, int Q, int N, int LS, const float2* Xc, const float2* H, const float2* ftw,
+                   float2* Rn, cudaStream_t st) {
+    k_node<PL, G, MINB><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, LS, Xc, H, ftw, Rn);
+  }
+  static void adj_g(int wrt, const AdjGArgs& a, const float2* ftw, cudaStream_t st) {
+    const int blocks = (a.units + G - 1) / G;
+    if (wrt == 2) k_adj_g<PL, G, MINB, 2><<<blocks, THREADS, smem_fft(), st>>>(a, ftw);
+    else k_adj_g<PL, G, MINB, 1><<<blocks, THREADS, smem_fft(), st>>>(a, ftw);
+  }
+  static void lrB_tail(int units, int M, int Q, int N, int NS, const float2* slots, const float2* Vt,
+                       const float2* ftw, float2* out, cudaStream_t st) {
+    k_lrB_tail<PL, G><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, NS, slots, Vt, ftw, out);
+  }
+  static cudaError_t prepare_lr() {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_node<PL, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft())))
+      return e;
+    if ((e = cudaFuncSetAttribute(k_adj_g<PL, G, MINB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft())))
+      return e;
+    if ((e = cudaFuncSetAttribute(k_adj_g<PL, G, MINB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft())))
+      return e;
+    return cudaFuncSetAttribute(k_lrB_tail<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+  }
 };
+
+// k_lr instantiations: Q in {4, 6, ..., 16} x loss mode x weighted ROI x gradient.
+template <int Q>
+struct LrLaunch {
+  template <int LM, bool HW, bool GRAD>
+  static void go(const LrArgs& a, int units, size_t smem, cudaStream_t st) {
+    k_lr<Q, LM, HW, GRAD><<<(units + 3) / 4, 128, smem, st>>>(a, units);
+  }
+  static void launch(int lm, bool hw, bool grad, const LrArgs& a, int units, size_t smem, cudaStream_t st) {
+    if (lm == 0) { hw ? go<0, true, false>(a, units, smem, st) : go<0, false, false>(a, units, smem, st); return; }
+    if (lm == 1) {
+      if (grad) hw ? go<1, true, true>(a, units, smem, st) : go<1, false, true>(a, units, smem, st);
+      else hw ? go<1, true, false>(a, units, smem, st) : go<1, false, false>(a, units, smem, st);
+      return;
+    }
+    if (grad) hw ? go<2, true, true>(a, units, smem, st) : go<2, false, true>(a, units, smem, st);
+    else hw ? go<2, true, false>(a, units, smem, st) : go<2, false, false>(a, units, smem, st);
+  }
+  static cudaError_t occupancy(int* bps, size_t smem) {  // the heaviest variant (LSE + gradient)
+    cudaError_t e = cudaFuncSetAttribute(k_lr<Q, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lr<Q, 1, false, true>, 128, smem);
+  }
+};
+
+template <class Fn>
+static bool with_Q(int Q, Fn&& fn) {
+  switch (Q) {
+    case 4: fn(LrLaunch<4>{}); return true;
+    case 6: fn(LrLaunch<6>{}); return true;
+    case 8: fn(LrLaunch<8>{}); return true;
+    case 10: fn(LrLaunch<10>{}); return true;
+    case 12: fn(LrLaunch<12>{}); return true;
+    case 14: fn(LrLaunch<14>{}); return true;
+    case 16: fn(LrLaunch<16>{}); return true;
+    default: return false;
+  }
+}
 
 template <class Fn>
 static bool with_P(int P, Fn&& fn) {
@@ -254,6 +329,60 @@ static KP make_kp(const sqngd_ctx_s* c, int want_S) {
   kp.want_S = want_S;
   kp.counter = c->counter;
   return kp;
+}
+
+// ----------------------------------------------------------------------------- Chebyshev engine tables
+// Doppler bin k of the inclusive uniform grid (Q8).
+static double grid_f(const sqngd_config& c, int k) {
+  return c.K == 1 ? c.f_lo : c.f_lo + (c.f_hi - c.f_lo) * (double)k / (double)(c.K - 1);
+}
+
+// Q Chebyshev nodes (first kind) of [f_lo, f_hi] and the Lagrange basis l_q(f_k) (barycentric form,
+// weights (-1)^q sin((2q+1) pi / 2Q)), in fp64.  Returns the interpolation error bound
+//   max_{k, t} | e^{j 2 pi t f_k} - sum_q l_q(f_k) e^{j 2 pi t f*_q} |,  t = (n - n_c)/N,
+// evaluated on 513 t-samples of [-(N-1)/2N, (N-1)/2N] (the error is smooth in t); by
+// Cauchy-Schwarz |At_interp - At| <= err * ||s|| ||w|| for every cell.
+static double lr_tables(const sqngd_config& c, int Q, std::vector<double>& fq, std::vector<double>& ell) {
+  const double ctr = 0.5 * (c.f_lo + c.f_hi), hw = 0.5 * (c.f_hi - c.f_lo);
+  fq.assign(Q, 0.0);
+  std::vector<double> bw(Q);
+  for (int q = 0; q < Q; ++q) {
+    const double th = (2.0 * q + 1.0) * M_PI / (2.0 * Q);
+    fq[q] = ctr + hw * std::cos(th);
+    bw[q] = ((q & 1) ? -1.0 : 1.0) * std::sin(th);
+  }
+  ell.assign((size_t)c.K * Q, 0.0);
+  for (int k = 0; k < c.K; ++k) {
+    const double f = grid_f(c, k);
+    int hit = -1;
+    for (int q = 0; q < Q; ++q)
+      if (std::fabs(f - fq[q]) <= 1e-15 * std::max(1.0, std::fabs(hw))) hit = q;
+    double* lr = &ell[(size_t)k * Q];
+    if (hit >= 0) {
+      lr[hit] = 1.0;
+      continue;
+    }
+    double den = 0.0;
+    for (int q = 0; q < Q; ++q) den += bw[q] / (f - fq[q]);
+    for (int q = 0; q < Q; ++q) lr[q] = bw[q] / (f - fq[q]) / den;
+  }
+  double err = 0.0;
+  const int NT = 513;
+  const double tmax = (c.N - 1) / (2.0 * c.N);
+  for (int k = 0; k < c.K; ++k) {
+    const double f = grid_f(c, k);
+    for (int i = 0; i < NT; ++i) {
+      const double t = -tmax + 2.0 * tmax * i / (NT - 1);
+      double re = std::cos(2.0 * M_PI * t * f), im = std::sin(2.0 * M_PI * t * f);
+      for (int q = 0; q < Q; ++q) {
+        const double a = 2.0 * M_PI * t * fq[q], lq = ell[(size_t)k * Q + q];
+        re -= lq * std::cos(a);
+        im -= lq * std::sin(a);
+      }
+      err = std::max(err, std::hypot(re, im));
+    }
+  }
+  return err;
 }
 
 // ----------------------------------------------------------------------------- C-ABI
@@ -356,13 +485,68 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   for (int md = 0; md < 3; ++md) ctx->slots[md] = (int64_t)ctx->sms * std::max(1, bps[md]) * G;
   ctx->units = (int64_t)cfg.R * cfg.M * cfg.K;
 
+  // Doppler engine (include/sqngd.h SQNGD_ENGINE_*): node count Q for lr_tol, tables, unit split.
+  std::vector<double> lr_fq, lr_ell;
+  if (cfg.doppler_engine < 0 || cfg.doppler_engine > 2) {
+    delete ctx;
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: doppler_engine");
+  }
+  if (cfg.doppler_engine != SQNGD_ENGINE_FFT && world == 1 && cfg.K >= 3) {
+    const double tol = cfg.lr_tol > 0 ? cfg.lr_tol : 1e-7;
+    for (int Q = 4; Q <= 16; Q += 2) {
+      const double err = lr_tables(cfg, Q, lr_fq, lr_ell);
+      if (err <= tol) {
+        ctx->Q = Q;
+        ctx->lr_err = err;
+        break;
+      }
+    }
+    ctx->lr = ctx->Q > 0 && (cfg.doppler_engine == SQNGD_ENGINE_CHEBYSHEV || 3 * ctx->Q <= cfg.K);
+  }
+  if (cfg.doppler_engine == SQNGD_ENGINE_CHEBYSHEV && !ctx->lr) {
+    delete ctx;
+    return fail(nullptr, SQNGD_E_INVALID,
+                "sqngd_create: CHEBYSHEV engine needs world == 1, K >= 3 and <= 16 nodes for lr_tol");
+  }
+  if (ctx->lr) {
+    ctx->QS = (ctx->Q + 3) & ~3;
+    ctx->nch = (L + 31) / 32;
+    ctx->LS = ctx->nch * 32;
+    const size_t lr_smem = sizeof(float) * (size_t)(cfg.K / 2 + 1) * ctx->QS;
+    cudaError_t e1 = cudaSuccess;
+    with_Q(ctx->Q, [&](auto Qc) { e1 = decltype(Qc)::occupancy(&ctx->lr_bps, lr_smem); });
+    cudaError_t e2 = cudaSuccess;
+    with_P(P, [&](auto Lc) { e2 = decltype(Lc)::prepare_lr(); });
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      std::string m = cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
+      delete ctx;
+      return fail(nullptr, SQNGD_E_CUDA, "sqngd_create: Chebyshev kernel setup", m.c_str());
+    }
+    // k-split: the fewest parts whose warp units fill whole waves of resident warps best.
+    const int64_t u1 = (int64_t)cfg.R * cfg.M * cfg.M * ctx->nch;
+    const double resident = (double)ctx->sms * std::max(1, ctx->lr_bps) * 4.0;
+    const int kmax = std::max(1, std::min(32, cfg.K / 2));
+    double best = 1e30;
+    for (int kp = 1; kp <= kmax; ++kp) {
+      const double waves = (double)u1 * kp / resident;
+      const double cost = std::ceil(waves) / waves + 0.02 * (kp - 1);
+      if (cost < best - 1e-9) {
+        best = cost;
+        ctx->kparts = kp;
+      }
+    }
+    ctx->units_lr = u1 * ctx->kparts;
+  }
+
   const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
   CK(cudaMalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
   CK(cudaMalloc(&ctx->H, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * cfg.K * P));
   CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->part.scale, sizeof(float) * ctx->units));
+  const int64_t uslots = std::max(ctx->units, ctx->units_lr);
+  const int64_t gslots = std::max(ctx->units, ctx->lr ? (int64_t)cfg.R * cfg.M * cfg.M * ctx->Q : (int64_t)0);
+  CK(cudaMalloc(&ctx->part.scale, sizeof(float) * uslots));
   CK(cudaMalloc(&ctx->counter, 2 * sizeof(int)));
   CK(cudaMalloc(&ctx->d_t, 2 * sizeof(long long)));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
@@ -371,10 +555,10 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->dq, sizeof(float) * RMN));
   CK(cudaMalloc(&ctx->lut, sizeof(int) * (size_t)cfg.R * (ctx->BR + 1)));
-  CK(cudaMalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * ctx->units));
-  CK(cudaMalloc(&ctx->part.m, sizeof(float) * ctx->units));
-  CK(cudaMalloc(&ctx->part.S, sizeof(float) * ctx->units));
-  CK(cudaMalloc(&ctx->part.g, sizeof(float2) * (size_t)ctx->units * P));
+  CK(cudaMalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * uslots));
+  CK(cudaMalloc(&ctx->part.m, sizeof(float) * uslots));
+  CK(cudaMalloc(&ctx->part.S, sizeof(float) * uslots));
+  CK(cudaMalloc(&ctx->part.g, sizeof(float2) * (size_t)gslots * P));
   CK(cudaMalloc(&ctx->red, sizeof(Red) * cfg.R));
   CK(cudaMalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
   CK(cudaMalloc(&ctx->red_grad, sizeof(float2) * RMN));
@@ -400,6 +584,47 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
       }
     }
     CK(cudaMemcpy(ctx->tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
+
+  if (ctx->lr) {  // Chebyshev engine tables (fp64-built) and node buffers
+    const int Q = ctx->Q, QH = Q / 2, Kp = cfg.K / 2;
+    const double nc = 0.5 * (cfg.N + 1);
+    std::vector<float2> vt((size_t)Q * cfg.N);
+    for (int q = 0; q < Q; ++q)
+      for (int n = 0; n < cfg.N; ++n) {  // V_q(n) = e^{j 2 pi (n - n_c) f*_q / N}, n one-based (Q2)
+        double cyc = ((double)(n + 1) - nc) * lr_fq[q] / (double)cfg.N;
+        cyc -= std::floor(cyc);
+        vt[(size_t)q * cfg.N + n] = make_float2((float)std::cos(2.0 * M_PI * cyc), (float)std::sin(2.0 * M_PI * cyc));
+      }
+    std::vector<float> cf((size_t)(Kp + 1) * ctx->QS, 0.f);
+    for (int p = 0; p < Kp; ++p)
+      for (int j = 0; j < QH; ++j) {
+        const double a = lr_ell[(size_t)p * Q + j], b = lr_ell[(size_t)p * Q + Q - 1 - j];
+        cf[(size_t)p * ctx->QS + j] = (float)(0.5 * (a + b));       // alpha_j
+        cf[(size_t)p * ctx->QS + QH + j] = (float)(0.5 * (a - b));  // beta_j
+      }
+    if (cfg.K & 1)
+      for (int j = 0; j < QH; ++j) cf[(size_t)Kp * ctx->QS + j] = (float)lr_ell[(size_t)Kp * Q + j];
+    CK(cudaMalloc(&ctx->Vt, sizeof(float2) * vt.size()));
+    CK(cudaMemcpy(ctx->Vt, vt.data(), sizeof(float2) * vt.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&ctx->coef, sizeof(float) * cf.size()));
+    CK(cudaMemcpy(ctx->coef, cf.data(), sizeof(float) * cf.size(), cudaMemcpyHostToDevice));
+    std::vector<float> wm((size_t)L, 1.f);
+    if (cfg.weights) {
+      std::vector<float> wts((size_t)cfg.K * L);
+      CK(cudaMemcpy(wts.data(), cfg.weights, wts.size() * sizeof(float), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < L; ++i) {
+        float mx = 0.f;
+        for (int k = 0; k < cfg.K; ++k) mx = std::max(mx, wts[(size_t)k * L + i]);
+        wm[i] = mx;
+      }
+    }
+    CK(cudaMalloc(&ctx->wmax, sizeof(float) * L));
+    CK(cudaMemcpy(ctx->wmax, wm.data(), sizeof(float) * L, cudaMemcpyHostToDevice));
+    const size_t pairs = (size_t)cfg.R * cfg.M * cfg.M;
+    CK(cudaMalloc(&ctx->Rn, sizeof(float2) * pairs * Q * ctx->LS));
+    CK(cudaMalloc(&ctx->Gn, sizeof(float2) * (size_t)ctx->kparts * pairs * Q * ctx->LS));
+    CK(cudaMalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ((cfg.N + 1) & ~1)));
   }
 
   if (world > 1) {
@@ -430,12 +655,21 @@ void sqngd_destroy(sqngd_ctx ctx) {
   }
   void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
-                  ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status};
+                  ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
+                  ctx->Gn, ctx->tslot};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   ctx->comm.destroy();
   delete ctx;
+}
+
+sqngd_status sqngd_engine_info(sqngd_ctx ctx, int32_t* engine, int32_t* q_nodes, double* err_bound) {
+  if (!ctx) return fail(nullptr, SQNGD_E_INVALID, "sqngd_engine_info: null ctx");
+  if (engine) *engine = ctx->lr ? SQNGD_ENGINE_CHEBYSHEV : SQNGD_ENGINE_FFT;
+  if (q_nodes) *q_nodes = ctx->lr ? ctx->Q : 0;
+  if (err_bound) *err_bound = ctx->lr ? ctx->lr_err : 0.0;
+  return SQNGD_OK;
 }
 
 sqngd_status sqngd_profile_enable(sqngd_ctx ctx, int on) {
@@ -523,12 +757,14 @@ static sqngd_status run_filter_fft(sqngd_ctx ctx, const float2* w, cudaStream_t 
   return launch_check(ctx, "filter fft");
 }
 
-// a3 (+ a6 when w is given): X cache of the waveform s over all units.
+// a3 (+ a6 when w is given): X cache of the waveform s over all units (Chebyshev engine: the
+// Q node modulations V_q instead of the K bins).
 static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st, const float2* w = nullptr) {
   const sqngd_config& c = ctx->cfg;
-  const int units = c.R * c.M * c.K;
+  const int nk = ctx->lr ? ctx->Q : c.K;
+  const int units = c.R * c.M * nk;
   with_P(ctx->P, [&](auto Lc) {
-    decltype(Lc)::xhat(units, c.M, c.N, c.K, s, ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
+    decltype(Lc)::xhat(units, c.M, c.N, nk, s, ctx->lr ? ctx->Vt : ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
   });
   ctx->launches += 1;
   return launch_check(ctx, "xhat");
@@ -536,6 +772,36 @@ static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st, co
 
 // Multi-GPU: max-then-sum protocol over the per-restart partials.
 static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad, int mode);
+
+// Chebyshev engine, forward part: node AFs (k_node) and the fused contraction / epilogue (k_lr),
+// then the per-restart reduction (keys, shift, S, unit scales, metrics).
+static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, const MetricsArgs& ma, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  const int node_units = c.R * c.M * c.M * ctx->Q;
+  with_P(ctx->P, [&](auto Lc) {
+    decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftw, ctx->Rn, st);
+  });
+  LrArgs a{};
+  a.R = c.R; a.M = c.M; a.N = c.N; a.L = ctx->L; a.K = c.K; a.nch = ctx->nch; a.kparts = ctx->kparts;
+  a.LS = ctx->LS; a.QS = ctx->QS;
+  a.tau_lo = c.tau_lo; a.tau_hi = c.tau_hi; a.excl0 = c.exclude_auto_zero_delay;
+  a.bp = (float)c.beta_or_p; a.invN = 1.0f / (float)c.N;
+  a.weights = c.weights; a.wmax = ctx->wmax; a.coef = ctx->coef; a.Rn = ctx->Rn; a.Gn = ctx->Gn;
+  a.af_mag = grad ? nullptr : af_mag; a.part = ctx->part;
+  const size_t smem = sizeof(float) * (size_t)(c.K / 2 + 1) * ctx->QS;
+  const int units = (int)ctx->units_lr;
+  {
+    ProfScope ps(ctx, cls, st);
+    with_Q(ctx->Q, [&](auto Qc) {
+      decltype(Qc)::launch(c.loss_mode, c.weights != nullptr, grad, a, units, smem, st);
+    });
+  }
+  const int GPR = (int)(ctx->units_lr / c.R);
+  k_reduce_groups<<<c.R, 1024, 0, st>>>(GPR, 0, (int)ctx->units_lr, c.loss_mode, c.beta_or_p, ctx->part, ctx->red,
+                                        ma, ctx->status);
+  ctx->launches += 3;
+  return launch_check(ctx, "chebyshev forward");
+}
 
 // Forward AF + metrics of (s, w).  Assumes H = FFT(w) is current.
 static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w, float* af_mag, MetricsOut* met,
@@ -549,6 +815,7 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
                  ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
+  if (ctx->lr) return run_lr(ctx, false, MODE_FWD, af_mag, ma, st);
   cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
   {
     ProfScope ps(ctx, MODE_FWD, st);
@@ -605,6 +872,44 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fa, ctx->red_grad, ctx->status, none);
     ctx->launches += 2;
     return launch_check(ctx, "sparse adjoint");
+  }
+  if (ctx->lr) {  // Chebyshev engine (single GPU)
+    if ((rc = run_lr(ctx, true, wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B, nullptr, ma, st))) return rc;
+    AdjGArgs ag{};
+    ag.M = c.M; ag.N = c.N; ag.Q = ctx->Q; ag.LS = ctx->LS; ag.nch = ctx->nch; ag.kparts = ctx->kparts;
+    ag.units = c.R * c.M * c.M * ctx->Q;
+    ag.gstride = (size_t)c.R * c.M * c.M * ctx->Q * ctx->LS;
+    ag.Gn = ctx->Gn; ag.scale = ctx->part.scale; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
+    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::adj_g(wrt, ag, ctx->ftw, st); });
+    CombineArgs ca{};
+    ca.M = c.M; ca.N = c.N; ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.red = ctx->red;
+    ca.f = fa;
+    ca.part = ctx->part;
+    ca.part.scale = nullptr;  // node cotangents were rescaled in k_adj_g
+    if (wrt == SQNGD_WRT_TRANSMIT) {
+      const int tu = c.R * c.M * ctx->Q;
+      with_P(ctx->P, [&](auto Lc) {
+        decltype(Lc)::lrB_tail(tu, c.M, ctx->Q, c.N, (c.N + 1) & ~1, ctx->part.g, ctx->Vt, ctx->ftw, ctx->tslot, st);
+      });
+      ca.K = ctx->Q; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = 0; ca.u_hi = tu; ca.part.g = ctx->tslot;
+      ca.len = c.N; ca.extra = 1.0; ca.fin = 1; ca.out = nullptr;
+      k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      ctx->launches += 3;
+      return launch_check(ctx, "chebyshev adjoint (transmit)");
+    }
+    ca.K = c.M * ctx->Q; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * c.M * ctx->Q;
+    ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
+    k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+    if (tail) {
+      with_P(ctx->P, [&](auto Lc) {
+        decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftw, fa, tail->ap, tail->w, tail->mw, tail->vw, ctx->H,
+                                  ctx->cm, ctx->status, st);
+      });
+    } else {
+      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftw, fa, ctx->status, st); });
+    }
+    ctx->launches += 3;
+    return launch_check(ctx, "chebyshev adjoint (filters)");
   }
   const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
   KP kp = make_kp(ctx, 1);

@@ -18,6 +18,7 @@ OK, E_INVALID, E_DEGENERATE, E_NONFINITE, E_CUDA, E_NCCL, E_NOMEM = range(7)
 WRT_FILTERS, WRT_TRANSMIT = 1, 2
 BLOCK_A, BLOCK_B, BLOCK_AB = 1, 2, 3
 LOSS_MAX, LOSS_LSE, LOSS_PNORM = 0, 1, 2
+ENGINE_AUTO, ENGINE_FFT, ENGINE_CHEBYSHEV = 0, 1, 2
 
 
 class SqngdError(RuntimeError):
@@ -42,6 +43,8 @@ class Config(C.Structure):
         ("adam_b1", C.c_double), ("adam_b2", C.c_double), ("adam_eps", C.c_double),
         ("n_h", C.c_int32), ("n_x", C.c_int32),
         ("weights", C.c_void_p),
+        ("doppler_engine", C.c_int32),
+        ("lr_tol", C.c_double),
     ]
 
 
@@ -103,6 +106,8 @@ def lib():
         L.sqngd_num_units.argtypes = [C.POINTER(Config)]
         L.sqngd_shard_range.restype = None
         L.sqngd_shard_range.argtypes = [i64, i32, i32, C.POINTER(i64), C.POINTER(i64)]
+        L.sqngd_engine_info.restype = i32
+        L.sqngd_engine_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         L.sqngd_version.restype = C.c_char_p
         L.sqngd_version.argtypes = []
         _lib = L
@@ -112,7 +117,7 @@ def lib():
 EXPORTED = ["sqngd_create", "sqngd_destroy", "sqngd_last_error", "sqngd_sync", "sqngd_quantize",
             "sqngd_af_forward", "sqngd_loss_grad_s", "sqngd_af_loss_grad", "sqngd_step",
             "sqngd_profile_enable", "sqngd_profile_read",
-            "sqngd_num_units", "sqngd_shard_range", "sqngd_version"]
+            "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info"]
 
 
 def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Config:
@@ -130,6 +135,8 @@ def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Co
         adam_eps=float(getattr(cfg, "adam_eps", 1e-8)),
         n_h=int(getattr(cfg, "n_h", 10)), n_x=int(getattr(cfg, "n_x", 10)),
         weights=weights_ptr,
+        doppler_engine=int(getattr(cfg, "doppler_engine", ENGINE_AUTO)),
+        lr_tol=float(getattr(cfg, "lr_tol", 0.0)),
     )
 
 
@@ -221,6 +228,12 @@ class Context:
         n = C.c_int64()
         self._check(lib().sqngd_profile_read(self.h, ms, cnt, C.byref(n), 1 if reset else 0))
         return dict(ms=list(ms), count=list(cnt), launches=n.value)
+
+    def engine_info(self) -> dict:
+        e, q, err = C.c_int32(), C.c_int32(), C.c_double()
+        self._check(lib().sqngd_engine_info(self.h, C.byref(e), C.byref(q), C.byref(err)))
+        return {"engine": {ENGINE_FFT: "fft", ENGINE_CHEBYSHEV: "chebyshev"}.get(e.value, "?"), "Q": q.value,
+                "err_bound": err.value}
 
     def sync(self):
         self._check(lib().sqngd_sync(self.h, self._stream()))
