@@ -79,27 +79,34 @@ struct MetricsArgs {
   int hist_stride, hist_col;
 };
 
-// Eqs. 7-10, 37-42 for restart r from the combined partials.
-__device__ void metrics_one(const MetricsArgs& a, int r, int* status) {
-  MetricsOut o;
-  double va, vc;
-  decode_key(a.red[r].key_a, a.M, a.N, a.K, a.L, o.argmax_auto, &va);
-  decode_key(a.red[r].key_c, a.M, a.N, a.K, a.L, o.argmax_cross, &vc);
-  o.wapsl = sqrt(va) / a.N;
-  o.wcpsl = sqrt(vc) / a.N;
-  o.wpsl = fmax(o.wapsl, o.wcpsl);
-  if (a.mode == 0) o.loss_wpsl = o.wpsl;
-  else if (a.red[r].m > -INFINITY && a.red[r].S > 0.0)
-    o.loss_wpsl = a.mode == 1 ? a.red[r].m + log(a.red[r].S) / a.bp : a.red[r].m * pow(a.red[r].S, 1.0 / a.bp);
-  else o.loss_wpsl = 0.0;
+// Eqs. 7-10, 37-42 for restart r from the combined partials.  Called by one whole warp
+// (all 32 lanes): lane m computes p_m (Eq. 38) for m = lane, lane + 32, ...; the fixed-order
+// xor-shuffle sum of (p_m - p_tar)^2 is deterministic; lane 0 writes the record.
+__device__ void metrics_warp(const MetricsArgs& a, int r, int* status) {
+  const int lane = threadIdx.x & 31;
   double lsn = 0.0;
-  for (int m = 0; m < a.M; ++m) {
+  for (int m = lane; m < a.M; m += 32) {
     const double2 c = a.cm[(size_t)r * a.M + m];
     const double p = sqrt(c.x * c.x + c.y * c.y) / a.N;
     if (a.p_out) a.p_out[(size_t)r * a.M + m] = p;
     if (p == 0.0) atomicOr(status, ST_DEGENERATE);
     lsn += (p - a.ptar) * (p - a.ptar);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsn += __shfl_xor_sync(0xffffffffu, lsn, o);
+  if (lane != 0) return;
+  MetricsOut o;
+  double va, vc;
+  const Red rr = a.red[r];
+  decode_key(rr.key_a, a.M, a.N, a.K, a.L, o.argmax_auto, &va);
+  decode_key(rr.key_c, a.M, a.N, a.K, a.L, o.argmax_cross, &vc);
+  o.wapsl = sqrt(va) / a.N;
+  o.wcpsl = sqrt(vc) / a.N;
+  o.wpsl = fmax(o.wapsl, o.wcpsl);
+  if (a.mode == 0) o.loss_wpsl = o.wpsl;
+  else if (rr.m > -INFINITY && rr.S > 0.0)
+    o.loss_wpsl = a.mode == 1 ? rr.m + log(rr.S) / a.bp : rr.m * exp(log(rr.S) / a.bp);
+  else o.loss_wpsl = 0.0;
   o.loss_snrl = lsn / a.M;
   o.loss = a.eps * o.loss_wpsl + (1.0 - a.eps) * o.loss_snrl;
   o.flags = a.flags;
@@ -163,8 +170,9 @@ __device__ void reduce_restart(int r, int GPR, int g_lo, int g_hi, int mode, dou
     red[r].S = S;
     red[r].key_a = a;
     red[r].key_c = cc;
-    if (ma.out || ma.loss_hist || ma.p_out) metrics_one(ma, r, status);
   }
+  __syncthreads();
+  if (threadIdx.x < 32 && (ma.out || ma.loss_hist || ma.p_out)) metrics_warp(ma, r, status);
   __syncthreads();
 }
 

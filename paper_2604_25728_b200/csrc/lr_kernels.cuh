@@ -27,21 +27,33 @@
 #include <stdint.h>
 
 #include "af_kernels.cuh"
+#include "common.cuh"
 
 namespace sq {
+
+// Per-restart record of the Chebyshev engine, filled by k_lr with order-independent
+// atomics (max of the unit shifts as positive-float bits, max of the packed keys), so
+// the result is deterministic; reset by k_node of the same evaluation.
+struct LrRed {
+  unsigned int mbits;  // max unit shift (float bits; 0 = none)
+  unsigned int pad;
+  unsigned long long key_a, key_c;
+};
 
 // Node AFs for every unit (r, m, l, q): R_{ml,q}(tau) = IFFT_P(X~_{m,q} conj(H_l))[(-tau) mod P]
 // (Eq. 36, Q1), stored at Rn[((r M + m) M + l) Q + q][tau + N - 1].
 template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB)
     k_node(int units, int M, int Q, int N, int LS, const float2* __restrict__ Xc, const float2* __restrict__ H,
-           const float2* __restrict__ ftw, float2* __restrict__ Rn) {
+           const float2* __restrict__ ftw, float2* __restrict__ Rn, int R, LrRed* lred) {
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
   const int u = blockIdx.x * G + grp;
   float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
   GroupSync sync{1 + grp, T, group_mask(T)};
+  if (blockIdx.x == 0)  // this evaluation's k_lr maxima
+    for (int i = threadIdx.x; i < R; i += blockDim.x) lred[i] = LrRed{0u, 0u, 0ull, 0ull};
   const int uu = u < units ? u : units - 1;
   const int q = uu % Q, pr = uu / Q;  // pr = (r M + m) M + l
   const int l = pr % M, rm = pr / M, r = rm / M;
@@ -62,16 +74,17 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
 }
 
 struct LrArgs {
-  int R, M, N, L, K, nch, kparts, LS, QS;  // QS: coefficient row stride (Q rounded up to 4)
+  int R, M, N, L, K, nch, kw, LS, QS;  // kw: warps (bin-pair ranges) per unit; QS: coefficient row stride
   int tau_lo, tau_hi, excl0;
   float bp, invN;
   const float* weights;  // [K][L] or nullptr
   const float* wmax;     // [L] max_k weights (HW only)
   const float* coef;     // [(K/2) + 1][QS]: alpha_0..alpha_{Q/2-1}, beta_0..beta_{Q/2-1}; last row: middle bin
   const float2* Rn;      // [R M M][Q][LS] node AFs
-  float2* Gn;            // [kparts][R M M][Q][LS] node cotangents (unit-scaled)
+  float2* Gn;            // [R M M][Q][LS] node cotangents (scaled to the unit shift)
   float* af_mag;         // [R][M][M][K][L] or nullptr (forward only)
-  Part part;             // unit slots, u = ((pair nch) + chunk) kparts + kpart
+  Part part;             // unit slots, u = pair nch + chunk
+  LrRed* lred;           // [R]
 };
 
 // One Doppler cell of the fused epilogue (a5 / a7): key tracking, surrogate term, cotangent.
@@ -111,31 +124,44 @@ __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int 
   return make_float2(A.x * gf, A.y * gf);
 }
 
-// Fused Doppler contraction + cell epilogue + adjoint contraction.  One warp per unit
-// (pair (r, m, l), 32 consecutive lags, one range of bin pairs); a thread owns one lag.
-// Each thread accumulates its surrogate sum and cotangents with its own shift (node
-// maximum + 40/beta for LSE, so no term overflows); the warp rescales to the unit's
-// shift at the end and writes (key, shift, sum) into the unit's slot and the node
-// cotangents G^_q(tau) = sum_k l_q(f_k) G~(tau, f_k) into Gn.  A thread whose cells
-// exceed its shift by more than 96/(beta log2 e) redoes the unit with the exact maximum.
+// Rescale factor of a sum accumulated with shift `from` to the shift `to` (LSE: e^{beta(from-to)};
+// PNORM: (from/to)^(p-1) for the cotangents, times from/to for the sum).
+template <int LM>
+__device__ __forceinline__ void lr_rescale(float from, float to, float lb, float bp, float& fS, float& fG) {
+  if (LM == 1) {
+    fS = fG = ex2a(lb * (from - to));
+  } else {
+    const float rt = to > 0.f ? from / to : 0.f;
+    fG = rt > 0.f ? ex2a((bp - 1.f) * lg2a(rt)) : 0.f;
+    fS = fG * rt;
+  }
+}
+
+// Fused Doppler contraction + cell epilogue + adjoint contraction.  One CTA per unit
+// (pair (r, m, l) x 32 consecutive lags); its kw warps split the bin pairs, a lane owns one
+// lag.  Each lane accumulates its surrogate sum and cotangents with its own shift (node
+// maximum + 40/beta for LSE, so no term overflows; identical in every warp of the unit);
+// a lane whose cells exceed that by more than 96/(beta log2 e) redoes its range with the
+// exact maximum.  The warps' partials are combined in shared memory in warp order, warp 0
+// rescales the lanes to the unit's shift and writes (key, shift, sum) into the unit's slot,
+// the node cotangents G^_q(tau) = sum_k l_q(f_k) G~(tau, f_k) into Gn, and the restart's
+// running maxima (LrRed) with atomicMax.
 template <int Q, int LM, bool HW, bool GRAD>
-__global__ void __launch_bounds__(128) k_lr(const LrArgs a, int units) {
+__global__ void __launch_bounds__(256) k_lr(const LrArgs a) {
   constexpr int QH = Q / 2;
+  constexpr int NR = GRAD ? 2 * Q + 4 : 4;  // per-lane reduction record (floats)
   extern __shared__ float4 lr_smem[];
-  float* cf = reinterpret_cast<float*>(lr_smem);
   const int Kp = a.K / 2;
   const bool odd = (a.K & 1) != 0;
-  const int ncf = (Kp + 1) * a.QS;
-  for (int i = threadIdx.x; i < ncf; i += blockDim.x) cf[i] = __ldg(a.coef + i);
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (u >= units) return;  // warp-uniform
-  const int kp = u % a.kparts;
-  const int c = (u / a.kparts) % a.nch;
-  const int pr = u / (a.kparts * a.nch);
+  // coefficients: warp-uniform float4 loads through L1 (every CTA of the SM reads the same table)
+  const float* cf = a.coef;
+  float* rs = reinterpret_cast<float*>(lr_smem);  // [kw][NR][32]
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int u = blockIdx.x;
+  const int c = u % a.nch;
+  const int pr = u / a.nch;
   const int M = a.M;
-  const int l = pr % M, m = (pr / M) % M;
+  const int l = pr % M, m = (pr / M) % M, r = pr / (M * M);
   const int idx = c * 32 + lane;
   const int tau = idx - (a.N - 1);
   const bool inL = idx < a.L;
@@ -155,8 +181,8 @@ __global__ void __launch_bounds__(128) k_lr(const LrArgs a, int units) {
       nm2 = fmaxf(nm2, fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)));
     }
   }
-  const int p0 = (int)((long long)Kp * kp / a.kparts), p1 = (int)((long long)Kp * (kp + 1) / a.kparts);
-  const bool do_mid = odd && kp == a.kparts - 1;
+  const int p0 = (int)((long long)Kp * wp / a.kw), p1 = (int)((long long)Kp * (wp + 1) / a.kw);
+  const bool do_mid = odd && wp == a.kw - 1;
   const float bp = a.bp;
   const float lb = bp * 1.4426950408889634f;
   const float wm = HW ? (inL ? __ldg(a.wmax + idx) : 0.f) : 1.f;
@@ -183,7 +209,7 @@ __global__ void __launch_bounds__(128) k_lr(const LrArgs a, int units) {
       float co[(Q + 3) & ~3];
 #pragma unroll
       for (int i = 0; i < (Q + 3) / 4; ++i) {
-        const float4 t4 = cp[i];
+        const float4 t4 = __ldg(cp + i);
         co[4 * i] = t4.x; co[4 * i + 1] = t4.y; co[4 * i + 2] = t4.z; co[4 * i + 3] = t4.w;
       }
       float2 Pe = make_float2(0.f, 0.f), Po = make_float2(0.f, 0.f);
@@ -209,7 +235,9 @@ __global__ void __launch_bounds__(128) k_lr(const LrArgs a, int units) {
       }
     }
     if (do_mid) {  // f = grid centre: beta = 0
-      const float* cm = cf + Kp * a.QS;
+      float cm[QH];
+#pragma unroll
+      for (int j = 0; j < QH; ++j) cm[j] = __ldg(cf + Kp * a.QS + j);
       float2 Pe = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < QH; ++j) {
@@ -234,37 +262,77 @@ __global__ void __launch_bounds__(128) k_lr(const LrArgs a, int units) {
     mrow = nullptr;  // the map was written in the first pass
   }
 
-  // ---- unit reduction: key, shift, sum; node cotangents
+  // ---- this warp's lane record: best cell key, shift, sum, cotangents
   float best = bl;
   int bk = kl;
   if (bmid > best) { best = bmid; bk = kmid; }
   if (bh > best) { best = bh; bk = kh; }
   const uint32_t cell = ((uint32_t)((m * M + l) * a.L + idx)) * (uint32_t)a.K + (uint32_t)bk;
   unsigned long long key = (valid && best >= 0.f) ? pack_key(best, cell) : 0ull;
+  float* rec = rs + (size_t)wp * NR * 32 + lane;
+  if (a.kw > 1) {
+    rec[0] = __uint_as_float((uint32_t)(key >> 32));
+    rec[32] = __uint_as_float((uint32_t)key);
+    rec[64] = shift;
+    rec[96] = S;
+    if (GRAD) {
+#pragma unroll
+      for (int j = 0; j < QH; ++j) {
+        rec[(4 + 4 * j) * 32] = GE[j].x;
+        rec[(5 + 4 * j) * 32] = GE[j].y;
+        rec[(6 + 4 * j) * 32] = GO[j].x;
+        rec[(7 + 4 * j) * 32] = GO[j].y;
+      }
+    }
+    __syncthreads();
+    if (wp != 0) return;
+    // warp 0: combine the kw records of each lane in warp order (deterministic)
+    for (int w = 1; w < a.kw; ++w) {
+      const float* o = rs + (size_t)w * NR * 32 + lane;
+      const unsigned long long ko =
+          ((unsigned long long)__float_as_uint(o[0]) << 32) | (unsigned long long)__float_as_uint(o[32]);
+      key = ko > key ? ko : key;
+      if (LM != 0) {
+        const float so = o[64];
+        const float mx = fmaxf(shift, so);
+        float fS0 = 1.f, fG0 = 1.f, fS1 = 1.f, fG1 = 1.f;
+        if (valid && so != shift) {  // only after a redo
+          lr_rescale<LM>(shift, mx, lb, bp, fS0, fG0);
+          lr_rescale<LM>(so, mx, lb, bp, fS1, fG1);
+        }
+        S = S * fS0 + o[96] * fS1;
+        if (GRAD) {
+#pragma unroll
+          for (int j = 0; j < QH; ++j) {
+            GE[j].x = GE[j].x * fG0 + o[(4 + 4 * j) * 32] * fG1;
+            GE[j].y = GE[j].y * fG0 + o[(5 + 4 * j) * 32] * fG1;
+            GO[j].x = GO[j].x * fG0 + o[(6 + 4 * j) * 32] * fG1;
+            GO[j].y = GO[j].y * fG0 + o[(7 + 4 * j) * 32] * fG1;
+          }
+        }
+        shift = mx;
+      }
+    }
+  }
+
+  // ---- unit reduction (warp 0): key, shift, sum; node cotangents; restart maxima
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
     key = y > key ? y : key;
   }
   float mw = 0.f, fS = 0.f, fG = 0.f;
-  if (LM == 1) {
-    mw = valid ? shift : -INFINITY;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-    fS = fG = valid ? ex2a(lb * (shift - mw)) : 0.f;
-  } else if (LM == 2) {
+  if (LM != 0) {
     mw = valid ? shift : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-    const float rt = valid && mw > 0.f ? shift / mw : 0.f;
-    fG = rt > 0.f ? ex2a((bp - 1.f) * lg2a(rt)) : 0.f;
-    fS = fG * rt;
+    if (valid) lr_rescale<LM>(shift, mw, lb, bp, fS, fG);
   }
   float Su = S * fS;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) Su += __shfl_xor_sync(0xffffffffu, Su, o);
   if (GRAD && inL) {
-    float2* gp = a.Gn + (size_t)kp * ((size_t)a.R * M * M * Q * a.LS) + (size_t)pr * Q * a.LS + idx;
+    float2* gp = a.Gn + (size_t)pr * Q * a.LS + idx;
 #pragma unroll
     for (int j = 0; j < QH; ++j) {
       gp[(size_t)j * a.LS] = make_float2((GE[j].x + GO[j].x) * fG, (GE[j].y + GO[j].y) * fG);
@@ -274,23 +342,415 @@ __global__ void __launch_bounds__(128) k_lr(const LrArgs a, int units) {
   if (lane == 0) {
     a.part.key[2 * (size_t)u] = is_auto ? key : 0ull;
     a.part.key[2 * (size_t)u + 1] = is_auto ? 0ull : key;
-    a.part.m[u] = mw;
+    a.part.m[u] = mw;  // 0: no valid lane
     a.part.S[u] = Su;
+    if (key) atomicMax(is_auto ? &a.lred[r].key_a : &a.lred[r].key_c, key);
+    if (LM != 0 && mw > 0.f) atomicMax(&a.lred[r].mbits, __float_as_uint(mw));
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Tensor-core variant of k_lr: the Doppler contraction and its adjoint as warp-level
+// mma.sync m16n8k8 TF32 products in 3xTF32 form (a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi,
+// fp32 accumulation: ~2^-21 relative, near the fp32 path's accuracy).  A warp owns 16 lags x a
+// range of 8-pair tiles; with g = lane / 4, c = lane % 4 a thread holds lags g and g + 8.
+//   forward  Pe = E . alpha, Po = O . beta : A[16 lags x 8 (j < Q/2, zero-padded)] x B[8 x 8 pairs]
+//   adjoint  GE += SG . alpha^T, GO += DG . beta^T : A[16 lags x 8 pairs] x B[8 pairs x 8 j]
+// The forward D fragment (rows g, g+8; pairs 2c, 2c+1) is exactly the adjoint A fragment
+// once the tile's pairs are ordered (2c -> k-column c, 2c+1 -> c+4), so G never leaves the
+// registers.  B fragments come pre-split (hi, lo) and pre-permuted from the host tables.
+// The middle bin of an odd K (f = grid centre, beta = 0) is one extra cell per lag, done on
+// the CUDA cores by the last warp of the unit.
+struct LrtArgs {
+  int R, M, N, L, K, nch, kw, LS, NT, NTF;  // nch: 16-lag chunks; NT: 8-pair tiles of the K/2 bin pairs; NTF: full ones
+  int tau_lo, tau_hi, excl0;
+  float bp, invN;
+  const float* weights;  // [K][L] or nullptr
+  const float* wmax;     // [L]
+  const float4* tabF;    // [NT][32][2]: forward B fragments {a_b0h, a_b1h, a_b0l, a_b1l}, {beta ...}
+  const float4* tabA;    // [NT][32][2]: adjoint B fragments
+  const float* coefm;    // [Q/2] middle-bin coefficients l_j(f_centre) (odd K)
+  const float2* Rn;      // [R M M][Q][LS]
+  float2* Gn;            // [R M M][Q][LS]
+  float* af_mag;         // forward only
+  Part part;             // unit slots, u = pair nch + chunk
+  LrRed* lred;
+};
+
+// x = hi + lo with hi = x truncated to TF32 (the tensor core reads the top 19 bits of an
+// operand register, so hi may be passed as the bits of x itself) and lo = x - hi exact.
+// (cvt.rna.tf32 is emulated on sm_100a: 4 integer ops; truncation is 2: LOP3 + FADD.)
+__device__ __forceinline__ void tf32_split(float x, uint32_t& h, uint32_t& l) {
+  h = __float_as_uint(x);
+  l = __float_as_uint(x - __uint_as_float(h & 0xFFFFE000u));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// d += (ah + al)(bh + bl), the al bl term dropped; small terms first.
+__device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], float4 b) {
+  mma_tf32(d, al, __float_as_uint(b.x), __float_as_uint(b.y));
+  mma_tf32(d, ah, __float_as_uint(b.z), __float_as_uint(b.w));
+  mma_tf32(d, ah, __float_as_uint(b.x), __float_as_uint(b.y));
+}
+__device__ __forceinline__ void split4(const float (&x)[4], uint32_t (&h)[4], uint32_t (&l)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tf32_split(x[i], h[i], l[i]);
+}
+
+template <int Q, int LM, bool HW, bool GRAD>
+__global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
+  constexpr int QH = Q / 2;
+  constexpr int NR = 6 + (GRAD ? 16 : 0);  // per-lane record: key(2), shift(2), S(2), GE/GO(16)
+  extern __shared__ float4 lr_smem[];
+  float* rs = reinterpret_cast<float*>(lr_smem);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int g = lane >> 2, cq = lane & 3;
+  const int u = blockIdx.x;
+  const int ch = u % a.nch;
+  const int pr = u / a.nch;
+  const int M = a.M;
+  const int l = pr % M, m = (pr / M) % M;
+  const bool is_auto = m == l;
+  int idx[2];
+  bool inL[2], valid[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    idx[h] = ch * 16 + g + 8 * h;
+    const int tau = idx[h] - (a.N - 1);
+    inL[h] = idx[h] < a.L;
+    valid[h] = inL[h] && tau >= a.tau_lo && tau <= a.tau_hi && !(is_auto && a.excl0 && tau == 0);
+  }
+  // node values -> A fragments (element e: row h = e & 1, column j = c + 4 (e >> 1))
+  uint32_t aErh[4], aErl[4], aEih[4], aEil[4], aOrh[4], aOrl[4], aOih[4], aOil[4];
+  float nm2[2] = {0.f, 0.f};
+  {
+    float Er[4], Ei[4], Or[4], Oi[4];
+    const float2* Rp = a.Rn + (size_t)pr * Q * a.LS;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int h = e & 1, j = cq + 4 * (e >> 1);
+      float2 x = make_float2(0.f, 0.f), y = x;
+      if (j < QH && inL[h]) {
+        x = __ldg(Rp + (size_t)j * a.LS + idx[h]);
+        y = __ldg(Rp + (size_t)(Q - 1 - j) * a.LS + idx[h]);
+      }
+      Er[e] = x.x + y.x; Ei[e] = x.y + y.y; Or[e] = x.x - y.x; Oi[e] = x.y - y.y;
+      nm2[h] = fmaxf(nm2[h], fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)));
+    }
+    split4(Er, aErh, aErl); split4(Ei, aEih, aEil); split4(Or, aOrh, aOrl); split4(Oi, aOih, aOil);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // the quad holds all j of its two lags
+    nm2[h] = fmaxf(nm2[h], __shfl_xor_sync(0xffffffffu, nm2[h], 1));
+    nm2[h] = fmaxf(nm2[h], __shfl_xor_sync(0xffffffffu, nm2[h], 2));
+  }
+  const float bp = a.bp;
+  const float lb = bp * 1.4426950408889634f;
+  float shift[2] = {0.f, 0.f};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float wm = HW ? (inL[h] ? __ldg(a.wmax + idx[h]) : 0.f) : 1.f;
+    if (LM == 1) shift[h] = sqrtf(nm2[h]) * a.invN * wm + 40.f / bp;
+    if (LM == 2) shift[h] = fmaxf(sqrtf(nm2[h]) * a.invN * wm, 1e-30f);
+  }
+  const int t0 = (int)((long long)a.NT * wp / a.kw), t1 = (int)((long long)a.NT * (wp + 1) / a.kw);
+  float* mrow[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    mrow[h] = (!GRAD && a.af_mag && inL[h]) ? a.af_mag + (size_t)pr * a.K * a.L + idx[h] : nullptr;
+
+  float bl[2], bh[2], S[2];
+  int kl[2], kh[2];
+  float GEr[4], GEi[4], GOr[4], GOi[4];
+  LrArgs la;  // lr_cell reads weights, L, bp only
+  la.weights = a.weights; la.L = a.L; la.bp = a.bp;
+  const int Kp = a.K / 2;
+  const bool odd = (a.K & 1) != 0;
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      bl[h] = bh[h] = -1.f;
+      kl[h] = kh[h] = 0;
+      S[h] = 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) GEr[i] = GEi[i] = GOr[i] = GOi[i] = 0.f;
+    const float lbN = lb * a.invN;
+    float nlbs[2], qN[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      nlbs[h] = valid[h] ? -lb * shift[h] : -INFINITY;
+      qN[h] = valid[h] ? a.invN / shift[h] : 0.f;
+    }
+    // one 8-pair tile: forward MMAs, 8 cells per thread, adjoint MMAs.  MASKED: the remainder
+    // tile of a K/2 that is not a multiple of 8 (pairs >= K/2 are zero padding).
+    auto tile = [&](int t, auto masked_c) {
+      constexpr bool MASKED = decltype(masked_c)::value;
+      const float4* tf = a.tabF + ((size_t)t * 32 + lane) * 2;
+      const float4 fa = __ldg(tf), fb = __ldg(tf + 1);
+      float Per[4] = {0.f, 0.f, 0.f, 0.f}, Pei[4] = {0.f, 0.f, 0.f, 0.f};
+      float Por[4] = {0.f, 0.f, 0.f, 0.f}, Poi[4] = {0.f, 0.f, 0.f, 0.f};
+      mma3(Per, aErh, aErl, fa);
+      mma3(Pei, aEih, aEil, fa);
+      mma3(Por, aOrh, aOrl, fb);
+      mma3(Poi, aOih, aOil, fb);
+      float SGr[4], SGi[4], DGr[4], DGi[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {  // D element e: row h = e >> 1, pair p = 8t + 2c + (e & 1)
+        const int h = e >> 1;
+        const int p = 8 * t + 2 * cq + (e & 1);
+        const float2 A0 = make_float2(Per[e] + Por[e], Pei[e] + Poi[e]);
+        const float2 A1 = make_float2(Per[e] - Por[e], Pei[e] - Poi[e]);
+        float2 G0, G1;
+        if (!MASKED) {
+          G0 = lr_cell<LM, HW, GRAD, false>(A0, p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bl[h], kl[h], S[h], mrow[h]);
+          G1 = lr_cell<LM, HW, GRAD, true>(A1, a.K - 1 - p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bh[h], kh[h], S[h],
+                                            mrow[h]);
+        } else {
+          const bool pv = p < Kp;
+          const bool v0 = valid[h] && pv;
+          float b0 = bl[h], b1 = bh[h];
+          int k0 = kl[h], k1 = kh[h];
+          G0 = lr_cell<LM, HW, GRAD, false>(A0, pv ? p : 0, la, idx[h], v0, lbN, v0 ? nlbs[h] : -INFINITY,
+                                            v0 ? qN[h] : 0.f, b0, k0, S[h], pv ? mrow[h] : nullptr);
+          G1 = lr_cell<LM, HW, GRAD, true>(A1, pv ? a.K - 1 - p : 0, la, idx[h], v0, lbN, v0 ? nlbs[h] : -INFINITY,
+                                           v0 ? qN[h] : 0.f, b1, k1, S[h], pv ? mrow[h] : nullptr);
+          if (pv) { bl[h] = b0; kl[h] = k0; bh[h] = b1; kh[h] = k1; }
+          if (!v0) G0 = G1 = make_float2(0.f, 0.f);
+        }
+        SGr[e] = G0.x + G1.x; SGi[e] = G0.y + G1.y;
+        DGr[e] = G0.x - G1.x; DGi[e] = G0.y - G1.y;
+      }
+      if (GRAD) {
+        const float4* ta = a.tabA + ((size_t)t * 32 + lane) * 2;
+        const float4 ga = __ldg(ta), gb = __ldg(ta + 1);
+        // D order (g,2c) (g,2c+1) (g+8,2c) (g+8,2c+1) -> A order (g,c) (g+8,c) (g,c+4) (g+8,c+4)
+        const float sr[4] = {SGr[0], SGr[2], SGr[1], SGr[3]}, si[4] = {SGi[0], SGi[2], SGi[1], SGi[3]};
+        const float dr[4] = {DGr[0], DGr[2], DGr[1], DGr[3]}, di[4] = {DGi[0], DGi[2], DGi[1], DGi[3]};
+        uint32_t hh[4], ll[4];
+        split4(sr, hh, ll); mma3(GEr, hh, ll, ga);
+        split4(si, hh, ll); mma3(GEi, hh, ll, ga);
+        split4(dr, hh, ll); mma3(GOr, hh, ll, gb);
+        split4(di, hh, ll); mma3(GOi, hh, ll, gb);
+      }
+    };
+    const int tf_end = t1 < a.NTF ? t1 : a.NTF;
+#pragma unroll 1
+    for (int t = t0; t < tf_end; ++t) tile(t, std::integral_constant<bool, false>{});
+    if (t1 > a.NTF && t0 <= a.NTF) tile(a.NTF, std::integral_constant<bool, true>{});
+    if (odd && wp == a.kw - 1) {
+      // middle bin f = grid centre (beta = 0) on the CUDA cores: At = sum_j alpha_j E_j, summed over the
+      // quad's j columns; every lane of the quad evaluates the cell (G is needed in all of them), the
+      // sum and the key are counted by lane c = 0 only.
+      const float am0 = cq < QH ? __ldg(a.coefm + cq) : 0.f, am1 = cq + 4 < QH ? __ldg(a.coefm + cq + 4) : 0.f;
+      float2 Am[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float e0r = __uint_as_float(aErh[h]), e0i = __uint_as_float(aEih[h]);  // hi holds x itself
+        const float e1r = __uint_as_float(aErh[2 + h]), e1i = __uint_as_float(aEih[2 + h]);
+        float xr = fmaf(am0, e0r, am1 * e1r), xi = fmaf(am0, e0i, am1 * e1i);
+        xr += __shfl_xor_sync(0xffffffffu, xr, 1);
+        xi += __shfl_xor_sync(0xffffffffu, xi, 1);
+        xr += __shfl_xor_sync(0xffffffffu, xr, 2);
+        xi += __shfl_xor_sync(0xffffffffu, xi, 2);
+        Am[h] = make_float2(xr, xi);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float Sm = 0.f, bm = bl[h];
+        int km = kl[h];
+        const float2 Gm = lr_cell<LM, HW, GRAD, false>(Am[h], Kp, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bm, km, Sm,
+                                                       cq == 0 ? mrow[h] : nullptr);
+        if (cq == 0) { S[h] += Sm; bl[h] = bm; kl[h] = km; }
+        if (GRAD) {
+#pragma unroll
+          for (int i = 2 * h; i < 2 * h + 2; ++i) {  // D elements of row h: j = 2c + (i & 1)
+            const int j = 2 * cq + (i & 1);
+            const float aj = j < QH ? __ldg(a.coefm + j) : 0.f;
+            GEr[i] = fmaf(aj, Gm.x, GEr[i]);
+            GEi[i] = fmaf(aj, Gm.y, GEi[i]);
+          }
+        }
+      }
+    }
+    if (LM == 0) break;
+    bool bad = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float vb = sqrtf(fmaxf(fmaxf(bl[h], bh[h]), 0.f)) * a.invN;
+      const bool bd = valid[h] && (LM == 1 ? lb * (vb - shift[h]) > 96.f
+                                           : (vb > shift[h] && (bp * log2f(vb / shift[h])) > 96.f));
+      bad |= bd;
+      if (bd) shift[h] = vb;
+    }
+    if (!__any_sync(0xffffffffu, bad) || pass == 1) break;
+    // lanes of a quad share rows: keep their shifts identical
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      shift[h] = fmaxf(shift[h], __shfl_xor_sync(0xffffffffu, shift[h], 1));
+      shift[h] = fmaxf(shift[h], __shfl_xor_sync(0xffffffffu, shift[h], 2));
+    }
+    mrow[0] = mrow[1] = nullptr;
+  }
+
+  // ---- lane record: key over both rows, per-row shift / sum, cotangent fragments
+  unsigned long long key = 0ull;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float best = bl[h];
+    int bk = kl[h];
+    if (bh[h] > best) { best = bh[h]; bk = kh[h]; }
+    const uint32_t cell = ((uint32_t)((m * M + l) * a.L + idx[h])) * (uint32_t)a.K + (uint32_t)bk;
+    const unsigned long long kk = (valid[h] && best >= 0.f) ? pack_key(best, cell) : 0ull;
+    key = kk > key ? kk : key;
+  }
+  if (a.kw > 1) {
+    float* rec = rs + (size_t)wp * NR * 32 + lane;
+    rec[0] = __uint_as_float((uint32_t)(key >> 32));
+    rec[32] = __uint_as_float((uint32_t)key);
+    rec[64] = shift[0]; rec[96] = shift[1];
+    rec[128] = S[0]; rec[160] = S[1];
+    if (GRAD) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        rec[(6 + i) * 32] = GEr[i];
+        rec[(10 + i) * 32] = GEi[i];
+        rec[(14 + i) * 32] = GOr[i];
+        rec[(18 + i) * 32] = GOi[i];
+      }
+    }
+    __syncthreads();
+    if (wp != 0) return;
+    for (int w = 1; w < a.kw; ++w) {
+      const float* o = rs + (size_t)w * NR * 32 + lane;
+      const unsigned long long ko =
+          ((unsigned long long)__float_as_uint(o[0]) << 32) | (unsigned long long)__float_as_uint(o[32]);
+      key = ko > key ? ko : key;
+      if (LM != 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float so = o[64 + 32 * h];
+          const float mx = fmaxf(shift[h], so);
+          float fS0 = 1.f, fG0 = 1.f, fS1 = 1.f, fG1 = 1.f;
+          if (valid[h] && so != shift[h]) {  // only after a redo
+            lr_rescale<LM>(shift[h], mx, lb, bp, fS0, fG0);
+            lr_rescale<LM>(so, mx, lb, bp, fS1, fG1);
+          }
+          S[h] = S[h] * fS0 + o[128 + 32 * h] * fS1;
+          if (GRAD) {
+#pragma unroll
+            for (int i = 2 * h; i < 2 * h + 2; ++i) {  // D elements of row h
+              GEr[i] = GEr[i] * fG0 + o[(6 + i) * 32] * fG1;
+              GEi[i] = GEi[i] * fG0 + o[(10 + i) * 32] * fG1;
+              GOr[i] = GOr[i] * fG0 + o[(14 + i) * 32] * fG1;
+              GOi[i] = GOi[i] * fG0 + o[(18 + i) * 32] * fG1;
+            }
+          }
+          shift[h] = mx;
+        }
+      }
+    }
+  }
+
+  // ---- unit reduction (warp 0)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+    key = y > key ? y : key;
+  }
+  float mw = 0.f, fS[2] = {0.f, 0.f}, fG[2] = {0.f, 0.f};
+  if (LM != 0) {
+    mw = fmaxf(valid[0] ? shift[0] : 0.f, valid[1] ? shift[1] : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (valid[h]) lr_rescale<LM>(shift[h], mw, lb, bp, fS[h], fG[h]);
+  }
+  // every lane of a quad holds the same row sums only for its own pairs: sum all lanes
+  float Su = S[0] * fS[0] + S[1] * fS[1];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Su += __shfl_xor_sync(0xffffffffu, Su, o);
+  if (GRAD) {
+    float2* gp = a.Gn + (size_t)pr * Q * a.LS;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // D element i: row h = i >> 1, j = 2c + (i & 1)
+      const int h = i >> 1, j = 2 * cq + (i & 1);
+      if (j < QH && inL[h]) {
+        const float f = fG[h];
+        gp[(size_t)j * a.LS + idx[h]] = make_float2((GEr[i] + GOr[i]) * f, (GEi[i] + GOi[i]) * f);
+        gp[(size_t)(Q - 1 - j) * a.LS + idx[h]] = make_float2((GEr[i] - GOr[i]) * f, (GEi[i] - GOi[i]) * f);
+      }
+    }
+  }
+  if (lane == 0) {
+    a.part.key[2 * (size_t)u] = is_auto ? key : 0ull;
+    a.part.key[2 * (size_t)u + 1] = is_auto ? 0ull : key;
+    a.part.m[u] = mw;
+    a.part.S[u] = Su;
+    const int r = pr / (M * M);
+    if (key) atomicMax(is_auto ? &a.lred[r].key_a : &a.lred[r].key_c, key);
+    if (LM != 0 && mw > 0.f) atomicMax(&a.lred[r].mbits, __float_as_uint(mw));
+  }
+}
+
+// Per restart: the global shift m (LrRed), S = sum_u S_u (m_u -> m), the reduction record
+// and the metrics (a6).  One block per restart, fixed order (deterministic).
+__global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int mode, double bp, Part part,
+                                                    const LrRed* __restrict__ lred, Red* red, MetricsArgs ma,
+                                                    int* status) {
+  __shared__ double shd[32];
+  const int r = blockIdx.x;
+  const float mf = __uint_as_float(lred[r].mbits);
+  const float lb = (float)(bp * 1.4426950408889634);
+  double S = 0.0;
+  if (mode != 0 && mf > 0.f) {
+    const float* Sp = part.S + (size_t)r * GPR;
+    const float* mp = part.m + (size_t)r * GPR;
+#pragma unroll 4
+    for (int g = threadIdx.x; g < GPR; g += blockDim.x) {
+      const float Sg = __ldcg(Sp + g), mg = __ldcg(mp + g);
+      float fS = 0.f, fG;
+      if (mode == 1) lr_rescale<1>(mg, mf, lb, (float)bp, fS, fG);
+      else lr_rescale<2>(mg, mf, lb, (float)bp, fS, fG);
+      S += (Sg > 0.f && mg > 0.f) ? (double)Sg * fS : 0.0;
+    }
+  }
+  auto dsum = [](double x, double y) { return x + y; };
+  S = block_reduce(S, dsum, shd);
+  if (threadIdx.x == 0) {
+    red[r].m = mf > 0.f ? (double)mf : -INFINITY;
+    red[r].S = S;
+    red[r].key_a = lred[r].key_a;
+    red[r].key_c = lred[r].key_c;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && (ma.out || ma.loss_hist || ma.p_out)) metrics_warp(ma, r, status);
+}
+
 struct AdjGArgs {
-  int M, N, Q, LS, nch, kparts, units;
-  size_t gstride;        // Gn stride between k-parts
-  const float2* Gn;      // node cotangents
-  const float* scale;    // per k_lr unit: rescale to the restart's shift (k_reduce_groups)
+  int M, N, Q, LS, nch, csh, units, mode;  // csh: log2 of the k_lr unit's lag chunk (5 or 4)
+  float bp;
+  const float2* Gn;      // node cotangents (unit-scaled)
+  const float* um;       // per k_lr unit: its shift (part.m)
+  const LrRed* lred;     // per restart: the global shift
   const float2* Xc;      // [R][M][Q][P] node spectra X~ (Step A)
   const float2* H;       // [R][M][P] filter spectra / P (Step B)
   float2* out;           // [units][P] spectral partials
+  // Step B: the last of the M groups of a node (r, m, q) to finish sums their partials over l
+  // (fixed order), transforms back and demodulates (k_lrB_tail's work, without a launch).
+  int* cnt;              // [R M Q] arrival counters (zero between launches: the last group resets)
+  const float2* Vt;      // [Q][N] node modulation
+  float2* tslot;         // [R M Q][NS] time-domain node partials
+  int NS;
 };
 
 // Node adjoint correlations, one transform per unit:
-//   G^_{ml,q} = FFT_P(G^ placed at (-tau) mod P) (scaled to the restart's shift), then
+//   G^_{ml,q} = FFT_P(G^ placed at (-tau) mod P) (rescaled to the restart's shift), then
 //   Step B (WRT 2), unit ((r M + m) Q + q) M + l:  out = G^ . H_l            (sum over l: k_lrB_tail)
 //   Step A (WRT 1), unit ((r M + l) M + m) Q + q:  out = X~_{m,q} . conj(G^)  (sum over m, q: combine)
 template <class PL, int G, int MINB, int WRT>
@@ -321,23 +781,22 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
   }
   const int pr = (r * M + m) * M + l;
   const float2* Gp = a.Gn + ((size_t)pr * Q + q) * a.LS;
-  const float* scp = a.scale + (size_t)pr * a.nch * a.kparts;
+  const float* ump = a.um + (size_t)pr * a.nch;
+  const float mf = __uint_as_float(a.lred[r].mbits);
+  const float lb = a.bp * 1.4426950408889634f;
   float2 v[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
+  for (int i = 0; i < E; ++i) {  // branch-free so that all loads issue back to back
     const int j = t + i * T;
-    float2 g = make_float2(0.f, 0.f);
-    if (j < N || j > P - N) {
-      const int idx = lag_of(j, N, P) + N - 1;
-      const float* sc = scp + (idx >> 5) * a.kparts;
-      for (int kp = 0; kp < a.kparts; ++kp) {
-        const float s = __ldg(sc + kp);
-        const float2 x = __ldg(Gp + kp * a.gstride + idx);
-        g.x = fmaf(s, x.x, g.x);
-        g.y = fmaf(s, x.y, g.y);
-      }
-    }
-    v[i] = g;
+    const bool in = j < N || j > P - N;
+    const int idx = in ? lag_of(j, N, P) + N - 1 : 0;
+    const float mu = __ldg(ump + (idx >> a.csh));
+    const float2 x = __ldg(Gp + idx);
+    float fS, fG;
+    if (a.mode == 1) lr_rescale<1>(mu, mf, lb, a.bp, fS, fG);
+    else lr_rescale<2>(mu, mf, lb, a.bp, fS, fG);
+    fG = (in && mu > 0.f && mf > 0.f) ? fG : 0.f;
+    v[i] = make_float2(x.x * fG, x.y * fG);
   }
   int par = 0;
   fft<PL, -1>(v, ftw, xbuf, t, par, sync);
@@ -347,6 +806,39 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
     const float2* Hl = a.H + ((size_t)r * M + l) * P;
 #pragma unroll
     for (int i = 0; i < E; ++i) out[t + i * T] = cmul(v[i], __ldg(Hl + t + i * T));
+    // arrival: the last group of node (r, m, q) does the tail
+    int* flag = reinterpret_cast<int*>(xbuf + FftSmem<PL>::XBUF);
+    const int node = uu / M;
+    __threadfence();
+    sync();
+    if (t == 0) {
+      const int old = atomicAdd(a.cnt + node, 1);
+      flag[0] = old == M - 1;
+      if (old == M - 1) a.cnt[node] = 0;
+    }
+    sync();
+    if (!flag[0]) return;
+    __threadfence();
+    const float2* sp = a.out + (size_t)node * M * P;
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = make_float2(0.f, 0.f);
+    for (int ll = 0; ll < M; ++ll) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = cadd(v[i], __ldcg(sp + (size_t)ll * P + t + i * T));
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i].y = -v[i].y;
+    fft<PL, -1>(v, ftw, xbuf, t, par, sync);  // v = conj(e), e = IFFT_P(sum_l G^ H_l)
+    const float2* vr = a.Vt + (size_t)q * N;
+    float2* o = a.tslot + (size_t)node * a.NS;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int n = t + i * T;
+      if (n < N) {
+        const float2 z = cmul(v[i], __ldg(vr + n));
+        o[n] = make_float2(z.x, -z.y);  // e conj(V_q)
+      }
+    }
   } else {
     const float2* X = a.Xc + (((size_t)r * M + m) * Q + q) * P;
 #pragma unroll

@@ -213,7 +213,7 @@ __global__ void k_sparse_adj(int M, int N, int K, int L, int wrt, double eps, co
 }
 
 __global__ void k_metrics(MetricsArgs a, int* status) {
-  if (threadIdx.x == 0) metrics_one(a, blockIdx.x, status);
+  metrics_warp(a, blockIdx.x, status);
 }
 
 // ------------------------------------------------------------------ finalize gradients
@@ -271,7 +271,7 @@ __device__ __forceinline__ void finalize_elem(const FinArgs& f, size_t e, float2
 
 __global__ void k_finalize_grad(FinArgs f, const float2* __restrict__ red_grad, int* status, MetricsArgs ma) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (threadIdx.x == 0 && blockIdx.x < (unsigned)f.R && (ma.out || ma.loss_hist)) metrics_one(ma, blockIdx.x, status);
+  if (threadIdx.x < 32 && blockIdx.x < (unsigned)f.R && (ma.out || ma.loss_hist)) metrics_warp(ma, blockIdx.x, status);
   if (e >= (size_t)f.R * f.M * f.N) return;
   finalize_elem(f, e, red_grad[e], snrl_coef(f, e / f.N), status);
 }
@@ -401,63 +401,68 @@ __global__ void __launch_bounds__(PL::T* G)
     v[i] = make_float2(x.x, -x.y);
   }
   int par = 0;
-  fft<PL, -1>(v, ftw, gsm, t, par, gops.sync);
-  const double2 gc = snrl_coef(f, row);
-  float c1, c2;
-  ap.corr(c1, c2);
-  float bad = 0.f;
-  double e = 0.0;
-#pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const int n = t + i * T;
-    float2 wn = make_float2(0.f, 0.f);
-    if (n < N) {
-      const size_t j = (size_t)row * N + n;
-      const float2 sv = f.s[j];
-      const float re = 2.f * (v[i].x + ((float)gc.x * sv.x + (float)gc.y * sv.y));   // d = conj(v)
-      const float im = 2.f * (-v[i].y + ((float)gc.x * sv.y - (float)gc.y * sv.x));
-      if (!isfinite(re) || !isfinite(im)) bad = 1.f;
-      if (f.grad_w) f.grad_w[j] = make_float2(re, im);
-      const float g2[2] = {re, im};
-      float x2[2] = {w[j].x, w[j].y};
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {  // Adam on the real parameters (Re w, Im w)
-        const size_t jj = 2 * j + q;
-        const float mi = ap.b1 * mw[jj] + (1.f - ap.b1) * g2[q];
-        const float vi = ap.b2 * vw[jj] + (1.f - ap.b2) * g2[q] * g2[q];
-        if (!skip_all) {
-          mw[jj] = mi;
-          vw[jj] = vi;
-        }
-        x2[q] -= ap.lr * (mi / c1) / (sqrtf(vi / c2) + ap.eps);
-      }
-      wn = make_float2(x2[0], x2[1]);
-      e += (double)wn.x * wn.x + (double)wn.y * wn.y;
-    }
-    v[i] = wn;
-  }
-  const float gbad = gops.max_f(bad);
-  const double en = gops.sum_d2(make_double2(e, 0.0)).x;
-  if (skip_all || gbad > 0.f || !(en > 0.0)) {
-    if (t == 0 && id < rows) atomicOr(status, gbad > 0.f ? ST_NONFINITE : (en > 0.0 ? 0 : ST_DEGENERATE));
-    return;  // uniform across the group
-  }
-  const float sc = (float)sqrt((double)N / en);
   double2 cacc = make_double2(0.0, 0.0);
+  // one inlined FFT instance for both transforms (IFFT of the spectral sum, then FFT of the new
+  // w): half the code, which matters on the few SMs this row kernel runs on (instruction cache)
+#pragma unroll 1
+  for (int ph = 0; ph < 2; ++ph) {
+    fft<PL, -1>(v, ftw, gsm, t, par, gops.sync);
+    if (ph == 1) break;
+    const double2 gc = snrl_coef(f, row);
+    float c1, c2;
+    ap.corr(c1, c2);
+    float bad = 0.f;
+    double e = 0.0;
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const int n = t + i * T;
-    v[i] = make_float2(v[i].x * sc, v[i].y * sc);
-    if (n < N) {
-      const size_t j = (size_t)row * N + n;
-      if (id < rows) w[j] = v[i];
-      const float2 sv = f.s[j];  // c_l = sum_n s_l(n) conj(w_l(n)) for the next evaluation
-      cacc.x += (double)sv.x * v[i].x + (double)sv.y * v[i].y;
-      cacc.y += (double)sv.y * v[i].x - (double)sv.x * v[i].y;
+    for (int i = 0; i < E; ++i) {
+      const int n = t + i * T;
+      float2 wn = make_float2(0.f, 0.f);
+      if (n < N) {
+        const size_t j = (size_t)row * N + n;
+        const float2 sv = f.s[j];
+        const float re = 2.f * (v[i].x + ((float)gc.x * sv.x + (float)gc.y * sv.y));   // d = conj(v)
+        const float im = 2.f * (-v[i].y + ((float)gc.x * sv.y - (float)gc.y * sv.x));
+        if (!isfinite(re) || !isfinite(im)) bad = 1.f;
+        if (f.grad_w) f.grad_w[j] = make_float2(re, im);
+        const float g2[2] = {re, im};
+        float x2[2] = {w[j].x, w[j].y};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {  // Adam on the real parameters (Re w, Im w)
+          const size_t jj = 2 * j + q;
+          const float mi = ap.b1 * mw[jj] + (1.f - ap.b1) * g2[q];
+          const float vi = ap.b2 * vw[jj] + (1.f - ap.b2) * g2[q] * g2[q];
+          if (!skip_all) {
+            mw[jj] = mi;
+            vw[jj] = vi;
+          }
+          x2[q] -= ap.lr * (mi / c1) / (sqrtf(vi / c2) + ap.eps);
+        }
+        wn = make_float2(x2[0], x2[1]);
+        e += (double)wn.x * wn.x + (double)wn.y * wn.y;
+      }
+      v[i] = wn;
     }
-  }
-  cacc = gops.sum_d2(cacc);
-  fft<PL, -1>(v, ftw, gsm, t, par, gops.sync);  // next H_l = FFT_P(w_l) / P
+    const float gbad = gops.max_f(bad);
+    const double en = gops.sum_d2(make_double2(e, 0.0)).x;
+    if (skip_all || gbad > 0.f || !(en > 0.0)) {
+      if (t == 0 && id < rows) atomicOr(status, gbad > 0.f ? ST_NONFINITE : (en > 0.0 ? 0 : ST_DEGENERATE));
+      return;  // uniform across the group
+    }
+    const float sc = (float)sqrt((double)N / en);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int n = t + i * T;
+      v[i] = make_float2(v[i].x * sc, v[i].y * sc);
+      if (n < N) {
+        const size_t j = (size_t)row * N + n;
+        if (id < rows) w[j] = v[i];
+        const float2 sv = f.s[j];  // c_l = sum_n s_l(n) conj(w_l(n)) for the next evaluation
+        cacc.x += (double)sv.x * v[i].x + (double)sv.y * v[i].y;
+        cacc.y += (double)sv.y * v[i].x - (double)sv.x * v[i].y;
+      }
+    }
+    cacc = gops.sum_d2(cacc);
+  }  // next H_l = FFT_P(w_l) / P
   if (id >= rows) return;
   if (t == 0) cm[row] = cacc;
   const float inv = 1.0f / (float)P;
@@ -467,29 +472,49 @@ __global__ void __launch_bounds__(PL::T* G)
 
 // dL/drho_i = -a c sum_e sech^2(c (z_e - rho_i)) dy_e, gathered per threshold over a chunk of
 // elements (partials [R][nchunk][BR], then a fixed-order sum).  sech^2 via MUFU, culled
-// (branch-free) outside |c (z - rho)| < 12 where it is < 1.6e-10.
-__global__ void k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
-                                const float* __restrict__ rho, const float* __restrict__ dy, float* part) {
-  __shared__ float2 zd[256];  // chunk <= 256: (z, dy)
+// outside |c (z - rho)| < 12 where it is < 1.6e-10: per element, a warp whose 32 (sorted)
+// thresholds all lie farther than 12/c from z skips it (warp-uniform test), so only the
+// ~2 x 12/c x B r_n thresholds near each z do the work.
+__global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
+                                                       const float* __restrict__ rho, const float* __restrict__ dy,
+                                                       float* part) {
+  __shared__ __align__(16) float2 zd[1024];  // chunk <= 1024: (z, dy), padded to a multiple of 4
   const int r = blockIdx.z;
   const int ch = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const float ri = i < BR ? rho[(size_t)r * BR + i] : 0.f;
+  const float ri = i < BR ? rho[(size_t)r * BR + i] : rho[(size_t)r * BR + BR - 1];
   const int e0 = ch * chunk, e1 = min(MN, e0 + chunk);
-  for (int e = e0 + threadIdx.x; e < e0 + 256; e += blockDim.x)
+  for (int e = e0 + threadIdx.x; e < e0 + ((e1 - e0 + 3) & ~3); e += blockDim.x)
     zd[e - e0] = e < e1 ? make_float2(z[(size_t)r * MN + e], dy[(size_t)r * MN + e]) : make_float2(1e30f, 0.f);
   __syncthreads();
+  const float win = 12.f / c;
+  float wlo = ri, whi = ri;  // the warp's threshold range (any order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+    whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+  }
+  wlo -= win;
+  whi += win;
   const float k2 = -2.f * 1.4426950408889634f;
   float acc = 0.f;
   const int n = e1 - e0;
-#pragma unroll 4
-  for (int q = 0; q < n; ++q) {
-    const float2 p = zd[q];
-    const float au = c * fabsf(p.x - ri);  // z - rho exact when close (Sterbenz)
-    const float e2 = ex2a_m(k2 * au);               // e^{-2|u|}
-    const float inv = rcp_m(1.f + e2);
-    const float sech2 = 4.f * e2 * inv * inv;        // sech^2(u)
-    acc = fmaf(au < 12.f ? sech2 : 0.f, p.y, acc);
+  const float4* zd4 = reinterpret_cast<const float4*>(zd);
+  for (int q = 0; q < n; q += 4) {  // four elements per (warp-uniform) window test
+    const float4 pa = zd4[q >> 1], pb = zd4[(q >> 1) + 1];
+    const float zz[4] = {pa.x, pa.z, pb.x, pb.z}, dd[4] = {pa.y, pa.w, pb.y, pb.w};
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) any |= zz[k] >= wlo && zz[k] <= whi;
+    if (!any) continue;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float au = c * fabsf(zz[k] - ri);   // z - rho exact when close (Sterbenz)
+      const float e2 = ex2a_m(k2 * au);         // e^{-2|u|}
+      const float inv = rcp_m(1.f + e2);
+      const float sech2 = 4.f * e2 * inv * inv;  // sech^2(u)
+      acc = fmaf(au < 12.f ? sech2 : 0.f, dd[k], acc);
+    }
   }
   if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
 }
@@ -582,6 +607,7 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
   ap.corr(c1, c2);
   const float lr = ap.lr, b1 = ap.b1, b2 = ap.b2, eps = ap.eps;
   if (za.z) {  // Adam on z (elementwise; the grad_rho gather already consumed the old z)
+#pragma unroll 4
     for (int i = threadIdx.x; i < za.MN; i += blockDim.x) {
       const size_t j = (size_t)blockIdx.x * za.MN + i;
       const float gi = za.g[j];
@@ -604,7 +630,8 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
       float gi;
       if (za.rho_part) {
         float acc = 0.f;
-        for (int ch = 0; ch < za.nchunk; ++ch) acc += za.rho_part[((size_t)blockIdx.x * za.nchunk + ch) * BR + i];
+#pragma unroll 8
+        for (int ch = 0; ch < za.nchunk; ++ch) acc += __ldg(za.rho_part + ((size_t)blockIdx.x * za.nchunk + ch) * BR + i);
         gi = za.coef * acc;
       } else {
         gi = g[j];

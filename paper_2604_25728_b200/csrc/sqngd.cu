@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sqngd.h"
@@ -78,16 +79,24 @@ struct sqngd_ctx_s {
   int* status = nullptr;       // latched device status bits
   // Chebyshev Doppler engine (lr_kernels.cuh): Q nodes, tables, node AFs / cotangents
   bool lr = false;
-  int Q = 0, QS = 0, nch = 0, kparts = 1, LS = 0;
-  int64_t units_lr = 0;        // k_lr units: R M^2 nch kparts
+  int Q = 0, QS = 0, nch = 0, kw = 1, LS = 0;
+  bool lr_tc = true;           // k_lrt (mma.sync 3xTF32) instead of the FP32 k_lr
+  int nch16 = 0, NT = 0, NTF = 0;
+  float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
+  float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
+  int64_t units_lr = 0;        // k_lr units (CTAs of kw warps): R M^2 nch
+  size_t lr_smem = 0;          // k_lr dynamic shared memory
+  LrRed* lred = nullptr;       // [R] k_lr running maxima
+  cudaStream_t side = nullptr; // graph branch for k_lr_finish (fork / join events)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double lr_err = 0.0;         // interpolation error bound of the chosen Q (host estimate)
   float2* Vt = nullptr;        // [Q][N] e^{j 2 pi (n - n_c) f*_q / N}
   float* coef = nullptr;       // [K/2 + 1][QS] alpha / beta rows
   float* wmax = nullptr;       // [L] max_k weights (weighted ROI)
   float2* Rn = nullptr;        // [R M M][Q][LS] node AFs
-  float2* Gn = nullptr;        // [kparts][R M M][Q][LS] node cotangents
+  float2* Gn = nullptr;        // [R M M][Q][LS] node cotangents
   float2* tslot = nullptr;     // [R M Q][N] Step-B node time-domain partials
-  int lr_bps = 1;              // k_lr CTAs per SM
+  int* lr_cnt = nullptr;       // [R M Q] k_adj_g arrival counters
   Comm comm;
   long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
   // CUDA graphs of sqngd_step (one per (state buffers, block, outputs, profiling))
@@ -235,8 +244,8 @@ struct Launch {
   static int groups_per_block() { return G; }
   // Chebyshev engine: node AFs, node adjoint correlations, Step-B node tail
   static void node(int units, int M, int Q, int N, int LS, const float2* Xc, const float2* H, const float2* ftw,
-                   float2* Rn, cudaStream_t st) {
-    k_node<PL, G, MINB><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, LS, Xc, H, ftw, Rn);
+                   float2* Rn, int R, LrRed* lred, cudaStream_t st) {
+    k_node<PL, G, MINB><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, LS, Xc, H, ftw, Rn, R, lred);
   }
   static void adj_g(int wrt, const AdjGArgs& a, const float2* ftw, cudaStream_t st) {
     const int blocks = (a.units + G - 1) / G;
@@ -264,9 +273,10 @@ template <int Q>
 struct LrLaunch {
   template <int LM, bool HW, bool GRAD>
   static void go(const LrArgs& a, int units, size_t smem, cudaStream_t st) {
-    k_lr<Q, LM, HW, GRAD><<<(units + 3) / 4, 128, smem, st>>>(a, units);
+    k_lr<Q, LM, HW, GRAD><<<units, 32 * a.kw, smem, st>>>(a);
   }
   static void launch(int lm, bool hw, bool grad, const LrArgs& a, int units, size_t smem, cudaStream_t st) {
+    // units = CTAs, a.kw warps each
     if (lm == 0) { hw ? go<0, true, false>(a, units, smem, st) : go<0, false, false>(a, units, smem, st); return; }
     if (lm == 1) {
       if (grad) hw ? go<1, true, true>(a, units, smem, st) : go<1, false, true>(a, units, smem, st);
@@ -276,10 +286,52 @@ struct LrLaunch {
     if (grad) hw ? go<2, true, true>(a, units, smem, st) : go<2, false, true>(a, units, smem, st);
     else hw ? go<2, true, false>(a, units, smem, st) : go<2, false, false>(a, units, smem, st);
   }
-  static cudaError_t occupancy(int* bps, size_t smem) {  // the heaviest variant (LSE + gradient)
-    cudaError_t e = cudaFuncSetAttribute(k_lr<Q, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lr<Q, 1, false, true>, 128, smem);
+  template <int LM, bool HW, bool GRAD>
+  static cudaError_t attr(size_t smem) {
+    return cudaFuncSetAttribute(k_lr<Q, LM, HW, GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  static cudaError_t prepare(size_t smem) {
+    cudaError_t e;
+    if ((e = attr<0, false, false>(smem)) || (e = attr<0, true, false>(smem)) || (e = attr<1, false, false>(smem)) ||
+        (e = attr<1, true, false>(smem)) || (e = attr<1, false, true>(smem)) || (e = attr<1, true, true>(smem)) ||
+        (e = attr<2, false, false>(smem)) || (e = attr<2, true, false>(smem)) || (e = attr<2, false, true>(smem)) ||
+        (e = attr<2, true, true>(smem)))
+      return e;
+    return cudaSuccess;
+  }
+  static cudaError_t occupancy(int* bps, int threads, size_t smem) {  // the heaviest variant (LSE + gradient)
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lr<Q, 1, false, true>, threads, smem);
+  }
+  // tensor-core variant
+  template <int LM, bool HW, bool GRAD>
+  static void go_t(const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
+    k_lrt<Q, LM, HW, GRAD><<<units, 32 * a.kw, smem, st>>>(a);
+  }
+  static void launch_t(int lm, bool hw, bool grad, const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
+    if (lm == 0) { hw ? go_t<0, true, false>(a, units, smem, st) : go_t<0, false, false>(a, units, smem, st); return; }
+    if (lm == 1) {
+      if (grad) hw ? go_t<1, true, true>(a, units, smem, st) : go_t<1, false, true>(a, units, smem, st);
+      else hw ? go_t<1, true, false>(a, units, smem, st) : go_t<1, false, false>(a, units, smem, st);
+      return;
+    }
+    if (grad) hw ? go_t<2, true, true>(a, units, smem, st) : go_t<2, false, true>(a, units, smem, st);
+    else hw ? go_t<2, true, false>(a, units, smem, st) : go_t<2, false, false>(a, units, smem, st);
+  }
+  template <int LM, bool HW, bool GRAD>
+  static cudaError_t attr_t(size_t smem) {
+    return cudaFuncSetAttribute(k_lrt<Q, LM, HW, GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  static cudaError_t prepare_t(size_t smem) {
+    cudaError_t e;
+    if ((e = attr_t<0, false, false>(smem)) || (e = attr_t<0, true, false>(smem)) || (e = attr_t<1, false, false>(smem)) ||
+        (e = attr_t<1, true, false>(smem)) || (e = attr_t<1, false, true>(smem)) || (e = attr_t<1, true, true>(smem)) ||
+        (e = attr_t<2, false, false>(smem)) || (e = attr_t<2, true, false>(smem)) || (e = attr_t<2, false, true>(smem)) ||
+        (e = attr_t<2, true, true>(smem)))
+      return e;
+    return cudaSuccess;
+  }
+  static cudaError_t occupancy_t(int* bps, int threads, size_t smem) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lrt<Q, 1, false, true>, threads, smem);
   }
 };
 
@@ -512,30 +564,55 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     ctx->QS = (ctx->Q + 3) & ~3;
     ctx->nch = (L + 31) / 32;
     ctx->LS = ctx->nch * 32;
-    const size_t lr_smem = sizeof(float) * (size_t)(cfg.K / 2 + 1) * ctx->QS;
-    cudaError_t e1 = cudaSuccess;
-    with_Q(ctx->Q, [&](auto Qc) { e1 = decltype(Qc)::occupancy(&ctx->lr_bps, lr_smem); });
-    cudaError_t e2 = cudaSuccess;
+    if (const char* ev = getenv("SQNGD_LR_TC")) ctx->lr_tc = ev[0] != '0';
+    ctx->nch16 = (L + 15) / 16;
+    const int Kp = cfg.K / 2;
+    ctx->NT = (Kp + 7) / 8;
+    ctx->NTF = Kp / 8;
+    ctx->units_lr = (int64_t)cfg.R * cfg.M * cfg.M * (ctx->lr_tc ? ctx->nch16 : ctx->nch);
+    // warps per unit (bin-pair split): the kw in {1, 2, 4, 8} whose CTAs fill whole waves best
+    const size_t cf_bytes = 0;  // coefficient tables are read through L1, not staged
+    const size_t rec_bytes = ctx->lr_tc ? sizeof(float) * 32 * 22 : sizeof(float) * 32 * (2 * ctx->Q + 4);
+    const size_t smem_max = cf_bytes + 8 * rec_bytes;
+    const int kmaxw = ctx->lr_tc ? ctx->NT : Kp;
+    cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+    double best = 1e30;
+    with_Q(ctx->Q, [&](auto Qc) {
+      using QC = decltype(Qc);
+      e1 = ctx->lr_tc ? QC::prepare_t(smem_max) : QC::prepare(smem_max);
+      for (int kw = 1; kw <= 8 && e1 == cudaSuccess; kw *= 2) {
+        if (kw > 1 && kw > kmaxw) break;
+        int bps = 0;
+        const size_t sm = cf_bytes + (kw > 1 ? kw * rec_bytes : 0);
+        e1 = ctx->lr_tc ? QC::occupancy_t(&bps, 32 * kw, sm) : QC::occupancy(&bps, 32 * kw, sm);
+        if (e1 != cudaSuccess || bps < 1) break;
+        const double waves = (double)ctx->units_lr / ((double)ctx->sms * bps);
+        const double warps_sm = (double)bps * kw;  // latency hiding: penalise < 20 resident warps
+        const double cost = std::ceil(waves) / waves * (warps_sm >= 20 ? 1.0 : 20.0 / warps_sm) * (1.0 + 0.01 * kw);
+        if (cost < best) {
+          best = cost;
+          ctx->kw = kw;
+          ctx->lr_smem = sm;
+        }
+      }
+    });
+    if (ctx->lr_tc) {  // measured (C3): one warp per unit is best for k_lrt (no CTA-level reduction)
+      ctx->kw = 1;
+      ctx->lr_smem = 0;
+    }
+    if (const char* ev = getenv("SQNGD_LR_KW")) {  // tuning override
+      const int kw = atoi(ev);
+      if (kw == 1 || kw == 2 || kw == 4 || kw == 8) {
+        ctx->kw = kw;
+        ctx->lr_smem = cf_bytes + (kw > 1 ? kw * rec_bytes : 0);
+      }
+    }
     with_P(P, [&](auto Lc) { e2 = decltype(Lc)::prepare_lr(); });
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
       std::string m = cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
       delete ctx;
       return fail(nullptr, SQNGD_E_CUDA, "sqngd_create: Chebyshev kernel setup", m.c_str());
     }
-    // k-split: the fewest parts whose warp units fill whole waves of resident warps best.
-    const int64_t u1 = (int64_t)cfg.R * cfg.M * cfg.M * ctx->nch;
-    const double resident = (double)ctx->sms * std::max(1, ctx->lr_bps) * 4.0;
-    const int kmax = std::max(1, std::min(32, cfg.K / 2));
-    double best = 1e30;
-    for (int kp = 1; kp <= kmax; ++kp) {
-      const double waves = (double)u1 * kp / resident;
-      const double cost = std::ceil(waves) / waves + 0.02 * (kp - 1);
-      if (cost < best - 1e-9) {
-        best = cost;
-        ctx->kparts = kp;
-      }
-    }
-    ctx->units_lr = u1 * ctx->kparts;
   }
 
   const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
@@ -609,6 +686,44 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     CK(cudaMemcpy(ctx->Vt, vt.data(), sizeof(float2) * vt.size(), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&ctx->coef, sizeof(float) * cf.size()));
     CK(cudaMemcpy(ctx->coef, cf.data(), sizeof(float) * cf.size(), cudaMemcpyHostToDevice));
+    {  // k_lrt B fragments: alpha / beta per (j, pair), TF32 hi + lo, in mma.sync m16n8k8 lane order
+      auto alpha = [&](int j, int p) -> double {
+        if (j >= QH || p >= Kp) return 0.0;
+        return 0.5 * (lr_ell[(size_t)p * Q + j] + lr_ell[(size_t)p * Q + Q - 1 - j]);
+      };
+      auto beta = [&](int j, int p) -> double {
+        if (j >= QH || p >= Kp) return 0.0;
+        return 0.5 * (lr_ell[(size_t)p * Q + j] - lr_ell[(size_t)p * Q + Q - 1 - j]);
+      };
+      auto tf32 = [](double x, float& hi, float& lo) {  // cvt.rna.tf32: round to nearest, ties away
+        float f = (float)x;
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        u = (u + 0x1000u) & 0xFFFFE000u;
+        std::memcpy(&hi, &u, 4);
+        lo = (float)(x - (double)hi);
+      };
+      auto frag = [&](double b0, double b1) {
+        float4 o;
+        tf32(b0, o.x, o.z);
+        tf32(b1, o.y, o.w);
+        return o;
+      };
+      std::vector<float4> tf((size_t)ctx->NT * 64), ta((size_t)ctx->NT * 64);
+      for (int t = 0; t < ctx->NT; ++t)
+        for (int ln = 0; ln < 32; ++ln) {
+          const int gg = ln >> 2, cc = ln & 3;
+          const size_t o = ((size_t)t * 32 + ln) * 2;
+          tf[o] = frag(alpha(cc, 8 * t + gg), alpha(cc + 4, 8 * t + gg));
+          tf[o + 1] = frag(beta(cc, 8 * t + gg), beta(cc + 4, 8 * t + gg));
+          ta[o] = frag(alpha(gg, 8 * t + 2 * cc), alpha(gg, 8 * t + 2 * cc + 1));
+          ta[o + 1] = frag(beta(gg, 8 * t + 2 * cc), beta(gg, 8 * t + 2 * cc + 1));
+        }
+      CK(cudaMalloc(&ctx->tabF, sizeof(float4) * tf.size()));
+      CK(cudaMemcpy(ctx->tabF, tf.data(), sizeof(float4) * tf.size(), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&ctx->tabA, sizeof(float4) * ta.size()));
+      CK(cudaMemcpy(ctx->tabA, ta.data(), sizeof(float4) * ta.size(), cudaMemcpyHostToDevice));
+    }
     std::vector<float> wm((size_t)L, 1.f);
     if (cfg.weights) {
       std::vector<float> wts((size_t)cfg.K * L);
@@ -623,7 +738,13 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     CK(cudaMemcpy(ctx->wmax, wm.data(), sizeof(float) * L, cudaMemcpyHostToDevice));
     const size_t pairs = (size_t)cfg.R * cfg.M * cfg.M;
     CK(cudaMalloc(&ctx->Rn, sizeof(float2) * pairs * Q * ctx->LS));
-    CK(cudaMalloc(&ctx->Gn, sizeof(float2) * (size_t)ctx->kparts * pairs * Q * ctx->LS));
+    CK(cudaMalloc(&ctx->Gn, sizeof(float2) * pairs * Q * ctx->LS));
+    CK(cudaMalloc(&ctx->lred, sizeof(LrRed) * cfg.R));
+    CK(cudaMalloc(&ctx->lr_cnt, sizeof(int) * (size_t)cfg.R * cfg.M * Q));
+    CK(cudaMemset(ctx->lr_cnt, 0, sizeof(int) * (size_t)cfg.R * cfg.M * Q));
+    CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     CK(cudaMalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ((cfg.N + 1) & ~1)));
   }
 
@@ -656,10 +777,13 @@ void sqngd_destroy(sqngd_ctx ctx) {
   void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   ctx->comm.destroy();
   delete ctx;
 }
@@ -775,30 +899,47 @@ static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad
 
 // Chebyshev engine, forward part: node AFs (k_node) and the fused contraction / epilogue (k_lr),
 // then the per-restart reduction (keys, shift, S, unit scales, metrics).
-static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, const MetricsArgs& ma, cudaStream_t st) {
+static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, const MetricsArgs& ma, cudaStream_t st,
+                           bool fork) {
   const sqngd_config& c = ctx->cfg;
   const int node_units = c.R * c.M * c.M * ctx->Q;
   with_P(ctx->P, [&](auto Lc) {
-    decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftw, ctx->Rn, st);
+    decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftw, ctx->Rn, c.R, ctx->lred, st);
   });
   LrArgs a{};
-  a.R = c.R; a.M = c.M; a.N = c.N; a.L = ctx->L; a.K = c.K; a.nch = ctx->nch; a.kparts = ctx->kparts;
+  a.R = c.R; a.M = c.M; a.N = c.N; a.L = ctx->L; a.K = c.K; a.nch = ctx->nch; a.kw = ctx->kw;
   a.LS = ctx->LS; a.QS = ctx->QS;
   a.tau_lo = c.tau_lo; a.tau_hi = c.tau_hi; a.excl0 = c.exclude_auto_zero_delay;
   a.bp = (float)c.beta_or_p; a.invN = 1.0f / (float)c.N;
   a.weights = c.weights; a.wmax = ctx->wmax; a.coef = ctx->coef; a.Rn = ctx->Rn; a.Gn = ctx->Gn;
-  a.af_mag = grad ? nullptr : af_mag; a.part = ctx->part;
-  const size_t smem = sizeof(float) * (size_t)(c.K / 2 + 1) * ctx->QS;
-  const int units = (int)ctx->units_lr;
-  {
+  a.af_mag = grad ? nullptr : af_mag; a.part = ctx->part; a.lred = ctx->lred;
+  if (ctx->lr_tc) {
+    LrtArgs t{};
+    t.R = c.R; t.M = c.M; t.N = c.N; t.L = ctx->L; t.K = c.K; t.nch = ctx->nch16; t.kw = ctx->kw; t.LS = ctx->LS;
+    t.NT = ctx->NT; t.NTF = ctx->NTF; t.coefm = ctx->coef + (size_t)(c.K / 2) * ctx->QS;
+    t.tau_lo = c.tau_lo; t.tau_hi = c.tau_hi; t.excl0 = c.exclude_auto_zero_delay;
+    t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
+    t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
+    t.af_mag = grad ? nullptr : af_mag; t.part = ctx->part; t.lred = ctx->lred;
     ProfScope ps(ctx, cls, st);
     with_Q(ctx->Q, [&](auto Qc) {
-      decltype(Qc)::launch(c.loss_mode, c.weights != nullptr, grad, a, units, smem, st);
+      decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad, t, (int)ctx->units_lr, ctx->lr_smem, st);
+    });
+  } else {
+    ProfScope ps(ctx, cls, st);
+    with_Q(ctx->Q, [&](auto Qc) {
+      decltype(Qc)::launch(c.loss_mode, c.weights != nullptr, grad, a, (int)ctx->units_lr, ctx->lr_smem, st);
     });
   }
   const int GPR = (int)(ctx->units_lr / c.R);
-  k_reduce_groups<<<c.R, 1024, 0, st>>>(GPR, 0, (int)ctx->units_lr, c.loss_mode, c.beta_or_p, ctx->part, ctx->red,
-                                        ma, ctx->status);
+  cudaStream_t fs = st;
+  if (fork) {  // k_lr_finish runs beside the adjoint kernels; run_loss_grad joins before the combine
+    CK(cudaEventRecord(ctx->ev_fork, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    fs = ctx->side;
+  }
+  k_lr_finish<<<c.R, 1024, 0, fs>>>(GPR, c.loss_mode, c.beta_or_p, ctx->part, ctx->lred, ctx->red, ma, ctx->status);
+  if (fork) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   ctx->launches += 3;
   return launch_check(ctx, "chebyshev forward");
 }
@@ -815,7 +956,7 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
                  ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
-  if (ctx->lr) return run_lr(ctx, false, MODE_FWD, af_mag, ma, st);
+  if (ctx->lr) return run_lr(ctx, false, MODE_FWD, af_mag, ma, st, false);
   cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
   {
     ProfScope ps(ctx, MODE_FWD, st);
@@ -874,12 +1015,13 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     return launch_check(ctx, "sparse adjoint");
   }
   if (ctx->lr) {  // Chebyshev engine (single GPU)
-    if ((rc = run_lr(ctx, true, wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B, nullptr, ma, st))) return rc;
+    if ((rc = run_lr(ctx, true, wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B, nullptr, ma, st, true))) return rc;
     AdjGArgs ag{};
-    ag.M = c.M; ag.N = c.N; ag.Q = ctx->Q; ag.LS = ctx->LS; ag.nch = ctx->nch; ag.kparts = ctx->kparts;
-    ag.units = c.R * c.M * c.M * ctx->Q;
-    ag.gstride = (size_t)c.R * c.M * c.M * ctx->Q * ctx->LS;
-    ag.Gn = ctx->Gn; ag.scale = ctx->part.scale; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
+    ag.M = c.M; ag.N = c.N; ag.Q = ctx->Q; ag.LS = ctx->LS;
+    ag.nch = ctx->lr_tc ? ctx->nch16 : ctx->nch; ag.csh = ctx->lr_tc ? 4 : 5;
+    ag.units = c.R * c.M * c.M * ctx->Q; ag.mode = c.loss_mode; ag.bp = (float)c.beta_or_p;
+    ag.Gn = ctx->Gn; ag.um = ctx->part.m; ag.lred = ctx->lred; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
+    ag.cnt = ctx->lr_cnt; ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
     with_P(ctx->P, [&](auto Lc) { decltype(Lc)::adj_g(wrt, ag, ctx->ftw, st); });
     CombineArgs ca{};
     ca.M = c.M; ca.N = c.N; ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.red = ctx->red;
@@ -887,16 +1029,15 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     ca.part = ctx->part;
     ca.part.scale = nullptr;  // node cotangents were rescaled in k_adj_g
     if (wrt == SQNGD_WRT_TRANSMIT) {
-      const int tu = c.R * c.M * ctx->Q;
-      with_P(ctx->P, [&](auto Lc) {
-        decltype(Lc)::lrB_tail(tu, c.M, ctx->Q, c.N, (c.N + 1) & ~1, ctx->part.g, ctx->Vt, ctx->ftw, ctx->tslot, st);
-      });
+      const int tu = c.R * c.M * ctx->Q;  // (k_adj_g's last group per node did k_lrB_tail's work)
+      CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // S and the metrics from k_lr_finish
       ca.K = ctx->Q; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = 0; ca.u_hi = tu; ca.part.g = ctx->tslot;
       ca.len = c.N; ca.extra = 1.0; ca.fin = 1; ca.out = nullptr;
       k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
       ctx->launches += 3;
       return launch_check(ctx, "chebyshev adjoint (transmit)");
     }
+    CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     ca.K = c.M * ctx->Q; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * c.M * ctx->Q;
     ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
     k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
