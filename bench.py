@@ -41,24 +41,38 @@ def fft_flops(P):
 
 
 def work_model(c):
-    """Algorithmic FP32 flops per launch of each fused kernel,
-    per restart: 5 P log2 P per complex FFT, 6 per complex multiply, 7 / 10 per cell."""
+    """Algorithmic FP32 flops per launch of each fused kernel of the per-bin FFT engine
+    (SURVEY.md §8(d)), per restart: 5 P log2 P per complex FFT, 6 per complex multiply, 7 / 10
+    per cell.  The Doppler-modulated FFTs X = FFT(s e^{j2pi nf/N}) (K M of them) are done by
+    k_xhat, not by the fused kernel, so they are not counted in its launch."""
     M, N, K, P = c.M, c.N, c.K, c.P
     cells = c.cells
     F = fft_flops(P)
-    fwd_body = K * (M * (6 * N + F) + M * M * (6 * P + F)) + 7 * cells      # F_fwd minus the filter FFTs
-    F_A = 10 * cells + K * M * M * (F + 8 * P) + M * F
+    fwd_body = K * M * M * (6 * P + F) + 7 * cells      # slices: cross-spectrum + IFFT + cell epilogue
+    F_A = 10 * cells + K * M * M * (F + 8 * P)
     F_B = 10 * cells + K * (M * M * (F + 8 * P) + M * (F + 6 * N))
     return {"fwd": fwd_body * c.R, "adjA": (fwd_body + F_A) * c.R, "adjB": (fwd_body + F_B) * c.R,
             "filter": M * F * c.R, "cells": cells * c.R}
 
 
-def traffic_bytes(kind):
+def work_model_lr(c, Q):
+    """Algorithmic flops per launch of the Chebyshev engine's fused kernel k_lrt:
+    per bin pair and lag, the symmetric contraction Pe = sum_{j<Q/2} alpha_j E_j, Po = sum beta_j O_j
+    (2 x Q/2 complex-by-real MACs = 4Q flops) and At = Pe +/- Po (4); the adjoint the same
+    (4Q + 4); the cell epilogue 7 (forward) / 10 (adjoint) per cell as in SURVEY.md §8(d).
+    Per cell: forward 2Q + 2 + 7, with gradient 4Q + 4 + 17."""
+    cells = c.cells * c.R
+    fwd = cells * (2 * Q + 2 + 7)
+    grad = cells * (4 * Q + 4 + 17)
+    return {"fwd": fwd, "adjA": grad, "adjB": grad, "cells": cells}
+
+
+def traffic_bytes(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
-    capture of this round (profiles/), or None."""
+    capture (profiles/traffic.json), or None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["dram_bytes_per_launch"]
-        return d.get({"adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>", "fwd": "k_af<FWD>"}[kind])
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["dram_bytes_per_launch"]
+        return d.get(kernel)
     except Exception:
         return None
 
@@ -244,68 +258,92 @@ def main():
     # a non-default stream: sqngd_step captures itself into a CUDA graph there and replays it
     side = torch.cuda.Stream(dev)
     torch.cuda.set_stream(side)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     # inputs: this rank's restarts r = rank*R .. (independent seeded problems)
     R = c.R
     z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, g), c.M * c.N).reshape(c.M, c.N)
                   for g in parallel.restart_ids(R, rank)])
     rho = inputs.init_thresholds(R, c.B, c.r_n)
-    ctx = sqngd.Context(c, device=local)
-    zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
-    q = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)
-    st = ctx.new_state(zt, rt, q["s_hard"])                    # w = s_hard (matched start, Q3)
-    hist = torch.zeros((R, c.n_h + c.n_x), dtype=torch.float64, device=dev)
-    hard = torch.empty(R * sqngd.METRICS_BYTES, dtype=torch.uint8, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    for _ in range(args.warmup):
-        ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
-    ctx.sync()
-
-    ctx.profile_read(reset=True)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        t_wall = time.perf_counter()
-        for i in range(args.steps):
-            flush.fill_(float(i))                                   # evict L2 between steps
-            evs[i][0].record(stream)
-            ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
-            evs[i][1].record(stream)
-        torch.cuda.synchronize(dev)
-        t_wall = time.perf_counter() - t_wall
-    if dist:
-        dist.barrier()
-    ctx.sync()
-    launches = ctx.profile_read(reset=True)["launches"]
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    # per-kernel times: a profiled pass over the same K steps, launched eagerly (CUDA events
-    # recorded on the launch stream around every fused kernel; graph replay cannot be timed so)
-    ctx.profile(True)
-    for i in range(args.steps):
-        flush.fill_(float(i))
-        ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
-    ctx.sync()
-    prof = ctx.profile_read(reset=True)
-    ctx.profile(False)
-    prof_step_ms = None
-    tot_ms = sum(step_ms)
-    tot_ms = parallel.max_over_ranks(tot_ms)
     evals_per_step = (c.n_h + c.n_x) * R * world
-    value = evals_per_step * args.steps / (tot_ms / 1e3)
-
-    # ---- roofline of the dominant fused kernel (live CUDA events on the launch stream)
-    wm = work_model(c)
-    names = ["fwd", "adjA", "adjB"]
-    dom = max(range(3), key=lambda i: prof["ms"][i])
-    avg_ms = prof["ms"][dom] / max(1, prof["count"][dom])
-    achieved = wm[names[dom]] / (avg_ms / 1e3) / 1e12
     sm_mhz, _, src = peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = sms * 128 * 2 * sm_mhz * 1e6 / 1e12
-    clocks = clk.summary()
+
+    def timed(cc, with_clocks):
+        """W warm-up + K timed sqngd_step(A+B) calls (CUDA-graph replay), then an eager profiled
+        pass over K more steps for the per-kernel CUDA-event times."""
+        ctx = sqngd.Context(cc, device=local)
+        zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
+        q = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)
+        st = ctx.new_state(zt, rt, q["s_hard"])                    # w = s_hard (matched start, Q3)
+        hist = torch.zeros((R, c.n_h + c.n_x), dtype=torch.float64, device=dev)
+        hard = torch.empty(R * sqngd.METRICS_BYTES, dtype=torch.uint8, device=dev)
+        for _ in range(args.warmup):
+            ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+        ctx.sync()
+        ctx.profile_read(reset=True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with ClockSampler(local) as clk:
+            t_wall = time.perf_counter()
+            for i in range(args.steps):
+                flush.fill_(float(i))                                   # evict L2 between steps
+                evs[i][0].record(stream)
+                ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+                evs[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+            t_wall = time.perf_counter() - t_wall
+        if dist:
+            dist.barrier()
+        ctx.sync()
+        launches = ctx.profile_read(reset=True)["launches"]
+        tot_ms = parallel.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs))
+        # per-kernel times: an eager pass over the same K steps (CUDA events recorded on the launch
+        # stream around every fused kernel; graph replay cannot be timed per kernel)
+        ctx.profile(True)
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+        ctx.sync()
+        prof = ctx.profile_read(reset=True)
+        ctx.profile(False)
+        info = ctx.engine_info()
+        value = evals_per_step * args.steps / (tot_ms / 1e3)
+        names = ["fwd", "adjA", "adjB"]
+        if info["engine"] == "chebyshev":
+            wm = work_model_lr(cc, info["Q"])
+            knames = {"fwd": "k_lrt<FWD>", "adjA": "k_lrt<ADJ>", "adjB": "k_lrt<ADJ>"}
+        else:
+            wm = work_model(cc)
+            knames = {"fwd": "k_af<FWD>", "adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>"}
+        dom = max(range(3), key=lambda i: prof["ms"][i])
+        avg_ms = prof["ms"][dom] / max(1, prof["count"][dom])
+        achieved = wm[names[dom]] / (avg_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "kernel": knames[names[dom]], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic_bytes(knames[names[dom]]), "avg_launch_ms": avg_ms,
+                "launches": prof["count"][dom], "flops_per_launch": wm[names[dom]],
+                "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
+                "share_of_step": prof["ms"][dom] / tot_ms,
+                "timing": "CUDA events around each fused-kernel launch on its stream, in an eager pass over the "
+                          "same K steps right after the timed (CUDA-graph) region"}
+        out = {"value": value, "ms_per_step": tot_ms / args.steps, "roofline": roof, "launches": launches,
+               "kernel_ms": {n: prof["ms"][i] / args.steps for i, n in enumerate(names)}, "engine": info,
+               "wall_s": t_wall}
+        if with_clocks:
+            out["clocks"] = clk.summary()
+        return ctx, st, hist, hard, out
+
+    # headline: the library's default engine for this config (AUTO: Chebyshev nodes on the paper's
+    # narrow Doppler grid); then the per-bin FFT engine on the same inputs, reported beside it
+    ctx, st, hist, hard, main_run = timed(c, True)
+    fft_run = None
+    if main_run["engine"]["engine"] != "fft":
+        ctxf, *_rest, fft_run = timed(c.with_(doppler_engine=sqngd.ENGINE_FFT), False)
+        ctxf.close()
+    value, tot_ms = main_run["value"], main_run["ms_per_step"] * args.steps
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the timing
     keys = ["z", "rho", "w", "m_z", "v_z", "m_rho", "v_rho", "m_w", "v_w"]
@@ -334,28 +372,29 @@ def main():
     e2e_ms = parallel.max_over_ranks(e2e_ms)
     e2e_value = evals_per_step * args.steps / (e2e_ms / 1e3)
     hm = sqngd.metrics_from_bytes(host_hard.numpy())
+    eng = main_run["engine"]
+    eng_desc = (f"chebyshev (Q={eng['Q']} nodes, |A| interpolation bound {eng['err_bound']:.1e} x N)"
+                if eng["engine"] == "chebyshev" else "fft (one modulated FFT correlation per Doppler bin)")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {**config_dict(c), "parallelism": f"restarts x{world} (independent, no collective)"},
+        "config": {**config_dict(c), "doppler_engine": eng_desc,
+                   "parallelism": f"restarts x{world} (independent, no collective)"},
         "cells_per_s": value * c.cells / c.R,
-        "roofline": {"bound": "alu", "kernel": {"fwd": "k_af<FWD>", "adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>"}[names[dom]],
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic_bytes(names[dom]), "avg_launch_ms": avg_ms, "launches": prof["count"][dom],
-                     "flops_per_launch": wm[names[dom]],
-                     "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
-                     "share_of_step": prof["ms"][dom] / tot_ms,
-                     "timing": "CUDA events around each fused-kernel launch on its stream, in an eager pass "
-                               "over the same K steps right after the timed (CUDA-graph) region"},
-        "kernel_ms": {n: prof["ms"][i] / args.steps for i, n in enumerate(names)},
-        "gpu_launches": launches,
-        "clocks": clocks,
+        "roofline": main_run["roofline"],
+        "kernel_ms": main_run["kernel_ms"],
+        "gpu_launches": main_run["launches"],
+        "clocks": main_run["clocks"],
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "wall_s": t_wall,
+        "wall_s": main_run["wall_s"],
         "final_hard_pslr_db": 20 * math.log10(max(hm[0]["wpsl"], 1e-30)),
     }
+    if fft_run is not None:
+        line["fft_engine"] = {"value": fft_run["value"], "unit": UNIT, "ms_per_step": fft_run["ms_per_step"],
+                              "cells_per_s": fft_run["value"] * c.cells / c.R, "roofline": fft_run["roofline"],
+                              "kernel_ms": fft_run["kernel_ms"], "gpu_launches": fft_run["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OMP_NUM_THREADS", str(cpu_info()))
         per_eval, nb = oracle_sample(c, budget_s=10.0)

@@ -13,7 +13,8 @@ from paper_2604_25728_b200 import inputs, sqngd  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-c = CF.CONFIGS[name].with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0)
+c = CF.CONFIGS[name].with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0,
+                           doppler_engine={"fft": 1, "cheb": 2}.get(os.environ.get("SQNGD_ENGINE", ""), 0))
 z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, r), c.M * c.N).reshape(c.M, c.N) for r in range(c.R)])
 rho = inputs.init_thresholds(c.R, c.B, c.r_n)
 ctx = sqngd.Context(c)
