@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (live && q < a.len) {
     const int klo = max(0, a.u_lo - ra * a.K), khi = min(a.K, a.u_hi - ra * a.K);
-#pragma unroll 4
+#pragma unroll 8
     for (int k = klo + kl; k < khi; k += 8) {
       const int u = ra * a.K + k;
       const float sc = a.part.scale ? __ldg(a.part.scale + u) : 1.f;  // null: slots pre-scaled (Chebyshev engine)
@@ -475,9 +475,24 @@ __global__ void __launch_bounds__(PL::T* G)
 // outside |c (z - rho)| < 12 where it is < 1.6e-10: per element, a warp whose 32 (sorted)
 // thresholds all lie farther than 12/c from z skips it (warp-uniform test), so only the
 // ~2 x 12/c x B r_n thresholds near each z do the work.
+// Finishing work done by last-arriving blocks (arrival counters, self-resetting; fixed-order sums):
+//   per (r, threshold block): grad_rho[i] = coef * sum_ch part[ch][i]  (when gsum != nullptr);
+//   per (r, element chunk):   Adam on the chunk's z (when zad.z != nullptr) -- after every
+//                             threshold block has read that chunk's old z.
+struct RhoFinish {
+  float coef;
+  float* gsum;      // [R][BR] or nullptr
+  int* cnt_tb;      // [R][gridDim.x]
+  int* cnt_ch;      // [R][gridDim.y]
+  float *z, *mz, *vz;
+  const float* gz;  // grad_z [R][MN]
+  AdamP ap;
+  const int* status;
+};
+
 __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
                                                        const float* __restrict__ rho, const float* __restrict__ dy,
-                                                       float* part) {
+                                                       float* part, RhoFinish fin) {
   __shared__ __align__(16) float2 zd[1024];  // chunk <= 1024: (z, dy), padded to a multiple of 4
   const int r = blockIdx.z;
   const int ch = blockIdx.y;
@@ -517,15 +532,43 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
     }
   }
   if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
-}
-
-__global__ void k_grad_rho_sum(int BR, int nchunk, float coef, const float* __restrict__ part, float* grad_rho) {
-  const int r = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= BR) return;
-  float acc = 0.f;
-  for (int ch = 0; ch < nchunk; ++ch) acc += part[((size_t)r * nchunk + ch) * BR + i];
-  grad_rho[(size_t)r * BR + i] = coef * acc;
+  if (!fin.gsum && !fin.z) return;
+  __shared__ int last_tb, last_ch;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last_tb = last_ch = 0;
+    if (fin.gsum) {
+      int* ct = fin.cnt_tb + (size_t)r * gridDim.x + blockIdx.x;
+      if (atomicAdd(ct, 1) == (int)gridDim.y - 1) { last_tb = 1; *ct = 0; }
+    }
+    if (fin.z) {
+      int* cc = fin.cnt_ch + (size_t)r * gridDim.y + ch;
+      if (atomicAdd(cc, 1) == (int)gridDim.x - 1) { last_ch = 1; *cc = 0; }
+    }
+  }
+  __syncthreads();
+  if (last_tb && i < BR) {  // fixed-order sum of this threshold's chunk partials
+    __threadfence();
+    float g = 0.f;
+    const float* pp = part + (size_t)r * gridDim.y * BR + i;
+#pragma unroll 8
+    for (int k = 0; k < (int)gridDim.y; ++k) g += __ldcg(pp + (size_t)k * BR);
+    fin.gsum[(size_t)r * BR + i] = fin.coef * g;
+  }
+  if (last_ch && !(*fin.status & ST_NONFINITE)) {  // Adam on this chunk's z (keep the last finite iterate)
+    float c1, c2;
+    fin.ap.corr(c1, c2);
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const size_t j = (size_t)r * MN + e;
+      const float gi = fin.gz[j];
+      const float mi = fin.ap.b1 * fin.mz[j] + (1.f - fin.ap.b1) * gi;
+      const float vi = fin.ap.b2 * fin.vz[j] + (1.f - fin.ap.b2) * gi * gi;
+      fin.mz[j] = mi;
+      fin.vz[j] = vi;
+      fin.z[j] -= fin.ap.lr * (mi / c1) / (sqrtf(vi / c2) + fin.ap.eps);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ a9 optimizer

@@ -61,6 +61,7 @@ struct sqngd_ctx_s {
   float2* H = nullptr;      // [R][M][P] filter spectra / P
   float2* Xc = nullptr;     // [R][M][K][P] X cache: FFT_P of the Doppler-modulated codes (a3)
   float2* ftw = nullptr;    // Stockham twiddle table of the plan
+  float2* ftwr = nullptr;   // twiddle table of the row kernels' plan (Launch::PLR)
   float2* s_soft = nullptr; // [R][M][N]
   float2* s_hard = nullptr;
   float* dq = nullptr;      // [R][M][N]
@@ -72,6 +73,7 @@ struct sqngd_ctx_s {
   float* dy = nullptr;         // [R][M][N]
   float* rho_part = nullptr;   // [R][nchunk][BR]
   int rho_chunk = 256, rho_nchunk = 1;
+  int* rho_cnt = nullptr;      // [R][64] threshold-block + [R][nchunk] element-chunk arrival counters
   float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
   float* gz = nullptr;         // [R][M][N]
   float* grho = nullptr;       // [R][BR]
@@ -171,6 +173,18 @@ struct Launch {
   static constexpr int G = plan_G(P);
   static constexpr int MINB = plan_MINB(P);
   static constexpr int THREADS = PL::T * G;
+  // latency-bound row kernels (one transform per filter row, few rows): 8 elements per thread,
+  // twice the threads per transform (measured: the E = 16 row kernel runs one warp per SMSP)
+  static constexpr int ER = P <= 8 ? P : 8;
+  using PLR = Plan<P, ER>;
+  static constexpr int GR = (P / ER) >= 128 ? 1 : 128 / (P / ER);
+  static constexpr int THREADS_R = PLR::T * GR;
+  static size_t smem_r() { return (size_t)GR * FftSmem<PLR>::TOTAL * sizeof(float2) + 16; }
+  static std::vector<float2> twiddles_r() {
+    std::vector<float2> t(PLR::TWSIZE, make_float2(1.f, 0.f));
+    build_twiddle_table<PLR>(t.data());
+    return t;
+  }
 
   template <int MODE>
   static size_t smem() { return (size_t)G * GroupSmem<PL, MODE>::TOTAL * sizeof(float2); }
@@ -190,9 +204,9 @@ struct Launch {
     if (e) return e;
     e = cudaFuncSetAttribute(k_rows_ifft<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
     if (e) return e;
-    e = cudaFuncSetAttribute(k_rows_ifft_fin<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+    e = cudaFuncSetAttribute(k_rows_ifft_fin<PLR, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r());
     if (e) return e;
-    e = cudaFuncSetAttribute(k_rows_adam_w<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+    e = cudaFuncSetAttribute(k_rows_adam_w<PLR, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r());
     if (e) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[0], k_af<PL, G, MINB, MODE_FWD>, THREADS, smem<MODE_FWD>());
     if (e) return e;
@@ -219,15 +233,15 @@ struct Launch {
     const int blocks = (rows + G - 1) / G;
     k_rows_ifft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, N, in, ftw, out);
   }
-  static void rows_adam_w(int rows, const float2* in, const float2* ftw, const FinArgs& f, const AdamP& ap,
+  static void rows_adam_w(int rows, const float2* in, const float2* ftwr, const FinArgs& f, const AdamP& ap,
                           float2* w, float* mw, float* vw, float2* H, double2* cm, int* status, cudaStream_t st) {
-    const int blocks = (rows + G - 1) / G;
-    k_rows_adam_w<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, in, ftw, f, ap, w, mw, vw, H, cm, status);
+    const int blocks = (rows + GR - 1) / GR;
+    k_rows_adam_w<PLR, GR><<<blocks, THREADS_R, smem_r(), st>>>(rows, in, ftwr, f, ap, w, mw, vw, H, cm, status);
   }
-  static void rows_ifft_fin(int rows, const float2* in, const float2* ftw, const FinArgs& f, int* status,
+  static void rows_ifft_fin(int rows, const float2* in, const float2* ftwr, const FinArgs& f, int* status,
                             cudaStream_t st) {
-    const int blocks = (rows + G - 1) / G;
-    k_rows_ifft_fin<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, in, ftw, f, status);
+    const int blocks = (rows + GR - 1) / GR;
+    k_rows_ifft_fin<PLR, GR><<<blocks, THREADS_R, smem_r(), st>>>(rows, in, ftwr, f, status);
   }
   static void af(int mode, const KP& kp, int64_t slots, const float2* Xc, const float2* H, const float2* tw,
                  const float2* ftw, float* af_mag, const Part& part, cudaStream_t st) {
@@ -518,12 +532,13 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, cuda_device));
   int bps[3] = {1, 1, 1}, G = 1;
   cudaError_t perr = cudaSuccess;
-  std::vector<float2> ftw_host;
+  std::vector<float2> ftw_host, ftwr_host;
   bool okP = with_P(P, [&](auto Lc) {
     using LC = decltype(Lc);
     perr = LC::prepare(bps);
     G = LC::groups_per_block();
     ftw_host = LC::twiddles();
+    ftwr_host = LC::twiddles_r();
   });
   if (!okP) {
     delete ctx;
@@ -621,6 +636,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * cfg.K * P));
   CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->ftwr, sizeof(float2) * ftwr_host.size()));
+  CK(cudaMemcpy(ctx->ftwr, ftwr_host.data(), sizeof(float2) * ftwr_host.size(), cudaMemcpyHostToDevice));
   const int64_t uslots = std::max(ctx->units, ctx->units_lr);
   const int64_t gslots = std::max(ctx->units, ctx->lr ? (int64_t)cfg.R * cfg.M * cfg.M * ctx->Q : (int64_t)0);
   CK(cudaMalloc(&ctx->part.scale, sizeof(float) * uslots));
@@ -642,6 +659,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->dy, sizeof(float) * RMN));
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
+  CK(cudaMalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (64 + ctx->rho_nchunk)));
+  CK(cudaMemset(ctx->rho_cnt, 0, sizeof(int) * (size_t)cfg.R * (64 + ctx->rho_nchunk)));
   CK(cudaMalloc(&ctx->gw, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->gz, sizeof(float) * RMN));
   CK(cudaMalloc(&ctx->grho, sizeof(float) * (size_t)cfg.R * ctx->BR));
@@ -777,7 +796,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
   void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1043,11 +1062,11 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
     if (tail) {
       with_P(ctx->P, [&](auto Lc) {
-        decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftw, fa, tail->ap, tail->w, tail->mw, tail->vw, ctx->H,
+        decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftwr, fa, tail->ap, tail->w, tail->mw, tail->vw, ctx->H,
                                   ctx->cm, ctx->status, st);
       });
     } else {
-      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftw, fa, ctx->status, st); });
+      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftwr, fa, ctx->status, st); });
     }
     ctx->launches += 3;
     return launch_check(ctx, "chebyshev adjoint (filters)");
@@ -1083,11 +1102,11 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
       k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
       if (tail) {  // + Adam(w), Pi_H, next H = FFT(w)/P and c_m, in the same row kernel
         with_P(ctx->P, [&](auto Lc) {
-          decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftw, fa, tail->ap, tail->w, tail->mw, tail->vw,
+          decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftwr, fa, tail->ap, tail->w, tail->mw, tail->vw,
                                     ctx->H, ctx->cm, ctx->status, st);
         });
       } else {
-        with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftw, fa, ctx->status, st); });
+        with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftwr, fa, ctx->status, st); });
       }
       ctx->launches += 2;
     }
@@ -1116,11 +1135,11 @@ static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho
   const sqngd_config& c = ctx->cfg;
   const int MN = c.M * c.N;
   dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
-  k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part);
-  dim3 g2((ctx->BR + 127) / 128, c.R);
-  const float coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
-  k_grad_rho_sum<<<g2, 128, 0, st>>>(ctx->BR, ctx->rho_nchunk, coef, ctx->rho_part, grad_rho);
-  ctx->launches += 2;
+  RhoFinish fin{};
+  fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
+  fin.gsum = grad_rho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64; fin.status = ctx->status;
+  k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
+  ctx->launches += 1;
   return launch_check(ctx, "grad rho");
 }
 
@@ -1246,12 +1265,16 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
         return rc;
       {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
         dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);
+        RhoFinish fin{};  // grad_rho sums and Adam(z) by last-arriving blocks
+        fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
+        fin.gsum = ctx->grho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64;
+        fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
+        fin.status = ctx->status;
         k_grad_rho_part<<<g1, 256, 0, st>>>(c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy,
-                                            ctx->rho_part);
-        const ZAdam za{stt->z, stt->m_z, stt->v_z, ctx->gz, c.M * c.N, ctx->rho_part, ctx->rho_nchunk,
-                       (float)(-(1.0 / (2.0 * c.B)) * c.c)};
+                                            ctx->rho_part, fin);
+        const ZAdam za{nullptr, nullptr, nullptr, nullptr, c.M * c.N, nullptr, 0, 0.f};
         k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
-                                                                      nullptr, ap(c.lr_z, 1, i), 1e-4f, 1.0f - 1e-4f,
+                                                                      ctx->grho, ap(c.lr_z, 1, i), 1e-4f, 1.0f - 1e-4f,
                                                                       1e-6f, ctx->status, za);
         ctx->launches += 2;
       }
