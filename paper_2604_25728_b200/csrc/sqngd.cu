@@ -62,6 +62,7 @@ struct sqngd_ctx_s {
   float2* Xc = nullptr;     // [R][M][K][P] X cache: FFT_P of the Doppler-modulated codes (a3)
   float2* ftw = nullptr;    // Stockham twiddle table of the plan
   float2* ftwr = nullptr;   // twiddle table of the row kernels' plan (Launch::PLR)
+  float2* ftwn = nullptr;   // twiddle table of the Chebyshev node kernels' plan (Launch::PLN)
   float2* s_soft = nullptr; // [R][M][N]
   float2* s_hard = nullptr;
   float* dq = nullptr;      // [R][M][N]
@@ -175,6 +176,21 @@ struct Launch {
   static constexpr int THREADS = PL::T * G;
   // latency-bound row kernels (one transform per filter row, few rows): 8 elements per thread,
   // twice the threads per transform (measured: the E = 16 row kernel runs one warp per SMSP)
+#ifndef SQNGD_EN
+#define SQNGD_EN 16
+#endif
+  // Chebyshev engine node kernels (k_node, k_adj_g, node k_xhat): few hundred units per launch
+  static constexpr int EN = P <= SQNGD_EN ? P : SQNGD_EN;
+  using PLN = Plan<P, EN>;
+  static constexpr int GN = (P / EN) >= 128 ? 1 : 128 / (P / EN);
+  static constexpr int THREADS_N = PLN::T * GN;
+  static constexpr int MINBN = (P / EN) * GN >= 512 ? 1 : (P / EN) * GN >= 256 ? 2 : 3;
+  static size_t smem_n() { return (size_t)GN * FftSmem<PLN>::TOTAL * sizeof(float2) + 16; }
+  static std::vector<float2> twiddles_n() {
+    std::vector<float2> t(PLN::TWSIZE, make_float2(1.f, 0.f));
+    build_twiddle_table<PLN>(t.data());
+    return t;
+  }
   static constexpr int ER = P <= 8 ? P : 8;
   using PLR = Plan<P, ER>;
   static constexpr int GR = (P / ER) >= 128 ? 1 : 128 / (P / ER);
@@ -229,6 +245,11 @@ struct Launch {
     const int blocks = (units + G - 1) / G;
     k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(units, M, N, K, s, dtw, ftw, Xc, w, cm);
   }
+  static void xhat_n(int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftwn,
+                     float2* Xc, const float2* w, double2* cm, cudaStream_t st) {
+    const int blocks = (units + GN - 1) / GN;
+    k_xhat<PLN, GN, MINBN><<<blocks, THREADS_N, smem_n(), st>>>(units, M, N, K, s, dtw, ftwn, Xc, w, cm);
+  }
   static void rows_ifft(int rows, int N, const float2* in, const float2* ftw, float2* out, cudaStream_t st) {
     const int blocks = (rows + G - 1) / G;
     k_rows_ifft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(rows, N, in, ftw, out);
@@ -257,14 +278,15 @@ struct Launch {
   }
   static int groups_per_block() { return G; }
   // Chebyshev engine: node AFs, node adjoint correlations, Step-B node tail
-  static void node(int units, int M, int Q, int N, int LS, const float2* Xc, const float2* H, const float2* ftw,
+  static void node(int units, int M, int Q, int N, int LS, const float2* Xc, const float2* H, const float2* ftwn,
                    float2* Rn, int R, LrRed* lred, cudaStream_t st) {
-    k_node<PL, G, MINB><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, LS, Xc, H, ftw, Rn, R, lred);
+    k_node<PLN, GN, MINBN><<<(units + GN - 1) / GN, THREADS_N, smem_n(), st>>>(units, M, Q, N, LS, Xc, H, ftwn, Rn, R,
+                                                                               lred);
   }
-  static void adj_g(int wrt, const AdjGArgs& a, const float2* ftw, cudaStream_t st) {
-    const int blocks = (a.units + G - 1) / G;
-    if (wrt == 2) k_adj_g<PL, G, MINB, 2><<<blocks, THREADS, smem_fft(), st>>>(a, ftw);
-    else k_adj_g<PL, G, MINB, 1><<<blocks, THREADS, smem_fft(), st>>>(a, ftw);
+  static void adj_g(int wrt, const AdjGArgs& a, const float2* ftwn, cudaStream_t st) {
+    const int blocks = (a.units + GN - 1) / GN;
+    if (wrt == 2) k_adj_g<PLN, GN, MINBN, 2><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
+    else k_adj_g<PLN, GN, MINBN, 1><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
   }
   static void lrB_tail(int units, int M, int Q, int N, int NS, const float2* slots, const float2* Vt,
                        const float2* ftw, float2* out, cudaStream_t st) {
@@ -272,11 +294,15 @@ struct Launch {
   }
   static cudaError_t prepare_lr() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_node<PL, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft())))
+    if ((e = cudaFuncSetAttribute(k_node<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
       return e;
-    if ((e = cudaFuncSetAttribute(k_adj_g<PL, G, MINB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft())))
+    if ((e = cudaFuncSetAttribute(k_adj_g<PLN, GN, MINBN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_n())))
       return e;
-    if ((e = cudaFuncSetAttribute(k_adj_g<PL, G, MINB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft())))
+    if ((e = cudaFuncSetAttribute(k_adj_g<PLN, GN, MINBN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_n())))
+      return e;
+    if ((e = cudaFuncSetAttribute(k_xhat<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
       return e;
     return cudaFuncSetAttribute(k_lrB_tail<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
   }
@@ -532,13 +558,14 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, cuda_device));
   int bps[3] = {1, 1, 1}, G = 1;
   cudaError_t perr = cudaSuccess;
-  std::vector<float2> ftw_host, ftwr_host;
+  std::vector<float2> ftw_host, ftwr_host, ftwn_host;
   bool okP = with_P(P, [&](auto Lc) {
     using LC = decltype(Lc);
     perr = LC::prepare(bps);
     G = LC::groups_per_block();
     ftw_host = LC::twiddles();
     ftwr_host = LC::twiddles_r();
+    ftwn_host = LC::twiddles_n();
   });
   if (!okP) {
     delete ctx;
@@ -636,6 +663,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * cfg.K * P));
   CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->ftwn, sizeof(float2) * ftwn_host.size()));
+  CK(cudaMemcpy(ctx->ftwn, ftwn_host.data(), sizeof(float2) * ftwn_host.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&ctx->ftwr, sizeof(float2) * ftwr_host.size()));
   CK(cudaMemcpy(ctx->ftwr, ftwr_host.data(), sizeof(float2) * ftwr_host.size(), cudaMemcpyHostToDevice));
   const int64_t uslots = std::max(ctx->units, ctx->units_lr);
@@ -796,7 +825,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
   void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -907,7 +936,8 @@ static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st, co
   const int nk = ctx->lr ? ctx->Q : c.K;
   const int units = c.R * c.M * nk;
   with_P(ctx->P, [&](auto Lc) {
-    decltype(Lc)::xhat(units, c.M, c.N, nk, s, ctx->lr ? ctx->Vt : ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
+    if (ctx->lr) decltype(Lc)::xhat_n(units, c.M, c.N, nk, s, ctx->Vt, ctx->ftwn, ctx->Xc, w, ctx->cm, st);
+    else decltype(Lc)::xhat(units, c.M, c.N, nk, s, ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
   });
   ctx->launches += 1;
   return launch_check(ctx, "xhat");
@@ -923,7 +953,7 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
   const sqngd_config& c = ctx->cfg;
   const int node_units = c.R * c.M * c.M * ctx->Q;
   with_P(ctx->P, [&](auto Lc) {
-    decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftw, ctx->Rn, c.R, ctx->lred, st);
+    decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftwn, ctx->Rn, c.R, ctx->lred, st);
   });
   LrArgs a{};
   a.R = c.R; a.M = c.M; a.N = c.N; a.L = ctx->L; a.K = c.K; a.nch = ctx->nch; a.kw = ctx->kw;
@@ -1041,7 +1071,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     ag.units = c.R * c.M * c.M * ctx->Q; ag.mode = c.loss_mode; ag.bp = (float)c.beta_or_p;
     ag.Gn = ctx->Gn; ag.um = ctx->part.m; ag.lred = ctx->lred; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
     ag.cnt = ctx->lr_cnt; ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
-    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::adj_g(wrt, ag, ctx->ftw, st); });
+    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::adj_g(wrt, ag, ctx->ftwn, st); });
     CombineArgs ca{};
     ca.M = c.M; ca.N = c.N; ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.red = ctx->red;
     ca.f = fa;
