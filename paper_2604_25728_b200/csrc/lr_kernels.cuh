@@ -29,6 +29,10 @@
 #include "af_kernels.cuh"
 #include "common.cuh"
 
+#ifndef SQNGD_LRT_PREFETCH
+#define SQNGD_LRT_PREFETCH 0
+#endif
+
 namespace sq {
 
 // Per-restart record of the Chebyshev engine, filled by k_lr with order-independent
@@ -89,10 +93,12 @@ struct LrArgs {
 
 // One Doppler cell of the fused epilogue (a5 / a7): key tracking, surrogate term, cotangent.
 // LM: 0 MAX (keys only), 1 LSE, 2 PNORM.  Returns G~ (unnormalised: gphi w At / |At|).
-template <int LM, bool HW, bool GRAD, bool GE_RULE>
+template <int LM, bool HW, bool GRAD, bool GE_RULE, bool GF_ONLY = false>
 __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int idx, bool valid, float lbN, float nlbs,
                                           float qN, float& best, int& bk, float& S, float* mrow) {
-  const float a2 = fmaf(A.x, A.x, A.y * A.y);
+  // |A|^2 + 1e-30: the floor keeps rsqrt finite at A = 0 and is far below one ulp of any
+  // non-negligible cell, so the key and the magnitude are unchanged
+  const float a2 = fmaf(A.x, A.x, fmaf(A.y, A.y, 1e-30f));
   float wt = 1.f, kv = a2;
   if (HW) {
     wt = valid ? __ldg(a.weights + (size_t)k * a.L + idx) : 0.f;
@@ -105,7 +111,7 @@ __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int 
     if (mrow) mrow[(size_t)k * a.L] = sqrtf(a2);
     return make_float2(0.f, 0.f);
   }
-  const float rsq = rsqa(fmaxf(a2, 1e-30f));
+  const float rsq = rsqa(a2);
   const float mag = a2 * rsq;
   if (mrow) mrow[(size_t)k * a.L] = mag;
   float phi, gphi;
@@ -121,6 +127,7 @@ __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int 
   S += phi;
   if (!GRAD) return make_float2(0.f, 0.f);
   const float gf = gphi * (HW ? wt * rsq : rsq);
+  if (GF_ONLY) return make_float2(gf, 0.f);  // the caller forms gf A itself (fused into its sums)
   return make_float2(A.x * gf, A.y * gf);
 }
 
@@ -488,10 +495,14 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
     }
     // one 8-pair tile: forward MMAs, 8 cells per thread, adjoint MMAs.  MASKED: the remainder
     // tile of a K/2 that is not a multiple of 8 (pairs >= K/2 are zero padding).
-    auto tile = [&](int t, auto masked_c) {
-      constexpr bool MASKED = decltype(masked_c)::value;
+    auto ldB = [&](int t, float4& x0, float4& x1, float4& y0, float4& y1) {
       const float4* tf = a.tabF + ((size_t)t * 32 + lane) * 2;
-      const float4 fa = __ldg(tf), fb = __ldg(tf + 1);
+      const float4* ta = a.tabA + ((size_t)t * 32 + lane) * 2;
+      x0 = __ldg(tf); x1 = __ldg(tf + 1);
+      if (GRAD) { y0 = __ldg(ta); y1 = __ldg(ta + 1); }
+    };
+    auto tile = [&](int t, auto masked_c, float4 fa, float4 fb, float4 ga, float4 gb) {
+      constexpr bool MASKED = decltype(masked_c)::value;
       float Per[4] = {0.f, 0.f, 0.f, 0.f}, Pei[4] = {0.f, 0.f, 0.f, 0.f};
       float Por[4] = {0.f, 0.f, 0.f, 0.f}, Poi[4] = {0.f, 0.f, 0.f, 0.f};
       mma3(Per, aErh, aErl, fa);
@@ -505,29 +516,34 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
         const int p = 8 * t + 2 * cq + (e & 1);
         const float2 A0 = make_float2(Per[e] + Por[e], Pei[e] + Poi[e]);
         const float2 A1 = make_float2(Per[e] - Por[e], Pei[e] - Poi[e]);
-        float2 G0, G1;
+        float gf0, gf1;  // cotangent factors: G = gf A
         if (!MASKED) {
-          G0 = lr_cell<LM, HW, GRAD, false>(A0, p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bl[h], kl[h], S[h], mrow[h]);
-          G1 = lr_cell<LM, HW, GRAD, true>(A1, a.K - 1 - p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bh[h], kh[h], S[h],
-                                            mrow[h]);
+          gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bl[h], kl[h], S[h],
+                                                   mrow[h]).x;
+          gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, a.K - 1 - p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bh[h],
+                                                  kh[h], S[h], mrow[h]).x;
         } else {
           const bool pv = p < Kp;
           const bool v0 = valid[h] && pv;
           float b0 = bl[h], b1 = bh[h];
           int k0 = kl[h], k1 = kh[h];
-          G0 = lr_cell<LM, HW, GRAD, false>(A0, pv ? p : 0, la, idx[h], v0, lbN, v0 ? nlbs[h] : -INFINITY,
-                                            v0 ? qN[h] : 0.f, b0, k0, S[h], pv ? mrow[h] : nullptr);
-          G1 = lr_cell<LM, HW, GRAD, true>(A1, pv ? a.K - 1 - p : 0, la, idx[h], v0, lbN, v0 ? nlbs[h] : -INFINITY,
-                                           v0 ? qN[h] : 0.f, b1, k1, S[h], pv ? mrow[h] : nullptr);
+          gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, pv ? p : 0, la, idx[h], v0, lbN, v0 ? nlbs[h] : -INFINITY,
+                                                   v0 ? qN[h] : 0.f, b0, k0, S[h], pv ? mrow[h] : nullptr).x;
+          gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, pv ? a.K - 1 - p : 0, la, idx[h], v0, lbN,
+                                                  v0 ? nlbs[h] : -INFINITY, v0 ? qN[h] : 0.f, b1, k1, S[h],
+                                                  pv ? mrow[h] : nullptr).x;
           if (pv) { bl[h] = b0; kl[h] = k0; bh[h] = b1; kh[h] = k1; }
-          if (!v0) G0 = G1 = make_float2(0.f, 0.f);
+          if (!v0) gf0 = gf1 = 0.f;
         }
-        SGr[e] = G0.x + G1.x; SGi[e] = G0.y + G1.y;
-        DGr[e] = G0.x - G1.x; DGi[e] = G0.y - G1.y;
+        if (GRAD) {  // SG = gf0 A0 + gf1 A1, DG = gf0 A0 - gf1 A1
+          const float tr = gf0 * A0.x, ti = gf0 * A0.y;
+          SGr[e] = fmaf(gf1, A1.x, tr); SGi[e] = fmaf(gf1, A1.y, ti);
+          DGr[e] = fmaf(-gf1, A1.x, tr); DGi[e] = fmaf(-gf1, A1.y, ti);
+        } else {
+          SGr[e] = SGi[e] = DGr[e] = DGi[e] = 0.f;
+        }
       }
       if (GRAD) {
-        const float4* ta = a.tabA + ((size_t)t * 32 + lane) * 2;
-        const float4 ga = __ldg(ta), gb = __ldg(ta + 1);
         // D order (g,2c) (g,2c+1) (g+8,2c) (g+8,2c+1) -> A order (g,c) (g+8,c) (g,c+4) (g+8,c+4)
         const float sr[4] = {SGr[0], SGr[2], SGr[1], SGr[3]}, si[4] = {SGi[0], SGi[2], SGi[1], SGi[3]};
         const float dr[4] = {DGr[0], DGr[2], DGr[1], DGr[3]}, di[4] = {DGi[0], DGi[2], DGi[1], DGi[3]};
@@ -539,9 +555,24 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
       }
     };
     const int tf_end = t1 < a.NTF ? t1 : a.NTF;
+    float4 nfa = make_float4(0.f, 0.f, 0.f, 0.f), nfb = nfa, nga = nfa, ngb = nfa;
+    if (t0 < tf_end) ldB(t0, nfa, nfb, nga, ngb);
 #pragma unroll 1
-    for (int t = t0; t < tf_end; ++t) tile(t, std::integral_constant<bool, false>{});
-    if (t1 > a.NTF && t0 <= a.NTF) tile(a.NTF, std::integral_constant<bool, true>{});
+    for (int t = t0; t < tf_end; ++t) {  // B fragments of the next tile are loaded one tile ahead
+      const float4 fa = nfa, fb = nfb, ga = nga, gb = ngb;
+#if SQNGD_LRT_PREFETCH
+      if (t + 1 < tf_end) ldB(t + 1, nfa, nfb, nga, ngb);
+      tile(t, std::integral_constant<bool, false>{}, fa, fb, ga, gb);
+#else
+      tile(t, std::integral_constant<bool, false>{}, fa, fb, ga, gb);
+      if (t + 1 < tf_end) ldB(t + 1, nfa, nfb, nga, ngb);
+#endif
+    }
+    if (t1 > a.NTF && t0 <= a.NTF) {
+      float4 fa, fb, ga = make_float4(0.f, 0.f, 0.f, 0.f), gb = ga;
+      ldB(a.NTF, fa, fb, ga, gb);
+      tile(a.NTF, std::integral_constant<bool, true>{}, fa, fb, ga, gb);
+    }
     if (odd && wp == a.kw - 1) {
       // middle bin f = grid centre (beta = 0) on the CUDA cores: At = sum_j alpha_j E_j, summed over the
       // quad's j columns; every lane of the quad evaluates the cell (G is needed in all of them), the

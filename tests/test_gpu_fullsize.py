@@ -22,9 +22,14 @@ def T(a):
     return torch.as_tensor(np.ascontiguousarray(a), device=DEV)
 
 
-def bench_cfg(name):
+ENGINES = {"fft": sqngd.ENGINE_FFT, "cheb": sqngd.ENGINE_CHEBYSHEV}
+
+
+def bench_cfg(name, engine="auto"):
+    """The bench configuration; `engine` forces a Doppler engine (auto: the library's choice,
+    Chebyshev on the narrow grids C1-C3, C5; FFT on C4)."""
     c = CF.CONFIGS[name]
-    return c.with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0)
+    return c.with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=ENGINES.get(engine, 0))
 
 
 def bench_inputs(c):
@@ -84,8 +89,9 @@ def check_forward(c, want_map, rows):
     return ctx, mg
 
 
-def test_c3_forward_sampled_rows_and_argmax():
-    check_forward(bench_cfg("C3"), want_map=True, rows=24)
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_c3_forward_sampled_rows_and_argmax(engine):
+    check_forward(bench_cfg("C3", engine), want_map=True, rows=24)
 
 
 def test_c4_forward_full_map():
@@ -105,15 +111,16 @@ def test_c4_forward_full_map():
     assert abs(20 * math.log10(mg["wpsl"] / ref_met[0]["wpsl"])) < 0.01
 
 
-def test_c5_forward_sampled_rows_and_argmax():
-    check_forward(bench_cfg("C5"), want_map=False, rows=12)
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_c5_forward_sampled_rows_and_argmax(engine):
+    check_forward(bench_cfg("C5", engine), want_map=False, rows=12)
 
 
-@pytest.mark.parametrize("name", ["C3", "C4"])
-def test_full_gradients_vs_oracle(name):
+@pytest.mark.parametrize("name,engine", [("C3", "fft"), ("C3", "cheb"), ("C4", "fft")])
+def test_full_gradients_vs_oracle(name, engine):
     """Step A (grad_w on s_hard) and Step B (grad_z, grad_rho through Q_A) against the full
     fp64 oracle at the benchmark size, with a perturbed (non-matched) filter bank."""
-    c = bench_cfg(name)
+    c = bench_cfg(name, engine)
     z, rho = bench_inputs(c)
     q = O.quantize(c, z, rho)
     w = (q["s_hard"] * np.exp(0.3j * np.cos(np.arange(c.N)))).astype(np.complex64)
@@ -139,11 +146,12 @@ def test_full_gradients_vs_oracle(name):
     assert rel(gr, gr_ref) < 1e-4, rel(gr, gr_ref)
 
 
-def test_c5_gradient_doppler_split_consistency():
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_c5_gradient_doppler_split_consistency(engine):
     """A property that holds at any size: the Step-B gradient of the full Doppler grid equals
     the max-then-sum combination (parallel.combine_lse arithmetic) of the gradients of its two
     halves, each evaluated by the same kernels (restart 0 of C5, P = 8192)."""
-    c = bench_cfg("C5").with_(R=1, eps_w=1.0)
+    c = bench_cfg("C5", engine).with_(R=1, eps_w=1.0)
     z, rho = bench_inputs(c.with_(R=1))
     q = O.quantize(c, z, rho)
     s = T(q["s_soft"].astype(np.complex64))
