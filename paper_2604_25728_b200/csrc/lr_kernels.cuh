@@ -877,6 +877,96 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
   }
 }
 
+// Node adjoints with the sum inside the CTA: NG groups of one CTA share one output unit and
+// split its inner index; their accumulators are summed in shared memory in group order
+// (deterministic), so the partial slots and the per-node arrival tail disappear.
+//   Step B (WRT 2), CTA = node (r, m, q):  e = IFFT_P(sum_l FFT(G^_{ml,q}) H_l),
+//            tslot[node][n] = e(n) conj(V_q(n))      (groups split l)
+//   Step A (WRT 1), CTA = (r, l, m):       out[(r l) m] = sum_q X~_{m,q} conj(FFT(G^_{ml,q}))
+//                                          (groups split q; the combine sums the M slots of row l)
+template <class PL, int NG, int WRT>
+__global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const float2* __restrict__ ftw) {
+  constexpr int E = PL::E, T = PL::T, P = PL::P;
+  extern __shared__ float4 smem_raw[];
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
+  GroupSync sync{1 + grp, T, group_mask(T)};
+  const int M = a.M, Q = a.Q, N = a.N;
+  const int u = blockIdx.x;
+  int r, m = 0, l = 0, q = 0;
+  if (WRT == 2) { q = u % Q; const int rm = u / Q; m = rm % M; r = rm / M; }
+  else { m = u % M; const int rl = u / M; l = rl % M; r = rl / M; }
+  const float mf = __uint_as_float(a.lred[r].mbits);
+  const float lb = a.bp * 1.4426950408889634f;
+  const int nin = WRT == 2 ? M : Q;  // inner index: l (Step B) or q (Step A)
+  float2 acc[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
+  int par = 0;
+  for (int it = grp; it < nin; it += NG) {
+    if (WRT == 2) l = it; else q = it;
+    const int pr = (r * M + m) * M + l;
+    const float2* Gp = a.Gn + ((size_t)pr * Q + q) * a.LS;
+    const float* ump = a.um + (size_t)pr * a.nch;
+    float2 v[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {  // branch-free so that all loads issue back to back
+      const int j = t + i * T;
+      const bool in = j < N || j > P - N;
+      const int idx = in ? lag_of(j, N, P) + N - 1 : 0;
+      const float mu = __ldg(ump + (idx >> a.csh));
+      const float2 x = __ldg(Gp + idx);
+      float fS, fG;
+      if (a.mode == 1) lr_rescale<1>(mu, mf, lb, a.bp, fS, fG);
+      else lr_rescale<2>(mu, mf, lb, a.bp, fS, fG);
+      fG = (in && mu > 0.f && mf > 0.f) ? fG : 0.f;
+      v[i] = make_float2(x.x * fG, x.y * fG);
+    }
+    fft<PL, -1>(v, ftw, xbuf, t, par, sync);
+    if (WRT == 2) {
+      const float2* Hl = a.H + ((size_t)r * M + l) * P;
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], __ldg(Hl + t + i * T)));
+    } else {
+      const float2* X = a.Xc + (((size_t)r * M + m) * Q + q) * P;
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(__ldg(X + t + i * T), v[i]));
+    }
+  }
+  // fixed-order sum of the groups' accumulators (the exchange buffers are free now)
+  __syncthreads();
+  if (grp != 0) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) xbuf[t + i * T] = acc[i];
+  }
+  __syncthreads();
+  if (grp != 0) return;
+  for (int g = 1; g < NG; ++g) {
+    const float2* ob = reinterpret_cast<float2*>(smem_raw) + g * (FftSmem<PL>::TOTAL);
+#pragma unroll
+    for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], ob[t + i * T]);
+  }
+  if (WRT == 1) {
+    float2* out = a.out + (size_t)u * P;
+#pragma unroll
+    for (int i = 0; i < E; ++i) out[t + i * T] = acc[i];
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) acc[i].y = -acc[i].y;
+  fft<PL, -1>(acc, ftw, xbuf, t, par, sync);  // acc = conj(e)
+  const float2* vr = a.Vt + (size_t)q * N;
+  float2* o = a.tslot + (size_t)u * a.NS;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    if (n < N) {
+      const float2 z = cmul(acc[i], __ldg(vr + n));
+      o[n] = make_float2(z.x, -z.y);  // e conj(V_q)
+    }
+  }
+}
+
 // Step B node tail, unit (r M + m) Q + q:  e = IFFT_P(sum_l G^_{ml,q} H_l) (fixed order),
 // out[u][n] = e(n) conj(V_q(n)) for n < N (row stride NS, even: the combine reads float4 pairs):
 // the node's share of dL/ds_m^* before the sum over q.

@@ -84,6 +84,7 @@ struct sqngd_ctx_s {
   bool lr = false;
   int Q = 0, QS = 0, nch = 0, kw = 1, LS = 0;
   bool lr_tc = true;           // k_lrt (mma.sync 3xTF32) instead of the FP32 k_lr
+  bool lr_cta = true;          // k_adj_gc (sums inside the CTA) instead of k_adj_g (slots + arrival tail)
   int nch16 = 0, NT = 0, NTF = 0;
   float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
@@ -288,6 +289,13 @@ struct Launch {
     if (wrt == 2) k_adj_g<PLN, GN, MINBN, 2><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
     else k_adj_g<PLN, GN, MINBN, 1><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
   }
+  // CTA-summed node adjoints: NGC groups per CTA (shared memory: NGC exchange buffers)
+  static constexpr int NGC = (PLN::T >= 512) ? 1 : (PLN::T >= 256 ? 2 : ((128 / PLN::T) > 4 ? 128 / PLN::T : 4));
+  static size_t smem_c() { return (size_t)NGC * FftSmem<PLN>::TOTAL * sizeof(float2) + 16; }
+  static void adj_gc(int wrt, const AdjGArgs& a, int ctas, const float2* ftwn, cudaStream_t st) {
+    if (wrt == 2) k_adj_gc<PLN, NGC, 2><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
+    else k_adj_gc<PLN, NGC, 1><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
+  }
   static void lrB_tail(int units, int M, int Q, int N, int NS, const float2* slots, const float2* Vt,
                        const float2* ftw, float2* out, cudaStream_t st) {
     k_lrB_tail<PL, G><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, NS, slots, Vt, ftw, out);
@@ -303,6 +311,10 @@ struct Launch {
                                   (int)smem_n())))
       return e;
     if ((e = cudaFuncSetAttribute(k_xhat<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
+      return e;
+    if ((e = cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c())))
+      return e;
+    if ((e = cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c())))
       return e;
     return cudaFuncSetAttribute(k_lrB_tail<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
   }
@@ -607,6 +619,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     ctx->nch = (L + 31) / 32;
     ctx->LS = ctx->nch * 32;
     if (const char* ev = getenv("SQNGD_LR_TC")) ctx->lr_tc = ev[0] != '0';
+    if (const char* ev = getenv("SQNGD_LR_CTA")) ctx->lr_cta = ev[0] != '0';
     ctx->nch16 = (L + 15) / 16;
     const int Kp = cfg.K / 2;
     ctx->NT = (Kp + 7) / 8;
@@ -1071,7 +1084,11 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     ag.units = c.R * c.M * c.M * ctx->Q; ag.mode = c.loss_mode; ag.bp = (float)c.beta_or_p;
     ag.Gn = ctx->Gn; ag.um = ctx->part.m; ag.lred = ctx->lred; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
     ag.cnt = ctx->lr_cnt; ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
-    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::adj_g(wrt, ag, ctx->ftwn, st); });
+    const bool cta_sum = ctx->lr_cta && wrt == SQNGD_WRT_TRANSMIT;  // Step A: 640 one-FFT units measured faster
+    with_P(ctx->P, [&](auto Lc) {
+      if (cta_sum) decltype(Lc)::adj_gc(wrt, ag, wrt == 2 ? c.R * c.M * ctx->Q : c.R * c.M * c.M, ctx->ftwn, st);
+      else decltype(Lc)::adj_g(wrt, ag, ctx->ftwn, st);
+    });
     CombineArgs ca{};
     ca.M = c.M; ca.N = c.N; ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.red = ctx->red;
     ca.f = fa;
@@ -1087,7 +1104,8 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
       return launch_check(ctx, "chebyshev adjoint (transmit)");
     }
     CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-    ca.K = c.M * ctx->Q; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * c.M * ctx->Q;
+    const int nsl = cta_sum ? c.M : c.M * ctx->Q;  // spectral slots per filter row
+    ca.K = nsl; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * nsl;
     ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
     k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
     if (tail) {
