@@ -475,6 +475,9 @@ __global__ void __launch_bounds__(PL::T* G)
 // outside |c (z - rho)| < 12 where it is < 1.6e-10: per element, a warp whose 32 (sorted)
 // thresholds all lie farther than 12/c from z skips it (warp-uniform test), so only the
 // ~2 x 12/c x B r_n thresholds near each z do the work.
+__device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float* vr, const float* g, const AdamP& ap,
+                                     float lo, float hi, float gap, float* sr);
+
 // Finishing work done by last-arriving blocks (arrival counters, self-resetting; fixed-order sums):
 //   per (r, threshold block): grad_rho[i] = coef * sum_ch part[ch][i]  (when gsum != nullptr);
 //   per (r, element chunk):   Adam on the chunk's z (when zad.z != nullptr) -- after every
@@ -488,6 +491,12 @@ struct RhoFinish {
   const float* gz;  // grad_z [R][MN]
   AdamP ap;
   const int* status;
+  // fused threshold update: the last threshold block of restart r to finish does Adam(rho) and
+  // the projection (dynamic shared memory 2 n2 floats)
+  int* cnt_r;       // [R] or nullptr (not fused)
+  float *rho, *mr, *vr;
+  AdamP apr;
+  float lo, hi, gap;
 };
 
 __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
@@ -555,6 +564,23 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
 #pragma unroll 8
     for (int k = 0; k < (int)gridDim.y; ++k) g += __ldcg(pp + (size_t)k * BR);
     fin.gsum[(size_t)r * BR + i] = fin.coef * g;
+  }
+  if (last_tb && fin.cnt_r) {  // the last threshold block of the restart: Adam(rho) + projection
+    __shared__ int last_r;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      last_r = atomicAdd(fin.cnt_r + r, 1) == (int)gridDim.x - 1;
+      if (last_r) fin.cnt_r[r] = 0;
+    }
+    __syncthreads();
+    if (last_r) {
+      __threadfence();
+      extern __shared__ float rho_sr[];
+      if (!(*fin.status & ST_NONFINITE))
+        adam_project_rho_dev(r, BR, fin.rho, fin.mr, fin.vr, fin.gsum + (size_t)r * BR, fin.apr, fin.lo, fin.hi,
+                             fin.gap, rho_sr);
+    }
   }
   if (last_ch && !(*fin.status & ST_NONFINITE)) {  // Adam on this chunk's z (keep the last finite iterate)
     float c1, c2;
@@ -626,42 +652,16 @@ __global__ void k_adam_project_w(int N, float* w, float* mw, float* vw, const fl
 }
 
 // Threshold projection: sort ascending, clamp to [lo, hi], forward min-gap sweep.
-// One block (1024 threads) per restart; BR <= 8192.
-// Step B update, one block per restart:
-//   grad_rho = coef * sum_chunks rho_part (when rho_part != nullptr, else g), Adam(rho), projection;
-//   Adam(z) on the restart's M N elements (when z != nullptr).
-struct ZAdam {
-  float* z;
-  float* m;
-  float* v;
-  const float* g;
-  int MN;
-  const float* rho_part;  // [R][nchunk][BR] gather partials of dL/drho (k_grad_rho_part)
-  int nchunk;
-  float coef;             // -a c
-};
-
-__global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
-                                   float lo, float hi, float gap, const int* status, ZAdam za) {
-  extern __shared__ float sr[];
-  __shared__ int flag;
-  if (*status & ST_NONFINITE) return;
+// Adam on rho of restart r, then the projection; called by one whole block (any size with
+// BR <= 32 blockDim), sr = 2 n2 floats of shared memory (n2 = next power of two >= BR).
+// g: the restart's gradient (read with ld.cg: it may come from other blocks of this launch).
+__device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float* vr, const float* g, const AdamP& ap,
+                                     float lo, float hi, float gap, float* sr) {
+  __shared__ int flag, swapped;
   float c1, c2;
   ap.corr(c1, c2);
   const float lr = ap.lr, b1 = ap.b1, b2 = ap.b2, eps = ap.eps;
-  if (za.z) {  // Adam on z (elementwise; the grad_rho gather already consumed the old z)
-#pragma unroll 4
-    for (int i = threadIdx.x; i < za.MN; i += blockDim.x) {
-      const size_t j = (size_t)blockIdx.x * za.MN + i;
-      const float gi = za.g[j];
-      const float mi = b1 * za.m[j] + (1.f - b1) * gi;
-      const float vi = b2 * za.v[j] + (1.f - b2) * gi * gi;
-      za.m[j] = mi;
-      za.v[j] = vi;
-      za.z[j] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
-    }
-  }
-  float* p = rho + (size_t)blockIdx.x * BR;
+  float* p = rho + (size_t)r * BR;
   int n2 = 1;
   while (n2 < BR) n2 <<= 1;
   if (threadIdx.x == 0) flag = 0;
@@ -669,16 +669,8 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {  // Adam step, then the projection
     float x = INFINITY;
     if (i < BR) {
-      const size_t j = (size_t)blockIdx.x * BR + i;
-      float gi;
-      if (za.rho_part) {
-        float acc = 0.f;
-#pragma unroll 8
-        for (int ch = 0; ch < za.nchunk; ++ch) acc += __ldg(za.rho_part + ((size_t)blockIdx.x * za.nchunk + ch) * BR + i);
-        gi = za.coef * acc;
-      } else {
-        gi = g[j];
-      }
+      const size_t j = (size_t)r * BR + i;
+      const float gi = __ldcg(g + i);
       const float mi = b1 * mr[j] + (1.f - b1) * gi;
       const float vi = b2 * vr[j] + (1.f - b2) * gi * gi;
       mr[j] = mi;
@@ -694,7 +686,6 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
   if (flag) {
     // nearly sorted (Adam moves each threshold by ~lr per step): odd-even transposition
     // rounds with early exit; a full bitonic sort only if that does not converge.
-    __shared__ int swapped;
     int rounds = 0;
     do {
       __syncthreads();
@@ -738,7 +729,7 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
     for (int i = threadIdx.x; i < BR; i += blockDim.x) q[i] = sr[i] - (float)i * gap;
     __syncthreads();
     for (int off = 1; off < BR; off <<= 1) {
-      float tmp[8];
+      float tmp[32];
       int cnt = 0;
       for (int i = threadIdx.x; i < BR; i += blockDim.x) tmp[cnt++] = (i >= off) ? fmaxf(q[i], q[i - off]) : q[i];
       __syncthreads();
@@ -753,6 +744,14 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
   }
   __syncthreads();
   for (int i = threadIdx.x; i < BR; i += blockDim.x) p[i] = sr[i];
+}
+
+// Step-B threshold update, one block per restart (when not fused into k_grad_rho_part).
+__global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
+                                   float lo, float hi, float gap, const int* status) {
+  extern __shared__ float sr[];
+  if (*status & ST_NONFINITE) return;  // keep the last finite iterate
+  adam_project_rho_dev(blockIdx.x, BR, rho, mr, vr, g + (size_t)blockIdx.x * BR, ap, lo, hi, gap, sr);
 }
 
 }  // namespace sq

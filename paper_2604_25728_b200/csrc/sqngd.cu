@@ -701,8 +701,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->dy, sizeof(float) * RMN));
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
-  CK(cudaMalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (64 + ctx->rho_nchunk)));
-  CK(cudaMemset(ctx->rho_cnt, 0, sizeof(int) * (size_t)cfg.R * (64 + ctx->rho_nchunk)));
+  CK(cudaMalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
+  CK(cudaMemset(ctx->rho_cnt, 0, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
   CK(cudaMalloc(&ctx->gw, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->gz, sizeof(float) * RMN));
   CK(cudaMalloc(&ctx->grho, sizeof(float) * (size_t)cfg.R * ctx->BR));
@@ -1313,17 +1313,23 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
         return rc;
       {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
         dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);
-        RhoFinish fin{};  // grad_rho sums and Adam(z) by last-arriving blocks
+        RhoFinish fin{};  // grad_rho sums, Adam(z) and Adam(rho) + projection by last-arriving blocks
         fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
         fin.gsum = ctx->grho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64;
         fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
         fin.status = ctx->status;
-        k_grad_rho_part<<<g1, 256, 0, st>>>(c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy,
-                                            ctx->rho_part, fin);
-        const ZAdam za{nullptr, nullptr, nullptr, nullptr, c.M * c.N, nullptr, 0, 0.f};
-        k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
-                                                                      ctx->grho, ap(c.lr_z, 1, i), 1e-4f, 1.0f - 1e-4f,
-                                                                      1e-6f, ctx->status, za);
+        const bool fuse_rho = ctx->BR <= 4096;  // 2 n2 floats within the default 48 KB
+        if (fuse_rho) {
+          fin.cnt_r = ctx->rho_cnt + (size_t)c.R * (64 + ctx->rho_nchunk);
+          fin.rho = stt->rho; fin.mr = stt->m_rho; fin.vr = stt->v_rho; fin.apr = ap(c.lr_z, 1, i);
+          fin.lo = 1e-4f; fin.hi = 1.0f - 1e-4f; fin.gap = 1e-6f;
+        }
+        k_grad_rho_part<<<g1, 256, fuse_rho ? 2 * n2 * sizeof(float) : 0, st>>>(
+            c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy, ctx->rho_part, fin);
+        if (!fuse_rho)
+          k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
+                                                                        ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
+                                                                        1.0f - 1e-4f, 1e-6f, ctx->status);
         ctx->launches += 2;
       }
       if ((rc = launch_check(ctx, "step B update"))) return rc;
