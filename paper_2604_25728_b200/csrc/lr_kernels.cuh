@@ -26,6 +26,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <cuda_fp16.h>
+
 #include "af_kernels.cuh"
 #include "common.cuh"
 
@@ -377,6 +379,8 @@ struct LrtArgs {
   const float4* tabF;    // [NT][32][2]: forward B fragments {a_b0h, a_b1h, a_b0l, a_b1l}, {beta ...}
   const float4* tabA;    // [NT][32][2]: adjoint B fragments
   const float* coefm;    // [Q/2] middle-bin coefficients l_j(f_centre) (odd K)
+  const uint4* tabF16;   // [NT][32]: forward B fragments, m16n8k16 f16 {alpha b0, b1, beta b0, b1}
+  const uint2* tabM16;   // [32]: middle-bin B fragment (column 0)
   const float2* Rn;      // [R M M][Q][LS]
   float2* Gn;            // [R M M][Q][LS]
   float* af_mag;         // forward only
@@ -408,6 +412,37 @@ __device__ __forceinline__ void split4(const float (&x)[4], uint32_t (&h)[4], ui
   for (int i = 0; i < 4; ++i) tf32_split(x[i], h[i], l[i]);
 }
 
+// Forward contraction in FP16 with the 3-term split packed along K (m16n8k16, one MMA per
+// product): A row = [hi(x_0..x_4) | lo(x_0..x_4) | hi(x_0..x_4) | 0], B column =
+// [hi(c_0..c_4); hi(c_0..c_4); lo(c_0..c_4); 0], so A.B = x_hi c_hi + x_lo c_hi + x_hi c_lo.
+// Range: |x| <= 2N <= 8192 and |c| < 3 fit FP16; lo parts below the FP16 normal range lose at
+// most 6e-8 absolute each, i.e. < 2e-7 N per cell (the parity floor is 2e-6 N).
+#ifndef SQNGD_LRT_F16
+#define SQNGD_LRT_F16 1
+#endif
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// K-column k of the packed split of x[0..4] (k < 15), as an FP16 value
+__device__ __forceinline__ unsigned short f16_col(int k, const float (&x)[5]) {
+  const int part = k / 5, j = k - 5 * part;
+  float v = x[0];
+  v = j == 1 ? x[1] : v;
+  v = j == 2 ? x[2] : v;
+  v = j == 3 ? x[3] : v;
+  v = j == 4 ? x[4] : v;
+  const __half hi = __float2half_rn(v);
+  const __half lo = __float2half_rn(v - __half2float(hi));
+  const __half r = part == 1 ? lo : (part < 3 ? hi : __float2half_rn(0.f));
+  return __half_as_ushort(r);
+}
+__device__ __forceinline__ uint32_t f16_pair(int k, const float (&x)[5]) {
+  return (uint32_t)f16_col(k, x) | ((uint32_t)f16_col(k + 1, x) << 16);
+}
+
 template <int Q, int LM, bool HW, bool GRAD>
 __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
   constexpr int QH = Q / 2;
@@ -432,9 +467,34 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
     valid[h] = inL[h] && tau >= a.tau_lo && tau <= a.tau_hi && !(is_auto && a.excl0 && tau == 0);
   }
   // node values -> A fragments (element e: row h = e & 1, column j = c + 4 (e >> 1))
-  uint32_t aErh[4], aErl[4], aEih[4], aEil[4], aOrh[4], aOrl[4], aOih[4], aOil[4];
+  constexpr bool F16 = SQNGD_LRT_F16 && Q <= 10;  // the packed split needs 3 Q/2 <= 15 K columns
+  uint32_t aEr[4], aEi[4], aOr[4], aOi[4];  // F16: m16n8k16 A fragments (rows g, g+8; K columns 2c.., 2c+8..)
+  uint32_t aErh[4], aErl[4], aEih[4], aEil[4], aOrh[4], aOrl[4], aOih[4], aOil[4];  // TF32 3x
   float nm2[2] = {0.f, 0.f};
-  {
+  if constexpr (F16) {
+    const float2* Rp = a.Rn + (size_t)pr * Q * a.LS;
+    float xs[4][2][5];  // (E_re, E_im, O_re, O_im) x row x j
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        float2 x = make_float2(0.f, 0.f), y = x;
+        if (j < QH && inL[h]) {
+          x = __ldg(Rp + (size_t)j * a.LS + idx[h]);
+          y = __ldg(Rp + (size_t)(Q - 1 - j) * a.LS + idx[h]);
+        }
+        xs[0][h][j] = x.x + y.x; xs[1][h][j] = x.y + y.y; xs[2][h][j] = x.x - y.x; xs[3][h][j] = x.y - y.y;
+        nm2[h] = fmaxf(nm2[h], fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)));
+      }
+    uint32_t* frag[4] = {aEr, aEi, aOr, aOi};
+#pragma unroll
+    for (int pidx = 0; pidx < 4; ++pidx) {
+      frag[pidx][0] = f16_pair(2 * cq, xs[pidx][0]);
+      frag[pidx][1] = f16_pair(2 * cq, xs[pidx][1]);
+      frag[pidx][2] = f16_pair(2 * cq + 8, xs[pidx][0]);
+      frag[pidx][3] = f16_pair(2 * cq + 8, xs[pidx][1]);
+    }
+  } else {
     float Er[4], Ei[4], Or[4], Oi[4];
     const float2* Rp = a.Rn + (size_t)pr * Q * a.LS;
 #pragma unroll
@@ -496,19 +556,34 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
     // one 8-pair tile: forward MMAs, 8 cells per thread, adjoint MMAs.  MASKED: the remainder
     // tile of a K/2 that is not a multiple of 8 (pairs >= K/2 are zero padding).
     auto ldB = [&](int t, float4& x0, float4& x1, float4& y0, float4& y1) {
-      const float4* tf = a.tabF + ((size_t)t * 32 + lane) * 2;
+      if constexpr (F16) {
+        const uint4 f16 = __ldg(a.tabF16 + (size_t)t * 32 + lane);
+        x0 = make_float4(__uint_as_float(f16.x), __uint_as_float(f16.y), __uint_as_float(f16.z),
+                         __uint_as_float(f16.w));
+        x1 = x0;
+      } else {
+        const float4* tf = a.tabF + ((size_t)t * 32 + lane) * 2;
+        x0 = __ldg(tf); x1 = __ldg(tf + 1);
+      }
       const float4* ta = a.tabA + ((size_t)t * 32 + lane) * 2;
-      x0 = __ldg(tf); x1 = __ldg(tf + 1);
       if (GRAD) { y0 = __ldg(ta); y1 = __ldg(ta + 1); }
     };
     auto tile = [&](int t, auto masked_c, float4 fa, float4 fb, float4 ga, float4 gb) {
       constexpr bool MASKED = decltype(masked_c)::value;
       float Per[4] = {0.f, 0.f, 0.f, 0.f}, Pei[4] = {0.f, 0.f, 0.f, 0.f};
       float Por[4] = {0.f, 0.f, 0.f, 0.f}, Poi[4] = {0.f, 0.f, 0.f, 0.f};
-      mma3(Per, aErh, aErl, fa);
-      mma3(Pei, aEih, aEil, fa);
-      mma3(Por, aOrh, aOrl, fb);
-      mma3(Poi, aOih, aOil, fb);
+      if constexpr (F16) {
+        mma_f16(Per, aEr, __float_as_uint(fa.x), __float_as_uint(fa.y));
+        mma_f16(Pei, aEi, __float_as_uint(fa.x), __float_as_uint(fa.y));
+        mma_f16(Por, aOr, __float_as_uint(fa.z), __float_as_uint(fa.w));
+        mma_f16(Poi, aOi, __float_as_uint(fa.z), __float_as_uint(fa.w));
+        (void)fb;
+      } else {
+        mma3(Per, aErh, aErl, fa);
+        mma3(Pei, aEih, aEil, fa);
+        mma3(Por, aOrh, aOrl, fb);
+        mma3(Poi, aOih, aOil, fb);
+      }
       float SGr[4], SGi[4], DGr[4], DGi[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {  // D element e: row h = e >> 1, pair p = 8t + 2c + (e & 1)
@@ -577,8 +652,18 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
       // middle bin f = grid centre (beta = 0) on the CUDA cores: At = sum_j alpha_j E_j, summed over the
       // quad's j columns; every lane of the quad evaluates the cell (G is needed in all of them), the
       // sum and the key are counted by lane c = 0 only.
-      const float am0 = cq < QH ? __ldg(a.coefm + cq) : 0.f, am1 = cq + 4 < QH ? __ldg(a.coefm + cq + 4) : 0.f;
       float2 Am[2];
+      if constexpr (F16) {  // one extra MMA pair: the middle-bin coefficients in B column 0 (held by the c = 0 lanes)
+        const uint2 bm = __ldg(a.tabM16 + lane);
+        float Mr[4] = {0.f, 0.f, 0.f, 0.f}, Mi[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_f16(Mr, aEr, bm.x, bm.y);
+        mma_f16(Mi, aEi, bm.x, bm.y);
+        const int src = lane & ~3;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          Am[h] = make_float2(__shfl_sync(0xffffffffu, Mr[2 * h], src), __shfl_sync(0xffffffffu, Mi[2 * h], src));
+      } else {
+      const float am0 = cq < QH ? __ldg(a.coefm + cq) : 0.f, am1 = cq + 4 < QH ? __ldg(a.coefm + cq + 4) : 0.f;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const float e0r = __uint_as_float(aErh[h]), e0i = __uint_as_float(aEih[h]);  // hi holds x itself
@@ -589,6 +674,7 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
         xr += __shfl_xor_sync(0xffffffffu, xr, 2);
         xi += __shfl_xor_sync(0xffffffffu, xi, 2);
         Am[h] = make_float2(xr, xi);
+      }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {

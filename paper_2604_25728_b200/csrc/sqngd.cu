@@ -1,6 +1,7 @@
 // libsqngd.so -- host side of the C-ABI (include/sqngd.h): context, validation,
 // launch configuration, and the orchestration of the kernels in af_kernels.cuh /
 // misc_kernels.cuh.  Every arithmetic step of the hot path runs on the GPU.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -88,6 +89,8 @@ struct sqngd_ctx_s {
   int nch16 = 0, NT = 0, NTF = 0;
   float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
+  uint4* tabF16 = nullptr;     // [NT][32] k_lrt forward B fragments (FP16 packed split)
+  uint2* tabM16 = nullptr;     // [32] k_lrt middle-bin B fragment
   int64_t units_lr = 0;        // k_lr units (CTAs of kw warps): R M^2 nch
   size_t lr_smem = 0;          // k_lr dynamic shared memory
   LrRed* lred = nullptr;       // [R] k_lr running maxima
@@ -780,6 +783,43 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
           ta[o] = frag(alpha(gg, 8 * t + 2 * cc), alpha(gg, 8 * t + 2 * cc + 1));
           ta[o + 1] = frag(beta(gg, 8 * t + 2 * cc), beta(gg, 8 * t + 2 * cc + 1));
         }
+      {  // FP16 packed-split forward fragments (m16n8k16): K rows [hi(c) ; hi(c) ; lo(c) ; 0]
+        auto f16 = [](double x) -> uint16_t { return __half_as_ushort(__float2half_rn((float)x)); };
+        auto split16 = [&](double x, int part) -> uint16_t {  // part 0: hi, 1: hi (for x_lo), 2: lo
+          const __half h = __float2half_rn((float)x);
+          if (part < 2) return __half_as_ushort(h);
+          return f16(x - (double)__half2float(h));
+        };
+        auto Bk = [&](int k, int p, bool is_alpha, bool mid) -> uint16_t {  // B[k][pair p]
+          if (k >= 15) return 0;
+          const int part = k / 5, j = k - 5 * part;
+          double c;
+          if (mid) c = (j < QH) ? lr_ell[(size_t)Kp * Q + j] : 0.0;
+          else c = is_alpha ? alpha(j, p) : beta(j, p);
+          return split16(c, part);
+        };
+        auto pack = [](uint16_t lo, uint16_t hi) { return (uint32_t)lo | ((uint32_t)hi << 16); };
+        std::vector<uint4> t16((size_t)ctx->NT * 32);
+        std::vector<uint2> m16(32);
+        for (int t = 0; t < ctx->NT; ++t)
+          for (int ln = 0; ln < 32; ++ln) {
+            const int gg = ln >> 2, cc = ln & 3, p = 8 * t + gg;
+            t16[(size_t)t * 32 + ln] = make_uint4(pack(Bk(2 * cc, p, true, false), Bk(2 * cc + 1, p, true, false)),
+                                                  pack(Bk(2 * cc + 8, p, true, false), Bk(2 * cc + 9, p, true, false)),
+                                                  pack(Bk(2 * cc, p, false, false), Bk(2 * cc + 1, p, false, false)),
+                                                  pack(Bk(2 * cc + 8, p, false, false), Bk(2 * cc + 9, p, false, false)));
+          }
+        for (int ln = 0; ln < 32; ++ln) {
+          const int gg = ln >> 2, cc = ln & 3;
+          const bool col0 = gg == 0 && (cfg.K & 1);
+          m16[ln] = make_uint2(col0 ? pack(Bk(2 * cc, 0, true, true), Bk(2 * cc + 1, 0, true, true)) : 0u,
+                               col0 ? pack(Bk(2 * cc + 8, 0, true, true), Bk(2 * cc + 9, 0, true, true)) : 0u);
+        }
+        CK(cudaMalloc(&ctx->tabF16, sizeof(uint4) * t16.size()));
+        CK(cudaMemcpy(ctx->tabF16, t16.data(), sizeof(uint4) * t16.size(), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&ctx->tabM16, sizeof(uint2) * 32));
+        CK(cudaMemcpy(ctx->tabM16, m16.data(), sizeof(uint2) * 32, cudaMemcpyHostToDevice));
+      }
       CK(cudaMalloc(&ctx->tabF, sizeof(float4) * tf.size()));
       CK(cudaMemcpy(ctx->tabF, tf.data(), sizeof(float4) * tf.size(), cudaMemcpyHostToDevice));
       CK(cudaMalloc(&ctx->tabA, sizeof(float4) * ta.size()));
@@ -838,7 +878,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
   void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -979,6 +1019,7 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
     LrtArgs t{};
     t.R = c.R; t.M = c.M; t.N = c.N; t.L = ctx->L; t.K = c.K; t.nch = ctx->nch16; t.kw = ctx->kw; t.LS = ctx->LS;
     t.NT = ctx->NT; t.NTF = ctx->NTF; t.coefm = ctx->coef + (size_t)(c.K / 2) * ctx->QS;
+    t.tabF16 = ctx->tabF16; t.tabM16 = ctx->tabM16;
     t.tau_lo = c.tau_lo; t.tau_hi = c.tau_hi; t.excl0 = c.exclude_auto_zero_delay;
     t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
     t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
