@@ -175,7 +175,8 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* state, int block, double* lo
    buffers, block, outputs) on a non-legacy stream and replays the graph afterwards
    (single GPU; SQNGD_NO_GRAPH=1 disables).
    Profiling (for the roofline in bench.py): when enabled, sqngd_step runs eagerly and every
-   fused AF kernel launch is bracketed by CUDA events on its launch stream.  sqngd_profile_read synchronizes and
+   launch of the dominant fused kernel (k_af for the FFT engine, k_lrt for the Chebyshev
+   engine) is bracketed by CUDA events on its launch stream.  sqngd_profile_read synchronizes and
    returns, per kernel class (0 forward, 1 Step-A adjoint, 2 Step-B adjoint), the summed
    device milliseconds ms[3] and launch counts count[3], plus `launches` = every kernel the
    library launched since the last reset (all classes, small kernels included). */

@@ -15,7 +15,7 @@
 // path of Eq. 36 with the node modulation V_q(n) = e^{j 2 pi (n - n_c) f*_q / N}
 // (k_xhat + k_node); the dense (K x Q) Doppler contraction and its adjoint run
 // fused with the cell epilogue in k_lr; the adjoint correlations go back through
-// the FFT path at the Q nodes only (k_adj_g, k_lrB_tail).  Transforms per
+// the FFT path at the Q nodes only (k_adj_g, k_adj_gc).  Transforms per
 // evaluation drop from O(M^2 K) to O(M^2 Q).
 //
 // Symmetry: the uniform grid and the Chebyshev nodes are both symmetric about the
@@ -877,7 +877,7 @@ struct AdjGArgs {
   const float2* H;       // [R][M][P] filter spectra / P (Step B)
   float2* out;           // [units][P] spectral partials
   // Step B: the last of the M groups of a node (r, m, q) to finish sums their partials over l
-  // (fixed order), transforms back and demodulates (k_lrB_tail's work, without a launch).
+  // (fixed order), transforms back and demodulates (used when SQNGD_LR_CTA=0; else k_adj_gc).
   int* cnt;              // [R M Q] arrival counters (zero between launches: the last group resets)
   const float2* Vt;      // [Q][N] node modulation
   float2* tslot;         // [R M Q][NS] time-domain node partials
@@ -886,7 +886,7 @@ struct AdjGArgs {
 
 // Node adjoint correlations, one transform per unit:
 //   G^_{ml,q} = FFT_P(G^ placed at (-tau) mod P) (rescaled to the restart's shift), then
-//   Step B (WRT 2), unit ((r M + m) Q + q) M + l:  out = G^ . H_l            (sum over l: k_lrB_tail)
+//   Step B (WRT 2), unit ((r M + m) Q + q) M + l:  out = G^ . H_l            (sum over l: the last group)
 //   Step A (WRT 1), unit ((r M + l) M + m) Q + q:  out = X~_{m,q} . conj(G^)  (sum over m, q: combine)
 template <class PL, int G, int MINB, int WRT>
 __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, const float2* __restrict__ ftw) {
@@ -1067,46 +1067,6 @@ __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const fl
     if (n < N) {
       const float2 z = cmul(acc[i], __ldg(vr + n));
       o[n] = make_float2(z.x, -z.y);  // e conj(V_q)
-    }
-  }
-}
-
-// Step B node tail, unit (r M + m) Q + q:  e = IFFT_P(sum_l G^_{ml,q} H_l) (fixed order),
-// out[u][n] = e(n) conj(V_q(n)) for n < N (row stride NS, even: the combine reads float4 pairs):
-// the node's share of dL/ds_m^* before the sum over q.
-template <class PL, int G>
-__global__ void __launch_bounds__(PL::T* G)
-    k_lrB_tail(int units, int M, int Q, int N, int NS, const float2* __restrict__ slots, const float2* __restrict__ Vt,
-               const float2* __restrict__ ftw, float2* __restrict__ out) {
-  constexpr int E = PL::E, T = PL::T, P = PL::P;
-  extern __shared__ float4 smem_raw[];
-  const int grp = threadIdx.x / T, t = threadIdx.x % T;
-  const int u = blockIdx.x * G + grp;
-  float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
-  GroupSync sync{1 + grp, T, group_mask(T)};
-  const int uu = u < units ? u : units - 1;
-  const int q = uu % Q;
-  float2 v[E];
-#pragma unroll
-  for (int i = 0; i < E; ++i) v[i] = make_float2(0.f, 0.f);
-  for (int l = 0; l < M; ++l) {
-    const float2* sp = slots + ((size_t)uu * M + l) * P;
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cadd(v[i], __ldg(sp + t + i * T));
-  }
-#pragma unroll
-  for (int i = 0; i < E; ++i) v[i].y = -v[i].y;
-  int par = 0;
-  fft<PL, -1>(v, ftw, xbuf, t, par, sync);  // v = conj(e)
-  if (u >= units) return;
-  const float2* vr = Vt + (size_t)q * N;
-  float2* o = out + (size_t)uu * NS;
-#pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const int n = t + i * T;
-    if (n < N) {
-      const float2 z = cmul(v[i], __ldg(vr + n));
-      o[n] = make_float2(z.x, -z.y);
     }
   }
 }

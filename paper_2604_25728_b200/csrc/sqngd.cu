@@ -300,10 +300,6 @@ struct Launch {
     if (wrt == 2) k_adj_gc<PLN, NGC, 2><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
     else k_adj_gc<PLN, NGC, 1><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
   }
-  static void lrB_tail(int units, int M, int Q, int N, int NS, const float2* slots, const float2* Vt,
-                       const float2* ftw, float2* out, cudaStream_t st) {
-    k_lrB_tail<PL, G><<<(units + G - 1) / G, THREADS, smem_fft(), st>>>(units, M, Q, N, NS, slots, Vt, ftw, out);
-  }
   static cudaError_t prepare_lr() {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_node<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
@@ -318,9 +314,7 @@ struct Launch {
       return e;
     if ((e = cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c())))
       return e;
-    if ((e = cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c())))
-      return e;
-    return cudaFuncSetAttribute(k_lrB_tail<PL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft());
+    return cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c());
   }
 };
 
@@ -1147,7 +1141,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     ca.part = ctx->part;
     ca.part.scale = nullptr;  // node cotangents were rescaled in k_adj_g
     if (wrt == SQNGD_WRT_TRANSMIT) {
-      const int tu = c.R * c.M * ctx->Q;  // (k_adj_g's last group per node did k_lrB_tail's work)
+      const int tu = c.R * c.M * ctx->Q;  // node time-domain partials (k_adj_gc / k_adj_g's last groups)
       CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // S and the metrics from k_lr_finish
       ca.K = ctx->Q; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = 0; ca.u_hi = tu; ca.part.g = ctx->tslot;
       ca.len = c.N; ca.extra = 1.0; ca.fin = 1; ca.out = nullptr;
