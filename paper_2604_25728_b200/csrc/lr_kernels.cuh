@@ -489,27 +489,36 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
   uint32_t aErh[4], aErl[4], aEih[4], aEil[4], aOrh[4], aOrl[4], aOih[4], aOil[4];  // TF32 3x
   float nm2[2] = {0.f, 0.f};
   if constexpr (F16) {
+    // this lane's four K columns k = 2c, 2c+1, 2c+8, 2c+9 -> (part, j): only those node values
+    // are loaded and converted (the quad's columns cover every j for the node maximum)
     const float2* Rp = a.Rn + (size_t)pr * Q * a.LS;
-    float xs[4][2][5];  // (E_re, E_im, O_re, O_im) x row x j
+    uint32_t* frag[4] = {aEr, aEi, aOr, aOi};
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int pidx = 0; pidx < 4; ++pidx)
 #pragma unroll
-      for (int j = 0; j < 5; ++j) {
+      for (int i = 0; i < 4; ++i) frag[pidx][i] = 0u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = 2 * cq + (t & 1) + 8 * (t >> 1);
+      const int part = k / 5, j = k - 5 * part;  // part 0: hi, 1: lo, 2: hi, 3: zero column
+      const bool col = part < 3 && j < QH;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
         float2 x = make_float2(0.f, 0.f), y = x;
-        if (j < QH && inL[h]) {
+        if (col && inL[h]) {
           x = __ldg(Rp + (size_t)j * a.LS + idx[h]);
           y = __ldg(Rp + (size_t)(Q - 1 - j) * a.LS + idx[h]);
         }
-        xs[0][h][j] = x.x + y.x; xs[1][h][j] = x.y + y.y; xs[2][h][j] = x.x - y.x; xs[3][h][j] = x.y - y.y;
         nm2[h] = fmaxf(nm2[h], fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)));
-      }
-    uint32_t* frag[4] = {aEr, aEi, aOr, aOi};
+        const float v4[4] = {x.x + y.x, x.y + y.y, x.x - y.x, x.y - y.y};
+        const int reg = h + 2 * (t >> 1), sh = 16 * (t & 1);
 #pragma unroll
-    for (int pidx = 0; pidx < 4; ++pidx) {
-      frag[pidx][0] = f16_pair(2 * cq, xs[pidx][0]);
-      frag[pidx][1] = f16_pair(2 * cq, xs[pidx][1]);
-      frag[pidx][2] = f16_pair(2 * cq + 8, xs[pidx][0]);
-      frag[pidx][3] = f16_pair(2 * cq + 8, xs[pidx][1]);
+        for (int pidx = 0; pidx < 4; ++pidx) {
+          const __half hi = __float2half_rn(v4[pidx]);
+          const __half hv = part == 1 ? __float2half_rn(v4[pidx] - __half2float(hi)) : hi;
+          frag[pidx][reg] |= (uint32_t)__half_as_ushort(hv) << sh;
+        }
+      }
     }
   } else {
     float Er[4], Ei[4], Or[4], Oi[4];
