@@ -414,8 +414,8 @@ __device__ __forceinline__ void split4(const float (&x)[4], uint32_t (&h)[4], ui
 }
 
 // Forward contraction in FP16 with the 3-term split packed along K (m16n8k16, one MMA per
-// product): A row = [hi(x_0..x_4) | lo(x_0..x_4) | hi(x_0..x_4) | 0], B column =
-// [hi(c_0..c_4); hi(c_0..c_4); lo(c_0..c_4); 0], so A.B = x_hi c_hi + x_lo c_hi + x_hi c_lo.
+// product): the 15 used K columns hold hi(x_j), lo(x_j), hi(x_j) against hi(c_j), hi(c_j),
+// lo(c_j) (j < 5; layout in k_lrt), so A.B = x_hi c_hi + x_lo c_hi + x_hi c_lo.
 // Range: |x| <= 2N <= 8192 and |c| < 3 fit FP16; lo parts below the FP16 normal range lose at
 // most 6e-8 absolute each, i.e. < 2e-7 N per cell (the parity floor is 2e-6 N).
 #ifndef SQNGD_LRT_F16
@@ -489,35 +489,39 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
   uint32_t aErh[4], aErl[4], aEih[4], aEil[4], aOrh[4], aOrl[4], aOih[4], aOil[4];  // TF32 3x
   float nm2[2] = {0.f, 0.f};
   if constexpr (F16) {
-    // this lane's four K columns k = 2c, 2c+1, 2c+8, 2c+9 -> (part, j): only those node values
-    // are loaded and converted (the quad's columns cover every j for the node maximum)
+    // K layout (16 columns): lane c holds k = 2c, 2c+1 (registers 0/1) and 2c+8, 2c+9 (2/3) and
+    // owns node pair j = c: (hi_c, lo_c | hi_c, e_c) with e = hi_4, lo_4, hi_4, 0 for c = 0..3;
+    // the host B table holds the matching (hi(a_c), hi(a_c) | lo(a_c), ...) rows, so the sum over K
+    // is x_hi a_hi + x_lo a_hi + x_hi a_lo for every j < 5.  Each lane loads two node pairs.
     const float2* Rp = a.Rn + (size_t)pr * Q * a.LS;
-    uint32_t* frag[4] = {aEr, aEi, aOr, aOi};
+    const bool own = cq < QH, ext = QH > 4 && cq < 3;
 #pragma unroll
-    for (int pidx = 0; pidx < 4; ++pidx)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) frag[pidx][i] = 0u;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int k = 2 * cq + (t & 1) + 8 * (t >> 1);
-      const int part = k / 5, j = k - 5 * part;  // part 0: hi, 1: lo, 2: hi, 3: zero column
-      const bool col = part < 3 && j < QH;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float2 x = make_float2(0.f, 0.f), y = x;
-        if (col && inL[h]) {
-          x = __ldg(Rp + (size_t)j * a.LS + idx[h]);
-          y = __ldg(Rp + (size_t)(Q - 1 - j) * a.LS + idx[h]);
+    for (int h = 0; h < 2; ++h) {
+      float2 x = make_float2(0.f, 0.f), y = x, x4 = x, y4 = x;
+      if (inL[h]) {
+        if (own) {
+          x = __ldg(Rp + (size_t)cq * a.LS + idx[h]);
+          y = __ldg(Rp + (size_t)(Q - 1 - cq) * a.LS + idx[h]);
         }
-        nm2[h] = fmaxf(nm2[h], fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)));
-        const float v4[4] = {x.x + y.x, x.y + y.y, x.x - y.x, x.y - y.y};
-        const int reg = h + 2 * (t >> 1), sh = 16 * (t & 1);
-#pragma unroll
-        for (int pidx = 0; pidx < 4; ++pidx) {
-          const __half hi = __float2half_rn(v4[pidx]);
-          const __half hv = part == 1 ? __float2half_rn(v4[pidx] - __half2float(hi)) : hi;
-          frag[pidx][reg] |= (uint32_t)__half_as_ushort(hv) << sh;
+        if (ext) {
+          x4 = __ldg(Rp + (size_t)4 * a.LS + idx[h]);
+          y4 = __ldg(Rp + (size_t)(Q - 5) * a.LS + idx[h]);
         }
+      }
+      nm2[h] = fmaxf(fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)),
+                     fmaxf(fmaf(x4.x, x4.x, x4.y * x4.y), fmaf(y4.x, y4.x, y4.y * y4.y)));
+      const float vc[4] = {x.x + y.x, x.y + y.y, x.x - y.x, x.y - y.y};
+      const float v4[4] = {x4.x + y4.x, x4.y + y4.y, x4.x - y4.x, x4.y - y4.y};
+      uint32_t* frag[4] = {aEr, aEi, aOr, aOi};
+#pragma unroll
+      for (int pidx = 0; pidx < 4; ++pidx) {
+        const __half hc = __float2half_rn(vc[pidx]);
+        const __half lc = __float2half_rn(vc[pidx] - __half2float(hc));
+        const __half h4 = __float2half_rn(v4[pidx]);
+        const __half l4 = __float2half_rn(v4[pidx] - __half2float(h4));
+        const __half e = cq == 1 ? l4 : h4;  // lane 3: x4 = y4 = 0
+        frag[pidx][h] = (uint32_t)__half_as_ushort(hc) | ((uint32_t)__half_as_ushort(lc) << 16);
+        frag[pidx][2 + h] = (uint32_t)__half_as_ushort(hc) | ((uint32_t)__half_as_ushort(e) << 16);
       }
     }
   } else {

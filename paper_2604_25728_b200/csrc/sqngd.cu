@@ -792,11 +792,20 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
           if (part < 2) return __half_as_ushort(h);
           return f16(x - (double)__half2float(h));
         };
+        // K row k (k_lrt layout): lane c = (k mod 8) / 2 owns node pair j = c; rows 2c, 2c+1 hold
+        // hi(c_c) (against hi(x_c), lo(x_c)), row 2c+8 lo(c_c) (against hi(x_c)), row 2c+9 the
+        // pair j = 4 share: hi(c_4), hi(c_4), lo(c_4), 0 for c = 0..3.
         auto Bk = [&](int k, int p, bool is_alpha, bool mid) -> uint16_t {  // B[k][pair p]
-          if (k >= 15) return 0;
-          const int part = k / 5, j = k - 5 * part;
+          const int cc = (k & 7) >> 1, t = k & 1, hi_half = k >> 3;
+          int j = cc, part = hi_half ? 2 : 0;
+          if (hi_half && t) {
+            if (cc == 3) return 0;
+            j = 4;
+            part = cc == 2 ? 2 : 0;
+          }
+          if (j >= QH) return 0;
           double c;
-          if (mid) c = (j < QH) ? lr_ell[(size_t)Kp * Q + j] : 0.0;
+          if (mid) c = lr_ell[(size_t)Kp * Q + j];
           else c = is_alpha ? alpha(j, p) : beta(j, p);
           return split16(c, part);
         };
