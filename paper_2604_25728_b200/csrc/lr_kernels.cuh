@@ -371,7 +371,6 @@ __global__ void __launch_bounds__(256) k_lr(const LrArgs a) {
 // The middle bin of an odd K (f = grid centre, beta = 0) is one extra cell per lag, done on
 // the CUDA cores by the last warp of the unit.
 struct LrtArgs {
-  int units;                                 // R M^2 nch (the grid may be smaller: persistent when kw == 1)
   int R, M, N, L, K, nch, kw, LS, NT, NTF;  // nch: 16-lag chunks; NT: 8-pair tiles of the K/2 bin pairs; NTF: full ones
   int tau_lo, tau_hi, excl0;
   float bp, invN;
@@ -452,27 +451,12 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
   float* rs = reinterpret_cast<float*>(lr_smem);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int g = lane >> 2, cq = lane & 3;
-  // persistent over units when kw == 1 (grid = resident warps): while unit u runs, the next
-  // unit's node values are prefetched into L1
-  for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-  if (u + (int)gridDim.x < a.units) {
-    const int un = u + gridDim.x, chn = un % a.nch, prn = un / a.nch;
-    const float2* Rq = a.Rn + (size_t)prn * Q * a.LS;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int ix = chn * 16 + g + 8 * h;
-      if (ix < a.L)
-#pragma unroll
-        for (int j = 0; j < QH; ++j) {
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(Rq + (size_t)j * a.LS + ix));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(Rq + (size_t)(Q - 1 - j) * a.LS + ix));
-        }
-    }
-  }
-  const int ch = u % a.nch;
-  const int pr = u / a.nch;
+  // grid (chunk, m M + l, restart): no integer divisions by runtime sizes
+  const int ch = blockIdx.x;
+  const int pr = (blockIdx.z * a.M * a.M) + blockIdx.y;
+  const int u = pr * a.nch + ch;
   const int M = a.M;
-  const int l = pr % M, m = (pr / M) % M;
+  const int m = blockIdx.y / M, l = blockIdx.y - m * M;
   const bool is_auto = m == l;
   int idx[2];
   bool inL[2], valid[2];
@@ -839,11 +823,10 @@ __global__ void __launch_bounds__(256) k_lrt(const LrtArgs a) {
     a.part.key[2 * (size_t)u + 1] = is_auto ? 0ull : key;
     a.part.m[u] = mw;
     a.part.S[u] = Su;
-    const int r = pr / (M * M);
+    const int r = blockIdx.z;
     if (key) atomicMax(is_auto ? &a.lred[r].key_a : &a.lred[r].key_c, key);
     if (LM != 0 && mw > 0.f) atomicMax(&a.lred[r].mbits, __float_as_uint(mw));
   }
-  }  // units
 }
 
 // Per restart: the global shift m (LrRed), S = sum_u S_u (m_u -> m), the reduction record

@@ -87,7 +87,6 @@ struct sqngd_ctx_s {
   bool lr_tc = true;           // k_lrt (mma.sync 3xTF32) instead of the FP32 k_lr
   bool lr_cta = true;          // k_adj_gc (sums inside the CTA) instead of k_adj_g (slots + arrival tail)
   int nch16 = 0, NT = 0, NTF = 0;
-  int64_t lrt_grid = 0;        // persistent k_lrt grid (resident one-warp CTAs), 0: one CTA per unit
   float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
   uint4* tabF16 = nullptr;     // [NT][32] k_lrt forward B fragments (FP16 packed split)
@@ -354,8 +353,8 @@ struct LrLaunch {
   }
   // tensor-core variant
   template <int LM, bool HW, bool GRAD>
-  static void go_t(const LrtArgs& a, int grid, size_t smem, cudaStream_t st) {
-    k_lrt<Q, LM, HW, GRAD><<<grid, 32 * a.kw, smem, st>>>(a);
+  static void go_t(const LrtArgs& a, int /*units*/, size_t smem, cudaStream_t st) {
+    k_lrt<Q, LM, HW, GRAD><<<dim3(a.nch, a.M * a.M, a.R), 32 * a.kw, smem, st>>>(a);
   }
   static void launch_t(int lm, bool hw, bool grad, const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
     if (lm == 0) { hw ? go_t<0, true, false>(a, units, smem, st) : go_t<0, false, false>(a, units, smem, st); return; }
@@ -652,13 +651,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     if (ctx->lr_tc) {  // measured (C3): one warp per unit is best for k_lrt (no CTA-level reduction)
       ctx->kw = 1;
       ctx->lr_smem = 0;
-      int bps = 0;  // persistent grid: all resident one-warp CTAs
-      with_Q(ctx->Q, [&](auto Qc) { decltype(Qc)::occupancy_t(&bps, 32, 0); });
-      ctx->lrt_grid = (int64_t)ctx->sms * std::max(1, bps);
-      // measured: the persistent grid (+ L1 prefetch of the next unit) is 3-5% slower than one CTA
-      // per unit at C3 and C5, so it is opt-in
-      const char* ev = getenv("SQNGD_LRT_PERSIST");
-      if (!(ev && ev[0] == '1')) ctx->lrt_grid = 0;
+      // (a persistent grid with an L1 prefetch of the next unit's node values measured 3-5% slower)
     }
     if (const char* ev = getenv("SQNGD_LR_KW")) {  // tuning override
       const int kw = atoi(ev);
@@ -1031,9 +1024,7 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
     t.R = c.R; t.M = c.M; t.N = c.N; t.L = ctx->L; t.K = c.K; t.nch = ctx->nch16; t.kw = ctx->kw; t.LS = ctx->LS;
     t.NT = ctx->NT; t.NTF = ctx->NTF; t.coefm = ctx->coef + (size_t)(c.K / 2) * ctx->QS;
     t.tabF16 = ctx->tabF16; t.tabM16 = ctx->tabM16;
-    t.units = (int)ctx->units_lr;
-    const int grid = ctx->kw == 1 && ctx->lrt_grid > 0 ? (int)std::min<int64_t>(ctx->units_lr, ctx->lrt_grid)
-                                                        : (int)ctx->units_lr;
+    const int grid = (int)ctx->units_lr;
     t.tau_lo = c.tau_lo; t.tau_hi = c.tau_hi; t.excl0 = c.exclude_auto_zero_delay;
     t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
     t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
