@@ -67,17 +67,30 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
   const bool ok = e0 < MN;
   const size_t e = (size_t)r * MN + (ok ? e0 : 0);
   const float x = z[e];
-  int lo = 0, hi = BR;
-  while (lo < hi) { int mid = (lo + hi) >> 1; if (rs[mid] <= x) lo = mid + 1; else hi = mid; }
-  const int cnt = lo;
+  // counts #{rs < v} (strict) or #{rs <= v} over the ascending thresholds: a guess from the
+  // near-uniform spacing (rho_i ~ (i + 1/2) / BR), corrected by a short walk, with a binary
+  // search if the walk would be long -- the same exact count as a plain binary search
+  auto count = [&](float v, bool le) -> int {
+    int i = (int)floorf(v * (float)BR + 0.5f);
+    i = i < 0 ? 0 : (i > BR ? BR : i);
+    for (int step = 0; step < 6; ++step) {
+      const bool below = i > 0 && (le ? rs[i - 1] > v : rs[i - 1] >= v);   // count too high
+      const bool above = i < BR && (le ? rs[i] <= v : rs[i] < v);          // count too low
+      if (!below && !above) return i;
+      i += above ? 1 : -1;
+    }
+    int lo = 0, hi = BR;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (le ? rs[mid] <= v : rs[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const int cnt = count(x, true);
   if (s_soft || dq) {
     const float W = 12.0f / c;
-    lo = 0; hi = cnt;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if (rs[mid] < x - W) lo = mid + 1; else hi = mid; }
-    const int i0 = lo;
-    lo = cnt; hi = BR;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if (rs[mid] <= x + W) lo = mid + 1; else hi = mid; }
-    const int i1 = lo;
+    const int i0 = count(x - W, false);
+    const int i1 = count(x + W, true);
     float resid = 0.f, sech = 0.f;
     for (int j = i0 + sub; j < i1; j += LPE) {
       const float u = c * (x - rs[j]);
