@@ -520,6 +520,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: beta_or_p must be > 0 for LSE / PNORM");
   if (cfg.B * cfg.r_n > 8192) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: B*r_n > 8192");
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: rank/world");
+  if (cfg.doppler_engine < 0 || cfg.doppler_engine > 2)
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: doppler_engine");
   const int L = 2 * cfg.N - 1;
   if ((double)cfg.M * cfg.M * L * cfg.K >= 4294967295.0)
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: M^2 (2N-1) K cell index exceeds 32 bits");
@@ -590,10 +592,6 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
 
   // Doppler engine (include/sqngd.h SQNGD_ENGINE_*): node count Q for lr_tol, tables, unit split.
   std::vector<double> lr_fq, lr_ell;
-  if (cfg.doppler_engine < 0 || cfg.doppler_engine > 2) {
-    delete ctx;
-    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: doppler_engine");
-  }
   if (cfg.doppler_engine != SQNGD_ENGINE_FFT && world == 1 && cfg.K >= 3) {
     const double tol = cfg.lr_tol > 0 ? cfg.lr_tol : 1e-7;
     for (int Q = 4; Q <= 16; Q += 2) {

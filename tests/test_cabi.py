@@ -62,7 +62,9 @@ def test_create_rejects_invalid_config_without_gpu(lib):
     from paper_2604_25728_b200.configs import C1
 
     h = C.c_void_p()
-    for bad in (C1.with_(B=1), C1.with_(N=1), C1.with_(K=0), C1.with_(tau_lo=-64), C1.with_(N=8192)):
+    empty_roi = C1.with_(M=1, tau_lo=0, tau_hi=0)      # auto map only, tau = 0 excluded (Eq. 8): no cells
+    for bad in (C1.with_(B=1), C1.with_(N=1), C1.with_(K=0), C1.with_(tau_lo=-64), C1.with_(N=8192), empty_roi,
+                C1.with_(doppler_engine=3)):
         cfg = sqngd.make_config(bad)
         st = lib.sqngd_create(C.byref(cfg), 0, None, 0, 1, C.byref(h))
         assert st == sqngd.E_INVALID

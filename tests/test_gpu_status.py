@@ -1,0 +1,82 @@
+"""Device-side error statuses through the C-ABI (include/sqngd.h): latched conditions are
+returned by sqngd_sync, and sqngd_step keeps the last finite iterate."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2604_25728_b200 import inputs, sqngd  # noqa: E402
+from paper_2604_25728_b200.configs import Cfg  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+ENGINES = [sqngd.ENGINE_FFT, sqngd.ENGINE_CHEBYSHEV]
+
+
+def T(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device=DEV)
+
+
+def cfg(engine, **kw):
+    return Cfg("st", M=2, N=48, B=4, K=31, f_lo=-0.5, f_hi=0.5, r_n=4, loss_mode=sqngd.LOSS_LSE, beta_or_p=60.0,
+               doppler_engine=engine, n_h=1, n_x=1, **kw)
+
+
+def sw(c, seed=3):
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=seed)
+    s = np.exp(2j * np.pi * z.astype(np.float64)).astype(np.complex64)
+    return z, s, s.copy()
+
+
+def expect(ctx, status):
+    with pytest.raises(sqngd.SqngdError) as ei:
+        ctx.sync()
+    assert ei.value.status == status, (ei.value.status, str(ei.value))
+    ctx.sync()  # the latch is cleared by the read
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_zero_filter_row_is_degenerate(engine):
+    """|w_m^H s_m| = 0 (Eq. 38 undefined for the SNRL term): E_DEGENERATE."""
+    c = cfg(engine)
+    _, s, w = sw(c)
+    w[0, 1] = 0
+    ctx = sqngd.Context(c)
+    ctx.af_forward(T(s), T(w))
+    expect(ctx, sqngd.E_DEGENERATE)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_nan_input_is_nonfinite(engine):
+    c = cfg(engine)
+    _, s, w = sw(c)
+    w[0, 0, 5] = np.nan
+    ctx = sqngd.Context(c)
+    ctx.loss_grad_s(T(s), T(w), sqngd.WRT_TRANSMIT)
+    expect(ctx, sqngd.E_NONFINITE)
+
+
+def test_unsorted_thresholds_are_invalid():
+    c = cfg(sqngd.ENGINE_FFT)
+    z, _, _ = sw(c)
+    rho = inputs.init_thresholds(1, c.B, c.r_n)
+    rho[0, [3, 4]] = rho[0, [4, 3]]
+    ctx = sqngd.Context(c)
+    ctx.quantize(T(z), T(rho))
+    expect(ctx, sqngd.E_INVALID)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_step_keeps_last_finite_iterate(engine):
+    """A non-finite gradient latches E_NONFINITE and sqngd_step applies no update."""
+    c = cfg(engine)
+    z, _, w = sw(c)
+    rho = inputs.init_thresholds(1, c.B, c.r_n)
+    w[0, 0, 7] = np.inf
+    ctx = sqngd.Context(c)
+    st = ctx.new_state(T(z), T(rho), T(w))
+    z0, rho0, w0 = st["z"].clone(), st["rho"].clone(), st["w"].clone()
+    ctx.step(st, sqngd.BLOCK_AB)
+    expect(ctx, sqngd.E_NONFINITE)
+    assert torch.equal(st["z"], z0) and torch.equal(st["rho"], rho0)
+    assert torch.equal(torch.view_as_real(st["w"]).nan_to_num(), torch.view_as_real(w0).nan_to_num())
