@@ -37,6 +37,10 @@ namespace sq {
 
 enum { MODE_FWD = 0, MODE_ADJ_A = 1, MODE_ADJ_B = 2 };
 
+#ifndef SQNGD_AF_TWS
+#define SQNGD_AF_TWS 0  // shared-memory twiddles: measured no gain (C3 FFT engine, C4)
+#endif
+
 struct KP {
   int R, M, N, K, L, P;
   int tau_lo, tau_hi, excl0;
@@ -356,6 +360,15 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   grpops.par = 0;
   grpops.t = t;
 
+#if SQNGD_AF_TWS
+  // the plan's Stockham twiddles, staged once per (persistent) CTA in shared memory
+  float2* tws = reinterpret_cast<float2*>(smem_raw) + G * GS::TOTAL;
+  for (int i = threadIdx.x; i < PL::TWSIZE; i += blockDim.x) tws[i] = __ldg(ftw + i);
+  __syncthreads();
+  const float2* twt = tws;
+#else
+  const float2* twt = ftw;
+#endif
   const int M = kp.M, N = kp.N, K = kp.K;
   const int mode = kp.loss_mode;
   const float bp = kp.beta_or_p;
@@ -411,7 +424,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
 #pragma unroll
         for (int i = 0; i < E; ++i) v[i] = make_float2(acc[i].x, -acc[i].y);
       }  // G phase: v already holds G
-      fft<PL, -1>(v, ftw, xbuf, t, par, grpops.sync);
+      fft<PL, -1, SQNGD_AF_TWS != 0>(v, twt, xbuf, t, par, grpops.sync);
       // ---- post
       if (slice_ph) {
         // v[i] = conj(r[j]), j = t + i T, A(tau) = r[(-tau) mod P]  (a5: fused epilogue)

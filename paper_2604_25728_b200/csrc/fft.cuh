@@ -183,7 +183,8 @@ struct GroupSync {
 // DIR = -1 forward, +1 unnormalized inverse.  sbuf: 2 * PADDED float2 of group-private
 // smem; tw: the plan's twiddle table (global, read through L1).
 // par: exchange parity (alternates the two buffers); must start equal in all threads.
-template <class PL, int DIR>
+// TWS: the twiddle table `tw` is in shared memory (plain loads) instead of global (__ldg).
+template <class PL, int DIR, bool TWS = false>
 __device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2* __restrict__ tw, float2* sbuf, int t,
                                     int& par, const GroupSync& sync) {
   constexpr int E = PL::E, T = PL::T;
@@ -201,7 +202,7 @@ __device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2* __restrict
         const float2* twp = tw + PL::twoff(p) + (j & (Ns - 1));
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          const float2 w = __ldg(twp + (r - 1) * Ns);
+          const float2 w = TWS ? twp[(r - 1) * Ns] : __ldg(twp + (r - 1) * Ns);
           x[r] = DIR < 0 ? cmul(x[r], w) : cmulc(x[r], w);
         }
       }

@@ -207,7 +207,9 @@ struct Launch {
   }
 
   template <int MODE>
-  static size_t smem() { return (size_t)G * GroupSmem<PL, MODE>::TOTAL * sizeof(float2); }
+  static size_t smem() {
+    return (size_t)G * GroupSmem<PL, MODE>::TOTAL * sizeof(float2) + (SQNGD_AF_TWS ? PL::TWSIZE * sizeof(float2) : 0);
+  }
   static size_t smem_fft() { return (size_t)G * FftSmem<PL>::TOTAL * sizeof(float2) + 16; }
 
   static cudaError_t prepare(int* blocks_per_sm) {
