@@ -671,7 +671,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
   CK(cudaMalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
   CK(cudaMalloc(&ctx->H, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
-  CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * cfg.K * P));
+  // X cache: K bins (FFT engine) or Q nodes (Chebyshev engine; Q may exceed K when forced)
+  CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * std::max(cfg.K, ctx->Q) * P));
   CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&ctx->ftwn, sizeof(float2) * ftwn_host.size()));

@@ -83,6 +83,10 @@ def fwd_cases():
         Cfg("wide", M=2, N=64, B=4, K=61, f_lo=-1.5, f_hi=1.5),              # more nodes
         Cfg("p2048", M=2, N=1024, B=16, K=33, f_lo=-0.5, f_hi=0.5),
         Cfg("p8192", M=1, N=4096, B=16, K=33, f_lo=-0.5, f_hi=0.5),
+        Cfg("n2", M=2, N=2, B=2, K=31, f_lo=-0.5, f_hi=0.5, r_n=1),          # 3 lags, one 16-lag chunk
+        Cfg("m1", M=1, N=33, B=4, K=63, f_lo=-0.5, f_hi=0.5),                 # no cross maps
+        Cfg("k3", M=2, N=40, B=4, K=3, f_lo=-0.05, f_hi=0.05),               # one bin pair + middle, Q = 6
+        Cfg("k5", M=2, N=40, B=4, K=5, f_lo=-0.5, f_hi=0.5),                 # partial tile, Q = 10
     ]
 
 
