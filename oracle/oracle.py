@@ -238,11 +238,17 @@ def step(cfg, state: dict, block: int = 3, grads_from=None):
     Step A (block & 1): n_h times [loss_grad on X_hard -> Adam(Re w, Im w) -> Pi_H].
     Step B (block & 2): n_x times [loss_grad on X_soft -> chain -> Adam(z), Adam(rho) -> rho projection].
     `grads_from`, if given, is a callable(kind, i, state) -> gradient arrays used
-    instead of the oracle's own (teacher forcing of Adam with an external gradient).
+    instead of the oracle's own (teacher forcing of Adam with an external gradient); in
+    generator mode Step B's pair is (dL/dtheta, dL/drho).
+    Generator mode (state["theta"] set, NEXT-2): z = f_theta(y0) at the start and after every
+    Step-B update; Step B's Adam acts on theta (rate cfg.lr_theta) instead of z (Alg. 1).
     Returns the per-inner-step loss history.
     """
     st = state
     hist = []
+    net = st.get("theta") is not None  # generator mode (NEXT-2): z = f_theta(y0), Adam on theta
+    if net:
+        st["z"] = _net_z(cfg, st)
     if block & 1:
         q = quantize(cfg, st["z"], st["rho"])
         for i in range(int(cfg.n_h)):
@@ -264,17 +270,57 @@ def step(cfg, state: dict, block: int = 3, grads_from=None):
                 gz, gr = grads_from("B", i, st)
             hist.append([m["loss"] for m in met])
             st["t_b"] += 1
-            adam(st["z"], st["m_z"], st["v_z"], gz, st["t_b"], cfg.lr_z, cfg.adam_b1, cfg.adam_b2, cfg.adam_eps)
+            if net:  # z = f_theta(y0): dL/dtheta through the generator (Eq. 20)
+                if grads_from is None:
+                    gth = _net_grad(cfg, st, gz)
+                else:
+                    gth = gz
+                adam(st["theta"], st["m_theta"], st["v_theta"], gth, st["t_b"], cfg.lr_theta, cfg.adam_b1,
+                     cfg.adam_b2, cfg.adam_eps)
+            else:
+                adam(st["z"], st["m_z"], st["v_z"], gz, st["t_b"], cfg.lr_z, cfg.adam_b1, cfg.adam_b2,
+                     cfg.adam_eps)
             adam(st["rho"], st["m_rho"], st["v_rho"], gr, st["t_b"], cfg.lr_z, cfg.adam_b1, cfg.adam_b2,
                  cfg.adam_eps)
             project_thresholds(st["rho"])
+            if net:
+                st["z"] = _net_z(cfg, st)
     return np.array(hist)
 
 
-def new_state(z, rho, w) -> dict:
+def _net_dims(cfg):
+    return int(cfg.M) * int(cfg.N), int(cfg.net_width), int(cfg.net_depth)
+
+
+def _net_z(cfg, st):
+    from oracle import net_oracle as NO
+
+    Din, W, D = _net_dims(cfg)
+    R = st["theta"].shape[0]
+    z, st["_tapes"] = NO.forward_batch(st["theta"], st["y0"], Din, W, D)
+    return np.ascontiguousarray(z.reshape(R, int(cfg.M), int(cfg.N)))
+
+
+def _net_grad(cfg, st, gz):
+    from oracle import net_oracle as NO
+
+    Din, W, D = _net_dims(cfg)
+    R = st["theta"].shape[0]
+    return np.ascontiguousarray(NO.backward_batch(st["theta"], st["_tapes"], np.asarray(gz).reshape(R, Din), Din, W, D))
+
+
+def new_state(z, rho, w, theta=None, y0=None) -> dict:
+    """fp64 optimizer state; with theta [R][P] and y0 [R][M N] the generator parameterizes z
+    (z is then recomputed as f_theta(y0) by step())."""
     z = _f64(z).copy()
     rho = _f64(rho).copy()
     w = _c128(w).copy()
-    return dict(z=z, rho=rho, w=w, m_z=np.zeros_like(z), v_z=np.zeros_like(z),
-                m_rho=np.zeros_like(rho), v_rho=np.zeros_like(rho),
-                m_w=np.zeros(w.size * 2), v_w=np.zeros(w.size * 2), t_a=0, t_b=0)
+    st = dict(z=z, rho=rho, w=w, m_z=np.zeros_like(z), v_z=np.zeros_like(z),
+              m_rho=np.zeros_like(rho), v_rho=np.zeros_like(rho),
+              m_w=np.zeros(w.size * 2), v_w=np.zeros(w.size * 2), t_a=0, t_b=0, theta=None)
+    if theta is not None:
+        st["theta"] = _f64(theta).copy()
+        st["y0"] = _f64(y0).copy()
+        st["m_theta"] = np.zeros_like(st["theta"])
+        st["v_theta"] = np.zeros_like(st["theta"])
+    return st

@@ -89,3 +89,39 @@ def random_sorted_thresholds(R: int, B: int, r_n: int, seed: int, jitter: float 
     base = (i + 0.5) / n
     rho = base[None, :] + jitter * (g.random((R, n)) - 0.5) / n
     return np.sort(rho, axis=1).astype(np.float32)
+
+
+# --------------------------------------------------------------------------- generator (NEXT-2)
+# Seeds of the generator draws are offset from the phase-parameter seeds so the streams differ.
+_Y0_SEED, _THETA_SEED = 500_000, 700_000
+
+
+def net_input(R: int, M: int, N: int, B: int, config_index: int = 0) -> np.ndarray:
+    """y0[R][M*N] fp32: the random normalized discrete phase Y0 of Alg. 1's initialization
+    (Eq. 19 vec() = the [m][n] flattening), levels b/B with b uniform in [0, B)."""
+    out = np.empty((R, M * N), dtype=np.float32)
+    for r in range(R):
+        u = uniform01_f32(_Y0_SEED + config_seed(config_index, r), M * N).astype(np.float64)
+        out[r] = (np.floor(u * B) / B).astype(np.float32)
+    return out
+
+
+def net_params(R: int, Din: int, W: int, D: int, config_index: int = 0, bias_scale: float = 0.0) -> np.ndarray:
+    """theta[R][P] fp32 in the flat C-ABI layout (include/sqngd.h, sqngd_net_*):
+    W_in [W][Din] | b_in [W] | D x (W1 [W][W] | b1 [W] | W2 [W][W] | b2 [W]) | W_out [Din][W] | b_out [Din].
+    Weights uniform in +-sqrt(3 / fan_in) (variance 1/fan_in); biases uniform in +-bias_scale
+    (0 by default)."""
+    sizes = [(W * Din, Din), (W, 0)]
+    for _ in range(D):
+        sizes += [(W * W, W), (W, 0), (W * W, W), (W, 0)]
+    sizes += [(Din * W, W), (Din, 0)]
+    P = sum(n for n, _ in sizes)
+    out = np.empty((R, P), dtype=np.float32)
+    for r in range(R):
+        u = uniform01_f32(_THETA_SEED + config_seed(config_index, r), P).astype(np.float64) * 2.0 - 1.0
+        o = 0
+        for n, fan_in in sizes:
+            scale = np.sqrt(3.0 / fan_in) if fan_in else bias_scale
+            out[r, o:o + n] = (u[o:o + n] * scale).astype(np.float32)
+            o += n
+    return out
