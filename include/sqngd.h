@@ -81,6 +81,10 @@ typedef struct {
   int32_t doppler_engine;          /* SQNGD_ENGINE_*: how the K Doppler bins are evaluated */
   double lr_tol;                   /* CHEBYSHEV: bound on |A_interp - A| / (||s|| ||w||)
                                       (0 => 1e-7); picks the node count Q at create       */
+  int32_t net_depth;               /* generator residual blocks D (paper: 5)       */
+  int32_t net_width;               /* generator hidden width W (paper: 128); 0 = no generator,
+                                      z is the direct parameter (Q13); else W % 8 == 0, <= 128 */
+  double lr_theta;                 /* Adam rate of theta (eta_x = 1e-5)             */
 } sqngd_config;
 
 /* Doppler engine (sqngd_config.doppler_engine).
@@ -118,6 +122,10 @@ typedef struct {
   float *m_z, *v_z, *m_rho, *v_rho; /* Adam moments, same shapes as z / rho               */
   float *m_w, *v_w;                 /* Adam moments of (Re w, Im w): [R][M][N][2]         */
   int64_t t_a, t_b;
+  /* Generator mode (cfg.net_width > 0): z = f_theta(y0) is written by sqngd_step (m_z, v_z unused)
+     and Step B's Adam acts on theta instead of z.  NULL when cfg.net_width == 0. */
+  float *theta, *m_theta, *v_theta; /* [R][sqngd_net_num_params] (layout: sqngd_net_forward)  */
+  const float* y0;                  /* [R][M N] fixed generator input (Alg. 1)       */
 } sqngd_state;
 
 /* Build the context: validates the config (SQNGD_E_INVALID), builds the fp64
@@ -165,11 +173,32 @@ sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho,
 /* a9: one Alg. 1 outer iteration restricted to `block`:
    A: n_h x [loss_grad(s_hard) -> Adam(Re w, Im w) -> Pi_H (Eq. 32)];
    B: n_x x [loss_grad(s_soft) -> Adam(z), Adam(rho) -> threshold projection (Q22)].
+   Generator mode: z = f_theta(y0) at the start and after every Step-B update; Step B's Adam
+   acts on theta (rate lr_theta) through sqngd_net_backward's adjoint instead of on z.
    loss_hist: NULL or DEVICE [R][n_h + n_x] doubles (loss of each inner step, in order,
    A first).  hard_out: NULL or DEVICE [R] metrics of the hard waveform after the block.
    On a latched non-finite value the remaining updates are skipped (state unchanged). */
 sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* state, int block, double* loss_hist,
                         sqngd_metrics* hard_out, sqngd_stream stream);
+
+/* Generator: z = f_theta(y0), the transmit-side ResNet of PAPER.md Eq. 20
+    with "5 residual blocks and a hidden width of 128 ... tanh ... sigmoid at the output"
+   (P:L583).  With Din = M N, W = cfg.net_width, D = cfg.net_depth (DESIGN.md §3 "Generator"):
+     h_0 = tanh(W_in y0 + b_in);  u_d = tanh(W1_d h_d + b1_d);  h_{d+1} = h_d + W2_d u_d + b2_d;
+     z = sigmoid(W_out h_D + b_out)
+   theta per restart, row-major, in this order:
+     W_in [W][Din] | b_in [W] | D x (W1 [W][W] | b1 [W] | W2 [W][W] | b2 [W]) | W_out [Din][W] | b_out [Din] | pad
+   where pad (< 4 floats, only when Din % 4 != 0) makes the per-restart stride P a multiple of 4;
+   the forward ignores it, Adam leaves it alone and the backward writes 0 there.
+   theta, y0 [R][Din], z [R][M][N] (= [R][Din]) are device pointers owned by the caller.
+   sqngd_net_forward keeps the activations (tape) in the context; sqngd_net_backward needs the tape
+   of the preceding forward with the same theta and y0, z its output, grad_z = dL/dz, and writes
+   every entry of grad_theta [R][P].  SQNGD_E_INVALID when the context has no generator. */
+int64_t sqngd_net_num_params(const sqngd_config* cfg); /* stride P per restart (parameters + pad);
+                                                         0 when net_width == 0 or invalid    */
+sqngd_status sqngd_net_forward(sqngd_ctx ctx, const float* theta, const float* y0, float* z, sqngd_stream stream);
+sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* y0, const float* z,
+                                const float* grad_z, float* grad_theta, sqngd_stream stream);
 
 /* sqngd_step captures itself into a CUDA graph on the first call with a given (state
    buffers, block, outputs) on a non-legacy stream and replays the graph afterwards

@@ -31,9 +31,12 @@ def num_params(Din: int, W: int, D: int) -> int:
 
 
 def unpack(theta: np.ndarray, Din: int, W: int, D: int) -> dict:
-    """Views into the flat parameter vector (same memory)."""
+    """Views into the flat parameter vector (same memory).  Entries past num_params (the C-ABI's
+    float4 stride padding, < 4 floats) are ignored."""
     theta = np.asarray(theta)
-    assert theta.shape == (num_params(Din, W, D),), theta.shape
+    n = num_params(Din, W, D)
+    assert theta.ndim == 1 and n <= theta.size < n + 4, theta.shape
+    theta = theta[:n]
     o = 0
 
     def take(n, shape):
@@ -48,7 +51,7 @@ def unpack(theta: np.ndarray, Din: int, W: int, D: int) -> dict:
                             "W2": take(W * W, (W, W)), "b2": take(W, (W,))})
     p["W_out"] = take(Din * W, (Din, W))
     p["b_out"] = take(Din, (Din,))
-    assert o == theta.size
+    assert o == n
     return p
 
 
@@ -70,7 +73,8 @@ def forward(theta, y0, Din: int, W: int, D: int):
 
 
 def backward(theta, tape: dict, gz, Din: int, W: int, D: int):
-    """dL/dtheta (flat, same layout) and dL/dy0 for the upstream dL/dz."""
+    """dL/dtheta (flat, same layout and length as theta; 0 in any padding) and dL/dy0 for the
+    upstream dL/dz."""
     th = np.asarray(theta, np.float64)
     p = unpack(th, Din, W, D)
     g = np.zeros_like(th)

@@ -31,10 +31,9 @@ def flags(verbose: bool = False) -> list[str]:
     f = [
         "-gencode", "arch=compute_100a,code=sm_100a",
         "-O3", "-lineinfo", "--std=c++17",
-        "-Xcompiler", "-fPIC", "-shared",
+        "-Xcompiler", "-fPIC",
         "-I", os.path.join(ROOT, "include"),
         f'-DSQNGD_NCCL_PATH="{_nccl_path()}"',
-        "-ldl",
     ]
     if verbose:
         f += ["-Xptxas", "-v"]
@@ -42,19 +41,41 @@ def flags(verbose: bool = False) -> list[str]:
 
 
 def sources() -> list[str]:
-    return [os.path.join(CSRC, "sqngd.cu")]
+    # two translation units compiled in parallel: the AF/loss/gradient path and the generator
+    return [os.path.join(CSRC, "sqngd.cu"), os.path.join(CSRC, "net.cu")]
 
 
-def deps() -> list[str]:
-    return sorted(glob.glob(os.path.join(CSRC, "*")) + [os.path.join(ROOT, "include", "sqngd.h")])
+def deps(src: str | None = None) -> list[str]:
+    """Files a translation unit depends on (all of csrc/ and the header when src is None)."""
+    hdr = os.path.join(ROOT, "include", "sqngd.h")
+    allf = [p for p in glob.glob(os.path.join(CSRC, "*")) if not p.endswith(".o")]
+    if src is None:
+        return sorted(allf + [hdr])
+    if os.path.basename(src) == "net.cu":
+        return [src] + [os.path.join(CSRC, f) for f in ("net.cuh", "adam.cuh")]
+    return sorted([p for p in allf if os.path.basename(p) != "net.cu"] + [hdr])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in deps())
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
-    cmd = [NVCC, *flags(verbose), "-o", LIB + ".tmp", *sources()]
-    subprocess.check_call(cmd)
+    objs, procs = [], []
+    for src in sources():  # objects are kept (git-ignored) so an unchanged unit is not recompiled
+        obj = os.path.join(CSRC, os.path.basename(src) + ".o")
+        objs.append(obj)
+        stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(
+            os.path.getmtime(p) for p in deps(src))
+        if stale:
+            procs.append(subprocess.Popen([NVCC, *flags(verbose), "-c", "-o", obj + ".tmp", src]))
+            procs[-1].obj = obj
+    rcs = [p.wait() for p in procs]
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), "nvcc")
+    for p in procs:
+        os.replace(p.obj + ".tmp", p.obj)
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
+                           *objs, "-ldl"])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

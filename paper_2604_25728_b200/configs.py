@@ -43,6 +43,9 @@ class Cfg:
     n_x: int = 10
     doppler_engine: int = 0         # 0 auto, 1 per-bin FFT, 2 Chebyshev nodes (include/sqngd.h)
     lr_tol: float = 0.0             # Chebyshev engine error bound (0 => library default 1e-7)
+    net_depth: int = 0              # generator residual blocks (paper: 5); 0 with net_width 0
+    net_width: int = 0              # generator hidden width (paper: 128); 0 = z is the direct parameter
+    lr_theta: float = 1e-5          # Adam rate of the generator parameters (eta_x)
     iterations: int = 1
     index: int = 0                  # config number used for input seeds
 

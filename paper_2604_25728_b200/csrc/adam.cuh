@@ -1,0 +1,22 @@
+// Status bits and the Adam parameter block, shared by every translation unit (no device code
+// with external linkage here: common.cuh's functions stay in one TU).
+#pragma once
+
+namespace sq {
+
+enum : int { ST_INVALID = 1, ST_DEGENERATE = 2, ST_NONFINITE = 4 };
+
+// Adam hyper-parameters; the step count t = dt[which] + off + 1 is read on the device so a
+// captured CUDA graph stays valid from one sqngd_step call to the next (bias corrections, Q15).
+struct AdamP {
+  float lr, b1, b2, eps;
+  const long long* dt;
+  int which, off;
+  __device__ __forceinline__ void corr(float& c1, float& c2) const {
+    const double t = (double)(dt[which] + off + 1);
+    c1 = (float)(1.0 - pow((double)b1, t));
+    c2 = (float)(1.0 - pow((double)b2, t));
+  }
+};
+
+}  // namespace sq

@@ -3,9 +3,10 @@
 #pragma once
 #include <stdint.h>
 
+#include "adam.cuh"
+
 namespace sq {
 
-enum : int { ST_INVALID = 1, ST_DEGENERATE = 2, ST_NONFINITE = 4 };
 
 __device__ __forceinline__ float ex2a_m(float x) {
   float y;
@@ -18,18 +19,6 @@ __device__ __forceinline__ float rcp_m(float x) {
   return y;
 }
 
-// Adam hyper-parameters; the step count t = dt[which] + off + 1 is read on the device so a
-// captured CUDA graph stays valid from one sqngd_step call to the next (bias corrections, Q15).
-struct AdamP {
-  float lr, b1, b2, eps;
-  const long long* dt;
-  int which, off;
-  __device__ __forceinline__ void corr(float& c1, float& c2) const {
-    const double t = (double)(dt[which] + off + 1);
-    c1 = (float)(1.0 - pow((double)b1, t));
-    c2 = (float)(1.0 - pow((double)b2, t));
-  }
-};
 
 struct Red {               // per restart, after combining all groups
   double m;                // shift of S and of the gradient partials

@@ -18,6 +18,7 @@
 #include "comm.h"
 #include "lr_kernels.cuh"
 #include "misc_kernels.cuh"
+#include "net.cuh"
 
 using namespace sq;
 
@@ -106,9 +107,14 @@ struct sqngd_ctx_s {
   int* lr_cnt = nullptr;       // [R M Q] k_adj_g arrival counters
   Comm comm;
   long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
+  // generator z = f_theta(y0) (net.cu, NEXT-2)
+  bool net = false;
+  NetDims nd{};
+  NetWs nws{};
+  float* net_ws = nullptr;
   // CUDA graphs of sqngd_step (one per (state buffers, block, outputs, profiling))
   struct GraphEntry {
-    const void* key[12];
+    const void* key[16];
     int block;
     bool prof;
     cudaGraphExec_t exec = nullptr;
@@ -493,6 +499,14 @@ extern "C" {
 
 const char* sqngd_version(void) { return "sqngd-b200 0.1 (sm_100a)"; }
 
+int64_t sqngd_net_num_params(const sqngd_config* cfg) {
+  if (!cfg || cfg->net_width <= 0) return 0;
+  NetDims d;
+  const char* why = "";
+  if (!net_dims(1, cfg->M * cfg->N, cfg->net_width, cfg->net_depth, &d, &why)) return 0;
+  return (int64_t)d.P;
+}
+
 int64_t sqngd_num_units(const sqngd_config* cfg) {
   return cfg ? (int64_t)cfg->R * cfg->M * cfg->K : 0;
 }
@@ -524,6 +538,12 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: rank/world");
   if (cfg.doppler_engine < 0 || cfg.doppler_engine > 2)
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: doppler_engine");
+  NetDims nd{};
+  if (cfg.net_width != 0) {
+    const char* why = "";
+    if (!net_dims(cfg.R, cfg.M * cfg.N, cfg.net_width, cfg.net_depth, &nd, &why) || !(cfg.lr_theta >= 0))
+      return fail(nullptr, SQNGD_E_INVALID, "sqngd_create", cfg.lr_theta >= 0 ? why : "lr_theta");
+  }
   const int L = 2 * cfg.N - 1;
   if ((double)cfg.M * cfg.M * L * cfg.K >= 4294967295.0)
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: M^2 (2N-1) K cell index exceeds 32 bits");
@@ -708,6 +728,13 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->met, sizeof(MetricsOut) * cfg.R));
   CK(cudaMalloc(&ctx->status, sizeof(int)));
   CK(cudaMemset(ctx->status, 0, sizeof(int)));
+  if (cfg.net_width != 0) {
+    ctx->net = true;
+    ctx->nd = nd;
+    CK(cudaMalloc(&ctx->net_ws, sizeof(float) * net_ws_floats(nd)));
+    ctx->nws = net_ws_carve(nd, ctx->net_ws);
+    CK(net_prepare(nd));
+  }
 
   // Doppler twiddles e^{j 2 pi n f_k / N}, n one-based (Eq. 33, Q2), phase reduced mod 1 in fp64.
   {
@@ -883,7 +910,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
   void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1313,6 +1340,25 @@ sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho,
   return SQNGD_OK;
 }
 
+sqngd_status sqngd_net_forward(sqngd_ctx ctx, const float* theta, const float* y0, float* z, sqngd_stream stream) {
+  if (!ctx || !theta || !y0 || !z) return fail(ctx, SQNGD_E_INVALID, "sqngd_net_forward: null argument");
+  if (!ctx->net) return fail(ctx, SQNGD_E_INVALID, "sqngd_net_forward: context has no generator (net_width == 0)");
+  CK(cudaSetDevice(ctx->dev));
+  CK(net_forward(ctx->nd, ctx->nws, theta, y0, z, true, S(stream), &ctx->launches));
+  return SQNGD_OK;
+}
+
+sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* y0, const float* z,
+                                const float* grad_z, float* grad_theta, sqngd_stream stream) {
+  if (!ctx || !theta || !y0 || !z || !grad_z || !grad_theta)
+    return fail(ctx, SQNGD_E_INVALID, "sqngd_net_backward: null argument");
+  if (!ctx->net) return fail(ctx, SQNGD_E_INVALID, "sqngd_net_backward: context has no generator (net_width == 0)");
+  CK(cudaSetDevice(ctx->dev));
+  CK(net_backward(ctx->nd, ctx->nws, const_cast<float*>(theta), y0, z, grad_z, grad_theta, nullptr, nullptr, AdamP{},
+                  ctx->status, S(stream), &ctx->launches));
+  return SQNGD_OK;
+}
+
 }  // extern "C"
 
 // The body of one sqngd_step: every launch goes to `st` (capturable).  Adam reads the
@@ -1325,6 +1371,9 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
   auto ap = [&](double lr, int which, int off) {
     return AdamP{(float)lr, (float)c.adam_b1, (float)c.adam_b2, (float)c.adam_eps, ctx->d_t, which, off};
   };
+  if (ctx->net) {  // waveform generation z = f_theta(y0) (Alg. 1)
+    CK(net_forward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, true, st, &ctx->launches));
+  }
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
     if ((rc = run_xhat(ctx, ctx->s_hard, st))) return rc;  // X_hard fixed for the whole block
@@ -1363,7 +1412,9 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
         RhoFinish fin{};  // grad_rho sums, Adam(z) and Adam(rho) + projection by last-arriving blocks
         fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
         fin.gsum = ctx->grho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64;
-        fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
+        if (!ctx->net) {  // direct z: Adam(z) by the last element-chunk blocks
+          fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
+        }
         fin.status = ctx->status;
         const bool fuse_rho = ctx->BR <= 4096;  // 2 n2 floats within the default 48 KB
         if (fuse_rho) {
@@ -1378,6 +1429,11 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
                                                                         ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
                                                                         1.0f - 1e-4f, 1e-6f, ctx->status);
         ctx->launches += 2;
+      }
+      if (ctx->net) {  // Adam on theta through the generator's adjoint, then z = f_theta(y0) again
+        CK(net_backward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, ctx->gz, nullptr, stt->m_theta, stt->v_theta,
+                        ap(c.lr_theta, 1, i), ctx->status, st, &ctx->launches));
+        CK(net_forward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, false, st, &ctx->launches));
       }
       if ((rc = launch_check(ctx, "step B update"))) return rc;
     }
@@ -1398,6 +1454,8 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
                         sqngd_stream stream) {
   if (!ctx || !stt || !stt->z || !stt->rho || !stt->w || (block & ~3) || !block)
     return fail(ctx, SQNGD_E_INVALID, "sqngd_step: bad argument");
+  if (ctx->net && (!stt->theta || !stt->m_theta || !stt->v_theta || !stt->y0))
+    return fail(ctx, SQNGD_E_INVALID, "sqngd_step: generator mode needs theta, m_theta, v_theta and y0");
   CK(cudaSetDevice(ctx->dev));
   const sqngd_config& c = ctx->cfg;
   const cudaStream_t st = S(stream);
@@ -1410,8 +1468,8 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
   if (!graph_ok) {
     if ((rc = step_body(ctx, stt, block, loss_hist, hard_out, st))) return rc;
   } else {
-    const void* key[12] = {stt->z, stt->rho, stt->w, stt->m_z, stt->v_z, stt->m_rho, stt->v_rho, stt->m_w, stt->v_w,
-                           loss_hist, hard_out, st};
+    const void* key[16] = {stt->z, stt->rho, stt->w, stt->m_z, stt->v_z, stt->m_rho, stt->v_rho, stt->m_w, stt->v_w,
+                           loss_hist, hard_out, st, stt->theta, stt->m_theta, stt->v_theta, stt->y0};
     sqngd_ctx_s::GraphEntry* ge = nullptr;
     for (auto* g : ctx->graphs)
       if (g->block == block && g->prof == ctx->prof && std::memcmp(g->key, key, sizeof(key)) == 0) ge = g;

@@ -108,15 +108,15 @@ def net_input(R: int, M: int, N: int, B: int, config_index: int = 0) -> np.ndarr
 
 def net_params(R: int, Din: int, W: int, D: int, config_index: int = 0, bias_scale: float = 0.0) -> np.ndarray:
     """theta[R][P] fp32 in the flat C-ABI layout (include/sqngd.h, sqngd_net_*):
-    W_in [W][Din] | b_in [W] | D x (W1 [W][W] | b1 [W] | W2 [W][W] | b2 [W]) | W_out [Din][W] | b_out [Din].
-    Weights uniform in +-sqrt(3 / fan_in) (variance 1/fan_in); biases uniform in +-bias_scale
+    W_in [W][Din] | b_in [W] | D x (W1 [W][W] | b1 [W] | W2 [W][W] | b2 [W]) | W_out [Din][W] | b_out [Din] | pad
+    (pad: zeros up to a multiple of 4 floats).  Weights uniform in +-sqrt(3 / fan_in) (variance 1/fan_in); biases uniform in +-bias_scale
     (0 by default)."""
     sizes = [(W * Din, Din), (W, 0)]
     for _ in range(D):
         sizes += [(W * W, W), (W, 0), (W * W, W), (W, 0)]
     sizes += [(Din * W, W), (Din, 0)]
     P = sum(n for n, _ in sizes)
-    out = np.empty((R, P), dtype=np.float32)
+    out = np.zeros((R, (P + 3) // 4 * 4), dtype=np.float32)  # + pad to the C-ABI's float4 stride
     for r in range(R):
         u = uniform01_f32(_THETA_SEED + config_seed(config_index, r), P).astype(np.float64) * 2.0 - 1.0
         o = 0

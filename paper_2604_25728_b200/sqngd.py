@@ -45,6 +45,8 @@ class Config(C.Structure):
         ("weights", C.c_void_p),
         ("doppler_engine", C.c_int32),
         ("lr_tol", C.c_double),
+        ("net_depth", C.c_int32), ("net_width", C.c_int32),
+        ("lr_theta", C.c_double),
     ]
 
 
@@ -66,6 +68,7 @@ class State(C.Structure):
         ("m_z", C.c_void_p), ("v_z", C.c_void_p), ("m_rho", C.c_void_p), ("v_rho", C.c_void_p),
         ("m_w", C.c_void_p), ("v_w", C.c_void_p),
         ("t_a", C.c_int64), ("t_b", C.c_int64),
+        ("theta", C.c_void_p), ("m_theta", C.c_void_p), ("v_theta", C.c_void_p), ("y0", C.c_void_p),
     ]
 
 
@@ -108,6 +111,12 @@ def lib():
         L.sqngd_shard_range.argtypes = [i64, i32, i32, C.POINTER(i64), C.POINTER(i64)]
         L.sqngd_engine_info.restype = i32
         L.sqngd_engine_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        L.sqngd_net_num_params.restype = i64
+        L.sqngd_net_num_params.argtypes = [C.POINTER(Config)]
+        L.sqngd_net_forward.restype = i32
+        L.sqngd_net_forward.argtypes = [vp, vp, vp, vp, vp]
+        L.sqngd_net_backward.restype = i32
+        L.sqngd_net_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.sqngd_version.restype = C.c_char_p
         L.sqngd_version.argtypes = []
         _lib = L
@@ -117,7 +126,8 @@ def lib():
 EXPORTED = ["sqngd_create", "sqngd_destroy", "sqngd_last_error", "sqngd_sync", "sqngd_quantize",
             "sqngd_af_forward", "sqngd_loss_grad_s", "sqngd_af_loss_grad", "sqngd_step",
             "sqngd_profile_enable", "sqngd_profile_read",
-            "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info"]
+            "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info",
+            "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward"]
 
 
 def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Config:
@@ -137,7 +147,14 @@ def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Co
         weights=weights_ptr,
         doppler_engine=int(getattr(cfg, "doppler_engine", ENGINE_AUTO)),
         lr_tol=float(getattr(cfg, "lr_tol", 0.0)),
+        net_depth=int(getattr(cfg, "net_depth", 0)), net_width=int(getattr(cfg, "net_width", 0)),
+        lr_theta=float(getattr(cfg, "lr_theta", 1e-5)),
     )
+
+
+def net_num_params(cfg) -> int:
+    """Generator parameters per restart (0 without a generator)."""
+    return int(lib().sqngd_net_num_params(C.byref(make_config(cfg))))
 
 
 def shard_range(units: int, rank: int, world: int) -> tuple[int, int]:
@@ -283,9 +300,28 @@ class Context:
                                              _ptr(gz), _ptr(gr), self._stream()))
         return met, gz, gr
 
-    def new_state(self, z, rho, w) -> dict:
+    def net_forward(self, theta, y0, z=None):
+        """z = f_theta(y0) ([R][M][N] float32); keeps the tape for net_backward."""
+        z = self._f((self.R, self.M, self.N)) if z is None else z
+        self._check(lib().sqngd_net_forward(self.h, _ptr(theta), _ptr(y0), _ptr(z), self._stream()))
+        return z
+
+    def net_backward(self, theta, y0, z, grad_z, out=None):
+        """dL/dtheta [R][P] from grad_z = dL/dz (after net_forward with the same theta, y0)."""
+        g = self.torch.empty_like(theta) if out is None else out
+        self._check(lib().sqngd_net_backward(self.h, _ptr(theta), _ptr(y0), _ptr(z), _ptr(grad_z), _ptr(g),
+                                             self._stream()))
+        return g
+
+    def new_state(self, z, rho, w, theta=None, y0=None) -> dict:
+        """Optimizer state; with theta [R][P] and y0 [R][M N] (generator mode) z is written by step()."""
         t = self.torch
         st = dict(z=z.clone().contiguous(), rho=rho.clone().contiguous(), w=w.clone().contiguous())
+        st["theta"] = st["m_theta"] = st["v_theta"] = st["y0"] = None
+        if theta is not None:
+            st["theta"] = theta.clone().contiguous()
+            st["m_theta"], st["v_theta"] = t.zeros_like(st["theta"]), t.zeros_like(st["theta"])
+            st["y0"] = y0.clone().contiguous()
         st["m_z"], st["v_z"] = t.zeros_like(st["z"]), t.zeros_like(st["z"])
         st["m_rho"], st["v_rho"] = t.zeros_like(st["rho"]), t.zeros_like(st["rho"])
         n = st["w"].numel() * 2
@@ -297,7 +333,9 @@ class Context:
     def step(self, st: dict, block: int = BLOCK_AB, hist=None, hard_met=None):
         cs = State(z=_ptr(st["z"]), rho=_ptr(st["rho"]), w=_ptr(st["w"]), m_z=_ptr(st["m_z"]), v_z=_ptr(st["v_z"]),
                    m_rho=_ptr(st["m_rho"]), v_rho=_ptr(st["v_rho"]), m_w=_ptr(st["m_w"]), v_w=_ptr(st["v_w"]),
-                   t_a=int(st["t_a"]), t_b=int(st["t_b"]))
+                   t_a=int(st["t_a"]), t_b=int(st["t_b"]),
+                   theta=_ptr(st.get("theta")), m_theta=_ptr(st.get("m_theta")), v_theta=_ptr(st.get("v_theta")),
+                   y0=_ptr(st.get("y0")))
         self._check(lib().sqngd_step(self.h, C.byref(cs), int(block), _ptr(hist), _ptr(hard_met), self._stream()))
         st["t_a"], st["t_b"] = cs.t_a, cs.t_b
         return st

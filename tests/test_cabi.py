@@ -34,9 +34,9 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_struct_layouts():
-    # sqngd_metrics: 6 doubles + 8 int32 + 2 uint32 = 88 bytes; sqngd_state: 9 pointers + 2 int64
+    # sqngd_metrics: 6 doubles + 8 int32 + 2 uint32 = 88 bytes; sqngd_state: 9 pointers + 2 int64 + 4 pointers
     assert sqngd.METRICS_BYTES == 88
-    assert C.sizeof(sqngd.State) == 9 * 8 + 16
+    assert C.sizeof(sqngd.State) == 9 * 8 + 16 + 4 * 8
 
 
 def test_version_and_units(lib):
@@ -64,8 +64,21 @@ def test_create_rejects_invalid_config_without_gpu(lib):
     h = C.c_void_p()
     empty_roi = C1.with_(M=1, tau_lo=0, tau_hi=0)      # auto map only, tau = 0 excluded (Eq. 8): no cells
     for bad in (C1.with_(B=1), C1.with_(N=1), C1.with_(K=0), C1.with_(tau_lo=-64), C1.with_(N=8192), empty_roi,
-                C1.with_(doppler_engine=3)):
+                C1.with_(doppler_engine=3), C1.with_(net_width=12, net_depth=5),
+                C1.with_(net_width=256, net_depth=5), C1.with_(net_width=128, net_depth=-1),
+                C1.with_(net_width=128, net_depth=40)):
         cfg = sqngd.make_config(bad)
         st = lib.sqngd_create(C.byref(cfg), 0, None, 0, 1, C.byref(h))
         assert st == sqngd.E_INVALID
         assert lib.sqngd_last_error(None)
+
+
+def test_generator_parameter_count(lib):
+    """sqngd_net_num_params = the closed form D (2 W^2 + 2 W) + (W Din + W) + (Din W + Din)."""
+    from paper_2604_25728_b200.configs import C1, C3
+
+    assert sqngd.net_num_params(C3) == 0
+    for c, W, D in ((C3, 128, 5), (C1, 32, 2), (C1.with_(M=3, N=37), 8, 0)):
+        Din = c.M * c.N
+        n = D * (2 * W * W + 2 * W) + 2 * W * Din + W + Din
+        assert sqngd.net_num_params(c.with_(net_width=W, net_depth=D)) == (n + 3) // 4 * 4  # float4 stride

@@ -27,6 +27,8 @@ def test_parameter_count_closed_form():
     assert NO.num_params(8192, 128, 5) == 2_270_592
     th = inputs.net_params(1, 40, 32, 3)
     assert th.shape == (1, NO.num_params(40, 32, 3))
+    th = inputs.net_params(1, 111, 16, 1)  # Din % 4 = 3: one pad float to the float4 stride
+    assert th.shape == (1, NO.num_params(111, 16, 1) + 1) and th[0, -1] == 0
 
 
 def test_gradients_match_central_differences():
@@ -148,7 +150,7 @@ def test_oracle_step_generator_mode():
                         lr_w=5e-2, lr_z=1e-4, lr_theta=1e-3, adam_b1=0.9, adam_b2=0.999, adam_eps=1e-8,
                         n_h=2, n_x=3, net_width=8, net_depth=2)
     Din = c.M * c.N
-    th = inputs.net_params(1, Din, 8, 2, config_index=4)
+    th = inputs.net_params(1, Din, 8, 2, config_index=4)[:, :NO.num_params(Din, 8, 2)]
     y0 = inputs.net_input(1, c.M, c.N, c.B, config_index=4)
     z0, _ = NO.forward(th[0].astype(np.float64), y0[0], Din, 8, 2)
     rho = inputs.init_thresholds(1, c.B, c.r_n)
