@@ -231,6 +231,8 @@ def main():
     ap.add_argument("--loss", default="lse", choices=["lse", "max", "pnorm"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-generator", dest="generator", action="store_false",
+                    help="skip the generator-mode (z = f_theta(y0)) line")
     args = ap.parse_args()
 
     c = CF.CONFIGS[args.config]
@@ -275,8 +277,17 @@ def main():
         pass over K more steps for the per-kernel CUDA-event times."""
         ctx = sqngd.Context(cc, device=local)
         zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
+        net = {}
+        if cc.net_width:  # generator mode: z = f_theta(y0) (NEXT-2), seeded theta and y0 per restart
+            Din = cc.M * cc.N
+            th = np.concatenate([inputs.net_params(1, Din, cc.net_width, cc.net_depth, config_index=cc.index * 1000 + g)
+                                 for g in parallel.restart_ids(R, rank)])
+            y0 = np.concatenate([inputs.net_input(1, cc.M, cc.N, cc.B, config_index=cc.index * 1000 + g)
+                                 for g in parallel.restart_ids(R, rank)])
+            net = dict(theta=torch.as_tensor(th, device=dev), y0=torch.as_tensor(y0, device=dev))
+            zt = ctx.net_forward(net["theta"], net["y0"])
         q = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)
-        st = ctx.new_state(zt, rt, q["s_hard"])                    # w = s_hard (matched start, Q3)
+        st = ctx.new_state(zt, rt, q["s_hard"], **net)             # w = s_hard (matched start, Q3)
         hist = torch.zeros((R, c.n_h + c.n_x), dtype=torch.float64, device=dev)
         hard = torch.empty(R * sqngd.METRICS_BYTES, dtype=torch.uint8, device=dev)
         for _ in range(args.warmup):
@@ -319,19 +330,24 @@ def main():
         else:
             wm = work_model(cc)
             knames = {"fwd": "k_af<FWD>", "adjA": "k_af<ADJ_A>", "adjB": "k_af<ADJ_B>"}
+        # classes that launch the same kernel (k_lrt<ADJ> serves Step A and Step B) are pooled
         dom = max(range(3), key=lambda i: prof["ms"][i])
-        avg_ms = prof["ms"][dom] / max(1, prof["count"][dom])
+        same = [i for i in range(3) if knames[names[i]] == knames[names[dom]]]
+        k_ms, k_cnt = sum(prof["ms"][i] for i in same), sum(prof["count"][i] for i in same)
+        avg_ms = k_ms / max(1, k_cnt)
         achieved = wm[names[dom]] / (avg_ms / 1e3) / 1e12
         roof = {"bound": "alu", "kernel": knames[names[dom]], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic_bytes(knames[names[dom]]), "avg_launch_ms": avg_ms,
-                "launches": prof["count"][dom], "flops_per_launch": wm[names[dom]],
+                "launches": k_cnt, "flops_per_launch": wm[names[dom]],
                 "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
-                "share_of_step": prof["ms"][dom] / tot_ms,
+                "share_of_step": k_ms / tot_ms,
                 "timing": "CUDA events around each fused-kernel launch on its stream, in an eager pass over the "
                           "same K steps right after the timed (CUDA-graph) region"}
         out = {"value": value, "ms_per_step": tot_ms / args.steps, "roofline": roof, "launches": launches,
                "kernel_ms": {n: prof["ms"][i] / args.steps for i, n in enumerate(names)}, "engine": info,
                "wall_s": t_wall}
+        if cc.net_width and prof["count"][3]:
+            out["net_update_ms"] = prof["ms"][3] / prof["count"][3]
         if with_clocks:
             out["clocks"] = clk.summary()
         return ctx, st, hist, hard, out
@@ -391,6 +407,28 @@ def main():
         "wall_s": main_run["wall_s"],
         "final_hard_pslr_db": 20 * math.log10(max(hm[0]["wpsl"], 1e-30)),
     }
+    if args.generator:  # NEXT-2: the same step with the paper's ResNet generator z = f_theta(y0)
+        W, D = 128, 5
+        cg = c.with_(net_width=W, net_depth=D, lr_theta=1e-5)
+        ctxg, *_rest, gen_run = timed(cg, False)
+        ctxg.close()
+        Din = c.M * c.N
+        P = sqngd.net_num_params(cg)
+        # algorithmic bytes of one generator update (backward + Adam + next forward): every parameter's
+        # (theta, m, v) read and written once (24 B), W_out read again by the forward, y0/z/dL/dz/z
+        upd_bytes = 24 * P * c.R + 4 * W * Din * c.R + 16 * Din * c.R
+        hbm = peaks()[1]
+        gbs = upd_bytes / (gen_run["net_update_ms"] / 1e3) / 1e9
+        line["generator"] = {
+            "arch": f"ResNet {D} residual blocks, width {W}, tanh / sigmoid (P:L583); {P} parameters per restart",
+            "value": gen_run["value"], "unit": UNIT, "ms_per_step": gen_run["ms_per_step"],
+            "gpu_launches": gen_run["launches"],
+            "update_ms": gen_run["net_update_ms"],
+            "roofline": {"bound": "hbm", "kernel": "generator update (k_net_out_bwd, k_net_mid_bwd, k_net_upd<ADAM>, "
+                                                   "k_net_mid_fwd, k_net_out)",
+                         "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+                         "bytes_per_update": upd_bytes,
+                         "timing": "CUDA events around each Step-B generator update in the eager profiled pass"}}
     if fft_run is not None:
         line["fft_engine"] = {"value": fft_run["value"], "unit": UNIT, "ms_per_step": fft_run["ms_per_step"],
                               "cells_per_s": fft_run["value"] * c.cells / c.R, "roofline": fft_run["roofline"],

@@ -205,9 +205,10 @@ sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* 
    (single GPU; SQNGD_NO_GRAPH=1 disables).
    Profiling (for the roofline in bench.py): when enabled, sqngd_step runs eagerly and every
    launch of the dominant fused kernel (k_af for the FFT engine, k_lrt for the Chebyshev
-   engine) is bracketed by CUDA events on its launch stream.  sqngd_profile_read synchronizes and
-   returns, per kernel class (0 forward, 1 Step-A adjoint, 2 Step-B adjoint), the summed
-   device milliseconds ms[3] and launch counts count[3], plus `launches` = every kernel the
+   engine), and each generator update of Step B, is bracketed by CUDA events on its launch stream.
+   sqngd_profile_read synchronizes and returns, per class (0 forward, 1 Step-A adjoint, 2 Step-B
+   adjoint, 3 generator backward + Adam(theta) + forward), the summed device milliseconds ms[4]
+   and counts count[4], plus `launches` = every kernel the
    library launched since the last reset (all classes, small kernels included). */
 sqngd_status sqngd_profile_enable(sqngd_ctx ctx, int on);
 sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64_t* launches, int reset);

@@ -13,14 +13,16 @@ namespace sq {
 
 constexpr int NET_CL = 8;        // CTAs per cluster of the layer-serial kernels (one cluster per restart)
 constexpr int NET_IN_COLS = 256; // columns of W_in per k_net_in CTA (one row per warp)
-constexpr int NET_OUT_ROWS = 64; // rows of W_out per k_net_out / k_net_out_bwd CTA
+constexpr int NET_FWD_ROWS = 64; // rows of W_out per k_net_out CTA (8 per warp)
+constexpr int NET_OUT_ROWS = 16; // rows of W_out per k_net_out_bwd CTA (2 per warp, loads up front)
 
 struct NetDims {
   int R = 0, Din = 0, W = 0, D = 0;
   size_t P = 0;                                   // parameters per restart
   size_t o_bin = 0, o_blk = 0, o_wout = 0, o_bout = 0;  // W_in at offset 0
   int n_in = 0;                                   // column chunks of W_in (partials of W_in y0)
-  int n_out = 0;                                  // row chunks of W_out (partials of W_out^T g)
+  int n_out = 0;                                  // clusters of W_out row chunks (partials of W_out^T g)
+  int n_hid = 0;                                  // k_net_hid CTAs per restart
   size_t smem_fwd = 0, smem_bwd = 0;              // dynamic shared memory of the cluster kernels
 };
 
@@ -29,6 +31,7 @@ struct NetWs {
   float* pin = nullptr;   // [R][n_in][W]  partials of W_in y0
   float* pout = nullptr;  // [R][n_out][W] partials of W_out^T (dL/do)
   float* ga0 = nullptr;   // [R][W] dL/d(W_in y0 + b_in)
+  float* gvec = nullptr;  // [R][D][2][W] hidden-gradient factors: dL/dh_{d+1}, dL/d(W1_d h_d + b1_d)
 };
 
 // Validates (W % 8 == 0, 8 <= W <= 128, D >= 0, shared memory of the cluster kernels <= 200 KB).

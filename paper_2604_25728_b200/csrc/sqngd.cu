@@ -939,8 +939,8 @@ sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64
   if (!ctx) return fail(nullptr, SQNGD_E_INVALID, "sqngd_profile_read: null ctx");
   CK(cudaSetDevice(ctx->dev));
   CK(cudaDeviceSynchronize());
-  double acc[3] = {0, 0, 0};
-  int64_t cnt[3] = {0, 0, 0};
+  double acc[4] = {0, 0, 0, 0};
+  int64_t cnt[4] = {0, 0, 0, 0};
   for (auto& mk : ctx->ev_marks) {
     float t = 0.f;
     CK(cudaEventElapsedTime(&t, ctx->ev_pool[mk.second], ctx->ev_pool[mk.second + 1]));
@@ -956,7 +956,7 @@ sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64
       cnt[std::get<0>(mk)] += 1;
     }
   }
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     if (ms) ms[i] = acc[i];
     if (count) count[i] = cnt[i];
   }
@@ -1431,6 +1431,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
         ctx->launches += 2;
       }
       if (ctx->net) {  // Adam on theta through the generator's adjoint, then z = f_theta(y0) again
+        ProfScope ps(ctx, 3, st);
         CK(net_backward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, ctx->gz, nullptr, stt->m_theta, stt->v_theta,
                         ap(c.lr_theta, 1, i), ctx->status, st, &ctx->launches));
         CK(net_forward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, false, st, &ctx->launches));

@@ -240,8 +240,8 @@ class Context:
         self._check(lib().sqngd_profile_enable(self.h, 1 if on else 0))
 
     def profile_read(self, reset: bool = True) -> dict:
-        ms = (C.c_double * 3)()
-        cnt = (C.c_int64 * 3)()
+        ms = (C.c_double * 4)()
+        cnt = (C.c_int64 * 4)()
         n = C.c_int64()
         self._check(lib().sqngd_profile_read(self.h, ms, cnt, C.byref(n), 1 if reset else 0))
         return dict(ms=list(ms), count=list(cnt), launches=n.value)
