@@ -200,6 +200,35 @@ sqngd_status sqngd_net_forward(sqngd_ctx ctx, const float* theta, const float* y
 sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* y0, const float* z,
                                 const float* grad_z, float* grad_theta, sqngd_stream stream);
 
+/* Alg. 1 driver.  Up to opts->T outer iterations of
+   sqngd_step(SQNGD_BLOCK_AB) on `state`, each followed by the hard-waveform metrics (Eq. 43 then
+   Eq. 7).  Per restart r the state with the lowest hard WPSL so far is copied into `best`
+   (DEVICE buffers z, rho, w, and theta in generator mode; the other members are ignored): the
+   output (X_hard, H) of Alg. 1 is quantize(best.z, best.rho) and best.w.  Stopping criterion
+   ("further reduction of L does not lead to improvement in the WPSL"): stop after
+   the outer iteration at which EVERY restart has gone opts->patience consecutive iterations
+   without a strict improvement of its hard WPSL (patience <= 0: run all T).
+   best_wpsl [R] doubles, best_iter [R] int32 (1-based outer iteration of the snapshot) and
+   wpsl_hist (NULL or [T][R] doubles, hard WPSL per iteration until the stop) are DEVICE pointers.
+   The bookkeeping runs on the device; the host polls the stop flag every opts->check_every
+   iterations, so the live `state` may run up to check_every - 1 iterations past the stop (the
+   snapshot, best_* and result->iterations follow the rule exactly; check_every = 1 is exact).
+   Returns after synchronizing `stream` (the latched device status, as sqngd_sync). */
+typedef struct {
+  int32_t T;           /* maximum outer iterations (the paper's T = 2000)          */
+  int32_t patience;    /* outer iterations without hard-WPSL improvement before stopping   */
+  int32_t check_every; /* >= 1: host polls the device stop flag every check_every steps    */
+} sqngd_run_opts;
+typedef struct {
+  int64_t iterations;  /* outer iterations until the rule stopped training (T if it did not) */
+  int64_t steps_run;   /* sqngd_step calls made (>= iterations, <= iterations + check_every - 1) */
+  int32_t stopped;     /* 1: stopped by the rule, 0: T reached                             */
+  int32_t reserved;
+} sqngd_run_result;
+sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd_run_opts* opts, sqngd_state* best,
+                       double* best_wpsl, int32_t* best_iter, double* wpsl_hist, sqngd_run_result* result,
+                       sqngd_stream stream);
+
 /* sqngd_step captures itself into a CUDA graph on the first call with a given (state
    buffers, block, outputs) on a non-legacy stream and replays the graph afterwards
    (single GPU; SQNGD_NO_GRAPH=1 disables).

@@ -41,8 +41,8 @@ def flags(verbose: bool = False) -> list[str]:
 
 
 def sources() -> list[str]:
-    # two translation units compiled in parallel: the AF/loss/gradient path and the generator
-    return [os.path.join(CSRC, "sqngd.cu"), os.path.join(CSRC, "net.cu")]
+    # translation units compiled in parallel: the AF/loss/gradient path, the generator, the Alg. 1 driver
+    return [os.path.join(CSRC, "sqngd.cu"), os.path.join(CSRC, "net.cu"), os.path.join(CSRC, "run.cu")]
 
 
 def deps(src: str | None = None) -> list[str]:
@@ -53,7 +53,9 @@ def deps(src: str | None = None) -> list[str]:
         return sorted(allf + [hdr])
     if os.path.basename(src) == "net.cu":
         return [src] + [os.path.join(CSRC, f) for f in ("net.cuh", "adam.cuh")]
-    return sorted([p for p in allf if os.path.basename(p) != "net.cu"] + [hdr])
+    if os.path.basename(src) == "run.cu":
+        return [src, os.path.join(CSRC, "run.cuh"), hdr]
+    return sorted([p for p in allf if os.path.basename(p) not in ("net.cu", "run.cu")] + [hdr])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(PL::T* G)
         const float re = 2.f * (v[i].x + ((float)gc.x * sv.x + (float)gc.y * sv.y));   // d = conj(v)
         const float im = 2.f * (-v[i].y + ((float)gc.x * sv.y - (float)gc.y * sv.x));
         if (!isfinite(re) || !isfinite(im)) bad = 1.f;
-        if (f.grad_w) f.grad_w[j] = make_float2(re, im);
+        if (f.grad_w && id < rows) f.grad_w[j] = make_float2(re, im);
         const float g2[2] = {re, im};
         float x2[2] = {w[j].x, w[j].y};
 #pragma unroll
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(PL::T* G)
           const size_t jj = 2 * j + q;
           const float mi = ap.b1 * mw[jj] + (1.f - ap.b1) * g2[q];
           const float vi = ap.b2 * vw[jj] + (1.f - ap.b2) * g2[q] * g2[q];
-          if (!skip_all) {
+          if (!skip_all && id < rows) {  // (a padding group duplicates the last row: no stores)
             mw[jj] = mi;
             vw[jj] = vi;
           }

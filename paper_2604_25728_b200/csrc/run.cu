@@ -1,0 +1,145 @@
+// The Algorithm-1 driver (Alg. 1, stopping criterion
+// P:L485 / P:L533): up to T outer iterations of sqngd_step(A+B), each followed by the hard-waveform
+// WPSL; per restart the best (lowest hard WPSL) state is kept as the output snapshot (Alg. 1
+// "Output: (X_hard, H)"), and training stops when no restart's hard WPSL has improved for
+// `patience` consecutive outer iterations (DESIGN.md §3 "Stopping rule").  The bookkeeping runs on
+// the device (k_run_track / k_run_done) so the loop needs no per-iteration host round trip; the host
+// polls the stop flag every `check_every` iterations.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "run.cuh"
+
+namespace {
+
+struct RunPtrs {
+  const float* z; const float* rho; const float* w; const float* theta;  // current state
+  float* bz; float* brho; float* bw; float* btheta;                     // best snapshot
+  size_t nz, nrho, nw, ntheta;                                           // floats per restart
+};
+
+struct RunDev {  // device-side bookkeeping (one allocation)
+  int done;                 // the rule fired (frozen afterwards)
+  int stop_iter;            // outer iterations run when it fired
+};
+
+// One block per restart: compare the hard WPSL of outer iteration t (1-based) with the best so far.
+__global__ void k_run_track(int t, const sqngd_metrics* hard, double* best_wpsl, int32_t* best_iter, int* stall,
+                            double* hist, int R, RunDev* rd, RunPtrs p) {
+  const int r = blockIdx.x;
+  __shared__ int improve;
+  if (rd->done) return;  // uniform: the rule already fired, the snapshot is final
+  if (threadIdx.x == 0) {
+    const double v = hard[r].wpsl;
+    if (hist) hist[(size_t)(t - 1) * R + r] = v;
+    improve = v < best_wpsl[r];  // strict improvement (a NaN never improves)
+    if (improve) {
+      best_wpsl[r] = v;
+      best_iter[r] = t;
+      stall[r] = 0;
+    } else {
+      stall[r] += 1;
+    }
+  }
+  __syncthreads();
+  if (!improve) return;
+  auto copy = [&](const float* src, float* dst, size_t n) {
+    if (!src || !dst) return;
+    for (size_t k = threadIdx.x; k < n; k += blockDim.x) dst[(size_t)r * n + k] = src[(size_t)r * n + k];
+  };
+  copy(p.z, p.bz, p.nz);
+  copy(p.rho, p.brho, p.nrho);
+  copy(p.w, p.bw, p.nw);
+  copy(p.theta, p.btheta, p.ntheta);
+}
+
+__global__ void k_run_done(int t, const int* stall, int R, int patience, RunDev* rd) {
+  if (rd->done || patience <= 0) return;
+  int all = 1;
+  for (int r = 0; r < R; ++r) all &= stall[r] >= patience;
+  if (all) {
+    rd->done = 1;
+    rd->stop_iter = t;
+  }
+}
+
+}  // namespace
+
+#define RK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess) {                                                             \
+      cleanup();                                                                         \
+      return sq_ctx_fail(ctx, SQNGD_E_CUDA, #x, cudaGetErrorString(e_));                 \
+    }                                                                                    \
+  } while (0)
+
+extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd_run_opts* opts, sqngd_state* best,
+                                  double* best_wpsl, int32_t* best_iter, double* wpsl_hist, sqngd_run_result* result,
+                                  sqngd_stream stream) {
+  if (!ctx || !state || !opts || !best || !best_wpsl || !best_iter || !result || opts->T < 1 ||
+      opts->check_every < 1 || !best->z || !best->rho || !best->w)
+    return sq_ctx_fail(ctx, SQNGD_E_INVALID, "sqngd_run: bad argument", "");
+  const sqngd_config& c = *sq_ctx_config(ctx);
+  const bool net = c.net_width > 0;
+  if (net && !best->theta) return sq_ctx_fail(ctx, SQNGD_E_INVALID, "sqngd_run: generator mode needs best->theta", "");
+  cudaSetDevice(sq_ctx_device(ctx));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  sqngd_metrics* hard = nullptr;
+  int* stall = nullptr;
+  RunDev* rd = nullptr;
+  RunDev* rd_host = nullptr;
+  auto cleanup = [&]() {
+    if (hard) cudaFree(hard);
+    if (stall) cudaFree(stall);
+    if (rd) cudaFree(rd);
+    if (rd_host) cudaFreeHost(rd_host);
+  };
+  RK(cudaMalloc(&hard, sizeof(sqngd_metrics) * c.R));
+  RK(cudaMalloc(&stall, sizeof(int) * c.R));
+  RK(cudaMalloc(&rd, sizeof(RunDev)));
+  RK(cudaMallocHost(&rd_host, sizeof(RunDev)));
+  RK(cudaMemsetAsync(stall, 0, sizeof(int) * c.R, st));
+  RK(cudaMemsetAsync(rd, 0, sizeof(RunDev), st));
+  {  // best_wpsl = +inf, best_iter = 0
+    static_assert(sizeof(double) == 8, "");
+    const double inf = INFINITY;
+    for (int r = 0; r < c.R; ++r) RK(cudaMemcpyAsync(best_wpsl + r, &inf, sizeof(double), cudaMemcpyHostToDevice, st));
+    RK(cudaMemsetAsync(best_iter, 0, sizeof(int32_t) * c.R, st));
+    RK(cudaStreamSynchronize(st));  // (the host `inf` is a stack value)
+  }
+  RunPtrs p{};
+  p.z = state->z; p.rho = state->rho; p.w = state->w; p.theta = net ? state->theta : nullptr;
+  p.bz = best->z; p.brho = best->rho; p.bw = best->w; p.btheta = net ? best->theta : nullptr;
+  p.nz = (size_t)c.M * c.N;
+  p.nrho = (size_t)c.B * c.r_n;
+  p.nw = 2 * (size_t)c.M * c.N;
+  p.ntheta = net ? (size_t)sqngd_net_num_params(&c) : 0;
+  int64_t t = 0;
+  bool stopped = false;
+  for (t = 1; t <= opts->T; ++t) {
+    sqngd_status s = sqngd_step(ctx, state, SQNGD_BLOCK_AB, nullptr, hard, stream);
+    if (s != SQNGD_OK) {
+      cleanup();
+      return s;
+    }
+    k_run_track<<<c.R, 256, 0, st>>>((int)t, hard, best_wpsl, best_iter, stall, wpsl_hist, c.R, rd, p);
+    k_run_done<<<1, 1, 0, st>>>((int)t, stall, c.R, opts->patience, rd);
+    RK(cudaGetLastError());
+    if (t % opts->check_every == 0 || t == opts->T) {
+      RK(cudaMemcpyAsync(rd_host, rd, sizeof(RunDev), cudaMemcpyDeviceToHost, st));
+      RK(cudaStreamSynchronize(st));
+      if (rd_host->done) {
+        stopped = true;
+        break;
+      }
+    }
+  }
+  result->iterations = stopped ? rd_host->stop_iter : opts->T;
+  result->steps_run = stopped ? t : opts->T;
+  result->stopped = stopped ? 1 : 0;
+  cleanup();
+  return sqngd_sync(ctx, stream);
+}

@@ -19,6 +19,7 @@
 #include "lr_kernels.cuh"
 #include "misc_kernels.cuh"
 #include "net.cuh"
+#include "run.cuh"
 
 using namespace sq;
 
@@ -520,6 +521,17 @@ void sqngd_shard_range(int64_t units, int rank, int world, int64_t* lo, int64_t*
 }
 
 const char* sqngd_last_error(sqngd_ctx ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+}  // extern "C"
+
+// internal accessors for run.cu (C++ linkage, not part of the C-ABI)
+const sqngd_config* sq_ctx_config(sqngd_ctx ctx) { return &ctx->cfg; }
+int sq_ctx_device(sqngd_ctx ctx) { return ctx->dev; }
+sqngd_status sq_ctx_fail(sqngd_ctx ctx, sqngd_status st, const char* what, const char* why) {
+  return fail(ctx, st, what, why);
+}
+
+extern "C" {
 
 sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void* nccl_unique_id, int rank,
                           int world, sqngd_ctx* out) {

@@ -72,6 +72,15 @@ class State(C.Structure):
     ]
 
 
+class RunOpts(C.Structure):
+    _fields_ = [("T", C.c_int32), ("patience", C.c_int32), ("check_every", C.c_int32)]
+
+
+class RunResult(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("steps_run", C.c_int64), ("stopped", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 _lib = None
 
 
@@ -117,6 +126,9 @@ def lib():
         L.sqngd_net_forward.argtypes = [vp, vp, vp, vp, vp]
         L.sqngd_net_backward.restype = i32
         L.sqngd_net_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.sqngd_run.restype = i32
+        L.sqngd_run.argtypes = [vp, C.POINTER(State), C.POINTER(RunOpts), C.POINTER(State), vp, vp, vp,
+                                C.POINTER(RunResult), vp]
         L.sqngd_version.restype = C.c_char_p
         L.sqngd_version.argtypes = []
         _lib = L
@@ -127,7 +139,7 @@ EXPORTED = ["sqngd_create", "sqngd_destroy", "sqngd_last_error", "sqngd_sync", "
             "sqngd_af_forward", "sqngd_loss_grad_s", "sqngd_af_loss_grad", "sqngd_step",
             "sqngd_profile_enable", "sqngd_profile_read",
             "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info",
-            "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward"]
+            "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward", "sqngd_run"]
 
 
 def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Config:
@@ -329,6 +341,32 @@ class Context:
         st["v_w"] = t.zeros(n, dtype=t.float32, device=self.device)
         st["t_a"], st["t_b"] = 0, 0
         return st
+
+    def run(self, st: dict, T: int, patience: int, check_every: int = 1, want_hist: bool = True):
+        """Alg. 1 driver (sqngd_run): returns (best snapshot dict, best_wpsl [R], best_iter [R],
+        wpsl_hist [T][R] or None, result dict); `st` is advanced in place."""
+        t = self.torch
+        best = {k: t.empty_like(st[k]) for k in ("z", "rho", "w")}
+        best["theta"] = t.empty_like(st["theta"]) if st.get("theta") is not None else None
+        bw = t.empty(self.R, dtype=t.float64, device=self.device)
+        bi = t.empty(self.R, dtype=t.int32, device=self.device)
+        hist = t.full((T, self.R), float("nan"), dtype=t.float64, device=self.device) if want_hist else None
+        cs = self._cstate(st)
+        cb = State(z=_ptr(best["z"]), rho=_ptr(best["rho"]), w=_ptr(best["w"]), theta=_ptr(best["theta"]))
+        res = RunResult()
+        opts = RunOpts(T=int(T), patience=int(patience), check_every=int(check_every))
+        self._check(lib().sqngd_run(self.h, C.byref(cs), C.byref(opts), C.byref(cb), _ptr(bw), _ptr(bi), _ptr(hist),
+                                    C.byref(res), self._stream()))
+        st["t_a"], st["t_b"] = cs.t_a, cs.t_b
+        return best, bw, bi, hist, {"iterations": res.iterations, "steps_run": res.steps_run,
+                                    "stopped": bool(res.stopped)}
+
+    def _cstate(self, st: dict) -> State:
+        return State(z=_ptr(st["z"]), rho=_ptr(st["rho"]), w=_ptr(st["w"]), m_z=_ptr(st["m_z"]), v_z=_ptr(st["v_z"]),
+                     m_rho=_ptr(st["m_rho"]), v_rho=_ptr(st["v_rho"]), m_w=_ptr(st["m_w"]), v_w=_ptr(st["v_w"]),
+                     t_a=int(st["t_a"]), t_b=int(st["t_b"]),
+                     theta=_ptr(st.get("theta")), m_theta=_ptr(st.get("m_theta")),
+                     v_theta=_ptr(st.get("v_theta")), y0=_ptr(st.get("y0")))
 
     def step(self, st: dict, block: int = BLOCK_AB, hist=None, hard_met=None):
         cs = State(z=_ptr(st["z"]), rho=_ptr(st["rho"]), w=_ptr(st["w"]), m_z=_ptr(st["m_z"]), v_z=_ptr(st["v_z"]),

@@ -268,3 +268,25 @@ def test_step_graph_replay_matches_eager():
         assert torch.equal(a[k], b[k]), k
     assert torch.equal(ha, hb) and torch.equal(ma, mb)
     assert a["t_a"] == b["t_a"] == 6 and a["t_b"] == b["t_b"] == 6
+
+
+@pytest.mark.parametrize("engine", [sqngd.ENGINE_FFT, sqngd.ENGINE_CHEBYSHEV])
+def test_step_deterministic_with_restarts(engine):
+    """R = 2 restarts, R M = 4 filter rows (not a multiple of the row kernel's groups per CTA): the
+    same Step-A sequence twice is bit-identical (a padding group once raced on the last row's Adam
+    moments)."""
+    c = Cfg("detR", M=2, N=32, B=4, K=9, f_lo=-0.5, f_hi=0.5, r_n=4, R=2, n_h=3, n_x=2, lr_w=0.3, lr_z=3e-2,
+            doppler_engine=engine)
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=31)
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    w = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
+    ctx = sqngd.Context(c)
+    outs = []
+    for _ in range(2):
+        st = ctx.new_state(T(z), T(rho), T(w))
+        for _ in range(6):
+            ctx.step(st, sqngd.BLOCK_AB)
+        outs.append(st)
+    ctx.sync()
+    for k in ("z", "rho", "w", "m_w", "v_w", "m_z", "v_z", "m_rho", "v_rho"):
+        assert torch.equal(outs[0][k], outs[1][k]), k

@@ -1,0 +1,105 @@
+"""Alg. 1 driver sqngd_run through the C-ABI.
+
+The reference is the stopping rule and best-snapshot rule written out here in Python and applied
+to the hard-WPSL history the driver reports, plus a replay: the driver's best snapshot must be
+bit-identical to the state after best_iter plain sqngd_step(A+B) calls from the same start
+(the steps are deterministic)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2604_25728_b200 import inputs, sqngd  # noqa: E402
+from paper_2604_25728_b200.configs import Cfg  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def rule(hist, patience):
+    """(stop iteration or None, best_iter [R], best_wpsl [R]) of the rule in include/sqngd.h."""
+    T, R = hist.shape
+    best = np.full(R, math.inf)
+    bi = np.zeros(R, int)
+    stall = np.zeros(R, int)
+    for t in range(1, T + 1):
+        for r in range(R):
+            v = hist[t - 1, r]
+            if v < best[r]:
+                best[r], bi[r], stall[r] = v, t, 0
+            else:
+                stall[r] += 1
+        if patience > 0 and (stall >= patience).all():
+            return t, bi, best
+    return None, bi, best
+
+
+def setup(c, idx):
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=idx)
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    w = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
+    return [torch.as_tensor(a, device=DEV) for a in (z, rho, w)]
+
+
+@pytest.mark.parametrize("patience,check_every", [(2, 1), (3, 4), (0, 1)])
+def test_run_rule_and_snapshot(patience, check_every):
+    c = Cfg("run", M=2, N=32, B=4, K=9, f_lo=-0.5, f_hi=0.5, r_n=4, R=2, n_h=2, n_x=2, lr_w=0.3, lr_z=3e-2)
+    T = 16
+    ctx = sqngd.Context(c)
+    z, rho, w = setup(c, 31)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        st = ctx.new_state(z, rho, w)
+        best, bw, bi, hist, res = ctx.run(st, T=T, patience=patience, check_every=check_every)
+    torch.cuda.synchronize()
+    h = hist.cpu().numpy()
+    stop, bi_ref, bw_ref = rule(np.nan_to_num(h, nan=math.inf)[: res["iterations"]], patience)
+    if patience > 0 and stop is not None:
+        assert res["stopped"] and res["iterations"] == stop
+        assert res["iterations"] <= res["steps_run"] <= res["iterations"] + check_every - 1
+        assert np.isnan(h[res["iterations"]:]).all()  # no history past the stop
+    else:
+        assert not res["stopped"] and res["iterations"] == T
+    np.testing.assert_array_equal(bi.cpu().numpy(), bi_ref)
+    np.testing.assert_array_equal(bw.cpu().numpy(), bw_ref)
+    assert np.isfinite(h[: res["iterations"]]).all() and (h[: res["iterations"]] > 0).all()
+    # replay: the snapshot of restart r is the state after bi[r] outer iterations (the same launch
+    # sequence as the driver's: every step also evaluates the hard metrics)
+    hard = torch.empty(c.R * sqngd.METRICS_BYTES, dtype=torch.uint8, device=DEV)
+    with torch.cuda.stream(side):
+        st2 = ctx.new_state(z, rho, w)
+        snaps = {}
+        for t in range(1, int(bi_ref.max()) + 1):
+            ctx.step(st2, sqngd.BLOCK_AB, hard_met=hard)
+            for r in range(c.R):
+                if bi_ref[r] == t:
+                    snaps[r] = {k: st2[k][r].clone() for k in ("z", "rho", "w")}
+    torch.cuda.synchronize()
+    for r in range(c.R):
+        for k in ("z", "rho", "w"):
+            assert torch.equal(best[k][r], snaps[r][k]), (r, k)
+
+
+def test_run_generator_mode_snapshot_has_theta():
+    c = Cfg("run_net", M=2, N=32, B=4, K=5, f_lo=-0.5, f_hi=0.5, r_n=4, n_h=1, n_x=2, lr_theta=1e-3,
+            net_width=16, net_depth=1)
+    ctx = sqngd.Context(c)
+    th = torch.as_tensor(inputs.net_params(1, c.M * c.N, 16, 1, config_index=5), device=DEV)
+    y0 = torch.as_tensor(inputs.net_input(1, c.M, c.N, c.B, config_index=5), device=DEV)
+    z = ctx.net_forward(th, y0)
+    rho = torch.as_tensor(inputs.init_thresholds(1, c.B, c.r_n), device=DEV)
+    w = ctx.quantize(z, rho, soft=False, want_b=False, want_dq=False)["s_hard"]
+    st = ctx.new_state(z, rho, w, theta=th, y0=y0)
+    best, bw, bi, hist, res = ctx.run(st, T=6, patience=0)
+    ctx.sync()
+    assert res["iterations"] == 6 and not res["stopped"]
+    b = int(bi.cpu().numpy()[0])
+    assert 1 <= b <= 6
+    assert bw.cpu().numpy()[0] == np.min(hist.cpu().numpy()[:, 0])
+    # the snapshot's z is the generator output of the snapshot's theta
+    z2 = ctx.net_forward(best["theta"], y0)
+    ctx.sync()
+    assert torch.equal(z2, best["z"])
