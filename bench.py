@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-generator", dest="generator", action="store_false",
                     help="skip the generator-mode (z = f_theta(y0)) line")
+    ap.add_argument("--no-torch", dest="torch_comparator", action="store_false",
+                    help="skip the torch.fft + autograd comparator line")
     args = ap.parse_args()
 
     c = CF.CONFIGS[args.config]
@@ -429,6 +431,22 @@ def main():
                          "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
                          "bytes_per_update": upd_bytes,
                          "timing": "CUDA events around each Step-B generator update in the eager profiled pass"}}
+    if args.torch_comparator:  # NEXT-4: the same Step-B loss+grad in torch.fft + autograd on this GPU
+        from tools.torch_autograd import time_torch_step_b
+
+        zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
+        wt = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"]
+        ev_s, ms_t, loss_t, gz_t = time_torch_step_b(c.with_(R=1), zt[:1], rt[:1], wt[:1], dev)
+        met, gz_o, _ = ctx.af_loss_grad(zt, rt, wt, sqngd.WRT_TRANSMIT)
+        ctx.sync()
+        loss_o = ctx.metrics(met)[0]["loss"]
+        gz_o = gz_o[:1].reshape(gz_t.shape)
+        line["torch_autograd"] = {
+            "what": "Step-B loss+grad (LSE) as torch.fft correlations + dense |A| + autograd on the same GPU "
+                    "(paper-style framework implementation; context, not a parity reference)",
+            "value": ev_s, "unit": "Step-B loss+grad evals/s", "ms_per_eval": ms_t,
+            "loss_rel_diff_vs_ours": abs(loss_t - loss_o) / abs(loss_o),
+            "grad_z_rel_diff_vs_ours": float(torch.linalg.norm(gz_t - gz_o) / torch.linalg.norm(gz_o))}
     if fft_run is not None:
         line["fft_engine"] = {"value": fft_run["value"], "unit": UNIT, "ms_per_step": fft_run["ms_per_step"],
                               "cells_per_s": fft_run["value"] * c.cells / c.R, "roofline": fft_run["roofline"],
