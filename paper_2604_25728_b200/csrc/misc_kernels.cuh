@@ -512,6 +512,10 @@ struct RhoFinish {
   float lo, hi, gap;
 };
 
+// SORT: the block sorts its chunk's (z, dy) pairs by z in shared memory (bitonic, deterministic), and
+// every warp then visits only the elements inside its threshold window (two binary searches)
+// instead of window-testing the whole chunk.  Requires chunk <= 256 (= blockDim.x).
+template <bool SORT>
 __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
                                                        const float* __restrict__ rho, const float* __restrict__ dy,
                                                        float* part, RhoFinish fin) {
@@ -521,10 +525,63 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const float ri = i < BR ? rho[(size_t)r * BR + i] : rho[(size_t)r * BR + BR - 1];
   const int e0 = ch * chunk, e1 = min(MN, e0 + chunk);
-  for (int e = e0 + threadIdx.x; e < e0 + ((e1 - e0 + 3) & ~3); e += blockDim.x)
-    zd[e - e0] = e < e1 ? make_float2(z[(size_t)r * MN + e], dy[(size_t)r * MN + e]) : make_float2(1e30f, 0.f);
+  if (SORT) {
+    for (int e = threadIdx.x; e < 256; e += blockDim.x)
+      zd[e] = e0 + e < e1 ? make_float2(z[(size_t)r * MN + e0 + e], dy[(size_t)r * MN + e0 + e])
+                          : make_float2(1e30f, 0.f);
+  } else {
+    for (int e = e0 + threadIdx.x; e < e0 + ((e1 - e0 + 3) & ~3); e += blockDim.x)
+      zd[e - e0] = e < e1 ? make_float2(z[(size_t)r * MN + e], dy[(size_t)r * MN + e]) : make_float2(1e30f, 0.f);
+  }
   __syncthreads();
   const float win = 12.f / c;
+  if (SORT) {
+    // bitonic sort of 256 (z, dy) pairs by z (ties by dy, so the order is a function of the values)
+    const int t = threadIdx.x;
+    for (int kk = 2; kk <= 256; kk <<= 1)
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        const int ixj = t ^ jj;
+        if (ixj > t) {
+          const float2 a = zd[t], b = zd[ixj];
+          const bool gt = a.x > b.x || (a.x == b.x && a.y > b.y);
+          if (gt == ((t & kk) == 0)) {
+            zd[t] = b;
+            zd[ixj] = a;
+          }
+        }
+        __syncthreads();
+      }
+    float wlo = ri, whi = ri;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+      whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+    }
+    wlo -= win;
+    whi += win;
+    int lo = 0, hi = 256;  // first index with z >= wlo
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (zd[mid].x < wlo) lo = mid + 1; else hi = mid;
+    }
+    int lo2 = lo, hi2 = 256;  // first index with z > whi
+    while (lo2 < hi2) {
+      const int mid = (lo2 + hi2) >> 1;
+      if (zd[mid].x <= whi) lo2 = mid + 1; else hi2 = mid;
+    }
+    const float k2 = -2.f * 1.4426950408889634f;
+    float acc = 0.f;
+    for (int e = lo; e < lo2; ++e) {
+      const float2 p = zd[e];
+      const float au = c * fabsf(p.x - ri);
+      const float e2 = ex2a_m(k2 * au);
+      const float inv = rcp_m(1.f + e2);
+      const float sech2 = 4.f * e2 * inv * inv;
+      acc = fmaf(au < 12.f ? sech2 : 0.f, p.y, acc);
+    }
+    if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
+  }
+  if (!SORT) {
   float wlo = ri, whi = ri;  // the warp's threshold range (any order)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -554,6 +611,7 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
     }
   }
   if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
+  }
   if (!fin.gsum && !fin.z) return;
   __shared__ int last_tb, last_ch;
   __threadfence();
@@ -679,18 +737,34 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
   while (n2 < BR) n2 <<= 1;
   if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {  // Adam step, then the projection
-    float x = INFINITY;
-    if (i < BR) {
-      const size_t j = (size_t)r * BR + i;
-      const float gi = __ldcg(g + i);
-      const float mi = b1 * mr[j] + (1.f - b1) * gi;
-      const float vi = b2 * vr[j] + (1.f - b2) * gi * gi;
-      mr[j] = mi;
-      vr[j] = vi;
-      x = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  for (int base = 0; base < n2; base += 8 * blockDim.x) {  // Adam step (all loads issued first), then the projection
+    float gv[8], mv[8], vv[8], pv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + k * blockDim.x + threadIdx.x;
+      if (i < BR) {
+        const size_t j = (size_t)r * BR + i;
+        gv[k] = __ldcg(g + i);
+        mv[k] = mr[j];
+        vv[k] = vr[j];
+        pv[k] = p[i];
+      }
     }
-    sr[i] = x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + k * blockDim.x + threadIdx.x;
+      if (i >= n2) break;
+      float x = INFINITY;
+      if (i < BR) {
+        const size_t j = (size_t)r * BR + i;
+        const float mi = b1 * mv[k] + (1.f - b1) * gv[k];
+        const float vi = b2 * vv[k] + (1.f - b2) * gv[k] * gv[k];
+        mr[j] = mi;
+        vr[j] = vi;
+        x = pv[k] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+      }
+      sr[i] = x;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i + 1 < BR; i += blockDim.x)

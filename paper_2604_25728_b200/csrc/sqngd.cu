@@ -77,6 +77,7 @@ struct sqngd_ctx_s {
   float* dy = nullptr;         // [R][M][N]
   float* rho_part = nullptr;   // [R][nchunk][BR]
   int rho_chunk = 256, rho_nchunk = 1;
+  bool rho_sort = true;        // k_grad_rho_part sorts its chunk (needs rho_chunk <= 256)
   int* rho_cnt = nullptr;      // [R][64] threshold-block + [R][nchunk] element-chunk arrival counters
   float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
   float* gz = nullptr;         // [R][M][N]
@@ -730,6 +731,12 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
   CK(cudaMalloc(&ctx->red_grad, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->dy, sizeof(float) * RMN));
+  if (const char* ev = getenv("SQNGD_RHO_CHUNK")) {  // tuning override: elements per grad-rho block
+    const int ch = atoi(ev);
+    if (ch >= 32 && ch <= 1024 && ch % 4 == 0) ctx->rho_chunk = ch;
+  }
+  if (const char* ev = getenv("SQNGD_RHO_SORT")) ctx->rho_sort = ev[0] != '0';
+  if (ctx->rho_chunk > 256) ctx->rho_sort = false;
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
   CK(cudaMalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
@@ -1272,7 +1279,8 @@ static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho
   RhoFinish fin{};
   fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
   fin.gsum = grad_rho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64; fin.status = ctx->status;
-  k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
+  if (ctx->rho_sort) k_grad_rho_part<true><<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
+  else k_grad_rho_part<false><<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
   ctx->launches += 1;
   return launch_check(ctx, "grad rho");
 }
@@ -1434,8 +1442,12 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
           fin.rho = stt->rho; fin.mr = stt->m_rho; fin.vr = stt->v_rho; fin.apr = ap(c.lr_z, 1, i);
           fin.lo = 1e-4f; fin.hi = 1.0f - 1e-4f; fin.gap = 1e-6f;
         }
-        k_grad_rho_part<<<g1, 256, fuse_rho ? 2 * n2 * sizeof(float) : 0, st>>>(
-            c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy, ctx->rho_part, fin);
+        if (ctx->rho_sort)
+          k_grad_rho_part<true><<<g1, 256, fuse_rho ? 2 * n2 * sizeof(float) : 0, st>>>(
+              c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy, ctx->rho_part, fin);
+        else
+          k_grad_rho_part<false><<<g1, 256, fuse_rho ? 2 * n2 * sizeof(float) : 0, st>>>(
+              c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy, ctx->rho_part, fin);
         if (!fuse_rho)
           k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
                                                                         ctx->grho, ap(c.lr_z, 1, i), 1e-4f,

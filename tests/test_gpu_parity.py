@@ -290,3 +290,25 @@ def test_step_deterministic_with_restarts(engine):
     ctx.sync()
     for k in ("z", "rho", "w", "m_w", "v_w", "m_z", "v_z", "m_rho", "v_rho"):
         assert torch.equal(outs[0][k], outs[1][k]), k
+
+
+@pytest.mark.parametrize("mode", [sqngd.LOSS_MAX, sqngd.LOSS_LSE])
+def test_correlation_mode_K1(mode):
+    """Correlation mode (K = 1, f = 0: the periodic-free aperiodic correlation workload of the
+    paper's Table I): map, metrics and both gradients against the oracle."""
+    c = Cfg("corr", M=4, N=256, B=8, K=1, f_lo=0.0, f_hi=0.0, r_n=8, loss_mode=mode,
+            beta_or_p=200.0 if mode == sqngd.LOSS_LSE else 0.0)
+    s, w = random_inputs(c, 41)
+    ctx = sqngd.Context(c)
+    assert ctx.engine_info()["engine"] == "fft"
+    met, _, amap = ctx.af_forward(T(s), T(w), want_map=True)
+    m = ctx.metrics(met)[0]
+    ref, _, A = O.af(c, s, w, want_A=True)
+    check_map(amap.cpu().numpy(), A, c.N)
+    assert abs(m["loss"] - ref[0]["loss"]) <= 1e-5 * abs(ref[0]["loss"])
+    _, gw = ctx.loss_grad_s(T(s), T(w), sqngd.WRT_FILTERS)
+    _, gs = ctx.loss_grad_s(T(s), T(w), sqngd.WRT_TRANSMIT)
+    ctx.sync()
+    _, gw_ref, gs_ref = O.loss_grad(c, s, w)
+    assert rel(gw.cpu().numpy(), gw_ref) < 1e-4
+    assert rel(gs.cpu().numpy(), gs_ref) < 1e-4
