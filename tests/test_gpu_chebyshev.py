@@ -242,3 +242,26 @@ def test_engine_selection():
     assert sqngd.Context(C4).engine_info()["engine"] == "fft"
     with pytest.raises(sqngd.SqngdError):
         sqngd.Context(C4.with_(doppler_engine=CHEB))
+
+
+def test_step_A_teacher_forced():
+    """One Step-A inner step on the Chebyshev engine (R = 2, R M = 6 rows): Adam(Re w, Im w) + Pi_H
+    applied to the GPU's own grad_w equals the oracle's."""
+    c = Cfg("stepA", M=3, N=40, B=4, K=31, f_lo=-0.5, f_hi=0.5, r_n=4, R=2, loss_mode=sqngd.LOSS_LSE,
+            beta_or_p=60.0, doppler_engine=CHEB, n_h=1, n_x=1, lr_w=5e-2)
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=19)
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    w = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
+    ctx = sqngd.Context(c)
+    st = ctx.new_state(T(z), T(rho), T(w))
+    _, gw = ctx.af_loss_grad(st["z"], st["rho"], st["w"], sqngd.WRT_FILTERS)
+    ctx.sync()
+    gw = gw.cpu().numpy().astype(np.complex128)
+    q = O.quantize(c, z, rho)
+    _, gw_ref, _ = O.loss_grad(c, q["s_hard"], w, want_w=True, want_s=False)
+    assert rel(gw, gw_ref) < 1e-4
+    ctx.step(st, sqngd.BLOCK_A)
+    ctx.sync()
+    ost = O.new_state(z, rho, w)
+    O.step(c, ost, block=1, grads_from=lambda kind, i, s_: gw)
+    np.testing.assert_allclose(st["w"].cpu().numpy(), ost["w"], rtol=0, atol=2e-6)
