@@ -114,6 +114,8 @@ struct sqngd_ctx_s {
   NetDims nd{};
   NetWs nws{};
   float* net_ws = nullptr;
+  cudaStream_t side_net = nullptr;               // graph branch: generator backward beside the grad-rho pass
+  cudaEvent_t ev_nf = nullptr, ev_nj = nullptr;
   // CUDA graphs of sqngd_step (one per (state buffers, block, outputs, profiling))
   struct GraphEntry {
     const void* key[16];
@@ -753,6 +755,9 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     CK(cudaMalloc(&ctx->net_ws, sizeof(float) * net_ws_floats(nd)));
     ctx->nws = net_ws_carve(nd, ctx->net_ws);
     CK(net_prepare(nd));
+    CK(cudaStreamCreateWithFlags(&ctx->side_net, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_nf, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_nj, cudaEventDisableTiming));
   }
 
   // Doppler twiddles e^{j 2 pi n f_k / N}, n one-based (Eq. 33, Q2), phase reduced mod 1 in fp64.
@@ -936,6 +941,9 @@ void sqngd_destroy(sqngd_ctx ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_nf) cudaEventDestroy(ctx->ev_nf);
+  if (ctx->ev_nj) cudaEventDestroy(ctx->ev_nj);
+  if (ctx->side_net) cudaStreamDestroy(ctx->side_net);
   ctx->comm.destroy();
   delete ctx;
 }
@@ -1427,6 +1435,16 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
       if ((rc = run_loss_grad(ctx, ctx->s_soft, w2, SQNGD_WRT_TRANSMIT, ctx->met, nullptr, nullptr, ctx->dq, ctx->gz,
                               loss_hist, col0 + i, st)))
         return rc;
+      // Generator mode: dL/dtheta + Adam(theta) only need dL/dz (and the tape), not the thresholds, so
+      // the generator backward runs on a forked branch beside the grad-rho pass (profiling: inline).
+      const bool fork_net = ctx->net && !ctx->prof;
+      if (fork_net) {
+        CK(cudaEventRecord(ctx->ev_nf, st));
+        CK(cudaStreamWaitEvent(ctx->side_net, ctx->ev_nf, 0));
+        CK(net_backward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, ctx->gz, nullptr, stt->m_theta, stt->v_theta,
+                        ap(c.lr_theta, 1, i), ctx->status, ctx->side_net, &ctx->launches));
+        CK(cudaEventRecord(ctx->ev_nj, ctx->side_net));
+      }
       {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
         dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);
         RhoFinish fin{};  // grad_rho sums, Adam(z) and Adam(rho) + projection by last-arriving blocks
@@ -1456,8 +1474,12 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
       }
       if (ctx->net) {  // Adam on theta through the generator's adjoint, then z = f_theta(y0) again
         ProfScope ps(ctx, 3, st);
-        CK(net_backward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, ctx->gz, nullptr, stt->m_theta, stt->v_theta,
-                        ap(c.lr_theta, 1, i), ctx->status, st, &ctx->launches));
+        if (fork_net) {
+          CK(cudaStreamWaitEvent(st, ctx->ev_nj, 0));
+        } else {
+          CK(net_backward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, ctx->gz, nullptr, stt->m_theta, stt->v_theta,
+                          ap(c.lr_theta, 1, i), ctx->status, st, &ctx->launches));
+        }
         CK(net_forward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, false, st, &ctx->launches));
       }
       if ((rc = launch_check(ctx, "step B update"))) return rc;
