@@ -103,3 +103,25 @@ def test_run_generator_mode_snapshot_has_theta():
     z2 = ctx.net_forward(best["theta"], y0)
     ctx.sync()
     assert torch.equal(z2, best["z"])
+
+
+def test_alg1_improves_hard_psl():
+    """NEXT-3 trend check: from the seeded matched start, 60 outer iterations of
+    Alg. 1 at C1 lower the hard-waveform PSL by more than 3 dB (measured: -11.6 -> -17.4 dB)."""
+    from paper_2604_25728_b200.configs import C1
+
+    c = C1.with_(loss_mode=sqngd.LOSS_LSE, beta_or_p=200.0)
+    ctx = sqngd.Context(c)
+    z = torch.as_tensor(inputs.phase_params(1, c.M, c.N, c.index), device=DEV)
+    rho = torch.as_tensor(inputs.init_thresholds(1, c.B, c.r_n), device=DEV)
+    w = ctx.quantize(z, rho, soft=False, want_b=False, want_dq=False)["s_hard"]
+    met, _, _ = ctx.af_forward(w, w)
+    start = ctx.metrics(met)[0]["wpsl"]
+    st = ctx.new_state(z, rho, w)
+    best, bw, bi, hist, res = ctx.run(st, T=60, patience=0)
+    ctx.sync()
+    assert 20 * math.log10(float(bw.cpu()[0])) < 20 * math.log10(start) - 3.0
+    # the snapshot is consistent: its hard waveform evaluates to the recorded best WPSL
+    q = ctx.quantize(best["z"], best["rho"], soft=False, want_b=False, want_dq=False)
+    met, _, _ = ctx.af_forward(q["s_hard"], best["w"])
+    assert ctx.metrics(met)[0]["wpsl"] == float(bw.cpu()[0])
