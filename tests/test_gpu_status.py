@@ -80,3 +80,25 @@ def test_step_keeps_last_finite_iterate(engine):
     expect(ctx, sqngd.E_NONFINITE)
     assert torch.equal(st["z"], z0) and torch.equal(st["rho"], rho0)
     assert torch.equal(torch.view_as_real(st["w"]).nan_to_num(), torch.view_as_real(w0).nan_to_num())
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_generator_step_keeps_last_finite_iterate(engine):
+    """Generator mode (NEXT-2): a non-finite gradient latches E_NONFINITE and neither theta, its
+    Adam moments nor rho move (the generator backward runs on a forked branch in the graph)."""
+    c = cfg(engine, net_width=16, net_depth=1, lr_theta=1e-3)
+    z, _, w = sw(c)
+    rho = inputs.init_thresholds(1, c.B, c.r_n)
+    w[0, 0, 7] = np.inf
+    th = T(inputs.net_params(1, c.M * c.N, 16, 1, config_index=6))
+    y0 = T(inputs.net_input(1, c.M, c.N, c.B, config_index=6))
+    ctx = sqngd.Context(c)
+    st = ctx.new_state(T(z), T(rho), T(w), theta=th, y0=y0)
+    th0, rho0 = st["theta"].clone(), st["rho"].clone()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):  # graph-captured step (forked generator branch)
+        ctx.step(st, sqngd.BLOCK_B)
+    side.synchronize()
+    expect(ctx, sqngd.E_NONFINITE)
+    assert torch.equal(st["theta"], th0) and torch.equal(st["rho"], rho0)
+    assert not st["m_theta"].any() and not st["v_theta"].any()
