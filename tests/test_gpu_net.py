@@ -184,3 +184,24 @@ def test_C3_generator_step_runs():
     assert np.abs(st["z"].cpu().numpy().reshape(Din) - zr).max() <= 2e-5
     m = sqngd.metrics_from_bytes(hard.cpu().numpy())[0]
     assert 0 < m["wpsl"] < 1
+
+
+@pytest.mark.parametrize("stream", ["0", "1"])
+def test_hidden_chain_variants_agree(stream, monkeypatch):
+    """The hidden layers run either on an 8-CTA cluster (DSMEM exchanges, the default) or on one CTA
+    streaming the matrices through a TMA ring (SQNGD_NET_STREAM=1, W in {32, 64, 128}, measured
+    slower); both match the oracle at the paper's 5 x 128."""
+    monkeypatch.setenv("SQNGD_NET_STREAM", stream)
+    c = Cfg("n_var", M=4, N=256, B=8, K=3, f_lo=-0.5, f_hi=0.5, r_n=2, R=2, net_width=128, net_depth=5)
+    Din = c.M * c.N
+    th = inputs.net_params(c.R, Din, 128, 5, config_index=9, bias_scale=0.1)
+    y0 = inputs.net_input(c.R, c.M, c.N, c.B, config_index=9)
+    gz = inputs.uniform01_f32(99, c.R * Din).reshape(c.R, Din) - np.float32(0.5)
+    ctx = sqngd.Context(c)
+    z = ctx.net_forward(T(th), T(y0))
+    g = ctx.net_backward(T(th), T(y0), z, T(gz.reshape(c.R, c.M, c.N)))
+    ctx.sync()
+    zr, tapes = NO.forward_batch(th.astype(np.float64), y0, Din, 128, 5)
+    assert np.abs(z.cpu().numpy().reshape(c.R, Din) - zr).max() <= 2e-5
+    gr = NO.backward_batch(th.astype(np.float64), tapes, gz, Din, 128, 5)
+    assert rel(g.cpu().numpy(), gr) <= 1e-4
