@@ -443,11 +443,18 @@ __device__ __forceinline__ uint32_t f16_pair(int k, const float (&x)[5]) {
   return (uint32_t)f16_col(k, x) | ((uint32_t)f16_col(k + 1, x) << 16);
 }
 
-// one warp per CTA (kw = 1); 20 resident CTAs/SM caps the registers at 96 (12 B of spills):
-// 21 warps/SM instead of 16 at the compiler's 128, measured 3-4% faster at C3 and C5
+#ifndef SQNGD_LRT_UNROLL
+#define SQNGD_LRT_UNROLL 1
+#endif
+constexpr int kLrtUnroll = SQNGD_LRT_UNROLL;  // tile-loop unroll of k_lrt (tuning)
+
+// one warp per CTA (kw = 1); 16 resident CTAs/SM caps the registers at 128 (no spills).  Re-measured
+// after the FP16 forward / lane-owned K layout: 128 registers beat the former cap of 96 (20 CTAs/SM,
+// 12 B of spills) by 2% at C3 (1.804 vs 1.840 ms per step) and 2.5% at C5; 154 registers (12 CTAs)
+// and a tile-loop unroll of 2 were slower (tools: SQNGD_LRT_MINB / SQNGD_LRT_UNROLL).
 #ifndef SQNGD_LRT_MAXT
 #define SQNGD_LRT_MAXT 32
-#define SQNGD_LRT_MINB 20
+#define SQNGD_LRT_MINB 16
 #endif
 template <int Q, int LM, bool HW, bool GRAD>
 __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const LrtArgs a) {
@@ -652,7 +659,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     const int tf_end = t1 < a.NTF ? t1 : a.NTF;
     float4 nfa = make_float4(0.f, 0.f, 0.f, 0.f), nfb = nfa, nga = nfa, ngb = nfa;
     if (t0 < tf_end) ldB(t0, nfa, nfb, nga, ngb);
-#pragma unroll 1
+#pragma unroll kLrtUnroll
     for (int t = t0; t < tf_end; ++t) {  // B fragments of the next tile are loaded one tile ahead
       const float4 fa = nfa, fb = nfb, ga = nga, gb = ngb;
 #if SQNGD_LRT_PREFETCH
