@@ -60,7 +60,19 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
   constexpr int LPE = 8;
   const int r = blockIdx.y;
   const float* rr = rho + (size_t)r * BR;
-  for (int i = threadIdx.x; i < BR; i += blockDim.x) rs[i] = rr[i];
+  for (int base = 0; base < BR; base += 8 * (int)blockDim.x) {  // 8 loads in flight per thread
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + k * blockDim.x + threadIdx.x;
+      v[k] = i < BR ? __ldg(rr + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + k * blockDim.x + threadIdx.x;
+      if (i < BR) rs[i] = v[k];
+    }
+  }
   __syncthreads();
   const int sub = threadIdx.x & (LPE - 1);
   const int e0 = blockIdx.x * (blockDim.x / LPE) + threadIdx.x / LPE;
