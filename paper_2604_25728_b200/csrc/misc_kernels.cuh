@@ -425,6 +425,21 @@ __global__ void __launch_bounds__(PL::T* G)
     const float2 x = __ldg(in + (size_t)row * P + t + i * T);
     v[i] = make_float2(x.x, -x.y);
   }
+  // the row's s, w and Adam moments, loaded up front: their latency hides behind the IFFT (inside
+  // the update loop the moment stores would otherwise serialize one round trip per element)
+  float2 sv[E], wv[E], mv[E], vv[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + i * T;
+    const size_t j = (size_t)row * N + (n < N ? n : 0);
+    sv[i] = f.s[j];
+    wv[i] = w[j];
+    mv[i] = reinterpret_cast<const float2*>(mw)[j];
+    vv[i] = reinterpret_cast<const float2*>(vw)[j];
+  }
+  const double2 gc = snrl_coef(f, row);
+  float c1, c2;
+  ap.corr(c1, c2);
   int par = 0;
   double2 cacc = make_double2(0.0, 0.0);
   // one inlined FFT instance for both transforms (IFFT of the spectral sum, then FFT of the new
@@ -433,9 +448,6 @@ __global__ void __launch_bounds__(PL::T* G)
   for (int ph = 0; ph < 2; ++ph) {
     fft<PL, -1>(v, ftw, gsm, t, par, gops.sync);
     if (ph == 1) break;
-    const double2 gc = snrl_coef(f, row);
-    float c1, c2;
-    ap.corr(c1, c2);
     float bad = 0.f;
     double e = 0.0;
 #pragma unroll
@@ -444,23 +456,23 @@ __global__ void __launch_bounds__(PL::T* G)
       float2 wn = make_float2(0.f, 0.f);
       if (n < N) {
         const size_t j = (size_t)row * N + n;
-        const float2 sv = f.s[j];
-        const float re = 2.f * (v[i].x + ((float)gc.x * sv.x + (float)gc.y * sv.y));   // d = conj(v)
-        const float im = 2.f * (-v[i].y + ((float)gc.x * sv.y - (float)gc.y * sv.x));
+        const float re = 2.f * (v[i].x + ((float)gc.x * sv[i].x + (float)gc.y * sv[i].y));   // d = conj(v)
+        const float im = 2.f * (-v[i].y + ((float)gc.x * sv[i].y - (float)gc.y * sv[i].x));
         if (!isfinite(re) || !isfinite(im)) bad = 1.f;
         if (f.grad_w && id < rows) f.grad_w[j] = make_float2(re, im);
         const float g2[2] = {re, im};
-        float x2[2] = {w[j].x, w[j].y};
+        float x2[2] = {wv[i].x, wv[i].y};
+        const float m2[2] = {mv[i].x, mv[i].y}, v2[2] = {vv[i].x, vv[i].y};
+        float mo[2], vo[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {  // Adam on the real parameters (Re w, Im w)
-          const size_t jj = 2 * j + q;
-          const float mi = ap.b1 * mw[jj] + (1.f - ap.b1) * g2[q];
-          const float vi = ap.b2 * vw[jj] + (1.f - ap.b2) * g2[q] * g2[q];
-          if (!skip_all && id < rows) {  // (a padding group duplicates the last row: no stores)
-            mw[jj] = mi;
-            vw[jj] = vi;
-          }
-          x2[q] -= ap.lr * (mi / c1) / (sqrtf(vi / c2) + ap.eps);
+          mo[q] = ap.b1 * m2[q] + (1.f - ap.b1) * g2[q];
+          vo[q] = ap.b2 * v2[q] + (1.f - ap.b2) * g2[q] * g2[q];
+          x2[q] -= ap.lr * (mo[q] / c1) / (sqrtf(vo[q] / c2) + ap.eps);
+        }
+        if (!skip_all && id < rows) {  // (a padding group duplicates the last row: no stores)
+          reinterpret_cast<float2*>(mw)[j] = make_float2(mo[0], mo[1]);
+          reinterpret_cast<float2*>(vw)[j] = make_float2(vo[0], vo[1]);
         }
         wn = make_float2(x2[0], x2[1]);
         e += (double)wn.x * wn.x + (double)wn.y * wn.y;
@@ -481,9 +493,9 @@ __global__ void __launch_bounds__(PL::T* G)
       if (n < N) {
         const size_t j = (size_t)row * N + n;
         if (id < rows) w[j] = v[i];
-        const float2 sv = f.s[j];  // c_l = sum_n s_l(n) conj(w_l(n)) for the next evaluation
-        cacc.x += (double)sv.x * v[i].x + (double)sv.y * v[i].y;
-        cacc.y += (double)sv.y * v[i].x - (double)sv.x * v[i].y;
+        // c_l = sum_n s_l(n) conj(w_l(n)) for the next evaluation
+        cacc.x += (double)sv[i].x * v[i].x + (double)sv[i].y * v[i].y;
+        cacc.y += (double)sv[i].y * v[i].x - (double)sv[i].x * v[i].y;
       }
     }
     cacc = gops.sum_d2(cacc);
