@@ -271,6 +271,42 @@ __device__ __forceinline__ double2 snrl_coef(const FinArgs& f, size_t row) {
   return make_double2(q * c.x, q * c.y);
 }
 
+// The element's inputs (s, w, dq), loaded ahead of the arithmetic by callers that batch them.
+struct FinIn {
+  float2 s, w;
+  float dq;
+};
+__device__ __forceinline__ FinIn finalize_load(const FinArgs& f, size_t e) {
+  FinIn in;
+  in.s = f.s[e];
+  in.w = f.wrt == 1 ? make_float2(0.f, 0.f) : f.w[e];
+  in.dq = (f.wrt != 1 && f.grad_z) ? f.dq[e] : 0.f;
+  return in;
+}
+__device__ __forceinline__ void finalize_pre(const FinArgs& f, size_t e, float2 rg, double2 gc, const FinIn& in,
+                                             int* status) {
+  const float gr = (float)gc.x, gi = (float)gc.y;
+  bool bad;
+  if (f.wrt == 1) {
+    const float2 sv = in.s;
+    const float re = rg.x + (gr * sv.x + gi * sv.y);
+    const float im = rg.y + (gr * sv.y - gi * sv.x);
+    if (f.grad_w) f.grad_w[e] = make_float2(2.f * re, 2.f * im);
+    bad = !isfinite(re) || !isfinite(im);
+  } else {
+    const float2 wv = in.w;
+    const float re = rg.x + (gr * wv.x - gi * wv.y);
+    const float im = rg.y + (gr * wv.y + gi * wv.x);
+    if (f.grad_s) f.grad_s[e] = make_float2(re, im);
+    const float2 sv = in.s;
+    const float d = 4.f * 3.14159265358979f * (im * sv.x - re * sv.y);  // Im(g conj(s))
+    if (f.dy) f.dy[e] = d;
+    if (f.grad_z) f.grad_z[e] = in.dq * d;
+    bad = !isfinite(re) || !isfinite(im);
+  }
+  if (bad) atomicOr(status, ST_NONFINITE);
+}
+
 __device__ __forceinline__ void finalize_elem(const FinArgs& f, size_t e, float2 rg, double2 gc, int* status) {
   const float gr = (float)gc.x, gi = (float)gc.y;
   bool bad;
@@ -352,6 +388,13 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   const bool live = m > -INFINITY && S > 0.0;
   const int q = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));  // two complex values per thread
   const int kl = threadIdx.x >> 5;                              // 8 k-lanes
+  FinIn fin0{}, fin1{};
+  double2 gcf = make_double2(0.0, 0.0);
+  if (a.fin && kl == 0 && q < a.len) {  // finalize inputs fetched now, overlapping the slot sums
+    fin0 = finalize_load(a.f, (size_t)ra * a.N + q);
+    if (q + 1 < a.len) fin1 = finalize_load(a.f, (size_t)ra * a.N + q + 1);
+    gcf = snrl_coef(a.f, ra);
+  }
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (live && q < a.len) {
     const int klo = max(0, a.u_lo - ra * a.K), khi = min(a.K, a.u_hi - ra * a.K);
@@ -385,9 +428,8 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
     const float nf = (float)norm;
     const float2 g0 = make_float2(t.x * nf, t.y * nf), g1 = make_float2(t.z * nf, t.w * nf);
     if (a.fin) {
-      const double2 gc = snrl_coef(a.f, ra);
-      finalize_elem(a.f, (size_t)ra * a.N + q, g0, gc, status);
-      if (q + 1 < a.len) finalize_elem(a.f, (size_t)ra * a.N + q + 1, g1, gc, status);
+      finalize_pre(a.f, (size_t)ra * a.N + q, g0, gcf, fin0, status);
+      if (q + 1 < a.len) finalize_pre(a.f, (size_t)ra * a.N + q + 1, g1, gcf, fin1, status);
     } else {
       float2* o = a.out + (size_t)ra * a.len + q;
       o[0] = g0;

@@ -144,37 +144,46 @@ __device__ __forceinline__ void net_in_block(const NetArgs& a, int bx, int by, i
   if (MODE != NM_FWD) gi = a.ga0[(size_t)r * a.W + i];
   float p = 0.f;
   if (VEC) {
+    // both float4 column groups' operands are loaded before any store (a store between them would
+    // serialize a second memory round trip)
+    float4 y4[2], w4[2], m4[2], v4[2];
+    bool in[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = j0 + h * 128 + lane * 4;
-      if (j >= a.Din) break;
-      const float4 y4 = *reinterpret_cast<const float4*>(y + j);
-      float4* wp = reinterpret_cast<float4*>(a.theta + base + j);
+      in[h] = j < a.Din;
+      const int jj = in[h] ? j : 0;
+      y4[h] = *reinterpret_cast<const float4*>(y + jj);
+      if (MODE != NM_GRAD) w4[h] = *reinterpret_cast<const float4*>(a.theta + base + jj);
+      if (MODE == NM_ADAM) {
+        m4[h] = *reinterpret_cast<const float4*>(a.m + base + jj);
+        v4[h] = *reinterpret_cast<const float4*>(a.v + base + jj);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!in[h]) break;
+      const int j = j0 + h * 128 + lane * 4;
+      const float4 yv = y4[h];
       if (MODE == NM_GRAD) {
-        *reinterpret_cast<float4*>(a.gtheta + base + j) = make_float4(gi * y4.x, gi * y4.y, gi * y4.z, gi * y4.w);
+        *reinterpret_cast<float4*>(a.gtheta + base + j) = make_float4(gi * yv.x, gi * yv.y, gi * yv.z, gi * yv.w);
         continue;
       }
-      float4 w4 = *wp, m4, v4;
-      float4 *mp = nullptr, *vp = nullptr;
-      if (MODE == NM_ADAM) {  // loaded before the status test resolves (one memory round trip)
-        mp = reinterpret_cast<float4*>(a.m + base + j);
-        vp = reinterpret_cast<float4*>(a.v + base + j);
-        m4 = *mp;
-        v4 = *vp;
-      }
+      float4 wv = w4[h];
       if (MODE == NM_ADAM && upd) {
-        w4.x = ad.upd(w4.x, m4.x, v4.x, gi * y4.x);
-        w4.y = ad.upd(w4.y, m4.y, v4.y, gi * y4.y);
-        w4.z = ad.upd(w4.z, m4.z, v4.z, gi * y4.z);
-        w4.w = ad.upd(w4.w, m4.w, v4.w, gi * y4.w);
-        *wp = w4;
-        *mp = m4;
-        *vp = v4;
+        float4 mv = m4[h], vv = v4[h];
+        wv.x = ad.upd(wv.x, mv.x, vv.x, gi * yv.x);
+        wv.y = ad.upd(wv.y, mv.y, vv.y, gi * yv.y);
+        wv.z = ad.upd(wv.z, mv.z, vv.z, gi * yv.z);
+        wv.w = ad.upd(wv.w, mv.w, vv.w, gi * yv.w);
+        *reinterpret_cast<float4*>(a.theta + base + j) = wv;
+        *reinterpret_cast<float4*>(a.m + base + j) = mv;
+        *reinterpret_cast<float4*>(a.v + base + j) = vv;
       }
-      p = fmaf(w4.x, y4.x, p);
-      p = fmaf(w4.y, y4.y, p);
-      p = fmaf(w4.z, y4.z, p);
-      p = fmaf(w4.w, y4.w, p);
+      p = fmaf(wv.x, yv.x, p);
+      p = fmaf(wv.y, yv.y, p);
+      p = fmaf(wv.z, yv.z, p);
+      p = fmaf(wv.w, yv.w, p);
     }
   } else {
 #pragma unroll
