@@ -235,9 +235,15 @@ def main():
                     help="skip the generator-mode (z = f_theta(y0)) line")
     ap.add_argument("--no-torch", dest="torch_comparator", action="store_false",
                     help="skip the torch.fft + autograd comparator line")
+    ap.add_argument("--restarts", type=int, default=0,
+                    help="independent restarts batched per GPU (default: the config's R)")
+    ap.add_argument("--batch-restarts", type=int, default=4,
+                    help="also time the config with this many restarts per GPU (context line; 0/1: skip)")
     args = ap.parse_args()
 
     c = CF.CONFIGS[args.config]
+    if args.restarts:
+        c = c.with_(R=args.restarts)
     mode = {"max": CF.LOSS_MAX, "lse": CF.LOSS_LSE, "pnorm": CF.LOSS_PNORM}[args.loss]
     c = c.with_(loss_mode=mode, beta_or_p={0: 0.0, 1: 200.0, 2: 16.0}[mode])
     if args.impl == "reference":
@@ -277,6 +283,11 @@ def main():
     def timed(cc, with_clocks):
         """W warm-up + K timed sqngd_step(A+B) calls (CUDA-graph replay), then an eager profiled
         pass over K more steps for the per-kernel CUDA-event times."""
+        R = cc.R
+        z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, g), c.M * c.N).reshape(c.M, c.N)
+                      for g in parallel.restart_ids(R, rank)])
+        rho = inputs.init_thresholds(R, c.B, c.r_n)
+        evals_per_step = (c.n_h + c.n_x) * R * world
         ctx = sqngd.Context(cc, device=local)
         zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
         net = {}
@@ -412,7 +423,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {**config_dict(c), "doppler_engine": eng_desc,
                    "parallelism": f"restarts x{world} (independent, no collective)"},
-        "cells_per_s": value * c.cells / c.R,
+        "cells_per_s": value * c.cells,
         "roofline": main_run["roofline"],
         "kernel_ms": main_run["kernel_ms"],
         "gpu_launches": main_run["launches"],
@@ -421,6 +432,14 @@ def main():
         "wall_s": main_run["wall_s"],
         "final_hard_pslr_db": 20 * math.log10(max(hm[0]["wpsl"], 1e-30)),
     }
+    if args.batch_restarts > 1 and c.R == 1:  # the same config with B independent restarts per GPU
+        ctxb, *_rest, b_run = timed(c.with_(R=args.batch_restarts), False)
+        ctxb.close()
+        line["restart_batched"] = {
+            "restarts_per_gpu": args.batch_restarts, "value": b_run["value"], "unit": UNIT,
+            "ms_per_step": b_run["ms_per_step"], "cells_per_s": b_run["value"] * c.cells,
+            "roofline": b_run["roofline"], "gpu_launches": b_run["launches"],
+            "what": "context: B independent seeded restarts batched in one context per GPU (the headline is R = 1)"}
     if args.generator:  # NEXT-2: the same step with the paper's ResNet generator z = f_theta(y0)
         W, D = 128, 5
         cg = c.with_(net_width=W, net_depth=D, lr_theta=1e-5)
@@ -461,7 +480,7 @@ def main():
             "grad_z_rel_diff_vs_ours": float(torch.linalg.norm(gz_t - gz_o) / torch.linalg.norm(gz_o))}
     if fft_run is not None:
         line["fft_engine"] = {"value": fft_run["value"], "unit": UNIT, "ms_per_step": fft_run["ms_per_step"],
-                              "cells_per_s": fft_run["value"] * c.cells / c.R, "roofline": fft_run["roofline"],
+                              "cells_per_s": fft_run["value"] * c.cells, "roofline": fft_run["roofline"],
                               "kernel_ms": fft_run["kernel_ms"], "gpu_launches": fft_run["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OMP_NUM_THREADS", str(cpu_info()))
