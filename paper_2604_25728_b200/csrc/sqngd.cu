@@ -690,7 +690,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     }
     if (const char* ev = getenv("SQNGD_LR_KW")) {  // tuning override
       const int kw = atoi(ev);
-      if (kw == 1 || kw == 2 || kw == 4 || kw == 8) {
+      // (k_lrt is compiled for SQNGD_LRT_MAXT threads per CTA: wider units only for the FP32 k_lr)
+      if ((kw == 1 || kw == 2 || kw == 4 || kw == 8) && (!ctx->lr_tc || kw * 32 <= SQNGD_LRT_MAXT)) {
         ctx->kw = kw;
         ctx->lr_smem = cf_bytes + (kw > 1 ? kw * rec_bytes : 0);
       }
