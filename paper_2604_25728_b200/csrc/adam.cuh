@@ -2,6 +2,11 @@
 // with external linkage here: common.cuh's functions stay in one TU).
 #pragma once
 
+// Programmatic dependent launch: every kernel first waits for its programmatic predecessors (a
+// no-op without one), so sqngd_step can turn the kernel-to-kernel edges of its CUDA graph into
+// programmatic edges and overlap each launch with the previous kernel's tail.
+#define SQ_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 namespace sq {
 
 enum : int { ST_INVALID = 1, ST_DEGENERATE = 2, ST_NONFINITE = 4 };

@@ -298,6 +298,7 @@ template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB)
     k_xhat(int units, int M, int N, int K, const float2* __restrict__ s, const float2* __restrict__ dtw,
            const float2* __restrict__ ftw, float2* __restrict__ Xc, const float2* __restrict__ w, double2* cm) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
@@ -344,6 +345,7 @@ template <class PL, int G, int MINB, int MODE>
 __global__ void __launch_bounds__(PL::T* G, MINB)
     k_af(const KP kp, const float2* __restrict__ Xc, const float2* __restrict__ Hh,
          const float2* __restrict__ dtw, const float2* __restrict__ ftw, float* __restrict__ af_mag, Part part) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   using GS = GroupSmem<PL, MODE>;
   extern __shared__ float4 smem_raw[];
@@ -527,6 +529,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
 template <class PL, int G>
 __global__ void __launch_bounds__(PL::T* G)
     k_rows_ifft(int rows, int N, const float2* __restrict__ in, const float2* __restrict__ ftw, float2* __restrict__ out) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
@@ -555,6 +558,7 @@ template <class PL, int G>
 __global__ void __launch_bounds__(PL::T* G)
     k_filter_fft(int RM, int N, const float2* __restrict__ w, const float2* __restrict__ ftw, float2* __restrict__ Hh,
                  const float2* __restrict__ s, double2* cm) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;

@@ -52,6 +52,7 @@ template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB)
     k_node(int units, int M, int Q, int N, int LS, const float2* __restrict__ Xc, const float2* __restrict__ H,
            const float2* __restrict__ ftw, float2* __restrict__ Rn, int R, LrRed* lred) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
@@ -157,6 +158,7 @@ __device__ __forceinline__ void lr_rescale(float from, float to, float lb, float
 // running maxima (LrRed) with atomicMax.
 template <int Q, int LM, bool HW, bool GRAD>
 __global__ void __launch_bounds__(256) k_lr(const LrArgs a) {
+  SQ_PDL_WAIT();
   constexpr int QH = Q / 2;
   constexpr int NR = GRAD ? 2 * Q + 4 : 4;  // per-lane reduction record (floats)
   extern __shared__ float4 lr_smem[];
@@ -458,6 +460,7 @@ constexpr int kLrtUnroll = SQNGD_LRT_UNROLL;  // tile-loop unroll of k_lrt (tuni
 #endif
 template <int Q, int LM, bool HW, bool GRAD>
 __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const LrtArgs a) {
+  SQ_PDL_WAIT();
   constexpr int QH = Q / 2;
   constexpr int NR = 6 + (GRAD ? 16 : 0);  // per-lane record: key(2), shift(2), S(2), GE/GO(16)
   extern __shared__ float4 lr_smem[];
@@ -847,6 +850,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
 __global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int mode, double bp, Part part,
                                                     const LrRed* __restrict__ lred, Red* red, MetricsArgs ma,
                                                     int* status) {
+  SQ_PDL_WAIT();
   __shared__ double shd[32];
   const int r = blockIdx.x;
   const float mf = __uint_as_float(lred[r].mbits);
@@ -899,6 +903,7 @@ struct AdjGArgs {
 //   Step A (WRT 1), unit ((r M + l) M + m) Q + q:  out = X~_{m,q} . conj(G^)  (sum over m, q: combine)
 template <class PL, int G, int MINB, int WRT>
 __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, const float2* __restrict__ ftw) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
@@ -999,6 +1004,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
 //                                          (groups split q; the combine sums the M slots of row l)
 template <class PL, int NG, int WRT>
 __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const float2* __restrict__ ftw) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;

@@ -14,6 +14,7 @@ namespace sq {
 // (Eq. 43 with the nearest-level snap of Q12; decision in fp64 like the oracle).
 __global__ void k_hard_lut(int B, int BR, double c, const float* __restrict__ rho, int* __restrict__ lut,
                            int* __restrict__ status) {
+  SQ_PDL_WAIT();
   const int r = blockIdx.y;
   const float* rr = rho + (size_t)r * BR;
   int* out = lut + (size_t)r * (BR + 1);
@@ -56,6 +57,7 @@ __global__ void k_hard_lut(int B, int BR, double c, const float* __restrict__ rh
 __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restrict__ z,
                            const float* __restrict__ rho, const int* __restrict__ lut, float2* s_soft,
                            float2* s_hard, uint8_t* b_hard, float* dq) {
+  SQ_PDL_WAIT();
   extern __shared__ float rs[];
   constexpr int LPE = 8;
   const int r = blockIdx.y;
@@ -148,6 +150,7 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
 // gradient combine.  One block of 1024 threads per restart, fixed order (deterministic).
 __global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp, Part part, Red* red,
                                 MetricsArgs ma, int* status) {
+  SQ_PDL_WAIT();
   __shared__ double shd[32];
   __shared__ unsigned long long shk[32];
   reduce_restart(blockIdx.x, GPR, g_lo, g_hi, mode, bp, part, red, ma, status, shd, shk);
@@ -155,6 +158,7 @@ __global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp
 
 // Multi-GPU: the shift m arrived from the all-reduce; refresh the per-group scales.
 __global__ void k_group_scales(int GPR, int g_lo, int g_hi, int mode, double bp, Part part, const Red* red) {
+  SQ_PDL_WAIT();
   const int r = blockIdx.x;
   const int lo = max(g_lo, r * GPR), hi = min(g_hi, (r + 1) * GPR);
   const double m = red[r].m;
@@ -179,6 +183,7 @@ __global__ void k_group_scales(int GPR, int g_lo, int g_hi, int mode, double bp,
 __global__ void k_sparse_adj(int M, int N, int K, int L, int wrt, double eps, const float* __restrict__ weights,
                              const float2* __restrict__ s, const float2* __restrict__ w,
                              const float2* __restrict__ dtw, const Red* __restrict__ red, float2* red_grad) {
+  SQ_PDL_WAIT();
   __shared__ double sre[256], sim[256];
   const int r = blockIdx.x;
   const unsigned long long ka = red[r].key_a, kc = red[r].key_c;
@@ -238,6 +243,7 @@ __global__ void k_sparse_adj(int M, int N, int K, int L, int wrt, double eps, co
 }
 
 __global__ void k_metrics(MetricsArgs a, int* status) {
+  SQ_PDL_WAIT();
   metrics_warp(a, blockIdx.x, status);
 }
 
@@ -331,6 +337,7 @@ __device__ __forceinline__ void finalize_elem(const FinArgs& f, size_t e, float2
 }
 
 __global__ void k_finalize_grad(FinArgs f, const float2* __restrict__ red_grad, int* status, MetricsArgs ma) {
+  SQ_PDL_WAIT();
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (threadIdx.x < 32 && blockIdx.x < (unsigned)f.R && (ma.out || ma.loss_hist)) metrics_warp(ma, blockIdx.x, status);
   if (e >= (size_t)f.R * f.M * f.N) return;
@@ -342,6 +349,7 @@ __global__ void k_finalize_grad(FinArgs f, const float2* __restrict__ red_grad, 
 template <class PL, int G>
 __global__ void __launch_bounds__(PL::T* G)
     k_rows_ifft_fin(int rows, const float2* __restrict__ in, const float2* __restrict__ ftw, FinArgs f, int* status) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
@@ -381,6 +389,7 @@ struct CombineArgs {
 // norm_r = eps/(2N) * extra * (LSE: 1/S_r, PNORM: S_r^{1/p-1}).
 // Block: 32 lanes x 2 complex (q) x 8 k-lanes.
 __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status) {
+  SQ_PDL_WAIT();
   __shared__ float4 sh[8][33];
   const int ra = blockIdx.y;
   const int r = ra / a.M;
@@ -446,6 +455,7 @@ template <class PL, int G>
 __global__ void __launch_bounds__(PL::T* G)
     k_rows_adam_w(int rows, const float2* __restrict__ in, const float2* __restrict__ ftw, FinArgs f, AdamP ap,
                   float2* w, float* mw, float* vw, float2* Hh, double2* cm, int* status) {
+  SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
   extern __shared__ float4 smem_raw[];
   const int grp = threadIdx.x / T, t = threadIdx.x % T;
@@ -585,6 +595,7 @@ template <bool SORT>
 __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
                                                        const float* __restrict__ rho, const float* __restrict__ dy,
                                                        float* part, RhoFinish fin) {
+  SQ_PDL_WAIT();
   __shared__ __align__(16) float2 zd[1024];  // chunk <= 1024: (z, dy), padded to a multiple of 4
   const int r = blockIdx.z;
   const int ch = blockIdx.y;
@@ -736,12 +747,14 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
 
 // ------------------------------------------------------------------ a9 optimizer
 __global__ void k_set_t(long long* dt, long long ta, long long tb) {
+  SQ_PDL_WAIT();
   dt[0] = ta;
   dt[1] = tb;
 }
 
 __global__ void k_adam(size_t n, float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
                        const float* __restrict__ g, AdamP ap, const int* __restrict__ status) {
+  SQ_PDL_WAIT();
   if (*status & ST_NONFINITE) return;  // keep the last finite iterate
   float c1, c2;
   ap.corr(c1, c2);
@@ -760,6 +773,7 @@ __global__ void k_adam(size_t n, float* __restrict__ x, float* __restrict__ m, f
 // One block per row; skipped entirely when a non-finite value is latched.
 __global__ void k_adam_project_w(int N, float* w, float* mw, float* vw, const float* __restrict__ g, AdamP ap,
                                  int* status) {
+  SQ_PDL_WAIT();
   __shared__ double sh[32];
   if (*status & ST_NONFINITE) return;
   float c1, c2;
@@ -902,6 +916,7 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
 // Step-B threshold update, one block per restart (when not fused into k_grad_rho_part).
 __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
                                    float lo, float hi, float gap, const int* status) {
+  SQ_PDL_WAIT();
   extern __shared__ float sr[];
   if (*status & ST_NONFINITE) return;  // keep the last finite iterate
   adam_project_rho_dev(blockIdx.x, BR, rho, mr, vr, g + (size_t)blockIdx.x * BR, ap, lo, hi, gap, sr);

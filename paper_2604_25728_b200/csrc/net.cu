@@ -226,6 +226,7 @@ __device__ __forceinline__ void net_in_block(const NetArgs& a, int bx, int by, i
 // Forward: grid (ceil(Din / 64), R), 256 threads; warp w owns rows 8w..8w+7 of the CTA's 64 (all eight
 // rows' loads issued before the reductions); lanes < W/4 own 4 columns.
 __global__ void __launch_bounds__(256) k_net_out(NetArgs a) {
+  SQ_PDL_WAIT();
   const int r = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int W4 = a.W >> 2;
   const float* __restrict__ hD = a.tape + ((size_t)r * (2 * a.D + 1) + a.D) * a.W;
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(256) k_net_out(NetArgs a) {
 // (fixed order), one partial per cluster.
 template <int MODE>
 __global__ void __cluster_dims__(NET_CL, 1, 1) __launch_bounds__(256) k_net_out_bwd(NetArgs a) {
+  SQ_PDL_WAIT();
   __shared__ float4 red[8][32];
   __shared__ float4 cpart[32];
   const int r = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -411,6 +413,7 @@ __device__ __forceinline__ void net_hid_block(const NetArgs& a, int bx, int r, c
 // blocks; grid (n_in ceil(W/8) + n_hid, R), 256 threads.  NM_FWD: the W_in y0 partials only.
 template <int MODE, bool VEC>
 __global__ void __launch_bounds__(256) k_net_upd(NetArgs a) {
+  SQ_PDL_WAIT();
   const int r = blockIdx.y;
   bool upd = true;
   AdamC ad{};
@@ -491,6 +494,7 @@ __device__ __forceinline__ void rows_dot4(const float* wsl, int s, int RW, int W
 // tape tv = [h_0..h_D | u_0..u_{D-1}] in shared memory and writes its column slice to global at the
 // end.  Exchange phase k (0: h_0, 1 + 2d: u_d, 2 + 2d: h_{d+1}) completes on xbar[k].
 __global__ void __cluster_dims__(NET_CL, 1, 1) __launch_bounds__(128) k_net_mid_fwd(NetArgs a) {
+  SQ_PDL_WAIT();
   extern __shared__ __align__(16) float sm[];
   __shared__ __align__(8) uint64_t bar, xbar[2 * NET_MAXD + 1];
   __shared__ float sred[128];
@@ -562,6 +566,7 @@ __global__ void __cluster_dims__(NET_CL, 1, 1) __launch_bounds__(128) k_net_mid_
 // W2_d^T gh and of W1_d^T ga (NET_CL x W floats each) into xb[0] / xb[1]; a buffer is refilled only
 // after every CTA has consumed it (the refill needs data each CTA sends after its reads).
 __global__ void __cluster_dims__(NET_CL, 1, 1) __launch_bounds__(128) k_net_mid_bwd(NetArgs a) {
+  SQ_PDL_WAIT();
   extern __shared__ __align__(16) float sm[];
   __shared__ __align__(8) uint64_t bar, xbar[2 * NET_MAXD + 1];
   cg::cluster_group cl = cg::this_cluster();
@@ -674,6 +679,7 @@ __device__ __forceinline__ void rows_dot8(const float* Wm, int W, const float* x
 }
 
 __global__ void __launch_bounds__(NET_ST) k_net_mid_fwd1(NetArgs a) {
+  SQ_PDL_WAIT();
   extern __shared__ __align__(16) float sm[];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ float sred[NET_ST];
@@ -745,6 +751,7 @@ __device__ __forceinline__ float cols_dot(const float* Wm, int W, const float* g
 }
 
 __global__ void __launch_bounds__(NET_ST) k_net_mid_bwd1(NetArgs a) {
+  SQ_PDL_WAIT();
   extern __shared__ __align__(16) float sm[];
   __shared__ __align__(8) uint64_t bar[3];
   __shared__ float sred[NET_ST];
