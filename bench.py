@@ -432,6 +432,29 @@ def main():
         "wall_s": main_run["wall_s"],
         "final_hard_pslr_db": 20 * math.log10(max(hm[0]["wpsl"], 1e-30)),
     }
+    # per-block and per-loss-mode breakdown (Step A vs Step B, MAX vs LSE), graph replay
+    def block_rate(cx, stx, block, n_evals, reps=10):
+        for _ in range(3):
+            cx.step(stx, block)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            cx.step(stx, block)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return n_evals * reps / (parallel.max_over_ranks(a.elapsed_time(b)) / 1e3)
+
+    breakdown = {"step_A_evals_per_s": block_rate(ctx, st, sqngd.BLOCK_A, c.n_h * c.R * world),
+                 "step_B_evals_per_s": block_rate(ctx, st, sqngd.BLOCK_B, c.n_x * c.R * world)}
+    if c.loss_mode != CF.LOSS_MAX:
+        cm = c.with_(loss_mode=CF.LOSS_MAX, beta_or_p=0.0)
+        ctxm = sqngd.Context(cm, device=local)
+        stm = ctxm.new_state(st["z"], st["rho"], st["w"])
+        breakdown["max_mode_evals_per_s"] = block_rate(ctxm, stm, sqngd.BLOCK_AB, (c.n_h + c.n_x) * c.R * world)
+        ctxm.close()
+    line["breakdown"] = {**breakdown, "unit": UNIT,
+                         "what": "Step A only (filters), Step B only (transmit), and the MAX loss (Eq. 37, O(N) "
+                                 "subgradient adjoint) instead of LSE; each 10 graph-replayed steps"}
     if args.batch_restarts > 1 and c.R == 1:  # the same config with B independent restarts per GPU
         ctxb, *_rest, b_run = timed(c.with_(R=args.batch_restarts), False)
         ctxb.close()
