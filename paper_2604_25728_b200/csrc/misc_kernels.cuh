@@ -865,8 +865,45 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
         }
         __syncthreads();
       }
-    } while (swapped && ++rounds < 64);
-    if (swapped) {
+    } while (swapped && ++rounds < 2);  // clusters of near-equal thresholds need many rounds: bitonic then
+    if (swapped && n2 == 2 * (int)blockDim.x && n2 >= 128) {
+      // bitonic sort with two elements per thread (2t, 2t+1) in registers: partner distances j <= 32
+      // stay inside the warp (xor shuffles, no barrier), larger ones go through shared memory
+      const int t = threadIdx.x;
+      float x0 = sr[2 * t], x1 = sr[2 * t + 1];
+      for (int kk = 2; kk <= n2; kk <<= 1) {
+        const bool up = ((2 * t) & kk) == 0;  // direction of this thread's pairs (both slots)
+        int j = kk >> 1;
+        if (j >= 64) {
+          sr[2 * t] = x0;
+          sr[2 * t + 1] = x1;
+          __syncthreads();
+          for (; j >= 64; j >>= 1) {
+            const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // pair t: i has bit j clear
+            const bool upi = (i & kk) == 0;
+            const float a = sr[i], b = sr[i | j];
+            if ((a > b) == upi) { sr[i] = b; sr[i | j] = a; }
+            __syncthreads();
+          }
+          x0 = sr[2 * t];
+          x1 = sr[2 * t + 1];
+        }
+        for (; j >= 2; j >>= 1) {  // partner of element 2t + b is 2 (t ^ j/2) + b: lane t ^ j/2
+          const int h = j >> 1;
+          const float y0 = __shfl_xor_sync(0xffffffffu, x0, h), y1 = __shfl_xor_sync(0xffffffffu, x1, h);
+          const bool keep_min = ((t & h) == 0) == up;  // lower index of an ascending pair keeps the min
+          x0 = keep_min ? fminf(x0, y0) : fmaxf(x0, y0);
+          x1 = keep_min ? fminf(x1, y1) : fmaxf(x1, y1);
+        }
+        if ((x0 > x1) == up) {  // j = 1: the thread's own pair
+          const float tmp = x0;
+          x0 = x1;
+          x1 = tmp;
+        }
+      }
+      sr[2 * t] = x0;
+      sr[2 * t + 1] = x1;
+    } else if (swapped) {
       for (int kk = 2; kk <= n2; kk <<= 1)
         for (int j = kk >> 1; j > 0; j >>= 1) {
           for (int i = threadIdx.x; i < n2; i += blockDim.x) {

@@ -78,6 +78,11 @@ struct sqngd_ctx_s {
   float* rho_part = nullptr;   // [R][nchunk][BR]
   int rho_chunk = 256, rho_nchunk = 1;
   bool rho_sort = true;        // k_grad_rho_part sorts its chunk (needs rho_chunk <= 256)
+  // Adam(rho) + projection: a 1024-thread kernel (default) or the last 256-thread grad-rho block.  As
+  // the optimization proceeds the thresholds form clusters that Adam reorders every step, so the
+  // projection's sort runs every step: measured at C3, the fused tail is 5 us/step faster in the
+  // first steps but 40 us/step slower after ~40 outer iterations (SQNGD_FUSE_RHO=1: fused).
+  bool fuse_rho = false;
   int* rho_cnt = nullptr;      // [R][64] threshold-block + [R][nchunk] element-chunk arrival counters
   float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
   float* gz = nullptr;         // [R][M][N]
@@ -741,6 +746,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     if (ch >= 32 && ch <= 1024 && ch % 4 == 0) ctx->rho_chunk = ch;
   }
   if (const char* ev = getenv("SQNGD_RHO_SORT")) ctx->rho_sort = ev[0] != '0';
+  if (const char* ev = getenv("SQNGD_FUSE_RHO")) ctx->fuse_rho = ev[0] == '1';
   if (ctx->rho_chunk > 256) ctx->rho_sort = false;
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
@@ -1486,7 +1492,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
           fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
         }
         fin.status = ctx->status;
-        const bool fuse_rho = ctx->BR <= 4096;  // 2 n2 floats within the default 48 KB
+        const bool fuse_rho = ctx->BR <= 4096 && ctx->fuse_rho;  // 2 n2 floats within the default 48 KB
         if (fuse_rho) {
           fin.cnt_r = ctx->rho_cnt + (size_t)c.R * (64 + ctx->rho_nchunk);
           fin.rho = stt->rho; fin.mr = stt->m_rho; fin.vr = stt->v_rho; fin.apr = ap(c.lr_z, 1, i);

@@ -312,3 +312,40 @@ def test_correlation_mode_K1(mode):
     _, gw_ref, gs_ref = O.loss_grad(c, s, w)
     assert rel(gw.cpu().numpy(), gw_ref) < 1e-4
     assert rel(gs.cpu().numpy(), gs_ref) < 1e-4
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_threshold_projection_with_clusters(fuse, monkeypatch):
+    """Thresholds in clusters of 64 spaced 1e-6 apart (the state long runs reach) with a large rate:
+    Adam reorders the clusters, so the projection (Q22: sort, clamp, min-gap sweep) does real work.
+    The GPU step (1024-thread projection kernel with the register/shuffle bitonic sort, or the fused
+    256-thread tail) matches the oracle's Adam + projection on the same gradient.  Tolerance 2e-5:
+    the fp32 min-gap sweep accumulates 1e-6 steps along a 64-long cluster."""
+    monkeypatch.setenv("SQNGD_FUSE_RHO", fuse)
+    c = Cfg("clus", M=2, N=64, B=16, K=9, f_lo=-0.5, f_hi=0.5, r_n=100, n_h=1, n_x=1, lr_z=1e-2,
+            doppler_engine=sqngd.ENGINE_FFT)
+    z = inputs.phase_params(1, c.M, c.N, config_index=17)
+    base = inputs.init_thresholds(1, c.B, c.r_n).astype(np.float64)[0]
+    rho = base.copy()
+    for g0 in range(0, c.BR, 64):  # squeeze each group of 64 around its mean
+        grp = slice(g0, min(g0 + 64, c.BR))
+        n = grp.stop - grp.start
+        rho[grp] = base[grp].mean() + (np.arange(n) - n / 2) * 1e-6
+    rho = rho.astype(np.float32)[None]
+    assert (np.diff(rho[0]) > 0).all()
+    w = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
+    ctx = sqngd.Context(c)
+    st = ctx.new_state(T(z), T(rho), T(w))
+    _, gz, gr = ctx.af_loss_grad(st["z"], st["rho"], st["w"], sqngd.WRT_TRANSMIT)
+    ctx.sync()
+    gz, gr = gz.cpu().numpy().astype(np.float64), gr.cpu().numpy().astype(np.float64)
+    ctx.step(st, sqngd.BLOCK_B)
+    ctx.sync()
+    ost = O.new_state(z, rho, w)
+    O.step(c, ost, block=2, grads_from=lambda kind, i, s_: (gz, gr))
+    r_gpu = st["rho"].cpu().numpy()
+    assert (np.diff(r_gpu[0]) >= 0).all()
+    np.testing.assert_allclose(r_gpu, ost["rho"], rtol=0, atol=2e-5)
+    # the oracle's update did reorder thresholds (the sort was exercised)
+    raw = rho.astype(np.float64) - 1e-2 * np.sign(gr)
+    assert (np.diff(raw[0]) < 0).any()
