@@ -17,7 +17,15 @@ struct AdamP {
   float lr, b1, b2, eps;
   const long long* dt;
   int which, off;
+  const float2* ct = nullptr;  // optional [2][cts] table of (c1, c2) per block and inner step (k_set_t)
+  int cts = 0;
   __device__ __forceinline__ void corr(float& c1, float& c2) const {
+    if (ct) {  // precomputed once per sqngd_step: one load instead of two fp64 pow chains
+      const float2 v = ct[which * cts + off];
+      c1 = v.x;
+      c2 = v.y;
+      return;
+    }
     const double t = (double)(dt[which] + off + 1);
     c1 = (float)(1.0 - pow((double)b1, t));
     c2 = (float)(1.0 - pow((double)b2, t));

@@ -746,10 +746,26 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
 }
 
 // ------------------------------------------------------------------ a9 optimizer
-__global__ void k_set_t(long long* dt, long long ta, long long tb) {
+// Adam step counters and the bias corrections (c1, c2) = (1 - b1^t, 1 - b2^t) of every inner step of
+// the coming sqngd_step (t = t_a + k + 1 for Step A, t_b + k + 1 for Step B), computed in fp64 exactly
+// as AdamP::corr does, so the update kernels read one table entry instead of two pow chains.
+__global__ void k_set_t(long long* dt, long long ta, long long tb, float2* ct, int cts, int nh, int nx, double b1,
+                        double b2) {
   SQ_PDL_WAIT();
-  dt[0] = ta;
-  dt[1] = tb;
+  if (threadIdx.x == 0) {
+    dt[0] = ta;
+    dt[1] = tb;
+  }
+  for (int k = threadIdx.x; k < cts; k += blockDim.x) {
+    if (k < nh) {
+      const double t = (double)(ta + k + 1);
+      ct[k] = make_float2((float)(1.0 - pow(b1, t)), (float)(1.0 - pow(b2, t)));
+    }
+    if (k < nx) {
+      const double t = (double)(tb + k + 1);
+      ct[cts + k] = make_float2((float)(1.0 - pow(b1, t)), (float)(1.0 - pow(b2, t)));
+    }
+  }
 }
 
 __global__ void k_adam(size_t n, float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,

@@ -114,6 +114,8 @@ struct sqngd_ctx_s {
   int* lr_cnt = nullptr;       // [R M Q] k_adj_g arrival counters
   Comm comm;
   long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
+  float2* d_ct = nullptr;      // [2][cts] bias corrections of the step's inner iterations (k_set_t)
+  int cts = 0;
   // generator z = f_theta(y0) (net.cu, NEXT-2)
   bool net = false;
   NetDims nd{};
@@ -726,6 +728,8 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   CK(cudaMalloc(&ctx->part.scale, sizeof(float) * uslots));
   CK(cudaMalloc(&ctx->counter, 2 * sizeof(int)));
   CK(cudaMalloc(&ctx->d_t, 2 * sizeof(long long)));
+  ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
+  CK(cudaMalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
   if (const char* e = getenv("SQNGD_PDL")) ctx->pdl = e[0] == '1';
   CK(cudaMalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
@@ -940,7 +944,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
     }
     delete g;
   }
-  void* ptrs[] = {ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+  void* ptrs[] = {ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
                   ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
@@ -1435,7 +1439,8 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
   float2* w2 = reinterpret_cast<float2*>(stt->w);
   sqngd_status rc;
   auto ap = [&](double lr, int which, int off) {
-    return AdamP{(float)lr, (float)c.adam_b1, (float)c.adam_b2, (float)c.adam_eps, ctx->d_t, which, off};
+    return AdamP{(float)lr, (float)c.adam_b1, (float)c.adam_b2, (float)c.adam_eps, ctx->d_t, which, off, ctx->d_ct,
+                 ctx->cts};
   };
   if (ctx->net) {  // waveform generation z = f_theta(y0) (Alg. 1)
     CK(net_forward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, true, st, &ctx->launches));
@@ -1545,7 +1550,7 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
   const sqngd_config& c = ctx->cfg;
   const cudaStream_t st = S(stream);
   sqngd_status rc;
-  k_set_t<<<1, 1, 0, st>>>(ctx->d_t, stt->t_a, stt->t_b);
+  k_set_t<<<1, 64, 0, st>>>(ctx->d_t, stt->t_a, stt->t_b, ctx->d_ct, ctx->cts, c.n_h, c.n_x, c.adam_b1, c.adam_b2);
   ctx->launches += 1;
   // Graph path: single GPU, a capturable (non-legacy) stream.
   const bool graph_ok = ctx->use_graphs && !ctx->prof && ctx->world == 1 && st != nullptr &&
