@@ -934,27 +934,39 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
   const float mf = __uint_as_float(a.lred[r].mbits);
   const float lb = a.bp * 1.4426950408889634f;
   float2 v[E];
+  float mu[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) {  // branch-free so that all loads issue back to back
+  for (int i = 0; i < E; ++i) {  // all loads first (the rescale below would otherwise wait on each)
     const int j = t + i * T;
     const bool in = j < N || j > P - N;
     const int idx = in ? lag_of(j, N, P) + N - 1 : 0;
-    const float mu = __ldg(ump + (idx >> a.csh));
-    const float2 x = __ldg(Gp + idx);
+    mu[i] = __ldg(ump + (idx >> a.csh));
+    v[i] = __ldg(Gp + idx);
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int j = t + i * T;
+    const bool in = j < N || j > P - N;
     float fS, fG;
-    if (a.mode == 1) lr_rescale<1>(mu, mf, lb, a.bp, fS, fG);
-    else lr_rescale<2>(mu, mf, lb, a.bp, fS, fG);
-    fG = (in && mu > 0.f && mf > 0.f) ? fG : 0.f;
-    v[i] = make_float2(x.x * fG, x.y * fG);
+    if (a.mode == 1) lr_rescale<1>(mu[i], mf, lb, a.bp, fS, fG);
+    else lr_rescale<2>(mu[i], mf, lb, a.bp, fS, fG);
+    fG = (in && mu[i] > 0.f && mf > 0.f) ? fG : 0.f;
+    v[i] = make_float2(v[i].x * fG, v[i].y * fG);
+  }
+  float2 hx[E];  // the spectrum the transform is multiplied with, fetched while the FFT runs (the
+                 // output stores below would otherwise serialize one load round trip per element)
+  {
+    const float2* HX = WRT == 2 ? a.H + ((size_t)r * M + l) * P : a.Xc + (((size_t)r * M + m) * Q + q) * P;
+#pragma unroll
+    for (int i = 0; i < E; ++i) hx[i] = __ldg(HX + t + i * T);
   }
   int par = 0;
   fft<PL, -1>(v, ftw, xbuf, t, par, sync);
   if (u >= a.units) return;
   float2* out = a.out + (size_t)uu * P;
   if (WRT == 2) {
-    const float2* Hl = a.H + ((size_t)r * M + l) * P;
 #pragma unroll
-    for (int i = 0; i < E; ++i) out[t + i * T] = cmul(v[i], __ldg(Hl + t + i * T));
+    for (int i = 0; i < E; ++i) out[t + i * T] = cmul(v[i], hx[i]);
     // arrival: the last group of node (r, m, q) does the tail
     int* flag = reinterpret_cast<int*>(xbuf + FftSmem<PL>::XBUF);
     const int node = uu / M;
@@ -989,9 +1001,8 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
       }
     }
   } else {
-    const float2* X = a.Xc + (((size_t)r * M + m) * Q + q) * P;
 #pragma unroll
-    for (int i = 0; i < E; ++i) out[t + i * T] = cmulc(__ldg(X + t + i * T), v[i]);
+    for (int i = 0; i < E; ++i) out[t + i * T] = cmulc(hx[i], v[i]);
   }
 }
 
@@ -1028,28 +1039,36 @@ __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const fl
     const float2* Gp = a.Gn + ((size_t)pr * Q + q) * a.LS;
     const float* ump = a.um + (size_t)pr * a.nch;
     float2 v[E];
+    float mu[E];
 #pragma unroll
-    for (int i = 0; i < E; ++i) {  // branch-free so that all loads issue back to back
+    for (int i = 0; i < E; ++i) {  // all loads first (the rescale below would otherwise wait on each)
       const int j = t + i * T;
       const bool in = j < N || j > P - N;
       const int idx = in ? lag_of(j, N, P) + N - 1 : 0;
-      const float mu = __ldg(ump + (idx >> a.csh));
-      const float2 x = __ldg(Gp + idx);
-      float fS, fG;
-      if (a.mode == 1) lr_rescale<1>(mu, mf, lb, a.bp, fS, fG);
-      else lr_rescale<2>(mu, mf, lb, a.bp, fS, fG);
-      fG = (in && mu > 0.f && mf > 0.f) ? fG : 0.f;
-      v[i] = make_float2(x.x * fG, x.y * fG);
+      mu[i] = __ldg(ump + (idx >> a.csh));
+      v[i] = __ldg(Gp + idx);
     }
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int j = t + i * T;
+      const bool in = j < N || j > P - N;
+      float fS, fG;
+      if (a.mode == 1) lr_rescale<1>(mu[i], mf, lb, a.bp, fS, fG);
+      else lr_rescale<2>(mu[i], mf, lb, a.bp, fS, fG);
+      fG = (in && mu[i] > 0.f && mf > 0.f) ? fG : 0.f;
+      v[i] = make_float2(v[i].x * fG, v[i].y * fG);
+    }
+    float2 hx[E];  // the spectrum the transform is multiplied with, fetched while the FFT runs
+    const float2* HX = WRT == 2 ? a.H + ((size_t)r * M + l) * P : a.Xc + (((size_t)r * M + m) * Q + q) * P;
+#pragma unroll
+    for (int i = 0; i < E; ++i) hx[i] = __ldg(HX + t + i * T);
     fft<PL, -1>(v, ftw, xbuf, t, par, sync);
     if (WRT == 2) {
-      const float2* Hl = a.H + ((size_t)r * M + l) * P;
 #pragma unroll
-      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], __ldg(Hl + t + i * T)));
+      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], hx[i]));
     } else {
-      const float2* X = a.Xc + (((size_t)r * M + m) * Q + q) * P;
 #pragma unroll
-      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(__ldg(X + t + i * T), v[i]));
+      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(hx[i], v[i]));
     }
   }
   // fixed-order sum of the groups' accumulators (the exchange buffers are free now)
