@@ -15,8 +15,25 @@ namespace sq {
 __global__ void k_hard_lut(int B, int BR, double c, const float* __restrict__ rho, int* __restrict__ lut,
                            int* __restrict__ status) {
   SQ_PDL_WAIT();
+  extern __shared__ float rr[];  // the restart's thresholds (the searches below are dependent chains)
   const int r = blockIdx.y;
-  const float* rr = rho + (size_t)r * BR;
+  {
+    const float* rg = rho + (size_t)r * BR;
+    for (int base = 0; base < BR; base += 8 * (int)blockDim.x) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = base + k * blockDim.x + threadIdx.x;
+        v[k] = i < BR ? __ldg(rg + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = base + k * blockDim.x + threadIdx.x;
+        if (i < BR) rr[i] = v[k];
+      }
+    }
+    __syncthreads();
+  }
   int* out = lut + (size_t)r * (BR + 1);
   const double W = 20.0 / c;
   const int lane = threadIdx.x & 31;
@@ -395,6 +412,8 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   const int r = ra / a.M;
   const double m = a.red[r].m, S = a.red[r].S;
   const bool live = m > -INFINITY && S > 0.0;
+  double norm = 0.0;  // (fp64 divide / pow issued now, off the critical path of the slot sums)
+  if (live) norm = a.eps / (2.0 * a.N) * a.extra * ((a.mode == 1) ? 1.0 / S : pow(S, 1.0 / a.bp - 1.0));
   const int q = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));  // two complex values per thread
   const int kl = threadIdx.x >> 5;                              // 8 k-lanes
   FinIn fin0{}, fin1{};
@@ -428,11 +447,6 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
       t.y += sh[j][threadIdx.x].y;
       t.z += sh[j][threadIdx.x].z;
       t.w += sh[j][threadIdx.x].w;
-    }
-    double norm = 0.0;
-    if (live) {
-      norm = a.eps / (2.0 * a.N) * a.extra;
-      norm *= (a.mode == 1) ? 1.0 / S : pow(S, 1.0 / a.bp - 1.0);
     }
     const float nf = (float)norm;
     const float2 g0 = make_float2(t.x * nf, t.y * nf), g1 = make_float2(t.z * nf, t.w * nf);

@@ -1036,7 +1036,8 @@ static sqngd_status run_quantize(sqngd_ctx ctx, const float* z, const float* rho
                                  uint8_t* b_hard, float* dq, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   if (s_hard || b_hard) {
-    k_hard_lut<<<dim3((ctx->BR + 1 + 7) / 8, c.R), 256, 0, st>>>(c.B, ctx->BR, c.c, rho, ctx->lut, ctx->status);
+    k_hard_lut<<<dim3((ctx->BR + 1 + 7) / 8, c.R), 256, ctx->BR * sizeof(float), st>>>(c.B, ctx->BR, c.c, rho, ctx->lut,
+                                                                                        ctx->status);
     ctx->launches += 1;
   }
   ctx->launches += 1;
