@@ -960,6 +960,42 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
     // forward sweep rho_i = max(rho_i, rho_{i-1} + gap) == max_{j<=i}(rho_j + (i-j) gap):
     // inclusive prefix max of q_j = rho_j - j gap (Hillis-Steele), value kept exact where inactive.
     float* q = sr + n2;
+    if (n2 == 2 * (int)blockDim.x && blockDim.x % 32 == 0 && blockDim.x <= 1024) {
+      // two elements per thread; warp scans with shuffles, one shared-memory pass over the warp
+      // totals (max is exact, so this equals the Hillis-Steele result bit for bit)
+      __shared__ float wtot[32];
+      const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+      const int i0 = 2 * t, i1 = 2 * t + 1;
+      const float a0 = i0 < BR ? sr[i0] - (float)i0 * gap : -INFINITY;
+      const float a1 = i1 < BR ? sr[i1] - (float)i1 * gap : -INFINITY;
+      float inc = fmaxf(a0, a1);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = fmaxf(inc, v);
+      }
+      float exc = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) exc = -INFINITY;
+      if (lane == 31) wtot[wp] = inc;
+      __syncthreads();
+      if (wp == 0) {
+        const int nw = blockDim.x >> 5;
+        float x = lane < nw ? wtot[lane] : -INFINITY;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float v = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x = fmaxf(x, v);
+        }
+        const float xe = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane < nw) wtot[lane] = lane == 0 ? -INFINITY : xe;  // exclusive warp offsets
+      }
+      __syncthreads();
+      const float base = fmaxf(wtot[wp], exc);
+      const float p0 = fmaxf(base, a0), p1 = fmaxf(p0, a1);
+      if (i0 < BR) q[i0] = p0;
+      if (i1 < BR) q[i1] = p1;
+      __syncthreads();
+    } else {
     for (int i = threadIdx.x; i < BR; i += blockDim.x) q[i] = sr[i] - (float)i * gap;
     __syncthreads();
     for (int off = 1; off < BR; off <<= 1) {
@@ -970,6 +1006,7 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
       cnt = 0;
       for (int i = threadIdx.x; i < BR; i += blockDim.x) q[i] = tmp[cnt++];
       __syncthreads();
+    }
     }
     for (int i = threadIdx.x; i < BR; i += blockDim.x) {
       const float qi = sr[i] - (float)i * gap;
