@@ -111,6 +111,12 @@ typedef struct {
   int32_t argmax_cross[4]; /* (m, l, tau, k) of WCPSL ((-1,...) when M == 1)            */
   uint32_t flags;          /* SQNGD_FLAG_*                                              */
   uint32_t n_cells;        /* |S|: sidelobe cells in the ROI                            */
+  double apslr_db;         /* Eq. 48: 20 log10(WAPSL) (-inf when 0)        */
+  double cpslr_db;         /* Eq. 48 of WCPSL (-inf when M == 1)                        */
+  double pslr_db;          /* Eq. 48 of WPSL                                            */
+  double snrl_db_max;      /* max_m SNRL_m, Eq. 10, from the literal norms;
+                              written by sqngd_af_forward and sqngd_step's hard_out,
+                              NaN in the loss+gradient calls                            */
 } sqngd_metrics;
 
 /* Optimizer state: caller-owned DEVICE buffers, mutated in place by sqngd_step.
@@ -151,9 +157,11 @@ sqngd_status sqngd_quantize(sqngd_ctx ctx, const float* z, const float* rho, flo
 /* a2-a6: all M^2 AF/CAF maps over (2N-1) lags x K Doppler bins by Doppler-modulated,
    zero-padded FFT correlation (Eqs. 33-36), fused with the ROI reduction (Eqs. 7-9,
    37-42).  s, w: complex [R][M][N].  af_mag: NULL or [R][M][M][K][2N-1] |A| (fp32).
-   metrics: [R] sqngd_metrics.  p_out: NULL or [R][M] doubles p_m (Eq. 38). */
+   metrics: [R] sqngd_metrics.  p_out: NULL or [R][M] doubles p_m (Eq. 38).
+   snrl_db_out: NULL or [R][M] doubles SNRL_m = 10 log10(||s_m||^2 ||w_m||^2 / |s_m^H w_m|^2)
+   (Eq. 10; +inf when s_m^H w_m = 0, which also latches SQNGD_E_DEGENERATE). */
 sqngd_status sqngd_af_forward(sqngd_ctx ctx, const float* s, const float* w, float* af_mag,
-                              sqngd_metrics* metrics, double* p_out, sqngd_stream stream);
+                              sqngd_metrics* metrics, double* p_out, double* snrl_db_out, sqngd_stream stream);
 
 /* a7-a8 for an explicit waveform s: loss and gradient by adjoint correlations.
    wrt = SQNGD_WRT_FILTERS: grad_w = dL/dRe w + j dL/dIm w = 2 dL/dw^* (Q16) [R][M][N] complex.
@@ -205,19 +213,25 @@ sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* 
    Eq. 7).  Per restart r the state with the lowest hard WPSL so far is copied into `best`
    (DEVICE buffers z, rho, w, and theta in generator mode; the other members are ignored): the
    output (X_hard, H) of Alg. 1 is quantize(best.z, best.rho) and best.w.  Stopping criterion
-   ("further reduction of L does not lead to improvement in the WPSL"): stop after
-   the outer iteration at which EVERY restart has gone opts->patience consecutive iterations
-   without a strict improvement of its hard WPSL (patience <= 0: run all T).
-   best_wpsl [R] doubles, best_iter [R] int32 (1-based outer iteration of the snapshot) and
-   wpsl_hist (NULL or [T][R] doubles, hard WPSL per iteration until the stop) are DEVICE pointers.
-   The bookkeeping runs on the device; the host polls the stop flag every opts->check_every
-   iterations, so the live `state` may run up to check_every - 1 iterations past the stop (the
-   snapshot, best_* and result->iterations follow the rule exactly; check_every = 1 is exact).
-   Returns after synchronizing `stream` (the latched device status, as sqngd_sync). */
+   ("further reduction of L does not lead to improvement in the WPSL"; DESIGN.md §3
+   "Stopping rule"): an outer iteration improves restart r when its hard WPSL is below the best so far
+   by more than opts->tol (1e-6); training stops after the outer iteration at which EVERY
+   restart has gone opts->patience consecutive iterations without an improvement and, when
+   opts->require_loss_decrease, has a hard loss L below the L of its last improvement (L kept
+   decreasing over the window).  patience <= 0: run all T.
+   best_wpsl [R] doubles, best_iter [R] int32 (1-based outer iteration of the snapshot), wpsl_hist and
+   loss_hist (NULL or [T][R] doubles: hard WPSL / hard loss per iteration until the stop) are DEVICE
+   pointers.  The bookkeeping runs on the device (its buffers are kept in the context); the host polls
+   the stop flag every opts->check_every iterations, so the live `state` may run up to check_every - 1
+   iterations past the stop (the snapshot, best_* and result->iterations follow the rule exactly;
+   check_every = 1 is exact).  Returns after synchronizing `stream` (the latched device status, as
+   sqngd_sync). */
 typedef struct {
   int32_t T;           /* maximum outer iterations (the paper's T = 2000)          */
   int32_t patience;    /* outer iterations without hard-WPSL improvement before stopping   */
   int32_t check_every; /* >= 1: host polls the device stop flag every check_every steps    */
+  int32_t require_loss_decrease; /* 1: also require L below its value at the last improvement */
+  double tol;          /* >= 0: minimum decrease of the hard WPSL (linear, / N) that counts */
 } sqngd_run_opts;
 typedef struct {
   int64_t iterations;  /* outer iterations until the rule stopped training (T if it did not) */
@@ -226,8 +240,8 @@ typedef struct {
   int32_t reserved;
 } sqngd_run_result;
 sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd_run_opts* opts, sqngd_state* best,
-                       double* best_wpsl, int32_t* best_iter, double* wpsl_hist, sqngd_run_result* result,
-                       sqngd_stream stream);
+                       double* best_wpsl, int32_t* best_iter, double* wpsl_hist, double* loss_hist,
+                       sqngd_run_result* result, sqngd_stream stream);
 
 /* sqngd_step captures itself into a CUDA graph on the first call with a given (state
    buffers, block, outputs) on a non-legacy stream and replays the graph afterwards

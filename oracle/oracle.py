@@ -181,6 +181,16 @@ def af(cfg, s, w, want_A: bool = False, weights=None):
     return [m.as_dict() for m in met], p, A
 
 
+def snrl_db(x, h) -> float:
+    """Eq. 10: SNRL = 10 log10(||x||^2 ||h||^2 / |x^H h|^2), the literal definition in fp64
+    (+inf when x^H h = 0)."""
+    x, h = _c128(x).ravel(), _c128(h).ravel()
+    c = abs(np.vdot(x, h)) ** 2            # |x^H h|^2
+    if c == 0.0:
+        return float("inf")
+    return float(10.0 * np.log10(np.vdot(x, x).real * np.vdot(h, h).real / c))
+
+
 # ---------------------------------------------------------------- O4
 def loss_grad(cfg, s, w, want_w: bool = True, want_s: bool = True, weights=None):
     """Returns (metrics list, grad_w = 2 dL/dw^*, grad_s = dL/ds^*)."""

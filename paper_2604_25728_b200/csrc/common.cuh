@@ -54,6 +54,8 @@ struct MetricsOut {       // mirrors sqngd_metrics (include/sqngd.h)
   double loss, loss_wpsl, loss_snrl, wapsl, wcpsl, wpsl;
   int32_t argmax_auto[4], argmax_cross[4];
   uint32_t flags, n_cells;
+  double apslr_db, cpslr_db, pslr_db;  // Eq. 48 of WAPSL, WCPSL, WPSL
+  double snrl_db_max;                  // max_m Eq. 10 (k_snrl; NaN where not computed)
 };
 
 struct MetricsArgs {
@@ -100,6 +102,11 @@ __device__ void metrics_warp(const MetricsArgs& a, int r, int* status) {
   o.loss = a.eps * o.loss_wpsl + (1.0 - a.eps) * o.loss_snrl;
   o.flags = a.flags;
   o.n_cells = a.n_cells;
+  // Eq. 48: PSLR = 20 log10(PSL / N); the maxima above are already normalised by N (Q5)
+  o.apslr_db = 20.0 * log10(o.wapsl);
+  o.cpslr_db = 20.0 * log10(o.wcpsl);
+  o.pslr_db = 20.0 * log10(o.wpsl);
+  o.snrl_db_max = __longlong_as_double(0x7ff8000000000000ll);
   if (!isfinite(o.loss)) atomicOr(status, ST_NONFINITE);
   if (a.out) a.out[r] = o;
   if (a.loss_hist) a.loss_hist[(size_t)r * a.hist_stride + a.hist_col] = o.loss;

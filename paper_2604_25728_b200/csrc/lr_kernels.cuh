@@ -98,7 +98,7 @@ struct LrArgs {
 // LM: 0 MAX (keys only), 1 LSE, 2 PNORM.  Returns G~ (unnormalised: gphi w At / |At|).
 template <int LM, bool HW, bool GRAD, bool GE_RULE, bool GF_ONLY = false>
 __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int idx, bool valid, float lbN, float nlbs,
-                                          float qN, float& best, int& bk, float& S, float* mrow) {
+                                          float qN, float& best, int& bk, float& S, float* mrow, float msc = 1.f) {
   // |A|^2 + 1e-30: the floor keeps rsqrt finite at A = 0 and is far below one ulp of any
   // non-negligible cell, so the key and the magnitude are unchanged
   const float a2 = fmaf(A.x, A.x, fmaf(A.y, A.y, 1e-30f));
@@ -111,12 +111,12 @@ __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int 
   best = upd ? kv : best;
   bk = upd ? k : bk;
   if (LM == 0) {
-    if (mrow) mrow[(size_t)k * a.L] = sqrtf(a2);
+    if (mrow) mrow[(size_t)k * a.L] = sqrtf(a2) * msc;
     return make_float2(0.f, 0.f);
   }
   const float rsq = rsqa(a2);
   const float mag = a2 * rsq;
-  if (mrow) mrow[(size_t)k * a.L] = mag;
+  if (mrow) mrow[(size_t)k * a.L] = mag * msc;
   float phi, gphi;
   if (LM == 1) {
     phi = ex2a(fmaf(lbN, HW ? wt * mag : mag, nlbs));
@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
   uint32_t aEr[4], aEi[4], aOr[4], aOi[4];  // F16: m16n8k16 A fragments (rows g, g+8; K columns 2c.., 2c+8..)
   uint32_t aErh[4], aErl[4], aEih[4], aEil[4], aOrh[4], aOrl[4], aOih[4], aOil[4];  // TF32 3x
   float nm2[2] = {0.f, 0.f};
+  float sc[2] = {1.f, 1.f}, isc[2] = {1.f, 1.f};  // per-lag prescale of the FP16 path (1 for TF32)
   if constexpr (F16) {
     // K layout (16 columns): lane c holds k = 2c, 2c+1 (registers 0/1) and 2c+8, 2c+9 (2/3) and
     // owns node pair j = c: (hi_c, lo_c | hi_c, e_c) with e = hi_4, lo_4, hi_4, 0 for c = 0..3;
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     // is x_hi a_hi + x_lo a_hi + x_hi a_lo for every j < 5.  Each lane loads two node pairs.
     const float2* Rp = a.Rn + (size_t)pr * Q * a.LS;
     const bool own = cq < QH, ext = QH > 4 && cq < 3;
+    float2 xv[2], yv[2], x4v[2], y4v[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float2 x = make_float2(0.f, 0.f), y = x, x4 = x, y4 = x;
@@ -510,6 +512,28 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
       }
       nm2[h] = fmaxf(fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)),
                      fmaxf(fmaf(x4.x, x4.x, x4.y * x4.y), fmaf(y4.x, y4.x, y4.y * y4.y)));
+      nm2[h] = fmaxf(nm2[h], __shfl_xor_sync(0xffffffffu, nm2[h], 1));
+      nm2[h] = fmaxf(nm2[h], __shfl_xor_sync(0xffffffffu, nm2[h], 2));
+      xv[h] = x; yv[h] = y; x4v[h] = x4; y4v[h] = y4;
+      // Per-lag power-of-two prescale sigma (exact): the node sums |E|, |O| <= 2 max_q |R_q| are
+      // brought to <= 8192, inside FP16's range and far above its subnormals whatever ||s|| ||w|| is
+      // (unscaled values overflow FP16 once ||s|| ||w|| > ~32K and lose their lo parts
+      // for small norms).  The cell epilogue works on sigma A: the cotangent gphi A / |A| is
+      // invariant, and the magnitude-based terms take the 1/sigma into their per-lag constants.
+      int ex = 0;
+      if (nm2[h] > 0.f) {
+        const float t = 8192.f / (2.f * sqrtf(nm2[h]));
+        ex = (int)((__float_as_uint(t) >> 23) & 0xFFu) - 127;
+        ex = ex < -100 ? -100 : (ex > 100 ? 100 : ex);
+      }
+      sc[h] = __uint_as_float((uint32_t)(127 + ex) << 23);
+      isc[h] = __uint_as_float((uint32_t)(127 - ex) << 23);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float2 x = make_float2(xv[h].x * sc[h], xv[h].y * sc[h]), y = make_float2(yv[h].x * sc[h], yv[h].y * sc[h]);
+      const float2 x4 = make_float2(x4v[h].x * sc[h], x4v[h].y * sc[h]);
+      const float2 y4 = make_float2(y4v[h].x * sc[h], y4v[h].y * sc[h]);
       const float vc[4] = {x.x + y.x, x.y + y.y, x.x - y.x, x.y - y.y};
       const float v4[4] = {x4.x + y4.x, x4.y + y4.y, x4.x - y4.x, x4.y - y4.y};
       uint32_t* frag[4] = {aEr, aEi, aOr, aOi};
@@ -576,12 +600,12 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) GEr[i] = GEi[i] = GOr[i] = GOi[i] = 0.f;
-    const float lbN = lb * a.invN;
-    float nlbs[2], qN[2];
+    float lbN[2], nlbs[2], qN[2];  // per lag: the prescale's 1/sigma folded into the magnitude terms
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      lbN[h] = lb * a.invN * isc[h];
       nlbs[h] = valid[h] ? -lb * shift[h] : -INFINITY;
-      qN[h] = valid[h] ? a.invN / shift[h] : 0.f;
+      qN[h] = valid[h] ? a.invN / shift[h] * isc[h] : 0.f;
     }
     // one 8-pair tile: forward MMAs, 8 cells per thread, adjoint MMAs.  MASKED: the remainder
     // tile of a K/2 that is not a multiple of 8 (pairs >= K/2 are zero padding).
@@ -623,20 +647,20 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         const float2 A1 = make_float2(Per[e] - Por[e], Pei[e] - Poi[e]);
         float gf0, gf1;  // cotangent factors: G = gf A
         if (!MASKED) {
-          gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bl[h], kl[h], S[h],
-                                                   mrow[h]).x;
-          gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, a.K - 1 - p, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bh[h],
-                                                  kh[h], S[h], mrow[h]).x;
+          gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, p, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h], bl[h], kl[h],
+                                                   S[h], mrow[h], isc[h]).x;
+          gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, a.K - 1 - p, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h],
+                                                  bh[h], kh[h], S[h], mrow[h], isc[h]).x;
         } else {
           const bool pv = p < Kp;
           const bool v0 = valid[h] && pv;
           float b0 = bl[h], b1 = bh[h];
           int k0 = kl[h], k1 = kh[h];
-          gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, pv ? p : 0, la, idx[h], v0, lbN, v0 ? nlbs[h] : -INFINITY,
-                                                   v0 ? qN[h] : 0.f, b0, k0, S[h], pv ? mrow[h] : nullptr).x;
-          gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, pv ? a.K - 1 - p : 0, la, idx[h], v0, lbN,
+          gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, pv ? p : 0, la, idx[h], v0, lbN[h], v0 ? nlbs[h] : -INFINITY,
+                                                   v0 ? qN[h] : 0.f, b0, k0, S[h], pv ? mrow[h] : nullptr, isc[h]).x;
+          gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, pv ? a.K - 1 - p : 0, la, idx[h], v0, lbN[h],
                                                   v0 ? nlbs[h] : -INFINITY, v0 ? qN[h] : 0.f, b1, k1, S[h],
-                                                  pv ? mrow[h] : nullptr).x;
+                                                  pv ? mrow[h] : nullptr, isc[h]).x;
           if (pv) { bl[h] = b0; kl[h] = k0; bh[h] = b1; kh[h] = k1; }
           if (!v0) gf0 = gf1 = 0.f;
         }
@@ -710,8 +734,8 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
       for (int h = 0; h < 2; ++h) {
         float Sm = 0.f, bm = bl[h];
         int km = kl[h];
-        const float2 Gm = lr_cell<LM, HW, GRAD, false>(Am[h], Kp, la, idx[h], valid[h], lbN, nlbs[h], qN[h], bm, km, Sm,
-                                                       cq == 0 ? mrow[h] : nullptr);
+        const float2 Gm = lr_cell<LM, HW, GRAD, false>(Am[h], Kp, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h], bm, km, Sm,
+                                                       cq == 0 ? mrow[h] : nullptr, isc[h]);
         if (cq == 0) { S[h] += Sm; bl[h] = bm; kl[h] = km; }
         if (GRAD) {
 #pragma unroll
@@ -728,7 +752,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     bool bad = false;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const float vb = sqrtf(fmaxf(fmaxf(bl[h], bh[h]), 0.f)) * a.invN;
+      const float vb = sqrtf(fmaxf(fmaxf(bl[h], bh[h]), 0.f)) * isc[h] * a.invN;
       const bool bd = valid[h] && (LM == 1 ? lb * (vb - shift[h]) > 96.f
                                            : (vb > shift[h] && (bp * log2f(vb / shift[h])) > 96.f));
       bad |= bd;
@@ -751,6 +775,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     float best = bl[h];
     int bk = kl[h];
     if (bh[h] > best) { best = bh[h]; bk = kh[h]; }
+    best *= isc[h] * isc[h];  // exact: sigma is a power of two
     const uint32_t cell = ((uint32_t)((m * M + l) * a.L + idx[h])) * (uint32_t)a.K + (uint32_t)bk;
     const unsigned long long kk = (valid[h] && best >= 0.f) ? pack_key(best, cell) : 0ull;
     key = kk > key ? kk : key;

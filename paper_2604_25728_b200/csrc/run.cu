@@ -26,19 +26,26 @@ struct RunDev {  // device-side bookkeeping (one allocation)
 };
 
 // One block per restart: compare the hard WPSL of outer iteration t (1-based) with the best so far.
-__global__ void k_run_track(int t, const sqngd_metrics* hard, double* best_wpsl, int32_t* best_iter, int* stall,
-                            double* hist, int R, RunDev* rd, RunPtrs p) {
+// An improvement is a decrease by more than `tol` ("by >= 1e-6, linear, N-normalized";
+// fp32 noise would otherwise keep resetting the stall counter); the hard loss L at the last
+// improvement is kept so the stop test can require that L kept decreasing over the window.
+__global__ void k_run_track(int t, const sqngd_metrics* hard, double tol, double* best_wpsl, int32_t* best_iter,
+                            int* stall, double* loss_ref, double* loss_cur, double* hist, double* lhist, int R,
+                            RunDev* rd, RunPtrs p) {
   const int r = blockIdx.x;
   __shared__ int improve;
   if (rd->done) return;  // uniform: the rule already fired, the snapshot is final
   if (threadIdx.x == 0) {
-    const double v = hard[r].wpsl;
+    const double v = hard[r].wpsl, L = hard[r].loss;
     if (hist) hist[(size_t)(t - 1) * R + r] = v;
-    improve = v < best_wpsl[r];  // strict improvement (a NaN never improves)
+    if (lhist) lhist[(size_t)(t - 1) * R + r] = L;
+    loss_cur[r] = L;
+    improve = v < best_wpsl[r] - tol || (t == 1 && v == v);  // (a NaN never improves)
     if (improve) {
       best_wpsl[r] = v;
       best_iter[r] = t;
       stall[r] = 0;
+      loss_ref[r] = L;
     } else {
       stall[r] += 1;
     }
@@ -55,10 +62,14 @@ __global__ void k_run_track(int t, const sqngd_metrics* hard, double* best_wpsl,
   copy(p.theta, p.btheta, p.ntheta);
 }
 
-__global__ void k_run_done(int t, const int* stall, int R, int patience, RunDev* rd) {
+// The rule fires when every restart has gone `patience` iterations without an improvement and (if
+// required) its hard loss L is below the value it had at the last improvement: "further reduction of
+// L does not lead to improvement in the WPSL".
+__global__ void k_run_done(int t, const int* stall, const double* loss_ref, const double* loss_cur, int R,
+                           int patience, int need_dec, RunDev* rd) {
   if (rd->done || patience <= 0) return;
   int all = 1;
-  for (int r = 0; r < R; ++r) all &= stall[r] >= patience;
+  for (int r = 0; r < R; ++r) all &= stall[r] >= patience && (!need_dec || loss_cur[r] < loss_ref[r]);
   if (all) {
     rd->done = 1;
     rd->stop_iter = t;
@@ -77,30 +88,31 @@ __global__ void k_run_done(int t, const int* stall, int R, int patience, RunDev*
   } while (0)
 
 extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd_run_opts* opts, sqngd_state* best,
-                                  double* best_wpsl, int32_t* best_iter, double* wpsl_hist, sqngd_run_result* result,
-                                  sqngd_stream stream) {
+                                  double* best_wpsl, int32_t* best_iter, double* wpsl_hist, double* loss_hist,
+                                  sqngd_run_result* result, sqngd_stream stream) {
+  auto cleanup = []() {};
   if (!ctx || !state || !opts || !best || !best_wpsl || !best_iter || !result || opts->T < 1 ||
-      opts->check_every < 1 || !best->z || !best->rho || !best->w)
+      opts->check_every < 1 || !best->z || !best->rho || !best->w || !(opts->tol >= 0.0))
     return sq_ctx_fail(ctx, SQNGD_E_INVALID, "sqngd_run: bad argument", "");
   const sqngd_config& c = *sq_ctx_config(ctx);
   const bool net = c.net_width > 0;
   if (net && !best->theta) return sq_ctx_fail(ctx, SQNGD_E_INVALID, "sqngd_run: generator mode needs best->theta", "");
-  cudaSetDevice(sq_ctx_device(ctx));
+  RK(cudaSetDevice(sq_ctx_device(ctx)));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  sqngd_metrics* hard = nullptr;
-  int* stall = nullptr;
-  RunDev* rd = nullptr;
-  RunDev* rd_host = nullptr;
-  auto cleanup = [&]() {
-    if (hard) cudaFree(hard);
-    if (stall) cudaFree(stall);
-    if (rd) cudaFree(rd);
-    if (rd_host) cudaFreeHost(rd_host);
-  };
-  RK(cudaMalloc(&hard, sizeof(sqngd_metrics) * c.R));
-  RK(cudaMalloc(&stall, sizeof(int) * c.R));
-  RK(cudaMalloc(&rd, sizeof(RunDev)));
-  RK(cudaMallocHost(&rd_host, sizeof(RunDev)));
+  // bookkeeping buffers live in the context (one allocation, reused by every call): the hard-metrics
+  // pointer handed to sqngd_step stays the same, so its step graph is captured once
+  const size_t R = (size_t)c.R;
+  const size_t off_stall = R * sizeof(sqngd_metrics), off_lref = off_stall + ((R * sizeof(int) + 7) & ~(size_t)7);
+  const size_t off_lcur = off_lref + R * sizeof(double), off_rd = off_lcur + R * sizeof(double);
+  void* host = nullptr;
+  char* ws = static_cast<char*>(sq_ctx_run_ws(ctx, off_rd + sizeof(RunDev), &host, sizeof(RunDev)));
+  if (!ws || !host) return sq_ctx_fail(ctx, SQNGD_E_NOMEM, "sqngd_run: workspace", "");
+  sqngd_metrics* hard = reinterpret_cast<sqngd_metrics*>(ws);
+  int* stall = reinterpret_cast<int*>(ws + off_stall);
+  double* loss_ref = reinterpret_cast<double*>(ws + off_lref);
+  double* loss_cur = reinterpret_cast<double*>(ws + off_lcur);
+  RunDev* rd = reinterpret_cast<RunDev*>(ws + off_rd);
+  RunDev* rd_host = static_cast<RunDev*>(host);
   RK(cudaMemsetAsync(stall, 0, sizeof(int) * c.R, st));
   RK(cudaMemsetAsync(rd, 0, sizeof(RunDev), st));
   {  // best_wpsl = +inf, best_iter = 0
@@ -121,12 +133,11 @@ extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd
   bool stopped = false;
   for (t = 1; t <= opts->T; ++t) {
     sqngd_status s = sqngd_step(ctx, state, SQNGD_BLOCK_AB, nullptr, hard, stream);
-    if (s != SQNGD_OK) {
-      cleanup();
-      return s;
-    }
-    k_run_track<<<c.R, 256, 0, st>>>((int)t, hard, best_wpsl, best_iter, stall, wpsl_hist, c.R, rd, p);
-    k_run_done<<<1, 1, 0, st>>>((int)t, stall, c.R, opts->patience, rd);
+    if (s != SQNGD_OK) return s;
+    k_run_track<<<c.R, 256, 0, st>>>((int)t, hard, opts->tol, best_wpsl, best_iter, stall, loss_ref, loss_cur,
+                                     wpsl_hist, loss_hist, c.R, rd, p);
+    k_run_done<<<1, 1, 0, st>>>((int)t, stall, loss_ref, loss_cur, c.R, opts->patience,
+                                opts->require_loss_decrease, rd);
     RK(cudaGetLastError());
     if (t % opts->check_every == 0 || t == opts->T) {
       RK(cudaMemcpyAsync(rd_host, rd, sizeof(RunDev), cudaMemcpyDeviceToHost, st));
@@ -140,6 +151,5 @@ extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd
   result->iterations = stopped ? rd_host->stop_iter : opts->T;
   result->steps_run = stopped ? t : opts->T;
   result->stopped = stopped ? 1 : 0;
-  cleanup();
   return sqngd_sync(ctx, stream);
 }

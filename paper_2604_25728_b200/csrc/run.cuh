@@ -5,3 +5,6 @@
 const sqngd_config* sq_ctx_config(sqngd_ctx ctx);
 int sq_ctx_device(sqngd_ctx ctx);
 sqngd_status sq_ctx_fail(sqngd_ctx ctx, sqngd_status st, const char* what, const char* why);
+// Driver workspace owned by the context: `dev_bytes` of device memory and `host_bytes` of pinned host
+// memory, allocated on first use (grown if needed) and freed by sqngd_destroy.  nullptr on failure.
+void* sq_ctx_run_ws(sqngd_ctx ctx, size_t dev_bytes, void** host, size_t host_bytes);

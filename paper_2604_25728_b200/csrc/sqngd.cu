@@ -113,6 +113,9 @@ struct sqngd_ctx_s {
   float2* tslot = nullptr;     // [R M Q][N] Step-B node time-domain partials
   int* lr_cnt = nullptr;       // [R M Q] k_adj_g arrival counters
   Comm comm;
+  void* run_dev = nullptr;     // sqngd_run bookkeeping (run.cu), reused across calls
+  void* run_host = nullptr;    // pinned stop-flag mirror
+  size_t run_dev_bytes = 0, run_host_bytes = 0;
   long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
   float2* d_ct = nullptr;      // [2][cts] bias corrections of the step's inner iterations (k_set_t)
   int cts = 0;
@@ -541,6 +544,24 @@ int sq_ctx_device(sqngd_ctx ctx) { return ctx->dev; }
 sqngd_status sq_ctx_fail(sqngd_ctx ctx, sqngd_status st, const char* what, const char* why) {
   return fail(ctx, st, what, why);
 }
+void* sq_ctx_run_ws(sqngd_ctx ctx, size_t dev_bytes, void** host, size_t host_bytes) {
+  if (dev_bytes > ctx->run_dev_bytes) {
+    if (ctx->run_dev) cudaFree(ctx->run_dev);
+    ctx->run_dev = nullptr;
+    ctx->run_dev_bytes = 0;
+    if (cudaMalloc(&ctx->run_dev, dev_bytes) != cudaSuccess) return nullptr;
+    ctx->run_dev_bytes = dev_bytes;
+  }
+  if (host_bytes > ctx->run_host_bytes) {
+    if (ctx->run_host) cudaFreeHost(ctx->run_host);
+    ctx->run_host = nullptr;
+    ctx->run_host_bytes = 0;
+    if (cudaMallocHost(&ctx->run_host, host_bytes) != cudaSuccess) return nullptr;
+    ctx->run_host_bytes = host_bytes;
+  }
+  *host = ctx->run_host;
+  return ctx->run_dev;
+}
 
 extern "C" {
 
@@ -753,6 +774,13 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   if (const char* ev = getenv("SQNGD_FUSE_RHO")) ctx->fuse_rho = ev[0] == '1';
   if (ctx->rho_chunk > 256) ctx->rho_sort = false;
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
+  {  // Adam(rho) + projection: 2 n2 floats of dynamic shared memory (64 KB at B r_n = 8192, above
+     // the 48 KB a launch gets without opting in)
+    int n2 = 1;
+    while (n2 < ctx->BR) n2 <<= 1;
+    CK(cudaFuncSetAttribute(k_adam_project_rho, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(2 * n2 * sizeof(float))));
+  }
   CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
   CK(cudaMalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
   CK(cudaMemset(ctx->rho_cnt, 0, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
@@ -950,6 +978,8 @@ void sqngd_destroy(sqngd_ctx ctx) {
                   ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (ctx->run_dev) cudaFree(ctx->run_dev);
+  if (ctx->run_host) cudaFreeHost(ctx->run_host);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -1294,6 +1324,15 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
   return launch_check(ctx, "finalize grad");
 }
 
+// a6 reporting (Eq. 10): SNRL_m and the restart's worst SNRL into the metrics, after the forward.
+static sqngd_status run_snrl(sqngd_ctx ctx, const float2* s, const float2* w, double* out, MetricsOut* met,
+                             cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  k_snrl<<<c.R, 256, 0, st>>>(c.M, c.N, s, w, out, met, ctx->status);
+  ctx->launches += 1;
+  return launch_check(ctx, "snrl");
+}
+
 static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho, float* grad_rho, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   const int MN = c.M * c.N;
@@ -1333,15 +1372,17 @@ sqngd_status sqngd_quantize(sqngd_ctx ctx, const float* z, const float* rho, flo
 }
 
 sqngd_status sqngd_af_forward(sqngd_ctx ctx, const float* s, const float* w, float* af_mag,
-                              sqngd_metrics* metrics, double* p_out, sqngd_stream stream) {
+                              sqngd_metrics* metrics, double* p_out, double* snrl_db_out, sqngd_stream stream) {
   if (!ctx || !s || !w) return fail(ctx, SQNGD_E_INVALID, "sqngd_af_forward: null argument");
   CK(cudaSetDevice(ctx->dev));
   const cudaStream_t st = S(stream);
   sqngd_status rc = run_filter_fft(ctx, reinterpret_cast<const float2*>(w), st);
   if (rc) return rc;
   MetricsOut* met = metrics ? reinterpret_cast<MetricsOut*>(metrics) : ctx->met;
-  return run_forward(ctx, reinterpret_cast<const float2*>(s), reinterpret_cast<const float2*>(w), af_mag, met, p_out,
-                     nullptr, 0, st);
+  if ((rc = run_forward(ctx, reinterpret_cast<const float2*>(s), reinterpret_cast<const float2*>(w), af_mag, met,
+                        p_out, nullptr, 0, st)))
+    return rc;
+  return run_snrl(ctx, reinterpret_cast<const float2*>(s), reinterpret_cast<const float2*>(w), snrl_db_out, met, st);
 }
 
 sqngd_status sqngd_loss_grad_s(sqngd_ctx ctx, const float* s, const float* w, int wrt, sqngd_metrics* metrics,
@@ -1535,6 +1576,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
     if ((rc = run_forward(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), nullptr, nullptr, 0,
                           st)))
       return rc;
+    if ((rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), st))) return rc;
   }
   return SQNGD_OK;
 }

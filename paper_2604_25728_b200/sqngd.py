@@ -56,6 +56,7 @@ class Metrics(C.Structure):
         ("wapsl", C.c_double), ("wcpsl", C.c_double), ("wpsl", C.c_double),
         ("argmax_auto", C.c_int32 * 4), ("argmax_cross", C.c_int32 * 4),
         ("flags", C.c_uint32), ("n_cells", C.c_uint32),
+        ("apslr_db", C.c_double), ("cpslr_db", C.c_double), ("pslr_db", C.c_double), ("snrl_db_max", C.c_double),
     ]
 
 
@@ -73,7 +74,8 @@ class State(C.Structure):
 
 
 class RunOpts(C.Structure):
-    _fields_ = [("T", C.c_int32), ("patience", C.c_int32), ("check_every", C.c_int32)]
+    _fields_ = [("T", C.c_int32), ("patience", C.c_int32), ("check_every", C.c_int32),
+                ("require_loss_decrease", C.c_int32), ("tol", C.c_double)]
 
 
 class RunResult(C.Structure):
@@ -103,7 +105,7 @@ def lib():
         L.sqngd_quantize.restype = i32
         L.sqngd_quantize.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
         L.sqngd_af_forward.restype = i32
-        L.sqngd_af_forward.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.sqngd_af_forward.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
         L.sqngd_loss_grad_s.restype = i32
         L.sqngd_loss_grad_s.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp]
         L.sqngd_af_loss_grad.restype = i32
@@ -127,7 +129,7 @@ def lib():
         L.sqngd_net_backward.restype = i32
         L.sqngd_net_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.sqngd_run.restype = i32
-        L.sqngd_run.argtypes = [vp, C.POINTER(State), C.POINTER(RunOpts), C.POINTER(State), vp, vp, vp,
+        L.sqngd_run.argtypes = [vp, C.POINTER(State), C.POINTER(RunOpts), C.POINTER(State), vp, vp, vp, vp,
                                 C.POINTER(RunResult), vp]
         L.sqngd_version.restype = C.c_char_p
         L.sqngd_version.argtypes = []
@@ -281,11 +283,15 @@ class Context:
                                          _ptr(out["b_hard"]), _ptr(out["dq"]), self._stream()))
         return out
 
-    def af_forward(self, s, w, want_map: bool = False, met_buf=None, want_p: bool = True):
-        amap = self._f((self.R, self.M, self.M, self.K, self.L)) if want_map else None
+    def af_forward(self, s, w, want_map: bool = False, met_buf=None, want_p: bool = True, snrl_out=None,
+                   map_out=None):
+        """Forward AF + metrics.  Returns (metrics buffer, p_m [R][M] or None, |A| map or None);
+        snrl_out: optional [R][M] float64 tensor that receives SNRL_m (Eq. 10, dB)."""
+        amap = map_out if map_out is not None else (self._f((self.R, self.M, self.M, self.K, self.L)) if want_map
+                                                    else None)
         p = self.torch.empty((self.R, self.M), dtype=self.torch.float64, device=self.device) if want_p else None
         met = self._met if met_buf is None else met_buf
-        self._check(lib().sqngd_af_forward(self.h, _ptr(s), _ptr(w), _ptr(amap), _ptr(met), _ptr(p),
+        self._check(lib().sqngd_af_forward(self.h, _ptr(s), _ptr(w), _ptr(amap), _ptr(met), _ptr(p), _ptr(snrl_out),
                                            self._stream()))
         return met, p, amap
 
@@ -342,24 +348,28 @@ class Context:
         st["t_a"], st["t_b"] = 0, 0
         return st
 
-    def run(self, st: dict, T: int, patience: int, check_every: int = 1, want_hist: bool = True):
+    def run(self, st: dict, T: int, patience: int, check_every: int = 1, want_hist: bool = True,
+            tol: float = 1e-6, require_loss_decrease: bool = True):
         """Alg. 1 driver (sqngd_run): returns (best snapshot dict, best_wpsl [R], best_iter [R],
-        wpsl_hist [T][R] or None, result dict); `st` is advanced in place."""
+        wpsl_hist [T][R] or None, result dict with the hard-loss history 'loss_hist'); `st` is
+        advanced in place."""
         t = self.torch
         best = {k: t.empty_like(st[k]) for k in ("z", "rho", "w")}
         best["theta"] = t.empty_like(st["theta"]) if st.get("theta") is not None else None
         bw = t.empty(self.R, dtype=t.float64, device=self.device)
         bi = t.empty(self.R, dtype=t.int32, device=self.device)
         hist = t.full((T, self.R), float("nan"), dtype=t.float64, device=self.device) if want_hist else None
+        lhist = t.full((T, self.R), float("nan"), dtype=t.float64, device=self.device) if want_hist else None
         cs = self._cstate(st)
         cb = State(z=_ptr(best["z"]), rho=_ptr(best["rho"]), w=_ptr(best["w"]), theta=_ptr(best["theta"]))
         res = RunResult()
-        opts = RunOpts(T=int(T), patience=int(patience), check_every=int(check_every))
+        opts = RunOpts(T=int(T), patience=int(patience), check_every=int(check_every),
+                       require_loss_decrease=1 if require_loss_decrease else 0, tol=float(tol))
         self._check(lib().sqngd_run(self.h, C.byref(cs), C.byref(opts), C.byref(cb), _ptr(bw), _ptr(bi), _ptr(hist),
-                                    C.byref(res), self._stream()))
+                                    _ptr(lhist), C.byref(res), self._stream()))
         st["t_a"], st["t_b"] = cs.t_a, cs.t_b
         return best, bw, bi, hist, {"iterations": res.iterations, "steps_run": res.steps_run,
-                                    "stopped": bool(res.stopped)}
+                                    "stopped": bool(res.stopped), "loss_hist": lhist}
 
     def _cstate(self, st: dict) -> State:
         return State(z=_ptr(st["z"]), rho=_ptr(st["rho"]), w=_ptr(st["w"]), m_z=_ptr(st["m_z"]), v_z=_ptr(st["v_z"]),

@@ -25,3 +25,21 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the achieved parity errors (tests/parity_util.RECORD) to $SQNGD_PARITY_LOG."""
+    path = os.environ.get("SQNGD_PARITY_LOG")
+    if not path:
+        return
+    import json
+
+    parity_util = sys.modules.get("parity_util")
+    if parity_util is None:
+        return
+    rec = parity_util.RECORD
+    if not rec:
+        return
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump(rec, f, indent=0)

@@ -34,8 +34,9 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_struct_layouts():
-    # sqngd_metrics: 6 doubles + 8 int32 + 2 uint32 = 88 bytes; sqngd_state: 9 pointers + 2 int64 + 4 pointers
-    assert sqngd.METRICS_BYTES == 88
+    # sqngd_metrics: 6 doubles + 8 int32 + 2 uint32 + 4 doubles (PSLR x3, SNRL) = 120 bytes;
+    # sqngd_state: 9 pointers + 2 int64 + 4 pointers
+    assert sqngd.METRICS_BYTES == 120
     assert C.sizeof(sqngd.State) == 9 * 8 + 16 + 4 * 8
 
 

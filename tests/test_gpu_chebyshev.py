@@ -3,8 +3,8 @@ against the fp64 oracle, through the C-ABI, on the same seeded fp32 inputs.
 
 The engine interpolates the AF in Doppler from Q exact node correlations; its error bound
 (lr_tol = 1e-7 of ||s|| ||w|| = N) is far inside the parity bar, so the bar is the same as the
-per-bin FFT engine's (tests/test_gpu_parity.py): |A| per cell 1e-4 rel + 2e-6 N, loss 1e-5 rel,
-PSL 0.01 dB, argmax identical when unique by > 1e-5, gradients 1e-4 normwise.  Every case forces
+per-bin FFT engine's (tests/parity_util.py): |A| per cell 1e-4 rel + 1e-6 N, loss 1e-5 rel,
+PSL 0.01 dB, argmax identical when unique by > 1e-5, gradients 1e-4 normwise and 1e-3 component-wise.  Every case forces
 the engine, and both engines are also compared with each other on the same inputs."""
 import math
 
@@ -16,6 +16,8 @@ torch = pytest.importorskip("torch")
 from oracle import oracle as O  # noqa: E402
 from paper_2604_25728_b200 import inputs, sqngd  # noqa: E402
 from paper_2604_25728_b200.configs import C1, Cfg  # noqa: E402
+
+from parity_util import check_grad, check_map  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -40,13 +42,6 @@ def weights_for(c, seed):
     wt = rng.uniform(0.5, 1.5, size=(c.K, c.lags)).astype(np.float32)
     wt[rng.uniform(size=wt.shape) < 0.1] = 0.0
     return wt
-
-
-def check_map(A_gpu, A_ref, N):
-    ref = np.abs(A_ref)
-    err = np.abs(A_gpu.astype(np.float64) - ref)
-    bad = err > 1e-4 * ref + 2e-6 * N
-    assert not bad.any(), f"{bad.sum()} cells off; worst abs {err.max():.3e} (N={N})"
 
 
 def argmax_unique(v_sorted):
@@ -82,7 +77,7 @@ def fwd_cases():
         Cfg("offcentre", M=2, N=100, B=4, K=40, f_lo=0.2, f_hi=1.1),         # even K, shifted grid
         Cfg("wide", M=2, N=64, B=4, K=61, f_lo=-1.5, f_hi=1.5),              # more nodes
         Cfg("p2048", M=2, N=1024, B=16, K=33, f_lo=-0.5, f_hi=0.5),
-        Cfg("p8192", M=1, N=4096, B=16, K=33, f_lo=-0.5, f_hi=0.5),
+        Cfg("p8192", M=2, N=4096, B=16, K=33, f_lo=-0.5, f_hi=0.5),       # cross maps at P = 8192
         Cfg("n2", M=2, N=2, B=2, K=31, f_lo=-0.5, f_hi=0.5, r_n=1),          # 3 lags, one 16-lag chunk
         Cfg("m1", M=1, N=33, B=4, K=63, f_lo=-0.5, f_hi=0.5),                 # no cross maps
         Cfg("k3", M=2, N=40, B=4, K=3, f_lo=-0.05, f_hi=0.05),               # one bin pair + middle, Q = 6
@@ -148,8 +143,8 @@ def test_gradients_explicit_waveform(c, mode):
     for r in range(c.R):
         assert abs(mA[r]["loss"] - ref_met[r]["loss"]) <= 1e-5 * ref_met[r]["loss"]
         assert abs(mB[r]["loss"] - ref_met[r]["loss"]) <= 1e-5 * ref_met[r]["loss"]
-    assert rel(gw, gw_ref) < 1e-4, rel(gw, gw_ref)
-    assert rel(gs, gs_ref) < 1e-4, rel(gs, gs_ref)
+    check_grad(gw, gw_ref, "grad_w")
+    check_grad(gs, gs_ref, "grad_s")
 
 
 @pytest.mark.parametrize("engine", [sqngd.ENGINE_FFT, CHEB])
@@ -172,8 +167,8 @@ def test_weighted_roi(engine, mode):
         assert abs(g["loss"] - o["loss"]) <= 1e-5 * o["loss"]
         assert abs(20 * math.log10(g["wpsl"] / o["wpsl"])) < 0.01
         assert g["n_cells"] == o["n_cells"]
-    assert rel(gw.cpu().numpy(), gw_ref) < 1e-4
-    assert rel(gs.cpu().numpy(), gs_ref) < 1e-4
+    check_grad(gw.cpu().numpy(), gw_ref, "grad_w (weighted)")
+    check_grad(gs.cpu().numpy(), gs_ref, "grad_s (weighted)")
 
 
 def test_engines_agree_and_ksplit():
@@ -192,7 +187,7 @@ def test_engines_agree_and_ksplit():
         out[eng] = (amap.cpu().numpy().astype(np.float64), m1, gs.cpu().numpy(), gw.cpu().numpy())
     a0, m0, gs0, gw0 = out[sqngd.ENGINE_FFT]
     a1, m1, gs1, gw1 = out[CHEB]
-    assert np.all(np.abs(a1 - a0) <= 1e-4 * a0 + 2e-6 * c.N)
+    assert np.all(np.abs(a1 - a0) <= 1e-4 * a0 + 1e-6 * c.N)
     assert abs(m1["loss"] - m0["loss"]) <= 1e-5 * m0["loss"]
     assert rel(gs1, gs0) < 1e-4 and rel(gw1, gw0) < 1e-4
 

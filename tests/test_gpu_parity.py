@@ -1,9 +1,9 @@
 """GPU (C-ABI) vs fp64 oracle on identical seeded fp32 inputs.
 
 Tolerances (BASELINE north star):
-  |A| per cell: | |A|_gpu - |A|_ref | <= 1e-4 |A|_ref + 2e-6 N      (fp32 FFT, -40 dB floor)
+  |A| per cell: | |A|_gpu - |A|_ref | <= 1e-4 |A|_ref + 1e-6 N      (tests/parity_util.py)
   loss:         relative 1e-5;   PSL: 0.01 dB;   argmax identical when unique by > 1e-5 rel.
-  gradients:    ||g_gpu - g_ref|| / ||g_ref|| <= 1e-4
+  gradients:    ||g_gpu - g_ref|| / ||g_ref|| <= 1e-4, component-wise 1e-3 on the support
   hard phase indices: bit-exact.
 """
 import math
@@ -16,6 +16,8 @@ torch = pytest.importorskip("torch")
 from oracle import oracle as O  # noqa: E402
 from paper_2604_25728_b200 import inputs, sqngd  # noqa: E402
 from paper_2604_25728_b200.configs import C1, Cfg  # noqa: E402
+
+from parity_util import check_grad, check_map, record  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -37,6 +39,7 @@ def cases_fwd():
         Cfg("p2048", M=2, N=1024, B=16, K=3, f_lo=-0.5, f_hi=0.5),
         Cfg("p4096", M=1, N=1500, B=4, K=2, f_lo=-0.5, f_hi=0.5),
         Cfg("p8192", M=1, N=4096, B=16, K=2, f_lo=-0.5, f_hi=0.5),
+        Cfg("p8192-m2", M=2, N=3001, B=16, K=3, f_lo=-0.5, f_hi=0.5),     # cross maps at P = 8192, ragged N
         Cfg("batch", M=2, N=48, B=4, K=5, f_lo=-0.5, f_hi=0.5, R=3),
         Cfg("roi", M=2, N=40, B=4, K=5, f_lo=-1.0, f_hi=1.0, tau_lo=-10, tau_hi=25),
     ]
@@ -49,15 +52,6 @@ def random_inputs(c, seed):
     # energy N per row (the feasible set of Eq. 31)
     w = (w * np.sqrt(c.N / np.sum(np.abs(w.astype(np.complex128)) ** 2, axis=-1, keepdims=True))).astype(np.complex64)
     return s, w
-
-
-def check_map(A_gpu, A_ref, N):
-    ref = np.abs(A_ref)
-    err = np.abs(A_gpu.astype(np.float64) - ref)
-    tol = 1e-4 * ref + 2e-6 * N
-    bad = err > tol
-    assert not bad.any(), f"{bad.sum()} cells off; worst abs {err.max():.3e} (N={N})"
-    return err.max() / N
 
 
 def argmax_unique(A_ref, c, auto: bool):
@@ -85,7 +79,7 @@ def argmax_unique(A_ref, c, auto: bool):
 @pytest.mark.parametrize("mode", [sqngd.LOSS_MAX, sqngd.LOSS_LSE, sqngd.LOSS_PNORM])
 def test_forward_map_and_metrics(c, mode):
     c = c.with_(loss_mode=mode, beta_or_p={0: 0.0, 1: 200.0, 2: 16.0}[mode])
-    if c.N >= 1500 and mode != sqngd.LOSS_LSE:
+    if c.N >= 1500 and mode != sqngd.LOSS_LSE and c.name != "p8192-m2":
         pytest.skip("large-N map checked once")
     s, w = random_inputs(c, 7)
     ctx = sqngd.Context(c)
@@ -141,8 +135,8 @@ def test_gradients_explicit_waveform(c, mode):
     for r in range(c.R):
         assert abs(mA[r]["loss"] - ref_met[r]["loss"]) <= 1e-5 * ref_met[r]["loss"]
         assert abs(mB[r]["loss"] - ref_met[r]["loss"]) <= 1e-5 * ref_met[r]["loss"]
-    assert rel(gw, gw_ref) < 1e-4, rel(gw, gw_ref)
-    assert rel(gs, gs_ref) < 1e-4, rel(gs, gs_ref)
+    check_grad(gw, gw_ref, "grad_w")
+    check_grad(gs, gs_ref, "grad_s")
 
 
 @pytest.mark.parametrize("B,r_n,c_", [(4, 3, 300.0), (8, 100, 300.0), (16, 100, 300.0), (4, 2, 30.0)])
@@ -159,7 +153,8 @@ def test_quantizer(B, r_n, c_):
     assert np.array_equal(b, q["b_hard"]), f"{(b != q['b_hard']).sum()} hard indices differ"
     np.testing.assert_allclose(out["s_hard"].cpu().numpy(), q["s_hard"], atol=2e-7)
     ph = np.angle(out["s_soft"].cpu().numpy().astype(np.complex128) * np.conj(q["s_soft"]))
-    assert np.abs(ph).max() < 2e-6, np.abs(ph).max()
+    record("s_soft phase rad", np.abs(ph).max(), 1e-6)
+    assert np.abs(ph).max() < 1e-6, np.abs(ph).max()
     dq = out["dq"].cpu().numpy()
     np.testing.assert_allclose(dq, q["dq"], rtol=2e-5, atol=1e-6 * q["dq"].max())
 
@@ -177,13 +172,13 @@ def test_transmit_chain_z_rho(mode):
     ctx = sqngd.Context(c)
     met, gz, gr = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
     ctx.sync()
-    assert rel(gz.cpu().numpy(), gz_ref) < 1e-4
-    assert rel(gr.cpu().numpy(), gr_ref) < 1e-4
+    check_grad(gz.cpu().numpy(), gz_ref, "grad_z")
+    check_grad(gr.cpu().numpy(), gr_ref, "grad_rho")
     # Step A flavour through (z, rho): s_hard then grad_w
     _, gw_ref, _ = O.loss_grad(c, q["s_hard"], w, want_s=False)
     met, gw = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_FILTERS)
     ctx.sync()
-    assert rel(gw.cpu().numpy(), gw_ref) < 1e-4
+    check_grad(gw.cpu().numpy(), gw_ref, "grad_w")
 
 
 def test_step_teacher_forced_and_invariants():
@@ -310,8 +305,8 @@ def test_correlation_mode_K1(mode):
     _, gs = ctx.loss_grad_s(T(s), T(w), sqngd.WRT_TRANSMIT)
     ctx.sync()
     _, gw_ref, gs_ref = O.loss_grad(c, s, w)
-    assert rel(gw.cpu().numpy(), gw_ref) < 1e-4
-    assert rel(gs.cpu().numpy(), gs_ref) < 1e-4
+    check_grad(gw.cpu().numpy(), gw_ref, "grad_w")
+    check_grad(gs.cpu().numpy(), gs_ref, "grad_s")
 
 
 @pytest.mark.parametrize("fuse", ["0", "1"])

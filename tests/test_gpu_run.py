@@ -19,20 +19,27 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-def rule(hist, patience):
-    """(stop iteration or None, best_iter [R], best_wpsl [R]) of the rule in include/sqngd.h."""
+def rule(hist, patience, lhist=None, tol=1e-6):
+    """(stop iteration or None, best_iter [R], best_wpsl [R]) of the rule in include/sqngd.h: an
+    improvement is a decrease of the hard WPSL by more than tol; stop when every restart
+    has `patience` iterations without one and (lhist given) its hard loss is below its value at the
+    last improvement ("further reduction of L does not lead to improvement in the WPSL")."""
     T, R = hist.shape
     best = np.full(R, math.inf)
     bi = np.zeros(R, int)
     stall = np.zeros(R, int)
+    lref = np.zeros(R)
     for t in range(1, T + 1):
         for r in range(R):
             v = hist[t - 1, r]
-            if v < best[r]:
+            if v < best[r] - tol:
                 best[r], bi[r], stall[r] = v, t, 0
+                if lhist is not None:
+                    lref[r] = lhist[t - 1, r]
             else:
                 stall[r] += 1
-        if patience > 0 and (stall >= patience).all():
+        dec = np.ones(R, bool) if lhist is None else lhist[t - 1] < lref
+        if patience > 0 and ((stall >= patience) & dec).all():
             return t, bi, best
     return None, bi, best
 
@@ -44,8 +51,9 @@ def setup(c, idx):
     return [torch.as_tensor(a, device=DEV) for a in (z, rho, w)]
 
 
-@pytest.mark.parametrize("patience,check_every", [(2, 1), (3, 4), (0, 1)])
-def test_run_rule_and_snapshot(patience, check_every):
+@pytest.mark.parametrize("patience,check_every,need_dec", [(2, 1, False), (3, 4, False), (0, 1, False), (2, 1, True),
+                                                        (3, 2, True)])
+def test_run_rule_and_snapshot(patience, check_every, need_dec):
     c = Cfg("run", M=2, N=32, B=4, K=9, f_lo=-0.5, f_hi=0.5, r_n=4, R=2, n_h=2, n_x=2, lr_w=0.3, lr_z=3e-2)
     T = 16
     ctx = sqngd.Context(c)
@@ -53,10 +61,13 @@ def test_run_rule_and_snapshot(patience, check_every):
     side = torch.cuda.Stream()
     with torch.cuda.stream(side):
         st = ctx.new_state(z, rho, w)
-        best, bw, bi, hist, res = ctx.run(st, T=T, patience=patience, check_every=check_every)
+        best, bw, bi, hist, res = ctx.run(st, T=T, patience=patience, check_every=check_every,
+                                          require_loss_decrease=need_dec)
     torch.cuda.synchronize()
     h = hist.cpu().numpy()
-    stop, bi_ref, bw_ref = rule(np.nan_to_num(h, nan=math.inf)[: res["iterations"]], patience)
+    lh = res["loss_hist"].cpu().numpy()
+    stop, bi_ref, bw_ref = rule(np.nan_to_num(h, nan=math.inf)[: res["iterations"]], patience,
+                                lh[: res["iterations"]] if need_dec else None)
     if patience > 0 and stop is not None:
         assert res["stopped"] and res["iterations"] == stop
         assert res["iterations"] <= res["steps_run"] <= res["iterations"] + check_every - 1

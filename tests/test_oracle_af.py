@@ -202,3 +202,24 @@ def test_roi_weights_and_lag_window():
     assert abs(met[0]["wapsl"] - 0.75) < 1e-14
     met, _, _ = O.af(cfg(N=N, tau_lo=2, tau_hi=3), one, one)
     assert abs(met[0]["wapsl"] - 0.5) < 1e-14
+
+
+def test_snrl_db_pins():
+    """O.snrl_db (Eq. 10) against SPEC's worked examples (h = x -> 0 dB,
+    h = 2x -> 0 dB, N = 2 x = [1,1] h = [1,0] -> 10 log10 2), Cauchy-Schwarz (>= 0, = 0 only for
+    h parallel to x) and the unimodular identity SNRL = -20 log10 p_m when ||x||^2 = ||h||^2 = N."""
+    g = golden_values("spec_examples.txt")
+    x = rnd(16, 3)
+    assert abs(O.snrl_db(x, x)) < 1e-12
+    assert abs(O.snrl_db(x, 2 * x)) < 1e-12
+    assert abs(O.snrl_db(x, (0.5 - 2j) * x)) < 1e-12
+    assert abs(O.snrl_db([1, 1], [1, 0]) - g["snrl_db_example"]) < 1e-4
+    for seed in range(5):
+        assert O.snrl_db(rnd(16, 10 + seed), rnd(16, 20 + seed)) > 0.0
+    assert O.snrl_db([1, 0], [0, 1]) == float("inf")
+    N = 32
+    s = np.exp(2j * np.pi * np.random.default_rng(4).random((1, 1, N)))
+    h = rnd((1, 1, N), 5)
+    h *= math.sqrt(N) / np.linalg.norm(h)
+    _, p, _ = O.af(cfg(N=N), s, h)
+    assert abs(O.snrl_db(s, h) + 20 * math.log10(p[0, 0])) < 1e-10
