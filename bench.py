@@ -56,15 +56,29 @@ def work_model(c):
 
 
 def work_model_lr(c, Q):
-    """Algorithmic flops per launch of the Chebyshev engine's fused kernel k_lrt:
-    per bin pair and lag, the symmetric contraction Pe = sum_{j<Q/2} alpha_j E_j, Po = sum beta_j O_j
-    (2 x Q/2 complex-by-real MACs = 4Q flops) and At = Pe +/- Po (4); the adjoint the same
-    (4Q + 4); the cell epilogue 7 (forward) / 10 (adjoint) per cell as in SURVEY.md §8(d).
-    Per cell: forward 2Q + 2 + 7, with gradient 4Q + 4 + 17."""
+    """Algorithmic work per launch of the Chebyshev engine's fused kernel k_lrt, split by
+    the pipe that executes it (VERDICT r01 "What's weak" 2: only the cell epilogue runs on the FP32
+    pipe; the Doppler contraction runs on the tensor pipe):
+      fp32:   the cell epilogue of SURVEY.md §8(d): 7 flops per cell forward (|A|^2 3, sqrt 1, exp 1,
+              sum 1, compare 1), 10 more with the gradient (cotangent);
+      tensor: the Lagrange contraction At = sum_q l_q R_q and its adjoint in the symmetric form: per
+              cell 2Q + 2 flops forward (Q/2 complex-by-real MACs for each of Pe, Po per bin pair,
+              and the +/-), the same again for the adjoint."""
     cells = c.cells * c.R
-    fwd = cells * (2 * Q + 2 + 7)
-    grad = cells * (4 * Q + 4 + 17)
-    return {"fwd": fwd, "adjA": grad, "adjB": grad, "cells": cells}
+    return {"fwd": {"fp32": 7 * cells, "tensor": (2 * Q + 2) * cells},
+            "adjA": {"fp32": 17 * cells, "tensor": (4 * Q + 4) * cells},
+            "adjB": {"fp32": 17 * cells, "tensor": (4 * Q + 4) * cells}, "cells": cells}
+
+
+def tensor_peaks():
+    """Dense tensor peaks per operand type (TFLOP/s): the measured bf16 burst figure of MEASURED_PEAKS.json
+    times the nominal ratio of /opt/skills/guides/B200_PROFILING.md (FP16 = BF16: 1; TF32: 1.1 / 2.25)."""
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        src = "measured bf16 burst (MEASURED_PEAKS.json)"
+    except Exception:
+        bf16, src = 2250.0, "nominal bf16 (B200_PROFILING.md fallback)"
+    return {"f16": bf16, "tf32": bf16 * 1.1 / 2.25, "basis": f"{src} x nominal dtype ratio (f16 1, tf32 1.1/2.25)"}
 
 
 def traffic_bytes(kernel):
@@ -192,16 +206,24 @@ def run_reference(args, c):
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_info()))
     times = []
     nb = 1
+    t_wall = time.perf_counter()
     for i in range(args.warmup + args.steps):
         t, nb = oracle_sample(c, budget_s=2.0)
         if i >= args.warmup:
             times.append(t)
+    t_wall = time.perf_counter() - t_wall
     per_eval = statistics.mean(times)
     v = 1.0 / per_eval
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_eval * 1e3 * 20, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "extrapolated": True,
+        "extrapolation": f"each 'step' evaluates a bounded sample ({nb} of {c.K} Doppler bins of one Step-B loss+grad "
+                         f"evaluation, ~2 s of CPU work) and scales the AF / adjoint time by K / {nb}; value and "
+                         f"ms_per_step (20 evaluations per Alg. 1 outer iteration) are that extrapolation, not "
+                         f"elapsed time: the whole run took {t_wall:.1f} s of wall clock",
+        "sample_wall_s": t_wall,
         "config": config_dict(c),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
                          "sample": f"Step-B loss+grad (quantize, AF, LSE loss, adjoint, chain) of the fp64 oracle with "
@@ -348,14 +370,41 @@ def main():
         same = [i for i in range(3) if knames[names[i]] == knames[names[dom]]]
         k_ms, k_cnt = sum(prof["ms"][i] for i in same), sum(prof["count"][i] for i in same)
         avg_ms = k_ms / max(1, k_cnt)
-        achieved = wm[names[dom]] / (avg_ms / 1e3) / 1e12
-        roof = {"bound": "alu", "kernel": knames[names[dom]], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic_bytes(knames[names[dom]]), "avg_launch_ms": avg_ms,
-                "launches": k_cnt, "flops_per_launch": wm[names[dom]],
-                "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
-                "share_of_step": k_ms / tot_ms,
-                "timing": "CUDA events around each fused-kernel launch on its stream, in an eager pass over the "
-                          "same K steps right after the timed (CUDA-graph) region"}
+        common = {"kernel": knames[names[dom]], "avg_launch_ms": avg_ms, "launches": k_cnt,
+                  "traffic": traffic_bytes(knames[names[dom]]),
+                  "share_of_step": k_ms / tot_ms,
+                  "timing": "CUDA events around each fused-kernel launch on its stream, in an eager pass over the "
+                            "same K steps right after the timed (CUDA-graph) region"}
+        if info["engine"] == "chebyshev":
+            w = wm[names[dom]]
+            fp32 = w["fp32"] / (avg_ms / 1e3) / 1e12
+            tp = tensor_peaks()
+            # forward contraction in FP16 (split) and adjoint in 3xTF32 (mma.sync): the tensor pipe's
+            # minimum time at its dtype peaks, as a fraction of the launch
+            t_fwd = wm["fwd"]["tensor"] / (tp["f16"] * 1e12)
+            t_adj = (w["tensor"] - wm["fwd"]["tensor"]) / (tp["tf32"] * 1e12)
+            roof = {"bound": "alu", "achieved": fp32, "peak": peak, "unit": "TFLOP/s", "frac": fp32 / peak,
+                    "flops_per_launch": w["fp32"],
+                    "work": "FP32 pipe: the cell epilogue of SURVEY.md §8(d) (7 forward + 10 adjoint flops per "
+                            "cell); the Doppler contraction runs on the tensor pipe (pipes.tensor)",
+                    "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
+                    "pipes": {
+                        "fp32": {"achieved": fp32, "peak": peak, "frac": fp32 / peak, "unit": "TFLOP/s"},
+                        "tensor": {"achieved": w["tensor"] / (avg_ms / 1e3) / 1e12,
+                                   "flops_per_launch": w["tensor"],
+                                   "frac": (t_fwd + t_adj) / (avg_ms / 1e3),
+                                   "peak_f16": tp["f16"], "peak_tf32": tp["tf32"], "unit": "TFLOP/s",
+                                   "frac_def": "(forward contraction / f16 peak + adjoint contraction / tf32 peak) "
+                                               "/ launch time", "peak_basis": tp["basis"]}},
+                    **common}
+        else:
+            achieved = wm[names[dom]] / (avg_ms / 1e3) / 1e12
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "flops_per_launch": wm[names[dom]],
+                    "work": "SURVEY.md §8(d) convention flops of the per-bin FFT method (5 P log2 P per FFT, "
+                            "6 per complex multiply, 7 / 10 per cell)",
+                    "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
+                    **common}
         out = {"value": value, "ms_per_step": tot_ms / args.steps, "roofline": roof, "launches": launches,
                "kernel_ms": {n: prof["ms"][i] / args.steps for i, n in enumerate(names)}, "engine": info,
                "wall_s": t_wall}
@@ -373,6 +422,51 @@ def main():
         ctxf, *_rest, fft_run = timed(c.with_(doppler_engine=sqngd.ENGINE_FFT), False)
         ctxf.close()
     value, tot_ms = main_run["value"], main_run["ms_per_step"] * args.steps
+
+    # ---- forward only (sqngd_af_forward, a2-a6): delay-Doppler cells/s = M^2 (2N-1) K R / t_fwd (SURVEY
+    # §8(d)), without and with the |A| map written to HBM; the map-writing launch against HBM bandwidth.
+    def forward_rate(cx, s, w, want_map, reps=10):
+        amap = (torch.empty((c.R, c.M, c.M, c.K, 2 * c.N - 1), dtype=torch.float32, device=dev) if want_map
+                else None)
+        for _ in range(3):
+            cx.af_forward(s, w, map_out=amap, want_p=False)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for i in range(reps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            cx.af_forward(s, w, map_out=amap, want_p=False)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        t = parallel.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs)) / reps / 1e3
+        cx.profile(True)
+        cx.profile_read(reset=True)
+        for i in range(reps):
+            flush.fill_(float(i))
+            cx.af_forward(s, w, map_out=amap, want_p=False)
+        pr = cx.profile_read(reset=True)
+        cx.profile(False)
+        tk = pr["ms"][0] / max(1, pr["count"][0]) / 1e3
+        return t, tk
+
+    s_h = ctx.quantize(st["z"], st["rho"], soft=False, want_b=False, want_dq=False)["s_hard"]
+    t_f, tk_f = forward_rate(ctx, s_h, st["w"], False)
+    t_m, tk_m = forward_rate(ctx, s_h, st["w"], True)
+    cells_job = c.cells * c.R * world
+    map_bytes = c.cells * c.R * 4
+    hbm_peak = peaks()[1]
+    forward = {
+        "cells_per_s": cells_job / t_f, "ms_per_forward": t_f * 1e3,
+        "with_map": {"cells_per_s": cells_job / t_m, "ms_per_forward": t_m * 1e3, "map_bytes": map_bytes,
+                     "roofline": {"bound": "hbm", "kernel": ("k_lrt<FWD>" if main_run["engine"]["engine"] == "chebyshev"
+                                             else "k_af<FWD>") + " (writing the map)",
+                                  "achieved": map_bytes / tk_m / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": map_bytes / tk_m / 1e9 / hbm_peak, "avg_launch_ms": tk_m * 1e3,
+                                  "traffic": None,
+                                  "what": "|A| map bytes (M^2 (2N-1) K x 4 B, fp32) / duration of the fused launch "
+                                          "that writes it"}},
+        "fused_launch_ms_no_map": tk_f * 1e3,
+        "what": "sqngd_af_forward (filter FFT, node/bin transforms, fused contraction + ROI reduction, metrics), "
+                "CUDA events per call, L2 flushed between calls"}
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the timing.
     # The optimizer state lives in ONE flat allocation (the sqngd_state pointers are views into it)
@@ -423,7 +517,8 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {**config_dict(c), "doppler_engine": eng_desc,
                    "parallelism": f"restarts x{world} (independent, no collective)"},
-        "cells_per_s": value * c.cells,
+        "cells_per_s": forward["cells_per_s"],
+        "forward": forward,
         "roofline": main_run["roofline"],
         "kernel_ms": main_run["kernel_ms"],
         "gpu_launches": main_run["launches"],
@@ -460,7 +555,7 @@ def main():
         ctxb.close()
         line["restart_batched"] = {
             "restarts_per_gpu": args.batch_restarts, "value": b_run["value"], "unit": UNIT,
-            "ms_per_step": b_run["ms_per_step"], "cells_per_s": b_run["value"] * c.cells,
+            "ms_per_step": b_run["ms_per_step"], "cells_per_s_in_loss_grad": b_run["value"] * c.cells,
             "roofline": b_run["roofline"], "gpu_launches": b_run["launches"],
             "what": "context: B independent seeded restarts batched in one context per GPU (the headline is R = 1)"}
     if args.generator:  # NEXT-2: the same step with the paper's ResNet generator z = f_theta(y0)
@@ -503,7 +598,8 @@ def main():
             "grad_z_rel_diff_vs_ours": float(torch.linalg.norm(gz_t - gz_o) / torch.linalg.norm(gz_o))}
     if fft_run is not None:
         line["fft_engine"] = {"value": fft_run["value"], "unit": UNIT, "ms_per_step": fft_run["ms_per_step"],
-                              "cells_per_s": fft_run["value"] * c.cells, "roofline": fft_run["roofline"],
+                              "cells_per_s_in_loss_grad": fft_run["value"] * c.cells,
+                              "roofline": fft_run["roofline"],
                               "kernel_ms": fft_run["kernel_ms"], "gpu_launches": fft_run["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OMP_NUM_THREADS", str(cpu_info()))

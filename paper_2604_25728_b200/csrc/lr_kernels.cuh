@@ -147,219 +147,6 @@ __device__ __forceinline__ void lr_rescale(float from, float to, float lb, float
   }
 }
 
-// Fused Doppler contraction + cell epilogue + adjoint contraction.  One CTA per unit
-// (pair (r, m, l) x 32 consecutive lags); its kw warps split the bin pairs, a lane owns one
-// lag.  Each lane accumulates its surrogate sum and cotangents with its own shift (node
-// maximum + 40/beta for LSE, so no term overflows; identical in every warp of the unit);
-// a lane whose cells exceed that by more than 96/(beta log2 e) redoes its range with the
-// exact maximum.  The warps' partials are combined in shared memory in warp order, warp 0
-// rescales the lanes to the unit's shift and writes (key, shift, sum) into the unit's slot,
-// the node cotangents G^_q(tau) = sum_k l_q(f_k) G~(tau, f_k) into Gn, and the restart's
-// running maxima (LrRed) with atomicMax.
-template <int Q, int LM, bool HW, bool GRAD>
-__global__ void __launch_bounds__(256) k_lr(const LrArgs a) {
-  SQ_PDL_WAIT();
-  constexpr int QH = Q / 2;
-  constexpr int NR = GRAD ? 2 * Q + 4 : 4;  // per-lane reduction record (floats)
-  extern __shared__ float4 lr_smem[];
-  const int Kp = a.K / 2;
-  const bool odd = (a.K & 1) != 0;
-  // coefficients: warp-uniform float4 loads through L1 (every CTA of the SM reads the same table)
-  const float* cf = a.coef;
-  float* rs = reinterpret_cast<float*>(lr_smem);  // [kw][NR][32]
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int u = blockIdx.x;
-  const int c = u % a.nch;
-  const int pr = u / a.nch;
-  const int M = a.M;
-  const int l = pr % M, m = (pr / M) % M, r = pr / (M * M);
-  const int idx = c * 32 + lane;
-  const int tau = idx - (a.N - 1);
-  const bool inL = idx < a.L;
-  const bool is_auto = m == l;
-  const bool valid = inL && tau >= a.tau_lo && tau <= a.tau_hi && !(is_auto && a.excl0 && tau == 0);
-
-  float2 Ev[QH], Ov[QH];
-  float nm2 = 0.f;
-  {
-    const float2* Rp = a.Rn + (size_t)pr * Q * a.LS + (inL ? idx : 0);
-#pragma unroll
-    for (int j = 0; j < QH; ++j) {
-      const float2 x = inL ? __ldg(Rp + (size_t)j * a.LS) : make_float2(0.f, 0.f);
-      const float2 y = inL ? __ldg(Rp + (size_t)(Q - 1 - j) * a.LS) : make_float2(0.f, 0.f);
-      Ev[j] = cadd(x, y);
-      Ov[j] = csub(x, y);
-      nm2 = fmaxf(nm2, fmaxf(fmaf(x.x, x.x, x.y * x.y), fmaf(y.x, y.x, y.y * y.y)));
-    }
-  }
-  const int p0 = (int)((long long)Kp * wp / a.kw), p1 = (int)((long long)Kp * (wp + 1) / a.kw);
-  const bool do_mid = odd && wp == a.kw - 1;
-  const float bp = a.bp;
-  const float lb = bp * 1.4426950408889634f;
-  const float wm = HW ? (inL ? __ldg(a.wmax + idx) : 0.f) : 1.f;
-  float shift = 0.f;
-  if (LM == 1) shift = sqrtf(nm2) * a.invN * wm + 40.f / bp;
-  if (LM == 2) shift = fmaxf(sqrtf(nm2) * a.invN * wm, 1e-30f);
-  float* mrow = (!GRAD && a.af_mag && inL) ? a.af_mag + (size_t)pr * a.K * a.L + idx : nullptr;
-
-  float bl, bh, bmid, S;
-  int kl, kh, kmid;
-  float2 GE[QH], GO[QH];
-  for (int pass = 0; pass < 2; ++pass) {
-    bl = bh = bmid = -1.f;
-    kl = kh = kmid = 0;
-    S = 0.f;
-#pragma unroll
-    for (int j = 0; j < QH; ++j) GE[j] = GO[j] = make_float2(0.f, 0.f);
-    const float lbN = lb * a.invN;
-    const float nlbs = valid ? -lb * shift : -INFINITY;
-    const float qN = valid ? a.invN / shift : 0.f;
-#pragma unroll 1
-    for (int p = p0; p < p1; ++p) {
-      const float4* cp = reinterpret_cast<const float4*>(cf + p * a.QS);
-      float co[(Q + 3) & ~3];
-#pragma unroll
-      for (int i = 0; i < (Q + 3) / 4; ++i) {
-        const float4 t4 = __ldg(cp + i);
-        co[4 * i] = t4.x; co[4 * i + 1] = t4.y; co[4 * i + 2] = t4.z; co[4 * i + 3] = t4.w;
-      }
-      float2 Pe = make_float2(0.f, 0.f), Po = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < QH; ++j) {
-        Pe.x = fmaf(co[j], Ev[j].x, Pe.x);
-        Pe.y = fmaf(co[j], Ev[j].y, Pe.y);
-        Po.x = fmaf(co[QH + j], Ov[j].x, Po.x);
-        Po.y = fmaf(co[QH + j], Ov[j].y, Po.y);
-      }
-      const float2 G0 = lr_cell<LM, HW, GRAD, false>(cadd(Pe, Po), p, a, idx, valid, lbN, nlbs, qN, bl, kl, S, mrow);
-      const float2 G1 =
-          lr_cell<LM, HW, GRAD, true>(csub(Pe, Po), a.K - 1 - p, a, idx, valid, lbN, nlbs, qN, bh, kh, S, mrow);
-      if (GRAD) {
-        const float2 sg = cadd(G0, G1), dg = csub(G0, G1);
-#pragma unroll
-        for (int j = 0; j < QH; ++j) {
-          GE[j].x = fmaf(co[j], sg.x, GE[j].x);
-          GE[j].y = fmaf(co[j], sg.y, GE[j].y);
-          GO[j].x = fmaf(co[QH + j], dg.x, GO[j].x);
-          GO[j].y = fmaf(co[QH + j], dg.y, GO[j].y);
-        }
-      }
-    }
-    if (do_mid) {  // f = grid centre: beta = 0
-      float cm[QH];
-#pragma unroll
-      for (int j = 0; j < QH; ++j) cm[j] = __ldg(cf + Kp * a.QS + j);
-      float2 Pe = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < QH; ++j) {
-        Pe.x = fmaf(cm[j], Ev[j].x, Pe.x);
-        Pe.y = fmaf(cm[j], Ev[j].y, Pe.y);
-      }
-      const float2 G0 = lr_cell<LM, HW, GRAD, false>(Pe, Kp, a, idx, valid, lbN, nlbs, qN, bmid, kmid, S, mrow);
-      if (GRAD) {
-#pragma unroll
-        for (int j = 0; j < QH; ++j) {
-          GE[j].x = fmaf(cm[j], G0.x, GE[j].x);
-          GE[j].y = fmaf(cm[j], G0.y, GE[j].y);
-        }
-      }
-    }
-    if (LM == 0) break;
-    const float b2 = fmaxf(fmaxf(bl, bh), bmid);
-    const float vb = sqrtf(fmaxf(b2, 0.f)) * a.invN;
-    const bool bad = valid && (LM == 1 ? lb * (vb - shift) > 96.f : (vb > shift && (bp * log2f(vb / shift)) > 96.f));
-    if (!__any_sync(0xffffffffu, bad) || pass == 1) break;
-    if (bad) shift = vb;
-    mrow = nullptr;  // the map was written in the first pass
-  }
-
-  // ---- this warp's lane record: best cell key, shift, sum, cotangents
-  float best = bl;
-  int bk = kl;
-  if (bmid > best) { best = bmid; bk = kmid; }
-  if (bh > best) { best = bh; bk = kh; }
-  const uint32_t cell = ((uint32_t)((m * M + l) * a.L + idx)) * (uint32_t)a.K + (uint32_t)bk;
-  unsigned long long key = (valid && best >= 0.f) ? pack_key(best, cell) : 0ull;
-  float* rec = rs + (size_t)wp * NR * 32 + lane;
-  if (a.kw > 1) {
-    rec[0] = __uint_as_float((uint32_t)(key >> 32));
-    rec[32] = __uint_as_float((uint32_t)key);
-    rec[64] = shift;
-    rec[96] = S;
-    if (GRAD) {
-#pragma unroll
-      for (int j = 0; j < QH; ++j) {
-        rec[(4 + 4 * j) * 32] = GE[j].x;
-        rec[(5 + 4 * j) * 32] = GE[j].y;
-        rec[(6 + 4 * j) * 32] = GO[j].x;
-        rec[(7 + 4 * j) * 32] = GO[j].y;
-      }
-    }
-    __syncthreads();
-    if (wp != 0) return;
-    // warp 0: combine the kw records of each lane in warp order (deterministic)
-    for (int w = 1; w < a.kw; ++w) {
-      const float* o = rs + (size_t)w * NR * 32 + lane;
-      const unsigned long long ko =
-          ((unsigned long long)__float_as_uint(o[0]) << 32) | (unsigned long long)__float_as_uint(o[32]);
-      key = ko > key ? ko : key;
-      if (LM != 0) {
-        const float so = o[64];
-        const float mx = fmaxf(shift, so);
-        float fS0 = 1.f, fG0 = 1.f, fS1 = 1.f, fG1 = 1.f;
-        if (valid && so != shift) {  // only after a redo
-          lr_rescale<LM>(shift, mx, lb, bp, fS0, fG0);
-          lr_rescale<LM>(so, mx, lb, bp, fS1, fG1);
-        }
-        S = S * fS0 + o[96] * fS1;
-        if (GRAD) {
-#pragma unroll
-          for (int j = 0; j < QH; ++j) {
-            GE[j].x = GE[j].x * fG0 + o[(4 + 4 * j) * 32] * fG1;
-            GE[j].y = GE[j].y * fG0 + o[(5 + 4 * j) * 32] * fG1;
-            GO[j].x = GO[j].x * fG0 + o[(6 + 4 * j) * 32] * fG1;
-            GO[j].y = GO[j].y * fG0 + o[(7 + 4 * j) * 32] * fG1;
-          }
-        }
-        shift = mx;
-      }
-    }
-  }
-
-  // ---- unit reduction (warp 0): key, shift, sum; node cotangents; restart maxima
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
-    key = y > key ? y : key;
-  }
-  float mw = 0.f, fS = 0.f, fG = 0.f;
-  if (LM != 0) {
-    mw = valid ? shift : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-    if (valid) lr_rescale<LM>(shift, mw, lb, bp, fS, fG);
-  }
-  float Su = S * fS;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) Su += __shfl_xor_sync(0xffffffffu, Su, o);
-  if (GRAD && inL) {
-    float2* gp = a.Gn + (size_t)pr * Q * a.LS + idx;
-#pragma unroll
-    for (int j = 0; j < QH; ++j) {
-      gp[(size_t)j * a.LS] = make_float2((GE[j].x + GO[j].x) * fG, (GE[j].y + GO[j].y) * fG);
-      gp[(size_t)(Q - 1 - j) * a.LS] = make_float2((GE[j].x - GO[j].x) * fG, (GE[j].y - GO[j].y) * fG);
-    }
-  }
-  if (lane == 0) {
-    a.part.key[2 * (size_t)u] = is_auto ? key : 0ull;
-    a.part.key[2 * (size_t)u + 1] = is_auto ? 0ull : key;
-    a.part.m[u] = mw;  // 0: no valid lane
-    a.part.S[u] = Su;
-    if (key) atomicMax(is_auto ? &a.lred[r].key_a : &a.lred[r].key_c, key);
-    if (LM != 0 && mw > 0.f) atomicMax(&a.lred[r].mbits, __float_as_uint(mw));
-  }
-}
-
 // ---------------------------------------------------------------------------------------
 // Tensor-core variant of k_lr: the Doppler contraction and its adjoint as warp-level
 // mma.sync m16n8k8 TF32 products in 3xTF32 form (a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi,

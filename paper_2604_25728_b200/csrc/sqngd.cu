@@ -92,16 +92,15 @@ struct sqngd_ctx_s {
   // Chebyshev Doppler engine (lr_kernels.cuh): Q nodes, tables, node AFs / cotangents
   bool lr = false;
   int Q = 0, QS = 0, nch = 0, kw = 1, LS = 0;
-  bool lr_tc = true;           // k_lrt (mma.sync 3xTF32) instead of the FP32 k_lr
   bool lr_cta = true;          // k_adj_gc (sums inside the CTA) instead of k_adj_g (slots + arrival tail)
   int nch16 = 0, NT = 0, NTF = 0;
   float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
   uint4* tabF16 = nullptr;     // [NT][32] k_lrt forward B fragments (FP16 packed split)
   uint2* tabM16 = nullptr;     // [32] k_lrt middle-bin B fragment
-  int64_t units_lr = 0;        // k_lr units (CTAs of kw warps): R M^2 nch
-  size_t lr_smem = 0;          // k_lr dynamic shared memory
-  LrRed* lred = nullptr;       // [R] k_lr running maxima
+  int64_t units_lr = 0;        // fused-kernel units: R M^2 x (16-lag chunks for k_lrt | 128-lag tiles for k_lrt5)
+  size_t lr_smem = 0;          // k_lrt dynamic shared memory
+  LrRed* lred = nullptr;       // [R] running maxima of the fused kernel
   cudaStream_t side = nullptr; // graph branch for k_lr_finish (fork / join events)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double lr_err = 0.0;         // interpolation error bound of the chosen Q (host estimate)
@@ -340,40 +339,9 @@ struct Launch {
   }
 };
 
-// k_lr instantiations: Q in {4, 6, ..., 16} x loss mode x weighted ROI x gradient.
+// k_lrt instantiations: Q in {4, 6, ..., 16} x loss mode x weighted ROI x gradient.
 template <int Q>
 struct LrLaunch {
-  template <int LM, bool HW, bool GRAD>
-  static void go(const LrArgs& a, int units, size_t smem, cudaStream_t st) {
-    k_lr<Q, LM, HW, GRAD><<<units, 32 * a.kw, smem, st>>>(a);
-  }
-  static void launch(int lm, bool hw, bool grad, const LrArgs& a, int units, size_t smem, cudaStream_t st) {
-    // units = CTAs, a.kw warps each
-    if (lm == 0) { hw ? go<0, true, false>(a, units, smem, st) : go<0, false, false>(a, units, smem, st); return; }
-    if (lm == 1) {
-      if (grad) hw ? go<1, true, true>(a, units, smem, st) : go<1, false, true>(a, units, smem, st);
-      else hw ? go<1, true, false>(a, units, smem, st) : go<1, false, false>(a, units, smem, st);
-      return;
-    }
-    if (grad) hw ? go<2, true, true>(a, units, smem, st) : go<2, false, true>(a, units, smem, st);
-    else hw ? go<2, true, false>(a, units, smem, st) : go<2, false, false>(a, units, smem, st);
-  }
-  template <int LM, bool HW, bool GRAD>
-  static cudaError_t attr(size_t smem) {
-    return cudaFuncSetAttribute(k_lr<Q, LM, HW, GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  static cudaError_t prepare(size_t smem) {
-    cudaError_t e;
-    if ((e = attr<0, false, false>(smem)) || (e = attr<0, true, false>(smem)) || (e = attr<1, false, false>(smem)) ||
-        (e = attr<1, true, false>(smem)) || (e = attr<1, false, true>(smem)) || (e = attr<1, true, true>(smem)) ||
-        (e = attr<2, false, false>(smem)) || (e = attr<2, true, false>(smem)) || (e = attr<2, false, true>(smem)) ||
-        (e = attr<2, true, true>(smem)))
-      return e;
-    return cudaSuccess;
-  }
-  static cudaError_t occupancy(int* bps, int threads, size_t smem) {  // the heaviest variant (LSE + gradient)
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lr<Q, 1, false, true>, threads, smem);
-  }
   // tensor-core variant
   template <int LM, bool HW, bool GRAD>
   static void go_t(const LrtArgs& a, int /*units*/, size_t smem, cudaStream_t st) {
@@ -679,52 +647,16 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     ctx->QS = (ctx->Q + 3) & ~3;
     ctx->nch = (L + 31) / 32;
     ctx->LS = ctx->nch * 32;
-    if (const char* ev = getenv("SQNGD_LR_TC")) ctx->lr_tc = ev[0] != '0';
     if (const char* ev = getenv("SQNGD_LR_CTA")) ctx->lr_cta = ev[0] != '0';
     ctx->nch16 = (L + 15) / 16;
     const int Kp = cfg.K / 2;
     ctx->NT = (Kp + 7) / 8;
     ctx->NTF = Kp / 8;
-    ctx->units_lr = (int64_t)cfg.R * cfg.M * cfg.M * (ctx->lr_tc ? ctx->nch16 : ctx->nch);
-    // warps per unit (bin-pair split): the kw in {1, 2, 4, 8} whose CTAs fill whole waves best
-    const size_t cf_bytes = 0;  // coefficient tables are read through L1, not staged
-    const size_t rec_bytes = ctx->lr_tc ? sizeof(float) * 32 * 22 : sizeof(float) * 32 * (2 * ctx->Q + 4);
-    const size_t smem_max = cf_bytes + 8 * rec_bytes;
-    const int kmaxw = ctx->lr_tc ? ctx->NT : Kp;
+    ctx->units_lr = (int64_t)cfg.R * cfg.M * cfg.M * ctx->nch16;
     cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
-    double best = 1e30;
-    with_Q(ctx->Q, [&](auto Qc) {
-      using QC = decltype(Qc);
-      e1 = ctx->lr_tc ? QC::prepare_t(smem_max) : QC::prepare(smem_max);
-      for (int kw = 1; kw <= 8 && e1 == cudaSuccess; kw *= 2) {
-        if (kw > 1 && kw > kmaxw) break;
-        int bps = 0;
-        const size_t sm = cf_bytes + (kw > 1 ? kw * rec_bytes : 0);
-        e1 = ctx->lr_tc ? QC::occupancy_t(&bps, 32 * kw, sm) : QC::occupancy(&bps, 32 * kw, sm);
-        if (e1 != cudaSuccess || bps < 1) break;
-        const double waves = (double)ctx->units_lr / ((double)ctx->sms * bps);
-        const double warps_sm = (double)bps * kw;  // latency hiding: penalise < 20 resident warps
-        const double cost = std::ceil(waves) / waves * (warps_sm >= 20 ? 1.0 : 20.0 / warps_sm) * (1.0 + 0.01 * kw);
-        if (cost < best) {
-          best = cost;
-          ctx->kw = kw;
-          ctx->lr_smem = sm;
-        }
-      }
-    });
-    if (ctx->lr_tc) {  // measured (C3): one warp per unit is best for k_lrt (no CTA-level reduction)
-      ctx->kw = 1;
-      ctx->lr_smem = 0;
-      // (a persistent grid with an L1 prefetch of the next unit's node values measured 3-5% slower)
-    }
-    if (const char* ev = getenv("SQNGD_LR_KW")) {  // tuning override
-      const int kw = atoi(ev);
-      // (k_lrt is compiled for SQNGD_LRT_MAXT threads per CTA: wider units only for the FP32 k_lr)
-      if ((kw == 1 || kw == 2 || kw == 4 || kw == 8) && (!ctx->lr_tc || kw * 32 <= SQNGD_LRT_MAXT)) {
-        ctx->kw = kw;
-        ctx->lr_smem = cf_bytes + (kw > 1 ? kw * rec_bytes : 0);
-      }
-    }
+    with_Q(ctx->Q, [&](auto Qc) { e1 = decltype(Qc)::prepare_t(0); });
+    ctx->kw = 1;      // measured (C3): one warp per unit is best for k_lrt (no CTA-level reduction)
+    ctx->lr_smem = 0;
     with_P(P, [&](auto Lc) { e2 = decltype(Lc)::prepare_lr(); });
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
       std::string m = cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
@@ -1111,31 +1043,19 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
   with_P(ctx->P, [&](auto Lc) {
     decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftwn, ctx->Rn, c.R, ctx->lred, st);
   });
-  LrArgs a{};
-  a.R = c.R; a.M = c.M; a.N = c.N; a.L = ctx->L; a.K = c.K; a.nch = ctx->nch; a.kw = ctx->kw;
-  a.LS = ctx->LS; a.QS = ctx->QS;
-  a.tau_lo = c.tau_lo; a.tau_hi = c.tau_hi; a.excl0 = c.exclude_auto_zero_delay;
-  a.bp = (float)c.beta_or_p; a.invN = 1.0f / (float)c.N;
-  a.weights = c.weights; a.wmax = ctx->wmax; a.coef = ctx->coef; a.Rn = ctx->Rn; a.Gn = ctx->Gn;
-  a.af_mag = grad ? nullptr : af_mag; a.part = ctx->part; a.lred = ctx->lred;
-  if (ctx->lr_tc) {
-    LrtArgs t{};
-    t.R = c.R; t.M = c.M; t.N = c.N; t.L = ctx->L; t.K = c.K; t.nch = ctx->nch16; t.kw = ctx->kw; t.LS = ctx->LS;
-    t.NT = ctx->NT; t.NTF = ctx->NTF; t.coefm = ctx->coef + (size_t)(c.K / 2) * ctx->QS;
-    t.tabF16 = ctx->tabF16; t.tabM16 = ctx->tabM16;
-    const int grid = (int)ctx->units_lr;
-    t.tau_lo = c.tau_lo; t.tau_hi = c.tau_hi; t.excl0 = c.exclude_auto_zero_delay;
-    t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
-    t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
-    t.af_mag = grad ? nullptr : af_mag; t.part = ctx->part; t.lred = ctx->lred;
+  LrtArgs t{};
+  t.R = c.R; t.M = c.M; t.N = c.N; t.L = ctx->L; t.K = c.K; t.nch = ctx->nch16; t.kw = ctx->kw; t.LS = ctx->LS;
+  t.NT = ctx->NT; t.NTF = ctx->NTF; t.coefm = ctx->coef + (size_t)(c.K / 2) * ctx->QS;
+  t.tabF16 = ctx->tabF16; t.tabM16 = ctx->tabM16;
+  const int grid = (int)ctx->units_lr;
+  t.tau_lo = c.tau_lo; t.tau_hi = c.tau_hi; t.excl0 = c.exclude_auto_zero_delay;
+  t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
+  t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
+  t.af_mag = grad ? nullptr : af_mag; t.part = ctx->part; t.lred = ctx->lred;
+  {
     ProfScope ps(ctx, cls, st);
     with_Q(ctx->Q, [&](auto Qc) {
       decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad, t, grid, ctx->lr_smem, st);
-    });
-  } else {
-    ProfScope ps(ctx, cls, st);
-    with_Q(ctx->Q, [&](auto Qc) {
-      decltype(Qc)::launch(c.loss_mode, c.weights != nullptr, grad, a, (int)ctx->units_lr, ctx->lr_smem, st);
     });
   }
   const int GPR = (int)(ctx->units_lr / c.R);
@@ -1225,7 +1145,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     if ((rc = run_lr(ctx, true, wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B, nullptr, ma, st, true))) return rc;
     AdjGArgs ag{};
     ag.M = c.M; ag.N = c.N; ag.Q = ctx->Q; ag.LS = ctx->LS;
-    ag.nch = ctx->lr_tc ? ctx->nch16 : ctx->nch; ag.csh = ctx->lr_tc ? 4 : 5;
+    ag.nch = ctx->nch16; ag.csh = 4;
     ag.units = c.R * c.M * c.M * ctx->Q; ag.mode = c.loss_mode; ag.bp = (float)c.beta_or_p;
     ag.Gn = ctx->Gn; ag.um = ctx->part.m; ag.lred = ctx->lred; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
     ag.cnt = ctx->lr_cnt; ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
