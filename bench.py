@@ -244,6 +244,60 @@ def config_dict(c):
 
 
 # --------------------------------------------------------------------------- GPU leg
+def work_sharded(args, world, rank, local, dev, stream, flush, name="C5"):
+    """BASELINE.json's C5 (M=16, N=4096, K=513, 8 restarts) as ONE problem over the N ranks: the library's
+    world > 1 mode (Chebyshev engine: each rank evaluates a slice of the R M (restart, transmit channel)
+    rows; one grouped NCCL all-reduce per loss+grad evaluation, captured in the step's CUDA graph).
+    value = loss+grad evals/s of the whole job (8 restarts x 20 per step / max-over-ranks step time)."""
+    import torch
+
+    from paper_2604_25728_b200 import sqngd
+
+    c = CF.CONFIGS[name].with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0)
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [sqngd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = sqngd.Context(c, device=local, nccl_uid=uid, rank=rank, world=world)
+    z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, r), c.M * c.N).reshape(c.M, c.N)
+                  for r in range(c.R)])
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
+    w = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"]
+    st = ctx.new_state(zt, rt, w)
+    steps, warm = max(2, min(args.steps, 5)), max(3, min(args.warmup, 3))
+    for _ in range(warm):
+        ctx.step(st, sqngd.BLOCK_AB)
+    ctx.sync()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(steps):
+        flush.fill_(float(i))
+        evs[i][0].record(stream)
+        ctx.step(st, sqngd.BLOCK_AB)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ctx.sync()
+    ms = parallel.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs)) / steps
+    info = ctx.engine_info()
+    ctx.close()
+    evals = (c.n_h + c.n_x) * c.R
+    return {"workload": f"{name}: M={c.M} N={c.N} L={c.B} K={c.K} R={c.R} (one problem)", "n_gpus": world,
+            "value": evals / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
+            "scaling": "strong", "engine": info["engine"],
+            "parallelism": f"work-sharded x{world}: (restart, transmit channel) rows, one grouped NCCL "
+                           f"all-reduce per loss+grad evaluation" if world > 1 else "1 GPU",
+            "what": "sqngd_step(A+B) of the 8-restart C5 problem; the driver's N=1 line carries the same "
+                    "block for the parallel-efficiency ratio"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -259,6 +313,8 @@ def main():
                     help="skip the torch.fft + autograd comparator line")
     ap.add_argument("--restarts", type=int, default=0,
                     help="independent restarts batched per GPU (default: the config's R)")
+    ap.add_argument("--no-work-sharded", dest="work_sharded", action="store_false",
+                    help="skip the work-sharded C5 line (one problem split over the N ranks)")
     ap.add_argument("--batch-restarts", type=int, default=4,
                     help="also time the config with this many restarts per GPU (context line; 0/1: skip)")
     args = ap.parse_args()
@@ -550,6 +606,8 @@ def main():
     line["breakdown"] = {**breakdown, "unit": UNIT,
                          "what": "Step A only (filters), Step B only (transmit), and the MAX loss (Eq. 37, O(N) "
                                  "subgradient adjoint) instead of LSE; each 10 graph-replayed steps"}
+    if args.work_sharded:  # C5 (8 restarts) with its pair / Doppler work sharded over the N ranks
+        line["work_sharded"] = work_sharded(args, world, rank, local, dev, stream, flush)
     if args.batch_restarts > 1 and c.R == 1:  # the same config with B independent restarts per GPU
         ctxb, *_rest, b_run = timed(c.with_(R=args.batch_restarts), False)
         ctxb.close()

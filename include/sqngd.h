@@ -94,9 +94,9 @@ typedef struct {
               Doppler nodes of [f_lo, f_hi], then the K-bin AF by the dense (K x Q)
               Lagrange contraction fused with the cell epilogue, and its adjoint;
               O(M^2 Q) transforms.  |A| is reproduced to lr_tol * ||s|| ||w|| (DESIGN.md
-              §3 "Chebyshev engine").  Single GPU only (world == 1).
-   AUTO:      CHEBYSHEV when world == 1 and the node count Q for lr_tol is <= 16 and
-              <= K/3 (narrow grids such as the paper's [-0.5, 0.5]); FFT otherwise. */
+              §3 "Chebyshev engine").
+   AUTO:      CHEBYSHEV when the node count Q for lr_tol is <= 16 and <= K/3 (narrow grids such
+              as the paper's [-0.5, 0.5]); FFT otherwise. */
 enum { SQNGD_ENGINE_AUTO = 0, SQNGD_ENGINE_FFT = 1, SQNGD_ENGINE_CHEBYSHEV = 2 };
 
 /* One per restart, written by the library into caller-owned DEVICE memory. */
@@ -136,9 +136,26 @@ typedef struct {
 
 /* Build the context: validates the config (SQNGD_E_INVALID), builds the fp64
    Doppler twiddle table and the workspace on `cuda_device`.  nccl_unique_id:
-   NULL for one GPU, else 128 bytes of an ncclUniqueId shared by all ranks. */
+   NULL for one GPU, else 128 bytes of an ncclUniqueId shared by all ranks.
+   Multi-GPU (world > 1): each rank evaluates a shard -- the FFT engine
+   a contiguous slice of the R M K (restart, channel, bin) units, the Chebyshev engine a contiguous slice
+   of the R M (restart, transmit channel) rows -- and every loss / gradient evaluation ends with ONE
+   grouped NCCL call (SUM of the fp64 [weighted S | weighted gradient] payload, MAX of the u64 keys,
+   against a reference shift all ranks share), after which every rank holds the full outputs and
+   applies the identical optimizer step.  sqngd_step captures the NCCL call into its CUDA graph. */
 sqngd_status sqngd_create(const sqngd_config* cfg, int cuda_device, const void* nccl_unique_id,
                           int rank, int world, sqngd_ctx* out);
+
+/* Single-device stand-in for NCCL (tests): a group of `world` (2..8) contexts in ONE process on the same
+   device, each driven by its own host thread; the grouped collective is a host barrier plus one
+   reduction kernel on the last-arriving rank's stream, ordered by CUDA events (no kernel waits on
+   another rank's kernel).  The contexts run the exact sharded path of world > 1; sqngd_step does not
+   capture a graph for them.  Destroy the group after its contexts. */
+typedef struct sqngd_loopback_s* sqngd_loopback;
+sqngd_loopback sqngd_loopback_create(int world); /* NULL if world is outside 2..8 */
+void sqngd_loopback_destroy(sqngd_loopback group);
+sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqngd_loopback group, int rank,
+                                   sqngd_ctx* out);
 void sqngd_destroy(sqngd_ctx ctx);
 /* Message for the last non-OK status (ctx may be NULL: last create error). */
 const char* sqngd_last_error(sqngd_ctx ctx);

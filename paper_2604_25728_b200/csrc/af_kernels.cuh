@@ -296,7 +296,7 @@ __device__ __forceinline__ void slice_terms(float2 (&v)[PL::E], const SliceCtx& 
 // a3: X_{m,k} = FFT_P(s_m e^{j 2 pi n f_k / N}) for every unit (r, m, k) -> X cache.
 template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB)
-    k_xhat(int units, int M, int N, int K, const float2* __restrict__ s, const float2* __restrict__ dtw,
+    k_xhat(int u0, int units, int M, int N, int K, const float2* __restrict__ s, const float2* __restrict__ dtw,
            const float2* __restrict__ ftw, float2* __restrict__ Xc, const float2* __restrict__ w, double2* cm) {
   SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   gops.redk = reinterpret_cast<unsigned long long*>(gsm + FftSmem<PL>::XBUF + 32);
   gops.par = 0;
   gops.t = t;
-  const int uu = u < units ? u : units - 1;
+  const int uu = u0 + (u < units ? u : units - 1);  // units [u0, u0 + units): this rank's shard
   const int k = uu % K, rm = uu / K;
   const float2* sr = s + (size_t)rm * N;
   const float2* twr = dtw + (size_t)k * N;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   int par = 0;
   fft<PL, -1>(v, ftw, xbuf, t, par, gops.sync);
   if (u >= units) return;
-  float2* out = Xc + (size_t)u * P;
+  float2* out = Xc + (size_t)uu * P;
 #pragma unroll
   for (int i = 0; i < E; ++i) out[t + i * T] = v[i];
 }

@@ -50,7 +50,7 @@ struct LrRed {
 // (Eq. 36, Q1), stored at Rn[((r M + m) M + l) Q + q][tau + N - 1].
 template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB)
-    k_node(int units, int M, int Q, int N, int LS, const float2* __restrict__ Xc, const float2* __restrict__ H,
+    k_node(int u0, int units, int M, int Q, int N, int LS, const float2* __restrict__ Xc, const float2* __restrict__ H,
            const float2* __restrict__ ftw, float2* __restrict__ Rn, int R, LrRed* lred) {
   SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   GroupSync sync{1 + grp, T, group_mask(T)};
   if (blockIdx.x == 0)  // this evaluation's k_lr maxima
     for (int i = threadIdx.x; i < R; i += blockDim.x) lred[i] = LrRed{0u, 0u, 0ull, 0ull};
-  const int uu = u < units ? u : units - 1;
+  const int uu = u0 + (u < units ? u : units - 1);  // units [u0, u0 + units): this rank's rows
   const int q = uu % Q, pr = uu / Q;  // pr = (r M + m) M + l
   const int l = pr % M, rm = pr / M, r = rm / M;
   const float2* X = Xc + ((size_t)rm * Q + q) * P;
@@ -161,6 +161,7 @@ __device__ __forceinline__ void lr_rescale(float from, float to, float lb, float
 // the CUDA cores by the last warp of the unit.
 struct LrtArgs {
   int R, M, N, L, K, nch, kw, LS, NT, NTF;  // nch: 16-lag chunks; NT: 8-pair tiles of the K/2 bin pairs; NTF: full ones
+  int row0;                                 // first (restart, transmit channel) row of this rank's shard
   int tau_lo, tau_hi, excl0;
   float bp, invN;
   const float* weights;  // [K][L] or nullptr
@@ -255,11 +256,14 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int g = lane >> 2, cq = lane & 3;
   // grid (chunk, m M + l, restart): no integer divisions by runtime sizes
+  // grid (chunk, l, row - row0): row = r M + m is this rank's (restart, transmit channel) row
   const int ch = blockIdx.x;
-  const int pr = (blockIdx.z * a.M * a.M) + blockIdx.y;
+  const int rm = a.row0 + (int)blockIdx.z;
+  const int pr = rm * a.M + blockIdx.y;
   const int u = pr * a.nch + ch;
   const int M = a.M;
-  const int m = blockIdx.y / M, l = blockIdx.y - m * M;
+  const int rr_ = rm / M;
+  const int m = rm - rr_ * M, l = blockIdx.y;
   const bool is_auto = m == l;
   int idx[2];
   bool inL[2], valid[2];
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     a.part.key[2 * (size_t)u + 1] = is_auto ? 0ull : key;
     a.part.m[u] = mw;
     a.part.S[u] = Su;
-    const int r = blockIdx.z;
+    const int r = rr_;
     if (key) atomicMax(is_auto ? &a.lred[r].key_a : &a.lred[r].key_c, key);
     if (LM != 0 && mw > 0.f) atomicMax(&a.lred[r].mbits, __float_as_uint(mw));
   }
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
 
 // Per restart: the global shift m (LrRed), S = sum_u S_u (m_u -> m), the reduction record
 // and the metrics (a6).  One block per restart, fixed order (deterministic).
-__global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int mode, double bp, Part part,
+__global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int g_lo, int g_hi, int mode, double bp, Part part,
                                                     const LrRed* __restrict__ lred, Red* red, MetricsArgs ma,
                                                     int* status) {
   SQ_PDL_WAIT();
@@ -671,8 +675,9 @@ __global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int mode, double bp
   if (mode != 0 && mf > 0.f) {
     const float* Sp = part.S + (size_t)r * GPR;
     const float* mp = part.m + (size_t)r * GPR;
+    const int glo = max(0, g_lo - r * GPR), ghi = min(GPR, g_hi - r * GPR);  // this rank's units
 #pragma unroll 4
-    for (int g = threadIdx.x; g < GPR; g += blockDim.x) {
+    for (int g = glo + threadIdx.x; g < ghi; g += blockDim.x) {
       const float Sg = __ldcg(Sp + g), mg = __ldcg(mp + g);
       float fS = 0.f, fG;
       if (mode == 1) lr_rescale<1>(mg, mf, lb, (float)bp, fS, fG);
@@ -694,26 +699,25 @@ __global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int mode, double bp
 
 struct AdjGArgs {
   int M, N, Q, LS, nch, csh, units, mode;  // csh: log2 of the k_lr unit's lag chunk (5 or 4)
+  int row_lo, row_hi;    // this rank's (restart, transmit channel) rows; other rows contribute zeros
+  int u0;                // k_adj_gc: first CTA unit of the shard
   float bp;
   const float2* Gn;      // node cotangents (unit-scaled)
   const float* um;       // per k_lr unit: its shift (part.m)
   const LrRed* lred;     // per restart: the global shift
   const float2* Xc;      // [R][M][Q][P] node spectra X~ (Step A)
   const float2* H;       // [R][M][P] filter spectra / P (Step B)
-  float2* out;           // [units][P] spectral partials
-  // Step B: the last of the M groups of a node (r, m, q) to finish sums their partials over l
-  // (fixed order), transforms back and demodulates (used when SQNGD_LR_CTA=0; else k_adj_gc).
-  int* cnt;              // [R M Q] arrival counters (zero between launches: the last group resets)
-  const float2* Vt;      // [Q][N] node modulation
+  float2* out;           // Step A: [units][P] spectral partials
+  const float2* Vt;      // [Q][N] node modulation (Step B)
   float2* tslot;         // [R M Q][NS] time-domain node partials
   int NS;
 };
 
-// Node adjoint correlations, one transform per unit:
-//   G^_{ml,q} = FFT_P(G^ placed at (-tau) mod P) (rescaled to the restart's shift), then
-//   Step B (WRT 2), unit ((r M + m) Q + q) M + l:  out = G^ . H_l            (sum over l: the last group)
-//   Step A (WRT 1), unit ((r M + l) M + m) Q + q:  out = X~_{m,q} . conj(G^)  (sum over m, q: combine)
-template <class PL, int G, int MINB, int WRT>
+// Step-A node adjoint correlations, one transform per unit ((r M + l) M + m) Q + q:
+//   out = X~_{m,q} . conj(FFT_P(G^_{ml,q} placed at (-tau) mod P))   (rescaled to the restart's shift);
+// the combine sums the M Q slots of filter row (r, l).  Units of rows (r, m) outside this rank's shard
+// write zero slots (multi-GPU, the all-reduce adds the other ranks' rows).
+template <class PL, int G, int MINB>
 __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, const float2* __restrict__ ftw) {
   SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
@@ -724,23 +728,22 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
   GroupSync sync{1 + grp, T, group_mask(T)};
   const int uu = u < a.units ? u : a.units - 1;
   const int M = a.M, Q = a.Q, N = a.N;
-  int r, m, l, q;
-  if (WRT == 2) {
-    l = uu % M;
-    const int rest = uu / M;
-    q = rest % Q;
-    const int rm = rest / Q;
-    m = rm % M;
-    r = rm / M;
-  } else {
-    q = uu % Q;
-    const int rest = uu / Q;
-    m = rest % M;
-    const int rl = rest / M;
-    l = rl % M;
-    r = rl / M;
+  const int q = uu % Q;
+  const int rest = uu / Q;
+  const int m = rest % M;
+  const int rl = rest / M;
+  const int l = rl % M;
+  const int r = rl / M;
+  const int row = r * M + m;
+  if (row < a.row_lo || row >= a.row_hi) {  // (uniform over the group)
+    if (u < a.units) {
+      float2* out = a.out + (size_t)uu * P;
+#pragma unroll
+      for (int i = 0; i < E; ++i) out[t + i * T] = make_float2(0.f, 0.f);
+    }
+    return;
   }
-  const int pr = (r * M + m) * M + l;
+  const int pr = row * M + l;
   const float2* Gp = a.Gn + ((size_t)pr * Q + q) * a.LS;
   const float* ump = a.um + (size_t)pr * a.nch;
   const float mf = __uint_as_float(a.lred[r].mbits);
@@ -768,7 +771,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
   float2 hx[E];  // the spectrum the transform is multiplied with, fetched while the FFT runs (the
                  // output stores below would otherwise serialize one load round trip per element)
   {
-    const float2* HX = WRT == 2 ? a.H + ((size_t)r * M + l) * P : a.Xc + (((size_t)r * M + m) * Q + q) * P;
+    const float2* HX = a.Xc + ((size_t)row * Q + q) * P;
 #pragma unroll
     for (int i = 0; i < E; ++i) hx[i] = __ldg(HX + t + i * T);
   }
@@ -776,56 +779,15 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
   fft<PL, -1>(v, ftw, xbuf, t, par, sync);
   if (u >= a.units) return;
   float2* out = a.out + (size_t)uu * P;
-  if (WRT == 2) {
 #pragma unroll
-    for (int i = 0; i < E; ++i) out[t + i * T] = cmul(v[i], hx[i]);
-    // arrival: the last group of node (r, m, q) does the tail
-    int* flag = reinterpret_cast<int*>(xbuf + FftSmem<PL>::XBUF);
-    const int node = uu / M;
-    __threadfence();
-    sync();
-    if (t == 0) {
-      const int old = atomicAdd(a.cnt + node, 1);
-      flag[0] = old == M - 1;
-      if (old == M - 1) a.cnt[node] = 0;
-    }
-    sync();
-    if (!flag[0]) return;
-    __threadfence();
-    const float2* sp = a.out + (size_t)node * M * P;
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = make_float2(0.f, 0.f);
-    for (int ll = 0; ll < M; ++ll) {
-#pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = cadd(v[i], __ldcg(sp + (size_t)ll * P + t + i * T));
-    }
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i].y = -v[i].y;
-    fft<PL, -1>(v, ftw, xbuf, t, par, sync);  // v = conj(e), e = IFFT_P(sum_l G^ H_l)
-    const float2* vr = a.Vt + (size_t)q * N;
-    float2* o = a.tslot + (size_t)node * a.NS;
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int n = t + i * T;
-      if (n < N) {
-        const float2 z = cmul(v[i], __ldg(vr + n));
-        o[n] = make_float2(z.x, -z.y);  // e conj(V_q)
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i) out[t + i * T] = cmulc(hx[i], v[i]);
-  }
+  for (int i = 0; i < E; ++i) out[t + i * T] = cmulc(hx[i], v[i]);
 }
 
-// Node adjoints with the sum inside the CTA: NG groups of one CTA share one output unit and
-// split its inner index; their accumulators are summed in shared memory in group order
-// (deterministic), so the partial slots and the per-node arrival tail disappear.
-//   Step B (WRT 2), CTA = node (r, m, q):  e = IFFT_P(sum_l FFT(G^_{ml,q}) H_l),
-//            tslot[node][n] = e(n) conj(V_q(n))      (groups split l)
-//   Step A (WRT 1), CTA = (r, l, m):       out[(r l) m] = sum_q X~_{m,q} conj(FFT(G^_{ml,q}))
-//                                          (groups split q; the combine sums the M slots of row l)
-template <class PL, int NG, int WRT>
+// Step-B node adjoints with the sum over l inside the CTA: NG groups of one CTA split l and their
+// accumulators are summed in shared memory in group order (deterministic).  CTA = node (r, m, q)
+// (u0 + blockIdx.x: this rank's rows):
+//   e = IFFT_P(sum_l FFT(G^_{ml,q}) H_l),   tslot[node][n] = e(n) conj(V_q(n)).
+template <class PL, int NG>
 __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const float2* __restrict__ ftw) {
   SQ_PDL_WAIT();
   constexpr int E = PL::E, T = PL::T, P = PL::P;
@@ -834,20 +796,17 @@ __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const fl
   float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
   GroupSync sync{1 + grp, T, group_mask(T)};
   const int M = a.M, Q = a.Q, N = a.N;
-  const int u = blockIdx.x;
-  int r, m = 0, l = 0, q = 0;
-  if (WRT == 2) { q = u % Q; const int rm = u / Q; m = rm % M; r = rm / M; }
-  else { m = u % M; const int rl = u / M; l = rl % M; r = rl / M; }
+  const int u = a.u0 + blockIdx.x;
+  const int q = u % Q, rm = u / Q;
+  const int r = rm / M;
   const float mf = __uint_as_float(a.lred[r].mbits);
   const float lb = a.bp * 1.4426950408889634f;
-  const int nin = WRT == 2 ? M : Q;  // inner index: l (Step B) or q (Step A)
   float2 acc[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
   int par = 0;
-  for (int it = grp; it < nin; it += NG) {
-    if (WRT == 2) l = it; else q = it;
-    const int pr = (r * M + m) * M + l;
+  for (int l = grp; l < M; l += NG) {
+    const int pr = rm * M + l;
     const float2* Gp = a.Gn + ((size_t)pr * Q + q) * a.LS;
     const float* ump = a.um + (size_t)pr * a.nch;
     float2 v[E];
@@ -871,17 +830,12 @@ __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const fl
       v[i] = make_float2(v[i].x * fG, v[i].y * fG);
     }
     float2 hx[E];  // the spectrum the transform is multiplied with, fetched while the FFT runs
-    const float2* HX = WRT == 2 ? a.H + ((size_t)r * M + l) * P : a.Xc + (((size_t)r * M + m) * Q + q) * P;
+    const float2* HX = a.H + ((size_t)r * M + l) * P;
 #pragma unroll
     for (int i = 0; i < E; ++i) hx[i] = __ldg(HX + t + i * T);
     fft<PL, -1>(v, ftw, xbuf, t, par, sync);
-    if (WRT == 2) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], hx[i]));
-    } else {
-#pragma unroll
-      for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmulc(hx[i], v[i]));
-    }
+    for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(v[i], hx[i]));
   }
   // fixed-order sum of the groups' accumulators (the exchange buffers are free now)
   __syncthreads();
@@ -895,12 +849,6 @@ __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const fl
     const float2* ob = reinterpret_cast<float2*>(smem_raw) + g * (FftSmem<PL>::TOTAL);
 #pragma unroll
     for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], ob[t + i * T]);
-  }
-  if (WRT == 1) {
-    float2* out = a.out + (size_t)u * P;
-#pragma unroll
-    for (int i = 0; i < E; ++i) out[t + i * T] = acc[i];
-    return;
   }
 #pragma unroll
   for (int i = 0; i < E; ++i) acc[i].y = -acc[i].y;

@@ -1062,4 +1062,106 @@ __global__ void __launch_bounds__(256) k_snrl(int M, int N, const float2* __rest
   if (threadIdx.x == 0 && met) met[r].snrl_db_max = worst;
 }
 
+// ------------------------------------------------------------------ a10 multi-GPU (comm.h)
+// c_m = sum_n s_m(n) conj(w_m(n)) (fp64) for every row: the sharded forward computes it only for the rows
+// it owns, but the metrics and the SNRL term need all of them on every rank.  One warp per row.
+__global__ void k_cm_rows(int RM, int N, const float2* __restrict__ s, const float2* __restrict__ w, double2* cm) {
+  SQ_PDL_WAIT();
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= RM) return;
+  const float2* sr = s + (size_t)row * N;
+  const float2* wr = w + (size_t)row * N;
+  double cr = 0.0, ci = 0.0;
+  for (int n = lane; n < N; n += 32) {
+    const float2 a = __ldg(sr + n), b = __ldg(wr + n);
+    cr += (double)a.x * b.x + (double)a.y * b.y;
+    ci += (double)a.y * b.x - (double)a.x * b.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+    ci += __shfl_xor_sync(0xffffffffu, ci, o);
+  }
+  if (lane == 0) cm[row] = make_double2(cr, ci);
+}
+
+struct WorldArgs {
+  int R, M, N, mode, with_grad;
+  double bp;
+  Red* red;                   // per restart: local (m, S, keys) in, global out
+  double* mref;               // [R] reference shift, identical on every rank
+  float2* grad;               // [R][M][N] local normalised gradient partial in, global out (or nullptr)
+  double* pay;                // [R][1 + 2 M N]
+  unsigned long long* key;    // [R][3]: key_a, key_c, bits(m_r)
+};
+
+__device__ __forceinline__ void world_weights(const WorldArgs& a, int r, double& wS, double& wG, double& m) {
+  const Red rr = a.red[r];
+  m = rr.m;
+  wS = wG = 0.0;
+  if (a.mode == 0 || !(rr.S > 0.0) || !(rr.m > -INFINITY)) return;
+  const double mr = a.mref[r];
+  if (a.mode == 1) {
+    wS = wG = exp(a.bp * (rr.m - mr)) * rr.S;
+  } else {
+    const double rho = rr.m / mr;
+    wS = pow(rho, a.bp) * rr.S;
+    wG = pow(rho, a.bp - 1.0) * pow(rr.S, 1.0 - 1.0 / a.bp);
+  }
+}
+
+// Pack: grid (blocks, R); block (0, r) writes the scalars, every block a slice of the weighted gradient.
+__global__ void __launch_bounds__(256) k_world_pack(WorldArgs a) {
+  SQ_PDL_WAIT();
+  const int r = blockIdx.y;
+  double wS, wG, m;
+  world_weights(a, r, wS, wG, m);
+  const size_t n = a.with_grad ? (size_t)2 * a.M * a.N : 0, stride = 1 + n;
+  double* p = a.pay + (size_t)r * stride;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p[0] = wS;
+    const Red rr = a.red[r];
+    a.key[3 * r] = rr.key_a;
+    a.key[3 * r + 1] = rr.key_c;
+    a.key[3 * r + 2] = (rr.m > 0.0) ? (unsigned long long)__double_as_longlong(rr.m) : 0ull;  // m >= 0: bits order
+    if (!isfinite(wS) || !isfinite(wG)) p[0] = INFINITY;  // fp64 weight overflow (beta |m_r - m_ref| > ~700)
+  }
+  const float* g = reinterpret_cast<const float*>(a.grad) + (size_t)r * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[1 + i] = wG * (double)g[i];
+}
+
+// Unpack: the global record (m = m_ref, S = sum wS, max keys) and the normalised global gradient; block
+// (0, r) then advances m_ref to the global maximum of the ranks' shifts for the next evaluation.
+__global__ void __launch_bounds__(256) k_world_unpack(WorldArgs a, int* status) {
+  SQ_PDL_WAIT();
+  const int r = blockIdx.y;
+  const size_t n = a.with_grad ? (size_t)2 * a.M * a.N : 0, stride = 1 + n;
+  const double* p = a.pay + (size_t)r * stride;
+  const double S = p[0];
+  double norm = 0.0;
+  if (a.mode != 0 && S > 0.0) norm = a.mode == 1 ? 1.0 / S : pow(S, 1.0 / a.bp - 1.0);
+  float* g = reinterpret_cast<float*>(a.grad) + (size_t)r * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    g[i] = (float)(p[1 + i] * norm);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double mr = a.mref[r];
+    Red rr;
+    rr.m = (a.mode != 0 && S > 0.0) ? mr : -INFINITY;
+    rr.S = a.mode != 0 ? S : 0.0;
+    rr.key_a = a.key[3 * r];
+    rr.key_c = a.key[3 * r + 1];
+    a.red[r] = rr;
+    if (!isfinite(S)) atomicOr(status, ST_NONFINITE);
+    const unsigned long long mb = a.key[3 * r + 2];
+    if (mb && a.mode != 0) a.mref[r] = __longlong_as_double((long long)mb);
+  }
+}
+
+// Reference shifts at create: 0 (LSE) or 1 (p-norm); v = w |A| / N is O(1).
+__global__ void k_world_init(int R, int mode, double* mref) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) mref[r] = mode == 2 ? 1.0 : 0.0;
+}
+
 }  // namespace sq

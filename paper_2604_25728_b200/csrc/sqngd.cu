@@ -92,7 +92,6 @@ struct sqngd_ctx_s {
   // Chebyshev Doppler engine (lr_kernels.cuh): Q nodes, tables, node AFs / cotangents
   bool lr = false;
   int Q = 0, QS = 0, nch = 0, kw = 1, LS = 0;
-  bool lr_cta = true;          // k_adj_gc (sums inside the CTA) instead of k_adj_g (slots + arrival tail)
   int nch16 = 0, NT = 0, NTF = 0;
   float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
@@ -110,8 +109,12 @@ struct sqngd_ctx_s {
   float2* Rn = nullptr;        // [R M M][Q][LS] node AFs
   float2* Gn = nullptr;        // [R M M][Q][LS] node cotangents
   float2* tslot = nullptr;     // [R M Q][N] Step-B node time-domain partials
-  int* lr_cnt = nullptr;       // [R M Q] k_adj_g arrival counters
-  Comm comm;
+  // multi-GPU (comm.h): this rank's shard, the grouped collective's buffers, the reference shifts
+  Comm* comm = nullptr;
+  int row_lo = 0, row_hi = 0;   // Chebyshev engine: (restart, transmit channel) rows [row_lo, row_hi)
+  double* pay = nullptr;        // [R][1 + 2 M N] fp64 SUM payload
+  unsigned long long* keyb = nullptr;  // [R][3] u64 MAX payload
+  double* mref = nullptr;       // [R] reference shift (previous evaluation's global maximum)
   void* run_dev = nullptr;     // sqngd_run bookkeeping (run.cu), reused across calls
   void* run_host = nullptr;    // pinned stop-flag mirror
   size_t run_dev_bytes = 0, run_host_bytes = 0;
@@ -266,15 +269,15 @@ struct Launch {
     const int blocks = (RM + G - 1) / G;
     k_filter_fft<PL, G><<<blocks, THREADS, smem_fft(), st>>>(RM, N, w, ftw, H, s, cm);
   }
-  static void xhat(int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftw, float2* Xc,
-                   const float2* w, double2* cm, cudaStream_t st) {
+  static void xhat(int u0, int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftw,
+                   float2* Xc, const float2* w, double2* cm, cudaStream_t st) {
     const int blocks = (units + G - 1) / G;
-    k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(units, M, N, K, s, dtw, ftw, Xc, w, cm);
+    k_xhat<PL, G, MINB><<<blocks, THREADS, smem_fft(), st>>>(u0, units, M, N, K, s, dtw, ftw, Xc, w, cm);
   }
-  static void xhat_n(int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftwn,
+  static void xhat_n(int u0, int units, int M, int N, int K, const float2* s, const float2* dtw, const float2* ftwn,
                      float2* Xc, const float2* w, double2* cm, cudaStream_t st) {
     const int blocks = (units + GN - 1) / GN;
-    k_xhat<PLN, GN, MINBN><<<blocks, THREADS_N, smem_n(), st>>>(units, M, N, K, s, dtw, ftwn, Xc, w, cm);
+    k_xhat<PLN, GN, MINBN><<<blocks, THREADS_N, smem_n(), st>>>(u0, units, M, N, K, s, dtw, ftwn, Xc, w, cm);
   }
   static void rows_ifft(int rows, int N, const float2* in, const float2* ftw, float2* out, cudaStream_t st) {
     const int blocks = (rows + G - 1) / G;
@@ -304,38 +307,30 @@ struct Launch {
   }
   static int groups_per_block() { return G; }
   // Chebyshev engine: node AFs, node adjoint correlations, Step-B node tail
-  static void node(int units, int M, int Q, int N, int LS, const float2* Xc, const float2* H, const float2* ftwn,
-                   float2* Rn, int R, LrRed* lred, cudaStream_t st) {
-    k_node<PLN, GN, MINBN><<<(units + GN - 1) / GN, THREADS_N, smem_n(), st>>>(units, M, Q, N, LS, Xc, H, ftwn, Rn, R,
-                                                                               lred);
+  static void node(int u0, int units, int M, int Q, int N, int LS, const float2* Xc, const float2* H,
+                   const float2* ftwn, float2* Rn, int R, LrRed* lred, cudaStream_t st) {
+    k_node<PLN, GN, MINBN><<<(units + GN - 1) / GN, THREADS_N, smem_n(), st>>>(u0, units, M, Q, N, LS, Xc, H, ftwn, Rn,
+                                                                               R, lred);
   }
-  static void adj_g(int wrt, const AdjGArgs& a, const float2* ftwn, cudaStream_t st) {
+  static void adj_g(const AdjGArgs& a, const float2* ftwn, cudaStream_t st) {  // Step A node adjoints
     const int blocks = (a.units + GN - 1) / GN;
-    if (wrt == 2) k_adj_g<PLN, GN, MINBN, 2><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
-    else k_adj_g<PLN, GN, MINBN, 1><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
+    k_adj_g<PLN, GN, MINBN><<<blocks, THREADS_N, smem_n(), st>>>(a, ftwn);
   }
-  // CTA-summed node adjoints: NGC groups per CTA (shared memory: NGC exchange buffers)
+  // Step-B node adjoints summed inside the CTA: NGC groups per CTA (shared memory: NGC exchange buffers)
   static constexpr int NGC = (PLN::T >= 512) ? 1 : (PLN::T >= 256 ? 2 : ((128 / PLN::T) > 4 ? 128 / PLN::T : 4));
   static size_t smem_c() { return (size_t)NGC * FftSmem<PLN>::TOTAL * sizeof(float2) + 16; }
-  static void adj_gc(int wrt, const AdjGArgs& a, int ctas, const float2* ftwn, cudaStream_t st) {
-    if (wrt == 2) k_adj_gc<PLN, NGC, 2><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
-    else k_adj_gc<PLN, NGC, 1><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
+  static void adj_gc(const AdjGArgs& a, int ctas, const float2* ftwn, cudaStream_t st) {
+    if (ctas > 0) k_adj_gc<PLN, NGC><<<ctas, PLN::T * NGC, smem_c(), st>>>(a, ftwn);
   }
   static cudaError_t prepare_lr() {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_node<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
       return e;
-    if ((e = cudaFuncSetAttribute(k_adj_g<PLN, GN, MINBN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_n())))
-      return e;
-    if ((e = cudaFuncSetAttribute(k_adj_g<PLN, GN, MINBN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_n())))
+    if ((e = cudaFuncSetAttribute(k_adj_g<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
       return e;
     if ((e = cudaFuncSetAttribute(k_xhat<PLN, GN, MINBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n())))
       return e;
-    if ((e = cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c())))
-      return e;
-    return cudaFuncSetAttribute(k_adj_gc<PLN, NGC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c());
+    return cudaFuncSetAttribute(k_adj_gc<PLN, NGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c());
   }
 };
 
@@ -344,8 +339,8 @@ template <int Q>
 struct LrLaunch {
   // tensor-core variant
   template <int LM, bool HW, bool GRAD>
-  static void go_t(const LrtArgs& a, int /*units*/, size_t smem, cudaStream_t st) {
-    k_lrt<Q, LM, HW, GRAD><<<dim3(a.nch, a.M * a.M, a.R), 32 * a.kw, smem, st>>>(a);
+  static void go_t(const LrtArgs& a, int rows, size_t smem, cudaStream_t st) {  // grid (chunk, l, row - row0)
+    if (rows > 0) k_lrt<Q, LM, HW, GRAD><<<dim3(a.nch, a.M, rows), 32 * a.kw, smem, st>>>(a);
   }
   static void launch_t(int lm, bool hw, bool grad, const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
     if (lm == 0) { hw ? go_t<0, true, false>(a, units, smem, st) : go_t<0, false, false>(a, units, smem, st); return; }
@@ -533,8 +528,10 @@ void* sq_ctx_run_ws(sqngd_ctx ctx, size_t dev_bytes, void** host, size_t host_by
 
 extern "C" {
 
-sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void* nccl_unique_id, int rank,
-                          int world, sqngd_ctx* out) {
+}  // extern "C"
+
+static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const void* nccl_unique_id, LoopGroup* group,
+                                int rank, int world, sqngd_ctx* out) {
   sqngd_ctx ctx = nullptr;
   if (!cfgp || !out) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: null argument");
   *out = nullptr;
@@ -626,7 +623,7 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
 
   // Doppler engine (include/sqngd.h SQNGD_ENGINE_*): node count Q for lr_tol, tables, unit split.
   std::vector<double> lr_fq, lr_ell;
-  if (cfg.doppler_engine != SQNGD_ENGINE_FFT && world == 1 && cfg.K >= 3) {
+  if (cfg.doppler_engine != SQNGD_ENGINE_FFT && cfg.K >= 3) {
     const double tol = cfg.lr_tol > 0 ? cfg.lr_tol : 1e-7;
     for (int Q = 4; Q <= 16; Q += 2) {
       const double err = lr_tables(cfg, Q, lr_fq, lr_ell);
@@ -641,13 +638,12 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
   if (cfg.doppler_engine == SQNGD_ENGINE_CHEBYSHEV && !ctx->lr) {
     delete ctx;
     return fail(nullptr, SQNGD_E_INVALID,
-                "sqngd_create: CHEBYSHEV engine needs world == 1, K >= 3 and <= 16 nodes for lr_tol");
+                "sqngd_create: CHEBYSHEV engine needs K >= 3 and <= 16 nodes for lr_tol");
   }
   if (ctx->lr) {
     ctx->QS = (ctx->Q + 3) & ~3;
     ctx->nch = (L + 31) / 32;
     ctx->LS = ctx->nch * 32;
-    if (const char* ev = getenv("SQNGD_LR_CTA")) ctx->lr_cta = ev[0] != '0';
     ctx->nch16 = (L + 15) / 16;
     const int Kp = cfg.K / 2;
     ctx->NT = (Kp + 7) / 8;
@@ -870,27 +866,75 @@ sqngd_status sqngd_create(const sqngd_config* cfgp, int cuda_device, const void*
     CK(cudaMalloc(&ctx->Rn, sizeof(float2) * pairs * Q * ctx->LS));
     CK(cudaMalloc(&ctx->Gn, sizeof(float2) * pairs * Q * ctx->LS));
     CK(cudaMalloc(&ctx->lred, sizeof(LrRed) * cfg.R));
-    CK(cudaMalloc(&ctx->lr_cnt, sizeof(int) * (size_t)cfg.R * cfg.M * Q));
-    CK(cudaMemset(ctx->lr_cnt, 0, sizeof(int) * (size_t)cfg.R * cfg.M * Q));
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     CK(cudaMalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ((cfg.N + 1) & ~1)));
   }
 
-  if (world > 1) {
-    if (!nccl_unique_id) {
-      sqngd_destroy(ctx);
-      return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: world > 1 needs an ncclUniqueId");
-    }
+  {  // this rank's shard of the Chebyshev engine's (restart, transmit channel) rows
+    int64_t lo, hi;
+    sqngd_shard_range((int64_t)cfg.R * cfg.M, rank, world, &lo, &hi);
+    ctx->row_lo = (int)lo;
+    ctx->row_hi = (int)hi;
+  }
+  if (world > 1) {  // one grouped collective per evaluation (comm.h)
+    CK(cudaMalloc(&ctx->pay, sizeof(double) * (size_t)cfg.R * (1 + 2 * (size_t)cfg.M * cfg.N)));
+    CK(cudaMalloc(&ctx->keyb, sizeof(unsigned long long) * 3 * cfg.R));
+    CK(cudaMalloc(&ctx->mref, sizeof(double) * cfg.R));
+    k_world_init<<<(cfg.R + 127) / 128, 128>>>(cfg.R, cfg.loss_mode, ctx->mref);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
     std::string why;
-    if (!ctx->comm.init(nccl_unique_id, rank, world, &why)) {
-      sqngd_destroy(ctx);
-      return fail(nullptr, SQNGD_E_NCCL, "sqngd_create: NCCL init", why.c_str());
+    if (group) {
+      LoopComm* lc = new LoopComm();
+      lc->g = group;
+      lc->rank = rank;
+      ctx->comm = lc;
+    } else {
+      if (!nccl_unique_id) {
+        sqngd_destroy(ctx);
+        return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: world > 1 needs an ncclUniqueId");
+      }
+      NcclComm* nc = new NcclComm();
+      ctx->comm = nc;
+      if (!nc->init(nccl_unique_id, rank, world, &why)) {
+        sqngd_destroy(ctx);
+        return fail(nullptr, SQNGD_E_NCCL, "sqngd_create: NCCL init", why.c_str());
+      }
     }
   }
   *out = ctx;
   return SQNGD_OK;
+}
+
+extern "C" {
+
+sqngd_status sqngd_create(const sqngd_config* cfg, int cuda_device, const void* nccl_unique_id, int rank, int world,
+                          sqngd_ctx* out) {
+  return create_impl(cfg, cuda_device, nccl_unique_id, nullptr, rank, world, out);
+}
+
+struct sqngd_loopback_s {
+  LoopGroup g;
+};
+
+sqngd_loopback sqngd_loopback_create(int world) {
+  if (world < 2 || world > kLoopMax) return nullptr;
+  sqngd_loopback lb = new sqngd_loopback_s();
+  if (!lb->g.init(world)) {
+    delete lb;
+    return nullptr;
+  }
+  return lb;
+}
+
+void sqngd_loopback_destroy(sqngd_loopback lb) { delete lb; }
+
+sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqngd_loopback group, int rank,
+                                   sqngd_ctx* out) {
+  if (!group) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create_loopback: null group");
+  return create_impl(cfg, cuda_device, nullptr, &group->g, rank, group->g.world, out);
 }
 
 void sqngd_destroy(sqngd_ctx ctx) {
@@ -907,7 +951,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
   void* ptrs[] = {ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot, ctx->lred, ctx->lr_cnt, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->pay, ctx->keyb, ctx->mref, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->run_dev) cudaFree(ctx->run_dev);
@@ -919,7 +963,10 @@ void sqngd_destroy(sqngd_ctx ctx) {
   if (ctx->ev_nf) cudaEventDestroy(ctx->ev_nf);
   if (ctx->ev_nj) cudaEventDestroy(ctx->ev_nj);
   if (ctx->side_net) cudaStreamDestroy(ctx->side_net);
-  ctx->comm.destroy();
+  if (ctx->comm) {
+    ctx->comm->destroy();
+    delete ctx->comm;
+  }
   delete ctx;
 }
 
@@ -1017,37 +1064,81 @@ static sqngd_status run_filter_fft(sqngd_ctx ctx, const float2* w, cudaStream_t 
   return launch_check(ctx, "filter fft");
 }
 
-// a3 (+ a6 when w is given): X cache of the waveform s over all units (Chebyshev engine: the
-// Q node modulations V_q instead of the K bins).
-static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st, const float2* w = nullptr) {
+// a3 (+ a6 when w is given): X cache of the waveform s over this rank's units (Chebyshev engine: the
+// Q node modulations V_q of its rows instead of the K bins).
+// full: the FFT engine's Step-A units (r, l, k) read X_{m,k} of every channel m, so with world > 1 its
+// Step-A X cache is computed for all units (replicated a3 work, 1/(M+1) of its transforms); the
+// forward and Step B read only their own units (r, m, k), the Chebyshev engine only its own rows.
+static sqngd_status run_xhat(sqngd_ctx ctx, const float2* s, cudaStream_t st, const float2* w = nullptr,
+                             bool full = false) {
   const sqngd_config& c = ctx->cfg;
-  const int nk = ctx->lr ? ctx->Q : c.K;
-  const int units = c.R * c.M * nk;
+  int u0, units;
+  if (ctx->lr) {
+    u0 = ctx->row_lo * ctx->Q;
+    units = (ctx->row_hi - ctx->row_lo) * ctx->Q;
+  } else if (full) {
+    u0 = 0;
+    units = c.R * c.M * c.K;
+  } else {
+    KP kp = make_kp(ctx, 0);
+    u0 = kp.u_lo;
+    units = kp.u_hi - kp.u_lo;
+  }
+  if (units <= 0) return SQNGD_OK;
   with_P(ctx->P, [&](auto Lc) {
-    if (ctx->lr) decltype(Lc)::xhat_n(units, c.M, c.N, nk, s, ctx->Vt, ctx->ftwn, ctx->Xc, w, ctx->cm, st);
-    else decltype(Lc)::xhat(units, c.M, c.N, nk, s, ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
+    if (ctx->lr) decltype(Lc)::xhat_n(u0, units, c.M, c.N, ctx->Q, s, ctx->Vt, ctx->ftwn, ctx->Xc, w, ctx->cm, st);
+    else decltype(Lc)::xhat(u0, units, c.M, c.N, c.K, s, ctx->tw, ctx->ftw, ctx->Xc, w, ctx->cm, st);
   });
   ctx->launches += 1;
   return launch_check(ctx, "xhat");
 }
 
-// Multi-GPU: max-then-sum protocol over the per-restart partials.
-static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad, int mode);
+// ---------------------------------------------------------------- multi-GPU (world > 1, comm.h)
+// c_m of every row (the shard's transforms computed only its own rows' c_m).
+static sqngd_status run_cm_rows(sqngd_ctx ctx, const float2* s, const float2* w, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  const int RM = c.R * c.M;
+  k_cm_rows<<<(RM + 7) / 8, 256, 0, st>>>(RM, c.N, s, w, ctx->cm);
+  ctx->launches += 1;
+  return launch_check(ctx, "cm rows");
+}
 
-// Chebyshev engine, forward part: node AFs (k_node) and the fused contraction / epilogue (k_lr),
-// then the per-restart reduction (keys, shift, S, unit scales, metrics).
+// The one grouped collective of an evaluation: local (m_r, S_r, keys) in ctx->red and, with a gradient,
+// the locally normalised partial in ctx->red_grad -> global red and red_grad on every rank.
+static sqngd_status world_combine(sqngd_ctx ctx, bool with_grad, cudaStream_t st) {
+  const sqngd_config& c = ctx->cfg;
+  WorldArgs wa{};
+  wa.R = c.R; wa.M = c.M; wa.N = c.N; wa.mode = c.loss_mode; wa.with_grad = with_grad ? 1 : 0;
+  wa.bp = c.beta_or_p; wa.red = ctx->red; wa.mref = ctx->mref; wa.grad = ctx->red_grad; wa.pay = ctx->pay;
+  wa.key = ctx->keyb;
+  const size_t n = with_grad ? (size_t)2 * c.M * c.N : 0;
+  const dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 256)), c.R);
+  k_world_pack<<<grid, 256, 0, st>>>(wa);
+  sqngd_status rc = launch_check(ctx, "world pack");
+  if (rc) return rc;
+  std::string why;
+  if (!ctx->comm->allreduce(ctx->pay, (size_t)c.R * (1 + n), ctx->keyb, (size_t)3 * c.R, st, &why))
+    return fail(ctx, SQNGD_E_NCCL, "grouped all-reduce", why.c_str());
+  // (the payload stride is 1 + n per restart: pack and unpack agree on it)
+  k_world_unpack<<<grid, 256, 0, st>>>(wa, ctx->status);
+  ctx->launches += 2;
+  return launch_check(ctx, "world unpack");
+}
+
+// Chebyshev engine, forward part: node AFs (k_node) and the fused contraction / epilogue (k_lrt), then
+// the per-restart reduction (keys, shift, S, metrics) -- over this rank's rows.
 static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, const MetricsArgs& ma, cudaStream_t st,
                            bool fork) {
   const sqngd_config& c = ctx->cfg;
-  const int node_units = c.R * c.M * c.M * ctx->Q;
+  const int rows = ctx->row_hi - ctx->row_lo;
   with_P(ctx->P, [&](auto Lc) {
-    decltype(Lc)::node(node_units, c.M, ctx->Q, c.N, ctx->LS, ctx->Xc, ctx->H, ctx->ftwn, ctx->Rn, c.R, ctx->lred, st);
+    decltype(Lc)::node(ctx->row_lo * c.M * ctx->Q, std::max(1, rows * c.M * ctx->Q), c.M, ctx->Q, c.N, ctx->LS,
+                       ctx->Xc, ctx->H, ctx->ftwn, ctx->Rn, c.R, ctx->lred, st);
   });
   LrtArgs t{};
   t.R = c.R; t.M = c.M; t.N = c.N; t.L = ctx->L; t.K = c.K; t.nch = ctx->nch16; t.kw = ctx->kw; t.LS = ctx->LS;
   t.NT = ctx->NT; t.NTF = ctx->NTF; t.coefm = ctx->coef + (size_t)(c.K / 2) * ctx->QS;
-  t.tabF16 = ctx->tabF16; t.tabM16 = ctx->tabM16;
-  const int grid = (int)ctx->units_lr;
+  t.tabF16 = ctx->tabF16; t.tabM16 = ctx->tabM16; t.row0 = ctx->row_lo;
   t.tau_lo = c.tau_lo; t.tau_hi = c.tau_hi; t.excl0 = c.exclude_auto_zero_delay;
   t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
   t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
@@ -1055,17 +1146,21 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
   {
     ProfScope ps(ctx, cls, st);
     with_Q(ctx->Q, [&](auto Qc) {
-      decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad, t, grid, ctx->lr_smem, st);
+      decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad, t, rows, ctx->lr_smem, st);
     });
   }
   const int GPR = (int)(ctx->units_lr / c.R);
+  const int g_lo = ctx->row_lo * c.M * ctx->nch16, g_hi = ctx->row_hi * c.M * ctx->nch16;
   cudaStream_t fs = st;
   if (fork) {  // k_lr_finish runs beside the adjoint kernels; run_loss_grad joins before the combine
     CK(cudaEventRecord(ctx->ev_fork, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     fs = ctx->side;
   }
-  k_lr_finish<<<c.R, 1024, 0, fs>>>(GPR, c.loss_mode, c.beta_or_p, ctx->part, ctx->lred, ctx->red, ma, ctx->status);
+  MetricsArgs mloc = ma;  // multi-GPU: the metrics follow the collective
+  if (ctx->world > 1) { mloc.out = nullptr; mloc.p_out = nullptr; mloc.loss_hist = nullptr; }
+  k_lr_finish<<<c.R, 1024, 0, fs>>>(GPR, g_lo, g_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->lred, ctx->red, mloc,
+                                    ctx->status);
   if (fork) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   ctx->launches += 3;
   return launch_check(ctx, "chebyshev forward");
@@ -1075,36 +1170,36 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
 static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w, float* af_mag, MetricsOut* met,
                                 double* p_out, double* hist, int hist_col, cudaStream_t st, bool xhat_ready = false) {
   const sqngd_config& c = ctx->cfg;
-  if (!xhat_ready) {
-    sqngd_status rx = run_xhat(ctx, s, st, w);
-    if (rx) return rx;
-  }
+  sqngd_status rc;
+  if (!xhat_ready && (rc = run_xhat(ctx, s, st, w))) return rc;
   KP kp = make_kp(ctx, c.loss_mode != 0);
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
                  ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
-  if (ctx->lr) return run_lr(ctx, false, MODE_FWD, af_mag, ma, st, false);
-  cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
-  {
-    ProfScope ps(ctx, MODE_FWD, st);
-    with_P(ctx->P, [&](auto Lc) {
-      decltype(Lc)::af(MODE_FWD, kp, ctx->slots[MODE_FWD], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, af_mag, ctx->part, st);
-    });
-  }
-  ctx->launches += 4;
-  sqngd_status rc = launch_check(ctx, "af forward");
-  if (rc) return rc;
-  if (ctx->world == 1) {
-    k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
-                                          ctx->red, ma, ctx->status);
+  MetricsArgs none = ma;
+  none.out = nullptr; none.p_out = nullptr; none.loss_hist = nullptr;
+  if (ctx->lr) {
+    if ((rc = run_lr(ctx, false, MODE_FWD, af_mag, ma, st, false))) return rc;
   } else {
-    MetricsArgs none = ma;
-    none.out = nullptr; none.p_out = nullptr; none.loss_hist = nullptr;
+    cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
+    {
+      ProfScope ps(ctx, MODE_FWD, st);
+      with_P(ctx->P, [&](auto Lc) {
+        decltype(Lc)::af(MODE_FWD, kp, ctx->slots[MODE_FWD], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, af_mag, ctx->part, st);
+      });
+    }
+    ctx->launches += 2;
+    if ((rc = launch_check(ctx, "af forward"))) return rc;
     k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
-                                          ctx->red, none, ctx->status);
-    if ((rc = allreduce_red(ctx, st, false, MODE_FWD))) return rc;
-    k_metrics<<<c.R, 32, 0, st>>>(ma, ctx->status);
+                                          ctx->red, ctx->world == 1 ? ma : none, ctx->status);
+    if ((rc = launch_check(ctx, "metrics"))) return rc;
   }
+  if (ctx->world == 1) return SQNGD_OK;
+  // multi-GPU: c_m of every row, the grouped collective, then the metrics
+  if ((rc = run_cm_rows(ctx, s, w, st))) return rc;
+  if ((rc = world_combine(ctx, false, st))) return rc;
+  k_metrics<<<c.R, 32, 0, st>>>(ma, ctx->status);
+  ctx->launches += 1;
   return launch_check(ctx, "metrics");
 }
 
@@ -1125,122 +1220,117 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
   const sqngd_config& c = ctx->cfg;
   sqngd_status rc;
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
-  if (!xhat_ready && (rc = run_xhat(ctx, s, st, w))) return rc;
+  if (!xhat_ready && (rc = run_xhat(ctx, s, st, w, wrt == SQNGD_WRT_FILTERS))) return rc;
   FinArgs fa{c.R, c.M, c.N, wrt, c.eps_w, ptar, ctx->cm, s, w, dq, grad_w, grad_s, ctx->dy, grad_z};
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
                  ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col};
+  MetricsArgs none = ma;
+  none.out = nullptr; none.loss_hist = nullptr;
   const size_t n = (size_t)c.R * c.M * c.N;
-  if (c.loss_mode == SQNGD_LOSS_MAX) {
+  const bool multi = ctx->world > 1;
+  if (c.loss_mode == SQNGD_LOSS_MAX) {  // Eq. 37: the exact maximum, its O(N) subgradient on every rank
     if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st, true))) return rc;
     k_sparse_adj<<<c.R, 256, 0, st>>>(c.M, c.N, c.K, ctx->L, wrt, c.eps_w, c.weights, s, w, ctx->tw, ctx->red,
                                       ctx->red_grad);
-    MetricsArgs none = ma;
-    none.out = nullptr;
-    none.loss_hist = nullptr;
     k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fa, ctx->red_grad, ctx->status, none);
     ctx->launches += 2;
     return launch_check(ctx, "sparse adjoint");
   }
-  if (ctx->lr) {  // Chebyshev engine (single GPU)
+  CombineArgs ca{};
+  ca.M = c.M; ca.N = c.N; ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.red = ctx->red;
+  ca.f = fa;
+  ca.part = ctx->part;
+  if (ctx->lr) {  // Chebyshev engine: this rank's rows
     if ((rc = run_lr(ctx, true, wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B, nullptr, ma, st, true))) return rc;
     AdjGArgs ag{};
     ag.M = c.M; ag.N = c.N; ag.Q = ctx->Q; ag.LS = ctx->LS;
     ag.nch = ctx->nch16; ag.csh = 4;
     ag.units = c.R * c.M * c.M * ctx->Q; ag.mode = c.loss_mode; ag.bp = (float)c.beta_or_p;
+    ag.row_lo = ctx->row_lo; ag.row_hi = ctx->row_hi; ag.u0 = ctx->row_lo * ctx->Q;
     ag.Gn = ctx->Gn; ag.um = ctx->part.m; ag.lred = ctx->lred; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
-    ag.cnt = ctx->lr_cnt; ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
-    const bool cta_sum = ctx->lr_cta && wrt == SQNGD_WRT_TRANSMIT;  // Step A: 640 one-FFT units measured faster
+    ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
     with_P(ctx->P, [&](auto Lc) {
-      if (cta_sum) decltype(Lc)::adj_gc(wrt, ag, wrt == 2 ? c.R * c.M * ctx->Q : c.R * c.M * c.M, ctx->ftwn, st);
-      else decltype(Lc)::adj_g(wrt, ag, ctx->ftwn, st);
+      if (wrt == SQNGD_WRT_TRANSMIT) decltype(Lc)::adj_gc(ag, (ctx->row_hi - ctx->row_lo) * ctx->Q, ctx->ftwn, st);
+      else decltype(Lc)::adj_g(ag, ctx->ftwn, st);
     });
-    CombineArgs ca{};
-    ca.M = c.M; ca.N = c.N; ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.red = ctx->red;
-    ca.f = fa;
-    ca.part = ctx->part;
-    ca.part.scale = nullptr;  // node cotangents were rescaled in k_adj_g
-    if (wrt == SQNGD_WRT_TRANSMIT) {
-      const int tu = c.R * c.M * ctx->Q;  // node time-domain partials (k_adj_gc / k_adj_g's last groups)
-      CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // S and the metrics from k_lr_finish
-      ca.K = ctx->Q; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = 0; ca.u_hi = tu; ca.part.g = ctx->tslot;
-      ca.len = c.N; ca.extra = 1.0; ca.fin = 1; ca.out = nullptr;
+    ca.part.scale = nullptr;  // node cotangents were rescaled in the adjoint kernels
+    CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // S and the metrics from k_lr_finish
+    if (wrt == SQNGD_WRT_TRANSMIT) {  // node time-domain partials of this rank's rows
+      ca.K = ctx->Q; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = ctx->row_lo * ctx->Q; ca.u_hi = ctx->row_hi * ctx->Q;
+      ca.part.g = ctx->tslot; ca.len = c.N; ca.extra = 1.0;
+      ca.fin = multi ? 0 : 1;
+      ca.out = multi ? ctx->red_grad : nullptr;
       k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
       ctx->launches += 3;
-      return launch_check(ctx, "chebyshev adjoint (transmit)");
-    }
-    CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-    const int nsl = cta_sum ? c.M : c.M * ctx->Q;  // spectral slots per filter row
-    ca.K = nsl; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * nsl;
-    ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
-    k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
-    if (tail) {
-      with_P(ctx->P, [&](auto Lc) {
-        decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftwr, fa, tail->ap, tail->w, tail->mw, tail->vw, ctx->H,
-                                  ctx->cm, ctx->status, st);
-      });
+      if ((rc = launch_check(ctx, "chebyshev adjoint (transmit)"))) return rc;
     } else {
-      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftwr, fa, ctx->status, st); });
+      const int nsl = c.M * ctx->Q;  // spectral slots per filter row (zeros for other ranks' rows)
+      ca.K = nsl; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * nsl;
+      ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
+      k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      ctx->launches += 3;
+      if (!multi) {
+        if (tail) {
+          with_P(ctx->P, [&](auto Lc) {
+            decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftwr, fa, tail->ap, tail->w, tail->mw, tail->vw,
+                                      ctx->H, ctx->cm, ctx->status, st);
+          });
+        } else {
+          with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftwr, fa, ctx->status, st); });
+        }
+        return launch_check(ctx, "chebyshev adjoint (filters)");
+      }
+      with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft(c.R * c.M, c.N, ctx->spec, ctx->ftw, ctx->red_grad, st); });
+      ctx->launches += 1;
     }
-    ctx->launches += 3;
-    return launch_check(ctx, "chebyshev adjoint (filters)");
-  }
-  const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
-  KP kp = make_kp(ctx, 1);
-  cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
-  {
-    ProfScope ps(ctx, mode, st);
-    with_P(ctx->P, [&](auto Lc) {
-      decltype(Lc)::af(mode, kp, ctx->slots[mode], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
-    });
-  }
-  ctx->launches += 1;
-  if ((rc = launch_check(ctx, "af adjoint"))) return rc;
-  CombineArgs ca{};
-  ca.M = c.M; ca.N = c.N; ca.K = c.K; ca.slot_stride = ctx->P; ca.u_lo = kp.u_lo; ca.u_hi = kp.u_hi;
-  ca.mode = c.loss_mode; ca.bp = c.beta_or_p; ca.eps = c.eps_w; ca.part = ctx->part; ca.red = ctx->red;
-  ca.f = fa;
-  MetricsArgs none = ma;
-  none.out = nullptr; none.loss_hist = nullptr;
-  k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red,
-                                        ctx->world == 1 ? ma : none, ctx->status);
-  ctx->launches += 1;
-  if (ctx->world == 1) {
-    // single GPU: Step B finalizes inside the combine, Step A inside the row IFFT.
-    if (mode == MODE_ADJ_B) {
-      ca.len = c.N; ca.extra = 1.0; ca.fin = 1; ca.out = nullptr;
+    if (!multi) return SQNGD_OK;
+  } else {  // per-bin FFT engine: this rank's units
+    const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
+    KP kp = make_kp(ctx, 1);
+    cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
+    {
+      ProfScope ps(ctx, mode, st);
+      with_P(ctx->P, [&](auto Lc) {
+        decltype(Lc)::af(mode, kp, ctx->slots[mode], ctx->Xc, ctx->H, ctx->tw, ctx->ftw, nullptr, ctx->part, st);
+      });
+    }
+    ctx->launches += 1;
+    if ((rc = launch_check(ctx, "af adjoint"))) return rc;
+    ca.K = c.K; ca.slot_stride = ctx->P; ca.u_lo = kp.u_lo; ca.u_hi = kp.u_hi;
+    k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red,
+                                          multi ? none : ma, ctx->status);
+    ctx->launches += 1;
+    if (mode == MODE_ADJ_B) {  // single GPU: finalize inside the combine
+      ca.len = c.N; ca.extra = 1.0; ca.fin = multi ? 0 : 1; ca.out = multi ? ctx->red_grad : nullptr;
       k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
       ctx->launches += 1;
     } else {
       ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
       k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
-      if (tail) {  // + Adam(w), Pi_H, next H = FFT(w)/P and c_m, in the same row kernel
-        with_P(ctx->P, [&](auto Lc) {
-          decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftwr, fa, tail->ap, tail->w, tail->mw, tail->vw,
-                                    ctx->H, ctx->cm, ctx->status, st);
-        });
-      } else {
-        with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftwr, fa, ctx->status, st); });
-      }
       ctx->launches += 2;
+      if (!multi) {  // single GPU: finalize inside the row IFFT (+ Adam(w), Pi_H, next H and c_m in the step)
+        if (tail) {
+          with_P(ctx->P, [&](auto Lc) {
+            decltype(Lc)::rows_adam_w(c.R * c.M, ctx->spec, ctx->ftwr, fa, tail->ap, tail->w, tail->mw, tail->vw,
+                                      ctx->H, ctx->cm, ctx->status, st);
+          });
+        } else {
+          with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft_fin(c.R * c.M, ctx->spec, ctx->ftwr, fa, ctx->status, st); });
+        }
+      } else {
+        with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft(c.R * c.M, c.N, ctx->spec, ctx->ftw, ctx->red_grad, st); });
+      }
     }
-    return launch_check(ctx, "combine");
+    if ((rc = launch_check(ctx, "combine"))) return rc;
+    if (!multi) return SQNGD_OK;
   }
-  // multi-GPU: max-then-sum all-reduce of the loss partials, local combine with the global
-  // shift, all-reduce of the gradient, then finalize.
-  if ((rc = allreduce_red(ctx, st, false, mode))) return rc;
-  k_group_scales<<<c.R, 256, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red);
-  ca.fin = 0;
-  if (mode == MODE_ADJ_B) {
-    ca.len = c.N; ca.extra = 1.0; ca.out = ctx->red_grad;
-    k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
-  } else {
-    ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.out = ctx->spec;
-    k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
-    with_P(ctx->P, [&](auto Lc) { decltype(Lc)::rows_ifft(c.R * c.M, c.N, ctx->spec, ctx->ftw, ctx->red_grad, st); });
-  }
-  if ((rc = allreduce_red(ctx, st, true, mode))) return rc;
-  k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fa, ctx->red_grad, ctx->status, ma);
-  ctx->launches += 4;
+  // multi-GPU: every row's c_m, the grouped collective, then the finalize (+ metrics) on every rank
+  if ((rc = run_cm_rows(ctx, s, w, st))) return rc;
+  if ((rc = world_combine(ctx, true, st))) return rc;
+  // (at least R blocks: block r < R also writes restart r's metrics)
+  k_finalize_grad<<<(unsigned)std::max<size_t>((n + 255) / 256, (size_t)c.R), 256, 0, st>>>(fa, ctx->red_grad,
+                                                                                             ctx->status, ma);
+  ctx->launches += 1;
   return launch_check(ctx, "finalize grad");
 }
 
@@ -1264,20 +1354,6 @@ static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho
   else k_grad_rho_part<false><<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
   ctx->launches += 1;
   return launch_check(ctx, "grad rho");
-}
-
-static sqngd_status allreduce_red(sqngd_ctx ctx, cudaStream_t st, bool with_grad, int mode) {
-  const sqngd_config& c = ctx->cfg;
-  std::string why;
-  if (!with_grad) {
-    if (!ctx->comm.reduce_red(ctx->red, c.R, c.loss_mode, c.beta_or_p, st, &why))
-      return fail(ctx, SQNGD_E_NCCL, "all-reduce (loss partials)", why.c_str());
-  } else {
-    if (!ctx->comm.sum_f32(reinterpret_cast<float*>(ctx->red_grad), (size_t)c.R * c.M * c.N * 2, st, &why))
-      return fail(ctx, SQNGD_E_NCCL, "all-reduce (gradient)", why.c_str());
-  }
-  (void)mode;
-  return SQNGD_OK;
 }
 
 // ----------------------------------------------------------------------------- C-ABI compute entry points
@@ -1409,7 +1485,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
   }
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
-    if ((rc = run_xhat(ctx, ctx->s_hard, st))) return rc;  // X_hard fixed for the whole block
+    if ((rc = run_xhat(ctx, ctx->s_hard, st, nullptr, true))) return rc;  // X_hard fixed for the block
     const bool fused = ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
     for (int i = 0; i < c.n_h; ++i) {
       if ((!fused || i == 0) && (rc = run_filter_fft(ctx, w2, st, ctx->s_hard))) return rc;
@@ -1515,8 +1591,8 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
   sqngd_status rc;
   k_set_t<<<1, 64, 0, st>>>(ctx->d_t, stt->t_a, stt->t_b, ctx->d_ct, ctx->cts, c.n_h, c.n_x, c.adam_b1, c.adam_b2);
   ctx->launches += 1;
-  // Graph path: single GPU, a capturable (non-legacy) stream.
-  const bool graph_ok = ctx->use_graphs && !ctx->prof && ctx->world == 1 && st != nullptr &&
+  // Graph path: one GPU or NCCL (the collective is captured with the step), a capturable (non-legacy) stream.
+  const bool graph_ok = ctx->use_graphs && !ctx->prof && (ctx->world == 1 || ctx->comm->capturable()) && st != nullptr &&
                         st != cudaStreamLegacy && st != cudaStreamPerThread;
   if (!graph_ok) {
     if ((rc = step_body(ctx, stt, block, loss_hist, hard_out, st))) return rc;

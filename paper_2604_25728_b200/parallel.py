@@ -5,10 +5,12 @@ Two ways the hot path spans GPUs:
 * independent restarts (bench.py --gpus N, "weak"): rank r optimizes its own seeded
   restarts, no data-path collective; only the timing is reduced (max over ranks);
 * one problem sharded over ranks (the library's world > 1 mode): each rank evaluates a
-  contiguous slice of the (restart, channel, Doppler) units and the per-restart
-  partials are combined by the max-then-sum protocol below.  libsqngd implements it
-  with NCCL (csrc/comm.h: k_red_pack / k_red_rescale / k_red_unpack); `combine_lse`
-  is the same arithmetic over torch.distributed so it is testable with gloo on CPU.
+  shard (FFT engine: a slice of the (restart, channel, bin) units; Chebyshev engine: a
+  slice of the (restart, transmit channel) rows) and ONE grouped collective per
+  evaluation combines the per-restart partials against a reference shift every rank
+  holds (csrc/comm.h, misc_kernels.cuh k_world_pack / k_world_unpack).  `combine_ref`
+  below restates that arithmetic over torch.distributed so the protocol is testable
+  with gloo on CPU (gloo has no grouped call: the SUM and the MAX are two calls there).
 """
 from __future__ import annotations
 
@@ -40,33 +42,37 @@ def max_over_ranks(x: float, group=None) -> float:
     return float(t.item())
 
 
-def combine_lse(m, S, G, beta: float, mode: int = 1, group=None):
-    """Combine per-rank LSE / p-norm partials of one restart.
+def combine_ref(m, S, g, m_ref: float, beta: float, mode: int = 1, group=None):
+    """One restart's combine of the library's world > 1 protocol (csrc/comm.h).
 
-    m: the rank's shift (max v over its cells, -inf if none); S: sum of phi at that shift;
-    G: the rank's unnormalized gradient (sum of phi-weighted cotangent contributions) at
-    that shift (a tensor).  Returns (m_global, S_global, G_global) at the global shift:
-      1. all-reduce MAX of m;  2. rescale S and G to it;  3. all-reduce SUM of S and G.
-    LSE: phi = e^{beta (v - m)}, rescale e^{beta (m_r - m)} for both S and G;
-    PNORM: phi = (v/m)^p, S rescales by (m_r/m)^p and G (weights (v/m)^{p-1}) by (m_r/m)^{p-1}.
-    """
+    m: the rank's shift (-inf if it has no cells); S: its sum of phi at that shift; g: its
+    gradient normalised locally (LSE: G / S, p-norm: G S^{1/p - 1}) as a float64 tensor; m_ref: the
+    reference shift, identical on every rank.  Weights (fp64):
+      LSE:    wS = wG = e^{beta (m - m_ref)} S
+      p-norm: wS = (m / m_ref)^p S,  wG = (m / m_ref)^{p-1} S^{1 - 1/p}
+    SUM of [wS | wG g] and MAX of m over ranks, then
+      LSE:    loss = m_ref + ln(sum wS) / beta,   grad = sum(wG g) / sum wS
+      p-norm: loss = m_ref (sum wS)^{1/p},        grad = sum(wG g) (sum wS)^{1/p - 1}
+    Returns (loss, grad, new m_ref = max over ranks of m)."""
     import torch
     import torch.distributed as dist
 
-    mt = torch.tensor([float(m)], dtype=torch.float64, device=G.device)
-    if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(mt, op=dist.ReduceOp.MAX, group=group)
-    mg = float(mt.item())
     if not (S > 0) or m == -math.inf:
-        sc_S = sc_G = 0.0
+        wS = wG = 0.0
     elif mode == 1:
-        sc_S = sc_G = math.exp(beta * (m - mg))
+        wS = wG = math.exp(beta * (m - m_ref)) * S
     else:
-        sc_S = (m / mg) ** beta
-        sc_G = (m / mg) ** (beta - 1.0)
-    St = torch.tensor([S * sc_S], dtype=torch.float64, device=G.device)
-    Gt = (G * sc_G).to(torch.float64)
+        rho = m / m_ref
+        wS = rho ** beta * S
+        wG = rho ** (beta - 1.0) * S ** (1.0 - 1.0 / beta)
+    pay = torch.cat([torch.tensor([wS], dtype=torch.float64), (g.to(torch.float64) * wG).reshape(-1)])
+    mx = torch.tensor([m if m > -math.inf else -1.0], dtype=torch.float64)
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(St, group=group)
-        dist.all_reduce(Gt, group=group)
-    return mg, float(St.item()), Gt
+        dist.all_reduce(pay, group=group)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+    St, Gt = float(pay[0]), pay[1:].reshape(g.shape)
+    if mode == 1:
+        loss, grad = m_ref + math.log(St) / beta, Gt / St
+    else:
+        loss, grad = m_ref * St ** (1.0 / beta), Gt * St ** (1.0 / beta - 1.0)
+    return loss, grad, float(mx.item())

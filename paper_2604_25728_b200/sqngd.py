@@ -131,6 +131,12 @@ def lib():
         L.sqngd_run.restype = i32
         L.sqngd_run.argtypes = [vp, C.POINTER(State), C.POINTER(RunOpts), C.POINTER(State), vp, vp, vp, vp,
                                 C.POINTER(RunResult), vp]
+        L.sqngd_loopback_create.restype = vp
+        L.sqngd_loopback_create.argtypes = [i32]
+        L.sqngd_loopback_destroy.restype = None
+        L.sqngd_loopback_destroy.argtypes = [vp]
+        L.sqngd_create_loopback.restype = i32
+        L.sqngd_create_loopback.argtypes = [C.POINTER(Config), i32, vp, i32, C.POINTER(vp)]
         L.sqngd_version.restype = C.c_char_p
         L.sqngd_version.argtypes = []
         _lib = L
@@ -141,7 +147,8 @@ EXPORTED = ["sqngd_create", "sqngd_destroy", "sqngd_last_error", "sqngd_sync", "
             "sqngd_af_forward", "sqngd_loss_grad_s", "sqngd_af_loss_grad", "sqngd_step",
             "sqngd_profile_enable", "sqngd_profile_read",
             "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info",
-            "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward", "sqngd_run"]
+            "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward", "sqngd_run",
+            "sqngd_loopback_create", "sqngd_loopback_destroy", "sqngd_create_loopback"]
 
 
 def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Config:
@@ -195,12 +202,50 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from the same libnccl the library dlopens (torch's bundled NCCL); rank 0
+    creates it and every rank passes it to Context(..., nccl_uid=, rank=, world=)."""
+    path = "libnccl.so.2"
+    try:
+        import nvidia.nccl
+
+        for p in nvidia.nccl.__path__:
+            cand = os.path.join(p, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                path = cand
+                break
+    except Exception:
+        pass
+    L = C.CDLL(path, mode=C.RTLD_GLOBAL)
+    buf = C.create_string_buffer(128)
+    rc = L.ncclGetUniqueId(buf)
+    if rc != 0:
+        raise SqngdError(E_NCCL, f"ncclGetUniqueId returned {rc}")
+    return buf.raw
+
+
+class Loopback:
+    """Single-device stand-in for NCCL (include/sqngd.h sqngd_loopback_*): `world` contexts of one process,
+    each driven by its own host thread, run the library's sharded multi-GPU path."""
+
+    def __init__(self, world: int):
+        self.world = int(world)
+        self.h = lib().sqngd_loopback_create(self.world)
+        if not self.h:
+            raise SqngdError(E_INVALID, f"sqngd_loopback_create({world})")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sqngd_loopback_destroy(self.h)
+            self.h = None
+
+
 class Context:
     """One library context on one device; tensors are torch CUDA tensors
     (complex64 for s/w/gradients, float32 for z/rho, contiguous)."""
 
     def __init__(self, cfg, device: int = 0, weights=None, nccl_uid: bytes | None = None, rank: int = 0,
-                 world: int = 1):
+                 world: int = 1, loopback: "Loopback | None" = None):
         import torch
 
         if not torch.cuda.is_available():
@@ -219,7 +264,10 @@ class Context:
         if nccl_uid is not None:
             uid = C.create_string_buffer(bytes(nccl_uid), 128)
         with torch.cuda.device(self.device):
-            st = lib().sqngd_create(C.byref(self.c_cfg), device, uid, rank, world, C.byref(h))
+            if loopback is not None:
+                st = lib().sqngd_create_loopback(C.byref(self.c_cfg), device, loopback.h, rank, C.byref(h))
+            else:
+                st = lib().sqngd_create(C.byref(self.c_cfg), device, uid, rank, world, C.byref(h))
         if st != OK:
             raise SqngdError(st, lib().sqngd_last_error(None).decode())
         self.h = h

@@ -1,0 +1,172 @@
+"""The library's multi-GPU path (include/sqngd.h world > 1) through the C-ABI, on one device.
+
+W contexts of one loopback group (sqngd_create_loopback), each driven by its own host thread and stream,
+run exactly the sharded code of world > 1 -- FFT engine: a slice of the (restart, channel, bin) units;
+Chebyshev engine: a slice of the (restart, transmit channel) rows -- and the single grouped collective
+per evaluation (SUM of the weighted fp64 payload, MAX of the keys, comm.h).  Every rank must return the
+full outputs, equal across ranks, matching the fp64 oracle (tests/parity_util.py bars) and the
+single-context result.  The loopback reduces in fixed rank order, so the ranks agree bit for bit.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2604_25728_b200 import configs as CF  # noqa: E402
+from paper_2604_25728_b200 import inputs, sqngd  # noqa: E402
+from paper_2604_25728_b200.configs import Cfg  # noqa: E402
+
+from parity_util import check_db, check_grad, check_loss, record  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+ENGINES = {"fft": sqngd.ENGINE_FFT, "cheb": sqngd.ENGINE_CHEBYSHEV}
+MODES = {"lse": (CF.LOSS_LSE, 60.0), "max": (CF.LOSS_MAX, 0.0), "pnorm": (CF.LOSS_PNORM, 8.0)}
+
+
+def T(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device=DEV)
+
+
+def on_ranks(cfg, world, fn):
+    """fn(ctx, rank) on `world` loopback contexts, one thread + stream each; returns the per-rank results."""
+    lb = sqngd.Loopback(world)
+    ctxs = [sqngd.Context(cfg, loopback=lb, rank=r) for r in range(world)]
+    out, errs = [None] * world, []
+
+    def work(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(ctxs[r], r)
+                s.synchronize()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in ctxs:
+        c.close()
+    lb.close()
+    assert not errs, errs
+    assert all(o is not None for o in out), "a rank did not finish"
+    return out
+
+
+def inputs_for(c, seed):
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=seed)
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    q = O.quantize(c, z, rho)
+    w = (q["s_hard"] * np.exp(0.3j * np.cos(0.41 * np.arange(c.N)))).astype(np.complex64)
+    return z, rho, q, w
+
+
+def eval_all(ctx, z, rho, w):
+    """Forward metrics, Step-A grad_w and Step-B grad_z / grad_rho of one context."""
+    s_h = ctx.quantize(T(z), T(rho))["s_hard"]
+    met, p, _ = ctx.af_forward(s_h, T(w))
+    mf = ctx.metrics(met)
+    met, gw = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_FILTERS)
+    mA = ctx.metrics(met)
+    met, gz, gr = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
+    mB = ctx.metrics(met)
+    ctx.sync()
+    return dict(mf=mf, p=p.cpu().numpy(), mA=mA, gw=gw.cpu().numpy(), mB=mB, gz=gz.cpu().numpy(), gr=gr.cpu().numpy())
+
+
+CASES = [
+    Cfg("mr-c1", M=2, N=64, B=4, K=33, f_lo=-0.5, f_hi=0.5, R=2, r_n=4, eps_w=0.4),
+    Cfg("mr-ragged", M=3, N=37, B=8, K=21, f_lo=-0.5, f_hi=0.5, R=2, r_n=3),
+]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", ["lse", "pnorm", "max"])
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+@pytest.mark.parametrize("c", CASES, ids=lambda c: c.name)
+def test_sharded_matches_oracle_and_single(c, engine, mode, world):
+    lm, bp = MODES[mode]
+    c = c.with_(loss_mode=lm, beta_or_p=bp, doppler_engine=ENGINES[engine])
+    z, rho, q, w = inputs_for(c, 91)
+    res = on_ranks(c, world, lambda ctx, r: eval_all(ctx, z, rho, w))
+    single = eval_all(sqngd.Context(c), z, rho, w)
+    refF, refp, _ = O.af(c, q["s_hard"], w)
+    refA, gw_ref, _ = O.loss_grad(c, q["s_hard"], w, want_s=False)
+    refB, _, gs_ref = O.loss_grad(c, q["s_soft"], w, want_w=False)
+    gz_ref, gr_ref = O.chain(c, z, rho, q["s_soft"], gs_ref)
+    for r in range(world):  # every rank holds the full, identical outputs
+        for k in ("gw", "gz", "gr", "p"):
+            assert np.array_equal(res[r][k], res[0][k]), (r, k)
+        for k in ("mf", "mA", "mB"):  # (snrl_db_max is NaN in the loss+gradient metrics: compare its repr)
+            assert repr(res[r][k]) == repr(res[0][k]), (r, k)
+    g = res[0]
+    for rr in range(c.R):
+        check_loss(g["mf"][rr]["loss"], refF[rr]["loss"], "sharded forward loss")
+        check_loss(g["mA"][rr]["loss"], refA[rr]["loss"], "sharded Step-A loss")
+        check_loss(g["mB"][rr]["loss"], refB[rr]["loss"], "sharded Step-B loss")
+        for key in ("wapsl", "wcpsl", "wpsl"):
+            check_db(g["mf"][rr][key], refF[rr][key], f"sharded {key}")
+        assert g["mf"][rr]["argmax_auto"] == single["mf"][rr]["argmax_auto"]
+        assert g["mf"][rr]["argmax_cross"] == single["mf"][rr]["argmax_cross"]
+    np.testing.assert_allclose(g["p"], refp, rtol=1e-6, atol=1e-7)
+    check_grad(g["gw"], gw_ref, "sharded grad_w")
+    check_grad(g["gz"], gz_ref, "sharded grad_z")
+    check_grad(g["gr"], gr_ref, "sharded grad_rho")
+    d = max(np.linalg.norm(g[k] - single[k]) / np.linalg.norm(single[k]) for k in ("gw", "gz", "gr"))
+    record("sharded vs single-context gradient rel", d, 1e-5)
+    assert d < 1e-5
+
+
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_sharded_step_matches_single(engine):
+    """Three Alg.-1 outer iterations (sqngd_step A+B, eager for the loopback group) on 2 ranks: the state
+    stays identical across ranks and within rounding of the single-context run."""
+    c = Cfg("mr-step", M=2, N=48, B=4, K=17, f_lo=-0.5, f_hi=0.5, R=2, r_n=4, n_h=2, n_x=2, lr_z=1e-3,
+            loss_mode=CF.LOSS_LSE, beta_or_p=60.0, doppler_engine=ENGINES[engine])
+    z, rho, q, w0 = inputs_for(c, 93)
+    w = q["s_hard"].astype(np.complex64)
+
+    def run(ctx, r):
+        st = ctx.new_state(T(z), T(rho), T(w))
+        hist = torch.zeros((c.R, c.n_h + c.n_x), dtype=torch.float64, device=DEV)
+        for _ in range(3):
+            ctx.step(st, sqngd.BLOCK_AB, hist=hist)
+        ctx.sync()
+        return {k: st[k].cpu().numpy() for k in ("z", "rho", "w")} | {"hist": hist.cpu().numpy()}
+
+    res = on_ranks(c, 2, run)
+    single = run(sqngd.Context(c), 0)
+    for k in ("z", "rho", "w", "hist"):
+        assert np.array_equal(res[1][k], res[0][k]), k
+    np.testing.assert_allclose(res[0]["hist"], single["hist"], rtol=1e-6)
+    np.testing.assert_allclose(res[0]["w"], single["w"], rtol=0, atol=1e-5)
+    np.testing.assert_allclose(res[0]["z"], single["z"], rtol=0, atol=1e-6)
+    np.testing.assert_allclose(res[0]["rho"], single["rho"], rtol=0, atol=1e-6)
+
+
+def test_c5_row_shard_gradient_8_ranks():
+    """The Chebyshev engine's row shard at C5 shape (M = 16, N = 4096, P = 8192) with 8 loopback ranks and
+    a reduced grid (K = 9 of the C5 grid): the sharded Step-B gradient equals the single-context one."""
+    c = CF.C5.with_(R=1, K=9, loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=sqngd.ENGINE_CHEBYSHEV)
+    z, rho, q, w = inputs_for(c, 5)
+
+    def run(ctx, r):
+        met, gz, gr = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
+        m = ctx.metrics(met)
+        ctx.sync()
+        return m, gz.cpu().numpy(), gr.cpu().numpy()
+
+    res = on_ranks(c, 8, run)
+    m1, gz1, gr1 = run(sqngd.Context(c), 0)
+    for r in range(8):
+        assert np.array_equal(res[r][1], res[0][1]) and np.array_equal(res[r][2], res[0][2])
+    check_loss(res[0][0][0]["loss"], m1[0]["loss"], "C5-shape 8-rank loss vs single")
+    d = np.linalg.norm(res[0][1] - gz1) / np.linalg.norm(gz1)
+    record("C5-shape 8-rank grad_z vs single", d, 1e-5)
+    assert d < 1e-5

@@ -1,9 +1,12 @@
 """World-size-2 tests of the multi-rank host logic on CPU (gloo backend).
 
-The max-then-sum protocol that libsqngd runs over NCCL (csrc/comm.h) is exercised
-here with torch.distributed/gloo: each rank evaluates half of the Doppler bins with the
-fp64 oracle, the partials are combined with parallel.combine_lse, and the result must
-equal the oracle's single-process evaluation of the full grid."""
+The one-collective protocol that libsqngd runs over NCCL (csrc/comm.h: weighted fp64 SUM
+against a shared reference shift, MAX of the keys) is exercised here with
+torch.distributed/gloo: each rank evaluates half of the Doppler bins with the fp64
+oracle, the partials are combined with parallel.combine_ref for several reference shifts
+(0, a stale previous maximum, the exact maximum), and the result must equal the
+oracle's single-process evaluation of the full grid.  The library's own sharded kernels
+are tested on the GPU through the loopback group (tests/test_gpu_multirank.py)."""
 import math
 import os
 import socket
@@ -67,16 +70,17 @@ def _worker(rank, port, mode, q):
         else:
             S_r = (L_r / m_r) ** p
             G_r = np.concatenate([gw.ravel(), gs.ravel()]) / S_r ** (1.0 / p - 1.0)
-        G = torch.from_numpy(np.stack([G_r.real, G_r.imag], -1))
-        m, S, Gt = parallel.combine_lse(m_r, S_r, G, p, mode=mode)
-        Gc = Gt.numpy()[..., 0] + 1j * Gt.numpy()[..., 1]
-        if mode == 1:
-            loss, grad = m + math.log(S) / p, Gc / S
-        else:
-            loss, grad = m * S ** (1.0 / p), Gc * S ** (1.0 / p - 1.0)
+        g_loc = G_r / S_r if mode == 1 else G_r * S_r ** (1.0 / p - 1.0)   # locally normalised
+        g = torch.from_numpy(np.stack([g_loc.real, g_loc.imag], -1))
+        outs = []
+        for m_ref in ((0.0 if mode == 1 else 1.0), 0.8, None):  # shared: the create value, a stale one, exact
+            if m_ref is None:  # the exact global maximum, from a previous round
+                _, _, m_ref = parallel.combine_ref(m_r, S_r, g, 0.0 if mode == 1 else 1.0, p, mode=mode)
+            loss, Gt, mg = parallel.combine_ref(m_r, S_r, g, m_ref, p, mode=mode)
+            outs.append((loss, Gt.numpy()[..., 0] + 1j * Gt.numpy()[..., 1], mg))
         tmax = parallel.max_over_ranks(float(rank + 1))
         if rank == 0:
-            q.put((loss, grad, tmax))
+            q.put((outs, tmax))
     finally:
         dist.destroy_process_group()
 
@@ -91,7 +95,7 @@ def test_sharded_lse_combine_matches_single_process(mode):
     procs = [ctx.Process(target=_worker, args=(r, port, mode, q)) for r in range(WORLD)]
     for p_ in procs:
         p_.start()
-    loss, grad, tmax = q.get(timeout=120)
+    outs, tmax = q.get(timeout=120)
     for p_ in procs:
         p_.join(timeout=60)
         assert p_.exitcode == 0
@@ -99,8 +103,10 @@ def test_sharded_lse_combine_matches_single_process(mode):
     s, w = _inputs(c)
     met, gw, gs = O.loss_grad(c, s, w)
     ref = np.concatenate([gw.ravel(), gs.ravel()])
-    assert abs(loss - met[0]["loss_wpsl"]) < 1e-12 * abs(met[0]["loss_wpsl"])
-    assert np.abs(grad - ref).max() < 1e-10 * np.abs(ref).max()
+    for loss, grad, mg in outs:  # exact for every reference shift
+        assert abs(loss - met[0]["loss_wpsl"]) < 1e-12 * abs(met[0]["loss_wpsl"])
+        assert np.abs(grad - ref).max() < 1e-10 * np.abs(ref).max()
+        assert mg == met[0]["wpsl"]          # the new reference: the global maximum
     assert tmax == float(WORLD)
 
 
