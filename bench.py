@@ -607,7 +607,10 @@ def main():
                          "what": "Step A only (filters), Step B only (transmit), and the MAX loss (Eq. 37, O(N) "
                                  "subgradient adjoint) instead of LSE; each 10 graph-replayed steps"}
     if args.work_sharded:  # C5 (8 restarts) with its pair / Doppler work sharded over the N ranks
-        line["work_sharded"] = work_sharded(args, world, rank, local, dev, stream, flush)
+        try:
+            line["work_sharded"] = work_sharded(args, world, rank, local, dev, stream, flush)
+        except Exception as e:  # reported, not fatal to the headline
+            line["work_sharded"] = {"error": f"{type(e).__name__}: {e}"}
     if args.batch_restarts > 1 and c.R == 1:  # the same config with B independent restarts per GPU
         ctxb, *_rest, b_run = timed(c.with_(R=args.batch_restarts), False)
         ctxb.close()
