@@ -701,6 +701,7 @@ struct AdjGArgs {
   int M, N, Q, LS, nch, csh, units, mode;  // csh: log2 of the k_lr unit's lag chunk (5 or 4)
   int row_lo, row_hi;    // this rank's (restart, transmit channel) rows; other rows contribute zeros
   int u0;                // k_adj_gc: first CTA unit of the shard
+  int lsplit;            // k_adj_gc: CTAs per node, each summing M / lsplit of the l (its own partial slot)
   float bp;
   const float2* Gn;      // node cotangents (unit-scaled)
   const float* um;       // per k_lr unit: its shift (part.m)
@@ -784,9 +785,10 @@ __global__ void __launch_bounds__(PL::T* G, MINB) k_adj_g(const AdjGArgs a, cons
 }
 
 // Step-B node adjoints with the sum over l inside the CTA: NG groups of one CTA split l and their
-// accumulators are summed in shared memory in group order (deterministic).  CTA = node (r, m, q)
-// (u0 + blockIdx.x: this rank's rows):
-//   e = IFFT_P(sum_l FFT(G^_{ml,q}) H_l),   tslot[node][n] = e(n) conj(V_q(n)).
+// accumulators are summed in shared memory in group order (deterministic).  CTA u = node * lsplit + h,
+// node = (r M + m) Q + q (u0 + blockIdx.x: this rank's rows); CTA h of a node takes the l in
+// [h M / lsplit, (h + 1) M / lsplit) (the IFFT is linear, so the combine adds the lsplit partials):
+//   e_h = IFFT_P(sum_l FFT(G^_{ml,q}) H_l),   tslot[u][n] = e_h(n) conj(V_q(n)).
 template <class PL, int NG>
 __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const float2* __restrict__ ftw) {
   SQ_PDL_WAIT();
@@ -797,15 +799,17 @@ __global__ void __launch_bounds__(PL::T* NG) k_adj_gc(const AdjGArgs a, const fl
   GroupSync sync{1 + grp, T, group_mask(T)};
   const int M = a.M, Q = a.Q, N = a.N;
   const int u = a.u0 + blockIdx.x;
-  const int q = u % Q, rm = u / Q;
+  const int node = u / a.lsplit, h = u - node * a.lsplit;
+  const int q = node % Q, rm = node / Q;
   const int r = rm / M;
+  const int l_lo = (int)((long long)M * h / a.lsplit), l_hi = (int)((long long)M * (h + 1) / a.lsplit);
   const float mf = __uint_as_float(a.lred[r].mbits);
   const float lb = a.bp * 1.4426950408889634f;
   float2 acc[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
   int par = 0;
-  for (int l = grp; l < M; l += NG) {
+  for (int l = l_lo + grp; l < l_hi; l += NG) {
     const int pr = rm * M + l;
     const float2* Gp = a.Gn + ((size_t)pr * Q + q) * a.LS;
     const float* ump = a.um + (size_t)pr * a.nch;

@@ -594,39 +594,26 @@ struct RhoFinish {
   const float* gz;  // grad_z [R][MN]
   AdamP ap;
   const int* status;
-  // fused threshold update: the last threshold block of restart r to finish does Adam(rho) and
-  // the projection (dynamic shared memory 2 n2 floats)
-  int* cnt_r;       // [R] or nullptr (not fused)
-  float *rho, *mr, *vr;
-  AdamP apr;
-  float lo, hi, gap;
 };
 
-// SORT: the block sorts its chunk's (z, dy) pairs by z in shared memory (bitonic, deterministic), and
-// every warp then visits only the elements inside its threshold window (two binary searches)
-// instead of window-testing the whole chunk.  Requires chunk <= 256 (= blockDim.x).
-template <bool SORT>
+// The block sorts its chunk's (z, dy) pairs by z in shared memory (bitonic, deterministic), and every
+// warp then visits only the elements inside its threshold window (two binary searches) instead of
+// window-testing the whole chunk.  chunk = 256 = blockDim.x.
 __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
                                                        const float* __restrict__ rho, const float* __restrict__ dy,
                                                        float* part, RhoFinish fin) {
   SQ_PDL_WAIT();
-  __shared__ __align__(16) float2 zd[1024];  // chunk <= 1024: (z, dy), padded to a multiple of 4
+  __shared__ __align__(16) float2 zd[256];  // the chunk's (z, dy)
   const int r = blockIdx.z;
   const int ch = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const float ri = i < BR ? rho[(size_t)r * BR + i] : rho[(size_t)r * BR + BR - 1];
   const int e0 = ch * chunk, e1 = min(MN, e0 + chunk);
-  if (SORT) {
-    for (int e = threadIdx.x; e < 256; e += blockDim.x)
-      zd[e] = e0 + e < e1 ? make_float2(z[(size_t)r * MN + e0 + e], dy[(size_t)r * MN + e0 + e])
-                          : make_float2(1e30f, 0.f);
-  } else {
-    for (int e = e0 + threadIdx.x; e < e0 + ((e1 - e0 + 3) & ~3); e += blockDim.x)
-      zd[e - e0] = e < e1 ? make_float2(z[(size_t)r * MN + e], dy[(size_t)r * MN + e]) : make_float2(1e30f, 0.f);
-  }
+  for (int e = threadIdx.x; e < 256; e += blockDim.x)
+    zd[e] = e0 + e < e1 ? make_float2(z[(size_t)r * MN + e0 + e], dy[(size_t)r * MN + e0 + e]) : make_float2(1e30f, 0.f);
   __syncthreads();
   const float win = 12.f / c;
-  if (SORT) {
+  {
     // bitonic sort of 256 (z, dy) pairs by z (ties by dy, so the order is a function of the values)
     const int t = threadIdx.x;
     for (int kk = 2; kk <= 256; kk <<= 1)
@@ -672,37 +659,6 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
     }
     if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
   }
-  if (!SORT) {
-  float wlo = ri, whi = ri;  // the warp's threshold range (any order)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
-    whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
-  }
-  wlo -= win;
-  whi += win;
-  const float k2 = -2.f * 1.4426950408889634f;
-  float acc = 0.f;
-  const int n = e1 - e0;
-  const float4* zd4 = reinterpret_cast<const float4*>(zd);
-  for (int q = 0; q < n; q += 4) {  // four elements per (warp-uniform) window test
-    const float4 pa = zd4[q >> 1], pb = zd4[(q >> 1) + 1];
-    const float zz[4] = {pa.x, pa.z, pb.x, pb.z}, dd[4] = {pa.y, pa.w, pb.y, pb.w};
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) any |= zz[k] >= wlo && zz[k] <= whi;
-    if (!any) continue;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float au = c * fabsf(zz[k] - ri);   // z - rho exact when close (Sterbenz)
-      const float e2 = ex2a_m(k2 * au);         // e^{-2|u|}
-      const float inv = rcp_m(1.f + e2);
-      const float sech2 = 4.f * e2 * inv * inv;  // sech^2(u)
-      acc = fmaf(au < 12.f ? sech2 : 0.f, dd[k], acc);
-    }
-  }
-  if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
-  }
   if (!fin.gsum && !fin.z) return;
   __shared__ int last_tb, last_ch;
   __threadfence();
@@ -726,23 +682,6 @@ __global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk
 #pragma unroll 8
     for (int k = 0; k < (int)gridDim.y; ++k) g += __ldcg(pp + (size_t)k * BR);
     fin.gsum[(size_t)r * BR + i] = fin.coef * g;
-  }
-  if (last_tb && fin.cnt_r) {  // the last threshold block of the restart: Adam(rho) + projection
-    __shared__ int last_r;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      last_r = atomicAdd(fin.cnt_r + r, 1) == (int)gridDim.x - 1;
-      if (last_r) fin.cnt_r[r] = 0;
-    }
-    __syncthreads();
-    if (last_r) {
-      __threadfence();
-      extern __shared__ float rho_sr[];
-      if (!(*fin.status & ST_NONFINITE))
-        adam_project_rho_dev(r, BR, fin.rho, fin.mr, fin.vr, fin.gsum + (size_t)r * BR, fin.apr, fin.lo, fin.hi,
-                             fin.gap, rho_sr);
-    }
   }
   if (last_ch && !(*fin.status & ST_NONFINITE)) {  // Adam on this chunk's z (keep the last finite iterate)
     float c1, c2;

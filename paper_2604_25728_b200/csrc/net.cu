@@ -639,188 +639,6 @@ __global__ void __cluster_dims__(NET_CL, 1, 1) __launch_bounds__(128) k_net_mid_
   // every CTA received all of its expected bytes, so no st.async can still target this CTA
 }
 
-// ---- single-CTA variants: one 512-thread CTA per restart streams the full hidden matrices through a
-// double-buffered shared-memory ring with TMA bulk copies (matrix s + 2 is fetched while s + 1 is
-// used), so there is no cross-CTA exchange at all; a layer costs one 64 KB bulk copy (W = 128).
-constexpr int NET_ST = 512;  // threads of the streamed kernels
-
-// hidden matrix s of the forward order (s = 2d: W1_d, s = 2d + 1: W2_d); offset in theta
-__device__ __forceinline__ size_t hid_off(const NetArgs& a, int d, int which) {
-  const size_t stride_d = 2 * (size_t)a.W * a.W + 2 * (size_t)a.W;
-  return a.o_blk + d * stride_d + (which ? (size_t)a.W * a.W + a.W : 0);
-}
-
-__device__ __forceinline__ void ring_fetch(const NetArgs& a, const float* th, float* buf, uint64_t* bar, int d, int which) {
-  const uint32_t bytes = (uint32_t)a.W * a.W * 4u;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of buf before the async write
-  mbar_expect_tx(bar, bytes);
-  bulk_g2s(buf, th + hid_off(a, d, which), bytes, bar);
-}
-
-// rows of a W x W matrix in shared memory dotted with x: warp w owns rows w, w + 16, ... (<= 8 each)
-__device__ __forceinline__ void rows_dot8(const float* Wm, int W, const float* x, int warp, int lane, float p[8]) {
-  const float4 xv = lane < (W >> 2) ? reinterpret_cast<const float4*>(x)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = warp + 16 * k;
-    p[k] = 0.f;
-    if (i < W && lane < (W >> 2)) {
-      const float4 w = reinterpret_cast<const float4*>(Wm + (size_t)i * W)[lane];
-      p[k] = w.x * xv.x;
-      p[k] = fmaf(w.y, xv.y, p[k]);
-      p[k] = fmaf(w.z, xv.z, p[k]);
-      p[k] = fmaf(w.w, xv.w, p[k]);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) p[k] += __shfl_xor_sync(0xffffffffu, p[k], o);
-}
-
-__global__ void __launch_bounds__(NET_ST) k_net_mid_fwd1(NetArgs a) {
-  SQ_PDL_WAIT();
-  extern __shared__ __align__(16) float sm[];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ float sred[NET_ST];
-  const int r = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int W = a.W, D = a.D, nm = 2 * D;
-  float* buf = sm;                                // [2][W][W]
-  float* tv = buf + 2 * (size_t)W * W;            // [2D+1][W] tape
-  float* bs = tv + (size_t)(2 * D + 1) * W;       // [2D][W] biases b1_d, b2_d
-  const float* th = a.theta + (size_t)r * a.P;
-  if (t == 0) {
-    mbar_init(&bar[0]);
-    mbar_init(&bar[1]);
-    if (nm > 0) ring_fetch(a, th, buf, &bar[0], 0, 0);
-    if (nm > 1) ring_fetch(a, th, buf + (size_t)W * W, &bar[1], 0, 1);
-  }
-  for (int k = t; k < nm * W; k += NET_ST) {
-    const int s2 = k / W, i = k - s2 * W;
-    bs[k] = th[hid_off(a, s2 >> 1, s2 & 1) + (size_t)W * W + i];
-  }
-  {  // h_0 = tanh(b_in + sum of the W_in y0 partials): S = NET_ST / W threads per column
-    const int S = NET_ST / W, j = t % W;
-    float acc = 0.f;
-    const float* pp = a.pin + (size_t)r * a.n_in * W + j;
-    for (int q = t / W; q < a.n_in; q += S) acc += pp[(size_t)q * W];
-    sred[t] = acc;
-    __syncthreads();
-    if (t < W) {
-      float g = th[a.o_bin + t];
-      for (int k = 0; k < S; ++k) g += sred[k * W + t];
-      tv[t] = tanhf(g);
-    }
-    __syncthreads();
-  }
-  float p[8];
-  for (int sx = 0; sx < nm; ++sx) {
-    const int b = sx & 1, d = sx >> 1;
-    mbar_wait(&bar[b], (uint32_t)((sx >> 1) & 1));
-    const float* Wm = buf + (size_t)b * W * W;
-    const float* x = (sx & 1) ? tv + (size_t)(D + 1 + d) * W : tv + (size_t)d * W;
-    rows_dot8(Wm, W, x, warp, lane, p);
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = warp + 16 * k;
-        if (i >= W) break;
-        if (sx & 1) tv[(size_t)(d + 1) * W + i] = tv[(size_t)d * W + i] + p[k] + bs[(size_t)sx * W + i];
-        else tv[(size_t)(D + 1 + d) * W + i] = tanhf(p[k] + bs[(size_t)sx * W + i]);
-      }
-    }
-    __syncthreads();  // buf[b] consumed, the new tape row visible
-    if (t == 0 && sx + 2 < nm) ring_fetch(a, th, buf + (size_t)b * W * W, &bar[b], (sx + 2) >> 1, sx & 1);
-  }
-  float* tape = a.tape + (size_t)r * (2 * D + 1) * W;
-  for (int k = t; k < (2 * D + 1) * W; k += NET_ST) tape[k] = tv[k];
-}
-
-// Reverse chain with transposed products out[j] = sum_i Wm[i][j] g[i]: thread (j = t % W, quarter
-// qd = t / W) sums its quarter of the rows, the quarters are added in order.
-__device__ __forceinline__ float cols_dot(const float* Wm, int W, const float* g, int t, float* sred) {
-  const int S = NET_ST / W, j = t % W, qd = t / W, rows = W / S;
-  float acc = 0.f;
-  for (int i = qd * rows; i < (qd + 1) * rows; ++i) acc = fmaf(Wm[(size_t)i * W + j], g[i], acc);
-  sred[t] = acc;
-  __syncthreads();
-  float out = 0.f;
-  if (t < W)
-    for (int k = 0; k < S; ++k) out += sred[k * W + t];
-  return out;
-}
-
-__global__ void __launch_bounds__(NET_ST) k_net_mid_bwd1(NetArgs a) {
-  SQ_PDL_WAIT();
-  extern __shared__ __align__(16) float sm[];
-  __shared__ __align__(8) uint64_t bar[3];
-  __shared__ float sred[NET_ST];
-  const int r = blockIdx.x, t = threadIdx.x;
-  const int W = a.W, D = a.D, nm = 2 * D;
-  float* buf = sm;                                // [2][W][W]
-  float* tv = buf + 2 * (size_t)W * W;            // [2D+1][W] tape
-  float* gh = tv + (size_t)(2 * D + 1) * W;       // [W]
-  float* ga = gh + W;                             // [W]
-  float* gv = ga + W;                             // [D][2][W]
-  const float* th = a.theta + (size_t)r * a.P;
-  const float* tape = a.tape + (size_t)r * (2 * D + 1) * W;
-  // reverse order: sx = 0, 1, ... -> (d, which) = (D-1, W2), (D-1, W1), (D-2, W2), ...
-  auto mat = [&](int sx, int& d, int& which) { d = D - 1 - (sx >> 1); which = (sx & 1) ? 0 : 1; };
-  if (t == 0) {
-    mbar_init(&bar[0]);
-    mbar_init(&bar[1]);
-    mbar_init(&bar[2]);
-    mbar_expect_tx(&bar[2], (2u * D + 1u) * W * 4u);
-    bulk_g2s(tv, tape, (2u * D + 1u) * W * 4u, &bar[2]);
-    int d, wh;
-    if (nm > 0) { mat(0, d, wh); ring_fetch(a, th, buf, &bar[0], d, wh); }
-    if (nm > 1) { mat(1, d, wh); ring_fetch(a, th, buf + (size_t)W * W, &bar[1], d, wh); }
-  }
-  {  // gh = W_out^T go from the n_out partials
-    const int S = NET_ST / W, j = t % W;
-    float acc = 0.f;
-    const float* pp = a.pout + (size_t)r * a.n_out * W + j;
-    for (int q = t / W; q < a.n_out; q += S) acc += pp[(size_t)q * W];
-    sred[t] = acc;
-    __syncthreads();
-    if (t < W) {
-      float g = 0.f;
-      for (int k = 0; k < S; ++k) g += sred[k * W + t];
-      gh[t] = g;
-    }
-    __syncthreads();
-  }
-  mbar_wait(&bar[2], 0);
-  for (int sx = 0; sx < nm; ++sx) {
-    const int b = sx & 1;
-    int d, wh;
-    mat(sx, d, wh);
-    mbar_wait(&bar[b], (uint32_t)((sx >> 1) & 1));
-    const float* Wm = buf + (size_t)b * W * W;
-    if (wh == 1) {  // W2_d: ga = (W2^T gh) tanh'(u_d); factors [gh | ga]
-      const float* u = tv + (size_t)(D + 1 + d) * W;
-      const float o = cols_dot(Wm, W, gh, t, sred);
-      if (t < W) {
-        gv[(size_t)d * 2 * W + t] = gh[t];
-        ga[t] = o * (1.f - u[t] * u[t]);
-        gv[(size_t)d * 2 * W + W + t] = ga[t];
-      }
-    } else {  // W1_d: gh += W1^T ga
-      const float o = cols_dot(Wm, W, ga, t, sred);
-      if (t < W) gh[t] += o;
-    }
-    __syncthreads();  // buf[b] consumed, gh / ga updated
-    if (t == 0 && sx + 2 < nm) {
-      int d2, wh2;
-      mat(sx + 2, d2, wh2);
-      ring_fetch(a, th, buf + (size_t)b * W * W, &bar[b], d2, wh2);
-    }
-  }
-  for (int j = t; j < W; j += NET_ST) a.ga0[(size_t)r * W + j] = gh[j] * (1.f - tv[j] * tv[j]);
-  float* gvec = a.gvec + (size_t)r * D * 2 * W;
-  for (int k = t; k < 2 * D * W; k += NET_ST) gvec[k] = gv[k];
-}
-
 NetArgs make_args(const NetDims& d, const NetWs& ws) {
   NetArgs a{};
   a.Din = d.Din; a.W = d.W; a.D = d.D; a.n_in = d.n_in; a.n_out = d.n_out;
@@ -858,16 +676,9 @@ bool net_dims(int R, int Din, int W, int D, NetDims* out, const char** why) {
   d.smem_bwd = (2 * (size_t)D * RW * w + (2 * (size_t)D + 1) * w + 2 * w + 2 * NET_CL * w + 128 + 2 * (size_t)D * w) *
                sizeof(float);
   if (d.smem_bwd > 200 * 1024) { *why = "generator: hidden layers exceed the cluster's shared memory (depth too large)"; return false; }
-  d.smem_fwd1 = (2 * w * w + (2 * (size_t)D + 1) * w + 2 * (size_t)D * w) * sizeof(float);
-  d.smem_bwd1 = (2 * w * w + (2 * (size_t)D + 1) * w + 2 * w + 2 * (size_t)D * w) * sizeof(float);
-  // Single-CTA streamed hidden chain: measured slower than the 8-CTA cluster at C3 (forward 18.4 vs
-  // 10.8 us, backward 16.6 vs 11.9 us: one SM pulls the 640 KB of hidden weights at ~50 GB/s), so it
-  // is opt-in (SQNGD_NET_STREAM=1).  It splits 512 threads evenly over columns and row quarters:
-  // W in {32, 64, 128}.
-  d.streamed = false;
-  if (const char* ev = getenv("SQNGD_NET_STREAM"))
-    d.streamed = ev[0] == '1' && NET_ST % W == 0 && (W * W) % NET_ST == 0 && d.smem_bwd1 <= 200 * 1024 &&
-                 d.smem_fwd1 <= 200 * 1024;
+  // (a single-CTA variant streaming the hidden matrices through a TMA ring measured slower than the
+  // 8-CTA cluster at C3 -- forward 18.4 vs 10.8 us, backward 16.6 vs 11.9 us: one SM pulls the 640 KB
+  // of hidden weights at ~50 GB/s -- and was removed in round 2)
   *out = d;
   return true;
 }
@@ -891,12 +702,6 @@ NetWs net_ws_carve(const NetDims& d, float* base) {
 
 cudaError_t net_prepare(const NetDims& d) {
   cudaError_t e;
-  if (d.streamed) {
-    e = cudaFuncSetAttribute(k_net_mid_fwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem_fwd1);
-    if (e) return e;
-    e = cudaFuncSetAttribute(k_net_mid_bwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem_bwd1);
-    if (e) return e;
-  }
   e = cudaFuncSetAttribute(k_net_mid_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem_fwd);
   if (e) return e;
   return cudaFuncSetAttribute(k_net_mid_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem_bwd);
@@ -912,8 +717,7 @@ cudaError_t net_forward(const NetDims& d, const NetWs& ws, const float* theta, c
     launch_upd<NM_FWD>(d, a, st);
     *launches += 1;
   }
-  if (d.streamed) k_net_mid_fwd1<<<d.R, NET_ST, d.smem_fwd1, st>>>(a);
-  else k_net_mid_fwd<<<dim3(NET_CL, d.R), 128, d.smem_fwd, st>>>(a);
+  k_net_mid_fwd<<<dim3(NET_CL, d.R), 128, d.smem_fwd, st>>>(a);
   k_net_out<<<dim3((d.Din + NET_FWD_ROWS - 1) / NET_FWD_ROWS, d.R), 256, 0, st>>>(a);
   *launches += 2;
   return cudaGetLastError();
@@ -928,13 +732,11 @@ cudaError_t net_backward(const NetDims& d, const NetWs& ws, float* theta, const 
   const dim3 go(d.n_out * NET_CL, d.R), gm(NET_CL, d.R);
   if (gtheta) {
     k_net_out_bwd<NM_GRAD><<<go, 256, 0, st>>>(a);
-    if (d.streamed) k_net_mid_bwd1<<<d.R, NET_ST, d.smem_bwd1, st>>>(a);
-    else k_net_mid_bwd<<<gm, 128, d.smem_bwd, st>>>(a);
+    k_net_mid_bwd<<<gm, 128, d.smem_bwd, st>>>(a);
     launch_upd<NM_GRAD>(d, a, st);
   } else {
     k_net_out_bwd<NM_ADAM><<<go, 256, 0, st>>>(a);
-    if (d.streamed) k_net_mid_bwd1<<<d.R, NET_ST, d.smem_bwd1, st>>>(a);
-    else k_net_mid_bwd<<<gm, 128, d.smem_bwd, st>>>(a);
+    k_net_mid_bwd<<<gm, 128, d.smem_bwd, st>>>(a);
     launch_upd<NM_ADAM>(d, a, st);
   }
   *launches += 3;

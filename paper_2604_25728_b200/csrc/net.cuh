@@ -24,8 +24,6 @@ struct NetDims {
   int n_out = 0;                                  // clusters of W_out row chunks (partials of W_out^T g)
   int n_hid = 0;                                  // k_net_hid CTAs per restart
   size_t smem_fwd = 0, smem_bwd = 0;              // dynamic shared memory of the cluster kernels
-  size_t smem_fwd1 = 0, smem_bwd1 = 0;            // ... of the single-CTA streamed kernels
-  bool streamed = false;                          // hidden layers: single-CTA streamed (else cluster)
 };
 
 struct NetWs {

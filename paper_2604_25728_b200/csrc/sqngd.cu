@@ -77,12 +77,8 @@ struct sqngd_ctx_s {
   float* dy = nullptr;         // [R][M][N]
   float* rho_part = nullptr;   // [R][nchunk][BR]
   int rho_chunk = 256, rho_nchunk = 1;
-  bool rho_sort = true;        // k_grad_rho_part sorts its chunk (needs rho_chunk <= 256)
-  // Adam(rho) + projection: a 1024-thread kernel (default) or the last 256-thread grad-rho block.  As
-  // the optimization proceeds the thresholds form clusters that Adam reorders every step, so the
-  // projection's sort runs every step: measured at C3, the fused tail is 5 us/step faster in the
-  // first steps but 40 us/step slower after ~40 outer iterations (SQNGD_FUSE_RHO=1: fused).
-  bool fuse_rho = false;
+  // Adam(rho) + projection: a 1024-thread kernel.  As the optimization proceeds the thresholds form
+  // clusters that Adam reorders every step, so the projection's sort runs every step.
   int* rho_cnt = nullptr;      // [R][64] threshold-block + [R][nchunk] element-chunk arrival counters
   float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
   float* gz = nullptr;         // [R][M][N]
@@ -93,6 +89,7 @@ struct sqngd_ctx_s {
   bool lr = false;
   int Q = 0, QS = 0, nch = 0, kw = 1, LS = 0;
   int nch16 = 0, NT = 0, NTF = 0;
+  int lsplit = 1;              // k_adj_gc CTAs per node (fills the GPU when R M Q nodes are few)
   float4* tabF = nullptr;      // [NT][32][2] k_lrt forward B fragments
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
   uint4* tabF16 = nullptr;     // [NT][32] k_lrt forward B fragments (FP16 packed split)
@@ -141,7 +138,6 @@ struct sqngd_ctx_s {
   std::vector<GraphEntry*> graphs;
   GraphEntry* capturing = nullptr;
   bool use_graphs = true;
-  bool pdl = false;            // programmatic kernel-to-kernel edges in the step graph (SQNGD_PDL=1: on)
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -680,7 +676,6 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
   CK(cudaMalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
-  if (const char* e = getenv("SQNGD_PDL")) ctx->pdl = e[0] == '1';
   CK(cudaMalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   CK(cudaMalloc(&ctx->s_soft, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
@@ -694,13 +689,6 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   CK(cudaMalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
   CK(cudaMalloc(&ctx->red_grad, sizeof(float2) * RMN));
   CK(cudaMalloc(&ctx->dy, sizeof(float) * RMN));
-  if (const char* ev = getenv("SQNGD_RHO_CHUNK")) {  // tuning override: elements per grad-rho block
-    const int ch = atoi(ev);
-    if (ch >= 32 && ch <= 1024 && ch % 4 == 0) ctx->rho_chunk = ch;
-  }
-  if (const char* ev = getenv("SQNGD_RHO_SORT")) ctx->rho_sort = ev[0] != '0';
-  if (const char* ev = getenv("SQNGD_FUSE_RHO")) ctx->fuse_rho = ev[0] == '1';
-  if (ctx->rho_chunk > 256) ctx->rho_sort = false;
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   {  // Adam(rho) + projection: 2 n2 floats of dynamic shared memory (64 KB at B r_n = 8192, above
      // the 48 KB a launch gets without opting in)
@@ -869,7 +857,9 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
-    CK(cudaMalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ((cfg.N + 1) & ~1)));
+    // (splitting each node's l sum over 2 CTAs to fill more SMs at C3 (80 nodes) measured no gain:
+    // 10543 vs 10685 evals/s; lsplit stays 1)
+    CK(cudaMalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ctx->lsplit * ((cfg.N + 1) & ~1)));
   }
 
   {  // this rank's shard of the Chebyshev engine's (restart, transmit channel) rows
@@ -1246,17 +1236,20 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     ag.M = c.M; ag.N = c.N; ag.Q = ctx->Q; ag.LS = ctx->LS;
     ag.nch = ctx->nch16; ag.csh = 4;
     ag.units = c.R * c.M * c.M * ctx->Q; ag.mode = c.loss_mode; ag.bp = (float)c.beta_or_p;
-    ag.row_lo = ctx->row_lo; ag.row_hi = ctx->row_hi; ag.u0 = ctx->row_lo * ctx->Q;
+    ag.row_lo = ctx->row_lo; ag.row_hi = ctx->row_hi; ag.lsplit = ctx->lsplit;
+    ag.u0 = ctx->row_lo * ctx->Q * ctx->lsplit;
     ag.Gn = ctx->Gn; ag.um = ctx->part.m; ag.lred = ctx->lred; ag.Xc = ctx->Xc; ag.H = ctx->H; ag.out = ctx->part.g;
     ag.Vt = ctx->Vt; ag.tslot = ctx->tslot; ag.NS = (c.N + 1) & ~1;
     with_P(ctx->P, [&](auto Lc) {
-      if (wrt == SQNGD_WRT_TRANSMIT) decltype(Lc)::adj_gc(ag, (ctx->row_hi - ctx->row_lo) * ctx->Q, ctx->ftwn, st);
+      if (wrt == SQNGD_WRT_TRANSMIT)
+        decltype(Lc)::adj_gc(ag, (ctx->row_hi - ctx->row_lo) * ctx->Q * ctx->lsplit, ctx->ftwn, st);
       else decltype(Lc)::adj_g(ag, ctx->ftwn, st);
     });
     ca.part.scale = nullptr;  // node cotangents were rescaled in the adjoint kernels
     CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // S and the metrics from k_lr_finish
     if (wrt == SQNGD_WRT_TRANSMIT) {  // node time-domain partials of this rank's rows
-      ca.K = ctx->Q; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = ctx->row_lo * ctx->Q; ca.u_hi = ctx->row_hi * ctx->Q;
+      const int QS_ = ctx->Q * ctx->lsplit;  // (node, half) slots per row
+      ca.K = QS_; ca.slot_stride = (c.N + 1) & ~1; ca.u_lo = ctx->row_lo * QS_; ca.u_hi = ctx->row_hi * QS_;
       ca.part.g = ctx->tslot; ca.len = c.N; ca.extra = 1.0;
       ca.fin = multi ? 0 : 1;
       ca.out = multi ? ctx->red_grad : nullptr;
@@ -1350,8 +1343,7 @@ static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho
   RhoFinish fin{};
   fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
   fin.gsum = grad_rho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64; fin.status = ctx->status;
-  if (ctx->rho_sort) k_grad_rho_part<true><<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
-  else k_grad_rho_part<false><<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
+  k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
   ctx->launches += 1;
   return launch_check(ctx, "grad rho");
 }
@@ -1440,35 +1432,6 @@ sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* 
 
 }  // extern "C"
 
-// Programmatic dependent launch inside the step graph: every kernel-to-kernel edge of the captured
-// graph becomes a programmatic edge, so the next kernel is launched while its predecessor drains
-// (every library kernel starts with griddepcontrol.wait, SQ_PDL_WAIT, before any dependent access).
-// Measured on sm_100a: a dependent kernel node costs 1.12 us, 0.88 us programmatic (tools/ubench_pdl.cu),
-// but the C3 step gains nothing (1.79 ms either way; generator mode -0.4%), so it is opt-in.
-static cudaError_t make_edges_programmatic(cudaGraph_t g, int* converted) {
-  size_t n = 0;
-  cudaError_t e = cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &n);
-  if (e != cudaSuccess || n == 0) return e;
-  std::vector<cudaGraphNode_t> from(n), to(n);
-  std::vector<cudaGraphEdgeData> ed(n);
-  if ((e = cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &n)) != cudaSuccess) return e;
-  *converted = 0;
-  for (size_t i = 0; i < n; ++i) {
-    cudaGraphNodeType tf, tt;
-    if ((e = cudaGraphNodeGetType(from[i], &tf)) != cudaSuccess) return e;
-    if ((e = cudaGraphNodeGetType(to[i], &tt)) != cudaSuccess) return e;
-    if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel || ed[i].type != cudaGraphDependencyTypeDefault)
-      continue;
-    if ((e = cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1)) != cudaSuccess) return e;
-    cudaGraphEdgeData pe{};
-    pe.type = cudaGraphDependencyTypeProgrammatic;
-    pe.from_port = cudaGraphKernelNodePortProgrammatic;
-    if ((e = cudaGraphAddDependencies_v2(g, &from[i], &to[i], &pe, 1)) != cudaSuccess) return e;
-    ++*converted;
-  }
-  return cudaSuccess;
-}
-
 // The body of one sqngd_step: every launch goes to `st` (capturable).  Adam reads the
 // step counters from ctx->d_t (set before the body), so the same graph serves every call.
 static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, double* loss_hist,
@@ -1535,22 +1498,11 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
           fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
         }
         fin.status = ctx->status;
-        const bool fuse_rho = ctx->BR <= 4096 && ctx->fuse_rho;  // 2 n2 floats within the default 48 KB
-        if (fuse_rho) {
-          fin.cnt_r = ctx->rho_cnt + (size_t)c.R * (64 + ctx->rho_nchunk);
-          fin.rho = stt->rho; fin.mr = stt->m_rho; fin.vr = stt->v_rho; fin.apr = ap(c.lr_z, 1, i);
-          fin.lo = 1e-4f; fin.hi = 1.0f - 1e-4f; fin.gap = 1e-6f;
-        }
-        if (ctx->rho_sort)
-          k_grad_rho_part<true><<<g1, 256, fuse_rho ? 2 * n2 * sizeof(float) : 0, st>>>(
-              c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy, ctx->rho_part, fin);
-        else
-          k_grad_rho_part<false><<<g1, 256, fuse_rho ? 2 * n2 * sizeof(float) : 0, st>>>(
-              c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy, ctx->rho_part, fin);
-        if (!fuse_rho)
-          k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
-                                                                        ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
-                                                                        1.0f - 1e-4f, 1e-6f, ctx->status);
+        k_grad_rho_part<<<g1, 256, 0, st>>>(c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy,
+                                            ctx->rho_part, fin);
+        k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
+                                                                      ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
+                                                                      1.0f - 1e-4f, 1e-6f, ctx->status);
         ctx->launches += 2;
       }
       if (ctx->net) {  // Adam on theta through the generator's adjoint, then z = f_theta(y0) again
@@ -1621,15 +1573,6 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
         delete ge;
         if (rc) return rc;
         return fail(ctx, SQNGD_E_CUDA, "sqngd_step: graph capture", cudaGetErrorString(e));
-      }
-      if (ctx->pdl) {
-        int nconv = 0;
-        e = make_edges_programmatic(graph, &nconv);
-        if (e != cudaSuccess) {
-          cudaGraphDestroy(graph);
-          delete ge;
-          return fail(ctx, SQNGD_E_CUDA, "sqngd_step: programmatic graph edges", cudaGetErrorString(e));
-        }
       }
       e = cudaGraphInstantiate(&ge->exec, graph, 0);
       cudaGraphDestroy(graph);

@@ -309,14 +309,12 @@ def test_correlation_mode_K1(mode):
     check_grad(gs.cpu().numpy(), gs_ref, "grad_s")
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
-def test_threshold_projection_with_clusters(fuse, monkeypatch):
+def test_threshold_projection_with_clusters():
     """Thresholds in clusters of 64 spaced 1e-6 apart (the state long runs reach) with a large rate:
     Adam reorders the clusters, so the projection (Q22: sort, clamp, min-gap sweep) does real work.
-    The GPU step (1024-thread projection kernel with the register/shuffle bitonic sort, or the fused
-    256-thread tail) matches the oracle's Adam + projection on the same gradient.  Tolerance 2e-5:
+    The GPU step (1024-thread projection kernel with the register/shuffle bitonic sort) matches the
+    oracle's Adam + projection on the same gradient.  Tolerance 2e-5:
     the fp32 min-gap sweep accumulates 1e-6 steps along a 64-long cluster."""
-    monkeypatch.setenv("SQNGD_FUSE_RHO", fuse)
     c = Cfg("clus", M=2, N=64, B=16, K=9, f_lo=-0.5, f_hi=0.5, r_n=100, n_h=1, n_x=1, lr_z=1e-2,
             doppler_engine=sqngd.ENGINE_FFT)
     z = inputs.phase_params(1, c.M, c.N, config_index=17)

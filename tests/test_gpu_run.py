@@ -136,3 +136,40 @@ def test_alg1_improves_hard_psl():
     q = ctx.quantize(best["z"], best["rho"], soft=False, want_b=False, want_dq=False)
     met, _, _ = ctx.af_forward(q["s_hard"], best["w"])
     assert ctx.metrics(met)[0]["wpsl"] == float(bw.cpu()[0])
+
+
+def _best_pslr(c, T=60, seed=7):
+    """Mean over the restarts of the Alg.-1 best snapshot's hard PSLR (Eq. 48), matched start."""
+    ctx = sqngd.Context(c)
+    z = torch.as_tensor(inputs.phase_params(c.R, c.M, c.N, config_index=seed), device=DEV)
+    rho = torch.as_tensor(inputs.init_thresholds(c.R, c.B, c.r_n), device=DEV)
+    w = ctx.quantize(z, rho, soft=False, want_b=False, want_dq=False)["s_hard"]
+    st = ctx.new_state(z, rho, w)
+    best, bw, bi, hist, res = ctx.run(st, T=T, patience=0, want_hist=False)
+    ctx.sync()
+    return float(np.mean(20 * np.log10(bw.cpu().numpy())))
+
+
+def test_trend_table2_snrl_relaxation():
+    """NEXT-3 reduced-T trend: the direction of PAPER.md Table II: a larger SNRL
+    allowance mu (Eq. 39, p_tar = 10^{-mu/20}) lets the filters trade mainlobe for sidelobes, so the
+    best hard PSL falls as mu grows (paper, M=2 N=512 B=4: -24.10 / -29.63 / -32.32 / -33.11 dB at
+    mu = 0 / 0.5 / 1 / 1.5).  Here C1 shape, 4 restarts, T = 60 (profiles/r02_trend_tables_II_III.json:
+    -16.09 / -17.38 / -17.85 / -18.10 dB)."""
+    from paper_2604_25728_b200.configs import C1
+
+    base = C1.with_(R=4, loss_mode=sqngd.LOSS_LSE, beta_or_p=200.0)
+    p = {mu: _best_pslr(base.with_(mu_db=mu)) for mu in (0.0, 0.5, 1.0, 1.5)}
+    assert p[0.0] > p[0.5] + 0.5 > p[1.5] + 0.5, p
+    assert p[1.0] < p[0.5] and p[1.5] <= p[1.0] + 0.05, p
+
+
+def test_trend_table3_doppler_range():
+    """The direction of PAPER.md Table III: a wider Doppler range is harder, so the best hard
+    PSL rises with it (paper: -48.87 / -43.09 / -36.10 dB for f in [-0.1, 0.1] / [-0.5, 0.5] / [-3, 3]).
+    Here C1 shape, 4 restarts, T = 60 (-19.07 / -17.38 / -14.91 dB)."""
+    from paper_2604_25728_b200.configs import C1
+
+    base = C1.with_(R=4, loss_mode=sqngd.LOSS_LSE, beta_or_p=200.0)
+    p = {f: _best_pslr(base.with_(f_lo=-f, f_hi=f)) for f in (0.1, 0.5, 3.0)}
+    assert p[0.1] + 0.5 < p[0.5] < p[3.0] - 0.5, p
