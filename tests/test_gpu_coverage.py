@@ -275,3 +275,36 @@ def test_step_b_many_thresholds(engine):
     np.testing.assert_allclose(st["z"].cpu().numpy(), ost["z"], rtol=0, atol=1e-6)
     np.testing.assert_allclose(st["rho"].cpu().numpy(), ost["rho"], rtol=0, atol=1e-6)
     assert (np.diff(st["rho"].cpu().numpy()[0]) > 0).all()
+
+
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_determinism_full_size(engine):
+    """Race hygiene at the benchmark size (compute-sanitizer is closed on this pool): the kernels with
+    dynamic scheduling (k_af's atomic unit counter), order-independent atomics (k_lrt / k_node maxima,
+    atomicMax keys) and arrival counters (k_grad_rho_part's last blocks) must give bit-identical
+    metrics and gradients on repeated C3 evaluations and on a repeated Alg.-1 step."""
+    c = CF.C3.with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=ENGINES[engine], n_h=2, n_x=2)
+    z, rho, q, w = seeded_inputs(c)
+    ctx = sqngd.Context(c)
+    outs = []
+    for _ in range(3):
+        mA, gw = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_FILTERS)
+        mA = mA.clone()
+        mB, gz, gr = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
+        outs.append((mA, gw.clone(), mB.clone(), gz.clone(), gr.clone()))
+    ctx.sync()
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert torch.equal(a, b)
+    sts = []
+    for _ in range(2):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            st = ctx.new_state(T(z), T(rho), T(w))
+            for _ in range(2):
+                ctx.step(st, sqngd.BLOCK_AB)
+        torch.cuda.synchronize()
+        sts.append(st)
+    ctx.sync()
+    for k in ("z", "rho", "w", "m_w", "v_w", "m_z", "v_z", "m_rho", "v_rho"):
+        assert torch.equal(sts[0][k], sts[1][k]), k
