@@ -134,6 +134,9 @@ struct sqngd_ctx_s {
     int64_t launches = 0;
     std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> marks;  // event-record nodes (profiling)
     bool replayed = false;
+    cudaGraph_t graph = nullptr;   // kept for the k_set_t node below
+    cudaGraphNode_t set_t = nullptr;  // the step counters' kernel node: its (t_a, t_b) are set per replay
+    cudaKernelNodeParams set_p{};
   };
   std::vector<GraphEntry*> graphs;
   GraphEntry* capturing = nullptr;
@@ -932,6 +935,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
   cudaSetDevice(ctx->dev);
   for (auto* g : ctx->graphs) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
     for (auto& mk : g->marks) {
       cudaEventDestroy(std::get<1>(mk));
       cudaEventDestroy(std::get<2>(mk));
@@ -1541,12 +1545,22 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
   const sqngd_config& c = ctx->cfg;
   const cudaStream_t st = S(stream);
   sqngd_status rc;
-  k_set_t<<<1, 64, 0, st>>>(ctx->d_t, stt->t_a, stt->t_b, ctx->d_ct, ctx->cts, c.n_h, c.n_x, c.adam_b1, c.adam_b2);
-  ctx->launches += 1;
+  // Adam step counters (k_set_t): launched ahead of the body, inside the graph when there is one (its
+  // (t_a, t_b) arguments are rewritten on the instantiated graph before every replay, so a step is one
+  // graph launch with no eager kernel in front of it).
+  long long ta = stt->t_a, tb = stt->t_b;
+  int cts = ctx->cts, nh = c.n_h, nx = c.n_x;
+  double b1 = c.adam_b1, b2 = c.adam_b2;
+  void* set_args[] = {&ctx->d_t, &ta, &tb, &ctx->d_ct, &cts, &nh, &nx, &b1, &b2};
+  auto launch_set_t = [&]() {
+    k_set_t<<<1, 64, 0, st>>>(ctx->d_t, ta, tb, ctx->d_ct, cts, nh, nx, b1, b2);
+    ctx->launches += 1;
+  };
   // Graph path: one GPU or NCCL (the collective is captured with the step), a capturable (non-legacy) stream.
   const bool graph_ok = ctx->use_graphs && !ctx->prof && (ctx->world == 1 || ctx->comm->capturable()) && st != nullptr &&
                         st != cudaStreamLegacy && st != cudaStreamPerThread;
   if (!graph_ok) {
+    launch_set_t();
     if ((rc = step_body(ctx, stt, block, loss_hist, hard_out, st))) return rc;
   } else {
     const void* key[16] = {stt->z, stt->rho, stt->w, stt->m_z, stt->v_z, stt->m_rho, stt->v_rho, stt->m_w, stt->v_w,
@@ -1562,6 +1576,7 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       ctx->capturing = ge;
       const int64_t l0 = ctx->launches;
+      launch_set_t();
       rc = step_body(ctx, stt, block, loss_hist, hard_out, st);
       ctx->capturing = nullptr;
       ge->launches = ctx->launches - l0;
@@ -1574,13 +1589,32 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
         if (rc) return rc;
         return fail(ctx, SQNGD_E_CUDA, "sqngd_step: graph capture", cudaGetErrorString(e));
       }
-      e = cudaGraphInstantiate(&ge->exec, graph, 0);
-      cudaGraphDestroy(graph);
+      // the k_set_t node: the graph's root kernel node running k_set_t
+      size_t nroot = 0;
+      CK(cudaGraphGetRootNodes(graph, nullptr, &nroot));
+      std::vector<cudaGraphNode_t> roots(nroot);
+      if (nroot) CK(cudaGraphGetRootNodes(graph, roots.data(), &nroot));
+      for (cudaGraphNode_t n : roots) {
+        cudaGraphNodeType ty;
+        CK(cudaGraphNodeGetType(n, &ty));
+        if (ty != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp{};
+        CK(cudaGraphKernelNodeGetParams(n, &kp));
+        if (kp.func == reinterpret_cast<void*>(&k_set_t)) { ge->set_t = n; ge->set_p = kp; }
+      }
+      e = ge->set_t ? cudaGraphInstantiate(&ge->exec, graph, 0) : cudaErrorInvalidValue;
+      ge->graph = graph;
       if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
         delete ge;
         return fail(ctx, SQNGD_E_CUDA, "sqngd_step: graph instantiate", cudaGetErrorString(e));
       }
       ctx->graphs.push_back(ge);
+    } else {
+      cudaKernelNodeParams kp = ge->set_p;
+      kp.kernelParams = set_args;
+      kp.extra = nullptr;
+      CK(cudaGraphExecKernelNodeSetParams(ge->exec, ge->set_t, &kp));
     }
     CK(cudaGraphLaunch(ge->exec, st));
     ge->replayed = true;

@@ -1,7 +1,4 @@
-export SQNGD_PARITY_LOG=gpurun_out/parity_r02a.json
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-timeout 1500 python -m pytest tests -m gpu -q -rf -p no:cacheprovider > gpurun_out/gputest_r02a.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/gputest_r02a.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r02a.log 2>&1
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-torch --no-generator --batch-restarts 0 > gpurun_out/bench_r02a.log 2>&1
-tail -5 gpurun_out/gputest_r02a.log
+# full GPU suite (+ parity record) and smoke
+SQNGD_PARITY_LOG=gpurun_out/parity_full.json timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/full.log 2>&1
+echo "tests rc=$?"; tail -3 gpurun_out/full.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/smoke.log
