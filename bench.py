@@ -4,8 +4,9 @@ A *step* is one Algorithm-1 outer iteration through the
 public C-ABI call sqngd_step(block = A+B): n_h = 10 Step-A loss+gradient
 evaluations (X_hard fixed, gradient to the filters, Adam, energy projection) and
 n_x = 10 Step-B evaluations (soft quantizer, gradient to z and rho through Q_A,
-Adam, threshold projection), then the hard-waveform metrics -- every row of
-SURVEY.md §8(a).  value = loss+gradient evaluations per second over all ranks.
+Adam, threshold projection), with the hard-waveform metrics (loss, WAPSL / WCPSL /
+WPSL, PSLR, SNRL) of the iterate the step starts from, scored by its first Step-A
+evaluation -- every row of SURVEY.md §8(a).  value = loss+gradient evaluations per second over all ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
 
@@ -239,7 +240,7 @@ def config_dict(c):
             "cells_per_eval": c.cells, "loss": {0: "max", 1: f"lse beta={c.beta_or_p}",
                                                   2: f"pnorm p={c.beta_or_p}"}[c.loss_mode],
             "step": "1 Alg.1 outer iteration: 10 Step-A + 10 Step-B loss+grad evals, Adam, projections, "
-                    "hard-waveform metrics",
+                    "hard-waveform metrics of the entry iterate (from the first Step-A evaluation)",
             "l2": "256 MiB L2 flush between timed steps (outside the per-step events)"}
 
 

@@ -201,7 +201,10 @@ sqngd_status sqngd_af_loss_grad(sqngd_ctx ctx, const float* z, const float* rho,
    Generator mode: z = f_theta(y0) at the start and after every Step-B update; Step B's Adam
    acts on theta (rate lr_theta) through sqngd_net_backward's adjoint instead of on z.
    loss_hist: NULL or DEVICE [R][n_h + n_x] doubles (loss of each inner step, in order,
-   A first).  hard_out: NULL or DEVICE [R] metrics of the hard waveform after the block.
+   A first).  hard_out: NULL or DEVICE [R] metrics of the hard-quantized iterate the step STARTS from
+   (X_hard of (z, rho) and w on entry, snrl_db_max included): with Step A they are its first
+   evaluation's (that evaluation is exactly this pair), without Step A an explicit forward runs
+   first.  The iterate a step returns is scored by the next step (or sqngd_af_forward).
    On a latched non-finite value the remaining updates are skipped (state unchanged). */
 sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* state, int block, double* loss_hist,
                         sqngd_metrics* hard_out, sqngd_stream stream);

@@ -68,6 +68,7 @@ struct MetricsArgs {
   double* p_out;
   double* loss_hist;
   int hist_stride, hist_col;
+  const double* snrl_in;  // [R] max_m SNRL_m (k_snrl) for the record, or nullptr (NaN in the record)
 };
 
 // Eqs. 7-10, 37-42 for restart r from the combined partials.  Called by one whole warp
@@ -106,7 +107,7 @@ __device__ void metrics_warp(const MetricsArgs& a, int r, int* status) {
   o.apslr_db = 20.0 * log10(o.wapsl);
   o.cpslr_db = 20.0 * log10(o.wcpsl);
   o.pslr_db = 20.0 * log10(o.wpsl);
-  o.snrl_db_max = __longlong_as_double(0x7ff8000000000000ll);
+  o.snrl_db_max = a.snrl_in ? a.snrl_in[r] : __longlong_as_double(0x7ff8000000000000ll);
   if (!isfinite(o.loss)) atomicOr(status, ST_NONFINITE);
   if (a.out) a.out[r] = o;
   if (a.loss_hist) a.loss_hist[(size_t)r * a.hist_stride + a.hist_col] = o.loss;

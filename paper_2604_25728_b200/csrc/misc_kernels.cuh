@@ -969,7 +969,8 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
 // the literal fp64 norms, one block per restart (fixed-order block sums); the restart's maximum goes
 // into metrics[r].snrl_db_max.  A zero s_m^H w_m gives +inf and latches ST_DEGENERATE.
 __global__ void __launch_bounds__(256) k_snrl(int M, int N, const float2* __restrict__ s, const float2* __restrict__ w,
-                                              double* snrl_out, MetricsOut* met, int* status) {
+                                              double* snrl_out, MetricsOut* met, int* status,
+                                              double* worst_out = nullptr) {
   SQ_PDL_WAIT();
   __shared__ double shd[32];
   const int r = blockIdx.x;
@@ -999,6 +1000,7 @@ __global__ void __launch_bounds__(256) k_snrl(int M, int N, const float2* __rest
     worst = fmax(worst, db);
   }
   if (threadIdx.x == 0 && met) met[r].snrl_db_max = worst;
+  if (threadIdx.x == 0 && worst_out) worst_out[r] = worst;
 }
 
 // ------------------------------------------------------------------ a10 multi-GPU (comm.h)

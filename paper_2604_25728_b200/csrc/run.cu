@@ -102,10 +102,14 @@ extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd
   // bookkeeping buffers live in the context (one allocation, reused by every call): the hard-metrics
   // pointer handed to sqngd_step stays the same, so its step graph is captured once
   const size_t R = (size_t)c.R;
+  const size_t nz = (size_t)c.M * c.N, nrho = (size_t)c.B * c.r_n, nw = 2 * (size_t)c.M * c.N;
+  const size_t nth = net ? (size_t)sqngd_net_num_params(&c) : 0;
   const size_t off_stall = R * sizeof(sqngd_metrics), off_lref = off_stall + ((R * sizeof(int) + 7) & ~(size_t)7);
   const size_t off_lcur = off_lref + R * sizeof(double), off_rd = off_lcur + R * sizeof(double);
+  const size_t off_cand = (off_rd + sizeof(RunDev) + 255) & ~(size_t)255;  // the iterate a step starts from
+  const size_t cand_floats = R * (nz + nrho + nw + nth);
   void* host = nullptr;
-  char* ws = static_cast<char*>(sq_ctx_run_ws(ctx, off_rd + sizeof(RunDev), &host, sizeof(RunDev)));
+  char* ws = static_cast<char*>(sq_ctx_run_ws(ctx, off_cand + cand_floats * sizeof(float), &host, sizeof(RunDev)));
   if (!ws || !host) return sq_ctx_fail(ctx, SQNGD_E_NOMEM, "sqngd_run: workspace", "");
   sqngd_metrics* hard = reinterpret_cast<sqngd_metrics*>(ws);
   int* stall = reinterpret_cast<int*>(ws + off_stall);
@@ -113,6 +117,10 @@ extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd
   double* loss_cur = reinterpret_cast<double*>(ws + off_lcur);
   RunDev* rd = reinterpret_cast<RunDev*>(ws + off_rd);
   RunDev* rd_host = static_cast<RunDev*>(host);
+  float* cz = reinterpret_cast<float*>(ws + off_cand);
+  float* crho = cz + R * nz;
+  float* cw = crho + R * nrho;
+  float* cth = cw + R * nw;
   RK(cudaMemsetAsync(stall, 0, sizeof(int) * c.R, st));
   RK(cudaMemsetAsync(rd, 0, sizeof(RunDev), st));
   {  // best_wpsl = +inf, best_iter = 0
@@ -122,24 +130,34 @@ extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd
     RK(cudaMemsetAsync(best_iter, 0, sizeof(int32_t) * c.R, st));
     RK(cudaStreamSynchronize(st));  // (the host `inf` is a stack value)
   }
-  RunPtrs p{};
-  p.z = state->z; p.rho = state->rho; p.w = state->w; p.theta = net ? state->theta : nullptr;
-  p.bz = best->z; p.brho = best->rho; p.bw = best->w; p.btheta = net ? best->theta : nullptr;
-  p.nz = (size_t)c.M * c.N;
-  p.nrho = (size_t)c.B * c.r_n;
-  p.nw = 2 * (size_t)c.M * c.N;
-  p.ntheta = net ? (size_t)sqngd_net_num_params(&c) : 0;
+  // Iterate t (the state after t outer iterations) is scored by the hard metrics of step t + 1, which
+  // evaluates it in its first Step-A evaluation (sqngd_step hard_out); its snapshot source is the copy
+  // taken before that step.  The last iterate is scored by one explicit forward after the loop.
+  RunPtrs pc{};  // snapshot source: the candidate copy
+  pc.z = cz; pc.rho = crho; pc.w = cw; pc.theta = net ? cth : nullptr;
+  pc.bz = best->z; pc.brho = best->rho; pc.bw = best->w; pc.btheta = net ? best->theta : nullptr;
+  pc.nz = nz; pc.nrho = nrho; pc.nw = nw; pc.ntheta = nth;
+  RunPtrs ps = pc;  // snapshot source: the live state (last iterate)
+  ps.z = state->z; ps.rho = state->rho; ps.w = state->w; ps.theta = net ? state->theta : nullptr;
+  auto track = [&](int it, const RunPtrs& p) -> cudaError_t {
+    k_run_track<<<c.R, 256, 0, st>>>(it, hard, opts->tol, best_wpsl, best_iter, stall, loss_ref, loss_cur, wpsl_hist,
+                                     loss_hist, c.R, rd, p);
+    k_run_done<<<1, 1, 0, st>>>(it, stall, loss_ref, loss_cur, c.R, opts->patience, opts->require_loss_decrease, rd);
+    return cudaGetLastError();
+  };
   int64_t t = 0;
   bool stopped = false;
   for (t = 1; t <= opts->T; ++t) {
+    if (t >= 2) {
+      RK(cudaMemcpyAsync(cz, state->z, sizeof(float) * R * nz, cudaMemcpyDeviceToDevice, st));
+      RK(cudaMemcpyAsync(crho, state->rho, sizeof(float) * R * nrho, cudaMemcpyDeviceToDevice, st));
+      RK(cudaMemcpyAsync(cw, state->w, sizeof(float) * R * nw, cudaMemcpyDeviceToDevice, st));
+      if (net) RK(cudaMemcpyAsync(cth, state->theta, sizeof(float) * R * nth, cudaMemcpyDeviceToDevice, st));
+    }
     sqngd_status s = sqngd_step(ctx, state, SQNGD_BLOCK_AB, nullptr, hard, stream);
     if (s != SQNGD_OK) return s;
-    k_run_track<<<c.R, 256, 0, st>>>((int)t, hard, opts->tol, best_wpsl, best_iter, stall, loss_ref, loss_cur,
-                                     wpsl_hist, loss_hist, c.R, rd, p);
-    k_run_done<<<1, 1, 0, st>>>((int)t, stall, loss_ref, loss_cur, c.R, opts->patience,
-                                opts->require_loss_decrease, rd);
-    RK(cudaGetLastError());
-    if (t % opts->check_every == 0 || t == opts->T) {
+    if (t >= 2) RK(track((int)t - 1, pc));
+    if (t % opts->check_every == 0) {
       RK(cudaMemcpyAsync(rd_host, rd, sizeof(RunDev), cudaMemcpyDeviceToHost, st));
       RK(cudaStreamSynchronize(st));
       if (rd_host->done) {
@@ -147,6 +165,15 @@ extern "C" sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd
         break;
       }
     }
+  }
+  if (!stopped) {  // the last iterate T
+    t = opts->T;
+    sqngd_status s = sq_ctx_hard_metrics(ctx, state, hard, stream);
+    if (s != SQNGD_OK) return s;
+    RK(track((int)opts->T, ps));
+    RK(cudaMemcpyAsync(rd_host, rd, sizeof(RunDev), cudaMemcpyDeviceToHost, st));
+    RK(cudaStreamSynchronize(st));
+    stopped = rd_host->done != 0;
   }
   result->iterations = stopped ? rd_host->stop_iter : opts->T;
   result->steps_run = stopped ? t : opts->T;

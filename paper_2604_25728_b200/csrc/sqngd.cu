@@ -116,6 +116,7 @@ struct sqngd_ctx_s {
   void* run_host = nullptr;    // pinned stop-flag mirror
   size_t run_dev_bytes = 0, run_host_bytes = 0;
   long long* d_t = nullptr;    // device Adam step counters (t_a, t_b) at the start of sqngd_step
+  double* snrl_w = nullptr;    // [R] max_m SNRL_m of the step's entry iterate (hard_out via Step A)
   float2* d_ct = nullptr;      // [2][cts] bias corrections of the step's inner iterations (k_set_t)
   int cts = 0;
   // generator z = f_theta(y0) (net.cu, NEXT-2)
@@ -676,6 +677,7 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   CK(cudaMalloc(&ctx->part.scale, sizeof(float) * uslots));
   CK(cudaMalloc(&ctx->counter, 2 * sizeof(int)));
   CK(cudaMalloc(&ctx->d_t, 2 * sizeof(long long)));
+  CK(cudaMalloc(&ctx->snrl_w, sizeof(double) * cfg.R));
   ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
   CK(cudaMalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
@@ -942,7 +944,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
     }
     delete g;
   }
-  void* ptrs[] = {ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+  void* ptrs[] = {ctx->snrl_w, ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
                   ctx->Gn, ctx->tslot, ctx->lred, ctx->pay, ctx->keyb, ctx->mref, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
@@ -1162,14 +1164,15 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
 
 // Forward AF + metrics of (s, w).  Assumes H = FFT(w) is current.
 static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w, float* af_mag, MetricsOut* met,
-                                double* p_out, double* hist, int hist_col, cudaStream_t st, bool xhat_ready = false) {
+                                double* p_out, double* hist, int hist_col, cudaStream_t st, bool xhat_ready = false,
+                                const double* snrl_in = nullptr) {
   const sqngd_config& c = ctx->cfg;
   sqngd_status rc;
   if (!xhat_ready && (rc = run_xhat(ctx, s, st, w))) return rc;
   KP kp = make_kp(ctx, c.loss_mode != 0);
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
-                 ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col};
+                 ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col, snrl_in};
   MetricsArgs none = ma;
   none.out = nullptr; none.p_out = nullptr; none.loss_hist = nullptr;
   if (ctx->lr) {
@@ -1210,20 +1213,20 @@ struct StepATail {
 static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* w, int wrt, MetricsOut* met,
                                   float2* grad_w, float2* grad_s, const float* dq, float* grad_z, double* hist,
                                   int hist_col, cudaStream_t st, bool xhat_ready = false,
-                                  const StepATail* tail = nullptr) {
+                                  const StepATail* tail = nullptr, const double* snrl_in = nullptr) {
   const sqngd_config& c = ctx->cfg;
   sqngd_status rc;
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
   if (!xhat_ready && (rc = run_xhat(ctx, s, st, w, wrt == SQNGD_WRT_FILTERS))) return rc;
   FinArgs fa{c.R, c.M, c.N, wrt, c.eps_w, ptar, ctx->cm, s, w, dq, grad_w, grad_s, ctx->dy, grad_z};
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
-                 ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col};
+                 ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col, snrl_in};
   MetricsArgs none = ma;
   none.out = nullptr; none.loss_hist = nullptr;
   const size_t n = (size_t)c.R * c.M * c.N;
   const bool multi = ctx->world > 1;
   if (c.loss_mode == SQNGD_LOSS_MAX) {  // Eq. 37: the exact maximum, its O(N) subgradient on every rank
-    if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st, true))) return rc;
+    if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st, true, snrl_in))) return rc;
     k_sparse_adj<<<c.R, 256, 0, st>>>(c.M, c.N, c.K, ctx->L, wrt, c.eps_w, c.weights, s, w, ctx->tw, ctx->red,
                                       ctx->red_grad);
     k_finalize_grad<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fa, ctx->red_grad, ctx->status, none);
@@ -1333,9 +1336,9 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
 
 // a6 reporting (Eq. 10): SNRL_m and the restart's worst SNRL into the metrics, after the forward.
 static sqngd_status run_snrl(sqngd_ctx ctx, const float2* s, const float2* w, double* out, MetricsOut* met,
-                             cudaStream_t st) {
+                             cudaStream_t st, double* worst_out = nullptr) {
   const sqngd_config& c = ctx->cfg;
-  k_snrl<<<c.R, 256, 0, st>>>(c.M, c.N, s, w, out, met, ctx->status);
+  k_snrl<<<c.R, 256, 0, st>>>(c.M, c.N, s, w, out, met, ctx->status, worst_out);
   ctx->launches += 1;
   return launch_check(ctx, "snrl");
 }
@@ -1450,20 +1453,37 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
   if (ctx->net) {  // waveform generation z = f_theta(y0) (Alg. 1)
     CK(net_forward(ctx->nd, ctx->nws, stt->theta, stt->y0, stt->z, true, st, &ctx->launches));
   }
+  // hard_out: the metrics of the hard-quantized iterate the step starts from.  With Step A they come from
+  // its first evaluation, which evaluates exactly that pair (X_hard, H) -- no extra AF pass; SNRL (Eq. 10)
+  // from k_snrl on the same pair.  Without Step A: an explicit forward first.
+  bool h_ready = false;  // H = FFT(w)/P of the current w is in ctx->H
+  if (hard_out && !(block & SQNGD_BLOCK_A)) {
+    if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
+    if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+    if ((rc = run_forward(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), nullptr, nullptr, 0,
+                          st)))
+      return rc;
+    if ((rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), st))) return rc;
+    h_ready = true;
+  }
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
     if ((rc = run_xhat(ctx, ctx->s_hard, st, nullptr, true))) return rc;  // X_hard fixed for the block
+    if (hard_out && (rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, nullptr, st, ctx->snrl_w))) return rc;
     const bool fused = ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
+    h_ready = fused && c.n_h > 0;  // the fused row kernel leaves H = FFT(w)/P of the updated w
     for (int i = 0; i < c.n_h; ++i) {
+      MetricsOut* met = (i == 0 && hard_out) ? reinterpret_cast<MetricsOut*>(hard_out) : ctx->met;
+      const double* snrl_in = (i == 0 && hard_out) ? ctx->snrl_w : nullptr;
       if ((!fused || i == 0) && (rc = run_filter_fft(ctx, w2, st, ctx->s_hard))) return rc;
       if (fused) {  // the row kernel also updates w and prepares H, c_m for the next inner step
         const StepATail tail{ap(c.lr_w, 0, i), w2, stt->m_w, stt->v_w};
-        if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, nullptr, nullptr, nullptr, nullptr,
-                                loss_hist, i, st, true, &tail)))
+        if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, met, nullptr, nullptr, nullptr, nullptr,
+                                loss_hist, i, st, true, &tail, snrl_in)))
           return rc;
       } else {
-        if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, ctx->met, ctx->gw, nullptr, nullptr,
-                                nullptr, loss_hist, i, st, true)))
+        if ((rc = run_loss_grad(ctx, ctx->s_hard, w2, SQNGD_WRT_FILTERS, met, ctx->gw, nullptr, nullptr,
+                                nullptr, loss_hist, i, st, true, nullptr, snrl_in)))
           return rc;
         k_adam_project_w<<<c.R * c.M, 1024, 0, st>>>(c.N, stt->w, stt->m_w, stt->v_w,
                                                      reinterpret_cast<const float*>(ctx->gw), ap(c.lr_w, 0, i),
@@ -1474,7 +1494,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
     }
   }
   if (block & SQNGD_BLOCK_B) {  // Step B: transmit parameters with H fixed
-    if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+    if (!h_ready && (rc = run_filter_fft(ctx, w2, st))) return rc;
     const int col0 = (block & SQNGD_BLOCK_A) ? c.n_h : 0;
     int n2 = 1;
     while (n2 < ctx->BR) n2 <<= 1;
@@ -1522,15 +1542,20 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
       if ((rc = launch_check(ctx, "step B update"))) return rc;
     }
   }
-  if (hard_out) {
-    if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
-    if ((rc = run_filter_fft(ctx, w2, st))) return rc;
-    if ((rc = run_forward(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), nullptr, nullptr, 0,
-                          st)))
-      return rc;
-    if ((rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, reinterpret_cast<MetricsOut*>(hard_out), st))) return rc;
-  }
   return SQNGD_OK;
+}
+
+// The hard-waveform metrics of a state (quantize, H, forward, SNRL): sqngd_run's last iterate.
+sqngd_status sq_ctx_hard_metrics(sqngd_ctx ctx, const sqngd_state* stt, sqngd_metrics* out, sqngd_stream stream) {
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = S(stream);
+  float2* w2 = reinterpret_cast<float2*>(stt->w);
+  MetricsOut* met = reinterpret_cast<MetricsOut*>(out);
+  sqngd_status rc;
+  if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
+  if ((rc = run_filter_fft(ctx, w2, st))) return rc;
+  if ((rc = run_forward(ctx, ctx->s_hard, w2, nullptr, met, nullptr, nullptr, 0, st))) return rc;
+  return run_snrl(ctx, ctx->s_hard, w2, nullptr, met, st);
 }
 
 extern "C" {

@@ -194,7 +194,7 @@ def test_engines_agree_and_ksplit():
 
 def test_transmit_chain_and_step():
     """The (z, rho) chain and one graph-replayed A+B block on the Chebyshev engine against the
-    oracle (teacher-forced gradients and the hard-waveform metrics after the block)."""
+    oracle (teacher-forced gradients and the hard-waveform metrics of the iterate the block starts from)."""
     c = Cfg("chain", M=2, N=48, B=4, K=31, f_lo=-0.5, f_hi=0.5, r_n=4, c=60.0, loss_mode=sqngd.LOSS_LSE,
             beta_or_p=60.0, doppler_engine=CHEB, n_h=2, n_x=2, lr_z=1e-3)
     z = inputs.phase_params(1, c.M, c.N, config_index=9)
@@ -218,10 +218,15 @@ def test_transmit_chain_and_step():
     ctx.sync()
     h = hist.cpu().numpy()[0]
     assert np.isfinite(h).all() and (h > 0).all()
+    # hard_out: the entry iterate (z, rho, w), scored by Step A's first evaluation; its loss is that
+    # evaluation's (loss history column 0), its SNRL from the literal norms (Eq. 10)
     hm = sqngd.metrics_from_bytes(hard.cpu().numpy())[0]
-    q2 = O.quantize(c, st["z"].cpu().numpy(), st["rho"].cpu().numpy())
-    om, _, _ = O.af(c, q2["s_hard"], st["w"].cpu().numpy())
+    q2 = O.quantize(c, z, rho)
+    om, _, _ = O.af(c, q2["s_hard"], w)
     assert abs(hm["wpsl"] - om[0]["wpsl"]) <= 1e-4 * om[0]["wpsl"]
+    assert abs(hm["loss"] - om[0]["loss"]) <= 1e-5 * abs(om[0]["loss"])
+    assert hm["loss"] == h[0]
+    assert abs(hm["snrl_db_max"] - max(O.snrl_db(q2["s_hard"][0, m], w[0, m]) for m in range(c.M))) <= 1e-6
 
 
 def test_engine_selection():

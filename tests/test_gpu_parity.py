@@ -210,6 +210,7 @@ def test_step_teacher_forced_and_invariants():
     _, gz, gr = ctx.af_loss_grad(st_a["z"], st_a["rho"], st_a["w"], sqngd.WRT_TRANSMIT)
     gz, gr = gz.cpu().numpy().astype(np.float64), gr.cpu().numpy().astype(np.float64)
     w_a = st_a["w"].clone()
+    z_a, rho_a = st_a["z"].cpu().numpy(), st_a["rho"].cpu().numpy()
     ctx.step(st_a, sqngd.BLOCK_B, hist=hist_b, hard_met=hard)
     ctx.sync()
     ost = O.new_state(st_a["z"].cpu().numpy() * 0 + z, rho, w_a.cpu().numpy())
@@ -219,10 +220,12 @@ def test_step_teacher_forced_and_invariants():
     assert torch.equal(st_a["w"], w_a)                                  # block isolation
     h = np.array([hist.cpu().numpy()[0, 0], hist_b.cpu().numpy()[0, 0]])
     assert np.isfinite(h).all() and (h > 0).all()
+    # hard_out: the metrics of the iterate the step started from (explicit forward: no Step A)
     hm = sqngd.metrics_from_bytes(hard.cpu().numpy())[0]
-    q2 = O.quantize(c, st_a["z"].cpu().numpy(), st_a["rho"].cpu().numpy())
-    om, _, _ = O.af(c, q2["s_hard"], st_a["w"].cpu().numpy())
+    q2 = O.quantize(c, z_a, rho_a)
+    om, _, _ = O.af(c, q2["s_hard"], w_a.cpu().numpy())
     assert abs(hm["wpsl"] - om[0]["wpsl"]) <= 1e-4 * om[0]["wpsl"]
+    assert np.isfinite(hm["snrl_db_max"])
 
 
 def test_determinism():
