@@ -966,41 +966,50 @@ __global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, con
 }
 
 // a6 reporting: SNRL_m = 10 log10(||s_m||^2 ||w_m||^2 / |s_m^H w_m|^2) (Eq. 10) from
-// the literal fp64 norms, one block per restart (fixed-order block sums); the restart's maximum goes
-// into metrics[r].snrl_db_max.  A zero s_m^H w_m gives +inf and latches ST_DEGENERATE.
-__global__ void __launch_bounds__(256) k_snrl(int M, int N, const float2* __restrict__ s, const float2* __restrict__ w,
-                                              double* snrl_out, MetricsOut* met, int* status,
-                                              double* worst_out = nullptr) {
+// the literal fp64 norms, one block per restart and one warp per channel (fixed-order lane sums, xor
+// shuffles); the restart's maximum goes into metrics[r].snrl_db_max and / or worst_out[r].  A zero
+// s_m^H w_m gives +inf and latches ST_DEGENERATE.  Launch with blockDim = 32 * min(M, 32).
+__global__ void __launch_bounds__(1024) k_snrl(int M, int N, const float2* __restrict__ s,
+                                               const float2* __restrict__ w, double* snrl_out, MetricsOut* met,
+                                               int* status, double* worst_out) {
   SQ_PDL_WAIT();
-  __shared__ double shd[32];
-  const int r = blockIdx.x;
-  auto dsum = [](double x, double y) { return x + y; };
+  __shared__ double wmax[32];
+  const int r = blockIdx.x, lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double worst = -INFINITY;
-  for (int m = 0; m < M; ++m) {
+  for (int m = wp; m < M; m += nw) {
     const float2* sr = s + ((size_t)r * M + m) * N;
     const float2* wr = w + ((size_t)r * M + m) * N;
     double ss = 0.0, ww = 0.0, cr = 0.0, ci = 0.0;
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-      const float2 a = sr[n], b = wr[n];
+#pragma unroll 8
+    for (int n = lane; n < N; n += 32) {  // (unrolled: 8 loads in flight per lane)
+      const float2 a = __ldg(sr + n), b = __ldg(wr + n);
       ss += (double)a.x * a.x + (double)a.y * a.y;
       ww += (double)b.x * b.x + (double)b.y * b.y;
       cr += (double)a.x * b.x + (double)a.y * b.y;  // s conj(w)
       ci += (double)a.y * b.x - (double)a.x * b.y;
     }
-    ss = block_reduce(ss, dsum, shd);
-    ww = block_reduce(ww, dsum, shd);
-    cr = block_reduce(cr, dsum, shd);
-    ci = block_reduce(ci, dsum, shd);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      ww += __shfl_xor_sync(0xffffffffu, ww, o);
+      cr += __shfl_xor_sync(0xffffffffu, cr, o);
+      ci += __shfl_xor_sync(0xffffffffu, ci, o);
+    }
     const double c2 = cr * cr + ci * ci;
     const double db = c2 > 0.0 ? 10.0 * log10(ss * ww / c2) : INFINITY;
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       if (snrl_out) snrl_out[(size_t)r * M + m] = db;
       if (!(c2 > 0.0)) atomicOr(status, ST_DEGENERATE);
     }
     worst = fmax(worst, db);
   }
-  if (threadIdx.x == 0 && met) met[r].snrl_db_max = worst;
-  if (threadIdx.x == 0 && worst_out) worst_out[r] = worst;
+  if (lane == 0) wmax[wp] = worst;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < nw; ++i) worst = fmax(worst, wmax[i]);
+    if (met) met[r].snrl_db_max = worst;
+    if (worst_out) worst_out[r] = worst;
+  }
 }
 
 // ------------------------------------------------------------------ a10 multi-GPU (comm.h)

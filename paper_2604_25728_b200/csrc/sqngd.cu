@@ -1338,7 +1338,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
 static sqngd_status run_snrl(sqngd_ctx ctx, const float2* s, const float2* w, double* out, MetricsOut* met,
                              cudaStream_t st, double* worst_out = nullptr) {
   const sqngd_config& c = ctx->cfg;
-  k_snrl<<<c.R, 256, 0, st>>>(c.M, c.N, s, w, out, met, ctx->status, worst_out);
+  k_snrl<<<c.R, 32 * std::min(c.M, 32), 0, st>>>(c.M, c.N, s, w, out, met, ctx->status, worst_out);
   ctx->launches += 1;
   return launch_check(ctx, "snrl");
 }
@@ -1469,7 +1469,17 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
   if (block & SQNGD_BLOCK_A) {  // Step A: filters with X_hard fixed
     if ((rc = run_quantize(ctx, stt->z, stt->rho, nullptr, ctx->s_hard, nullptr, nullptr, st))) return rc;
     if ((rc = run_xhat(ctx, ctx->s_hard, st, nullptr, true))) return rc;  // X_hard fixed for the block
-    if (hard_out && (rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, nullptr, st, ctx->snrl_w))) return rc;
+    if (hard_out) {  // SNRL of the entry pair; on the Chebyshev engine beside the first evaluation (its
+                     // k_lr_finish, which reads it, runs later on the same side stream and is joined)
+      const bool side = ctx->lr && ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
+      cudaStream_t ss = st;
+      if (side) {
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        ss = ctx->side;
+      }
+      if ((rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, nullptr, ss, ctx->snrl_w))) return rc;
+    }
     const bool fused = ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
     h_ready = fused && c.n_h > 0;  // the fused row kernel leaves H = FFT(w)/P of the updated w
     for (int i = 0; i < c.n_h; ++i) {

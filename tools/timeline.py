@@ -28,14 +28,16 @@ torch.cuda.set_stream(side)
 ctx = sqngd.Context(c)
 zt, rt = torch.as_tensor(z, device="cuda"), torch.as_tensor(rho, device="cuda")
 st = ctx.new_state(zt, rt, ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"])
+hist = torch.zeros((c.R, c.n_h + c.n_x), dtype=torch.float64, device="cuda")
+hard = torch.empty(c.R * sqngd.METRICS_BYTES, dtype=torch.uint8, device="cuda")
 for _ in range(3):
-    ctx.step(st, sqngd.BLOCK_AB)
+    ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     ev[0].record()
     for _ in range(steps):
-        ctx.step(st, sqngd.BLOCK_AB)
+        ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)  # as bench.py times it
     ev[1].record()
     torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / steps
