@@ -246,9 +246,12 @@ constexpr int kLrtUnroll = SQNGD_LRT_UNROLL;  // tile-loop unroll of k_lrt (tuni
 #define SQNGD_LRT_MAXT 32
 #define SQNGD_LRT_MINB 16
 #endif
-template <int Q, int LM, bool HW, bool GRAD>
+// KM: kernel mode -- 0 forward (sums, keys), 1 forward + adjoint (cotangents), 2 forward writing the
+// |A| map; the map stores are compiled only into mode 2.
+template <int Q, int LM, bool HW, int KM>
 __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const LrtArgs a) {
   SQ_PDL_WAIT();
+  constexpr bool GRAD = KM == 1, MAP = KM == 2;
   constexpr int QH = Q / 2;
   constexpr int NR = 6 + (GRAD ? 16 : 0);  // per-lane record: key(2), shift(2), S(2), GE/GO(16)
   extern __shared__ float4 lr_smem[];
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
   float* mrow[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
-    mrow[h] = (!GRAD && a.af_mag && inL[h]) ? a.af_mag + (size_t)pr * a.K * a.L + idx[h] : nullptr;
+    mrow[h] = (MAP && a.af_mag && inL[h]) ? a.af_mag + (size_t)pr * a.K * a.L + idx[h] : nullptr;
 
   float bl[2], bh[2], S[2];
   int kl[2], kh[2];

@@ -338,35 +338,43 @@ struct Launch {
 template <int Q>
 struct LrLaunch {
   // tensor-core variant
-  template <int LM, bool HW, bool GRAD>
+  template <int LM, bool HW, int KM>
   static void go_t(const LrtArgs& a, int rows, size_t smem, cudaStream_t st) {  // grid (chunk, l, row - row0)
-    if (rows > 0) k_lrt<Q, LM, HW, GRAD><<<dim3(a.nch, a.M, rows), 32 * a.kw, smem, st>>>(a);
+    if (rows > 0) k_lrt<Q, LM, HW, KM><<<dim3(a.nch, a.M, rows), 32 * a.kw, smem, st>>>(a);
   }
-  static void launch_t(int lm, bool hw, bool grad, const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
-    if (lm == 0) { hw ? go_t<0, true, false>(a, units, smem, st) : go_t<0, false, false>(a, units, smem, st); return; }
-    if (lm == 1) {
-      if (grad) hw ? go_t<1, true, true>(a, units, smem, st) : go_t<1, false, true>(a, units, smem, st);
-      else hw ? go_t<1, true, false>(a, units, smem, st) : go_t<1, false, false>(a, units, smem, st);
-      return;
-    }
-    if (grad) hw ? go_t<2, true, true>(a, units, smem, st) : go_t<2, false, true>(a, units, smem, st);
-    else hw ? go_t<2, true, false>(a, units, smem, st) : go_t<2, false, false>(a, units, smem, st);
+  template <int LM>
+  static void go_lm(bool hw, int km, const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
+    if (km == 0) hw ? go_t<LM, true, 0>(a, units, smem, st) : go_t<LM, false, 0>(a, units, smem, st);
+    else if (km == 2) hw ? go_t<LM, true, 2>(a, units, smem, st) : go_t<LM, false, 2>(a, units, smem, st);
+    else if constexpr (LM != 0) hw ? go_t<LM, true, 1>(a, units, smem, st) : go_t<LM, false, 1>(a, units, smem, st);
   }
-  template <int LM, bool HW, bool GRAD>
+  // km: 0 forward, 1 forward + adjoint (LSE / p-norm only), 2 forward writing the |A| map
+  static void launch_t(int lm, bool hw, int km, const LrtArgs& a, int units, size_t smem, cudaStream_t st) {
+    if (lm == 0) go_lm<0>(hw, km, a, units, smem, st);
+    else if (lm == 1) go_lm<1>(hw, km, a, units, smem, st);
+    else go_lm<2>(hw, km, a, units, smem, st);
+  }
+  template <int LM, bool HW, int KM>
   static cudaError_t attr_t(size_t smem) {
-    return cudaFuncSetAttribute(k_lrt<Q, LM, HW, GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_lrt<Q, LM, HW, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  template <int LM>
+  static cudaError_t attr_lm(size_t smem) {
+    cudaError_t e;
+    if ((e = attr_t<LM, false, 0>(smem)) || (e = attr_t<LM, true, 0>(smem)) || (e = attr_t<LM, false, 2>(smem)) ||
+        (e = attr_t<LM, true, 2>(smem)))
+      return e;
+    if constexpr (LM != 0)
+      if ((e = attr_t<LM, false, 1>(smem)) || (e = attr_t<LM, true, 1>(smem))) return e;
+    return cudaSuccess;
   }
   static cudaError_t prepare_t(size_t smem) {
     cudaError_t e;
-    if ((e = attr_t<0, false, false>(smem)) || (e = attr_t<0, true, false>(smem)) || (e = attr_t<1, false, false>(smem)) ||
-        (e = attr_t<1, true, false>(smem)) || (e = attr_t<1, false, true>(smem)) || (e = attr_t<1, true, true>(smem)) ||
-        (e = attr_t<2, false, false>(smem)) || (e = attr_t<2, true, false>(smem)) || (e = attr_t<2, false, true>(smem)) ||
-        (e = attr_t<2, true, true>(smem)))
-      return e;
+    if ((e = attr_lm<0>(smem)) || (e = attr_lm<1>(smem)) || (e = attr_lm<2>(smem))) return e;
     return cudaSuccess;
   }
   static cudaError_t occupancy_t(int* bps, int threads, size_t smem) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lrt<Q, 1, false, true>, threads, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lrt<Q, 1, false, 1>, threads, smem);
   }
 };
 
@@ -1142,7 +1150,7 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
   {
     ProfScope ps(ctx, cls, st);
     with_Q(ctx->Q, [&](auto Qc) {
-      decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad, t, rows, ctx->lr_smem, st);
+      decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad ? 1 : (af_mag ? 2 : 0), t, rows, ctx->lr_smem, st);
     });
   }
   const int GPR = (int)(ctx->units_lr / c.R);
