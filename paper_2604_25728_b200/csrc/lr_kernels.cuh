@@ -98,7 +98,8 @@ struct LrArgs {
 // LM: 0 MAX (keys only), 1 LSE, 2 PNORM.  Returns G~ (unnormalised: gphi w At / |At|).
 template <int LM, bool HW, bool GRAD, bool GE_RULE, bool GF_ONLY = false>
 __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int idx, bool valid, float lbN, float nlbs,
-                                          float qN, float& best, int& bk, float& S, float* mrow, float msc = 1.f) {
+                                          float qN, float& best, int& bk, float& S, float* mcell, bool mst,
+                                          float msc = 1.f) {
   // |A|^2 + 1e-30: the floor keeps rsqrt finite at A = 0 and is far below one ulp of any
   // non-negligible cell, so the key and the magnitude are unchanged
   const float a2 = fmaf(A.x, A.x, fmaf(A.y, A.y, 1e-30f));
@@ -111,12 +112,12 @@ __device__ __forceinline__ float2 lr_cell(float2 A, int k, const LrArgs& a, int 
   best = upd ? kv : best;
   bk = upd ? k : bk;
   if (LM == 0) {
-    if (mrow) mrow[(size_t)k * a.L] = sqrtf(a2) * msc;
+    if (mst) *mcell = sqrtf(a2) * msc;  // (mcell: this cell's |A| map address)
     return make_float2(0.f, 0.f);
   }
   const float rsq = rsqa(a2);
   const float mag = a2 * rsq;
-  if (mrow) mrow[(size_t)k * a.L] = mag * msc;
+  if (mst) *mcell = mag * msc;
   float phi, gphi;
   if (LM == 1) {
     phi = ex2a(fmaf(lbN, HW ? wt * mag : mag, nlbs));
@@ -377,6 +378,17 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
 #pragma unroll
   for (int h = 0; h < 2; ++h)
     mrow[h] = (MAP && a.af_mag && inL[h]) ? a.af_mag + (size_t)pr * a.K * a.L + idx[h] : nullptr;
+  // MAP: per-lag bases of the two bin streams of this lane (bins 2c and K-1-2c), advanced per tile
+  bool mok[2];
+  float* mb0[2];
+  float* mb1[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    mok[h] = mrow[h] != nullptr;
+    if (!mok[h]) mrow[h] = a.af_mag;  // (a valid base; nothing is stored through it)
+    mb0[h] = mrow[h] + (ptrdiff_t)(2 * cq) * a.L;
+    mb1[h] = mrow[h] + (ptrdiff_t)(a.K - 1 - 2 * cq) * a.L;
+  }
 
   float bl[2], bh[2], S[2];
   int kl[2], kh[2];
@@ -439,22 +451,26 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         const int p = 8 * t + 2 * cq + (e & 1);
         const float2 A0 = make_float2(Per[e] + Por[e], Pei[e] + Poi[e]);
         const float2 A1 = make_float2(Per[e] - Por[e], Pei[e] - Poi[e]);
+        // map addresses (MAP only): bin p = 8t + 2c + (e & 1) and bin K-1-p of this lag row
+        const ptrdiff_t mo = (ptrdiff_t)8 * t * a.L + ((e & 1) ? a.L : 0);
+        float* mc0 = mb0[h] + mo;
+        float* mc1 = mb1[h] - mo;
         float gf0, gf1;  // cotangent factors: G = gf A
         if (!MASKED) {
           gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, p, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h], bl[h], kl[h],
-                                                   S[h], mrow[h], isc[h]).x;
+                                                   S[h], mc0, MAP && mok[h], isc[h]).x;
           gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, a.K - 1 - p, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h],
-                                                  bh[h], kh[h], S[h], mrow[h], isc[h]).x;
+                                                  bh[h], kh[h], S[h], mc1, MAP && mok[h], isc[h]).x;
         } else {
           const bool pv = p < Kp;
           const bool v0 = valid[h] && pv;
           float b0 = bl[h], b1 = bh[h];
           int k0 = kl[h], k1 = kh[h];
           gf0 = lr_cell<LM, HW, GRAD, false, true>(A0, pv ? p : 0, la, idx[h], v0, lbN[h], v0 ? nlbs[h] : -INFINITY,
-                                                   v0 ? qN[h] : 0.f, b0, k0, S[h], pv ? mrow[h] : nullptr, isc[h]).x;
+                                                   v0 ? qN[h] : 0.f, b0, k0, S[h], mc0, MAP && mok[h] && pv, isc[h]).x;
           gf1 = lr_cell<LM, HW, GRAD, true, true>(A1, pv ? a.K - 1 - p : 0, la, idx[h], v0, lbN[h],
                                                   v0 ? nlbs[h] : -INFINITY, v0 ? qN[h] : 0.f, b1, k1, S[h],
-                                                  pv ? mrow[h] : nullptr, isc[h]).x;
+                                                  mc1, MAP && mok[h] && pv, isc[h]).x;
           if (pv) { bl[h] = b0; kl[h] = k0; bh[h] = b1; kh[h] = k1; }
           if (!v0) gf0 = gf1 = 0.f;
         }
@@ -531,7 +547,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         float Sm = 0.f, bm = bl[h];
         int km = kl[h];
         const float2 Gm = lr_cell<LM, HW, GRAD, false>(Am[h], Kp, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h], bm, km, Sm,
-                                                       cq == 0 ? mrow[h] : nullptr, isc[h]);
+                                                       mrow[h] + (ptrdiff_t)Kp * a.L, MAP && mok[h] && cq == 0, isc[h]);
         if (cq == 0) { S[h] += Sm; bl[h] = bm; kl[h] = km; }
         if (GRAD) {
 #pragma unroll
@@ -561,7 +577,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
       shift[h] = fmaxf(shift[h], __shfl_xor_sync(0xffffffffu, shift[h], 1));
       shift[h] = fmaxf(shift[h], __shfl_xor_sync(0xffffffffu, shift[h], 2));
     }
-    mrow[0] = mrow[1] = nullptr;
+    mok[0] = mok[1] = false;  // (the map holds the first pass)
   }
 
   // ---- lane record: key over both rows, per-row shift / sum, cotangent fragments
