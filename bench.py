@@ -526,11 +526,16 @@ def main():
                 "CUDA events per call, L2 flushed between calls"}
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the timing.
-    # The optimizer state lives in ONE flat allocation (the sqngd_state pointers are views into it)
-    # and the step's outputs (loss history, hard metrics) in another, so each direction is one copy.
+    # The optimizer state and the step's outputs (loss history, hard metrics) live in ONE device
+    # allocation (the sqngd_state pointers are views into it): the state goes up in one H2D copy and
+    # state + outputs come back in one D2H copy.
     keys = ["z", "rho", "w", "m_z", "v_z", "m_rho", "v_rho", "m_w", "v_w"]
     sizes = {k: st[k].numel() * (2 if st[k].is_complex() else 1) for k in keys}
-    flat = torch.empty(sum(sizes.values()), dtype=torch.float32, device=dev)
+    nst = sum(sizes.values())
+    hist_b = hist.numel() * 8
+    sb = (4 * nst + 7) // 8 * 8
+    buf = torch.empty(sb + hist_b + hard.numel(), dtype=torch.uint8, device=dev)
+    flat = buf[:4 * nst].view(torch.float32)
     est, o = {"t_a": st["t_a"], "t_b": st["t_b"]}, 0
     for k in keys:
         v = flat[o:o + sizes[k]]
@@ -538,23 +543,22 @@ def main():
         est[k] = v.view(st[k].shape)
         est[k].copy_(st[k])
         o += sizes[k]
-    hist_b = hist.numel() * 8
-    outb = torch.empty(hist_b + hard.numel(), dtype=torch.uint8, device=dev)
+    outb = buf[sb:]
     ehist = outb[:hist_b].view(torch.float64).view(hist.shape)
     ehard = outb[hist_b:]
-    host_state = flat.cpu().pin_memory()
-    host_out = torch.empty_like(outb, device="cpu").pin_memory()
-    h2d = flat.numel() * 4
-    d2h = h2d + outb.numel()
+    host_buf = buf.cpu().pin_memory()
+    host_state = host_buf[:4 * nst]
+    host_out = host_buf[sb:]
+    h2d = 4 * nst
+    d2h = buf.numel()
     e2e_ev = []
     for i in range(args.warmup + args.steps):
         flush.fill_(float(i))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        flat.copy_(host_state, non_blocking=True)
+        buf[:4 * nst].copy_(host_state, non_blocking=True)
         ctx.step(est, sqngd.BLOCK_AB, hist=ehist, hard_met=ehard)
-        host_state.copy_(flat, non_blocking=True)
-        host_out.copy_(outb, non_blocking=True)
+        host_buf.copy_(buf, non_blocking=True)
         b.record(stream)
         if i >= args.warmup:
             e2e_ev.append((a, b))

@@ -20,6 +20,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 eng = {"fft": 1, "cheb": 2}.get(sys.argv[3] if len(sys.argv) > 3 else "auto", 0)
 out = sys.argv[4] if len(sys.argv) > 4 else None
+e2e = len(sys.argv) > 5 and sys.argv[5] == "e2e"  # bench.py's e2e loop: state up, step, state + outputs down
 c = CF.CONFIGS[name].with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=eng)
 z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, r), c.M * c.N).reshape(c.M, c.N) for r in range(c.R)])
 rho = inputs.init_thresholds(c.R, c.B, c.r_n)
@@ -30,14 +31,41 @@ zt, rt = torch.as_tensor(z, device="cuda"), torch.as_tensor(rho, device="cuda")
 st = ctx.new_state(zt, rt, ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"])
 hist = torch.zeros((c.R, c.n_h + c.n_x), dtype=torch.float64, device="cuda")
 hard = torch.empty(c.R * sqngd.METRICS_BYTES, dtype=torch.uint8, device="cuda")
-for _ in range(3):
+if e2e:
+    keys = ["z", "rho", "w", "m_z", "v_z", "m_rho", "v_rho", "m_w", "v_w"]
+    sizes = {k: st[k].numel() * (2 if st[k].is_complex() else 1) for k in keys}
+    nst = sum(sizes.values())
+    buf = torch.empty(4 * nst + hist.numel() * 8 + hard.numel(), dtype=torch.uint8, device="cuda")
+    flat = buf[:4 * nst].view(torch.float32)
+    est, o = {"t_a": st["t_a"], "t_b": st["t_b"]}, 0
+    for k in keys:
+        v = flat[o:o + sizes[k]]
+        v = v.view(torch.complex64) if st[k].is_complex() else v
+        est[k] = v.view(st[k].shape)
+        est[k].copy_(st[k])
+        o += sizes[k]
+    hist = buf[4 * nst:4 * nst + hist.numel() * 8].view(torch.float64).view(hist.shape)
+    hard = buf[4 * nst + hist.numel() * 8:]
+    st = est
+    host_buf = buf.cpu().pin_memory()
+
+
+def one_step():
+    if e2e:
+        buf[:4 * nst].copy_(host_buf[:4 * nst], non_blocking=True)
     ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)
+    if e2e:
+        host_buf.copy_(buf, non_blocking=True)
+
+
+for _ in range(3):
+    one_step()
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     ev[0].record()
     for _ in range(steps):
-        ctx.step(st, sqngd.BLOCK_AB, hist=hist, hard_met=hard)  # as bench.py times it
+        one_step()  # as bench.py times it
     ev[1].record()
     torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / steps
@@ -46,7 +74,7 @@ for e in prof.events():
     if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0:
         nm = e.name
         if "memcpy" in nm.lower() or "memset" in nm.lower():
-            print(f"non-kernel device activity: {nm} {e.time_range.elapsed_us():.2f} us")
+            print(f"non-kernel device activity: {nm} {e.time_range.elapsed_us():.2f} us at {e.time_range.start}")
             continue
         ks.append((e.time_range.start, e.time_range.end, nm.split("(")[0].replace("void ", "")[:48]))
 ks.sort()
