@@ -80,12 +80,20 @@ def test_run_rule_and_snapshot(patience, check_every, need_dec):
     assert np.isfinite(h[: res["iterations"]]).all() and (h[: res["iterations"]] > 0).all()
     # replay: the snapshot of restart r is the state after bi[r] outer iterations (the same launch
     # sequence as the driver's: every step also evaluates the hard metrics)
+    # and every reported history entry is the hard metrics of that iterate: an independent forward
+    # (sqngd_af_forward on the iterate's hard waveform) and the next step's hard_out (entry iterate)
     hard = torch.empty(c.R * sqngd.METRICS_BYTES, dtype=torch.uint8, device=DEV)
+    n_it = res["iterations"]
     with torch.cuda.stream(side):
         st2 = ctx.new_state(z, rho, w)
-        snaps = {}
-        for t in range(1, int(bi_ref.max()) + 1):
+        snaps, fwd, entry = {}, [], []
+        for t in range(1, max(int(bi_ref.max()), n_it) + 1):
             ctx.step(st2, sqngd.BLOCK_AB, hard_met=hard)
+            if t >= 2:
+                entry.append([m["wpsl"] for m in sqngd.metrics_from_bytes(hard.cpu().numpy())])
+            s_h = ctx.quantize(st2["z"], st2["rho"], soft=False, want_b=False, want_dq=False)["s_hard"]
+            met, _, _ = ctx.af_forward(s_h, st2["w"])
+            fwd.append([m["wpsl"] for m in ctx.metrics(met)])
             for r in range(c.R):
                 if bi_ref[r] == t:
                     snaps[r] = {k: st2[k][r].clone() for k in ("z", "rho", "w")}
@@ -93,6 +101,10 @@ def test_run_rule_and_snapshot(patience, check_every, need_dec):
     for r in range(c.R):
         for k in ("z", "rho", "w"):
             assert torch.equal(best[k][r], snaps[r][k]), (r, k)
+    fwd = np.array(fwd)[:n_it]
+    np.testing.assert_allclose(h[:n_it], fwd, rtol=1e-6)
+    if len(entry):
+        np.testing.assert_allclose(np.array(entry)[: n_it - 1], fwd[: len(entry)][: n_it - 1], rtol=1e-6)
 
 
 def test_run_generator_mode_snapshot_has_theta():
