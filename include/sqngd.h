@@ -241,11 +241,13 @@ sqngd_status sqngd_net_backward(sqngd_ctx ctx, const float* theta, const float* 
    decreasing over the window).  patience <= 0: run all T.
    best_wpsl [R] doubles, best_iter [R] int32 (1-based outer iteration of the snapshot), wpsl_hist and
    loss_hist (NULL or [T][R] doubles: hard WPSL / hard loss per iteration until the stop) are DEVICE
-   pointers.  The bookkeeping runs on the device (its buffers are kept in the context); the host polls
-   the stop flag every opts->check_every iterations, so the live `state` may run up to check_every - 1
-   iterations past the stop (the snapshot, best_* and result->iterations follow the rule exactly;
-   check_every = 1 is exact).  Returns after synchronizing `stream` (the latched device status, as
-   sqngd_sync). */
+   pointers.  Iterate t is scored by the hard_out of step t + 1 (its first Step-A evaluation, from a
+   copy of the state taken before that step) and the last iterate by one forward after the loop
+   (DESIGN.md §3 "Hard metrics of an outer iteration").  The bookkeeping runs on the device (its
+   buffers are kept in the context); the host polls the stop flag every opts->check_every steps, so
+   the live `state` may run up to check_every steps past the stopping iterate (the snapshot, best_*
+   and result->iterations follow the rule exactly).  Returns after synchronizing `stream` (the latched
+   device status, as sqngd_sync). */
 typedef struct {
   int32_t T;           /* maximum outer iterations (the paper's T = 2000)          */
   int32_t patience;    /* outer iterations without hard-WPSL improvement before stopping   */
@@ -255,7 +257,8 @@ typedef struct {
 } sqngd_run_opts;
 typedef struct {
   int64_t iterations;  /* outer iterations until the rule stopped training (T if it did not) */
-  int64_t steps_run;   /* sqngd_step calls made (>= iterations, <= iterations + check_every - 1) */
+  int64_t steps_run;   /* sqngd_step calls made (iterations < steps_run <= iterations + check_every
+                          when stopped; T otherwise)                                          */
   int32_t stopped;     /* 1: stopped by the rule, 0: T reached                             */
   int32_t reserved;
 } sqngd_run_result;
