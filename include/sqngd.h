@@ -257,7 +257,7 @@ typedef struct {
 } sqngd_run_opts;
 typedef struct {
   int64_t iterations;  /* outer iterations until the rule stopped training (T if it did not) */
-  int64_t steps_run;   /* sqngd_step calls made (iterations < steps_run <= iterations + check_every
+  int64_t steps_run;   /* sqngd_step calls made (iterations <= steps_run <= iterations + check_every
                           when stopped; T otherwise)                                          */
   int32_t stopped;     /* 1: stopped by the rule, 0: T reached                             */
   int32_t reserved;

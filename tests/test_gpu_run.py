@@ -71,7 +71,7 @@ def test_run_rule_and_snapshot(patience, check_every, need_dec):
     if patience > 0 and stop is not None:
         assert res["stopped"] and res["iterations"] == stop
         # iterate t is scored by step t + 1 (hard_out = the entry iterate), so the rule is seen one step later
-        assert res["iterations"] < res["steps_run"] <= res["iterations"] + check_every
+        assert res["iterations"] <= res["steps_run"] <= res["iterations"] + check_every
         assert np.isnan(h[res["iterations"]:]).all()  # no history past the stop
     else:
         assert not res["stopped"] and res["iterations"] == T
