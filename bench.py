@@ -482,8 +482,8 @@ def main():
 
     # ---- forward only (sqngd_af_forward, a2-a6): delay-Doppler cells/s = M^2 (2N-1) K R / t_fwd (SURVEY
     # §8(d)), without and with the |A| map written to HBM; the map-writing launch against HBM bandwidth.
-    def forward_rate(cx, s, w, want_map, reps=10):
-        amap = (torch.empty((c.R, c.M, c.M, c.K, 2 * c.N - 1), dtype=torch.float32, device=dev) if want_map
+    def forward_rate(cx, s, w, want_map, reps=10, ld=None):
+        amap = (torch.empty((c.R, c.M, c.M, c.K, ld or (2 * c.N - 1)), dtype=torch.float32, device=dev) if want_map
                 else None)
         for _ in range(3):
             cx.af_forward(s, w, map_out=amap, want_p=False)
@@ -508,9 +508,15 @@ def main():
     s_h = ctx.quantize(st["z"], st["rho"], soft=False, want_b=False, want_dq=False)["s_hard"]
     t_f, tk_f = forward_rate(ctx, s_h, st["w"], False)
     t_m, tk_m = forward_rate(ctx, s_h, st["w"], True)
+    # the same map with rows on 128-byte boundaries (cfg.map_ld: pitch 2N-1 rounded up to 32 floats)
+    ld = (2 * c.N - 1 + 31) // 32 * 32
+    ctxp = sqngd.Context(c.with_(map_ld=ld), device=local)
+    t_p, tk_p = forward_rate(ctxp, s_h, st["w"], True, ld=ld)
+    ctxp.close()
     cells_job = c.cells * c.R * world
     map_bytes = c.cells * c.R * 4
     hbm_peak = peaks()[1]
+    kname = ("k_lrt<FWD>" if main_run["engine"]["engine"] == "chebyshev" else "k_af<FWD>") + " (writing the map)"
     forward = {
         "cells_per_s": cells_job / t_f, "ms_per_forward": t_f * 1e3,
         "with_map": {"cells_per_s": cells_job / t_m, "ms_per_forward": t_m * 1e3, "map_bytes": map_bytes,
@@ -521,6 +527,12 @@ def main():
                                   "traffic": None,
                                   "what": "|A| map bytes (M^2 (2N-1) K x 4 B, fp32) / duration of the fused launch "
                                           "that writes it"}},
+        "with_map_pitched": {"map_ld": ld, "cells_per_s": cells_job / t_p, "ms_per_forward": t_p * 1e3,
+                             "roofline": {"bound": "hbm", "kernel": kname + f", rows pitched to {ld} floats",
+                                          "achieved": map_bytes / tk_p / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                          "frac": map_bytes / tk_p / 1e9 / hbm_peak, "avg_launch_ms": tk_p * 1e3,
+                                          "traffic": None,
+                                          "what": "the same |A| bytes (the pad is not written) / launch duration"}},
         "fused_launch_ms_no_map": tk_f * 1e3,
         "what": "sqngd_af_forward (filter FFT, node/bin transforms, fused contraction + ROI reduction, metrics), "
                 "CUDA events per call, L2 flushed between calls"}

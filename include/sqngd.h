@@ -11,7 +11,7 @@
  *   - Complex arrays are interleaved fp32 pairs (re, im): "float*" of 2x length.
  *   - Layouts are row-major: s, w, z = [R][M][N] (the paper's X[:, m] = s[m][:],
  *     P:L91-94; vec() column stacking = this flattening);
- *     rho = [R][B*r_n]; the optional AF magnitude map = [R][M][M][K][2N-1] with
+ *     rho = [R][B*r_n]; the optional AF magnitude map = [R][M][M][K][ld] (ld = map_ld, or 2N-1) with
  *     lag tau stored at index tau + N - 1 (Eq. 6 labels, Q1).
  *   - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default
  *     stream).  The return status reports launch-time errors; device-side
@@ -85,6 +85,10 @@ typedef struct {
   int32_t net_width;               /* generator hidden width W (paper: 128); 0 = no generator,
                                       z is the direct parameter (Q13); else W % 8 == 0, <= 128 */
   double lr_theta;                 /* Adam rate of theta (eta_x = 1e-5)             */
+  int32_t map_ld;                  /* row pitch (floats) of the optional |A| map of
+                                      sqngd_af_forward: 0 => 2N-1 (dense); else >= 2N-1, e.g.
+                                      2N rounded up to 32 so every bin row starts on a 128-byte
+                                      boundary (whole-sector stores; the pad is not written)   */
 } sqngd_config;
 
 /* Doppler engine (sqngd_config.doppler_engine).
@@ -173,7 +177,8 @@ sqngd_status sqngd_quantize(sqngd_ctx ctx, const float* z, const float* rho, flo
 
 /* a2-a6: all M^2 AF/CAF maps over (2N-1) lags x K Doppler bins by Doppler-modulated,
    zero-padded FFT correlation (Eqs. 33-36), fused with the ROI reduction (Eqs. 7-9,
-   37-42).  s, w: complex [R][M][N].  af_mag: NULL or [R][M][M][K][2N-1] |A| (fp32).
+   37-42).  s, w: complex [R][M][N].  af_mag: NULL or [R][M][M][K][ld] |A| (fp32), ld = cfg.map_ld
+   or 2N-1 (lag tau at column tau + N - 1; columns >= 2N-1 of a pitched row are not written).
    metrics: [R] sqngd_metrics.  p_out: NULL or [R][M] doubles p_m (Eq. 38).
    snrl_db_out: NULL or [R][M] doubles SNRL_m = 10 log10(||s_m||^2 ||w_m||^2 / |s_m^H w_m|^2)
    (Eq. 10; +inf when s_m^H w_m = 0, which also latches SQNGD_E_DEGENERATE). */

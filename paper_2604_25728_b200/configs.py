@@ -46,6 +46,7 @@ class Cfg:
     net_depth: int = 0              # generator residual blocks (paper: 5); 0 with net_width 0
     net_width: int = 0              # generator hidden width (paper: 128); 0 = z is the direct parameter
     lr_theta: float = 1e-5          # Adam rate of the generator parameters (eta_x)
+    map_ld: int = 0                 # |A| map row pitch (0 = dense 2N-1; include/sqngd.h)
     iterations: int = 1
     index: int = 0                  # config number used for input seeds
 

@@ -51,6 +51,7 @@ struct KP {
   int u_lo, u_hi;        // units evaluated by this rank (multi-GPU slice of R*M*K)
   int want_S;            // forward: accumulate surrogate sums
   int* counter;          // dynamic unit counter (zeroed before the launch)
+  int mld;               // |A| map row pitch (floats)
 };
 
 
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
         sc.k = k;
         if constexpr (MODE == MODE_FWD) {
           if (af_mag) {
-            float* mrow = af_mag + ((((size_t)r * M + m) * M + l) * K + k) * (size_t)kp.L + N - 1;
+            float* mrow = af_mag + ((((size_t)r * M + m) * M + l) * K + k) * (size_t)kp.mld + N - 1;
 #pragma unroll
             for (int i = 0; i < E; ++i) {
               const int j = t + i * T;

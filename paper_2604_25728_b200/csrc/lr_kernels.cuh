@@ -175,6 +175,7 @@ struct LrtArgs {
   const float2* Rn;      // [R M M][Q][LS]
   float2* Gn;            // [R M M][Q][LS]
   float* af_mag;         // forward only
+  int mld;               // |A| map row pitch (floats)
   Part part;             // unit slots, u = pair nch + chunk
   LrRed* lred;
 };
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
   float* mrow[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
-    mrow[h] = (MAP && a.af_mag && inL[h]) ? a.af_mag + (size_t)pr * a.K * a.L + idx[h] : nullptr;
+    mrow[h] = (MAP && a.af_mag && inL[h]) ? a.af_mag + (size_t)pr * a.K * a.mld + idx[h] : nullptr;
   // MAP: per-lag bases of the two bin streams of this lane (bins 2c and K-1-2c), advanced per tile
   bool mok[2];
   float* mb0[2];
@@ -386,8 +387,8 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
   for (int h = 0; h < 2; ++h) {
     mok[h] = mrow[h] != nullptr;
     if (!mok[h]) mrow[h] = a.af_mag;  // (a valid base; nothing is stored through it)
-    mb0[h] = mrow[h] + (ptrdiff_t)(2 * cq) * a.L;
-    mb1[h] = mrow[h] + (ptrdiff_t)(a.K - 1 - 2 * cq) * a.L;
+    mb0[h] = mrow[h] + (ptrdiff_t)(2 * cq) * a.mld;
+    mb1[h] = mrow[h] + (ptrdiff_t)(a.K - 1 - 2 * cq) * a.mld;
   }
 
   float bl[2], bh[2], S[2];
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         const float2 A0 = make_float2(Per[e] + Por[e], Pei[e] + Poi[e]);
         const float2 A1 = make_float2(Per[e] - Por[e], Pei[e] - Poi[e]);
         // map addresses (MAP only): bin p = 8t + 2c + (e & 1) and bin K-1-p of this lag row
-        const ptrdiff_t mo = (ptrdiff_t)8 * t * a.L + ((e & 1) ? a.L : 0);
+        const ptrdiff_t mo = (ptrdiff_t)8 * t * a.mld + ((e & 1) ? a.mld : 0);
         float* mc0 = mb0[h] + mo;
         float* mc1 = mb1[h] - mo;
         float gf0, gf1;  // cotangent factors: G = gf A
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         float Sm = 0.f, bm = bl[h];
         int km = kl[h];
         const float2 Gm = lr_cell<LM, HW, GRAD, false>(Am[h], Kp, la, idx[h], valid[h], lbN[h], nlbs[h], qN[h], bm, km, Sm,
-                                                       mrow[h] + (ptrdiff_t)Kp * a.L, MAP && mok[h] && cq == 0, isc[h]);
+                                                       mrow[h] + (ptrdiff_t)Kp * a.mld, MAP && mok[h] && cq == 0, isc[h]);
         if (cq == 0) { S[h] += Sm; bl[h] = bm; kl[h] = km; }
         if (GRAD) {
 #pragma unroll

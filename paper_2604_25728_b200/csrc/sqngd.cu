@@ -423,6 +423,7 @@ static KP make_kp(const sqngd_ctx_s* c, int want_S) {
   kp.u_lo = (int)lo; kp.u_hi = (int)hi;
   kp.want_S = want_S;
   kp.counter = c->counter;
+  kp.mld = g.map_ld > 0 ? g.map_ld : c->L;
   return kp;
 }
 
@@ -552,6 +553,8 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   if (cfg.loss_mode != 0 && !(cfg.beta_or_p > 0))
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: beta_or_p must be > 0 for LSE / PNORM");
   if (cfg.B * cfg.r_n > 8192) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: B*r_n > 8192");
+  if (cfg.map_ld != 0 && cfg.map_ld < 2 * cfg.N - 1)
+    return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: map_ld must be 0 or >= 2N-1");
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: rank/world");
   if (cfg.doppler_engine < 0 || cfg.doppler_engine > 2)
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: doppler_engine");
@@ -1147,6 +1150,7 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
   t.bp = (float)c.beta_or_p; t.invN = 1.0f / (float)c.N;
   t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
   t.af_mag = grad ? nullptr : af_mag; t.part = ctx->part; t.lred = ctx->lred;
+  t.mld = c.map_ld > 0 ? c.map_ld : ctx->L;
   {
     ProfScope ps(ctx, cls, st);
     with_Q(ctx->Q, [&](auto Qc) {

@@ -47,6 +47,7 @@ class Config(C.Structure):
         ("lr_tol", C.c_double),
         ("net_depth", C.c_int32), ("net_width", C.c_int32),
         ("lr_theta", C.c_double),
+        ("map_ld", C.c_int32),
     ]
 
 
@@ -170,6 +171,7 @@ def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Co
         lr_tol=float(getattr(cfg, "lr_tol", 0.0)),
         net_depth=int(getattr(cfg, "net_depth", 0)), net_width=int(getattr(cfg, "net_width", 0)),
         lr_theta=float(getattr(cfg, "lr_theta", 1e-5)),
+        map_ld=int(getattr(cfg, "map_ld", 0)),
     )
 
 
@@ -258,6 +260,7 @@ class Context:
             self._weights = torch.as_tensor(np.asarray(weights, np.float32), device=self.device).contiguous()
         self.R, self.M, self.N, self.B, self.BR = int(cfg.R), int(cfg.M), int(cfg.N), int(cfg.B), int(cfg.B * cfg.r_n)
         self.K, self.L = int(cfg.K), 2 * int(cfg.N) - 1
+        self.map_ld = int(getattr(cfg, "map_ld", 0)) or self.L  # |A| map row pitch
         self.c_cfg = make_config(cfg, _ptr(self._weights))
         h = C.c_void_p()
         uid = None
@@ -335,7 +338,7 @@ class Context:
                    map_out=None):
         """Forward AF + metrics.  Returns (metrics buffer, p_m [R][M] or None, |A| map or None);
         snrl_out: optional [R][M] float64 tensor that receives SNRL_m (Eq. 10, dB)."""
-        amap = map_out if map_out is not None else (self._f((self.R, self.M, self.M, self.K, self.L)) if want_map
+        amap = map_out if map_out is not None else (self._f((self.R, self.M, self.M, self.K, self.map_ld)) if want_map
                                                     else None)
         p = self.torch.empty((self.R, self.M), dtype=self.torch.float64, device=self.device) if want_p else None
         met = self._met if met_buf is None else met_buf

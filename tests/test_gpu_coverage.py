@@ -308,3 +308,32 @@ def test_determinism_full_size(engine):
     ctx.sync()
     for k in ("z", "rho", "w", "m_w", "v_w", "m_z", "v_z", "m_rho", "v_rho"):
         assert torch.equal(sts[0][k], sts[1][k]), k
+
+
+@pytest.mark.parametrize("ld", [96, 128])
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_map_pitch(engine, ld):
+    """cfg.map_ld: the |A| map with a padded row pitch holds exactly the dense map's values in its first
+    2N-1 columns and leaves the pad untouched (ragged N = 37: dense rows of 73 floats)."""
+    c = Cfg("pitch", M=3, N=37, B=4, K=21, f_lo=-0.5, f_hi=0.5, R=2, r_n=3, doppler_engine=ENGINES[engine])
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=17)
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    s = O.quantize(c, z, rho)["s_hard"]
+    w = (s * np.exp(0.2j * np.sin(0.3 * np.arange(c.N)))).astype(np.complex64)
+    L = 2 * c.N - 1
+    ctx = sqngd.Context(c)
+    met_d, _, dense = ctx.af_forward(T(s), T(w), want_map=True)
+    md = ctx.metrics(met_d)
+    cp = sqngd.Context(c.with_(map_ld=ld))
+    buf = torch.full((c.R, c.M, c.M, c.K, ld), float("nan"), dtype=torch.float32, device=DEV)
+    met_p, _, pitched = cp.af_forward(T(s), T(w), map_out=buf)
+    mp = cp.metrics(met_p)
+    ctx.sync(); cp.sync()
+    assert torch.equal(pitched[..., :L], dense)
+    assert torch.isnan(pitched[..., L:]).all()
+    assert repr(mp) == repr(md)
+
+
+def test_map_pitch_rejected_below_2n_minus_1():
+    with pytest.raises(Exception):
+        sqngd.Context(Cfg("bad_pitch", M=2, N=16, B=4, K=5, f_lo=-0.5, f_hi=0.5, r_n=2, map_ld=20))
