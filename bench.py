@@ -262,35 +262,47 @@ def work_sharded(args, world, rank, local, dev, stream, flush, name="C5"):
         obj = [sqngd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    ctx = sqngd.Context(c, device=local, nccl_uid=uid, rank=rank, world=world)
     z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, r), c.M * c.N).reshape(c.M, c.N)
                   for r in range(c.R)])
     rho = inputs.init_thresholds(c.R, c.B, c.r_n)
-    zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
-    w = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"]
-    st = ctx.new_state(zt, rt, w)
     steps, warm = max(2, min(args.steps, 5)), max(3, min(args.warmup, 3))
-    for _ in range(warm):
-        ctx.step(st, sqngd.BLOCK_AB)
-    ctx.sync()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    if world > 1:
-        import torch.distributed as dist
 
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    for i in range(steps):
-        flush.fill_(float(i))
-        evs[i][0].record(stream)
-        ctx.step(st, sqngd.BLOCK_AB)
-        evs[i][1].record(stream)
-    torch.cuda.synchronize(dev)
-    ctx.sync()
-    ms = parallel.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs)) / steps
-    info = ctx.engine_info()
-    ctx.close()
+    def run(uid_):
+        ctx = sqngd.Context(c, device=local, nccl_uid=uid_, rank=rank, world=world)
+        zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
+        w = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"]
+        st = ctx.new_state(zt, rt, w)
+        for _ in range(warm):
+            ctx.step(st, sqngd.BLOCK_AB)
+        ctx.sync()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(steps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            ctx.step(st, sqngd.BLOCK_AB)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        ctx.sync()
+        ms_ = parallel.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs)) / steps
+        info_ = ctx.engine_info()
+        ctx.close()
+        return ms_, info_
+
+    ms, info = run(uid)
+    # at N = 1, the same problem through the collective path over a 1-rank NCCL communicator (pack,
+    # grouped NCCL all-reduce captured in the graph, unpack): the sharded code's own single-GPU cost
+    ms_1r = run(sqngd.nccl_unique_id())[0] if world == 1 else None
     evals = (c.n_h + c.n_x) * c.R
-    return {"workload": f"{name}: M={c.M} N={c.N} L={c.B} K={c.K} R={c.R} (one problem)", "n_gpus": world,
+    extra = {} if ms_1r is None else {"collective_path_1rank": {
+        "value": evals / (ms_1r / 1e3), "ms_per_step": ms_1r,
+        "what": "the same steps with an ncclUniqueId at world = 1: the sharded path and its grouped NCCL "
+                "all-reduce over a 1-rank communicator"}}
+    return {**extra, "workload": f"{name}: M={c.M} N={c.N} L={c.B} K={c.K} R={c.R} (one problem)", "n_gpus": world,
             "value": evals / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
             "scaling": "strong", "engine": info["engine"],
             "parallelism": f"work-sharded x{world}: (restart, transmit channel) rows, one grouped NCCL "

@@ -140,7 +140,8 @@ typedef struct {
 
 /* Build the context: validates the config (SQNGD_E_INVALID), builds the fp64
    Doppler twiddle table and the workspace on `cuda_device`.  nccl_unique_id:
-   NULL for one GPU, else 128 bytes of an ncclUniqueId shared by all ranks.
+   NULL for one GPU, else 128 bytes of an ncclUniqueId shared by all ranks (with world == 1 an id
+   selects the same collective path over a 1-rank NCCL communicator: the NCCL backend on one GPU).
    Multi-GPU (world > 1): each rank evaluates a shard -- the FFT engine
    a contiguous slice of the R M K (restart, channel, bin) units, the Chebyshev engine a contiguous slice
    of the R M (restart, transmit channel) rows -- and every loss / gradient evaluation ends with ONE

@@ -51,6 +51,7 @@ constexpr int plan_MINB(int P) {
 struct sqngd_ctx_s {
   sqngd_config cfg{};
   int dev = 0, rank = 0, world = 1;
+  bool multi = false;  // the sharded path with its grouped collective (world > 1, or a 1-rank NCCL context)
   int P = 0, L = 0, BR = 0, sms = 0;
   uint32_t n_cells = 0, flags = 0;
   // persistent grid: resident groups per fused-kernel mode (0 fwd, 1 adj A, 2 adj B)
@@ -884,7 +885,11 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
     ctx->row_lo = (int)lo;
     ctx->row_hi = (int)hi;
   }
-  if (world > 1) {  // one grouped collective per evaluation (comm.h)
+  // One grouped collective per evaluation (comm.h) for world > 1.  With world == 1 an ncclUniqueId
+  // still selects the collective path over a 1-rank NCCL communicator: the same code (pack, grouped
+  // NCCL calls captured in the step graph, unpack) runs on one GPU.
+  if (world > 1 || nccl_unique_id) {
+    ctx->multi = true;
     CK(cudaMalloc(&ctx->pay, sizeof(double) * (size_t)cfg.R * (1 + 2 * (size_t)cfg.M * cfg.N)));
     CK(cudaMalloc(&ctx->keyb, sizeof(unsigned long long) * 3 * cfg.R));
     CK(cudaMalloc(&ctx->mref, sizeof(double) * cfg.R));
@@ -1166,7 +1171,7 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
     fs = ctx->side;
   }
   MetricsArgs mloc = ma;  // multi-GPU: the metrics follow the collective
-  if (ctx->world > 1) { mloc.out = nullptr; mloc.p_out = nullptr; mloc.loss_hist = nullptr; }
+  if (ctx->multi) { mloc.out = nullptr; mloc.p_out = nullptr; mloc.loss_hist = nullptr; }
   k_lr_finish<<<c.R, 1024, 0, fs>>>(GPR, g_lo, g_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->lred, ctx->red, mloc,
                                     ctx->status);
   if (fork) CK(cudaEventRecord(ctx->ev_join, ctx->side));
@@ -1200,10 +1205,10 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
     ctx->launches += 2;
     if ((rc = launch_check(ctx, "af forward"))) return rc;
     k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
-                                          ctx->red, ctx->world == 1 ? ma : none, ctx->status);
+                                          ctx->red, ctx->multi ? none : ma, ctx->status);
     if ((rc = launch_check(ctx, "metrics"))) return rc;
   }
-  if (ctx->world == 1) return SQNGD_OK;
+  if (!ctx->multi) return SQNGD_OK;
   // multi-GPU: c_m of every row, the grouped collective, then the metrics
   if ((rc = run_cm_rows(ctx, s, w, st))) return rc;
   if ((rc = world_combine(ctx, false, st))) return rc;
@@ -1236,7 +1241,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
   MetricsArgs none = ma;
   none.out = nullptr; none.loss_hist = nullptr;
   const size_t n = (size_t)c.R * c.M * c.N;
-  const bool multi = ctx->world > 1;
+  const bool multi = ctx->multi;
   if (c.loss_mode == SQNGD_LOSS_MAX) {  // Eq. 37: the exact maximum, its O(N) subgradient on every rank
     if ((rc = run_forward(ctx, s, w, nullptr, met, nullptr, hist, hist_col, st, true, snrl_in))) return rc;
     k_sparse_adj<<<c.R, 256, 0, st>>>(c.M, c.N, c.K, ctx->L, wrt, c.eps_w, c.weights, s, w, ctx->tw, ctx->red,
@@ -1483,7 +1488,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
     if ((rc = run_xhat(ctx, ctx->s_hard, st, nullptr, true))) return rc;  // X_hard fixed for the block
     if (hard_out) {  // SNRL of the entry pair; on the Chebyshev engine beside the first evaluation (its
                      // k_lr_finish, which reads it, runs later on the same side stream and is joined)
-      const bool side = ctx->lr && ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
+      const bool side = ctx->lr && !ctx->multi && c.loss_mode != SQNGD_LOSS_MAX;
       cudaStream_t ss = st;
       if (side) {
         CK(cudaEventRecord(ctx->ev_fork, st));
@@ -1492,7 +1497,7 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
       }
       if ((rc = run_snrl(ctx, ctx->s_hard, w2, nullptr, nullptr, ss, ctx->snrl_w))) return rc;
     }
-    const bool fused = ctx->world == 1 && c.loss_mode != SQNGD_LOSS_MAX;
+    const bool fused = !ctx->multi && c.loss_mode != SQNGD_LOSS_MAX;
     h_ready = fused && c.n_h > 0;  // the fused row kernel leaves H = FFT(w)/P of the updated w
     for (int i = 0; i < c.n_h; ++i) {
       MetricsOut* met = (i == 0 && hard_out) ? reinterpret_cast<MetricsOut*>(hard_out) : ctx->met;
@@ -1604,7 +1609,7 @@ sqngd_status sqngd_step(sqngd_ctx ctx, sqngd_state* stt, int block, double* loss
     ctx->launches += 1;
   };
   // Graph path: one GPU or NCCL (the collective is captured with the step), a capturable (non-legacy) stream.
-  const bool graph_ok = ctx->use_graphs && !ctx->prof && (ctx->world == 1 || ctx->comm->capturable()) && st != nullptr &&
+  const bool graph_ok = ctx->use_graphs && !ctx->prof && (!ctx->multi || ctx->comm->capturable()) && st != nullptr &&
                         st != cudaStreamLegacy && st != cudaStreamPerThread;
   if (!graph_ok) {
     launch_set_t();

@@ -170,3 +170,49 @@ def test_c5_row_shard_gradient_8_ranks():
     d = np.linalg.norm(res[0][1] - gz1) / np.linalg.norm(gz1)
     record("C5-shape 8-rank grad_z vs single", d, 1e-5)
     assert d < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["lse", "pnorm", "max"])
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_nccl_one_rank_collective_path(engine, mode):
+    """The NCCL backend itself on one GPU: an ncclUniqueId with world = 1 runs the sharded code path with
+    its grouped collective (k_world_pack, ncclGroupStart / AllReduce SUM fp64 + MAX u64 / GroupEnd,
+    k_world_unpack, k_finalize_grad) over a 1-rank communicator; it must match the oracle and the plain
+    single-GPU context, eagerly and inside the step's CUDA graph."""
+    lm, bp = MODES[mode]
+    c = CASES[1].with_(loss_mode=lm, beta_or_p=bp, doppler_engine=ENGINES[engine])
+    z, rho, q, w = inputs_for(c, 97)
+    ctx = sqngd.Context(c, nccl_uid=sqngd.nccl_unique_id(), rank=0, world=1)
+    got = eval_all(ctx, z, rho, w)
+    single = eval_all(sqngd.Context(c), z, rho, w)
+    refA, gw_ref, _ = O.loss_grad(c, q["s_hard"], w, want_s=False)
+    refB, _, gs_ref = O.loss_grad(c, q["s_soft"], w, want_w=False)
+    gz_ref, gr_ref = O.chain(c, z, rho, q["s_soft"], gs_ref)
+    for rr in range(c.R):
+        check_loss(got["mA"][rr]["loss"], refA[rr]["loss"], "1-rank NCCL Step-A loss")
+        check_loss(got["mB"][rr]["loss"], refB[rr]["loss"], "1-rank NCCL Step-B loss")
+        assert got["mf"][rr]["argmax_auto"] == single["mf"][rr]["argmax_auto"]
+    check_grad(got["gw"], gw_ref, "1-rank NCCL grad_w")
+    check_grad(got["gz"], gz_ref, "1-rank NCCL grad_z")
+    check_grad(got["gr"], gr_ref, "1-rank NCCL grad_rho")
+    d = max(np.linalg.norm(got[k] - single[k]) / np.linalg.norm(single[k]) for k in ("gw", "gz", "gr"))
+    record("1-rank NCCL vs single-context gradient rel", d, 1e-5)
+    assert d < 1e-5
+    # the step graph with the NCCL calls captured (non-legacy stream), three outer iterations
+    cs = c.with_(n_h=2, n_x=2, lr_z=1e-3)
+    wq = q["s_hard"].astype(np.complex64)
+    res = {}
+    for name, kw in (("nccl", dict(nccl_uid=sqngd.nccl_unique_id(), rank=0, world=1)), ("single", {})):
+        cx = sqngd.Context(cs, **kw)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            st = cx.new_state(T(z), T(rho), T(wq))
+            hist = torch.zeros((cs.R, cs.n_h + cs.n_x), dtype=torch.float64, device=DEV)
+            for _ in range(3):
+                cx.step(st, sqngd.BLOCK_AB, hist=hist)
+        s.synchronize()
+        cx.sync()
+        res[name] = {k: st[k].cpu().numpy() for k in ("z", "rho", "w")} | {"hist": hist.cpu().numpy()}
+    np.testing.assert_allclose(res["nccl"]["hist"], res["single"]["hist"], rtol=1e-6)
+    np.testing.assert_allclose(res["nccl"]["w"], res["single"]["w"], rtol=0, atol=1e-5)
+    np.testing.assert_allclose(res["nccl"]["z"], res["single"]["z"], rtol=0, atol=1e-6)
