@@ -285,6 +285,12 @@ sqngd_status sqngd_run(sqngd_ctx ctx, sqngd_state* state, const sqngd_run_opts* 
 sqngd_status sqngd_profile_enable(sqngd_ctx ctx, int on);
 sqngd_status sqngd_profile_read(sqngd_ctx ctx, double* ms, int64_t* count, int64_t* launches, int reset);
 
+/* Debug: with the environment variable SQNGD_GUARD=1 at sqngd_create, every workspace buffer of the
+   context is allocated with a 4 KiB guard band on each side (filled with 0x5A).  sqngd_check_guards
+   synchronizes the device and sets *corrupted to the number of buffers whose guard bands changed (an
+   out-of-bounds write by a kernel), or -1 when the context was created without guards. */
+sqngd_status sqngd_check_guards(sqngd_ctx ctx, int64_t* corrupted);
+
 /* Host utilities (no GPU needed). */
 int64_t sqngd_num_units(const sqngd_config* cfg); /* R * M * K evaluation units */
 /* Contiguous slice [lo, hi) of the units owned by `rank` of `world`. */

@@ -49,6 +49,33 @@ constexpr int plan_MINB(int P) {
 }  // namespace
 
 struct sqngd_ctx_s {
+  // Device allocations of the workspace.  With SQNGD_GUARD=1 (read at create) every buffer gets a
+  // 4 KiB guard band on each side filled with 0x5A; sqngd_check_guards verifies the bands (an
+  // out-of-bounds write by any kernel into a neighbouring guard shows up as a changed byte).
+  static constexpr size_t kGuard = 4096;
+  bool guard = false;
+  std::vector<std::pair<char*, size_t>> guarded;  // (base, user bytes)
+  template <class T>
+  cudaError_t dmalloc(T** p, size_t bytes) {
+    if (!guard) return cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuard);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemset(base, 0x5A, bytes + 2 * kGuard)) != cudaSuccess) return e;
+    guarded.push_back({base, bytes});
+    *p = reinterpret_cast<T*>(base + kGuard);
+    return cudaSuccess;
+  }
+  void dfree(void* p) {
+    if (!p) return;
+    for (auto& g : guarded)
+      if (g.first + kGuard == p) {
+        cudaFree(g.first);
+        g.first = nullptr;
+        return;
+      }
+    cudaFree(p);
+  }
   sqngd_config cfg{};
   int dev = 0, rank = 0, world = 1;
   bool multi = false;  // the sharded path with its grouped collective (world > 1, or a 1-rank NCCL context)
@@ -522,7 +549,7 @@ void* sq_ctx_run_ws(sqngd_ctx ctx, size_t dev_bytes, void** host, size_t host_by
     if (ctx->run_dev) cudaFree(ctx->run_dev);
     ctx->run_dev = nullptr;
     ctx->run_dev_bytes = 0;
-    if (cudaMalloc(&ctx->run_dev, dev_bytes) != cudaSuccess) return nullptr;
+    if (ctx->dmalloc(&ctx->run_dev, dev_bytes) != cudaSuccess) return nullptr;
     ctx->run_dev_bytes = dev_bytes;
   }
   if (host_bytes > ctx->run_host_bytes) {
@@ -570,6 +597,7 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
     return fail(nullptr, SQNGD_E_INVALID, "sqngd_create: M^2 (2N-1) K cell index exceeds 32 bits");
 
   ctx = new sqngd_ctx_s();
+  if (const char* e = getenv("SQNGD_GUARD")) ctx->guard = e[0] == '1';
   ctx->cfg = cfg;
   ctx->dev = cuda_device;
   ctx->rank = rank;
@@ -674,38 +702,38 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   }
 
   const size_t RMN = (size_t)cfg.R * cfg.M * cfg.N;
-  CK(cudaMalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
-  CK(cudaMalloc(&ctx->H, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
+  CK(ctx->dmalloc(&ctx->tw, sizeof(float2) * (size_t)cfg.K * cfg.N));
+  CK(ctx->dmalloc(&ctx->H, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   // X cache: K bins (FFT engine) or Q nodes (Chebyshev engine; Q may exceed K when forced)
-  CK(cudaMalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * std::max(cfg.K, ctx->Q) * P));
-  CK(cudaMalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
+  CK(ctx->dmalloc(&ctx->Xc, sizeof(float2) * (size_t)cfg.R * cfg.M * std::max(cfg.K, ctx->Q) * P));
+  CK(ctx->dmalloc(&ctx->ftw, sizeof(float2) * ftw_host.size()));
   CK(cudaMemcpy(ctx->ftw, ftw_host.data(), sizeof(float2) * ftw_host.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->ftwn, sizeof(float2) * ftwn_host.size()));
+  CK(ctx->dmalloc(&ctx->ftwn, sizeof(float2) * ftwn_host.size()));
   CK(cudaMemcpy(ctx->ftwn, ftwn_host.data(), sizeof(float2) * ftwn_host.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->ftwr, sizeof(float2) * ftwr_host.size()));
+  CK(ctx->dmalloc(&ctx->ftwr, sizeof(float2) * ftwr_host.size()));
   CK(cudaMemcpy(ctx->ftwr, ftwr_host.data(), sizeof(float2) * ftwr_host.size(), cudaMemcpyHostToDevice));
   const int64_t uslots = std::max(ctx->units, ctx->units_lr);
   const int64_t gslots = std::max(ctx->units, ctx->lr ? (int64_t)cfg.R * cfg.M * cfg.M * ctx->Q : (int64_t)0);
-  CK(cudaMalloc(&ctx->part.scale, sizeof(float) * uslots));
-  CK(cudaMalloc(&ctx->counter, 2 * sizeof(int)));
-  CK(cudaMalloc(&ctx->d_t, 2 * sizeof(long long)));
-  CK(cudaMalloc(&ctx->snrl_w, sizeof(double) * cfg.R));
+  CK(ctx->dmalloc(&ctx->part.scale, sizeof(float) * uslots));
+  CK(ctx->dmalloc(&ctx->counter, 2 * sizeof(int)));
+  CK(ctx->dmalloc(&ctx->d_t, 2 * sizeof(long long)));
+  CK(ctx->dmalloc(&ctx->snrl_w, sizeof(double) * cfg.R));
   ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
-  CK(cudaMalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
+  CK(ctx->dmalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
-  CK(cudaMalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
-  CK(cudaMalloc(&ctx->s_soft, sizeof(float2) * RMN));
-  CK(cudaMalloc(&ctx->s_hard, sizeof(float2) * RMN));
-  CK(cudaMalloc(&ctx->dq, sizeof(float) * RMN));
-  CK(cudaMalloc(&ctx->lut, sizeof(int) * (size_t)cfg.R * (ctx->BR + 1)));
-  CK(cudaMalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * uslots));
-  CK(cudaMalloc(&ctx->part.m, sizeof(float) * uslots));
-  CK(cudaMalloc(&ctx->part.S, sizeof(float) * uslots));
-  CK(cudaMalloc(&ctx->part.g, sizeof(float2) * (size_t)gslots * P));
-  CK(cudaMalloc(&ctx->red, sizeof(Red) * cfg.R));
-  CK(cudaMalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
-  CK(cudaMalloc(&ctx->red_grad, sizeof(float2) * RMN));
-  CK(cudaMalloc(&ctx->dy, sizeof(float) * RMN));
+  CK(ctx->dmalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
+  CK(ctx->dmalloc(&ctx->s_soft, sizeof(float2) * RMN));
+  CK(ctx->dmalloc(&ctx->s_hard, sizeof(float2) * RMN));
+  CK(ctx->dmalloc(&ctx->dq, sizeof(float) * RMN));
+  CK(ctx->dmalloc(&ctx->lut, sizeof(int) * (size_t)cfg.R * (ctx->BR + 1)));
+  CK(ctx->dmalloc(&ctx->part.key, sizeof(unsigned long long) * 2 * uslots));
+  CK(ctx->dmalloc(&ctx->part.m, sizeof(float) * uslots));
+  CK(ctx->dmalloc(&ctx->part.S, sizeof(float) * uslots));
+  CK(ctx->dmalloc(&ctx->part.g, sizeof(float2) * (size_t)gslots * P));
+  CK(ctx->dmalloc(&ctx->red, sizeof(Red) * cfg.R));
+  CK(ctx->dmalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
+  CK(ctx->dmalloc(&ctx->red_grad, sizeof(float2) * RMN));
+  CK(ctx->dmalloc(&ctx->dy, sizeof(float) * RMN));
   ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   {  // Adam(rho) + projection: 2 n2 floats of dynamic shared memory (64 KB at B r_n = 8192, above
      // the 48 KB a launch gets without opting in)
@@ -714,19 +742,19 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
     CK(cudaFuncSetAttribute(k_adam_project_rho, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(2 * n2 * sizeof(float))));
   }
-  CK(cudaMalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
-  CK(cudaMalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
+  CK(ctx->dmalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
+  CK(ctx->dmalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
   CK(cudaMemset(ctx->rho_cnt, 0, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
-  CK(cudaMalloc(&ctx->gw, sizeof(float2) * RMN));
-  CK(cudaMalloc(&ctx->gz, sizeof(float) * RMN));
-  CK(cudaMalloc(&ctx->grho, sizeof(float) * (size_t)cfg.R * ctx->BR));
-  CK(cudaMalloc(&ctx->met, sizeof(MetricsOut) * cfg.R));
-  CK(cudaMalloc(&ctx->status, sizeof(int)));
+  CK(ctx->dmalloc(&ctx->gw, sizeof(float2) * RMN));
+  CK(ctx->dmalloc(&ctx->gz, sizeof(float) * RMN));
+  CK(ctx->dmalloc(&ctx->grho, sizeof(float) * (size_t)cfg.R * ctx->BR));
+  CK(ctx->dmalloc(&ctx->met, sizeof(MetricsOut) * cfg.R));
+  CK(ctx->dmalloc(&ctx->status, sizeof(int)));
   CK(cudaMemset(ctx->status, 0, sizeof(int)));
   if (cfg.net_width != 0) {
     ctx->net = true;
     ctx->nd = nd;
-    CK(cudaMalloc(&ctx->net_ws, sizeof(float) * net_ws_floats(nd)));
+    CK(ctx->dmalloc(&ctx->net_ws, sizeof(float) * net_ws_floats(nd)));
     ctx->nws = net_ws_carve(nd, ctx->net_ws);
     CK(net_prepare(nd));
     CK(cudaStreamCreateWithFlags(&ctx->side_net, cudaStreamNonBlocking));
@@ -767,9 +795,9 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
       }
     if (cfg.K & 1)
       for (int j = 0; j < QH; ++j) cf[(size_t)Kp * ctx->QS + j] = (float)lr_ell[(size_t)Kp * Q + j];
-    CK(cudaMalloc(&ctx->Vt, sizeof(float2) * vt.size()));
+    CK(ctx->dmalloc(&ctx->Vt, sizeof(float2) * vt.size()));
     CK(cudaMemcpy(ctx->Vt, vt.data(), sizeof(float2) * vt.size(), cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&ctx->coef, sizeof(float) * cf.size()));
+    CK(ctx->dmalloc(&ctx->coef, sizeof(float) * cf.size()));
     CK(cudaMemcpy(ctx->coef, cf.data(), sizeof(float) * cf.size(), cudaMemcpyHostToDevice));
     {  // k_lrt B fragments: alpha / beta per (j, pair), TF32 hi + lo, in mma.sync m16n8k8 lane order
       auto alpha = [&](int j, int p) -> double {
@@ -845,14 +873,14 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
           m16[ln] = make_uint2(col0 ? pack(Bk(2 * cc, 0, true, true), Bk(2 * cc + 1, 0, true, true)) : 0u,
                                col0 ? pack(Bk(2 * cc + 8, 0, true, true), Bk(2 * cc + 9, 0, true, true)) : 0u);
         }
-        CK(cudaMalloc(&ctx->tabF16, sizeof(uint4) * t16.size()));
+        CK(ctx->dmalloc(&ctx->tabF16, sizeof(uint4) * t16.size()));
         CK(cudaMemcpy(ctx->tabF16, t16.data(), sizeof(uint4) * t16.size(), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&ctx->tabM16, sizeof(uint2) * 32));
+        CK(ctx->dmalloc(&ctx->tabM16, sizeof(uint2) * 32));
         CK(cudaMemcpy(ctx->tabM16, m16.data(), sizeof(uint2) * 32, cudaMemcpyHostToDevice));
       }
-      CK(cudaMalloc(&ctx->tabF, sizeof(float4) * tf.size()));
+      CK(ctx->dmalloc(&ctx->tabF, sizeof(float4) * tf.size()));
       CK(cudaMemcpy(ctx->tabF, tf.data(), sizeof(float4) * tf.size(), cudaMemcpyHostToDevice));
-      CK(cudaMalloc(&ctx->tabA, sizeof(float4) * ta.size()));
+      CK(ctx->dmalloc(&ctx->tabA, sizeof(float4) * ta.size()));
       CK(cudaMemcpy(ctx->tabA, ta.data(), sizeof(float4) * ta.size(), cudaMemcpyHostToDevice));
     }
     std::vector<float> wm((size_t)L, 1.f);
@@ -865,18 +893,18 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
         wm[i] = mx;
       }
     }
-    CK(cudaMalloc(&ctx->wmax, sizeof(float) * L));
+    CK(ctx->dmalloc(&ctx->wmax, sizeof(float) * L));
     CK(cudaMemcpy(ctx->wmax, wm.data(), sizeof(float) * L, cudaMemcpyHostToDevice));
     const size_t pairs = (size_t)cfg.R * cfg.M * cfg.M;
-    CK(cudaMalloc(&ctx->Rn, sizeof(float2) * pairs * Q * ctx->LS));
-    CK(cudaMalloc(&ctx->Gn, sizeof(float2) * pairs * Q * ctx->LS));
-    CK(cudaMalloc(&ctx->lred, sizeof(LrRed) * cfg.R));
+    CK(ctx->dmalloc(&ctx->Rn, sizeof(float2) * pairs * Q * ctx->LS));
+    CK(ctx->dmalloc(&ctx->Gn, sizeof(float2) * pairs * Q * ctx->LS));
+    CK(ctx->dmalloc(&ctx->lred, sizeof(LrRed) * cfg.R));
     CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     // (splitting each node's l sum over 2 CTAs to fill more SMs at C3 (80 nodes) measured no gain:
     // 10543 vs 10685 evals/s; lsplit stays 1)
-    CK(cudaMalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ctx->lsplit * ((cfg.N + 1) & ~1)));
+    CK(ctx->dmalloc(&ctx->tslot, sizeof(float2) * (size_t)cfg.R * cfg.M * Q * ctx->lsplit * ((cfg.N + 1) & ~1)));
   }
 
   {  // this rank's shard of the Chebyshev engine's (restart, transmit channel) rows
@@ -890,9 +918,9 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   // NCCL calls captured in the step graph, unpack) runs on one GPU.
   if (world > 1 || nccl_unique_id) {
     ctx->multi = true;
-    CK(cudaMalloc(&ctx->pay, sizeof(double) * (size_t)cfg.R * (1 + 2 * (size_t)cfg.M * cfg.N)));
-    CK(cudaMalloc(&ctx->keyb, sizeof(unsigned long long) * 3 * cfg.R));
-    CK(cudaMalloc(&ctx->mref, sizeof(double) * cfg.R));
+    CK(ctx->dmalloc(&ctx->pay, sizeof(double) * (size_t)cfg.R * (1 + 2 * (size_t)cfg.M * cfg.N)));
+    CK(ctx->dmalloc(&ctx->keyb, sizeof(unsigned long long) * 3 * cfg.R));
+    CK(ctx->dmalloc(&ctx->mref, sizeof(double) * cfg.R));
     k_world_init<<<(cfg.R + 127) / 128, 128>>>(cfg.R, cfg.loss_mode, ctx->mref);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -948,6 +976,29 @@ sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqn
   return create_impl(cfg, cuda_device, nullptr, &group->g, rank, group->g.world, out);
 }
 
+sqngd_status sqngd_check_guards(sqngd_ctx ctx, int64_t* corrupted) {
+  if (!ctx || !corrupted) return fail(ctx, SQNGD_E_INVALID, "sqngd_check_guards: null argument");
+  *corrupted = -1;
+  if (!ctx->guard) return SQNGD_OK;
+  CK(cudaSetDevice(ctx->dev));
+  CK(cudaDeviceSynchronize());
+  const size_t G = sqngd_ctx_s::kGuard;
+  std::vector<unsigned char> band(G);
+  int64_t bad = 0;
+  for (auto& g : ctx->guarded) {
+    if (!g.first) continue;
+    bool ok = true;
+    for (int side = 0; side < 2 && ok; ++side) {
+      CK(cudaMemcpy(band.data(), g.first + (side ? G + g.second : 0), G, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < G; ++i)
+        if (band[i] != 0x5A) { ok = false; break; }
+    }
+    bad += ok ? 0 : 1;
+  }
+  *corrupted = bad;
+  return SQNGD_OK;
+}
+
 void sqngd_destroy(sqngd_ctx ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
@@ -964,9 +1015,8 @@ void sqngd_destroy(sqngd_ctx ctx) {
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
                   ctx->Gn, ctx->tslot, ctx->lred, ctx->pay, ctx->keyb, ctx->mref, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
-  if (ctx->run_dev) cudaFree(ctx->run_dev);
+  for (void* p : ptrs) ctx->dfree(p);
+  if (ctx->run_dev) ctx->dfree(ctx->run_dev);
   if (ctx->run_host) cudaFreeHost(ctx->run_host);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);

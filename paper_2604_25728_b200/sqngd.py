@@ -115,6 +115,8 @@ def lib():
         L.sqngd_step.argtypes = [vp, C.POINTER(State), i32, vp, vp, vp]
         L.sqngd_profile_enable.restype = i32
         L.sqngd_profile_enable.argtypes = [vp, i32]
+        L.sqngd_check_guards.restype = i32
+        L.sqngd_check_guards.argtypes = [vp, C.POINTER(C.c_int64)]
         L.sqngd_profile_read.restype = i32
         L.sqngd_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64), i32]
         L.sqngd_num_units.restype = i64
@@ -149,7 +151,7 @@ EXPORTED = ["sqngd_create", "sqngd_destroy", "sqngd_last_error", "sqngd_sync", "
             "sqngd_profile_enable", "sqngd_profile_read",
             "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info",
             "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward", "sqngd_run",
-            "sqngd_loopback_create", "sqngd_loopback_destroy", "sqngd_create_loopback"]
+            "sqngd_loopback_create", "sqngd_loopback_destroy", "sqngd_create_loopback", "sqngd_check_guards"]
 
 
 def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Config:
@@ -428,6 +430,12 @@ class Context:
                      t_a=int(st["t_a"]), t_b=int(st["t_b"]),
                      theta=_ptr(st.get("theta")), m_theta=_ptr(st.get("m_theta")),
                      v_theta=_ptr(st.get("v_theta")), y0=_ptr(st.get("y0")))
+
+    def check_guards(self) -> int:
+        """Buffers whose guard bands changed (SQNGD_GUARD=1 at create), or -1 without guards."""
+        n = C.c_int64(0)
+        self._check(lib().sqngd_check_guards(self.h, C.byref(n)))
+        return int(n.value)
 
     def step(self, st: dict, block: int = BLOCK_AB, hist=None, hard_met=None):
         cs = State(z=_ptr(st["z"]), rho=_ptr(st["rho"]), w=_ptr(st["w"]), m_z=_ptr(st["m_z"]), v_z=_ptr(st["v_z"]),
