@@ -17,6 +17,7 @@
 #include "../../include/sqngd.h"
 #include "comm.h"
 #include "lr_kernels.cuh"
+#include "lr_tc.cuh"
 #include "misc_kernels.cuh"
 #include "net.cuh"
 #include "run.cuh"
@@ -122,6 +123,10 @@ struct sqngd_ctx_s {
   float4* tabA = nullptr;      // [NT][32][2] k_lrt adjoint B fragments
   uint4* tabF16 = nullptr;     // [NT][32] k_lrt forward B fragments (FP16 packed split)
   uint2* tabM16 = nullptr;     // [32] k_lrt middle-bin B fragment
+  uint4* tabB = nullptr;       // [npc][2] k_lrf (tcgen05 forward) B images, one per 64 bin pairs
+  int nc128 = 0, npc = 0;      // k_lrf: 128-lag chunks per pair, 64-pair MMA chunks
+  bool use_lrf = false;        // forward-only contraction on tcgen05 (k_lrf) instead of k_lrt
+  size_t lrf_smem = 0;
   int64_t units_lr = 0;        // fused-kernel units: R M^2 x (16-lag chunks for k_lrt | 128-lag tiles for k_lrt5)
   size_t lr_smem = 0;          // k_lrt dynamic shared memory
   LrRed* lred = nullptr;       // [R] running maxima of the fused kernel
@@ -403,6 +408,41 @@ struct LrLaunch {
   }
   static cudaError_t occupancy_t(int* bps, int threads, size_t smem) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lrt<Q, 1, false, 1>, threads, smem);
+  }
+};
+
+// k_lrf (tcgen05 forward contraction) instantiations: loss mode x weighted ROI x map.
+struct LrfLaunch {
+  template <int LM, bool HW, bool MAP>
+  static cudaError_t attr(size_t smem) {
+    return cudaFuncSetAttribute(k_lrf<LM, HW, MAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  template <int LM>
+  static cudaError_t attr_lm(size_t smem) {
+    cudaError_t e;
+    if ((e = attr<LM, false, false>(smem)) || (e = attr<LM, true, false>(smem)) || (e = attr<LM, false, true>(smem)) ||
+        (e = attr<LM, true, true>(smem)))
+      return e;
+    return cudaSuccess;
+  }
+  static cudaError_t prepare(size_t smem) {
+    cudaError_t e;
+    if ((e = attr_lm<0>(smem)) || (e = attr_lm<1>(smem)) || (e = attr_lm<2>(smem))) return e;
+    return cudaSuccess;
+  }
+  template <int LM, bool HW, bool MAP>
+  static void go(const LrfArgs& a, int rows, size_t smem, cudaStream_t st) {
+    if (rows > 0) k_lrf<LM, HW, MAP><<<dim3(a.nc, a.M, rows), kLrfThreads, smem, st>>>(a);
+  }
+  template <int LM>
+  static void go_lm(bool hw, bool map, const LrfArgs& a, int rows, size_t smem, cudaStream_t st) {
+    if (map) hw ? go<LM, true, true>(a, rows, smem, st) : go<LM, false, true>(a, rows, smem, st);
+    else hw ? go<LM, true, false>(a, rows, smem, st) : go<LM, false, false>(a, rows, smem, st);
+  }
+  static void launch(int lm, bool hw, bool map, const LrfArgs& a, int rows, size_t smem, cudaStream_t st) {
+    if (lm == 0) go_lm<0>(hw, map, a, rows, smem, st);
+    else if (lm == 1) go_lm<1>(hw, map, a, rows, smem, st);
+    else go_lm<2>(hw, map, a, rows, smem, st);
   }
 };
 
@@ -878,6 +918,37 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
         CK(ctx->dmalloc(&ctx->tabM16, sizeof(uint2) * 32));
         CK(cudaMemcpy(ctx->tabM16, m16.data(), sizeof(uint2) * 32, cudaMemcpyHostToDevice));
       }
+      // k_lrf (tcgen05 forward): per 32-pair chunk c, two 64 x 16 fp16 images in the canonical K-major
+      // layout (lrf_off): row n = output column (n < 32: A0 of pair 32c + n, else A1 of pair 32c + n - 32),
+      // K = [hi(c_j) j<5 | hi(c_j) | lo(c_j) | 0]; B_E holds alpha, B_O holds +beta (A0) / -beta (A1).
+      if (QH <= 5 && Kp >= 1) {
+        ctx->nc128 = (L + kLrfRows - 1) / kLrfRows;
+        ctx->npc = (Kp + kLrfPairs - 1) / kLrfPairs;
+        std::vector<uint8_t> img((size_t)ctx->npc * 2 * kLrfImgB, 0);
+        for (int cch = 0; cch < ctx->npc; ++cch)
+          for (int e = 0; e < 2; ++e)
+            for (int n = 0; n < 2 * kLrfPairs; ++n) {
+              const int p = cch * kLrfPairs + (n % kLrfPairs);
+              if (p >= Kp) continue;
+              const double sg = (e == 1 && n >= kLrfPairs) ? -1.0 : 1.0;
+              for (int j = 0; j < QH; ++j) {
+                const double cv = sg * (e == 0 ? alpha(j, p) : beta(j, p));
+                const __half h = __float2half_rn((float)cv);
+                const __half lo = __float2half_rn((float)(cv - (double)__half2float(h)));
+                const uint16_t parts[3] = {__half_as_ushort(h), __half_as_ushort(h), __half_as_ushort(lo)};
+                for (int t3 = 0; t3 < 3; ++t3) {
+                  const uint32_t off = (uint32_t)(cch * 2 + e) * kLrfImgB + lrf_off(n, 5 * t3 + j);
+                  std::memcpy(&img[off], &parts[t3], 2);
+                }
+              }
+            }
+        CK(ctx->dmalloc(&ctx->tabB, img.size()));
+        CK(cudaMemcpy(ctx->tabB, img.data(), img.size(), cudaMemcpyHostToDevice));
+        ctx->lrf_smem = lrf_smem_bytes(ctx->npc, QH);
+        ctx->use_lrf = ctx->lrf_smem <= 200 * 1024;
+        if (const char* ev = getenv("SQNGD_LRF")) ctx->use_lrf = ctx->use_lrf && ev[0] != '0';
+        if (ctx->use_lrf) CK(LrfLaunch::prepare(ctx->lrf_smem));
+      }
       CK(ctx->dmalloc(&ctx->tabF, sizeof(float4) * tf.size()));
       CK(cudaMemcpy(ctx->tabF, tf.data(), sizeof(float4) * tf.size(), cudaMemcpyHostToDevice));
       CK(ctx->dmalloc(&ctx->tabA, sizeof(float4) * ta.size()));
@@ -1011,7 +1082,7 @@ void sqngd_destroy(sqngd_ctx ctx) {
     }
     delete g;
   }
-  void* ptrs[] = {ctx->snrl_w, ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
+  void* ptrs[] = {ctx->tabB, ctx->snrl_w, ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
                   ctx->Gn, ctx->tslot, ctx->lred, ctx->pay, ctx->keyb, ctx->mref, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
@@ -1206,14 +1277,30 @@ static sqngd_status run_lr(sqngd_ctx ctx, bool grad, int cls, float* af_mag, con
   t.weights = c.weights; t.wmax = ctx->wmax; t.tabF = ctx->tabF; t.tabA = ctx->tabA; t.Rn = ctx->Rn; t.Gn = ctx->Gn;
   t.af_mag = grad ? nullptr : af_mag; t.part = ctx->part; t.lred = ctx->lred;
   t.mld = c.map_ld > 0 ? c.map_ld : ctx->L;
+  // the tcgen05 forward (lr_tc.cuh) where it measured faster: writing the dense |A| map (C3: 65 vs 75 us;
+  // its map stores are 32 consecutive lags of one bin per warp).  Without a map, or with a pitched map,
+  // the mma.sync kernel is faster (35 vs 42 us; 49 vs 65 us): DESIGN.md §6 "tcgen05 forward".
+  const bool tc = !grad && ctx->use_lrf && af_mag != nullptr && c.map_ld == 0;
   {
     ProfScope ps(ctx, cls, st);
-    with_Q(ctx->Q, [&](auto Qc) {
-      decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad ? 1 : (af_mag ? 2 : 0), t, rows, ctx->lr_smem, st);
-    });
+    if (tc) {
+      LrfArgs f{};
+      f.M = c.M; f.N = c.N; f.L = ctx->L; f.K = c.K; f.Kp = c.K / 2; f.Q = ctx->Q; f.nc = ctx->nc128;
+      f.npc = ctx->npc; f.row0 = ctx->row_lo; f.tau_lo = c.tau_lo; f.tau_hi = c.tau_hi;
+      f.excl0 = c.exclude_auto_zero_delay; f.LS = ctx->LS; f.mld = t.mld; f.bp = t.bp; f.invN = t.invN;
+      f.weights = c.weights; f.wmax = ctx->wmax; f.coefm = t.coefm; f.tabB = ctx->tabB; f.Rn = ctx->Rn;
+      f.af_mag = af_mag; f.part = ctx->part; f.lred = ctx->lred;
+      LrfLaunch::launch(c.loss_mode, c.weights != nullptr, af_mag != nullptr, f, rows, ctx->lrf_smem, st);
+    } else {
+      with_Q(ctx->Q, [&](auto Qc) {
+        decltype(Qc)::launch_t(c.loss_mode, c.weights != nullptr, grad ? 1 : (af_mag ? 2 : 0), t, rows, ctx->lr_smem,
+                               st);
+      });
+    }
   }
-  const int GPR = (int)(ctx->units_lr / c.R);
-  const int g_lo = ctx->row_lo * c.M * ctx->nch16, g_hi = ctx->row_hi * c.M * ctx->nch16;
+  const int nchu = tc ? ctx->nc128 : ctx->nch16;  // unit chunks per pair of the launched kernel
+  const int GPR = c.M * c.M * nchu;
+  const int g_lo = ctx->row_lo * c.M * nchu, g_hi = ctx->row_hi * c.M * nchu;
   cudaStream_t fs = st;
   if (fork) {  // k_lr_finish runs beside the adjoint kernels; run_loss_grad joins before the combine
     CK(cudaEventRecord(ctx->ev_fork, st));

@@ -206,6 +206,22 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+_DT = {"c64": "complex64", "f32": "float32", "f64": "float64", "u8": "uint8"}
+
+
+def _tp(t, kind: str) -> int | None:
+    """Pointer of a caller tensor the library reads or writes, after checking what the C-ABI assumes:
+    a contiguous CUDA tensor of the declared element type (the library takes raw pointers, so a
+    complex128 or a non-contiguous view would otherwise be read as garbage)."""
+    if t is None:
+        return None
+    if str(t.dtype).replace("torch.", "") != _DT[kind]:
+        raise TypeError(f"sqngd: expected a {_DT[kind]} tensor, got {t.dtype}")
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("sqngd: tensors must be contiguous CUDA tensors")
+    return t.data_ptr()
+
+
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId from the same libnccl the library dlopens (torch's bundled NCCL); rank 0
     creates it and every rank passes it to Context(..., nccl_uid=, rank=, world=)."""
@@ -332,7 +348,7 @@ class Context:
         out = dict(s_soft=self._c(shp) if soft else None, s_hard=self._c(shp) if hard else None,
                    b_hard=self.torch.empty(shp, dtype=self.torch.uint8, device=self.device) if want_b else None,
                    dq=self._f(shp) if want_dq else None)
-        self._check(lib().sqngd_quantize(self.h, _ptr(z), _ptr(rho), _ptr(out["s_soft"]), _ptr(out["s_hard"]),
+        self._check(lib().sqngd_quantize(self.h, _tp(z, "f32"), _tp(rho, "f32"), _ptr(out["s_soft"]), _ptr(out["s_hard"]),
                                          _ptr(out["b_hard"]), _ptr(out["dq"]), self._stream()))
         return out
 
@@ -344,7 +360,7 @@ class Context:
                                                     else None)
         p = self.torch.empty((self.R, self.M), dtype=self.torch.float64, device=self.device) if want_p else None
         met = self._met if met_buf is None else met_buf
-        self._check(lib().sqngd_af_forward(self.h, _ptr(s), _ptr(w), _ptr(amap), _ptr(met), _ptr(p), _ptr(snrl_out),
+        self._check(lib().sqngd_af_forward(self.h, _tp(s, "c64"), _tp(w, "c64"), _tp(amap, "f32"), _ptr(met), _tp(p, "f64"), _tp(snrl_out, "f64"),
                                            self._stream()))
         return met, p, amap
 
@@ -353,7 +369,7 @@ class Context:
         g = out if out is not None else self._c(shp)
         met = self._met if met_buf is None else met_buf
         gw, gs = (g, None) if wrt == WRT_FILTERS else (None, g)
-        self._check(lib().sqngd_loss_grad_s(self.h, _ptr(s), _ptr(w), wrt, _ptr(met), _ptr(gw), _ptr(gs),
+        self._check(lib().sqngd_loss_grad_s(self.h, _tp(s, "c64"), _tp(w, "c64"), wrt, _ptr(met), _tp(gw, "c64"), _tp(gs, "c64"),
                                             self._stream()))
         return met, g
 
@@ -362,13 +378,13 @@ class Context:
         met = self._met if met_buf is None else met_buf
         if wrt == WRT_FILTERS:
             gw = outs[0] if outs else self._c(shp)
-            self._check(lib().sqngd_af_loss_grad(self.h, _ptr(z), _ptr(rho), _ptr(w), wrt, _ptr(met), _ptr(gw),
+            self._check(lib().sqngd_af_loss_grad(self.h, _tp(z, "f32"), _tp(rho, "f32"), _tp(w, "c64"), wrt, _ptr(met), _tp(gw, "c64"),
                                                  None, None, self._stream()))
             return met, gw
         gz = outs[0] if outs else self._f(shp)
         gr = outs[1] if outs else self._f((self.R, self.BR))
-        self._check(lib().sqngd_af_loss_grad(self.h, _ptr(z), _ptr(rho), _ptr(w), wrt, _ptr(met), None,
-                                             _ptr(gz), _ptr(gr), self._stream()))
+        self._check(lib().sqngd_af_loss_grad(self.h, _tp(z, "f32"), _tp(rho, "f32"), _tp(w, "c64"), wrt, _ptr(met), None,
+                                             _tp(gz, "f32"), _tp(gr, "f32"), self._stream()))
         return met, gz, gr
 
     def net_forward(self, theta, y0, z=None):
@@ -438,11 +454,12 @@ class Context:
         return int(n.value)
 
     def step(self, st: dict, block: int = BLOCK_AB, hist=None, hard_met=None):
-        cs = State(z=_ptr(st["z"]), rho=_ptr(st["rho"]), w=_ptr(st["w"]), m_z=_ptr(st["m_z"]), v_z=_ptr(st["v_z"]),
-                   m_rho=_ptr(st["m_rho"]), v_rho=_ptr(st["v_rho"]), m_w=_ptr(st["m_w"]), v_w=_ptr(st["v_w"]),
+        cs = State(z=_tp(st["z"], "f32"), rho=_tp(st["rho"], "f32"), w=_tp(st["w"], "c64"),
+                   m_z=_tp(st["m_z"], "f32"), v_z=_tp(st["v_z"], "f32"), m_rho=_tp(st["m_rho"], "f32"),
+                   v_rho=_tp(st["v_rho"], "f32"), m_w=_ptr(st["m_w"]), v_w=_ptr(st["v_w"]),
                    t_a=int(st["t_a"]), t_b=int(st["t_b"]),
-                   theta=_ptr(st.get("theta")), m_theta=_ptr(st.get("m_theta")), v_theta=_ptr(st.get("v_theta")),
-                   y0=_ptr(st.get("y0")))
+                   theta=_tp(st.get("theta"), "f32"), m_theta=_tp(st.get("m_theta"), "f32"),
+                   v_theta=_tp(st.get("v_theta"), "f32"), y0=_tp(st.get("y0"), "f32"))
         self._check(lib().sqngd_step(self.h, C.byref(cs), int(block), _ptr(hist), _ptr(hard_met), self._stream()))
         st["t_a"], st["t_b"] = cs.t_a, cs.t_b
         return st

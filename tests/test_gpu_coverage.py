@@ -318,7 +318,7 @@ def test_map_pitch(engine, ld):
     c = Cfg("pitch", M=3, N=37, B=4, K=21, f_lo=-0.5, f_hi=0.5, R=2, r_n=3, doppler_engine=ENGINES[engine])
     z = inputs.phase_params(c.R, c.M, c.N, config_index=17)
     rho = inputs.init_thresholds(c.R, c.B, c.r_n)
-    s = O.quantize(c, z, rho)["s_hard"]
+    s = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
     w = (s * np.exp(0.2j * np.sin(0.3 * np.arange(c.N)))).astype(np.complex64)
     L = 2 * c.N - 1
     ctx = sqngd.Context(c)
@@ -329,11 +329,41 @@ def test_map_pitch(engine, ld):
     met_p, _, pitched = cp.af_forward(T(s), T(w), map_out=buf)
     mp = cp.metrics(met_p)
     ctx.sync(); cp.sync()
-    assert torch.equal(pitched[..., :L], dense)
+    # (the dense map comes from the tcgen05 forward, the pitched one from the mma.sync forward: equal
+    # within the engine's rounding, far inside the parity floor)
+    assert (pitched[..., :L] - dense).abs().max().item() <= 1e-6 * c.N
     assert torch.isnan(pitched[..., L:]).all()
-    assert repr(mp) == repr(md)
+    assert abs(mp[0]["loss"] - md[0]["loss"]) <= 1e-6 * abs(md[0]["loss"])
 
 
 def test_map_pitch_rejected_below_2n_minus_1():
     with pytest.raises(Exception):
         sqngd.Context(Cfg("bad_pitch", M=2, N=16, B=4, K=5, f_lo=-0.5, f_hi=0.5, r_n=2, map_ld=20))
+
+
+@pytest.mark.parametrize("mode", ["lse", "pnorm", "max"])
+def test_tcgen05_forward_matches_mma_sync(mode):
+    """The map-writing forward runs on the tcgen05 kernel (k_lrf, lr_tc.cuh) and the metrics-only forward on
+    the mma.sync kernel (k_lrt): same cells within 1e-6 N, same keys / argmax, and the metrics of both calls
+    agree; both against the oracle map."""
+    lm, bp = MODES[mode]
+    c = Cfg("tcf", M=3, N=37, B=8, K=21, f_lo=-0.5, f_hi=0.5, R=2, r_n=3, loss_mode=lm, beta_or_p=bp,
+            doppler_engine=ENGINES["cheb"])
+    z = inputs.phase_params(c.R, c.M, c.N, config_index=29)
+    rho = inputs.init_thresholds(c.R, c.B, c.r_n)
+    s = O.quantize(c, z, rho)["s_hard"].astype(np.complex64)
+    w = (s * np.exp(0.25j * np.sin(0.2 * np.arange(c.N)))).astype(np.complex64)
+    ctx = sqngd.Context(c)
+    met, _, amap = ctx.af_forward(T(s), T(w), want_map=True)
+    m_map = ctx.metrics(met)
+    met2, _, _ = ctx.af_forward(T(s), T(w))
+    m_nomap = ctx.metrics(met2)
+    ctx.sync()
+    ref, _, refmap = O.af(c, s, w, want_A=True)
+    check_map(amap.cpu().numpy(), np.abs(refmap), c.N, what="tcgen05 forward map")
+    for r in range(c.R):
+        assert m_map[r]["argmax_auto"] == m_nomap[r]["argmax_auto"]
+        assert m_map[r]["argmax_cross"] == m_nomap[r]["argmax_cross"]
+        check_loss(m_map[r]["loss"], ref[r]["loss"], "tcgen05 forward loss")
+        check_db(m_map[r]["wpsl"], ref[r]["wpsl"], "tcgen05 forward wpsl")
+        assert abs(m_map[r]["loss"] - m_nomap[r]["loss"]) <= 1e-6 * abs(m_nomap[r]["loss"])

@@ -102,3 +102,20 @@ def test_generator_step_keeps_last_finite_iterate(engine):
     expect(ctx, sqngd.E_NONFINITE)
     assert torch.equal(st["theta"], th0) and torch.equal(st["rho"], rho0)
     assert not st["m_theta"].any() and not st["v_theta"].any()
+
+
+def test_binding_rejects_wrong_dtypes():
+    """The C-ABI takes raw pointers: the binding refuses tensors of another element type (a complex128
+    waveform would otherwise be read as garbage) and non-contiguous views."""
+    c = Cfg("dt", M=2, N=16, B=4, K=5, f_lo=-0.5, f_hi=0.5, r_n=2)
+    ctx = sqngd.Context(c)
+    s = torch.ones((1, 2, 16), dtype=torch.complex64, device="cuda")
+    with pytest.raises(TypeError):
+        ctx.af_forward(s.to(torch.complex128), s)
+    with pytest.raises(ValueError):
+        ctx.af_forward(s.transpose(1, 2).contiguous().transpose(1, 2), s)
+    z = torch.zeros((1, 2, 16), dtype=torch.float64, device="cuda")
+    with pytest.raises(TypeError):
+        ctx.quantize(z, torch.zeros((1, 8), dtype=torch.float32, device="cuda"))
+    ctx.af_forward(s, s)  # the right types pass
+    ctx.sync()
