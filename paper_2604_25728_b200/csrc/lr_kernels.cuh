@@ -204,6 +204,10 @@ __device__ __forceinline__ void split4(const float (&x)[4], uint32_t (&h)[4], ui
   for (int i = 0; i < 4; ++i) tf32_split(x[i], h[i], l[i]);
 }
 
+// split4 with the A-fragment reorder of k_lrt's adjoint (x in D order: (g,2c) (g,2c+1) (g+8,2c) (g+8,2c+1);
+// h, l in A order (g,c) (g+8,c) (g,c+4) (g+8,c+4)), the two subtractions per pair packed.
+__device__ __forceinline__ void split4_pk(const float (&x)[4], uint32_t (&h)[4], uint32_t (&l)[4]);
+
 // Forward contraction in FP16 with the 3-term split packed along K (m16n8k16, one MMA per
 // product): the 15 used K columns hold hi(x_j), lo(x_j), hi(x_j) against hi(c_j), hi(c_j),
 // lo(c_j) (j < 5; layout in k_lrt), so A.B = x_hi c_hi + x_lo c_hi + x_hi c_lo.
@@ -235,6 +239,62 @@ __device__ __forceinline__ uint32_t f16_pair(int k, const float (&x)[5]) {
   return (uint32_t)f16_col(k, x) | ((uint32_t)f16_col(k + 1, x) << 16);
 }
 
+// Packed FP32 pairs (PTX .f32x2, sm_100a FADD2 / FMUL2 / FFMA2): one issue slot for the same
+// operation on two lanes' values.  Measured on B200 (tools/ubench_ffma2.cu): FFMA2 runs at the FP32
+// pipe's lane rate (127 lane-FMA/clk/SM, as scalar FFMA), so it does not raise the FP32 peak; it
+// halves the issue slots of the FP32 work, which is what bounds the k_lrt epilogue (issue-bound,
+// DESIGN.md §6).  Each lane is an IEEE fp32 operation with round-to-nearest, as the scalar op.
+#ifndef SQNGD_LRT_PACKED
+#define SQNGD_LRT_PACKED 1
+#endif
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float a;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(a) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float b;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+__device__ __forceinline__ void split4_pk(const float (&x)[4], uint32_t (&h)[4], uint32_t (&l)[4]) {
+  // x in D order; the fragment quads h, l pair (x0, x2) and (x1, x3), so the subtractions pack over those
+  const f32x2 v02 = pk2(x[0], x[2]), v13 = pk2(x[1], x[3]);
+  const f32x2 t02 = pk2(__uint_as_float(__float_as_uint(x[0]) & 0xFFFFE000u), __uint_as_float(__float_as_uint(x[2]) & 0xFFFFE000u));
+  const f32x2 t13 = pk2(__uint_as_float(__float_as_uint(x[1]) & 0xFFFFE000u), __uint_as_float(__float_as_uint(x[3]) & 0xFFFFE000u));
+  const f32x2 d02 = sub2(v02, t02), d13 = sub2(v13, t13);
+  h[0] = __float_as_uint(x[0]); h[1] = __float_as_uint(x[2]); h[2] = __float_as_uint(x[1]); h[3] = __float_as_uint(x[3]);
+  l[0] = __float_as_uint(lo2(d02)); l[1] = __float_as_uint(hi2(d02));
+  l[2] = __float_as_uint(lo2(d13)); l[3] = __float_as_uint(hi2(d13));
+}
+
 #ifndef SQNGD_LRT_UNROLL
 #define SQNGD_LRT_UNROLL 1
 #endif
@@ -254,6 +314,7 @@ template <int Q, int LM, bool HW, int KM>
 __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const LrtArgs a) {
   SQ_PDL_WAIT();
   constexpr bool GRAD = KM == 1, MAP = KM == 2;
+  constexpr bool PK = SQNGD_LRT_PACKED && !HW && !MAP;  // packed-FP32 epilogue for the full tiles
   constexpr int QH = Q / 2;
   constexpr int NR = 6 + (GRAD ? 16 : 0);  // per-lane record: key(2), shift(2), S(2), GE/GO(16)
   extern __shared__ float4 lr_smem[];
@@ -407,6 +468,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) GEr[i] = GEi[i] = GOr[i] = GOi[i] = 0.f;
+    f32x2 S2[2] = {0ull, 0ull};  // packed-path sums (two cells per lane of the pair), folded into S below
     float lbN[2], nlbs[2], qN[2];  // per lag: the prescale's 1/sigma folded into the magnitude terms
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -446,6 +508,65 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         mma3(Poi, aOih, aOil, fb);
       }
       float SGr[4], SGi[4], DGr[4], DGi[4];
+      if constexpr (PK && !MASKED) {
+        // The same cells as the scalar loop below, two at a time: the D elements (2h, 2h + 1) of lag row h
+        // (bins p, p + 1 and K-1-p, K-2-p) form packed pairs; MUFU and the argmax keys stay per cell.
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e0 = 2 * h;
+          const int p = 8 * t + 2 * cq;
+          const f32x2 per = pk2(Per[e0], Per[e0 + 1]), por = pk2(Por[e0], Por[e0 + 1]);
+          const f32x2 pei = pk2(Pei[e0], Pei[e0 + 1]), poi = pk2(Poi[e0], Poi[e0 + 1]);
+          const f32x2 x0 = add2(per, por), y0 = add2(pei, poi);  // A0: bins p, p + 1
+          const f32x2 x1 = sub2(per, por), y1 = sub2(pei, poi);  // A1: bins K-1-p, K-2-p
+          const f32x2 eps = pk2(1e-30f, 1e-30f);
+          const f32x2 q0 = fma2(x0, x0, fma2(y0, y0, eps)), q1 = fma2(x1, x1, fma2(y1, y1, eps));
+          // keys in the scalar loop's cell order (ties: the lowest bin, as lr_cell's > / >= rules)
+          {
+            const float c0 = lo2(q0), c1 = lo2(q1), c2 = hi2(q0), c3 = hi2(q1);
+            bool u = c0 > bl[h]; bl[h] = u ? c0 : bl[h]; kl[h] = u ? p : kl[h];
+            u = c1 >= bh[h]; bh[h] = u ? c1 : bh[h]; kh[h] = u ? a.K - 1 - p : kh[h];
+            u = c2 > bl[h]; bl[h] = u ? c2 : bl[h]; kl[h] = u ? p + 1 : kl[h];
+            u = c3 >= bh[h]; bh[h] = u ? c3 : bh[h]; kh[h] = u ? a.K - 2 - p : kh[h];
+          }
+          if constexpr (LM != 0) {
+            const f32x2 r0 = pk2(rsqa(lo2(q0)), rsqa(hi2(q0))), r1 = pk2(rsqa(lo2(q1)), rsqa(hi2(q1)));
+            const f32x2 m0 = mul2(q0, r0), m1 = mul2(q1, r1);  // |A|
+            f32x2 g0, g1, ph0, ph1;                             // gphi, phi
+            if constexpr (LM == 1) {
+              const f32x2 lbv = pk2(lbN[h], lbN[h]), nlv = pk2(nlbs[h], nlbs[h]);
+              const f32x2 z0 = fma2(lbv, m0, nlv), z1 = fma2(lbv, m1, nlv);
+              g0 = pk2(ex2a(lo2(z0)), ex2a(hi2(z0)));
+              g1 = pk2(ex2a(lo2(z1)), ex2a(hi2(z1)));
+              ph0 = g0; ph1 = g1;
+            } else {
+              const f32x2 qv = pk2(qN[h], qN[h]), bm = pk2(a.bp - 1.f, a.bp - 1.f);
+              const f32x2 w0 = mul2(m0, qv), w1 = mul2(m1, qv);
+              const f32x2 l0 = mul2(bm, pk2(lg2a(lo2(w0)), lg2a(hi2(w0))));
+              const f32x2 l1 = mul2(bm, pk2(lg2a(lo2(w1)), lg2a(hi2(w1))));
+              g0 = pk2(ex2a(lo2(l0)), ex2a(hi2(l0)));
+              g1 = pk2(ex2a(lo2(l1)), ex2a(hi2(l1)));
+              ph0 = mul2(g0, w0); ph1 = mul2(g1, w1);
+            }
+            S2[h] = add2(S2[h], add2(ph0, ph1));
+            if constexpr (GRAD) {
+              // SG = gf0 A0 + gf1 A1, DG = gf0 A0 - gf1 A1 (gf = gphi / |A|) per element, on the scalar
+              // pipe: the adjoint's A fragments pair the elements (2h, 2h + 2), not this (2h, 2h + 1), and
+              // scalar results are placed in fragment order for free, packed ones would need moves
+              const f32x2 f0 = mul2(g0, r0), f1 = mul2(g1, r1);
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const float gf0 = i ? hi2(f0) : lo2(f0), gf1 = i ? hi2(f1) : lo2(f1);
+                const float a0x = i ? hi2(x0) : lo2(x0), a0y = i ? hi2(y0) : lo2(y0);
+                const float a1x = i ? hi2(x1) : lo2(x1), a1y = i ? hi2(y1) : lo2(y1);
+                const float tr = gf0 * a0x, ti = gf0 * a0y;
+                SGr[e0 + i] = fmaf(gf1, a1x, tr); SGi[e0 + i] = fmaf(gf1, a1y, ti);
+                DGr[e0 + i] = fmaf(-gf1, a1x, tr); DGi[e0 + i] = fmaf(-gf1, a1y, ti);
+              }
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {  // D element e: row h = e >> 1, pair p = 8t + 2c + (e & 1)
         const int h = e >> 1;
@@ -483,7 +604,14 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
           SGr[e] = SGi[e] = DGr[e] = DGi[e] = 0.f;
         }
       }
-      if (GRAD) {
+      }
+      if (GRAD && PK && !MASKED) {  // the same split, its subtractions packed
+        uint32_t hh[4], ll[4];
+        split4_pk(SGr, hh, ll); mma3(GEr, hh, ll, ga);
+        split4_pk(SGi, hh, ll); mma3(GEi, hh, ll, ga);
+        split4_pk(DGr, hh, ll); mma3(GOr, hh, ll, gb);
+        split4_pk(DGi, hh, ll); mma3(GOi, hh, ll, gb);
+      } else if (GRAD) {
         // D order (g,2c) (g,2c+1) (g+8,2c) (g+8,2c+1) -> A order (g,c) (g+8,c) (g,c+4) (g+8,c+4)
         const float sr[4] = {SGr[0], SGr[2], SGr[1], SGr[3]}, si[4] = {SGi[0], SGi[2], SGi[1], SGi[3]};
         const float dr[4] = {DGr[0], DGr[2], DGr[1], DGr[3]}, di[4] = {DGi[0], DGi[2], DGi[1], DGi[3]};
@@ -509,6 +637,10 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
         tile(t, std::integral_constant<bool, false>{}, fa, fb, ga, gb);
         if (t + 1 < tf_end) ldB(t + 1, nfa, nfb, nga, ngb);
       }
+    }
+    if constexpr (PK && LM != 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) S[h] += lo2(S2[h]) + hi2(S2[h]);
     }
     if (t1 > a.NTF && t0 <= a.NTF) {
       float4 fa, fb, ga = make_float4(0.f, 0.f, 0.f, 0.f), gb = ga;
