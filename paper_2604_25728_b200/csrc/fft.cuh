@@ -37,13 +37,75 @@ __device__ __forceinline__ void static_for(Fn&& fn) {
   }
 }
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Packed FP32 pairs (PTX .f32x2, sm_100a FADD2 / FMUL2 / FFMA2): one issue slot for the same
+// operation on two lanes' values.  Measured on B200 (tools/ubench_ffma2.cu): FFMA2 runs at the FP32
+// pipe's lane rate (127 lane-FMA/clk/SM, as scalar FFMA), so it does not raise the FP32 peak; it
+// halves the issue slots of the FP32 work (the k_lrt epilogue and the FFT kernels are issue-bound,
+// DESIGN.md §6).  Each lane is an IEEE fp32 operation with round-to-nearest, as the scalar op.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float a;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(a) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float b;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+#ifndef SQNGD_CPACKED
+#define SQNGD_CPACKED 1
+#endif
+__device__ __forceinline__ f32x2 f2p(float2 a) { return pk2(a.x, a.y); }
+__device__ __forceinline__ float2 p2f(f32x2 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// Complex arithmetic on (re, im) pairs.  Packed: an add is one FADD2; a product is one FMUL2 and one FFMA2
+//   a b = (a.x, a.y) b.x + (-a.y, a.x) b.y,   a conj(b) = (a.x, a.y) b.x + (a.y, -a.x) b.y
+// (ptxas folds the swap, the one-sided negation and the broadcasts of b.x / b.y into operand modifiers).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  if (SQNGD_CPACKED) return p2f(add2(f2p(a), f2p(b)));
+  return make_float2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  if (SQNGD_CPACKED) return p2f(sub2(f2p(a), f2p(b)));
+  return make_float2(a.x - b.x, a.y - b.y);
+}
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  if (SQNGD_CPACKED) return p2f(fma2(pk2(-a.y, a.x), pk2(b.y, b.y), mul2(f2p(a), pk2(b.x, b.x))));
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 // a * conj(b)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  if (SQNGD_CPACKED) return p2f(fma2(pk2(a.y, -a.x), pk2(b.y, b.y), mul2(f2p(a), pk2(b.x, b.x))));
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
 
@@ -98,6 +160,7 @@ __device__ __forceinline__ float2 twc(float2 x) {
   } else {
     constexpr float c = (float)cos64(q);
     constexpr float s = (float)(DIR * sin64(q));
+    if (SQNGD_CPACKED) return cmul(x, make_float2(c, s));
     return make_float2(fmaf(x.x, c, -x.y * s), fmaf(x.x, s, x.y * c));
   }
 }

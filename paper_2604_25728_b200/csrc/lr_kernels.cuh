@@ -239,50 +239,9 @@ __device__ __forceinline__ uint32_t f16_pair(int k, const float (&x)[5]) {
   return (uint32_t)f16_col(k, x) | ((uint32_t)f16_col(k + 1, x) << 16);
 }
 
-// Packed FP32 pairs (PTX .f32x2, sm_100a FADD2 / FMUL2 / FFMA2): one issue slot for the same
-// operation on two lanes' values.  Measured on B200 (tools/ubench_ffma2.cu): FFMA2 runs at the FP32
-// pipe's lane rate (127 lane-FMA/clk/SM, as scalar FFMA), so it does not raise the FP32 peak; it
-// halves the issue slots of the FP32 work, which is what bounds the k_lrt epilogue (issue-bound,
-// DESIGN.md §6).  Each lane is an IEEE fp32 operation with round-to-nearest, as the scalar op.
 #ifndef SQNGD_LRT_PACKED
 #define SQNGD_LRT_PACKED 1
 #endif
-typedef unsigned long long f32x2;
-__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float lo2(f32x2 v) {
-  float a;
-  asm("mov.b64 {%0, _}, %1;" : "=f"(a) : "l"(v));
-  return a;
-}
-__device__ __forceinline__ float hi2(f32x2 v) {
-  float b;
-  asm("mov.b64 {_, %0}, %1;" : "=f"(b) : "l"(v));
-  return b;
-}
-__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
 
 __device__ __forceinline__ void split4_pk(const float (&x)[4], uint32_t (&h)[4], uint32_t (&l)[4]) {
   // x in D order; the fragment quads h, l pair (x0, x2) and (x1, x3), so the subtractions pack over those

@@ -5,6 +5,6 @@ for v in "" $AB_VARIANTS "" $AB_VARIANTS; do
   python - "${v:-default}" <<'PY'
 import json,sys
 d=json.loads(open('gpurun_out/bench_ab.log').read().strip().splitlines()[-1])
-print(f"{sys.argv[1]:12s} value {d['value']:.0f} ms/step {d['ms_per_step']:.4f} k_lrt {d['roofline']['avg_launch_ms']*1e3:.1f} us  A {d['breakdown']['step_A_evals_per_s']:.0f} B {d['breakdown']['step_B_evals_per_s']:.0f} fwd_nomap {d['forward']['fused_launch_ms_no_map']*1e3:.1f} us")
+print(f"{sys.argv[1]:12s} value {d['value']:.0f} ms/step {d['ms_per_step']:.4f} k_lrt {d['roofline']['avg_launch_ms']*1e3:.1f} us  A {d['breakdown']['step_A_evals_per_s']:.0f} B {d['breakdown']['step_B_evals_per_s']:.0f} fwd_nomap {d['forward']['fused_launch_ms_no_map']*1e3:.1f} us fft {d.get('fft_engine',{}).get('value',0):.0f}")
 PY
 done
