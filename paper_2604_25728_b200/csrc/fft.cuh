@@ -91,23 +91,31 @@ __device__ __forceinline__ float2 p2f(f32x2 v) {
 // Complex arithmetic on (re, im) pairs.  Packed: an add is one FADD2; a product is one FMUL2 and one FFMA2
 //   a b = (a.x, a.y) b.x + (-a.y, a.x) b.y,   a conj(b) = (a.x, a.y) b.x + (a.y, -a.x) b.y
 // (ptxas folds the swap, the one-sided negation and the broadcasts of b.x / b.y into operand modifiers).
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
-  if (SQNGD_CPACKED) return p2f(add2(f2p(a), f2p(b)));
+template <bool PK>
+__device__ __forceinline__ float2 cadd_p(float2 a, float2 b) {
+  if (PK) return p2f(add2(f2p(a), f2p(b)));
   return make_float2(a.x + b.x, a.y + b.y);
 }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) {
-  if (SQNGD_CPACKED) return p2f(sub2(f2p(a), f2p(b)));
+template <bool PK>
+__device__ __forceinline__ float2 csub_p(float2 a, float2 b) {
+  if (PK) return p2f(sub2(f2p(a), f2p(b)));
   return make_float2(a.x - b.x, a.y - b.y);
 }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  if (SQNGD_CPACKED) return p2f(fma2(pk2(-a.y, a.x), pk2(b.y, b.y), mul2(f2p(a), pk2(b.x, b.x))));
+template <bool PK>
+__device__ __forceinline__ float2 cmul_p(float2 a, float2 b) {
+  if (PK) return p2f(fma2(pk2(-a.y, a.x), pk2(b.y, b.y), mul2(f2p(a), pk2(b.x, b.x))));
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 // a * conj(b)
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
-  if (SQNGD_CPACKED) return p2f(fma2(pk2(a.y, -a.x), pk2(b.y, b.y), mul2(f2p(a), pk2(b.x, b.x))));
+template <bool PK>
+__device__ __forceinline__ float2 cmulc_p(float2 a, float2 b) {
+  if (PK) return p2f(fma2(pk2(a.y, -a.x), pk2(b.y, b.y), mul2(f2p(a), pk2(b.x, b.x))));
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return cadd_p<SQNGD_CPACKED>(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return csub_p<SQNGD_CPACKED>(a, b); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return cmul_p<SQNGD_CPACKED>(a, b); }
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) { return cmulc_p<SQNGD_CPACKED>(a, b); }
 
 // cos(2 pi i / 64), i = 0..16, to full float precision (first quadrant).
 __host__ __device__ constexpr double kCos64(int i) {
@@ -138,7 +146,7 @@ __host__ __device__ constexpr double cos64(int k) {
 __host__ __device__ constexpr double sin64(int k) { return cos64(k - 16); }
 
 // x * W_R^{DIR*k}, W_R = e^{2 pi i / R}; DIR = -1 forward transform.
-template <int R, int DIR, int k>
+template <int R, int DIR, int k, bool PK = SQNGD_CPACKED>
 __device__ __forceinline__ float2 twc(float2 x) {
   constexpr int kk = ((k % R) + R) % R;
   constexpr int q = kk * (64 / R);  // angle in units of 2 pi / 64
@@ -160,21 +168,21 @@ __device__ __forceinline__ float2 twc(float2 x) {
   } else {
     constexpr float c = (float)cos64(q);
     constexpr float s = (float)(DIR * sin64(q));
-    if (SQNGD_CPACKED) return cmul(x, make_float2(c, s));
+    if (PK) return cmul_p<true>(x, make_float2(c, s));
     return make_float2(fmaf(x.x, c, -x.y * s), fmaf(x.x, s, x.y * c));
   }
 }
 
 // R-point DFT in registers (natural order in and out), radix-2 decimation in time.
 // DIR = -1: X[q] = sum_n x[n] e^{-2 pi i q n / R};  DIR = +1: unnormalized inverse.
-template <int R, int DIR>
+template <int R, int DIR, bool PK = SQNGD_CPACKED>
 __device__ __forceinline__ void dft(float2* v) {
   if constexpr (R == 1) {
     return;
   } else if constexpr (R == 2) {
     float2 a = v[0], b = v[1];
-    v[0] = cadd(a, b);
-    v[1] = csub(a, b);
+    v[0] = cadd_p<PK>(a, b);
+    v[1] = csub_p<PK>(a, b);
   } else {
     float2 ev[R / 2], od[R / 2];
 #pragma unroll
@@ -182,13 +190,13 @@ __device__ __forceinline__ void dft(float2* v) {
       ev[i] = v[2 * i];
       od[i] = v[2 * i + 1];
     }
-    dft<R / 2, DIR>(ev);
-    dft<R / 2, DIR>(od);
+    dft<R / 2, DIR, PK>(ev);
+    dft<R / 2, DIR, PK>(od);
     static_for<0, R / 2>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
-      float2 t = twc<R, DIR, k>(od[k]);
-      v[k] = cadd(ev[k], t);
-      v[k + R / 2] = csub(ev[k], t);
+      float2 t = twc<R, DIR, k, PK>(od[k]);
+      v[k] = cadd_p<PK>(ev[k], t);
+      v[k + R / 2] = csub_p<PK>(ev[k], t);
     });
   }
 }
@@ -247,7 +255,8 @@ struct GroupSync {
 // smem; tw: the plan's twiddle table (global, read through L1).
 // par: exchange parity (alternates the two buffers); must start equal in all threads.
 // TWS: the twiddle table `tw` is in shared memory (plain loads) instead of global (__ldg).
-template <class PL, int DIR, bool TWS = false>
+// PK: complex arithmetic on packed FP32 pairs (fewer issue slots, more registers: per kernel, measured).
+template <class PL, int DIR, bool TWS = false, bool PK = SQNGD_CPACKED>
 __device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2* __restrict__ tw, float2* sbuf, int t,
                                     int& par, const GroupSync& sync) {
   constexpr int E = PL::E, T = PL::T;
@@ -266,10 +275,10 @@ __device__ __forceinline__ void fft(float2 (&v)[PL::E], const float2* __restrict
 #pragma unroll
         for (int r = 1; r < R; ++r) {
           const float2 w = TWS ? twp[(r - 1) * Ns] : __ldg(twp + (r - 1) * Ns);
-          x[r] = DIR < 0 ? cmul(x[r], w) : cmulc(x[r], w);
+          x[r] = DIR < 0 ? cmul_p<PK>(x[r], w) : cmulc_p<PK>(x[r], w);
         }
       }
-      dft<R, DIR>(x);
+      dft<R, DIR, PK>(x);
       if constexpr (p == PL::NP - 1) {
 #pragma unroll
         for (int r = 0; r < R; ++r) v[b + r * NB] = x[r];

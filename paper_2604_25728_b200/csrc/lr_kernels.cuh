@@ -31,6 +31,9 @@
 #include "af_kernels.cuh"
 #include "common.cuh"
 
+#ifndef SQNGD_NODE_PK  // k_node's transforms: scalar complex arithmetic (packed: 110 vs 85 registers, slower)
+#define SQNGD_NODE_PK 0
+#endif
 #ifndef SQNGD_LRT_PREFETCH
 #define SQNGD_LRT_PREFETCH 0
 #endif
@@ -70,7 +73,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
 #pragma unroll
   for (int i = 0; i < E; ++i) v[i] = cmulc(__ldg(Hl + t + i * T), __ldg(X + t + i * T));  // conj(X conj(H))
   int par = 0;
-  fft<PL, -1>(v, ftw, xbuf, t, par, sync);  // v = conj(r)
+  fft<PL, -1, false, SQNGD_NODE_PK>(v, ftw, xbuf, t, par, sync);  // v = conj(r)
   if (u >= units) return;
   float2* out = Rn + (size_t)uu * LS + (N - 1);
 #pragma unroll

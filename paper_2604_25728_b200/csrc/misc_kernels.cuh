@@ -585,6 +585,94 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
 //   per (r, threshold block): grad_rho[i] = coef * sum_ch part[ch][i]  (when gsum != nullptr);
 //   per (r, element chunk):   Adam on the chunk's z (when zad.z != nullptr) -- after every
 //                             threshold block has read that chunk's old z.
+// Adam on z (direct parameterization), by the blocks 1.. of k_adam_project_rho (after k_grad_rho read z).
+struct ZAdam {
+  float *z, *mz, *vz;  // z == nullptr: none (generator mode)
+  const float* gz;     // grad_z [R][MN]
+  int MN;
+  AdamP ap;
+};
+
+// dL/drho_i = coef sum_n sech^2(c (z_n - rho_i)) dy_n over the window |c (z_n - rho_i)| < 12 (the chain of
+// Eq. 25 through Q_A, the same terms as k_grad_rho_part), in one pass without sorting.  Block = TB
+// consecutive thresholds x TPT lanes each (rho ascending, so their union window is one z interval).  Per
+// chunk of CH elements the block compacts, in a fixed order (thread, then element), the (z, dy) whose z lies
+// in the union window (block-wide exclusive scan of the per-thread counts), and lane `sub` of a threshold
+// sums every TPT-th compacted element; the TPT lanes combine by a fixed xor tree.  Deterministic.
+template <int TB>
+__global__ void __launch_bounds__(256) k_grad_rho(int MN, int BR, float c, float coef, const float* __restrict__ z,
+                                                  const float* __restrict__ rho, const float* __restrict__ dy,
+                                                  float* __restrict__ gsum) {
+  SQ_PDL_WAIT();
+  constexpr int TPT = 256 / TB, EPT = 16, CH = 256 * EPT;
+  static_assert(TPT >= 1 && (TPT & (TPT - 1)) == 0 && TPT <= 32, "TPT lanes per threshold, within a warp");
+  __shared__ float2 buf[CH];
+  __shared__ int wsum[8];
+  const int r = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int i0 = blockIdx.x * TB;
+  const int i = min(i0 + t / TPT, BR - 1);
+  const int sub = t % TPT;
+  const float* rr = rho + (size_t)r * BR;
+  const float ri = __ldg(rr + i);
+  const float W = 12.f / c;
+  const float zlo = __ldg(rr + i0) - W, zhi = __ldg(rr + min(i0 + TB, BR) - 1) + W;
+  const float* zr = z + (size_t)r * MN;
+  const float* dr = dy + (size_t)r * MN;
+  const float k2 = -2.f * 1.4426950408889634f;
+  float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int base = 0; base < MN; base += CH) {
+    float zv[EPT];
+    unsigned inm = 0u;
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int e = base + k * 256 + t;
+      zv[k] = e < MN ? __ldg(zr + e) : 0.f;
+      const bool in = e < MN && zv[k] >= zlo && zv[k] <= zhi;
+      inm |= in ? (1u << k) : 0u;
+      cnt += in ? 1 : 0;
+    }
+    // block-wide exclusive scan of cnt
+    int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    int off = x - cnt, n = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int v = wsum[w];
+      off += w < wid ? v : 0;
+      n += v;
+    }
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (inm & (1u << k)) buf[off++] = make_float2(zv[k], __ldg(dr + base + k * 256 + t));
+    __syncthreads();
+    // four independent partial sums per lane (element e + j TPT, j < 4, of each group of 4 TPT)
+    for (int e = sub; e < n; e += 4 * TPT) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ej = e + j * TPT;
+        const float2 p = ej < n ? buf[ej] : make_float2(ri + 2.f * W, 0.f);
+        const float au = c * fabsf(p.x - ri);
+        const float e2 = ex2a_m(k2 * au);
+        const float inv = rcp_m(1.f + e2);
+        const float sech2 = 4.f * e2 * inv * inv;
+        acc4[j] = fmaf(au < 12.f ? sech2 : 0.f, p.y, acc4[j]);
+      }
+    }
+    __syncthreads();  // (buf and wsum are rewritten by the next chunk)
+  }
+  float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+#pragma unroll
+  for (int o = 1; o < TPT; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (sub == 0 && i0 + t / TPT < BR) gsum[(size_t)r * BR + i0 + t / TPT] = coef * acc;
+}
+
 struct RhoFinish {
   float coef;
   float* gsum;      // [R][BR] or nullptr
@@ -957,12 +1045,37 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
 }
 
 // Step-B threshold update, one block per restart (when not fused into k_grad_rho_part).
-__global__ void k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
-                                   float lo, float hi, float gap, const int* status) {
+__global__ void __launch_bounds__(1024) k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
+                                   float lo, float hi, float gap, const int* status, ZAdam za) {
   SQ_PDL_WAIT();
   extern __shared__ float sr[];
   if (*status & ST_NONFINITE) return;  // keep the last finite iterate
-  adam_project_rho_dev(blockIdx.x, BR, rho, mr, vr, g + (size_t)blockIdx.x * BR, ap, lo, hi, gap, sr);
+  if (blockIdx.x > 0) {  // Adam(z): 4 elements per thread of chunk blockIdx.x - 1 (grid (1 + chunks, R))
+    float c1, c2;
+    za.ap.corr(c1, c2);
+    const int r = blockIdx.y;
+    float gv[4], mv[4], vv[4], zv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = (blockIdx.x - 1) * 4 * blockDim.x + k * blockDim.x + threadIdx.x;
+      const size_t j = (size_t)r * za.MN + (e < za.MN ? e : 0);
+      gv[k] = za.gz[j]; mv[k] = za.mz[j]; vv[k] = za.vz[j]; zv[k] = za.z[j];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = (blockIdx.x - 1) * 4 * blockDim.x + k * blockDim.x + threadIdx.x;
+      if (e < za.MN) {
+        const size_t j = (size_t)r * za.MN + e;
+        const float mi = za.ap.b1 * mv[k] + (1.f - za.ap.b1) * gv[k];
+        const float vi = za.ap.b2 * vv[k] + (1.f - za.ap.b2) * gv[k] * gv[k];
+        za.mz[j] = mi;
+        za.vz[j] = vi;
+        za.z[j] = zv[k] - za.ap.lr * (mi / c1) / (sqrtf(vi / c2) + za.ap.eps);
+      }
+    }
+    return;
+  }
+  adam_project_rho_dev(blockIdx.y, BR, rho, mr, vr, g + (size_t)blockIdx.y * BR, ap, lo, hi, gap, sr);
 }
 
 // a6 reporting: SNRL_m = 10 log10(||s_m||^2 ||w_m||^2 / |s_m^H w_m|^2) (Eq. 10) from

@@ -41,6 +41,7 @@ thread_local std::string g_last_error;
 #ifndef SQNGD_MINB128
 #define SQNGD_MINB128 3
 #endif
+constexpr int kRhoTB = 16;  // k_grad_rho: thresholds per block (16 lanes each)
 constexpr int plan_E(int P) { return P <= SQNGD_E ? P : SQNGD_E; }
 constexpr int plan_G(int P) { return (P / plan_E(P)) >= 128 ? 1 : 128 / (P / plan_E(P)); }
 constexpr int plan_MINB(int P) {
@@ -106,6 +107,7 @@ struct sqngd_ctx_s {
   float* dy = nullptr;         // [R][M][N]
   float* rho_part = nullptr;   // [R][nchunk][BR]
   int rho_chunk = 256, rho_nchunk = 1;
+  bool rho_onepass = true;     // k_grad_rho (one pass, no sort); SQNGD_RHO_ONEPASS=0: k_grad_rho_part
   // Adam(rho) + projection: a 1024-thread kernel.  As the optimization proceeds the thresholds form
   // clusters that Adam reorders every step, so the projection's sort runs every step.
   int* rho_cnt = nullptr;      // [R][64] threshold-block + [R][nchunk] element-chunk arrival counters
@@ -761,6 +763,7 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
   CK(ctx->dmalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
+  if (const char* e = getenv("SQNGD_RHO_ONEPASS")) ctx->rho_onepass = e[0] != '0';
   CK(ctx->dmalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   CK(ctx->dmalloc(&ctx->s_soft, sizeof(float2) * RMN));
   CK(ctx->dmalloc(&ctx->s_hard, sizeof(float2) * RMN));
@@ -1500,11 +1503,16 @@ static sqngd_status run_snrl(sqngd_ctx ctx, const float2* s, const float2* w, do
 static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho, float* grad_rho, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   const int MN = c.M * c.N;
-  dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
-  RhoFinish fin{};
-  fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
-  fin.gsum = grad_rho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64; fin.status = ctx->status;
-  k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
+  if (ctx->rho_onepass) {
+    k_grad_rho<kRhoTB><<<dim3((ctx->BR + kRhoTB - 1) / kRhoTB, c.R), 256, 0, st>>>(
+        MN, ctx->BR, (float)c.c, (float)(-(1.0 / (2.0 * c.B)) * c.c), z, rho, ctx->dy, grad_rho);
+  } else {
+    dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
+    RhoFinish fin{};
+    fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
+    fin.gsum = grad_rho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64; fin.status = ctx->status;
+    k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
+  }
   ctx->launches += 1;
   return launch_check(ctx, "grad rho");
 }
@@ -1677,7 +1685,19 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
                         ap(c.lr_theta, 1, i), ctx->status, ctx->side_net, &ctx->launches));
         CK(cudaEventRecord(ctx->ev_nj, ctx->side_net));
       }
-      {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
+      ZAdam za{};
+      if (ctx->rho_onepass && !ctx->net) {  // one-pass dL/drho, then Adam(z) and Adam(rho) + projection
+        za.z = stt->z; za.mz = stt->m_z; za.vz = stt->v_z; za.gz = ctx->gz; za.MN = c.M * c.N; za.ap = ap(c.lr_z, 1, i);
+      }
+      if (ctx->rho_onepass) {
+        k_grad_rho<kRhoTB><<<dim3((ctx->BR + kRhoTB - 1) / kRhoTB, c.R), 256, 0, st>>>(
+            c.M * c.N, ctx->BR, (float)c.c, (float)(-(1.0 / (2.0 * c.B)) * c.c), stt->z, stt->rho, ctx->dy, ctx->grho);
+        const int zch = za.z ? (c.M * c.N + 4095) / 4096 : 0;
+        k_adam_project_rho<<<dim3(1 + zch, c.R), 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
+                                                                      ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
+                                                                      1.0f - 1e-4f, 1e-6f, ctx->status, za);
+        ctx->launches += 2;
+      } else {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
         dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);
         RhoFinish fin{};  // grad_rho sums, Adam(z) and Adam(rho) + projection by last-arriving blocks
         fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
@@ -1688,9 +1708,9 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
         fin.status = ctx->status;
         k_grad_rho_part<<<g1, 256, 0, st>>>(c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy,
                                             ctx->rho_part, fin);
-        k_adam_project_rho<<<c.R, 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
+        k_adam_project_rho<<<dim3(1, c.R), 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
                                                                       ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
-                                                                      1.0f - 1e-4f, 1e-6f, ctx->status);
+                                                                      1.0f - 1e-4f, 1e-6f, ctx->status, ZAdam{});
         ctx->launches += 2;
       }
       if (ctx->net) {  // Adam on theta through the generator's adjoint, then z = f_theta(y0) again
