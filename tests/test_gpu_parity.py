@@ -345,3 +345,23 @@ def test_threshold_projection_with_clusters():
     # the oracle's update did reorder thresholds (the sort was exercised)
     raw = rho.astype(np.float64) - 1e-2 * np.sign(gr)
     assert (np.diff(raw[0]) < 0).any()
+
+
+def test_grad_rho_clustered_z_multichunk():
+    """k_grad_rho (one pass, window compaction per 4096-element chunk): z clustered in a narrow band so
+    every threshold block's window union holds whole chunks (MN = 2 x 2600 -> two chunks, the second
+    ragged), thresholds clustered around the band; grad_z / grad_rho against the oracle chain (Eq. 25)."""
+    c = Cfg("rhoclu", M=2, N=2600, B=8, K=3, f_lo=-0.5, f_hi=0.5, r_n=24, c=300.0,
+            loss_mode=sqngd.LOSS_LSE, beta_or_p=60.0)
+    rng = np.random.default_rng(77)
+    z = (0.5 + 0.01 * (rng.random((1, c.M, c.N)) - 0.5)).astype(np.float32)
+    rho = np.sort(0.5 + 0.02 * (rng.random((1, c.B * c.r_n)) - 0.5)).astype(np.float32)
+    _, w = random_inputs(c, 5)
+    q = O.quantize(c, z, rho)
+    _, _, gs = O.loss_grad(c, q["s_soft"], w, want_w=False)
+    gz_ref, gr_ref = O.chain(c, z, rho, q["s_soft"], gs)
+    ctx = sqngd.Context(c)
+    met, gz, gr = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
+    ctx.sync()
+    check_grad(gz.cpu().numpy(), gz_ref, "grad_z (clustered z)")
+    check_grad(gr.cpu().numpy(), gr_ref, "grad_rho (clustered z, 2 chunks)")
