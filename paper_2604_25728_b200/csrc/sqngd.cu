@@ -41,7 +41,10 @@ thread_local std::string g_last_error;
 #ifndef SQNGD_MINB128
 #define SQNGD_MINB128 3
 #endif
-constexpr int kRhoTB = 16;  // k_grad_rho: thresholds per block (16 lanes each)
+#ifndef SQNGD_RHO_TB
+#define SQNGD_RHO_TB 16
+#endif
+constexpr int kRhoTB = SQNGD_RHO_TB;  // k_grad_rho: thresholds per block (256 / TB lanes each)
 constexpr int plan_E(int P) { return P <= SQNGD_E ? P : SQNGD_E; }
 constexpr int plan_G(int P) { return (P / plan_E(P)) >= 128 ? 1 : 128 / (P / plan_E(P)); }
 constexpr int plan_MINB(int P) {
