@@ -594,7 +594,7 @@ struct ZAdam {
 };
 
 // dL/drho_i = coef sum_n sech^2(c (z_n - rho_i)) dy_n over the window |c (z_n - rho_i)| < 12 (the chain of
-// Eq. 25 through Q_A, the same terms as k_grad_rho_part), in one pass without sorting.  Block = TB
+// Eq. 25 through Q_A; the oracle's chain()), in one pass without sorting.  Block = TB
 // consecutive thresholds x TPT lanes each (rho ascending, so their union window is one z interval).  Per
 // chunk of CH elements the block compacts, in a fixed order (thread, then element), the (z, dy) whose z lies
 // in the union window (block-wide exclusive scan of the per-thread counts), and lane `sub` of a threshold
@@ -673,118 +673,6 @@ __global__ void __launch_bounds__(256) k_grad_rho(int MN, int BR, float c, float
   if (sub == 0 && i0 + t / TPT < BR) gsum[(size_t)r * BR + i0 + t / TPT] = coef * acc;
 }
 
-struct RhoFinish {
-  float coef;
-  float* gsum;      // [R][BR] or nullptr
-  int* cnt_tb;      // [R][gridDim.x]
-  int* cnt_ch;      // [R][gridDim.y]
-  float *z, *mz, *vz;
-  const float* gz;  // grad_z [R][MN]
-  AdamP ap;
-  const int* status;
-};
-
-// The block sorts its chunk's (z, dy) pairs by z in shared memory (bitonic, deterministic), and every
-// warp then visits only the elements inside its threshold window (two binary searches) instead of
-// window-testing the whole chunk.  chunk = 256 = blockDim.x.
-__global__ void __launch_bounds__(256) k_grad_rho_part(int MN, int BR, int chunk, float c, const float* __restrict__ z,
-                                                       const float* __restrict__ rho, const float* __restrict__ dy,
-                                                       float* part, RhoFinish fin) {
-  SQ_PDL_WAIT();
-  __shared__ __align__(16) float2 zd[256];  // the chunk's (z, dy)
-  const int r = blockIdx.z;
-  const int ch = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const float ri = i < BR ? rho[(size_t)r * BR + i] : rho[(size_t)r * BR + BR - 1];
-  const int e0 = ch * chunk, e1 = min(MN, e0 + chunk);
-  for (int e = threadIdx.x; e < 256; e += blockDim.x)
-    zd[e] = e0 + e < e1 ? make_float2(z[(size_t)r * MN + e0 + e], dy[(size_t)r * MN + e0 + e]) : make_float2(1e30f, 0.f);
-  __syncthreads();
-  const float win = 12.f / c;
-  {
-    // bitonic sort of 256 (z, dy) pairs by z (ties by dy, so the order is a function of the values)
-    const int t = threadIdx.x;
-    for (int kk = 2; kk <= 256; kk <<= 1)
-      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        const int ixj = t ^ jj;
-        if (ixj > t) {
-          const float2 a = zd[t], b = zd[ixj];
-          const bool gt = a.x > b.x || (a.x == b.x && a.y > b.y);
-          if (gt == ((t & kk) == 0)) {
-            zd[t] = b;
-            zd[ixj] = a;
-          }
-        }
-        __syncthreads();
-      }
-    float wlo = ri, whi = ri;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      wlo = fminf(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
-      whi = fmaxf(whi, __shfl_xor_sync(0xffffffffu, whi, o));
-    }
-    wlo -= win;
-    whi += win;
-    int lo = 0, hi = 256;  // first index with z >= wlo
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (zd[mid].x < wlo) lo = mid + 1; else hi = mid;
-    }
-    int lo2 = lo, hi2 = 256;  // first index with z > whi
-    while (lo2 < hi2) {
-      const int mid = (lo2 + hi2) >> 1;
-      if (zd[mid].x <= whi) lo2 = mid + 1; else hi2 = mid;
-    }
-    const float k2 = -2.f * 1.4426950408889634f;
-    float acc = 0.f;
-    for (int e = lo; e < lo2; ++e) {
-      const float2 p = zd[e];
-      const float au = c * fabsf(p.x - ri);
-      const float e2 = ex2a_m(k2 * au);
-      const float inv = rcp_m(1.f + e2);
-      const float sech2 = 4.f * e2 * inv * inv;
-      acc = fmaf(au < 12.f ? sech2 : 0.f, p.y, acc);
-    }
-    if (i < BR) part[((size_t)r * gridDim.y + ch) * BR + i] = acc;
-  }
-  if (!fin.gsum && !fin.z) return;
-  __shared__ int last_tb, last_ch;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    last_tb = last_ch = 0;
-    if (fin.gsum) {
-      int* ct = fin.cnt_tb + (size_t)r * gridDim.x + blockIdx.x;
-      if (atomicAdd(ct, 1) == (int)gridDim.y - 1) { last_tb = 1; *ct = 0; }
-    }
-    if (fin.z) {
-      int* cc = fin.cnt_ch + (size_t)r * gridDim.y + ch;
-      if (atomicAdd(cc, 1) == (int)gridDim.x - 1) { last_ch = 1; *cc = 0; }
-    }
-  }
-  __syncthreads();
-  if (last_tb && i < BR) {  // fixed-order sum of this threshold's chunk partials
-    __threadfence();
-    float g = 0.f;
-    const float* pp = part + (size_t)r * gridDim.y * BR + i;
-#pragma unroll 8
-    for (int k = 0; k < (int)gridDim.y; ++k) g += __ldcg(pp + (size_t)k * BR);
-    fin.gsum[(size_t)r * BR + i] = fin.coef * g;
-  }
-  if (last_ch && !(*fin.status & ST_NONFINITE)) {  // Adam on this chunk's z (keep the last finite iterate)
-    float c1, c2;
-    fin.ap.corr(c1, c2);
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const size_t j = (size_t)r * MN + e;
-      const float gi = fin.gz[j];
-      const float mi = fin.ap.b1 * fin.mz[j] + (1.f - fin.ap.b1) * gi;
-      const float vi = fin.ap.b2 * fin.vz[j] + (1.f - fin.ap.b2) * gi * gi;
-      fin.mz[j] = mi;
-      fin.vz[j] = vi;
-      fin.z[j] -= fin.ap.lr * (mi / c1) / (sqrtf(vi / c2) + fin.ap.eps);
-    }
-  }
-}
 
 // ------------------------------------------------------------------ a9 optimizer
 // Adam step counters and the bias corrections (c1, c2) = (1 - b1^t, 1 - b2^t) of every inner step of
@@ -1044,7 +932,7 @@ __device__ void adam_project_rho_dev(int r, int BR, float* rho, float* mr, float
   for (int i = threadIdx.x; i < BR; i += blockDim.x) p[i] = sr[i];
 }
 
-// Step-B threshold update, one block per restart (when not fused into k_grad_rho_part).
+// Step-B update: block (0, r) Adam(rho) + projection of restart r; blocks (1.., r) Adam(z), 4096 elements each.
 __global__ void __launch_bounds__(1024) k_adam_project_rho(int BR, float* rho, float* mr, float* vr, const float* __restrict__ g, AdamP ap,
                                    float lo, float hi, float gap, const int* status, ZAdam za) {
   SQ_PDL_WAIT();

@@ -108,12 +108,8 @@ struct sqngd_ctx_s {
   double2* cm = nullptr;    // [R][M]
   float2* red_grad = nullptr;  // [R][M][N]
   float* dy = nullptr;         // [R][M][N]
-  float* rho_part = nullptr;   // [R][nchunk][BR]
-  int rho_chunk = 256, rho_nchunk = 1;
-  bool rho_onepass = true;     // k_grad_rho (one pass, no sort); SQNGD_RHO_ONEPASS=0: k_grad_rho_part
   // Adam(rho) + projection: a 1024-thread kernel.  As the optimization proceeds the thresholds form
   // clusters that Adam reorders every step, so the projection's sort runs every step.
-  int* rho_cnt = nullptr;      // [R][64] threshold-block + [R][nchunk] element-chunk arrival counters
   float2* gw = nullptr;        // step scratch: grad_w [R][M][N]
   float* gz = nullptr;         // [R][M][N]
   float* grho = nullptr;       // [R][BR]
@@ -766,7 +762,6 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
   CK(ctx->dmalloc(&ctx->d_ct, 2 * sizeof(float2) * ctx->cts));
   if (const char* e = getenv("SQNGD_NO_GRAPH")) ctx->use_graphs = !(e[0] == '1');
-  if (const char* e = getenv("SQNGD_RHO_ONEPASS")) ctx->rho_onepass = e[0] != '0';
   CK(ctx->dmalloc(&ctx->spec, sizeof(float2) * (size_t)cfg.R * cfg.M * P));
   CK(ctx->dmalloc(&ctx->s_soft, sizeof(float2) * RMN));
   CK(ctx->dmalloc(&ctx->s_hard, sizeof(float2) * RMN));
@@ -780,7 +775,6 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   CK(ctx->dmalloc(&ctx->cm, sizeof(double2) * cfg.R * cfg.M));
   CK(ctx->dmalloc(&ctx->red_grad, sizeof(float2) * RMN));
   CK(ctx->dmalloc(&ctx->dy, sizeof(float) * RMN));
-  ctx->rho_nchunk = (int)((cfg.M * cfg.N + ctx->rho_chunk - 1) / ctx->rho_chunk);
   {  // Adam(rho) + projection: 2 n2 floats of dynamic shared memory (64 KB at B r_n = 8192, above
      // the 48 KB a launch gets without opting in)
     int n2 = 1;
@@ -788,9 +782,6 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
     CK(cudaFuncSetAttribute(k_adam_project_rho, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(2 * n2 * sizeof(float))));
   }
-  CK(ctx->dmalloc(&ctx->rho_part, sizeof(float) * (size_t)cfg.R * ctx->rho_nchunk * ctx->BR));
-  CK(ctx->dmalloc(&ctx->rho_cnt, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
-  CK(cudaMemset(ctx->rho_cnt, 0, sizeof(int) * (size_t)cfg.R * (65 + ctx->rho_nchunk)));
   CK(ctx->dmalloc(&ctx->gw, sizeof(float2) * RMN));
   CK(ctx->dmalloc(&ctx->gz, sizeof(float) * RMN));
   CK(ctx->dmalloc(&ctx->grho, sizeof(float) * (size_t)cfg.R * ctx->BR));
@@ -1089,9 +1080,9 @@ void sqngd_destroy(sqngd_ctx ctx) {
     delete g;
   }
   void* ptrs[] = {ctx->tabB, ctx->snrl_w, ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
-                  ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy, ctx->rho_part,
+                  ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy,
                   ctx->gw, ctx->gz, ctx->grho, ctx->met, ctx->status, ctx->Vt, ctx->coef, ctx->wmax, ctx->Rn,
-                  ctx->Gn, ctx->tslot, ctx->lred, ctx->pay, ctx->keyb, ctx->mref, ctx->tabF, ctx->tabA, ctx->rho_cnt, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
+                  ctx->Gn, ctx->tslot, ctx->lred, ctx->pay, ctx->keyb, ctx->mref, ctx->tabF, ctx->tabA, ctx->ftwr, ctx->ftwn, ctx->tabF16, ctx->tabM16, ctx->net_ws};
   for (void* p : ptrs) ctx->dfree(p);
   if (ctx->run_dev) ctx->dfree(ctx->run_dev);
   if (ctx->run_host) cudaFreeHost(ctx->run_host);
@@ -1506,16 +1497,8 @@ static sqngd_status run_snrl(sqngd_ctx ctx, const float2* s, const float2* w, do
 static sqngd_status run_grad_rho(sqngd_ctx ctx, const float* z, const float* rho, float* grad_rho, cudaStream_t st) {
   const sqngd_config& c = ctx->cfg;
   const int MN = c.M * c.N;
-  if (ctx->rho_onepass) {
-    k_grad_rho<kRhoTB><<<dim3((ctx->BR + kRhoTB - 1) / kRhoTB, c.R), 256, 0, st>>>(
-        MN, ctx->BR, (float)c.c, (float)(-(1.0 / (2.0 * c.B)) * c.c), z, rho, ctx->dy, grad_rho);
-  } else {
-    dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);  // thresholds x element chunks x restarts
-    RhoFinish fin{};
-    fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
-    fin.gsum = grad_rho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64; fin.status = ctx->status;
-    k_grad_rho_part<<<g1, 256, 0, st>>>(MN, ctx->BR, ctx->rho_chunk, (float)c.c, z, rho, ctx->dy, ctx->rho_part, fin);
-  }
+  k_grad_rho<kRhoTB><<<dim3((ctx->BR + kRhoTB - 1) / kRhoTB, c.R), 256, 0, st>>>(
+      MN, ctx->BR, (float)c.c, (float)(-(1.0 / (2.0 * c.B)) * c.c), z, rho, ctx->dy, grad_rho);
   ctx->launches += 1;
   return launch_check(ctx, "grad rho");
 }
@@ -1688,32 +1671,17 @@ static sqngd_status step_body(sqngd_ctx ctx, const sqngd_state* stt, int block, 
                         ap(c.lr_theta, 1, i), ctx->status, ctx->side_net, &ctx->launches));
         CK(cudaEventRecord(ctx->ev_nj, ctx->side_net));
       }
-      ZAdam za{};
-      if (ctx->rho_onepass && !ctx->net) {  // one-pass dL/drho, then Adam(z) and Adam(rho) + projection
-        za.z = stt->z; za.mz = stt->m_z; za.vz = stt->v_z; za.gz = ctx->gz; za.MN = c.M * c.N; za.ap = ap(c.lr_z, 1, i);
-      }
-      if (ctx->rho_onepass) {
+      {  // one-pass dL/drho (k_grad_rho), then Adam(z) (blocks 1..) and Adam(rho) + projection (block 0)
+        ZAdam za{};
+        if (!ctx->net) {
+          za.z = stt->z; za.mz = stt->m_z; za.vz = stt->v_z; za.gz = ctx->gz; za.MN = c.M * c.N; za.ap = ap(c.lr_z, 1, i);
+        }
         k_grad_rho<kRhoTB><<<dim3((ctx->BR + kRhoTB - 1) / kRhoTB, c.R), 256, 0, st>>>(
             c.M * c.N, ctx->BR, (float)c.c, (float)(-(1.0 / (2.0 * c.B)) * c.c), stt->z, stt->rho, ctx->dy, ctx->grho);
         const int zch = za.z ? (c.M * c.N + 4095) / 4096 : 0;
         k_adam_project_rho<<<dim3(1 + zch, c.R), 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
                                                                       ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
                                                                       1.0f - 1e-4f, 1e-6f, ctx->status, za);
-        ctx->launches += 2;
-      } else {  // dL/drho gather, then one block per restart: sum, Adam(rho) + projection, Adam(z)
-        dim3 g1((ctx->BR + 255) / 256, ctx->rho_nchunk, c.R);
-        RhoFinish fin{};  // grad_rho sums, Adam(z) and Adam(rho) + projection by last-arriving blocks
-        fin.coef = (float)(-(1.0 / (2.0 * c.B)) * c.c);
-        fin.gsum = ctx->grho; fin.cnt_tb = ctx->rho_cnt; fin.cnt_ch = ctx->rho_cnt + (size_t)c.R * 64;
-        if (!ctx->net) {  // direct z: Adam(z) by the last element-chunk blocks
-          fin.z = stt->z; fin.mz = stt->m_z; fin.vz = stt->v_z; fin.gz = ctx->gz; fin.ap = ap(c.lr_z, 1, i);
-        }
-        fin.status = ctx->status;
-        k_grad_rho_part<<<g1, 256, 0, st>>>(c.M * c.N, ctx->BR, ctx->rho_chunk, (float)c.c, stt->z, stt->rho, ctx->dy,
-                                            ctx->rho_part, fin);
-        k_adam_project_rho<<<dim3(1, c.R), 1024, 2 * n2 * sizeof(float), st>>>(ctx->BR, stt->rho, stt->m_rho, stt->v_rho,
-                                                                      ctx->grho, ap(c.lr_z, 1, i), 1e-4f,
-                                                                      1.0f - 1e-4f, 1e-6f, ctx->status, ZAdam{});
         ctx->launches += 2;
       }
       if (ctx->net) {  // Adam on theta through the generator's adjoint, then z = f_theta(y0) again

@@ -281,7 +281,7 @@ def test_step_b_many_thresholds(engine):
 def test_determinism_full_size(engine):
     """Race hygiene at the benchmark size (compute-sanitizer is closed on this pool): the kernels with
     dynamic scheduling (k_af's atomic unit counter), order-independent atomics (k_lrt / k_node maxima,
-    atomicMax keys) and arrival counters (k_grad_rho_part's last blocks) must give bit-identical
+    atomicMax keys) and the one-pass threshold gradient's block-ordered sums must give bit-identical
     metrics and gradients on repeated C3 evaluations and on a repeated Alg.-1 step."""
     c = CF.C3.with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=ENGINES[engine], n_h=2, n_x=2)
     z, rho, q, w = seeded_inputs(c)
