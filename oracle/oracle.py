@@ -10,6 +10,7 @@ Functions mirror the hot path's semantics:
   loss_grad(cfg, s, w)               O4  closed-form adjoint sums
   chain(cfg, z, rho, s, grad_s)      O4  through Eqs. 23-24
   adam / project_filters / project_thresholds / step   O5 (Alg. 1)
+  stopping_check(hist, patience, lhist)                 O6 (SPEC S:L542-550 stopping_check)
 """
 from __future__ import annotations
 
@@ -334,3 +335,34 @@ def new_state(z, rho, w, theta=None, y0=None) -> dict:
         st["m_theta"] = np.zeros_like(st["theta"])
         st["v_theta"] = np.zeros_like(st["theta"])
     return st
+
+
+# ---------------------------------------------------------------- O6
+def stopping_check(hist, patience, lhist=None, tol=1e-6):
+    """Algorithm 1's stopping criterion over an outer-iteration history, as SPEC S:L542-545 reads
+    P:L485 ("Training terminates when further reduction of L does not lead to improvement in the
+    WPSL"): an improvement is a decrease of the best hard WPSL (linear, N-normalized) by more than
+    `tol` = 1e-6; stop at the first outer iteration t (1-based) at which every restart has gone
+    `patience` iterations without one while (lhist given) its loss L is below its value at its last
+    improvement, i.e. L kept decreasing over the window.  (t = T stops Algorithm 1 regardless, P:L534;
+    the caller's loop bound.)  hist, lhist: [T][R].  Returns (stop t or None, best_iter [R] (0: none),
+    best_wpsl [R])."""
+    hist = np.asarray(hist, dtype=np.float64)
+    T, R = hist.shape
+    best = np.full(R, np.inf)
+    bi = np.zeros(R, int)
+    stall = np.zeros(R, int)
+    lref = np.zeros(R)
+    for t in range(1, T + 1):
+        for r in range(R):
+            v = hist[t - 1, r]
+            if v < best[r] - tol:
+                best[r], bi[r], stall[r] = v, t, 0
+                if lhist is not None:
+                    lref[r] = lhist[t - 1, r]
+            else:
+                stall[r] += 1
+        dec = np.ones(R, bool) if lhist is None else np.asarray(lhist)[t - 1] < lref
+        if patience > 0 and ((stall >= patience) & dec).all():
+            return t, bi, best
+    return None, bi, best

@@ -1,7 +1,8 @@
 """Alg. 1 driver sqngd_run through the C-ABI.
 
-The reference is the stopping rule and best-snapshot rule written out here in Python and applied
-to the hard-WPSL history the driver reports, plus a replay: the driver's best snapshot must be
+The reference is the oracle's stopping_check (O6: the stopping rule and best-snapshot rule of
+P:L485 / SPEC S:L542-545, pinned by SPEC's examples in tests/test_oracle_quant_grad.py) applied to
+the hard-WPSL history the driver reports, plus a replay: the driver's best snapshot must be
 bit-identical to the state after best_iter plain sqngd_step(A+B) calls from the same start
 (the steps are deterministic)."""
 import math
@@ -17,31 +18,6 @@ from paper_2604_25728_b200.configs import Cfg  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
-
-
-def rule(hist, patience, lhist=None, tol=1e-6):
-    """(stop iteration or None, best_iter [R], best_wpsl [R]) of the rule in include/sqngd.h: an
-    improvement is a decrease of the hard WPSL by more than tol; stop when every restart
-    has `patience` iterations without one and (lhist given) its hard loss is below its value at the
-    last improvement ("further reduction of L does not lead to improvement in the WPSL")."""
-    T, R = hist.shape
-    best = np.full(R, math.inf)
-    bi = np.zeros(R, int)
-    stall = np.zeros(R, int)
-    lref = np.zeros(R)
-    for t in range(1, T + 1):
-        for r in range(R):
-            v = hist[t - 1, r]
-            if v < best[r] - tol:
-                best[r], bi[r], stall[r] = v, t, 0
-                if lhist is not None:
-                    lref[r] = lhist[t - 1, r]
-            else:
-                stall[r] += 1
-        dec = np.ones(R, bool) if lhist is None else lhist[t - 1] < lref
-        if patience > 0 and ((stall >= patience) & dec).all():
-            return t, bi, best
-    return None, bi, best
 
 
 def setup(c, idx):
@@ -66,7 +42,7 @@ def test_run_rule_and_snapshot(patience, check_every, need_dec):
     torch.cuda.synchronize()
     h = hist.cpu().numpy()
     lh = res["loss_hist"].cpu().numpy()
-    stop, bi_ref, bw_ref = rule(np.nan_to_num(h, nan=math.inf)[: res["iterations"]], patience,
+    stop, bi_ref, bw_ref = O.stopping_check(np.nan_to_num(h, nan=math.inf)[: res["iterations"]], patience,
                                 lh[: res["iterations"]] if need_dec else None)
     if patience > 0 and stop is not None:
         assert res["stopped"] and res["iterations"] == stop

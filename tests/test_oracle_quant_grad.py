@@ -240,3 +240,33 @@ def test_step_block_isolation_and_feasibility():
     np.testing.assert_array_equal(st["w"], w0)
     assert np.all(np.diff(st["rho"], axis=1) > 0)
     assert st["t_a"] == 2 and st["t_b"] == 2
+
+
+# ---------------------------------------------------------------- O6 stopping_check pins
+# SPEC S:L546-550 stopping_check examples and P:L485 / Alg. 1.
+def test_stopping_check_spec_examples():
+    T = 12
+    improving = np.linspace(0.5, 0.3, T)[:, None]              # strictly improving (steps 0.018 >> 1e-6)
+    assert O.stopping_check(improving, patience=3)[0] is None   # -> continue through t = T
+    # flat hard WPSL for `patience` iterations while L keeps decreasing -> stop at the patience-th flat step
+    flat = np.r_[np.linspace(0.5, 0.4, 5), np.full(T - 5, 0.4)][:, None]
+    L = np.linspace(1.0, 0.5, T)[:, None]
+    stop, bi, bw = O.stopping_check(flat, patience=3, lhist=L)
+    assert stop == 5 + 3 and bi[0] == 5 and bw[0] == 0.4
+    # the same flat WPSL while L rises: no stop (the criterion needs "further reduction of L")
+    assert O.stopping_check(flat, patience=3, lhist=L[::-1].copy())[0] is None
+    # improvements below the 1e-6 tolerance do not reset the window ("by >= 1e-6")
+    creep = np.r_[np.linspace(0.5, 0.4, 5), 0.4 - 1e-7 * np.arange(1, T - 4)][:, None]
+    assert O.stopping_check(creep, patience=3)[0] == 8
+    # two restarts: stop only when every restart has stalled (best snapshot per restart)
+    two = np.c_[flat[:, 0], improving[:, 0]]
+    stop, bi, bw = O.stopping_check(two, patience=3)
+    assert stop is None and bi[1] == T and bw[1] == improving[-1, 0]
+    # best-snapshot monotonicity: the running best is nonincreasing
+    rng = np.random.default_rng(3)
+    h = rng.random((T, 2))
+    prev = np.full(2, np.inf)
+    for t in range(1, T + 1):
+        _, _, b = O.stopping_check(h[:t], patience=0)
+        assert (b <= prev).all()
+        prev = b
