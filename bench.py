@@ -600,6 +600,14 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "precision": ("fp32 CUDA-core arithmetic (FFTs, cell epilogue, reductions; fp64 for the restart sums, "
+                      "energies and Adam bias corrections); the Chebyshev engine's Doppler contraction on "
+                      "split-precision MMAs (fp16 3-term forward, tf32 3x adjoint: ~fp32 accuracy) plus its "
+                      "interpolation bound; against the fp64 oracle the GPU suite's worst per-cell "
+                      "|d|A||/N is 4.6e-7 (bar 1e-6) and worst normwise gradient error 2.6e-6 (bar 1e-4): "
+                      "profiles/r02h_parity_errors.json") if eng["engine"] == "chebyshev" else
+                     "fp32 CUDA-core arithmetic (fp64 restart sums / energies); parity against the fp64 oracle "
+                     "in profiles/r02h_parity_errors.json",
         "config": {**config_dict(c), "doppler_engine": eng_desc,
                    "parallelism": f"restarts x{world} (independent, no collective)"},
         "cells_per_s": forward["cells_per_s"],
