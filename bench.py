@@ -92,6 +92,29 @@ def traffic_bytes(kernel):
         return None
 
 
+def warp_instr(kernel, cfg_name):
+    """Executed warp-instructions per launch of `kernel` at config `cfg_name` from the committed ncu
+    capture (profiles/traffic.json), or None (a property of the kernel and the problem size)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["warp_instructions_per_launch"]
+        return d.get(f"{kernel}@{cfg_name}")
+    except Exception:
+        return None
+
+
+def issue_pipe(kernel, cfg_name, avg_ms, sms, sm_mhz):
+    """Issue-slot use of the dominant kernel: its ncu-counted warp-instructions per launch over the live
+    launch time, against one warp-instruction per clock per SM sub-partition (4 per SM)."""
+    n = warp_instr(kernel, cfg_name)
+    if not n:
+        return None
+    peak = sms * 4 * sm_mhz * 1e6
+    ach = n / (avg_ms / 1e3)
+    return {"achieved": ach / 1e9, "peak": peak / 1e9, "frac": ach / peak, "unit": "G warp-instr/s",
+            "warp_instr_per_launch": n, "basis": f"ncu smsp__inst_executed.sum (profiles/traffic.json) / launch time; "
+                                                 f"peak {sms} SM x 4 issue slots x {sm_mhz:.0f} MHz"}
+
+
 def peaks():
     try:
         p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -474,6 +497,11 @@ def main():
                             "6 per complex multiply, 7 / 10 per cell)",
                     "peak_basis": f"{sms} SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz ({src} sm_max_mhz)",
                     **common}
+        # issue slots (both engines are issue-bound): the ncu instruction count of the same kernel at the
+        # same size (C3, one restart) over the live launch time
+        iss = issue_pipe(knames[names[dom]], cc.name, avg_ms, sms, sm_mhz) if cc.R == 1 else None
+        if iss:
+            roof.setdefault("pipes", {})["issue"] = iss
         out = {"value": value, "ms_per_step": tot_ms / args.steps, "roofline": roof, "launches": launches,
                "kernel_ms": {n: prof["ms"][i] / args.steps for i, n in enumerate(names)}, "engine": info,
                "wall_s": t_wall}
