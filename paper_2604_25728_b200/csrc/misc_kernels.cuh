@@ -404,10 +404,11 @@ struct CombineArgs {
 // Unit slots -> per-row sums in true units of dL_wpsl / d(.)^*:
 // out[ra][q] = norm_r * sum_k scale_u slot_u[q],  u = ra K + k  (fixed order),
 // norm_r = eps/(2N) * extra * (LSE: 1/S_r, PNORM: S_r^{1/p-1}).
-// Block: 32 lanes x 2 complex (q) x 8 k-lanes.
-__global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status) {
+// Block: 32 lanes x 2 complex (q) x KL k-lanes (16 for the long slot lists: one load round trip per lane).
+template <int KL>
+__global__ void __launch_bounds__(32 * KL) k_combine_rows(CombineArgs a, int* status) {
   SQ_PDL_WAIT();
-  __shared__ float4 sh[8][33];
+  __shared__ float4 sh[KL][33];
   const int ra = blockIdx.y;
   const int r = ra / a.M;
   const double m = a.red[r].m, S = a.red[r].S;
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   double norm = 0.0;  // (fp64 divide / pow issued now, off the critical path of the slot sums)
   if (live) norm = a.eps / (2.0 * a.N) * a.extra * ((a.mode == 1) ? 1.0 / S : pow(S, 1.0 / a.bp - 1.0));
   const int q = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));  // two complex values per thread
-  const int kl = threadIdx.x >> 5;                              // 8 k-lanes
+  const int kl = threadIdx.x >> 5;                              // KL k-lanes
   FinIn fin0{}, fin1{};
   double2 gcf = make_double2(0.0, 0.0);
   if (a.fin && kl == 0 && q < a.len) {  // finalize inputs fetched now, overlapping the slot sums
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   if (live && q < a.len) {
     const int klo = max(0, a.u_lo - ra * a.K), khi = min(a.K, a.u_hi - ra * a.K);
 #pragma unroll 8
-    for (int k = klo + kl; k < khi; k += 8) {
+    for (int k = klo + kl; k < khi; k += KL) {
       const int u = ra * a.K + k;
       const float sc = a.part.scale ? __ldg(a.part.scale + u) : 1.f;  // null: slots pre-scaled (Chebyshev engine)
       const float4 v = __ldg(reinterpret_cast<const float4*>(a.part.g + (size_t)u * a.slot_stride + q));
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(256) k_combine_rows(CombineArgs a, int* status
   if (kl == 0 && q < a.len) {
     float4 t = sh[0][threadIdx.x];
 #pragma unroll
-    for (int j = 1; j < 8; ++j) {
+    for (int j = 1; j < KL; ++j) {
       t.x += sh[j][threadIdx.x].x;
       t.y += sh[j][threadIdx.x].y;
       t.z += sh[j][threadIdx.x].z;

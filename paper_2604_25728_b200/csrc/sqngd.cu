@@ -1351,6 +1351,14 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
   return launch_check(ctx, "metrics");
 }
 
+// k_combine_rows with 16 k-lanes (512 threads) for the long slot lists (>= 64 slots per row: the FFT
+// engine's K bins, the Chebyshev Step-A M Q spectral slots), 8 otherwise; SQNGD_COMB_KL=8 forces 8.
+static void launch_combine(sqngd_ctx ctx, const CombineArgs& ca, dim3 grid, cudaStream_t st) {
+  static const int force8 = [] { const char* e = getenv("SQNGD_COMB_KL"); return e && e[0] == '8'; }();
+  if (ca.K >= 64 && !force8) k_combine_rows<16><<<grid, 512, 0, st>>>(ca, ctx->status);
+  else k_combine_rows<8><<<grid, 256, 0, st>>>(ca, ctx->status);
+}
+
 // Loss + gradient of an explicit waveform s.  Assumes H = FFT(w) is current.
 // wrt 1: writes grad_w (2 dL/dw^*); wrt 2: grad_s (dL/ds^*), dy and grad_z if dq/grad_z given.
 // Step-A optimizer tail fused into the gradient's last kernel (sqngd_step, single GPU).
@@ -1411,14 +1419,14 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
       ca.part.g = ctx->tslot; ca.len = c.N; ca.extra = 1.0;
       ca.fin = multi ? 0 : 1;
       ca.out = multi ? ctx->red_grad : nullptr;
-      k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      launch_combine(ctx, ca, dim3((c.N + 63) / 64, c.R * c.M), st);
       ctx->launches += 3;
       if ((rc = launch_check(ctx, "chebyshev adjoint (transmit)"))) return rc;
     } else {
       const int nsl = c.M * ctx->Q;  // spectral slots per filter row (zeros for other ranks' rows)
       ca.K = nsl; ca.slot_stride = ctx->P; ca.u_lo = 0; ca.u_hi = c.R * c.M * nsl;
       ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
-      k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      launch_combine(ctx, ca, dim3((ctx->P + 63) / 64, c.R * c.M), st);
       ctx->launches += 3;
       if (!multi) {
         if (tail) {
@@ -1453,11 +1461,11 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     ctx->launches += 1;
     if (mode == MODE_ADJ_B) {  // single GPU: finalize inside the combine
       ca.len = c.N; ca.extra = 1.0; ca.fin = multi ? 0 : 1; ca.out = multi ? ctx->red_grad : nullptr;
-      k_combine_rows<<<dim3((c.N + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      launch_combine(ctx, ca, dim3((c.N + 63) / 64, c.R * c.M), st);
       ctx->launches += 1;
     } else {
       ca.len = ctx->P; ca.extra = 1.0 / ctx->P; ca.fin = 0; ca.out = ctx->spec;
-      k_combine_rows<<<dim3((ctx->P + 63) / 64, c.R * c.M), 256, 0, st>>>(ca, ctx->status);
+      launch_combine(ctx, ca, dim3((ctx->P + 63) / 64, c.R * c.M), st);
       ctx->launches += 2;
       if (!multi) {  // single GPU: finalize inside the row IFFT (+ Adam(w), Pi_H, next H and c_m in the step)
         if (tail) {
