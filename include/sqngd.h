@@ -55,6 +55,12 @@ enum { SQNGD_WRT_FILTERS = 1, /* Step A: waveform fixed, gradient t
        SQNGD_WRT_TRANSMIT = 2 /* Step B: filters fixed, gradient to z and rho      */ };
 enum { SQNGD_BLOCK_A = 1, SQNGD_BLOCK_B = 2, SQNGD_BLOCK_AB = 3 };
 enum { SQNGD_FLAG_NO_CROSS = 1,     /* M == 1: WCPSL := 0 (no cross terms, Eq. 9)              */
+       SQNGD_FLAG_TIE = 2,          /* the WAPSL or WCPSL maximum (or WAPSL == WCPSL) is attained by more
+                                       than one cell in the engine's fp32 arithmetic; the reported argmax is
+                                       the lowest (m, l, tau, k) (Eqs. 7-9).  Exact
+                                       between cells of different evaluation units; within a Chebyshev
+                                       unit, two bins of one lag on the same side of the grid centre are
+                                       not compared.  Single-context only (world == 1).  */
        SQNGD_FLAG_DOPPLER_ALIAS = 4 /* grid reaches beyond [-N/2, N/2]; |A| is N-periodic in f */ };
 
 /* Problem definition (copied into the context at create). */

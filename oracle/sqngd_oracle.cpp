@@ -50,7 +50,7 @@ typedef struct {
   int32_t argmax_auto[4];              // (m, l, tau, k)
   int32_t argmax_cross[4];
   int32_t n_cells;                     // |S|, sidelobe cells in the ROI
-  int32_t flags;                       // 1: M == 1 (no cross terms)
+  int32_t flags;                       // 1: M == 1 (no cross terms); 2: tied maximum (Q17)
 } oracle_metrics;
 
 }  // extern "C"
@@ -141,6 +141,7 @@ LossParts loss_from_cube(const oracle_cfg& c, const cd* s, const cd* w, const st
   std::memset(&lp.met, 0, sizeof(lp.met));
   for (int i = 0; i < 4; ++i) lp.met.argmax_auto[i] = lp.met.argmax_cross[i] = lp.arg[i] = -1;
   double wa = -1.0, wc = -1.0;
+  int na = 0, nc = 0;  // cells attaining the running maxima (ties, SQNGD_FLAG_TIE)
   int n_cells = 0;
   for (int m = 0; m < M; ++m)
     for (int l = 0; l < M; ++l)
@@ -153,15 +154,20 @@ LossParts loss_from_cube(const oracle_cfg& c, const cd* s, const cd* w, const st
           double v = wt * std::abs(A[(((size_t)m * M + l) * K + k) * L + (tau + N - 1)]) / N;
           int idx[4] = {m, l, tau, k};
           if (is_auto) {
-            if (v > wa) { wa = v; std::memcpy(lp.met.argmax_auto, idx, sizeof(idx)); }
+            if (v > wa) { wa = v; na = 1; std::memcpy(lp.met.argmax_auto, idx, sizeof(idx)); }
+            else if (v == wa) ++na;
           } else {
-            if (v > wc) { wc = v; std::memcpy(lp.met.argmax_cross, idx, sizeof(idx)); }
+            if (v > wc) { wc = v; nc = 1; std::memcpy(lp.met.argmax_cross, idx, sizeof(idx)); }
+            else if (v == wc) ++nc;
           }
         }
   lp.met.n_cells = n_cells;
   lp.met.wapsl = wa < 0 ? 0.0 : wa;
   lp.met.wcpsl = wc < 0 ? 0.0 : wc;
   if (M == 1) lp.met.flags |= 1;
+  // 2: a maximum attained by more than one cell, or WAPSL == WCPSL -- the lexicographic rule decided
+  // the reported argmax (Q17; the flag of the C-ABI's SQNGD_FLAG_TIE)
+  if (na > 1 || nc > 1 || (wa >= 0.0 && wa == wc)) lp.met.flags |= 2;
   // WPSL = max(WAPSL, WCPSL) (Eq. 7); tie between the two -> lexicographically lower cell.
   if (wa > wc || (wa == wc && wa >= 0 && lex_less(lp.met.argmax_auto, lp.met.argmax_cross)))
     std::memcpy(lp.arg, lp.met.argmax_auto, sizeof(lp.arg));

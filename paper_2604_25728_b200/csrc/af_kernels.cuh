@@ -51,6 +51,8 @@ struct KP {
   int u_lo, u_hi;        // units evaluated by this rank (multi-GPU slice of R*M*K)
   int want_S;            // forward: accumulate surrogate sums
   int* counter;          // dynamic unit counter (zeroed before the launch)
+  uint32_t* tiew;        // [R][2] 1 + float bits of the largest value at which a group saw two cells tie (zeroed with counter)
+  int track_tie;         // 1: track ties (SQNGD_FLAG_TIE requested)
   int mld;               // |A| map row pitch (floats)
 };
 
@@ -221,8 +223,9 @@ struct SliceCtx {
 // (the rare path of the running argmax: taken only when a slice reaches the running max).
 template <class PL, bool HW>
 __device__ __forceinline__ uint32_t argmax_index(const float2 (&v)[PL::E], float kv, const SliceCtx& sc, int t, int N,
-                                              int K) {
+                                              int K, int& cnt) {
   uint32_t best = 0xFFFFFFFFu;
+  cnt = 0;  // cells of value kv (SQNGD_FLAG_TIE)
 #pragma unroll
   for (int i = 0; i < PL::E; ++i) {
     if (!((sc.roi >> i) & 1u)) continue;
@@ -234,6 +237,7 @@ __device__ __forceinline__ uint32_t argmax_index(const float2 (&v)[PL::E], float
       x *= wt * wt;
     }
     if (x == kv) {
+      ++cnt;
       const uint32_t idx = (sc.base_idx + (uint32_t)lag) * (uint32_t)K + (uint32_t)sc.k;
       best = idx < best ? idx : best;
     }
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   int par = 0, gpar = 0;
   int cur_r = -1;
   unsigned long long key_a = 0ull, key_c = 0ull;  // packed (w^2 |A|^2, ~index) maxima
+  uint32_t tie_a = 0u, tie_c = 0u;                 // largest value at which two of the group's cells tied
   float2 v[E];
   float2 acc[MODE == MODE_FWD ? 1 : E];
 
@@ -401,6 +406,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
     if (r != cur_r) {  // group-uniform running (value, index) maxima, kept across units of one restart
       cur_r = r;
       key_a = key_c = 0ull;
+      tie_a = tie_c = 0u;
     }
     if constexpr (MODE != MODE_FWD) {
 #pragma unroll
@@ -454,9 +460,19 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
         unsigned long long& kcat = is_auto ? key_a : key_c;
         if (gmax2 >= 0.f && __float_as_uint(gmax2) >= (uint32_t)(kcat >> 32)) {
           uint32_t idx = 0xFFFFFFFFu;
+          int cnt = 0;
           if (lmax2 == gmax2)
-            idx = has_w ? argmax_index<PL, true>(v, lmax2, sc, t, N, K) : argmax_index<PL, false>(v, lmax2, sc, t, N, K);
+            idx = has_w ? argmax_index<PL, true>(v, lmax2, sc, t, N, K, cnt)
+                        : argmax_index<PL, false>(v, lmax2, sc, t, N, K, cnt);
           const unsigned long long cand = grpops.max_u64(lmax2 == gmax2 ? pack_key(gmax2, idx) : 0ull);
+          // SQNGD_FLAG_TIE: two cells of this slice, or a cell of an earlier slice, at the value gmax2
+          if (MODE == MODE_FWD && kp.track_tie) {  // (uniform; forward only: the adjoints keep their code)
+            const float ncell = grpops.sum_f((float)cnt);
+            if (ncell >= 2.f || (kcat != 0ull && (uint32_t)(kcat >> 32) == __float_as_uint(gmax2))) {
+              uint32_t& tcat = is_auto ? tie_a : tie_c;
+              tcat = max(tcat, __float_as_uint(gmax2) + 1u);
+            }
+          }
           kcat = cand > kcat ? cand : kcat;
         }
         // ---- surrogate sums (and a7: the cotangent) with a unit-uniform running shift
@@ -514,6 +530,8 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
     if (t == 0) {
       part.key[2 * (size_t)u] = key_a;
       part.key[2 * (size_t)u + 1] = key_c;
+      if (MODE == MODE_FWD && tie_a) atomicMax(kp.tiew + 2 * r, tie_a);
+      if (MODE == MODE_FWD && tie_c) atomicMax(kp.tiew + 2 * r + 1, tie_c);
       part.m[u] = ushift;
       part.S[u] = uS;
     }

@@ -24,7 +24,23 @@ struct Red {               // per restart, after combining all groups
   double m;                // shift of S and of the gradient partials
   double S;                // sum of phi at shift m
   unsigned long long key_a, key_c;
+  uint32_t tie, pad;       // tie: SQNGD_FLAG_TIE of this restart's maxima (0 after a multi-GPU combine)
 };
+
+// The packed key with its index part un-inverted: the max over these gives the HIGHEST index among
+// the keys of the maximal value, the max over the keys themselves the lowest -- two different indices
+// of one value mean a tie between two slots (SQNGD_FLAG_TIE).
+__device__ __forceinline__ unsigned long long key_hi_index(unsigned long long k) {
+  return k ? ((k & 0xFFFFFFFF00000000ull) | (~k & 0xFFFFFFFFull)) : 0ull;
+}
+// Tie of a category's maximum: between two slots (lowest-index key k vs highest-index key kh of the
+// same value) or inside one (tv: 1 + the float bits of the largest value at which a unit saw two of its
+// cells tie; 0: none).
+__device__ __forceinline__ bool key_tied(unsigned long long k, unsigned long long kh, uint32_t tv) {
+  if (!k) return false;
+  const uint32_t v = (uint32_t)(k >> 32);
+  return ((uint32_t)(kh >> 32) == v && kh != key_hi_index(k)) || tv == v + 1u;
+}
 
 
 struct Part {                // one slot per unit u = (r * M + a) * K + k
@@ -69,6 +85,7 @@ struct MetricsArgs {
   double* loss_hist;
   int hist_stride, hist_col;
   const double* snrl_in;  // [R] max_m SNRL_m (k_snrl) for the record, or nullptr (NaN in the record)
+  int tie_scan;           // 1: compute SQNGD_FLAG_TIE (a record the caller reads); 0: flag left clear
 };
 
 // Eqs. 7-10, 37-42 for restart r from the combined partials.  Called by one whole warp
@@ -101,7 +118,7 @@ __device__ void metrics_warp(const MetricsArgs& a, int r, int* status) {
   else o.loss_wpsl = 0.0;
   o.loss_snrl = lsn / a.M;
   o.loss = a.eps * o.loss_wpsl + (1.0 - a.eps) * o.loss_snrl;
-  o.flags = a.flags;
+  o.flags = a.flags | (rr.tie ? 2u : 0u);  // 2 = SQNGD_FLAG_TIE
   o.n_cells = a.n_cells;
   // Eq. 48: PSLR = 20 log10(PSL / N); the maxima above are already normalised by N (Q5)
   o.apslr_db = 20.0 * log10(o.wapsl);
@@ -133,20 +150,30 @@ __device__ __forceinline__ T_ block_reduce(T_ x, Op op, T_* sh) {
 // Partials are read with ld.global.cg: in the fused kernel's last CTA they were written by
 // other SMs in the same launch.
 __device__ void reduce_restart(int r, int GPR, int g_lo, int g_hi, int mode, double bp, Part part, Red* red,
-                               const MetricsArgs& ma, int* status, double* shd, unsigned long long* shk) {
+                               const MetricsArgs& ma, int* status, double* shd, unsigned long long* shk,
+                               const uint32_t* tiew) {
   const int lo = max(g_lo, r * GPR), hi = min(g_hi, (r + 1) * GPR);
   double mloc = -INFINITY;
-  unsigned long long a = 0, cc = 0;
+  unsigned long long a = 0, cc = 0, ah = 0, ch = 0;  // ah, ch: highest-index keys (ties, SQNGD_FLAG_TIE)
   for (int g = lo + threadIdx.x; g < hi; g += blockDim.x) {
     if (__ldcg(part.S + g) > 0.f) mloc = fmax(mloc, (double)__ldcg(part.m + g));
-    a = max(a, __ldcg(part.key + 2 * g));
-    cc = max(cc, __ldcg(part.key + 2 * g + 1));
+    const unsigned long long ka = __ldcg(part.key + 2 * g), kc = __ldcg(part.key + 2 * g + 1);
+    a = max(a, ka);
+    cc = max(cc, kc);
+    if (ma.tie_scan) {
+      ah = max(ah, key_hi_index(ka));
+      ch = max(ch, key_hi_index(kc));
+    }
   }
   auto dmax = [](double x, double y) { return fmax(x, y); };
   auto umax = [](unsigned long long x, unsigned long long y) { return x > y ? x : y; };
   const double m = block_reduce(mloc, dmax, shd);
   a = block_reduce(a, umax, shk);
   cc = block_reduce(cc, umax, shk);
+  if (ma.tie_scan) {  // (uniform)
+    ah = block_reduce(ah, umax, shk);
+    ch = block_reduce(ch, umax, shk);
+  }
   double S = 0.0;
   const float mf = (float)m;
   const float lb = (float)(bp * 1.4426950408889634);
@@ -167,6 +194,8 @@ __device__ void reduce_restart(int r, int GPR, int g_lo, int g_hi, int mode, dou
     red[r].S = S;
     red[r].key_a = a;
     red[r].key_c = cc;
+    red[r].tie = ma.tie_scan && (key_tied(a, ah, tiew ? tiew[2 * r] : 0u) || key_tied(cc, ch, tiew ? tiew[2 * r + 1] : 0u) ||
+                  (a && (a >> 32) == (cc >> 32))) ? 1u : 0u;
   }
   __syncthreads();
   if (threadIdx.x < 32 && (ma.out || ma.loss_hist || ma.p_out)) metrics_warp(ma, r, status);

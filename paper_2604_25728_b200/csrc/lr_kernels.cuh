@@ -45,9 +45,25 @@ namespace sq {
 // the result is deterministic; reset by k_node of the same evaluation.
 struct LrRed {
   unsigned int mbits;  // max unit shift (float bits; 0 = none)
-  unsigned int pad;
+  unsigned int tie_a;  // 1 + float bits of the largest value at which a unit saw two of its cells tie (auto)
   unsigned long long key_a, key_c;
+  unsigned int tie_c;  // (cross maps)
+  unsigned int pad;
 };
+
+// Warp max of packed keys that also notes a tie: at the butterfly stage where the two halves holding
+// two distinct cells of the maximal value meet, both halves carry that value with different indices.
+__device__ __forceinline__ unsigned long long warp_key_max_tie(unsigned long long key, uint32_t& tv) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+    if (y && key && (y >> 32) == (key >> 32) && y != key) tv = max(tv, (uint32_t)(key >> 32) + 1u);
+    key = y > key ? y : key;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tv = max(tv, __shfl_xor_sync(0xffffffffu, tv, o));
+  return key;
+}
 
 // Node AFs for every unit (r, m, l, q): R_{ml,q}(tau) = IFFT_P(X~_{m,q} conj(H_l))[(-tau) mod P]
 // (Eq. 36, Q1), stored at Rn[((r M + m) M + l) Q + q][tau + N - 1].
@@ -63,7 +79,7 @@ __global__ void __launch_bounds__(PL::T* G, MINB)
   float2* xbuf = reinterpret_cast<float2*>(smem_raw) + grp * (FftSmem<PL>::TOTAL);
   GroupSync sync{1 + grp, T, group_mask(T)};
   if (blockIdx.x == 0)  // this evaluation's k_lr maxima
-    for (int i = threadIdx.x; i < R; i += blockDim.x) lred[i] = LrRed{0u, 0u, 0ull, 0ull};
+    for (int i = threadIdx.x; i < R; i += blockDim.x) lred[i] = LrRed{};
   const int uu = u0 + (u < units ? u : units - 1);  // units [u0, u0 + units): this rank's rows
   const int q = uu % Q, pr = uu / Q;  // pr = (r M + m) M + l
   const int l = pr % M, rm = pr / M, r = rm / M;
@@ -677,14 +693,20 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
 
   // ---- lane record: key over both rows, per-row shift / sum, cotangent fragments
   unsigned long long key = 0ull;
+  // SQNGD_FLAG_TIE inside the unit (forward modes only: the loss+gradient kernel keeps its code; its
+  // evaluations flag ties between units, k_lr_finish): 1 + the largest value at which two cells tie
+  constexpr bool TT = !GRAD;
+  uint32_t tv = 0u;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float best = bl[h];
     int bk = kl[h];
+    const bool eq = bh[h] == best;  // the lag's two bin streams (below / above the grid centre) tie
     if (bh[h] > best) { best = bh[h]; bk = kh[h]; }
     best *= isc[h] * isc[h];  // exact: sigma is a power of two
     const uint32_t cell = ((uint32_t)((m * M + l) * a.L + idx[h])) * (uint32_t)a.K + (uint32_t)bk;
     const unsigned long long kk = (valid[h] && best >= 0.f) ? pack_key(best, cell) : 0ull;
+    if (TT && kk && (eq || (key && (kk >> 32) == (key >> 32)))) tv = max(tv, (uint32_t)(kk >> 32) + 1u);
     key = kk > key ? kk : key;
   }
   if (a.kw > 1) {
@@ -736,10 +758,14 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
   }
 
   // ---- unit reduction (warp 0)
+  if constexpr (TT) {
+    key = warp_key_max_tie(key, tv);
+  } else {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
-    key = y > key ? y : key;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+      key = y > key ? y : key;
+    }
   }
   float mw = 0.f, fS[2] = {0.f, 0.f}, fG[2] = {0.f, 0.f};
   if (LM != 0) {
@@ -773,6 +799,7 @@ __global__ void __launch_bounds__(SQNGD_LRT_MAXT, SQNGD_LRT_MINB) k_lrt(const Lr
     a.part.S[u] = Su;
     const int r = rr_;
     if (key) atomicMax(is_auto ? &a.lred[r].key_a : &a.lred[r].key_c, key);
+    if (TT && tv) atomicMax(is_auto ? &a.lred[r].tie_a : &a.lred[r].tie_c, tv);
     if (LM != 0 && mw > 0.f) atomicMax(&a.lred[r].mbits, __float_as_uint(mw));
   }
 }
@@ -803,14 +830,33 @@ __global__ void __launch_bounds__(1024) k_lr_finish(int GPR, int g_lo, int g_hi,
   }
   auto dsum = [](double x, double y) { return x + y; };
   S = block_reduce(S, dsum, shd);
+  const bool want_met = ma.out || ma.loss_hist || ma.p_out;
+  const bool scan = want_met && ma.tie_scan;
+  // SQNGD_FLAG_TIE between units: the highest-index unit keys (only when a metrics record is written)
+  unsigned long long ah = 0ull, ch = 0ull;
+  if (scan) {
+    __shared__ unsigned long long shk[32];
+    const unsigned long long* kp = part.key + 2 * (size_t)r * GPR;
+    const int glo = max(0, g_lo - r * GPR), ghi = min(GPR, g_hi - r * GPR);
+    for (int g = glo + threadIdx.x; g < ghi; g += blockDim.x) {
+      ah = max(ah, key_hi_index(__ldcg(kp + 2 * g)));
+      ch = max(ch, key_hi_index(__ldcg(kp + 2 * g + 1)));
+    }
+    auto umax = [](unsigned long long x, unsigned long long y) { return x > y ? x : y; };
+    ah = block_reduce(ah, umax, shk);
+    ch = block_reduce(ch, umax, shk);
+  }
   if (threadIdx.x == 0) {
+    const LrRed lr = lred[r];
     red[r].m = mf > 0.f ? (double)mf : -INFINITY;
     red[r].S = S;
-    red[r].key_a = lred[r].key_a;
-    red[r].key_c = lred[r].key_c;
+    red[r].key_a = lr.key_a;
+    red[r].key_c = lr.key_c;
+    red[r].tie = (scan && (key_tied(lr.key_a, ah, lr.tie_a) || key_tied(lr.key_c, ch, lr.tie_c) ||
+                               (lr.key_a && (lr.key_a >> 32) == (lr.key_c >> 32)))) ? 1u : 0u;
   }
   __syncthreads();
-  if (threadIdx.x < 32 && (ma.out || ma.loss_hist || ma.p_out)) metrics_warp(ma, r, status);
+  if (threadIdx.x < 32 && want_met) metrics_warp(ma, r, status);
 }
 
 struct AdjGArgs {

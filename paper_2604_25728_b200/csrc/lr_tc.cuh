@@ -398,12 +398,10 @@ __global__ void __launch_bounds__(kLrfThreads, 2) k_lrf(const LrfArgs a) {
     const uint32_t cell = ((uint32_t)((m * M + l) * a.L + idx)) * (uint32_t)a.K + (uint32_t)bk;
     key = (valid && best >= 0.f) ? pack_key(bu, cell) : 0ull;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
-    key = y > key ? y : key;
-  }
+  uint32_t tv = 0u;  // SQNGD_FLAG_TIE (ties between lanes and between warps of the unit)
+  key = warp_key_max_tie(key, tv);
   if (lane == 0) s_key[wp] = key;
+  if (lane == 0 && tv) atomicMax(is_auto ? &a.lred[r].tie_a : &a.lred[r].tie_c, tv);
   float mw = 0.f;
   if (LM != 0) {
     mw = valid ? shift : 0.f;
@@ -431,10 +429,13 @@ __global__ void __launch_bounds__(kLrfThreads, 2) k_lrf(const LrfArgs a) {
   if (tid == 0) {
     unsigned long long kk = s_key[0];
     float St = s_red[0];
+    uint32_t tw = 0u;
     for (int w = 1; w < kLrfThreads / 32; ++w) {
+      if (s_key[w] && kk && (s_key[w] >> 32) == (kk >> 32) && s_key[w] != kk) tw = max(tw, (uint32_t)(kk >> 32) + 1u);
       kk = s_key[w] > kk ? s_key[w] : kk;
       St += s_red[w];
     }
+    if (tw) atomicMax(is_auto ? &a.lred[r].tie_a : &a.lred[r].tie_c, tw);
     a.part.key[2 * (size_t)u] = is_auto ? kk : 0ull;
     a.part.key[2 * (size_t)u + 1] = is_auto ? 0ull : kk;
     a.part.m[u] = mw;

@@ -166,11 +166,11 @@ __global__ void k_quantize(int MN, int B, int BR, float c, const float* __restri
 // [r * GPR, (r+1) * GPR) intersected with [g_lo, g_hi); per-unit rescale factors for the
 // gradient combine.  One block of 1024 threads per restart, fixed order (deterministic).
 __global__ void k_reduce_groups(int GPR, int g_lo, int g_hi, int mode, double bp, Part part, Red* red,
-                                MetricsArgs ma, int* status) {
+                                MetricsArgs ma, int* status, const uint32_t* tiew) {
   SQ_PDL_WAIT();
   __shared__ double shd[32];
   __shared__ unsigned long long shk[32];
-  reduce_restart(blockIdx.x, GPR, g_lo, g_hi, mode, bp, part, red, ma, status, shd, shk);
+  reduce_restart(blockIdx.x, GPR, g_lo, g_hi, mode, bp, part, red, ma, status, shd, shk, tiew);
 }
 
 // Multi-GPU: the shift m arrived from the all-reduce; refresh the per-group scales.
@@ -1103,6 +1103,7 @@ __global__ void __launch_bounds__(256) k_world_unpack(WorldArgs a, int* status) 
     rr.S = a.mode != 0 ? S : 0.0;
     rr.key_a = a.key[3 * r];
     rr.key_c = a.key[3 * r + 1];
+    rr.tie = rr.pad = 0u;  // (ties between ranks are not tracked)
     a.red[r] = rr;
     if (!isfinite(S)) atomicOr(status, ST_NONFINITE);
     const unsigned long long mb = a.key[3 * r + 2];

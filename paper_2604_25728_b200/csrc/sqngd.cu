@@ -492,6 +492,8 @@ static KP make_kp(const sqngd_ctx_s* c, int want_S) {
   kp.u_lo = (int)lo; kp.u_hi = (int)hi;
   kp.want_S = want_S;
   kp.counter = c->counter;
+  kp.tiew = reinterpret_cast<uint32_t*>(c->counter + 2);
+  kp.track_tie = 0;
   kp.mld = g.map_ld > 0 ? g.map_ld : c->L;
   return kp;
 }
@@ -756,7 +758,9 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
   const int64_t uslots = std::max(ctx->units, ctx->units_lr);
   const int64_t gslots = std::max(ctx->units, ctx->lr ? (int64_t)cfg.R * cfg.M * cfg.M * ctx->Q : (int64_t)0);
   CK(ctx->dmalloc(&ctx->part.scale, sizeof(float) * uslots));
-  CK(ctx->dmalloc(&ctx->counter, 2 * sizeof(int)));
+  // [0]: the FFT engine's dynamic unit counter; [1]: unused; [2, 2 + 2R): the per-restart tie words
+  // (KP::tiew), zeroed together with the counter before every FFT-engine launch
+  CK(ctx->dmalloc(&ctx->counter, (2 + 2 * (size_t)cfg.R) * sizeof(int)));
   CK(ctx->dmalloc(&ctx->d_t, 2 * sizeof(long long)));
   CK(ctx->dmalloc(&ctx->snrl_w, sizeof(double) * cfg.R));
   ctx->cts = std::max(1, std::max(cfg.n_h, cfg.n_x));
@@ -1324,12 +1328,14 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
   const double ptar = std::pow(10.0, -c.mu_db / 20.0);
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
                  ctx->red, ctx->cm, met, p_out, hist, c.n_h + c.n_x, hist_col, snrl_in};
+  ma.tie_scan = met != nullptr && met != ctx->met;  // a record the caller reads: SQNGD_FLAG_TIE
+  kp.track_tie = ma.tie_scan;
   MetricsArgs none = ma;
   none.out = nullptr; none.p_out = nullptr; none.loss_hist = nullptr;
   if (ctx->lr) {
     if ((rc = run_lr(ctx, false, MODE_FWD, af_mag, ma, st, false))) return rc;
   } else {
-    cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
+    cudaMemsetAsync(ctx->counter, 0, (2 + 2 * (size_t)c.R) * sizeof(int), st);
     {
       ProfScope ps(ctx, MODE_FWD, st);
       with_P(ctx->P, [&](auto Lc) {
@@ -1339,7 +1345,8 @@ static sqngd_status run_forward(sqngd_ctx ctx, const float2* s, const float2* w,
     ctx->launches += 2;
     if ((rc = launch_check(ctx, "af forward"))) return rc;
     k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part,
-                                          ctx->red, ctx->multi ? none : ma, ctx->status);
+                                          ctx->red, ctx->multi ? none : ma, ctx->status,
+                                          kp.tiew);
     if ((rc = launch_check(ctx, "metrics"))) return rc;
   }
   if (!ctx->multi) return SQNGD_OK;
@@ -1380,6 +1387,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
   FinArgs fa{c.R, c.M, c.N, wrt, c.eps_w, ptar, ctx->cm, s, w, dq, grad_w, grad_s, ctx->dy, grad_z};
   MetricsArgs ma{c.M, c.N, c.K, ctx->L, c.loss_mode, c.beta_or_p, c.eps_w, ptar, ctx->n_cells, ctx->flags,
                  ctx->red, ctx->cm, met, nullptr, hist, c.n_h + c.n_x, hist_col, snrl_in};
+  ma.tie_scan = met != nullptr && met != ctx->met;  // a record the caller reads: SQNGD_FLAG_TIE
   MetricsArgs none = ma;
   none.out = nullptr; none.loss_hist = nullptr;
   const size_t n = (size_t)c.R * c.M * c.N;
@@ -1446,7 +1454,8 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
   } else {  // per-bin FFT engine: this rank's units
     const int mode = wrt == SQNGD_WRT_FILTERS ? MODE_ADJ_A : MODE_ADJ_B;
     KP kp = make_kp(ctx, 1);
-    cudaMemsetAsync(ctx->counter, 0, sizeof(int), st);
+    kp.track_tie = ma.tie_scan;
+    cudaMemsetAsync(ctx->counter, 0, (2 + 2 * (size_t)c.R) * sizeof(int), st);
     {
       ProfScope ps(ctx, mode, st);
       with_P(ctx->P, [&](auto Lc) {
@@ -1457,7 +1466,7 @@ static sqngd_status run_loss_grad(sqngd_ctx ctx, const float2* s, const float2* 
     if ((rc = launch_check(ctx, "af adjoint"))) return rc;
     ca.K = c.K; ca.slot_stride = ctx->P; ca.u_lo = kp.u_lo; ca.u_hi = kp.u_hi;
     k_reduce_groups<<<c.R, 1024, 0, st>>>(c.M * c.K, kp.u_lo, kp.u_hi, c.loss_mode, c.beta_or_p, ctx->part, ctx->red,
-                                          multi ? none : ma, ctx->status);
+                                          multi ? none : ma, ctx->status, kp.tiew);
     ctx->launches += 1;
     if (mode == MODE_ADJ_B) {  // single GPU: finalize inside the combine
       ca.len = c.N; ca.extra = 1.0; ca.fin = multi ? 0 : 1; ca.out = multi ? ctx->red_grad : nullptr;

@@ -19,6 +19,7 @@ WRT_FILTERS, WRT_TRANSMIT = 1, 2
 BLOCK_A, BLOCK_B, BLOCK_AB = 1, 2, 3
 LOSS_MAX, LOSS_LSE, LOSS_PNORM = 0, 1, 2
 ENGINE_AUTO, ENGINE_FFT, ENGINE_CHEBYSHEV = 0, 1, 2
+FLAG_NO_CROSS, FLAG_TIE, FLAG_DOPPLER_ALIAS = 1, 2, 4  # sqngd_metrics.flags (include/sqngd.h)
 
 
 class SqngdError(RuntimeError):

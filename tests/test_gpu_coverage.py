@@ -188,12 +188,58 @@ def test_argmax_tie_identical_channels(engine):
     assert np.array_equal(am[0, 0, 0], am[0, 1, 1]) and np.array_equal(am[0, 0, 1], am[0, 1, 0])
     assert m["argmax_auto"][:2] == (0, 0) and m["argmax_cross"][:2] == (0, 1), (m["argmax_auto"], m["argmax_cross"])
     assert ref[0]["argmax_auto"][:2] == (0, 0) and ref[0]["argmax_cross"][:2] == (0, 1)
+    # SQNGD_FLAG_TIE (the tied maxima sit in different evaluation units of both engines)
+    assert ref[0]["flags"] & sqngd.FLAG_TIE and m["flags"] & sqngd.FLAG_TIE
     v = np.abs(A[0, 0]) / c.N
     tau = np.arange(-(c.N - 1), c.N)
     for mp, key in ((v[0][:, tau != 0], "argmax_auto"), (v[1], "argmax_cross")):
         vals = np.sort(mp.ravel())[::-1]
         if vals[0] - vals[1] > 1e-5 * vals[0]:
             assert m[key] == ref[0][key], (key, m[key], ref[0][key])
+
+
+def _second_gap(A, c, auto):
+    """Relative gap between the largest and the largest strictly smaller value of a category (fp64)."""
+    v = np.abs(A[0]) / c.N
+    tau = np.arange(-(c.N - 1), c.N)
+    roi = (tau >= c.tau_lo) & (tau <= c.tau_hi)
+    vals = np.concatenate([v[a, b][:, roi & ((tau != 0) if a == b else True)].ravel()
+                           for a in range(c.M) for b in range(c.M) if (a == b) == auto])
+    top = vals.max()
+    rest = vals[vals < top]
+    return (top - rest.max()) / top if rest.size else 1.0
+
+
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_tie_flag_vs_oracle(engine):
+    """SQNGD_FLAG_TIE against the oracle's exact count of maximal cells (Q17).  (i) generic mismatched
+    pairs: no tie on either side; (ii) M = 3 with w_1 = w_2 and the ROI on tau >= 1: the maps (m, 1)
+    and (m, 2) are the same arithmetic on both sides (inside one FFT-engine unit (m, k) for the cross
+    pair (0, 1) / (0, 2), in different Chebyshev units), so every tie is exact and the flags must agree;
+    cases whose distinct values lie within 1e-5 of each other are skipped (an fp32 near-tie)."""
+    flagged = 0
+    for seed in range(4):
+        for dup in (False, True):
+            c = Cfg("tf", M=3, N=120, B=4, K=17, f_lo=-0.5, f_hi=0.5, loss_mode=CF.LOSS_MAX, beta_or_p=0.0,
+                    doppler_engine=ENGINES[engine], tau_lo=1 if dup else -119, tau_hi=119)
+            s = np.exp(2j * np.pi * inputs.phase_params(1, c.M, c.N, config_index=80 + seed).astype(np.float64))
+            w = s * np.exp(1j * 0.5 * inputs.random_complex(s.shape, 90 + seed).real)
+            if dup:
+                w[0, 2] = w[0, 1]
+            s, w = s.astype(np.complex64), w.astype(np.complex64)
+            ref, _, A = O.af(c, s, w, want_A=True)
+            if min(_second_gap(A, c, True), _second_gap(A, c, False)) < 1e-5 and not ref[0]["flags"] & 2:
+                continue
+            ctx = sqngd.Context(c)
+            met, _, _ = ctx.af_forward(T(s), T(w))
+            ctx.sync()
+            m = ctx.metrics(met)[0]
+            assert bool(m["flags"] & sqngd.FLAG_TIE) == bool(ref[0]["flags"] & 2), (seed, dup, m, ref[0])
+            if not dup:
+                assert not ref[0]["flags"] & 2
+            flagged += bool(ref[0]["flags"] & 2)
+    assert flagged >= 1
+    record("tie flag cases flagged", flagged, 0)
 
 
 @pytest.mark.parametrize("engine", ["fft", "cheb"])

@@ -149,6 +149,34 @@ def test_barker13_pslr():
     assert abs(side.max() - 1.0) < 1e-12
 
 
+def test_tie_flag_barker13_and_constructions():
+    """Flag 2 (SQNGD_FLAG_TIE): the maximum is attained by more than one cell.
+    Barker-13 at zero Doppler has its 12 unit sidelobes exactly tied (integer sums, exact in fp64);
+    two identical channels tie their auto maps (and their cross maps); a generic random pair does not."""
+    lines = [l for l in open(os.path.join(GOLD, "barker13.txt")) if not l.startswith("#")]
+    code = np.array([float(x) for x in lines[0].split()]).reshape(1, 1, 13).astype(complex)
+    met, _, _ = O.af(cfg(N=13), code, code)
+    assert met[0]["flags"] & 2
+    s1 = np.exp(2j * np.pi * np.random.default_rng(5).random(40))
+    w1 = s1 * np.exp(0.3j * np.arange(40) ** 0.5)
+    s = np.stack([s1, s1])[None]
+    w = np.stack([w1, w1])[None]
+    met, _, _ = O.af(cfg(M=2, N=40, K=7, f_lo=-0.5, f_hi=0.5), s, w)
+    assert met[0]["flags"] & 2 and met[0]["argmax_auto"][:2] == (0, 0)
+    # (mismatched: with w = s the auto maps' |A(-tau, -f)| = |A(tau, f)| symmetry ties them too)
+    met, _, _ = O.af(cfg(M=2, N=40, K=7, f_lo=-0.5, f_hi=0.5), rnd((1, 2, 40), 91), rnd((1, 2, 40), 93))
+    assert not met[0]["flags"] & 2
+    met, _, _ = O.af(cfg(M=2, N=40, K=7, f_lo=-0.5, f_hi=0.5), s, s.copy())
+    assert met[0]["flags"] & 2
+    # one tied pair planted by symmetry: a real code's |A(tau, -f)| = |A(tau, f)|, and the grid is symmetric
+    x = np.sign(rnd((1, 1, 31), 92).real).astype(complex)
+    met, _, A = O.af(cfg(N=31, K=5, f_lo=-0.5, f_hi=0.5, exclude_auto_zero_delay=1), x, x, want_A=True)
+    v = np.abs(A[0, 0, 0]).copy()
+    v[:, 30] = -1
+    n_max = int(np.sum(v == v.max()))
+    assert n_max >= 2 and bool(met[0]["flags"] & 2) == (n_max >= 2)
+
+
 def test_snrl_and_targets():
     g = golden_values("spec_examples.txt")
     # Eq. 10 via p_m: SNRL = 10 log10(||x||^2 ||h||^2 / (N p)^2)
