@@ -167,6 +167,30 @@ sqngd_loopback sqngd_loopback_create(int world); /* NULL if world is outside 2..
 void sqngd_loopback_destroy(sqngd_loopback group);
 sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqngd_loopback group, int rank,
                                    sqngd_ctx* out);
+/* The loopback group's reduction kernel.  on = 0 (default): one plain reduction kernel.  on = 1: the
+   peer-memory all-reduce kernel below (k_peer_allreduce) over windows of the group's contexts, its
+   signal phase launched for every rank and then its wait + reduce phase for every rank on one stream
+   (every wait already satisfied), so the kernel that runs between GPUs is validated on one device. */
+sqngd_status sqngd_loopback_set_peer(sqngd_loopback group, int on);
+
+/* In-kernel all-reduce over NVLink peer memory instead of NCCL (DESIGN.md §7
+   "In-kernel all-reduce"; no passage of the paper, which is single-GPU).  For a context created
+   with world >= 1 and an ncclUniqueId:
+     sqngd_peer_export  allocates this rank's window (epochs, flags, a double-buffered stage of the
+                        grouped payload) and writes its 64-byte CUDA IPC handle to handle64 (host);
+     sqngd_peer_attach  handles = world x 64 bytes (host), rank-major, every rank's exported handle
+                        (exchanged by the caller, e.g. torch.distributed.all_gather_object); maps the
+                        peers' windows, drops the step graphs captured so far and replaces the NCCL
+                        backend: from then on every evaluation's grouped collective is ONE kernel of
+                        this library (stage + signal over NVLink, wait, rank-ordered sum / max read from
+                        the peers' stages; identical bits on every rank), captured in the step graph.
+   Ranks must be separate processes on P2P-capable devices of one node (CUDA IPC); every rank calls
+   both functions before its next evaluation.  A rank that never signals makes the waiting kernels
+   give up after 30 s: SQNGD_E_NCCL from sqngd_sync, the context is unusable afterwards.
+   SQNGD_E_INVALID: not a multi-GPU context / attach before export; SQNGD_E_CUDA: IPC mapping failed
+   (the NCCL backend stays in place). */
+sqngd_status sqngd_peer_export(sqngd_ctx ctx, void* handle64);
+sqngd_status sqngd_peer_attach(sqngd_ctx ctx, const void* handles);
 void sqngd_destroy(sqngd_ctx ctx);
 /* Message for the last non-OK status (ctx may be NULL: last create error). */
 const char* sqngd_last_error(sqngd_ctx ctx);

@@ -93,6 +93,180 @@ struct NcclComm : Comm {
   }
 };
 
+// ------------------------------------------------------------------------------- peer memory
+// The same grouped all-reduce as ONE kernel of our own over NVLink peer memory (SURVEY §8(f) NEXT-4,
+// DESIGN.md §7 "In-kernel all-reduce").  Every rank owns a WINDOW (one cudaMalloc, exported with
+// cudaIpcGetMemHandle and mapped by its peers):
+//   [ epoch[kPeerBlocks] | flag[kPeerMax][kPeerBlocks] | stage[2][cap_sum doubles + cap_max u64] ]
+// Block b of k_peer_allreduce owns slice b of the payload on every rank (same grid on every rank):
+//   phase A  e = epoch[b] + 1;  copy slice b of (sum, mx) into the own stage[e & 1];  fence;  store e
+//            into flag[rank][b] of EVERY rank's window (st.release.sys over NVLink);
+//   phase B  wait until the own flag[r][b] >= e for every r (ld.acquire.sys, clock watchdog);  read slice b
+//            of every rank's stage[e & 1] (own rank locally, peers over NVLink, L1 bypassed) and write
+//            sum_r / max_r in RANK ORDER into the caller's buffers (bit-identical on every rank);
+//            epoch[b] = e.
+// A peer can be at most one epoch ahead (its epoch e + 1 wait needs this rank's e + 1 signal), so the two
+// stage parities suffice and the flags only grow.  No host-side argument changes between calls (the
+// epoch lives in the window), so the launch replays inside the step's CUDA graph.  A block waits only on
+// the same-numbered block of its peers, never on a block of its own grid.
+constexpr int kPeerMax = 8;
+constexpr int kPeerBlocks = 128;
+struct PeerArgs {
+  unsigned char* win[kPeerMax];  // every rank's window, as mapped into this process
+  int world, rank;
+  size_t cap_sum, cap_max;       // stage capacity (elements), identical on every rank
+  int* status;                   // the context's latched device status (bit 16: peer wait timed out)
+};
+__host__ __device__ inline size_t peer_flags_bytes() { return sizeof(unsigned long long) * (size_t)(1 + kPeerMax) * kPeerBlocks; }
+__host__ __device__ inline size_t peer_stage_bytes(size_t cap_sum, size_t cap_max) { return 8 * (cap_sum + cap_max); }
+__host__ __device__ inline size_t peer_window_bytes(size_t cap_sum, size_t cap_max) {
+  return peer_flags_bytes() + 2 * peer_stage_bytes(cap_sum, cap_max);
+}
+constexpr int kPeerPhaseA = 1, kPeerPhaseB = 2;
+constexpr int kPeerTimeoutBit = 1 << 16;
+
+__device__ __forceinline__ void peer_st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long peer_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long peer_ld_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_peer_allreduce(PeerArgs a, double* sum, size_t nsum, unsigned long long* mx,
+                                                        size_t nmax, int phases, unsigned long long timeout_ns) {
+  typedef unsigned long long u64;
+  const int b = blockIdx.x, nb = gridDim.x, t = threadIdx.x;
+  u64* own = reinterpret_cast<u64*>(a.win[a.rank]);
+  const u64 e = own[b] + 1;  // epoch[b]: written only by this block's previous launch
+  const size_t stage_off = peer_flags_bytes() + (size_t)(e & 1) * peer_stage_bytes(a.cap_sum, a.cap_max);
+  const size_t cs = (nsum + nb - 1) / nb, cm = (nmax + nb - 1) / nb;
+  const size_t s0 = min(nsum, (size_t)b * cs), s1 = min(nsum, s0 + cs);
+  const size_t m0 = min(nmax, (size_t)b * cm), m1 = min(nmax, m0 + cm);
+  if (phases & kPeerPhaseA) {
+    u64* st_sum = reinterpret_cast<u64*>(a.win[a.rank] + stage_off);
+    u64* st_max = st_sum + a.cap_sum;
+    const u64* src = reinterpret_cast<const u64*>(sum);
+    for (size_t i = s0 + t; i < s1; i += blockDim.x) st_sum[i] = src[i];
+    for (size_t i = m0 + t; i < m1; i += blockDim.x) st_max[i] = mx[i];
+    __threadfence_system();
+    __syncthreads();
+    if (t < a.world)
+      peer_st_release(reinterpret_cast<u64*>(a.win[t]) + (size_t)(1 + a.rank) * kPeerBlocks + b, e);
+  }
+  if (phases & kPeerPhaseB) {
+    __shared__ int timed_out;
+    if (t == 0) timed_out = 0;
+    __syncthreads();
+    if (t < a.world) {
+      const u64* f = own + (size_t)(1 + t) * kPeerBlocks + b;
+      u64 t0 = 0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while (peer_ld_acquire(f) < e) {
+        u64 t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > timeout_ns) {  // a peer never signalled: latch the error, do not hang the GPU
+          timed_out = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    if (timed_out) {
+      if (t == 0) atomicOr(a.status, kPeerTimeoutBit);
+      return;  // epoch[b] is not advanced: the context is unusable after a timeout (sqngd_sync reports it)
+    }
+    for (size_t i = s0 + t; i < s1; i += blockDim.x) {
+      double s = 0.0;
+      for (int r = 0; r < a.world; ++r)  // fixed rank order
+        s += __longlong_as_double((long long)peer_ld_u64(reinterpret_cast<const u64*>(a.win[r] + stage_off) + i));
+      sum[i] = s;
+    }
+    for (size_t i = m0 + t; i < m1; i += blockDim.x) {
+      u64 m = 0ull;
+      for (int r = 0; r < a.world; ++r) {
+        const u64 v = peer_ld_u64(reinterpret_cast<const u64*>(a.win[r] + stage_off) + a.cap_sum + i);
+        m = v > m ? v : m;
+      }
+      mx[i] = m;
+    }
+    __syncthreads();
+    if (t == 0) own[b] = e;
+  }
+}
+
+inline int peer_grid(size_t nsum, size_t nmax) {
+  const size_t n = nsum > nmax ? nsum : nmax;
+  const size_t g = (n + 1023) / 1024;  // >= 4 elements per thread before another block is worth its flags
+  return (int)(g < 1 ? 1 : (g > (size_t)kPeerBlocks ? (size_t)kPeerBlocks : g));
+}
+
+// One rank's window: allocated zeroed (epoch 0, flags 0), exported / attached through CUDA IPC.
+struct PeerWindow {
+  unsigned char* base = nullptr;
+  size_t cap_sum = 0, cap_max = 0;
+  cudaError_t alloc(size_t cs, size_t cm) {
+    cap_sum = cs;
+    cap_max = cm;
+    cudaError_t e = cudaMalloc(&base, peer_window_bytes(cs, cm));
+    if (e != cudaSuccess) return e;
+    return cudaMemset(base, 0, peer_window_bytes(cs, cm));
+  }
+  void release() {
+    if (base) cudaFree(base);
+    base = nullptr;
+  }
+};
+
+struct PeerComm : Comm {
+  PeerWindow own;
+  PeerArgs args{};
+  bool opened[kPeerMax] = {};
+  unsigned long long timeout_ns = 30ull * 1000000000ull;
+  // handles: world x CUDA_IPC_HANDLE_SIZE bytes, rank-major, every rank's exported window (this rank's
+  // own entry is ignored: the local pointer is used).
+  bool attach(const void* handles, int rank, int world, int* status, std::string* why) {
+    if (world < 1 || world > kPeerMax || !own.base) { *why = "peer attach: world outside 1..8 or no window"; return false; }
+    args.world = world;
+    args.rank = rank;
+    args.cap_sum = own.cap_sum;
+    args.cap_max = own.cap_max;
+    args.status = status;
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) { args.win[r] = own.base; continue; }
+      cudaIpcMemHandle_t h;
+      memcpy(&h, (const char*)handles + (size_t)r * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) { *why = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e); return false; }
+      args.win[r] = (unsigned char*)p;
+      opened[r] = true;
+    }
+    return true;
+  }
+  bool allreduce(double* sum, size_t nsum, unsigned long long* mx, size_t nmax, cudaStream_t st,
+                 std::string* why) override {
+    if (nsum > own.cap_sum || nmax > own.cap_max) { *why = "peer all-reduce: payload larger than the window"; return false; }
+    k_peer_allreduce<<<peer_grid(nsum, nmax), 256, 0, st>>>(args, sum, nsum, mx, nmax, kPeerPhaseA | kPeerPhaseB, timeout_ns);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { *why = cudaGetErrorString(e); return false; }
+    return true;
+  }
+  bool capturable() const override { return true; }
+  void destroy() override {
+    for (int r = 0; r < kPeerMax; ++r)
+      if (opened[r]) { cudaIpcCloseMemHandle(args.win[r]); opened[r] = false; }
+    own.release();
+  }
+};
+
 // ------------------------------------------------------------------------------- loopback
 constexpr int kLoopMax = 8;
 struct LoopPtrs {
@@ -124,6 +298,13 @@ struct LoopGroup {
   cudaEvent_t done = nullptr;
   size_t nsum = 0, nmax = 0;
   std::string err;
+  // peer mode (sqngd_loopback_set_peer): the reduction is k_peer_allreduce itself, phase A for every
+  // rank and then phase B for every rank on one stream (every wait is already satisfied: no kernel waits
+  // on another rank's kernel), over windows of the W contexts on this device.
+  bool peer = false;
+  PeerWindow win[kLoopMax];
+  int* status[kLoopMax] = {};
+  size_t cap_sum = 0, cap_max = 0;  // window capacity: the contexts' largest payload
   bool init(int w) {
     world = w;
     for (int r = 0; r < w; ++r)
@@ -134,15 +315,20 @@ struct LoopGroup {
     for (int r = 0; r < world; ++r)
       if (ready[r]) cudaEventDestroy(ready[r]);
     if (done) cudaEventDestroy(done);
+    for (int r = 0; r < world; ++r) win[r].release();
   }
 };
 
 struct LoopComm : Comm {
   LoopGroup* g = nullptr;
   int rank = 0;
+  int* status = nullptr;
+  size_t cap_sum = 0, cap_max = 0;
   bool allreduce(double* sum, size_t nsum, unsigned long long* mx, size_t nmax, cudaStream_t st,
                  std::string* why) override {
     std::unique_lock<std::mutex> lk(g->mu);
+    if (cap_sum > g->cap_sum) g->cap_sum = cap_sum;
+    if (cap_max > g->cap_max) g->cap_max = cap_max;
     if (g->arrived == 0) {
       g->nsum = nsum;
       g->nmax = nmax;
@@ -152,6 +338,7 @@ struct LoopComm : Comm {
     }
     g->ptrs.sum[rank] = sum;
     g->ptrs.mx[rank] = mx;
+    g->status[rank] = status;
     cudaEventRecord(g->ready[rank], st);
     const long long gen = g->generation;
     if (++g->arrived == g->world) {  // last to arrive: reduce on this stream, release the others
@@ -159,7 +346,27 @@ struct LoopComm : Comm {
         for (int r = 0; r < g->world; ++r) cudaStreamWaitEvent(st, g->ready[r], 0);
         const size_t n = nsum > nmax ? nsum : nmax;
         const int blocks = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
-        k_loop_reduce<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(g->ptrs, g->world, nsum, nmax);
+        if (g->peer) {
+          for (int r = 0; r < g->world && g->err.empty(); ++r)
+            if (!g->win[r].base && g->win[r].alloc(g->cap_sum, g->cap_max) != cudaSuccess)
+              g->err = "loopback: peer window allocation";
+          if (g->err.empty() && (nsum > g->win[0].cap_sum || nmax > g->win[0].cap_max))
+            g->err = "loopback: payload larger than the peer windows";
+          for (int ph = kPeerPhaseA; ph <= kPeerPhaseB && g->err.empty(); ph <<= 1)
+            for (int r = 0; r < g->world; ++r) {
+              PeerArgs a{};
+              for (int q = 0; q < g->world; ++q) a.win[q] = g->win[q].base;
+              a.world = g->world;
+              a.rank = r;
+              a.cap_sum = g->win[0].cap_sum;
+              a.cap_max = g->win[0].cap_max;
+              a.status = g->status[r];
+              k_peer_allreduce<<<peer_grid(nsum, nmax), 256, 0, st>>>(a, g->ptrs.sum[r], nsum, g->ptrs.mx[r], nmax, ph,
+                                                                       2000000000ull);
+            }
+        } else {
+          k_loop_reduce<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(g->ptrs, g->world, nsum, nmax);
+        }
         cudaEventRecord(g->done, st);
       }
       g->arrived = 0;

@@ -142,6 +142,7 @@ struct sqngd_ctx_s {
   float2* tslot = nullptr;     // [R M Q][N] Step-B node time-domain partials
   // multi-GPU (comm.h): this rank's shard, the grouped collective's buffers, the reference shifts
   Comm* comm = nullptr;
+  PeerComm* peer_pending = nullptr;  // window exported (sqngd_peer_export), not yet attached
   int row_lo = 0, row_hi = 0;   // Chebyshev engine: (restart, transmit channel) rows [row_lo, row_hi)
   double* pay = nullptr;        // [R][1 + 2 M N] fp64 SUM payload
   unsigned long long* keyb = nullptr;  // [R][3] u64 MAX payload
@@ -174,6 +175,18 @@ struct sqngd_ctx_s {
     cudaKernelNodeParams set_p{};
   };
   std::vector<GraphEntry*> graphs;
+  void drop_graphs() {
+    for (auto* g : graphs) {
+      if (g->exec) cudaGraphExecDestroy(g->exec);
+      if (g->graph) cudaGraphDestroy(g->graph);
+      for (auto& mk : g->marks) {
+        cudaEventDestroy(std::get<1>(mk));
+        cudaEventDestroy(std::get<2>(mk));
+      }
+      delete g;
+    }
+    graphs.clear();
+  }
   GraphEntry* capturing = nullptr;
   bool use_graphs = true;
   // profiling
@@ -1001,6 +1014,9 @@ static sqngd_status create_impl(const sqngd_config* cfgp, int cuda_device, const
       LoopComm* lc = new LoopComm();
       lc->g = group;
       lc->rank = rank;
+      lc->status = ctx->status;
+      lc->cap_sum = (size_t)cfg.R * (1 + 2 * (size_t)cfg.M * cfg.N);
+      lc->cap_max = (size_t)3 * cfg.R;
       ctx->comm = lc;
     } else {
       if (!nccl_unique_id) {
@@ -1042,6 +1058,58 @@ sqngd_loopback sqngd_loopback_create(int world) {
 
 void sqngd_loopback_destroy(sqngd_loopback lb) { delete lb; }
 
+sqngd_status sqngd_loopback_set_peer(sqngd_loopback lb, int on) {
+  if (!lb) return fail(nullptr, SQNGD_E_INVALID, "sqngd_loopback_set_peer: null group");
+  std::unique_lock<std::mutex> lk(lb->g.mu);
+  lb->g.peer = on != 0;
+  return SQNGD_OK;
+}
+
+sqngd_status sqngd_peer_export(sqngd_ctx ctx, void* handle64) {
+  if (!ctx || !handle64) return fail(ctx, SQNGD_E_INVALID, "sqngd_peer_export: null argument");
+  if (!ctx->multi || !ctx->comm) return fail(ctx, SQNGD_E_INVALID, "sqngd_peer_export: not a multi-GPU context");
+  CK(cudaSetDevice(ctx->dev));
+  if (!ctx->peer_pending) {
+    ctx->peer_pending = new PeerComm();
+    const sqngd_config& c = ctx->cfg;
+    cudaError_t e = ctx->peer_pending->own.alloc((size_t)c.R * (1 + 2 * (size_t)c.M * c.N), (size_t)3 * c.R);
+    if (e != cudaSuccess) {
+      delete ctx->peer_pending;
+      ctx->peer_pending = nullptr;
+      return fail(ctx, SQNGD_E_NOMEM, "sqngd_peer_export: window", cudaGetErrorString(e));
+    }
+    CK(cudaDeviceSynchronize());
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->peer_pending->own.base));
+  memcpy(handle64, &h, sizeof(h));
+  return SQNGD_OK;
+}
+
+sqngd_status sqngd_peer_attach(sqngd_ctx ctx, const void* handles) {
+  if (!ctx || !handles) return fail(ctx, SQNGD_E_INVALID, "sqngd_peer_attach: null argument");
+  if (!ctx->peer_pending) return fail(ctx, SQNGD_E_INVALID, "sqngd_peer_attach: call sqngd_peer_export first");
+  CK(cudaSetDevice(ctx->dev));
+  std::string why;
+  if (!ctx->peer_pending->attach(handles, ctx->rank, ctx->world, ctx->status, &why)) {
+    ctx->peer_pending->destroy();
+    delete ctx->peer_pending;
+    ctx->peer_pending = nullptr;
+    return fail(ctx, SQNGD_E_CUDA, "sqngd_peer_attach", why.c_str());
+  }
+  CK(cudaDeviceSynchronize());
+  // the step graphs captured so far hold the previous backend's collective: drop them
+  ctx->drop_graphs();
+  if (ctx->comm) {
+    ctx->comm->destroy();
+    delete ctx->comm;
+  }
+  ctx->comm = ctx->peer_pending;
+  ctx->peer_pending = nullptr;
+  return SQNGD_OK;
+}
+
 sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqngd_loopback group, int rank,
                                    sqngd_ctx* out) {
   if (!group) return fail(nullptr, SQNGD_E_INVALID, "sqngd_create_loopback: null group");
@@ -1074,14 +1142,11 @@ sqngd_status sqngd_check_guards(sqngd_ctx ctx, int64_t* corrupted) {
 void sqngd_destroy(sqngd_ctx ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
-  for (auto* g : ctx->graphs) {
-    if (g->exec) cudaGraphExecDestroy(g->exec);
-    if (g->graph) cudaGraphDestroy(g->graph);
-    for (auto& mk : g->marks) {
-      cudaEventDestroy(std::get<1>(mk));
-      cudaEventDestroy(std::get<2>(mk));
-    }
-    delete g;
+  ctx->drop_graphs();
+  if (ctx->peer_pending) {
+    ctx->peer_pending->destroy();
+    delete ctx->peer_pending;
+    ctx->peer_pending = nullptr;
   }
   void* ptrs[] = {ctx->tabB, ctx->snrl_w, ctx->d_ct, ctx->d_t, ctx->tw, ctx->H, ctx->Xc, ctx->ftw, ctx->part.scale, ctx->counter, ctx->spec, ctx->s_soft, ctx->s_hard, ctx->dq, ctx->lut, ctx->part.key, ctx->part.m,
                   ctx->part.S, ctx->part.g, ctx->red, ctx->cm, ctx->red_grad, ctx->dy,
@@ -1163,6 +1228,7 @@ sqngd_status sqngd_sync(sqngd_ctx ctx, sqngd_stream stream) {
   if (st & ST_NONFINITE) return fail(ctx, SQNGD_E_NONFINITE, "non-finite loss or gradient");
   if (st & ST_DEGENERATE) return fail(ctx, SQNGD_E_DEGENERATE, "degenerate mainlobe or zero-energy filter");
   if (st & ST_INVALID) return fail(ctx, SQNGD_E_INVALID, "thresholds rho not ascending");
+  if (st & kPeerTimeoutBit) return fail(ctx, SQNGD_E_NCCL, "peer all-reduce: a rank did not signal in time");
   return SQNGD_OK;
 }
 

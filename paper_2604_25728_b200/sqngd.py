@@ -139,6 +139,12 @@ def lib():
         L.sqngd_loopback_create.argtypes = [i32]
         L.sqngd_loopback_destroy.restype = None
         L.sqngd_loopback_destroy.argtypes = [vp]
+        L.sqngd_loopback_set_peer.restype = i32
+        L.sqngd_loopback_set_peer.argtypes = [vp, i32]
+        L.sqngd_peer_export.restype = i32
+        L.sqngd_peer_export.argtypes = [vp, vp]
+        L.sqngd_peer_attach.restype = i32
+        L.sqngd_peer_attach.argtypes = [vp, vp]
         L.sqngd_create_loopback.restype = i32
         L.sqngd_create_loopback.argtypes = [C.POINTER(Config), i32, vp, i32, C.POINTER(vp)]
         L.sqngd_version.restype = C.c_char_p
@@ -152,7 +158,8 @@ EXPORTED = ["sqngd_create", "sqngd_destroy", "sqngd_last_error", "sqngd_sync", "
             "sqngd_profile_enable", "sqngd_profile_read",
             "sqngd_num_units", "sqngd_shard_range", "sqngd_version", "sqngd_engine_info",
             "sqngd_net_num_params", "sqngd_net_forward", "sqngd_net_backward", "sqngd_run",
-            "sqngd_loopback_create", "sqngd_loopback_destroy", "sqngd_create_loopback", "sqngd_check_guards"]
+            "sqngd_loopback_create", "sqngd_loopback_destroy", "sqngd_create_loopback", "sqngd_check_guards",
+            "sqngd_loopback_set_peer", "sqngd_peer_export", "sqngd_peer_attach"]
 
 
 def make_config(cfg, weights_ptr: int | None = None, R: int | None = None) -> Config:
@@ -249,11 +256,15 @@ class Loopback:
     """Single-device stand-in for NCCL (include/sqngd.h sqngd_loopback_*): `world` contexts of one process,
     each driven by its own host thread, run the library's sharded multi-GPU path."""
 
-    def __init__(self, world: int):
+    def __init__(self, world: int, peer: bool = False):
         self.world = int(world)
         self.h = lib().sqngd_loopback_create(self.world)
         if not self.h:
             raise SqngdError(E_INVALID, f"sqngd_loopback_create({world})")
+        if peer:  # reduce with the peer-memory all-reduce kernel (phase by phase) instead of the plain one
+            st = lib().sqngd_loopback_set_peer(self.h, 1)
+            if st != OK:
+                raise SqngdError(st, "sqngd_loopback_set_peer")
 
     def close(self):
         if getattr(self, "h", None):
@@ -294,6 +305,22 @@ class Context:
             raise SqngdError(st, lib().sqngd_last_error(None).decode())
         self.h = h
         self._met = torch.empty(self.R * METRICS_BYTES, dtype=torch.uint8, device=self.device)
+
+    def enable_peer_allreduce(self, rank: int = 0, world: int = 1):
+        """Replace the NCCL backend by the library's own in-kernel all-reduce over peer memory
+        (sqngd_peer_export / sqngd_peer_attach): the window handles are exchanged with
+        torch.distributed.all_gather_object when world > 1 (argument marshalling only)."""
+        mine = C.create_string_buffer(64)
+        with self.torch.cuda.device(self.device):
+            self._check(lib().sqngd_peer_export(self.h, mine))
+            handles = [mine.raw]
+            if world > 1:
+                import torch.distributed as dist
+
+                handles = [None] * world
+                dist.all_gather_object(handles, mine.raw)
+            buf = C.create_string_buffer(b"".join(handles), 64 * world)
+            self._check(lib().sqngd_peer_attach(self.h, buf))
 
     def close(self):
         if getattr(self, "h", None):

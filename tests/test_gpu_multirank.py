@@ -31,9 +31,10 @@ def T(a):
     return torch.as_tensor(np.ascontiguousarray(a), device=DEV)
 
 
-def on_ranks(cfg, world, fn):
-    """fn(ctx, rank) on `world` loopback contexts, one thread + stream each; returns the per-rank results."""
-    lb = sqngd.Loopback(world)
+def on_ranks(cfg, world, fn, peer=False):
+    """fn(ctx, rank) on `world` loopback contexts, one thread + stream each; returns the per-rank results.
+    peer: the group reduces with the in-kernel peer-memory all-reduce (k_peer_allreduce) phase by phase."""
+    lb = sqngd.Loopback(world, peer=peer)
     ctxs = [sqngd.Context(cfg, loopback=lb, rank=r) for r in range(world)]
     out, errs = [None] * world, []
 
@@ -216,3 +217,108 @@ def test_nccl_one_rank_collective_path(engine, mode):
     np.testing.assert_allclose(res["nccl"]["hist"], res["single"]["hist"], rtol=1e-6)
     np.testing.assert_allclose(res["nccl"]["w"], res["single"]["w"], rtol=0, atol=1e-5)
     np.testing.assert_allclose(res["nccl"]["z"], res["single"]["z"], rtol=0, atol=1e-6)
+
+
+# ------------------------------------------------- in-kernel all-reduce over peer memory (NEXT-4)
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", ["lse", "max"])
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_peer_allreduce_kernel_in_loopback(engine, mode, world):
+    """k_peer_allreduce (stage + flag signal, flag wait, rank-ordered read of every rank's stage) as the
+    loopback group's reduction, its two phases launched rank by rank (no kernel waits on another): the
+    sharded results must equal the plain loopback reduction BIT FOR BIT (both sum in rank order), stay
+    identical across ranks, and match the oracle.  Two evaluations per rank and call site use both
+    stage parities and growing epochs."""
+    lm, bp = MODES[mode]
+    c = CASES[1].with_(loss_mode=lm, beta_or_p=bp, doppler_engine=ENGINES[engine])
+    z, rho, q, w = inputs_for(c, 95)
+
+    def twice(ctx, r):
+        eval_all(ctx, z, rho, w)
+        return eval_all(ctx, z, rho, w)
+
+    res = on_ranks(c, world, twice, peer=True)
+    plain = on_ranks(c, world, twice, peer=False)
+    for r in range(world):
+        for k in ("gw", "gz", "gr", "p"):
+            assert np.array_equal(res[r][k], plain[0][k]), (r, k)
+        for k in ("mf", "mA", "mB"):
+            assert repr(res[r][k]) == repr(plain[0][k]), (r, k)
+    _, gw_ref, _ = O.loss_grad(c, q["s_hard"], w, want_s=False)
+    _, _, gs_ref = O.loss_grad(c, q["s_soft"], w, want_w=False)
+    gz_ref, gr_ref = O.chain(c, z, rho, q["s_soft"], gs_ref)
+    check_grad(res[0]["gw"], gw_ref, "peer all-reduce grad_w")
+    check_grad(res[0]["gz"], gz_ref, "peer all-reduce grad_z")
+    check_grad(res[0]["gr"], gr_ref, "peer all-reduce grad_rho")
+
+
+def test_peer_allreduce_c5_payload_8_ranks():
+    """The peer kernel on a payload that spans all its blocks (C5 shape: 1 + 2 M N = 131073 doubles per
+    restart, 128 blocks) with 8 ranks: bit-identical to the plain loopback reduction."""
+    c = CF.C5.with_(R=1, K=9, loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=sqngd.ENGINE_CHEBYSHEV)
+    z, rho, q, w = inputs_for(c, 5)
+
+    def run(ctx, r):
+        met, gz, gr = ctx.af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
+        m = ctx.metrics(met)
+        ctx.sync()
+        return m, gz.cpu().numpy(), gr.cpu().numpy()
+
+    res = on_ranks(c, 8, run, peer=True)
+    plain = on_ranks(c, 8, run, peer=False)
+    for r in range(8):
+        assert np.array_equal(res[r][1], plain[0][1]) and np.array_equal(res[r][2], plain[0][2])
+        assert repr(res[r][0]) == repr(plain[0][0])
+
+
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_peer_backend_one_rank_single_launch(engine):
+    """The peer backend proper (sqngd_peer_export / sqngd_peer_attach replacing NCCL) at world = 1: the
+    single-launch form of the kernel (signal, wait and reduce in one launch, against its own window),
+    eagerly and captured in the step's CUDA graph over several replays (the epoch lives in the window,
+    so replays need no new arguments).  Must equal the 1-rank NCCL path bit for bit."""
+    c = CASES[1].with_(loss_mode=CF.LOSS_LSE, beta_or_p=60.0, doppler_engine=ENGINES[engine])
+    z, rho, q, w = inputs_for(c, 97)
+    res = {}
+    for name in ("peer", "nccl"):
+        ctx = sqngd.Context(c, nccl_uid=sqngd.nccl_unique_id(), rank=0, world=1)
+        if name == "peer":
+            ctx.enable_peer_allreduce()
+        eval_all(ctx, z, rho, w)
+        res[name] = eval_all(ctx, z, rho, w)
+        ctx.close()
+    for k in ("gw", "gz", "gr", "p"):
+        assert np.array_equal(res["peer"][k], res["nccl"][k]), k
+    cs = c.with_(n_h=2, n_x=2, lr_z=1e-3)
+    wq = q["s_hard"].astype(np.complex64)
+    out = {}
+    for name in ("peer", "nccl"):
+        cx = sqngd.Context(cs, nccl_uid=sqngd.nccl_unique_id(), rank=0, world=1)
+        if name == "peer":
+            cx.enable_peer_allreduce()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            st = cx.new_state(T(z), T(rho), T(wq))
+            hist = torch.zeros((cs.R, cs.n_h + cs.n_x), dtype=torch.float64, device=DEV)
+            for _ in range(4):
+                cx.step(st, sqngd.BLOCK_AB, hist=hist)
+        s.synchronize()
+        cx.sync()
+        out[name] = {k: st[k].cpu().numpy() for k in ("z", "rho", "w")} | {"hist": hist.cpu().numpy()}
+        cx.close()
+    for k in ("z", "rho", "w", "hist"):
+        assert np.array_equal(out["peer"][k], out["nccl"][k]), k
+
+
+def test_peer_attach_errors():
+    """attach before export, and export on a single-GPU context, are rejected (SQNGD_E_INVALID)."""
+    import ctypes as C
+
+    c = CASES[0].with_(loss_mode=CF.LOSS_LSE, beta_or_p=60.0)
+    plain = sqngd.Context(c)
+    buf = C.create_string_buffer(64)
+    assert sqngd.lib().sqngd_peer_export(plain.h, buf) == sqngd.E_INVALID
+    plain.close()
+    ctx = sqngd.Context(c, nccl_uid=sqngd.nccl_unique_id(), rank=0, world=1)
+    assert sqngd.lib().sqngd_peer_attach(ctx.h, buf) == sqngd.E_INVALID
+    ctx.close()
