@@ -278,20 +278,25 @@ def work_sharded(args, world, rank, local, dev, stream, flush, name="C5"):
     from paper_2604_25728_b200 import sqngd
 
     c = CF.CONFIGS[name].with_(loss_mode=CF.LOSS_LSE, beta_or_p=200.0)
-    uid = None
-    if world > 1:
+    def fresh_uid():  # one ncclUniqueId per communicator, rank 0's, broadcast
+        if world == 1:
+            return None
         import torch.distributed as dist
 
         obj = [sqngd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        return obj[0]
+
+    uid = fresh_uid()
     z = np.stack([inputs.uniform01_f32(inputs.config_seed(c.index, r), c.M * c.N).reshape(c.M, c.N)
                   for r in range(c.R)])
     rho = inputs.init_thresholds(c.R, c.B, c.r_n)
     steps, warm = max(2, min(args.steps, 5)), max(3, min(args.warmup, 3))
 
-    def run(uid_):
+    def run(uid_, peer=False):
         ctx = sqngd.Context(c, device=local, nccl_uid=uid_, rank=rank, world=world)
+        if peer:  # the library's own in-kernel all-reduce over peer memory instead of NCCL
+            ctx.enable_peer_allreduce(rank, world)
         zt, rt = torch.as_tensor(z, device=dev), torch.as_tensor(rho, device=dev)
         w = ctx.quantize(zt, rt, soft=False, want_b=False, want_dq=False)["s_hard"]
         st = ctx.new_state(zt, rt, w)
@@ -325,6 +330,17 @@ def work_sharded(args, world, rank, local, dev, stream, flush, name="C5"):
         "value": evals / (ms_1r / 1e3), "ms_per_step": ms_1r,
         "what": "the same steps with an ncclUniqueId at world = 1: the sharded path and its grouped NCCL "
                 "all-reduce over a 1-rank communicator"}}
+    # the same sharded steps with the collective as ONE kernel of the library over peer memory
+    # (sqngd_peer_export / sqngd_peer_attach; NEXT-4).  Between ranks it has never run (one GPU per box
+    # here): a failure is reported, the NCCL numbers above stand.
+    try:
+        ms_p = run(fresh_uid() if world > 1 else sqngd.nccl_unique_id(), peer=True)[0]
+        extra["peer_allreduce"] = {
+            "value": evals / (ms_p / 1e3), "ms_per_step": ms_p, "n_gpus": world,
+            "what": "k_peer_allreduce (stage + flag over NVLink peer memory, wait, rank-ordered read) instead of "
+                    "the grouped NCCL call, captured in the step graph" + (" (1 rank: its own window)" if world == 1 else "")}
+    except Exception as e:
+        extra["peer_allreduce"] = {"error": f"{type(e).__name__}: {e}"}
     return {**extra, "workload": f"{name}: M={c.M} N={c.N} L={c.B} K={c.K} R={c.R} (one problem)", "n_gpus": world,
             "value": evals / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
             "scaling": "strong", "engine": info["engine"],
