@@ -171,6 +171,8 @@ sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqn
    peer-memory all-reduce kernel below (k_peer_allreduce) over windows of the group's contexts, its
    signal phase launched for every rank and then its wait + reduce phase for every rank on one stream
    (every wait already satisfied), so the kernel that runs between GPUs is validated on one device. */
+/* on = 2: the fused form (k_world_peer: pack + all-reduce + unpack in one kernel, the default of the
+   peer backend below), again phase by phase. */
 sqngd_status sqngd_loopback_set_peer(sqngd_loopback group, int on);
 
 /* In-kernel all-reduce over NVLink peer memory instead of NCCL (DESIGN.md §7
@@ -182,8 +184,11 @@ sqngd_status sqngd_loopback_set_peer(sqngd_loopback group, int on);
                         (exchanged by the caller, e.g. torch.distributed.all_gather_object); maps the
                         peers' windows, drops the step graphs captured so far and replaces the NCCL
                         backend: from then on every evaluation's grouped collective is ONE kernel of
-                        this library (stage + signal over NVLink, wait, rank-ordered sum / max read from
-                        the peers' stages; identical bits on every rank), captured in the step graph.
+                        this library (k_world_peer: the weighted payload computed straight into the
+                        stage, flag signal over NVLink, wait, rank-ordered sum / max read from the
+                        peers' stages, normalised global gradient and record written; identical bits on
+                        every rank), captured in the step graph.  Environment SQNGD_PEER_FUSED=0 at
+                        attach selects the 3-launch form (pack, k_peer_allreduce, unpack).
    Ranks must be separate processes on P2P-capable devices of one node (CUDA IPC); every rank calls
    both functions before its next evaluation.  A rank that never signals makes the waiting kernels
    give up after 30 s: SQNGD_E_NCCL from sqngd_sync, the context is unusable afterwards.

@@ -14,7 +14,9 @@
 // The fp64 weights cannot overflow for beta |m_r - m_ref| < 700, so the combine is exact (no second
 // round); the restart's loss is m_ref + ln(sum wS) / beta (LSE) or m_ref (sum wS)^{1/p}.
 //
-// Backends: NCCL (dlopen'ed torch-bundled libnccl.so.2; one ncclGroupStart/End around the SUM and the
+// Backends: PEER (below: the collective as one kernel of this library over NVLink peer memory, selected by
+// sqngd_peer_export / sqngd_peer_attach; world_peer.cuh fuses pack and unpack into it),
+// NCCL (dlopen'ed torch-bundled libnccl.so.2; one ncclGroupStart/End around the SUM and the
 // MAX all-reduce; capturable into the step's CUDA graph), and a single-device LOOPBACK group for tests:
 // the W contexts of one process, each driven by its own host thread, meet in a host barrier; the last
 // to arrive makes its stream wait for every rank's event, sums / maxes the W buffers in one kernel
@@ -37,12 +39,17 @@
 
 namespace sq {
 
+struct WorldArgs;  // misc_kernels.cuh
+
 struct Comm {
   virtual ~Comm() {}
   // In-place grouped all-reduce: SUM of nsum doubles, MAX of nmax u64, as one collective call.
   virtual bool allreduce(double* sum, size_t nsum, unsigned long long* mx, size_t nmax, cudaStream_t st,
                          std::string* why) = 0;
   virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
+  // Optional: the whole combine (pack, all-reduce, unpack) as ONE kernel (world_peer.cuh).
+  virtual bool has_fused() const { return false; }
+  virtual bool fused(const WorldArgs*, cudaStream_t, std::string*) { return false; }
   virtual void destroy() {}
 };
 
@@ -230,6 +237,9 @@ struct PeerComm : Comm {
   PeerArgs args{};
   bool opened[kPeerMax] = {};
   unsigned long long timeout_ns = 30ull * 1000000000ull;
+  bool use_fused = true;  // fixed at attach: the fused and the 3-launch form must not share a window
+  bool has_fused() const override { return use_fused; }
+  bool fused(const WorldArgs* wa, cudaStream_t st, std::string* why) override;  // world_peer.cuh
   // handles: world x CUDA_IPC_HANDLE_SIZE bytes, rank-major, every rank's exported window (this rank's
   // own entry is ignored: the local pointer is used).
   bool attach(const void* handles, int rank, int world, int* status, std::string* why) {
@@ -302,6 +312,8 @@ struct LoopGroup {
   // rank and then phase B for every rank on one stream (every wait is already satisfied: no kernel waits
   // on another rank's kernel), over windows of the W contexts on this device.
   bool peer = false;
+  bool peer_fused = false;                   // (peer) the whole combine in k_world_peer, phase by phase
+  const WorldArgs* wargs[kLoopMax] = {};     // (peer_fused) every rank's combine arguments
   PeerWindow win[kLoopMax];
   int* status[kLoopMax] = {};
   size_t cap_sum = 0, cap_max = 0;  // window capacity: the contexts' largest payload
@@ -324,6 +336,8 @@ struct LoopComm : Comm {
   int rank = 0;
   int* status = nullptr;
   size_t cap_sum = 0, cap_max = 0;
+  bool has_fused() const override { return g->peer && g->peer_fused; }
+  bool fused(const WorldArgs* wa, cudaStream_t st, std::string* why) override;  // world_peer.cuh
   bool allreduce(double* sum, size_t nsum, unsigned long long* mx, size_t nmax, cudaStream_t st,
                  std::string* why) override {
     std::unique_lock<std::mutex> lk(g->mu);

@@ -19,6 +19,7 @@
 #include "lr_kernels.cuh"
 #include "lr_tc.cuh"
 #include "misc_kernels.cuh"
+#include "world_peer.cuh"
 #include "net.cuh"
 #include "run.cuh"
 
@@ -1062,6 +1063,7 @@ sqngd_status sqngd_loopback_set_peer(sqngd_loopback lb, int on) {
   if (!lb) return fail(nullptr, SQNGD_E_INVALID, "sqngd_loopback_set_peer: null group");
   std::unique_lock<std::mutex> lk(lb->g.mu);
   lb->g.peer = on != 0;
+  lb->g.peer_fused = on == 2;
   return SQNGD_OK;
 }
 
@@ -1098,6 +1100,7 @@ sqngd_status sqngd_peer_attach(sqngd_ctx ctx, const void* handles) {
     ctx->peer_pending = nullptr;
     return fail(ctx, SQNGD_E_CUDA, "sqngd_peer_attach", why.c_str());
   }
+  if (const char* ev = getenv("SQNGD_PEER_FUSED")) ctx->peer_pending->use_fused = !(ev[0] == '0');
   CK(cudaDeviceSynchronize());
   // the step graphs captured so far hold the previous backend's collective: drop them
   ctx->drop_graphs();
@@ -1312,6 +1315,12 @@ static sqngd_status world_combine(sqngd_ctx ctx, bool with_grad, cudaStream_t st
   wa.bp = c.beta_or_p; wa.red = ctx->red; wa.mref = ctx->mref; wa.grad = ctx->red_grad; wa.pay = ctx->pay;
   wa.key = ctx->keyb;
   const size_t n = with_grad ? (size_t)2 * c.M * c.N : 0;
+  if (ctx->comm->has_fused()) {  // pack + all-reduce over peer memory + unpack in one kernel (world_peer.cuh)
+    std::string why;
+    if (!ctx->comm->fused(&wa, st, &why)) return fail(ctx, SQNGD_E_NCCL, "fused peer combine", why.c_str());
+    ctx->launches += 1;
+    return launch_check(ctx, "world peer");
+  }
   const dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 256)), c.R);
   k_world_pack<<<grid, 256, 0, st>>>(wa);
   sqngd_status rc = launch_check(ctx, "world pack");

@@ -220,10 +220,11 @@ def test_nccl_one_rank_collective_path(engine, mode):
 
 
 # ------------------------------------------------- in-kernel all-reduce over peer memory (NEXT-4)
+@pytest.mark.parametrize("form", [1, 2], ids=["allreduce", "fused"])
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("mode", ["lse", "max"])
+@pytest.mark.parametrize("mode", ["lse", "pnorm", "max"])
 @pytest.mark.parametrize("engine", ["fft", "cheb"])
-def test_peer_allreduce_kernel_in_loopback(engine, mode, world):
+def test_peer_allreduce_kernel_in_loopback(engine, mode, world, form):
     """k_peer_allreduce (stage + flag signal, flag wait, rank-ordered read of every rank's stage) as the
     loopback group's reduction, its two phases launched rank by rank (no kernel waits on another): the
     sharded results must equal the plain loopback reduction BIT FOR BIT (both sum in rank order), stay
@@ -237,7 +238,7 @@ def test_peer_allreduce_kernel_in_loopback(engine, mode, world):
         eval_all(ctx, z, rho, w)
         return eval_all(ctx, z, rho, w)
 
-    res = on_ranks(c, world, twice, peer=True)
+    res = on_ranks(c, world, twice, peer=form)  # 1: k_peer_allreduce between pack and unpack, 2: k_world_peer
     plain = on_ranks(c, world, twice, peer=False)
     for r in range(world):
         for k in ("gw", "gz", "gr", "p"):
@@ -252,7 +253,8 @@ def test_peer_allreduce_kernel_in_loopback(engine, mode, world):
     check_grad(res[0]["gr"], gr_ref, "peer all-reduce grad_rho")
 
 
-def test_peer_allreduce_c5_payload_8_ranks():
+@pytest.mark.parametrize("form", [1, 2], ids=["allreduce", "fused"])
+def test_peer_allreduce_c5_payload_8_ranks(form):
     """The peer kernel on a payload that spans all its blocks (C5 shape: 1 + 2 M N = 131073 doubles per
     restart, 128 blocks) with 8 ranks: bit-identical to the plain loopback reduction."""
     c = CF.C5.with_(R=1, K=9, loss_mode=CF.LOSS_LSE, beta_or_p=200.0, doppler_engine=sqngd.ENGINE_CHEBYSHEV)
@@ -264,20 +266,56 @@ def test_peer_allreduce_c5_payload_8_ranks():
         ctx.sync()
         return m, gz.cpu().numpy(), gr.cpu().numpy()
 
-    res = on_ranks(c, 8, run, peer=True)
+    res = on_ranks(c, 8, run, peer=form)
     plain = on_ranks(c, 8, run, peer=False)
     for r in range(8):
         assert np.array_equal(res[r][1], plain[0][1]) and np.array_equal(res[r][2], plain[0][2])
         assert repr(res[r][0]) == repr(plain[0][0])
 
 
+@pytest.mark.parametrize("form", [1, 2], ids=["allreduce", "fused"])
+@pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("engine", ["fft", "cheb"])
-def test_peer_backend_one_rank_single_launch(engine):
+def test_peer_kernels_slices_across_restarts(engine, world, form):
+    """R = 3 restarts of 1 + 2 M N = 2401 payload values over 8 blocks of 901: restarts span several blocks
+    and blocks straddle two restarts, so the fused kernel's waits on the scalar owners of the touched
+    restarts and, for an owner, on the own rank's blocks that still read the local record, all occur.
+    Bit-identical to the plain loopback reduction over two evaluations; Step-B gradient vs the oracle."""
+    c = Cfg("mr-multi", M=4, N=300, B=4, K=9, f_lo=-0.5, f_hi=0.5, R=3, r_n=4, loss_mode=CF.LOSS_LSE,
+            beta_or_p=60.0, doppler_engine=ENGINES[engine])
+    z, rho, q, w = inputs_for(c, 99)
+
+    def twice(ctx, r):
+        eval_all(ctx, z, rho, w)
+        return eval_all(ctx, z, rho, w)
+
+    res = on_ranks(c, world, twice, peer=form)
+    plain = on_ranks(c, world, twice, peer=False)
+    for r in range(world):
+        for k in ("gw", "gz", "gr", "p"):
+            assert np.array_equal(res[r][k], plain[0][k]), (r, k)
+        for k in ("mf", "mA", "mB"):
+            assert repr(res[r][k]) == repr(plain[0][k]), (r, k)
+    _, _, gs_ref = O.loss_grad(c, q["s_soft"], w, want_w=False)
+    gz_ref, gr_ref = O.chain(c, z, rho, q["s_soft"], gs_ref)
+    check_grad(res[0]["gz"], gz_ref, "peer kernels (slices across restarts) grad_z")
+    check_grad(res[0]["gr"], gr_ref, "peer kernels (slices across restarts) grad_rho")
+
+
+MULTI = Cfg("mr-multi1", M=4, N=300, B=4, K=9, f_lo=-0.5, f_hi=0.5, R=3, r_n=4)
+
+
+@pytest.mark.parametrize("base", [CASES[1], MULTI], ids=lambda c: c.name)
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["fused", "allreduce"])
+@pytest.mark.parametrize("engine", ["fft", "cheb"])
+def test_peer_backend_one_rank_single_launch(engine, fused, base, monkeypatch):
     """The peer backend proper (sqngd_peer_export / sqngd_peer_attach replacing NCCL) at world = 1: the
     single-launch form of the kernel (signal, wait and reduce in one launch, against its own window),
     eagerly and captured in the step's CUDA graph over several replays (the epoch lives in the window,
-    so replays need no new arguments).  Must equal the 1-rank NCCL path bit for bit."""
-    c = CASES[1].with_(loss_mode=CF.LOSS_LSE, beta_or_p=60.0, doppler_engine=ENGINES[engine])
+    so replays need no new arguments).  Must equal the 1-rank NCCL path bit for bit.  mr-multi1 (3 restarts
+    over 8 blocks) makes the blocks of one launch wait on one another's flags for real."""
+    monkeypatch.setenv("SQNGD_PEER_FUSED", fused)  # read at attach: k_world_peer or pack + k_peer_allreduce + unpack
+    c = base.with_(loss_mode=CF.LOSS_LSE, beta_or_p=60.0, doppler_engine=ENGINES[engine])
     z, rho, q, w = inputs_for(c, 97)
     res = {}
     for name in ("peer", "nccl"):
