@@ -109,7 +109,7 @@ struct NcclComm : Comm {
 //   phase A  e = epoch[b] + 1;  copy slice b of (sum, mx) into the own stage[e & 1];  fence;  store e
 //            into flag[rank][b] of EVERY rank's window (st.release.sys over NVLink);
 //   phase B  wait until the own flag[r][b] >= e for every r (ld.acquire.sys, clock watchdog);  read slice b
-//            of every rank's stage[e & 1] (own rank locally, peers over NVLink, L1 bypassed) and write
+//            of every rank's stage[e & 1] (own rank locally, peers over NVLink, ld.global.cg) and write
 //            sum_r / max_r in RANK ORDER into the caller's buffers (bit-identical on every rank);
 //            epoch[b] = e.
 // A peer can be at most one epoch ahead (its epoch e + 1 wait needs this rank's e + 1 signal), so the two
@@ -118,6 +118,7 @@ struct NcclComm : Comm {
 // the same-numbered block of its peers, never on a block of its own grid.
 constexpr int kPeerMax = 8;
 constexpr int kPeerBlocks = 128;
+constexpr int kPeerThreads = 512;  // 128 x 512 threads x 4 loads in flight cover the HBM latency-bandwidth product
 struct PeerArgs {
   unsigned char* win[kPeerMax];  // every rank's window, as mapped into this process
   int world, rank;
@@ -140,13 +141,8 @@ __device__ __forceinline__ unsigned long long peer_ld_acquire(const unsigned lon
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned long long peer_ld_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
-__global__ void __launch_bounds__(256) k_peer_allreduce(PeerArgs a, double* sum, size_t nsum, unsigned long long* mx,
+__global__ void __launch_bounds__(kPeerThreads) k_peer_allreduce(PeerArgs a, double* sum, size_t nsum, unsigned long long* mx,
                                                         size_t nmax, int phases, unsigned long long timeout_ns) {
   typedef unsigned long long u64;
   const int b = blockIdx.x, nb = gridDim.x, t = threadIdx.x;
@@ -160,9 +156,11 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(PeerArgs a, double* sum,
     u64* st_sum = reinterpret_cast<u64*>(a.win[a.rank] + stage_off);
     u64* st_max = st_sum + a.cap_sum;
     const u64* src = reinterpret_cast<const u64*>(sum);
+#pragma unroll 4
     for (size_t i = s0 + t; i < s1; i += blockDim.x) st_sum[i] = src[i];
     for (size_t i = m0 + t; i < m1; i += blockDim.x) st_max[i] = mx[i];
-    __threadfence_system();
+    // the block's stage writes happen-before the barrier; the signalling threads' release at system
+    // scope is cumulative over them (the pattern of a grid barrier: bar.sync, then one fence + flag)
     __syncthreads();
     if (t < a.world)
       peer_st_release(reinterpret_cast<u64*>(a.win[t]) + (size_t)(1 + a.rank) * kPeerBlocks + b, e);
@@ -190,16 +188,18 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(PeerArgs a, double* sum,
       if (t == 0) atomicOr(a.status, kPeerTimeoutBit);
       return;  // epoch[b] is not advanced: the context is unusable after a timeout (sqngd_sync reports it)
     }
+    // (the acquires above, then the barrier, order these loads after the peers' stage writes; .cg: L2)
+#pragma unroll 4
     for (size_t i = s0 + t; i < s1; i += blockDim.x) {
       double s = 0.0;
       for (int r = 0; r < a.world; ++r)  // fixed rank order
-        s += __longlong_as_double((long long)peer_ld_u64(reinterpret_cast<const u64*>(a.win[r] + stage_off) + i));
+        s += __ldcg(reinterpret_cast<const double*>(a.win[r] + stage_off) + i);
       sum[i] = s;
     }
     for (size_t i = m0 + t; i < m1; i += blockDim.x) {
       u64 m = 0ull;
       for (int r = 0; r < a.world; ++r) {
-        const u64 v = peer_ld_u64(reinterpret_cast<const u64*>(a.win[r] + stage_off) + a.cap_sum + i);
+        const u64 v = __ldcg(reinterpret_cast<const u64*>(a.win[r] + stage_off) + a.cap_sum + i);
         m = v > m ? v : m;
       }
       mx[i] = m;
@@ -264,7 +264,7 @@ struct PeerComm : Comm {
   bool allreduce(double* sum, size_t nsum, unsigned long long* mx, size_t nmax, cudaStream_t st,
                  std::string* why) override {
     if (nsum > own.cap_sum || nmax > own.cap_max) { *why = "peer all-reduce: payload larger than the window"; return false; }
-    k_peer_allreduce<<<peer_grid(nsum, nmax), 256, 0, st>>>(args, sum, nsum, mx, nmax, kPeerPhaseA | kPeerPhaseB, timeout_ns);
+    k_peer_allreduce<<<peer_grid(nsum, nmax), kPeerThreads, 0, st>>>(args, sum, nsum, mx, nmax, kPeerPhaseA | kPeerPhaseB, timeout_ns);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { *why = cudaGetErrorString(e); return false; }
     return true;
@@ -375,7 +375,7 @@ struct LoopComm : Comm {
               a.cap_sum = g->win[0].cap_sum;
               a.cap_max = g->win[0].cap_max;
               a.status = g->status[r];
-              k_peer_allreduce<<<peer_grid(nsum, nmax), 256, 0, st>>>(a, g->ptrs.sum[r], nsum, g->ptrs.mx[r], nmax, ph,
+              k_peer_allreduce<<<peer_grid(nsum, nmax), kPeerThreads, 0, st>>>(a, g->ptrs.sum[r], nsum, g->ptrs.mx[r], nmax, ph,
                                                                        2000000000ull);
             }
         } else {

@@ -32,7 +32,7 @@ __device__ __forceinline__ bool peer_wait(const unsigned long long* f, unsigned 
   return true;
 }
 
-__global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, int phases, unsigned long long timeout_ns) {
+__global__ void __launch_bounds__(kPeerThreads) k_world_peer(WorldArgs a, PeerArgs pa, int phases, unsigned long long timeout_ns) {
   typedef unsigned long long u64;
   const int b = blockIdx.x, G = gridDim.x, t = threadIdx.x;
   u64* own = reinterpret_cast<u64*>(pa.win[pa.rank]);
@@ -46,9 +46,14 @@ __global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, in
     u64* st_key = reinterpret_cast<u64*>(st_sum) + pa.cap_sum;
     int rc = -1;
     double wS = 0.0, wG = 0.0, m = 0.0;
-    for (size_t i = i0 + t; i < i1; i += blockDim.x) {
-      const int r = (int)(i / stride);
-      const size_t j = i - (size_t)r * stride;
+    int r = (int)(min(T, i0 + t) / stride);
+    size_t j = i0 + t - (size_t)r * stride;
+#pragma unroll 2
+    for (size_t i = i0 + t; i < i1; i += blockDim.x, j += blockDim.x) {
+      while (j >= stride) {  // (restart, offset) of i without a 64-bit division per element
+        j -= stride;
+        ++r;
+      }
       if (r != rc) {
         world_weights(a, r, wS, wG, m);
         rc = r;
@@ -63,8 +68,7 @@ __global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, in
         st_sum[i] = wG * (double)reinterpret_cast<const float*>(a.grad)[(size_t)r * n + (j - 1)];
       }
     }
-    __threadfence_system();
-    __syncthreads();
+    __syncthreads();  // (the release below is cumulative over the block's stage writes, as in k_peer_allreduce)
     if (t < pa.world) peer_st_release(reinterpret_cast<u64*>(pa.win[t]) + (size_t)(1 + pa.rank) * kPeerBlocks + b, e);
   }
   if (phases & kPeerPhaseB) {
@@ -94,13 +98,18 @@ __global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, in
     }
     int rc = -1;
     double S = 0.0, norm = 0.0;
-    for (size_t i = i0 + t; i < i1; i += blockDim.x) {
-      const int r = (int)(i / stride);
-      const size_t j = i - (size_t)r * stride;
+    int r = (int)(min(T, i0 + t) / stride);
+    size_t j = i0 + t - (size_t)r * stride;
+#pragma unroll 2
+    for (size_t i = i0 + t; i < i1; i += blockDim.x, j += blockDim.x) {
+      while (j >= stride) {  // (restart, offset) of i without a 64-bit division per element
+        j -= stride;
+        ++r;
+      }
       if (r != rc) {
         S = 0.0;
         for (int q = 0; q < W; ++q)  // fixed rank order
-          S += __longlong_as_double((long long)peer_ld_u64(reinterpret_cast<const u64*>(pa.win[q] + stage_off) + (size_t)r * stride));
+          S += __ldcg(reinterpret_cast<const double*>(pa.win[q] + stage_off) + (size_t)r * stride);
         norm = 0.0;
         if (a.mode != 0 && S > 0.0) norm = a.mode == 1 ? 1.0 / S : pow(S, 1.0 / a.bp - 1.0);
         rc = r;
@@ -111,7 +120,7 @@ __global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, in
           const u64* kq = reinterpret_cast<const u64*>(pa.win[q] + stage_off) + pa.cap_sum + 3 * (size_t)r;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const u64 v = peer_ld_u64(kq + c);
+            const u64 v = __ldcg(kq + c);
             key[c] = v > key[c] ? v : key[c];
           }
         }
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, in
       } else {
         double s = 0.0;
         for (int q = 0; q < W; ++q)
-          s += __longlong_as_double((long long)peer_ld_u64(reinterpret_cast<const u64*>(pa.win[q] + stage_off) + i));
+          s += __ldcg(reinterpret_cast<const double*>(pa.win[q] + stage_off) + i);
         reinterpret_cast<float*>(a.grad)[(size_t)r * n + (j - 1)] = (float)(s * norm);
       }
     }
@@ -138,7 +147,7 @@ __global__ void __launch_bounds__(256) k_world_peer(WorldArgs a, PeerArgs pa, in
 }
 
 inline bool PeerComm::fused(const WorldArgs* wa, cudaStream_t st, std::string* why) {
-  k_world_peer<<<peer_grid(own.cap_sum, own.cap_max), 256, 0, st>>>(*wa, args, kPeerPhaseA | kPeerPhaseB, timeout_ns);
+  k_world_peer<<<peer_grid(own.cap_sum, own.cap_max), kPeerThreads, 0, st>>>(*wa, args, kPeerPhaseA | kPeerPhaseB, timeout_ns);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { *why = cudaGetErrorString(e); return false; }
   return true;
@@ -169,7 +178,7 @@ inline bool LoopComm::fused(const WorldArgs* wa, cudaStream_t st, std::string* w
         a.cap_sum = g->win[0].cap_sum;
         a.cap_max = g->win[0].cap_max;
         a.status = g->status[r];
-        k_world_peer<<<peer_grid(a.cap_sum, a.cap_max), 256, 0, st>>>(*g->wargs[r], a, ph, 2000000000ull);
+        k_world_peer<<<peer_grid(a.cap_sum, a.cap_max), kPeerThreads, 0, st>>>(*g->wargs[r], a, ph, 2000000000ull);
       }
     cudaEventRecord(g->done, st);
     g->arrived = 0;
