@@ -337,8 +337,9 @@ def work_sharded(args, world, rank, local, dev, stream, flush, name="C5"):
         ms_p = run(fresh_uid() if world > 1 else sqngd.nccl_unique_id(), peer=True)[0]
         extra["peer_allreduce"] = {
             "value": evals / (ms_p / 1e3), "ms_per_step": ms_p, "n_gpus": world,
-            "what": "k_peer_allreduce (stage + flag over NVLink peer memory, wait, rank-ordered read) instead of "
-                    "the grouped NCCL call, captured in the step graph" + (" (1 rank: its own window)" if world == 1 else "")}
+            "what": "k_world_peer (pack + all-reduce over NVLink peer memory + unpack in one kernel: stage, flag "
+                    "signal, wait, rank-ordered read) instead of pack + the grouped NCCL call + unpack, captured "
+                    "in the step graph" + (" (1 rank: its own window)" if world == 1 else "")}
     except Exception as e:
         extra["peer_allreduce"] = {"error": f"{type(e).__name__}: {e}"}
     return {**extra, "workload": f"{name}: M={c.M} N={c.N} L={c.B} K={c.K} R={c.R} (one problem)", "n_gpus": world,
