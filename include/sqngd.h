@@ -172,7 +172,8 @@ sqngd_status sqngd_create_loopback(const sqngd_config* cfg, int cuda_device, sqn
    signal phase launched for every rank and then its wait + reduce phase for every rank on one stream
    (every wait already satisfied), so the kernel that runs between GPUs is validated on one device. */
 /* on = 2: the fused form (k_world_peer: pack + all-reduce + unpack in one kernel, the default of the
-   peer backend below), again phase by phase. */
+   peer backend below), again phase by phase.  on = 3 (tests of the watchdog): as 2, but the last rank's
+   signal phase is never launched, so every rank's wait gives up after 2 s and latches SQNGD_E_NCCL. */
 sqngd_status sqngd_loopback_set_peer(sqngd_loopback group, int on);
 
 /* In-kernel all-reduce over NVLink peer memory instead of NCCL (DESIGN.md §7

@@ -314,6 +314,7 @@ struct LoopGroup {
   bool peer = false;
   bool peer_fused = false;                   // (peer) the whole combine in k_world_peer, phase by phase
   const WorldArgs* wargs[kLoopMax] = {};     // (peer_fused) every rank's combine arguments
+  int drop_signal_rank = -1;                 // (tests) this rank's phase A is not launched: the watchdog path
   PeerWindow win[kLoopMax];
   int* status[kLoopMax] = {};
   size_t cap_sum = 0, cap_max = 0;  // window capacity: the contexts' largest payload

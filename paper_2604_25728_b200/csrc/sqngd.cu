@@ -1063,7 +1063,8 @@ sqngd_status sqngd_loopback_set_peer(sqngd_loopback lb, int on) {
   if (!lb) return fail(nullptr, SQNGD_E_INVALID, "sqngd_loopback_set_peer: null group");
   std::unique_lock<std::mutex> lk(lb->g.mu);
   lb->g.peer = on != 0;
-  lb->g.peer_fused = on == 2;
+  lb->g.peer_fused = on == 2 || on == 3;
+  lb->g.drop_signal_rank = on == 3 ? lb->g.world - 1 : -1;
   return SQNGD_OK;
 }
 
@@ -1228,10 +1229,11 @@ sqngd_status sqngd_sync(sqngd_ctx ctx, sqngd_stream stream) {
   int st = 0;
   CK(cudaMemcpy(&st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost));
   CK(cudaMemset(ctx->status, 0, sizeof(int)));
+  // (first: without the combine everything downstream is a symptom)
+  if (st & kPeerTimeoutBit) return fail(ctx, SQNGD_E_NCCL, "peer all-reduce: a rank did not signal in time");
   if (st & ST_NONFINITE) return fail(ctx, SQNGD_E_NONFINITE, "non-finite loss or gradient");
   if (st & ST_DEGENERATE) return fail(ctx, SQNGD_E_DEGENERATE, "degenerate mainlobe or zero-energy filter");
   if (st & ST_INVALID) return fail(ctx, SQNGD_E_INVALID, "thresholds rho not ascending");
-  if (st & kPeerTimeoutBit) return fail(ctx, SQNGD_E_NCCL, "peer all-reduce: a rank did not signal in time");
   return SQNGD_OK;
 }
 

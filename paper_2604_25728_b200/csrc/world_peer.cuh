@@ -171,6 +171,7 @@ inline bool LoopComm::fused(const WorldArgs* wa, cudaStream_t st, std::string* w
         g->err = "loopback: peer window allocation";
     for (int ph = kPeerPhaseA; ph <= kPeerPhaseB && g->err.empty(); ph <<= 1)
       for (int r = 0; r < g->world; ++r) {
+        if (ph == kPeerPhaseA && r == g->drop_signal_rank) continue;  // (tests) a rank that never signals
         PeerArgs a{};
         for (int q = 0; q < g->world; ++q) a.win[q] = g->win[q].base;
         a.world = g->world;

@@ -263,7 +263,8 @@ class Loopback:
             raise SqngdError(E_INVALID, f"sqngd_loopback_create({world})")
         if peer:  # reduce with the peer-memory kernels (phase by phase) instead of the plain reduction:
             # True / 1 = k_peer_allreduce between pack and unpack, 2 / "fused" = k_world_peer (all in one)
-            st = lib().sqngd_loopback_set_peer(self.h, 2 if peer in (2, "fused") else 1)
+            # 3 / "drop": fused, with the last rank's signal phase dropped (the wait watchdog's test)
+            st = lib().sqngd_loopback_set_peer(self.h, 3 if peer in (3, "drop") else 2 if peer in (2, "fused") else 1)
             if st != OK:
                 raise SqngdError(st, "sqngd_loopback_set_peer")
 

@@ -360,3 +360,34 @@ def test_peer_attach_errors():
     ctx = sqngd.Context(c, nccl_uid=sqngd.nccl_unique_id(), rank=0, world=1)
     assert sqngd.lib().sqngd_peer_attach(ctx.h, buf) == sqngd.E_INVALID
     ctx.close()
+
+
+def test_peer_wait_watchdog_latches_error():
+    """A rank that never signals: the waiting kernels give up (2 s in the loopback group), latch the
+    time-out bit and return -- sqngd_sync reports SQNGD_E_NCCL on every rank, the GPU does not hang."""
+    c = CASES[0].with_(loss_mode=CF.LOSS_LSE, beta_or_p=60.0)
+    z, rho, q, w = inputs_for(c, 91)
+    lb = sqngd.Loopback(2, peer="drop")
+    ctxs = [sqngd.Context(c, loopback=lb, rank=r) for r in range(2)]
+    got = [None, None]
+
+    def work(r):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            try:
+                ctxs[r].af_loss_grad(T(z), T(rho), T(w), sqngd.WRT_TRANSMIT)
+                ctxs[r].sync()
+                got[r] = "no error"
+            except sqngd.SqngdError as e:
+                got[r] = e.status
+            s.synchronize()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    for cx in ctxs:
+        cx.close()
+    lb.close()
+    assert got == [sqngd.E_NCCL, sqngd.E_NCCL], got
