@@ -74,6 +74,16 @@ def test_create_rejects_invalid_config_without_gpu(lib):
         assert lib.sqngd_last_error(None)
 
 
+def test_peer_api_rejects_null_arguments_without_gpu(lib):
+    """The peer-memory all-reduce entry points (include/sqngd.h sqngd_peer_export / _attach,
+    sqngd_loopback_set_peer) check their arguments before any CUDA call."""
+    buf = C.create_string_buffer(64)
+    assert lib.sqngd_peer_export(None, buf) == sqngd.E_INVALID
+    assert lib.sqngd_peer_attach(None, buf) == sqngd.E_INVALID
+    assert lib.sqngd_loopback_set_peer(None, 1) == sqngd.E_INVALID
+    assert b"null" in lib.sqngd_last_error(None)
+
+
 def test_generator_parameter_count(lib):
     """sqngd_net_num_params = the closed form D (2 W^2 + 2 W) + (W Din + W) + (Din W + Din)."""
     from paper_2604_25728_b200.configs import C1, C3
